@@ -1,0 +1,222 @@
+/*
+ * tgcu — B200-native (sm_100a) TaylorGrid query → loss-fused backward → TV →
+ * Adam hot path, behind a C ABI.
+ *
+ * Every entry point replaces a reference function of
+ * /root/reference/proj/core (cited per declaration). Conventions:
+ *   - plain pointers + sizes, no C++/torch types; all functions return an
+ *     int status (TGCU_OK or one of the TGCU_ERR_* classes below, mirroring
+ *     the reference's exception classes, errors.hpp:9-34) and set a
+ *     thread-local message readable with tgcu_last_error();
+ *   - a tgcu_grid owns the device-resident fp32 coefficients (reference AoS
+ *     layout: vertex-major, x fastest, per-vertex block [f0 | f1 | f2 upper
+ *     triangle], taylor_grid.hpp:27-31), the Adam moments, an optional
+ *     gradient buffer and all scratch;
+ *   - point/sample arrays are fp32. `flags & TGCU_HOST` means the pointers
+ *     are host memory (copied in/out inside the call); otherwise device
+ *     memory on the grid's device. `stream` is a cudaStream_t (NULL = the
+ *     legacy default stream).
+ *   - calls are synchronous (errors surface on return) unless TGCU_ASYNC is
+ *     passed; async errors are sticky and reported by tgcu_sync().
+ */
+#ifndef TGCU_H
+#define TGCU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: exception classes of errors.hpp:9-34 plus CUDA failures. */
+enum {
+    TGCU_OK = 0,
+    TGCU_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (require_arg) */
+    TGCU_ERR_CONFIG = 2,           /* tg::ConfigError */
+    TGCU_ERR_INGEST = 3,           /* tg::IngestError */
+    TGCU_ERR_NUMERICAL = 4,        /* tg::NumericalError */
+    TGCU_ERR_RESOURCE = 5,         /* tg::ResourceError */
+    TGCU_ERR_CUDA = 6              /* CUDA runtime failure / no device */
+};
+
+/* Call flags. */
+enum {
+    TGCU_HOST = 1,   /* point / value pointers are host memory */
+    TGCU_ASYNC = 2,  /* do not synchronize; errors become sticky */
+    TGCU_SORTED = 4,      /* eval: points are sorted by tgcu_sort_points (brick-binned query) */
+    TGCU_EXPORT_GRAD = 8  /* train_step: also write the full gradient to the grid grad buffer
+                             (validation mode; the fused path otherwise never stores it) */
+};
+
+/* tg::GridSpec (grid_spec.hpp:19-24). */
+typedef struct {
+    int dim;           /* 2 or 3 */
+    int res[3];        /* vertices per axis (>= 2); res[2] ignored for dim 2 */
+    double origin[3];
+    double extent[3];
+    int order;         /* 0..2 */
+} tgcu_grid_spec;
+
+/* tg::InitOptions (taylor_grid.hpp:17-25). */
+enum {
+    TGCU_INIT_ZEROS = 0,
+    TGCU_INIT_CONSTANT = 1,
+    TGCU_INIT_SMALL_UNIFORM = 2,  /* reference Rng stream, host-generated (bit-identical draws) */
+    TGCU_INIT_HASH_GAUSSIAN = 3   /* epsilon * N(0,1) from a counter hash of (seed, index), on
+                                     device: for multi-GB throughput grids (BASELINE C4) */
+};
+typedef struct {
+    int mode;
+    double constant;
+    double epsilon;
+    uint64_t seed;
+    uint64_t memory_cap_bytes; /* cap on fp64-equivalent coefficient bytes, as the reference */
+} tgcu_init_options;
+
+/* tg::LossConfig (sdf_loss.hpp:15-25). batch_size is the caller's n;
+ * the eikonal points are the batch itself (EikonalPointSource::ReuseBatch). */
+typedef struct {
+    double lambda1;
+    double lambda2;
+    double k;
+    int use_weighting;
+    int use_tv;
+    int differentiate_weight;
+} tgcu_loss_config;
+
+/* tg::LossTerms (schedule.hpp:43-48). */
+typedef struct {
+    double total;
+    double fit;
+    double eik;
+    double tv;
+} tgcu_loss_terms;
+
+/* tg::AdamConfig (adam.hpp:9-14). */
+typedef struct {
+    double lr;
+    double beta1;
+    double beta2;
+    double eps;
+} tgcu_adam_config;
+
+typedef struct tgcu_grid tgcu_grid;
+
+const char* tgcu_last_error(void);
+const char* tgcu_version(void);
+
+/* coeff_count (grid_spec.cpp:10-19). */
+int tgcu_coeff_count(int order, int dim, int* out);
+
+/* init_grid (taylor_grid.cpp:162-188): validate (grid_spec.cpp:21-33), cap
+ * check (ResourceError), allocate on `device`, initialise. opts may be NULL
+ * (Zeros, 4 GiB cap). */
+int tgcu_grid_create(const tgcu_grid_spec* spec, const tgcu_init_options* opts, int device,
+                     tgcu_grid** out);
+int tgcu_grid_destroy(tgcu_grid* g);
+int tgcu_grid_spec_of(const tgcu_grid* g, tgcu_grid_spec* out);
+int64_t tgcu_grid_coeff_total(const tgcu_grid* g);
+/* Device pointer of the current fp32 coefficient array (AoS, coeff_total floats). */
+float* tgcu_grid_coeffs(tgcu_grid* g);
+
+/* TaylorGrid::coeffs interop in the reference layout (fp64 <-> fp32 at the boundary). */
+int tgcu_grid_upload_f64(tgcu_grid* g, const double* coeffs, int64_t n);
+int tgcu_grid_download_f64(tgcu_grid* g, double* coeffs, int64_t n);
+int tgcu_grid_upload_f32(tgcu_grid* g, const float* coeffs, int64_t n, int flags);
+int tgcu_grid_download_f32(tgcu_grid* g, float* coeffs, int64_t n, int flags);
+/* all_finite (taylor_grid.cpp:190-195). */
+int tgcu_grid_all_finite(tgcu_grid* g, int* out);
+
+/* eval / eval_with_spatial_gradient (taylor_grid.cpp:197-203), batched:
+ * pts n×3 (x, y, z; z ignored in 2D), values n, spatial_grad n×3 or NULL.
+ * A NaN coordinate -> TGCU_ERR_INVALID_ARGUMENT (locate, grid_spec.cpp:46-48). */
+int tgcu_eval(tgcu_grid* g, const float* pts, int64_t n, float* values, float* spatial_grad,
+              int flags, void* stream);
+
+/* Morton/brick sort of query points for the brick-binned query
+ * (eval with TGCU_SORTED). perm (nullable) receives the source index of each
+ * output point. Device pointers only. */
+int tgcu_sort_points(tgcu_grid* g, const float* pts, int64_t n, float* sorted_pts, int64_t* perm,
+                     void* stream);
+
+/* backprop_value_and_spatial (taylor_grid.cpp:223-229), batched: adds
+ * upstream[i]·∂f/∂c + upstream_vec[i]·∂∇f/∂c into grad (device, coeff_total
+ * floats). upstream or upstream_vec may be NULL (= zeros; backprop_point /
+ * backprop_spatial_chain, :205-221). */
+int tgcu_backprop(tgcu_grid* g, const float* pts, const float* upstream, const float* upstream_vec,
+                  int64_t n, float* grad, int flags, void* stream);
+
+/* Device gradient buffer owned by the grid (coeff_total floats, zeroed at
+ * creation). */
+float* tgcu_grid_grad(tgcu_grid* g);
+int tgcu_grad_zero(tgcu_grid* g, float* grad, void* stream);
+/* Copy a device gradient buffer (NULL = the grid's own) to host fp64. */
+int tgcu_grad_download_f64(tgcu_grid* g, const float* grad, double* out, int64_t n);
+
+/* tv_loss (sdf_loss.cpp:155-257). grad may be NULL (value only). */
+int tgcu_tv_loss(tgcu_grid* g, float* grad, double scale, double* out, void* stream);
+
+/* total_loss (sdf_loss.cpp:259-292), reuse-batch eikonal: samples n×4
+ * (x, y, z, gt). grad (device) may be NULL. Unfused path (gather, atomic
+ * scatter into grad, then TV). */
+int tgcu_total_loss(tgcu_grid* g, const float* samples, int64_t n, const tgcu_loss_config* cfg,
+                    float* grad, tgcu_loss_terms* out, int flags, void* stream);
+
+/* AdamState (adam.hpp:17-32): reset moments and t (AdamState::reset). */
+int tgcu_adam_reset(tgcu_grid* g, const tgcu_adam_config* cfg);
+int tgcu_adam_get_t(const tgcu_grid* g, int64_t* t);
+/* adam_step (adam.cpp:12-56) on the grid's coefficients with grad (device):
+ * non-finite grad -> TGCU_ERR_NUMERICAL naming the first index, params untouched. */
+int tgcu_adam_step(tgcu_grid* g, const float* grad, void* stream);
+/* Moment interop (reference layout, fp64 <-> fp32). */
+int tgcu_adam_download_f64(tgcu_grid* g, double* m, double* v, int64_t n);
+
+/* One fused training step = the run_schedule / cmd_bench inner loop
+ * (schedule.cpp:66-92, tools/main.cpp:640-644): zero grad → total_loss →
+ * finite-loss check → adam_step, as one device pipeline (point binning →
+ * fused brick kernel → finalize). The gradient never touches HBM. On a
+ * non-finite loss or gradient the step is not committed (params, moments and
+ * t stay as before) and TGCU_ERR_NUMERICAL is returned (sticky under
+ * TGCU_ASYNC; "stage 0 step k" / "index i" in the message). out may be NULL. */
+int tgcu_train_step(tgcu_grid* g, const float* samples, int64_t n, const tgcu_loss_config* cfg,
+                    tgcu_loss_terms* out, int flags, void* stream);
+/* Wait for the grid's outstanding async work and report any sticky error.
+ * If last_terms is not NULL it receives the most recent step's LossTerms. */
+int tgcu_sync(tgcu_grid* g, tgcu_loss_terms* last_terms);
+/* Per-step LossTerms of the last `count` async steps (oldest first, up to the
+ * trace capacity of 4096). */
+int tgcu_trace(tgcu_grid* g, tgcu_loss_terms* out, int count);
+
+/* Live timing of the fused brick kernel: CUDA events recorded on the launch
+ * stream around every k_brick_step launch between begin and end; end returns
+ * the summed device milliseconds and the number of timed launches. */
+int tgcu_profile_begin(tgcu_grid* g);
+int tgcu_profile_end(tgcu_grid* g, double* total_ms, int* launches);
+
+/* Number of kernels this library launched since the counter was reset. */
+int64_t tgcu_launch_count(void);
+void tgcu_reset_launch_count(void);
+
+/* Host-side seeded input generation with the reference Rng semantics
+ * (rng.hpp:14-74): mt19937_64, uniform = (x>>11)·2^-53, Box–Muller gaussian.
+ * shape: 0 = sphere r=param0 (3D), 1 = 2D circle r=0.5 ∪ box (BASELINE C1),
+ * 2 = procedural min-union of 64 seeded primitives (C3/C5).
+ * Writes n×4 floats (x, y, z, gt). near_frac of the points are near-surface
+ * (surface point + N(0, sigma) per axis, clamped), the rest uniform in the
+ * domain box (uniform first, as sample_sphere_points, sampling.cpp:94-103). */
+int tgcu_sample(int shape, int dim, uint64_t seed, int64_t n, double near_frac, double sigma,
+                double param0, float* out4);
+/* Device-side uniform points in [lo, hi]^dim from a counter hash (n×3,
+ * device pointer; z = 0 in 2D). For large synthetic query sets. */
+int tgcu_sample_uniform_device(int dim, uint64_t seed, int64_t n, double lo, double hi, float* out3,
+                               void* stream);
+/* Uniform query points in [lo, hi]^dim (n×3, z = 0 in 2D). */
+int tgcu_sample_uniform(int dim, uint64_t seed, int64_t n, double lo, double hi, float* out3);
+/* Analytic target SDF of a shape at points (n×3 fp64 in, n out). */
+int tgcu_shape_sdf(int shape, int dim, double param0, const double* pts, int64_t n, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TGCU_H */

@@ -1,0 +1,318 @@
+// TEST INFRASTRUCTURE — NOT PART OF THE PRODUCT.
+//
+// extern "C" shim over the reference library's own hot-path functions
+// (/root/reference/proj/core, compiled unmodified by oracle/Makefile into
+// oracle/_ref/libtgref.so). It lets the Python tests pin the C restatement
+// (tg_oracle.c) against the real reference, generate golden vectors, and time
+// the reference CPU path for bench.py's cpu_baseline / --impl reference legs.
+// Nothing here is linked into the product library.
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "taylorgrid/adam.hpp"
+#include "taylorgrid/errors.hpp"
+#include "taylorgrid/parallel.hpp"
+#include "taylorgrid/rng.hpp"
+#include "taylorgrid/sampling.hpp"
+#include "taylorgrid/sdf_loss.hpp"
+#include "taylorgrid/taylor_grid.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+tg::GridSpec make_spec(int dim, const int* res, const double* origin, const double* extent,
+                       int order) {
+    tg::GridSpec s;
+    s.dim = dim;
+    for (int a = 0; a < 3; ++a) {
+        s.resolution[a] = res[a];
+        s.origin[a] = origin[a];
+        s.extent[a] = extent[a];
+    }
+    s.order = order;
+    return s;
+}
+
+// Wraps reference coefficients without copying is impossible (TaylorGrid owns a
+// std::vector), so grids are built per call from the caller's array.
+tg::TaylorGrid make_grid(const tg::GridSpec& spec, const double* coeffs) {
+    tg::InitOptions opts;
+    opts.memory_cap_bytes = ~0ull;
+    tg::TaylorGrid g = tg::init_grid(spec, opts);
+    std::memcpy(g.coeffs.data(), coeffs, g.coeffs.size() * sizeof(double));
+    return g;
+}
+
+std::vector<tg::SdfSample> make_batch(const double* samples, int64_t n, int dim) {
+    std::vector<tg::SdfSample> batch(static_cast<std::size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+        batch[i].point = {samples[4 * i], samples[4 * i + 1], dim == 3 ? samples[4 * i + 2] : 0.0};
+        batch[i].gt_sdf = samples[4 * i + 3];
+    }
+    return batch;
+}
+
+tg::LossConfig make_loss(double lambda1, double lambda2, double k, int use_weighting, int use_tv,
+                         int differentiate_weight) {
+    tg::LossConfig c;
+    c.lambda1 = lambda1;
+    c.lambda2 = lambda2;
+    c.k = k;
+    c.use_weighting = use_weighting != 0;
+    c.use_tv = use_tv != 0;
+    c.differentiate_weight = differentiate_weight != 0;
+    return c;
+}
+
+int fail(const std::exception& e, int code) {
+    g_err = e.what();
+    return code;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tgr_last_error() { return g_err.c_str(); }
+
+int tgr_coeff_count(int order, int dim) {
+    try {
+        return tg::coeff_count(order, dim);
+    } catch (const std::exception& e) {
+        return -fail(e, 1);
+    }
+}
+
+int tgr_locate(int dim, const int* res, const double* origin, const double* extent, int order,
+               const double* p, int* cell, double* local, int64_t* vid) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        const tg::CellRef r = tg::locate(spec, {p[0], p[1], p[2]});
+        for (int a = 0; a < 3; ++a) {
+            cell[a] = r.cell[a];
+            local[a] = r.local[a];
+        }
+        for (int c = 0; c < 8; ++c) vid[c] = r.vertex_ids[c];
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, 1);
+    }
+}
+
+// Batched eval: pts n×3, vals n, grads n×3 (nullable).
+int tgr_eval(int dim, const int* res, const double* origin, const double* extent, int order,
+             const double* coeffs, const double* pts, int64_t n, double* vals, double* grads) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        const tg::TaylorGrid grid = make_grid(spec, coeffs);
+        for (int64_t i = 0; i < n; ++i) {
+            const tg::Vec3 p{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+            if (grads) {
+                const tg::EvalResult er = tg::eval_with_spatial_gradient(grid, p);
+                vals[i] = er.value;
+                for (int a = 0; a < 3; ++a) grads[3 * i + a] = er.spatial_gradient[a];
+            } else {
+                vals[i] = tg::eval(grid, p);
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+// Batched backprop_value_and_spatial into grad (coeff_total entries).
+int tgr_backprop(int dim, const int* res, const double* origin, const double* extent, int order,
+                 const double* coeffs, const double* pts, const double* upstream,
+                 const double* upstream_vec, int64_t n, double* grad) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        const tg::TaylorGrid grid = make_grid(spec, coeffs);
+        std::span<double> g(grad, grid.coeffs.size());
+        for (int64_t i = 0; i < n; ++i) {
+            const tg::Vec3 p{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+            const tg::Vec3 uv{upstream_vec[3 * i], upstream_vec[3 * i + 1], upstream_vec[3 * i + 2]};
+            tg::backprop_value_and_spatial(grid, p, upstream[i], uv, g);
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+double tgr_adaptive_weight(double d_hat, double d, double k) { return tg::adaptive_weight(d_hat, d, k); }
+
+int tgr_tv_loss(int dim, const int* res, const double* origin, const double* extent, int order,
+                const double* coeffs, double* grad, double scale, int threads, double* out) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        const tg::TaylorGrid grid = make_grid(spec, coeffs);
+        std::span<double> g;
+        if (grad) g = std::span<double>(grad, grid.coeffs.size());
+        *out = tg::tv_loss(grid, g, scale, threads);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+int tgr_total_loss(int dim, const int* res, const double* origin, const double* extent, int order,
+                   const double* coeffs, const double* samples, int64_t n, double lambda1,
+                   double lambda2, double k, int use_weighting, int use_tv, int differentiate_weight,
+                   double* grad, int threads, double* terms) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        const tg::TaylorGrid grid = make_grid(spec, coeffs);
+        const auto batch = make_batch(samples, n, dim);
+        const auto cfg = make_loss(lambda1, lambda2, k, use_weighting, use_tv, differentiate_weight);
+        std::span<double> g;
+        if (grad) g = std::span<double>(grad, grid.coeffs.size());
+        const tg::LossTerms t = tg::total_loss(grid, batch, cfg, g, threads);
+        terms[0] = t.total;
+        terms[1] = t.fit;
+        terms[2] = t.eik;
+        terms[3] = t.tv;
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, 1);
+    } catch (const std::exception& e) {
+        return fail(e, 4);
+    }
+}
+
+// adam_step on caller arrays; returns 0, or 4 with the NumericalError text.
+int tgr_adam_step(double* p, const double* g, double* m, double* v, int64_t n, int64_t* t, double lr,
+                  double beta1, double beta2, double eps, int threads) {
+    try {
+        tg::AdamConfig c{lr, beta1, beta2, eps};
+        tg::AdamState st(static_cast<std::size_t>(n), c);
+        std::memcpy(st.m.data(), m, n * sizeof(double));
+        std::memcpy(st.v.data(), v, n * sizeof(double));
+        st.t = *t;
+        tg::adam_step(std::span<double>(p, n), std::span<const double>(g, n), st, threads);
+        std::memcpy(m, st.m.data(), n * sizeof(double));
+        std::memcpy(v, st.v.data(), n * sizeof(double));
+        *t = st.t;
+        return 0;
+    } catch (const tg::NumericalError& e) {
+        return fail(e, 4);
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+// Training trajectory in the cmd_bench loop shape (tools/main.cpp:639-644):
+// per step zero grad -> total_loss -> finite check -> adam_step. Batches are
+// supplied by the caller (steps × n × 4). coeffs is updated in place; the
+// per-step LossTerms go to terms_out (steps × 4).
+int tgr_train(int dim, const int* res, const double* origin, const double* extent, int order,
+              double* coeffs, const double* batches, int64_t n, int steps, double lambda1,
+              double lambda2, double k, int use_weighting, int use_tv, int differentiate_weight,
+              double lr, double beta1, double beta2, double eps, int threads, double* terms_out,
+              double* seconds_out) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        tg::TaylorGrid grid = make_grid(spec, coeffs);
+        const auto cfg = make_loss(lambda1, lambda2, k, use_weighting, use_tv, differentiate_weight);
+        tg::AdamState state(grid.coeffs.size(), tg::AdamConfig{lr, beta1, beta2, eps});
+        std::vector<double> grad(grid.coeffs.size());
+        double secs = 0.0;
+        for (int s = 0; s < steps; ++s) {
+            const auto batch = make_batch(batches + 4 * n * static_cast<int64_t>(s), n, dim);
+            const auto t0 = std::chrono::steady_clock::now();
+            std::fill(grad.begin(), grad.end(), 0.0);
+            const tg::LossTerms t = tg::total_loss(grid, batch, cfg, grad, threads);
+            if (!std::isfinite(t.total)) {
+                throw tg::NumericalError("run_schedule: non-finite loss at stage 0 step " +
+                                         std::to_string(s));
+            }
+            tg::adam_step(grid.coeffs, grad, state, threads);
+            secs += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (terms_out) {
+                terms_out[4 * s] = t.total;
+                terms_out[4 * s + 1] = t.fit;
+                terms_out[4 * s + 2] = t.eik;
+                terms_out[4 * s + 3] = t.tv;
+            }
+        }
+        std::memcpy(coeffs, grid.coeffs.data(), grid.coeffs.size() * sizeof(double));
+        if (seconds_out) *seconds_out = secs;
+        return 0;
+    } catch (const tg::NumericalError& e) {
+        return fail(e, 4);
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+// Query throughput of the reference: parallel_for + eval. Returns
+// the wall seconds of the eval loop only.
+int tgr_eval_timed(int dim, const int* res, const double* origin, const double* extent, int order,
+                   const double* coeffs, const double* pts, int64_t n, double* vals, int threads,
+                   double* seconds_out) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        const tg::TaylorGrid grid = make_grid(spec, coeffs);
+        const auto t0 = std::chrono::steady_clock::now();
+        tg::parallel_for(n, threads, [&](int64_t b, int64_t e, int) {
+            for (int64_t i = b; i < e; ++i) vals[i] = tg::eval(grid, {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]});
+        });
+        *seconds_out = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+// Reference sampler: sample_sphere_points (sampling.cpp:140-159) with the
+// uniform:near:ray ratio given; out is total×4 (x, y, z, gt).
+int tgr_sample_sphere(double radius, int64_t total, int r0, int r1, int r2, double sigma_near,
+                      uint64_t seed, double* out) {
+    try {
+        tg::SamplingConfig c;
+        c.total = total;
+        c.ratio = {r0, r1, r2};
+        c.sigma_near = sigma_near;
+        c.seed = seed;
+        const tg::SampleSet s = tg::sample_sphere_points(radius, c);
+        for (std::size_t i = 0; i < s.samples.size(); ++i) {
+            for (int a = 0; a < 3; ++a) out[4 * i + a] = s.samples[i].point[a];
+            out[4 * i + 3] = s.samples[i].gt_sdf;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+// Raw Rng stream access for pinning the product's seeded generator.
+void tgr_rng_uniform(uint64_t seed, int64_t n, double* out) {
+    tg::Rng r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = r.uniform();
+}
+void tgr_rng_gaussian(uint64_t seed, int64_t n, double* out) {
+    tg::Rng r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = r.gaussian();
+}
+
+int tgr_upsample(int dim, const int* res, const double* origin, const double* extent, int order,
+                 const double* coeffs, const int* new_res, double* out) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        const tg::TaylorGrid grid = make_grid(spec, coeffs);
+        const tg::TaylorGrid up = tg::upsample(grid, {new_res[0], new_res[1], new_res[2]});
+        std::memcpy(out, up.coeffs.data(), up.coeffs.size() * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,438 @@
+/*
+ * TEST INFRASTRUCTURE — NOT PART OF THE PRODUCT. See tg_oracle.h.
+ *
+ * Plain-C fp64 restatement of the reference hot path. Every operation keeps
+ * the reference's association order (no FMA contraction: built with
+ * -ffp-contract=off) so results agree with the reference build bit for bit;
+ * tests/test_oracle_cpu.py asserts exactly that.
+ */
+#include "tg_oracle.h"
+
+#include <math.h>
+#include <stddef.h>
+#include <string.h>
+
+/* Hessian upper-triangle pairs, row-major (taylor_grid.cpp:14-15). */
+static const int kPairs2[3][2] = {{0, 0}, {0, 1}, {1, 1}};
+static const int kPairs3[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+
+int tgo_coeff_count(int order, int dim) {
+    if (dim != 2 && dim != 3) return -1;
+    if (order < 0 || order > 2) return -1;
+    if (order == 0) return 1;
+    if (order == 1) return 1 + dim;
+    return 1 + dim + dim * (dim + 1) / 2;
+}
+
+int64_t tgo_vertex_count(const tgo_spec* s) {
+    int64_t n = 1;
+    for (int a = 0; a < s->dim; ++a) n *= s->res[a];
+    return n;
+}
+
+/* GridSpec::spacing (grid_spec.hpp:29). */
+static double spacing(const tgo_spec* s, int a) { return s->extent[a] / (s->res[a] - 1); }
+
+/* GridSpec::vertex_index, x fastest (grid_spec.hpp:41-45). */
+static int64_t vertex_index(const tgo_spec* s, const int v[3]) {
+    int64_t idx = v[s->dim - 1];
+    for (int a = s->dim - 2; a >= 0; --a) idx = idx * s->res[a] + v[a];
+    return idx;
+}
+
+/* locate: NaN check, clamp_point, fp64 division, floor, clamp to the last
+ * cell (grid_spec.cpp:35-43, :45-69). */
+int tgo_locate(const tgo_spec* s, const double p_in[3], int cell[3], double local[3],
+               int64_t vid[8]) {
+    for (int a = 0; a < s->dim; ++a)
+        if (isnan(p_in[a])) return -1;
+    cell[0] = cell[1] = cell[2] = 0;
+    local[0] = local[1] = local[2] = 0.0;
+    for (int a = 0; a < s->dim; ++a) {
+        const double lo = s->origin[a];
+        const double hi = s->origin[a] + s->extent[a];
+        const double p = p_in[a] < lo ? lo : (p_in[a] > hi ? hi : p_in[a]);
+        const double h = spacing(s, a);
+        const double t = (p - s->origin[a]) / h;
+        int c = (int)floor(t);
+        const int max_cell = s->res[a] - 2;
+        if (c < 0) c = 0;
+        if (c > max_cell) c = max_cell;
+        cell[a] = c;
+        local[a] = t - c;
+    }
+    const int corners = 1 << s->dim;
+    for (int c = 0; c < corners; ++c) {
+        int v[3] = {cell[0], cell[1], cell[2]};
+        for (int a = 0; a < s->dim; ++a) v[a] += (c >> a) & 1;
+        vid[c] = vertex_index(s, v);
+    }
+    return 0;
+}
+
+/* Per-corner multilinear geometry (taylor_grid.cpp:29-64). */
+typedef struct {
+    int count;
+    double w[8];
+    double dw[8][3];
+    double delta[8][3];
+    int64_t vid[8];
+} corners_t;
+
+static void make_corners(const tgo_spec* s, const double local[3], const int64_t vid[8],
+                         corners_t* c) {
+    double h[3] = {1.0, 1.0, 1.0};
+    double inv_h[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < s->dim; ++a) {
+        h[a] = spacing(s, a);
+        inv_h[a] = 1.0 / h[a];
+    }
+    c->count = 1 << s->dim;
+    for (int i = 0; i < c->count; ++i) {
+        double sa[3];
+        int bit[3] = {0, 0, 0};
+        for (int a = 0; a < s->dim; ++a) {
+            bit[a] = (i >> a) & 1;
+            sa[a] = bit[a] ? local[a] : 1.0 - local[a];
+        }
+        double w = 1.0;
+        for (int a = 0; a < s->dim; ++a) w *= sa[a];
+        c->w[i] = w;
+        for (int a = 0; a < 3; ++a) c->dw[i][a] = 0.0;
+        for (int a = 0; a < s->dim; ++a) {
+            double other = 1.0;
+            for (int b = 0; b < s->dim; ++b)
+                if (b != a) other *= sa[b];
+            c->dw[i][a] = (bit[a] ? 1.0 : -1.0) * inv_h[a] * other;
+        }
+        for (int a = 0; a < 3; ++a) c->delta[i][a] = 0.0;
+        for (int a = 0; a < s->dim; ++a) c->delta[i][a] = (local[a] - bit[a]) * h[a];
+        c->vid[i] = vid[i];
+    }
+}
+
+/* One vertex's truncated Taylor polynomial and its offset gradient
+ * (taylor_grid.cpp:68-98). grad may be NULL. */
+static double taylor_poly(const double* b, int order, int dim, const double d[3], double grad[3]) {
+    double v = b[0];
+    if (grad) grad[0] = grad[1] = grad[2] = 0.0;
+    if (order >= 1) {
+        for (int a = 0; a < dim; ++a) {
+            v += b[1 + a] * d[a];
+            if (grad) grad[a] += b[1 + a];
+        }
+    }
+    if (order >= 2) {
+        const int(*pairs)[2] = dim == 2 ? kPairs2 : kPairs3;
+        const int npairs = dim * (dim + 1) / 2;
+        const double* q = b + 1 + dim;
+        for (int t = 0; t < npairs; ++t) {
+            const int j = pairs[t][0], k = pairs[t][1];
+            const double c = q[t];
+            if (j == k) {
+                v += 0.5 * c * d[j] * d[j];
+                if (grad) grad[j] += c * d[j];
+            } else {
+                v += c * d[j] * d[k];
+                if (grad) {
+                    grad[j] += c * d[k];
+                    grad[k] += c * d[j];
+                }
+            }
+        }
+    }
+    return v;
+}
+
+double tgo_eval(const tgo_spec* s, const double* coeffs, const double p[3], double grad_out[3]) {
+    int cell[3];
+    double local[3];
+    int64_t vid[8];
+    if (tgo_locate(s, p, cell, local, vid) != 0) return NAN;
+    corners_t c;
+    make_corners(s, local, vid, &c);
+    const int K = tgo_coeff_count(s->order, s->dim);
+    double value = 0.0;
+    double g[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < c.count; ++i) {
+        const double* b = coeffs + c.vid[i] * K;
+        double tg[3];
+        const double tv = taylor_poly(b, s->order, s->dim, c.delta[i], grad_out ? tg : NULL);
+        value += c.w[i] * tv;
+        if (grad_out)
+            for (int a = 0; a < s->dim; ++a) g[a] += c.dw[i][a] * tv + c.w[i] * tg[a];
+    }
+    if (grad_out) {
+        grad_out[0] = g[0];
+        grad_out[1] = g[1];
+        grad_out[2] = g[2];
+    }
+    return value;
+}
+
+/* accumulate_cell (taylor_grid.cpp:123-152). */
+static void accumulate_cell(const tgo_spec* s, const corners_t* c, double upstream,
+                            const double gvec[3], double* grad) {
+    const int K = tgo_coeff_count(s->order, s->dim);
+    const int dim = s->dim;
+    for (int i = 0; i < c->count; ++i) {
+        double* g = grad + c->vid[i] * K;
+        const double* d = c->delta[i];
+        const double dot = gvec[0] * c->dw[i][0] + gvec[1] * c->dw[i][1] + gvec[2] * c->dw[i][2];
+        const double alpha = upstream * c->w[i] + dot;
+        const double beta = c->w[i];
+        g[0] += alpha;
+        if (s->order >= 1)
+            for (int a = 0; a < dim; ++a) g[1 + a] += alpha * d[a] + beta * gvec[a];
+        if (s->order >= 2) {
+            const int(*pairs)[2] = dim == 2 ? kPairs2 : kPairs3;
+            const int npairs = dim * (dim + 1) / 2;
+            double* q = g + 1 + dim;
+            for (int t = 0; t < npairs; ++t) {
+                const int j = pairs[t][0], k = pairs[t][1];
+                if (j == k)
+                    q[t] += alpha * 0.5 * d[j] * d[j] + beta * gvec[j] * d[j];
+                else
+                    q[t] += alpha * d[j] * d[k] + beta * (gvec[j] * d[k] + gvec[k] * d[j]);
+            }
+        }
+    }
+}
+
+void tgo_backprop(const tgo_spec* s, const double p[3], double upstream, const double gvec[3],
+                  double* grad) {
+    int cell[3];
+    double local[3];
+    int64_t vid[8];
+    if (tgo_locate(s, p, cell, local, vid) != 0) return;
+    corners_t c;
+    make_corners(s, local, vid, &c);
+    accumulate_cell(s, &c, upstream, gvec, grad);
+}
+
+/* sigmoid / w' / dw'/dd / sign (sdf_loss.cpp:15-27). */
+static double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
+static double w_prime(double d, double k) { return 1.0 - fabs(2.0 * sigmoid(k * d) - 1.0); }
+static double w_prime_deriv(double d, double k) {
+    if (d == 0.0) return 0.0;
+    const double s = sigmoid(k * d);
+    const double ds = 2.0 * k * s * (1.0 - s);
+    return d > 0.0 ? -ds : ds;
+}
+static double sign_of(double x) { return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0); }
+
+double tgo_adaptive_weight(double d_hat, double d, double k) {
+    const double a = w_prime(d_hat, k), b = w_prime(d, k);
+    return a < b ? b : a; /* std::max */
+}
+
+/* tv_loss: x/y pairs slice by slice, then z pairs in the even/odd phase
+ * order the reference uses, so per-vertex accumulation order matches
+ * (sdf_loss.cpp:155-257). */
+double tgo_tv_loss(const tgo_spec* s, const double* coeffs, double* g, double scale) {
+    const int K = tgo_coeff_count(s->order, s->dim);
+    const int dim = s->dim;
+    int64_t pair_count = 0;
+    for (int a = 0; a < dim; ++a) {
+        int64_t n = s->res[a] - 1;
+        for (int b = 0; b < dim; ++b)
+            if (b != a) n *= s->res[b];
+        pair_count += n;
+    }
+    const double inv_norm = 1.0 / ((double)pair_count * K);
+    const double gscale = 2.0 * scale * inv_norm;
+    const int rx = s->res[0], ry = s->res[1], rz = dim == 3 ? s->res[2] : 1;
+    const int64_t sy = rx, sz = (int64_t)rx * ry;
+
+    double total = 0.0;
+    for (int z = 0; z < rz; ++z) {
+        double sum = 0.0;
+        for (int y = 0; y < ry; ++y) {
+            for (int x = 0; x < rx; ++x) {
+                const int64_t v = z * sz + y * sy + x;
+                const double* cv = coeffs + v * K;
+                if (x + 1 < rx) {
+                    const double* cu = cv + K;
+                    for (int ch = 0; ch < K; ++ch) {
+                        const double d = cu[ch] - cv[ch];
+                        sum += d * d;
+                        if (g) {
+                            g[v * K + ch] -= gscale * d;
+                            g[v * K + K + ch] += gscale * d;
+                        }
+                    }
+                }
+                if (y + 1 < ry) {
+                    const double* cu = cv + sy * K;
+                    for (int ch = 0; ch < K; ++ch) {
+                        const double d = cu[ch] - cv[ch];
+                        sum += d * d;
+                        if (g) {
+                            g[v * K + ch] -= gscale * d;
+                            g[(v + sy) * K + ch] += gscale * d;
+                        }
+                    }
+                }
+            }
+        }
+        total += sum;
+    }
+    if (dim == 3 && rz > 1) {
+        /* z pairs: the reference runs even z then odd z (two phases) for the
+         * grad, and adds per-z sums in z order for the value. */
+        for (int phase = 0; phase < 2; ++phase) {
+            for (int z = phase; z < rz - 1; z += 2) {
+                for (int64_t i = 0; i < sz; ++i) {
+                    const int64_t v = z * sz + i;
+                    const double* cv = coeffs + v * K;
+                    const double* cu = cv + sz * K;
+                    for (int ch = 0; ch < K; ++ch) {
+                        const double d = cu[ch] - cv[ch];
+                        if (g) {
+                            g[v * K + ch] -= gscale * d;
+                            g[(v + sz) * K + ch] += gscale * d;
+                        }
+                    }
+                }
+            }
+        }
+        for (int z = 0; z < rz - 1; ++z) {
+            double sum = 0.0;
+            for (int64_t i = 0; i < sz; ++i) {
+                const double* cv = coeffs + (z * sz + i) * K;
+                const double* cu = cv + sz * K;
+                for (int ch = 0; ch < K; ++ch) {
+                    const double d = cu[ch] - cv[ch];
+                    sum += d * d;
+                }
+            }
+            total += sum;
+        }
+    }
+    return total * inv_norm;
+}
+
+/* point_terms_chunk, sequential (sdf_loss.cpp:37-85). */
+static void point_terms(const tgo_spec* s, const double* coeffs, const double* samples, int64_t n,
+                        const tgo_loss_cfg* cfg, int want_eik, double recon_scale,
+                        double eik_scale, double* grad, double* recon_out, double* eik_out) {
+    const double inv_n = 1.0 / (double)n;
+    double recon = 0.0, eik = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        const double* sm = samples + 4 * i;
+        double p[3] = {sm[0], sm[1], s->dim == 3 ? sm[2] : 0.0};
+        const double gt = sm[3];
+        double sg[3] = {0.0, 0.0, 0.0};
+        const double value = tgo_eval(s, coeffs, p, want_eik ? sg : NULL);
+        const double resid = value - gt;
+        const double w = cfg->use_weighting ? tgo_adaptive_weight(value, gt, cfg->k) : 1.0;
+        recon += w * fabs(resid);
+        double upstream = 0.0;
+        double uvec[3] = {0.0, 0.0, 0.0};
+        if (grad) {
+            upstream = recon_scale * inv_n * w * sign_of(resid);
+            if (cfg->use_weighting && cfg->differentiate_weight) {
+                const double wp_pred = w_prime(value, cfg->k);
+                const double wp_gt = w_prime(gt, cfg->k);
+                if (wp_pred > wp_gt)
+                    upstream += recon_scale * inv_n * fabs(resid) * w_prime_deriv(value, cfg->k);
+            }
+        }
+        if (want_eik) {
+            const double nrm = sqrt(sg[0] * sg[0] + sg[1] * sg[1] + sg[2] * sg[2]);
+            const double r = nrm - 1.0;
+            eik += r * r;
+            if (grad && nrm > 0.0) {
+                const double sc = eik_scale * inv_n * 2.0 * r / nrm;
+                uvec[0] = sc * sg[0];
+                uvec[1] = sc * sg[1];
+                uvec[2] = sc * sg[2];
+            }
+        }
+        if (grad) tgo_backprop(s, p, upstream, uvec, grad);
+    }
+    *recon_out = recon;
+    *eik_out = eik;
+}
+
+void tgo_total_loss(const tgo_spec* s, const double* coeffs, const double* samples, int64_t n,
+                    const tgo_loss_cfg* cfg, double* grad, double terms_out[4]) {
+    double fit = 0.0, eik = 0.0, tv = 0.0, recon_sum = 0.0, eik_sum = 0.0;
+    const int want_eik = cfg->lambda1 > 0.0;
+    point_terms(s, coeffs, samples, n, cfg, want_eik, 1.0, want_eik ? cfg->lambda1 : 0.0, grad,
+                &recon_sum, &eik_sum);
+    fit = recon_sum / (double)n;
+    if (want_eik) eik = eik_sum / (double)n;
+    if (cfg->use_tv && cfg->lambda2 > 0.0)
+        tv = tgo_tv_loss(s, coeffs, grad, cfg->lambda2);
+    else if (cfg->use_tv)
+        tv = tgo_tv_loss(s, coeffs, NULL, 1.0);
+    terms_out[0] = fit + cfg->lambda1 * eik + cfg->lambda2 * tv;
+    terms_out[1] = fit;
+    terms_out[2] = eik;
+    terms_out[3] = tv;
+}
+
+int64_t tgo_adam_step(double* p, const double* g, double* m, double* v, int64_t n, int64_t* t,
+                      double lr, double beta1, double beta2, double eps) {
+    for (int64_t i = 0; i < n; ++i)
+        if (!isfinite(g[i])) return i;
+    *t += 1;
+    const double bc1 = 1.0 - pow(beta1, (double)*t);
+    const double bc2 = 1.0 - pow(beta2, (double)*t);
+    for (int64_t i = 0; i < n; ++i) {
+        const double gi = g[i];
+        m[i] = beta1 * m[i] + (1.0 - beta1) * gi;
+        v[i] = beta2 * v[i] + (1.0 - beta2) * gi * gi;
+        const double mhat = m[i] / bc1;
+        const double vhat = v[i] / bc2;
+        p[i] -= lr * mhat / (sqrt(vhat) + eps);
+    }
+    return -1;
+}
+
+void tgo_multilinear_resample(const tgo_spec* old_spec, const double* data, int channels,
+                              const int new_res[3], double* out) {
+    tgo_spec ng = *old_spec;
+    for (int a = 0; a < 3; ++a) ng.res[a] = new_res[a];
+    const int dim = ng.dim;
+    const int64_t nv = tgo_vertex_count(&ng);
+    memset(out, 0, sizeof(double) * (size_t)(nv * channels));
+    int v[3] = {0, 0, 0};
+    for (int64_t idx = 0; idx < nv; ++idx) {
+        double p[3] = {0.0, 0.0, 0.0};
+        for (int a = 0; a < dim; ++a) p[a] = ng.origin[a] + spacing(&ng, a) * v[a];
+        int cell[3];
+        double local[3];
+        int64_t vid[8];
+        tgo_locate(old_spec, p, cell, local, vid);
+        double w[8];
+        const int corners = 1 << dim;
+        for (int i = 0; i < corners; ++i) {
+            double wi = 1.0;
+            for (int a = 0; a < dim; ++a) {
+                const int bit = (i >> a) & 1;
+                wi *= bit ? local[a] : 1.0 - local[a];
+            }
+            w[i] = wi;
+        }
+        double* dst = out + idx * channels;
+        for (int i = 0; i < corners; ++i) {
+            const double* src = data + vid[i] * channels;
+            for (int ch = 0; ch < channels; ++ch) dst[ch] += w[i] * src[ch];
+        }
+        for (int a = 0; a < dim; ++a) {
+            if (++v[a] < ng.res[a]) break;
+            v[a] = 0;
+        }
+    }
+}
+
+/* Test helper: the device locate's division t = x / h via Markstein's
+ * correction with a correctly rounded reciprocal (tg_device.cuh div_by_h),
+ * evaluated with C99 fma so the CPU test can compare it with IEEE division. */
+double tgo_markstein_div(double x, double h, double inv_h) {
+    const double q = x * inv_h;
+    const double r = fma(-q, h, x);
+    return fma(r, inv_h, q);
+}

@@ -1,0 +1,716 @@
+// C-ABI entry points of libtgcu (include/tgcu.h): handle lifetime, host/device
+// staging, error mapping, and the stream-ordered drivers of the kernels.
+#include <atomic>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tg_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+int set_err(int code, const std::string& m) {
+    g_err = m;
+    return code;
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return TGCU_OK;
+    } catch (const tgcu::Error& e) {
+        return set_err(e.code, e.what());
+    } catch (const std::bad_alloc& e) {
+        return set_err(TGCU_ERR_RESOURCE, e.what());
+    } catch (const std::exception& e) {
+        return set_err(TGCU_ERR_CUDA, e.what());
+    }
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+namespace tgcu {
+
+void count_launch(int n) { g_launches += n; }
+
+static void set_device(const Grid& g) { TGCU_CUDA(cudaSetDevice(g.device)); }
+
+void prof_mark(Grid& g, cudaStream_t s, int which) {
+    if (which == 0 && g.prof_used + 2 > g.prof_ev.size()) {
+        for (int i = 0; i < 256; ++i) {
+            cudaEvent_t e;
+            TGCU_CUDA(cudaEventCreate(&e));
+            g.prof_ev.push_back(e);
+        }
+    }
+    TGCU_CUDA(cudaEventRecord(g.prof_ev[g.prof_used++], s));
+}
+
+void ensure_staging(Grid& g, int64_t floats) {
+    if (g.staging_cap >= floats) return;
+    if (g.staging) TGCU_CUDA(cudaFree(g.staging));
+    g.staging = nullptr;
+    TGCU_CUDA(cudaMalloc(&g.staging, sizeof(float) * floats));
+    g.staging_cap = floats;
+}
+
+void ensure_scratch(Grid& g, int64_t doubles) {
+    if (g.scratch_cap >= doubles) return;
+    if (g.scratch_d) TGCU_CUDA(cudaFree(g.scratch_d));
+    g.scratch_d = nullptr;
+    TGCU_CUDA(cudaMalloc(&g.scratch_d, sizeof(double) * doubles));
+    g.scratch_cap = doubles;
+}
+
+void ensure_bins(Grid& g, int64_t points) {
+    const int64_t need = points << g.spec.dim;  // worst case 2^D copies per point
+    if (g.binned_cap >= need) return;
+    if (g.binned) TGCU_CUDA(cudaFree(g.binned));
+    g.binned = nullptr;
+    TGCU_CUDA(cudaMalloc(&g.binned, sizeof(float4) * need));
+    g.binned_cap = need;
+}
+
+// Ping-pong parameters + Adam moments (both slots), zero moments.
+void ensure_optimizer(Grid& g) {
+    if (g.m[0]) return;
+    if (!g.p[1]) TGCU_CUDA(cudaMalloc(&g.p[1], sizeof(float) * g.NC));
+    for (int i = 0; i < 2; ++i) {
+        TGCU_CUDA(cudaMalloc(&g.m[i], sizeof(float) * g.NC));
+        TGCU_CUDA(cudaMalloc(&g.v[i], sizeof(float) * g.NC));
+        TGCU_CUDA(cudaMemset(g.m[i], 0, sizeof(float) * g.NC));
+        TGCU_CUDA(cudaMemset(g.v[i], 0, sizeof(float) * g.NC));
+    }
+}
+
+void ensure_grad(Grid& g) {
+    if (g.grad) return;
+    TGCU_CUDA(cudaMalloc(&g.grad, sizeof(float) * g.NC));
+    TGCU_CUDA(cudaMemset(g.grad, 0, sizeof(float) * g.NC));
+}
+
+static void validate_spec(const tgcu_grid_spec& s) {
+    // GridSpec::validate (grid_spec.cpp:21-33) + coeff_count ranges.
+    require(s.dim == 2 || s.dim == 3, "coeff_count: dim must be 2 or 3, got " + std::to_string(s.dim));
+    require(s.order >= 0 && s.order <= 2, "coeff_count: order must be in {0,1,2}, got " + std::to_string(s.order));
+    for (int a = 0; a < s.dim; ++a) {
+        require(s.res[a] >= 2, "GridSpec: resolution must be >= 2 per axis, got " + std::to_string(s.res[a]) +
+                                   " on axis " + std::to_string(a));
+        require(s.extent[a] > 0.0 && std::isfinite(s.extent[a]),
+                "GridSpec: extent must be positive and finite on axis " + std::to_string(a));
+        require(std::isfinite(s.origin[a]), "GridSpec: origin must be finite");
+        const double h = s.extent[a] / (s.res[a] - 1);
+        require(std::isfinite(h) && h > 0.0, "GridSpec: cell spacing must be positive");
+    }
+}
+
+static int coeff_count_of(int order, int dim) {
+    return order == 0 ? 1 : (order == 1 ? 1 + dim : 1 + dim + dim * (dim + 1) / 2);
+}
+
+// Seeded host generator with the reference Rng semantics (rng.hpp:14-51).
+struct HostRng {
+    uint64_t mt[312];
+    int idx = 312;
+    explicit HostRng(uint64_t seed) {
+        mt[0] = seed;
+        for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i;
+    }
+    uint64_t next() {
+        if (idx >= 312) {
+            for (int i = 0; i < 312; ++i) {
+                const uint64_t x = (mt[i] & 0xFFFFFFFF80000000ULL) | (mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+                uint64_t xa = x >> 1;
+                if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+                mt[i] = mt[(i + 156) % 312] ^ xa;
+            }
+            idx = 0;
+        }
+        uint64_t x = mt[idx++];
+        x ^= (x >> 29) & 0x5555555555555555ULL;
+        x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+        x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+        x ^= x >> 43;
+        return x;
+    }
+    double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+};
+
+}  // namespace tgcu
+
+using namespace tgcu;
+
+extern "C" {
+
+const char* tgcu_last_error(void) { return g_err.c_str(); }
+const char* tgcu_version(void) { return "tgcu 0.1 (sm_100a)"; }
+int64_t tgcu_launch_count(void) { return g_launches.load(); }
+void tgcu_reset_launch_count(void) { g_launches = 0; }
+
+int tgcu_coeff_count(int order, int dim, int* out) {
+    return guard([&] {
+        require(dim == 2 || dim == 3, "coeff_count: dim must be 2 or 3, got " + std::to_string(dim));
+        require(order >= 0 && order <= 2, "coeff_count: order must be in {0,1,2}, got " + std::to_string(order));
+        *out = coeff_count_of(order, dim);
+    });
+}
+
+int tgcu_grid_create(const tgcu_grid_spec* spec, const tgcu_init_options* opts_in, int device, tgcu_grid** out) {
+    *out = nullptr;
+    tgcu_grid* h = nullptr;
+    const int rc = guard([&] {
+        require(spec != nullptr, "tgcu_grid_create: spec is NULL");
+        tgcu_grid_spec s = *spec;
+        if (s.dim == 2) s.res[2] = 1;
+        validate_spec(s);
+        tgcu_init_options opts{TGCU_INIT_ZEROS, 0.0, 1e-4, 0, 4ull << 30};
+        if (opts_in) opts = *opts_in;
+        const int K = coeff_count_of(s.order, s.dim);
+        int64_t V = 1;
+        for (int a = 0; a < s.dim; ++a) V *= s.res[a];
+        const uint64_t bytes = (uint64_t)(V * K) * sizeof(double);
+        if (bytes > opts.memory_cap_bytes)
+            throw Error(TGCU_ERR_RESOURCE, "init_grid: " + std::to_string(bytes) + " bytes exceeds memory cap of " +
+                                               std::to_string(opts.memory_cap_bytes));
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw Error(TGCU_ERR_CUDA, "tgcu: no CUDA device available (the product path has no CPU fallback)");
+        require(device >= 0 && device < ndev, "tgcu_grid_create: bad device " + std::to_string(device));
+        h = new tgcu_grid();
+        Grid& g = h->g;
+        g.spec = s;
+        g.K = K;
+        g.V = V;
+        g.NC = V * K;
+        g.device = device;
+        TGCU_CUDA(cudaSetDevice(device));
+        DevSpec& d = g.ds;
+        for (int a = 0; a < 3; ++a) {
+            const bool act = a < s.dim;
+            d.res[a] = act ? s.res[a] : 1;
+            d.origin[a] = act ? s.origin[a] : 0.0;
+            d.hi[a] = act ? s.origin[a] + s.extent[a] : 0.0;
+            d.h[a] = act ? s.extent[a] / (s.res[a] - 1) : 1.0;
+            d.inv_h[a] = act ? 1.0 / d.h[a] : 0.0;
+            d.hf[a] = (float)d.h[a];
+            d.inv_hf[a] = (float)d.inv_h[a];
+        }
+        d.sy = s.res[0];
+        d.sz = (long long)s.res[0] * (s.dim == 3 ? s.res[1] : 1);
+        // Parameters now; the ping-pong copy and the Adam moments on first
+        // optimiser use (ensure_optimizer), so query-only grids cost 4 B/coeff.
+        TGCU_CUDA(cudaMalloc(&g.p[0], sizeof(float) * g.NC));
+        TGCU_CUDA(cudaMalloc(&g.st, sizeof(Status)));
+        TGCU_CUDA(cudaMallocHost(&g.st_host, sizeof(Status)));
+        Status st0{};
+        st0.nan_point = ULLONG_MAX;
+        st0.bad_grad = ULLONG_MAX;
+        TGCU_CUDA(cudaMemcpy(g.st, &st0, sizeof(Status), cudaMemcpyHostToDevice));
+        // Brick decomposition (train.cu / query.cu).
+        const int B = s.dim == 3 ? kBrick3 : kBrick2;
+        g.NB = 1;
+        for (int a = 0; a < 3; ++a) {
+            g.brick[a] = a < s.dim ? B : 1;
+            g.nb[a] = a < s.dim ? (s.res[a] + B - 1) / B : 1;
+            g.NB *= g.nb[a];
+        }
+        TGCU_CUDA(cudaMalloc(&g.bin_count, sizeof(int) * (g.NB + 1)));
+        TGCU_CUDA(cudaMalloc(&g.bin_off, sizeof(int) * (g.NB + 1)));
+        TGCU_CUDA(cudaMalloc(&g.bin_cursor, sizeof(int) * (g.NB + 1)));
+        TGCU_CUDA(cudaMalloc(&g.partials, sizeof(double) * 4 * g.NB));
+        TGCU_CUDA(cudaMalloc(&g.d_trace, sizeof(tgcu_loss_terms) * kTraceCap));
+        TGCU_CUDA(cudaMallocHost(&g.h_terms, sizeof(tgcu_loss_terms)));
+        // init_grid modes (taylor_grid.cpp:174-186).
+        float* p = g.p[0];
+        TGCU_CUDA(cudaMemset(p, 0, sizeof(float) * g.NC));
+        if (opts.mode == TGCU_INIT_CONSTANT) {
+            launch_fill_f0(g, p, (float)opts.constant, 0);
+        } else if (opts.mode == TGCU_INIT_SMALL_UNIFORM) {
+            std::vector<float> hbuf(g.NC);
+            HostRng r(opts.seed);
+            for (int64_t i = 0; i < g.NC; ++i) hbuf[i] = (float)r.uniform(-opts.epsilon, opts.epsilon);
+            TGCU_CUDA(cudaMemcpy(p, hbuf.data(), sizeof(float) * g.NC, cudaMemcpyHostToDevice));
+        } else if (opts.mode == TGCU_INIT_HASH_GAUSSIAN) {
+            launch_hash_gaussian(p, g.NC, opts.seed, opts.epsilon, 0);
+        }
+        TGCU_CUDA(cudaDeviceSynchronize());
+    });
+    if (rc != TGCU_OK) {
+        if (h) tgcu_grid_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return TGCU_OK;
+}
+
+int tgcu_grid_destroy(tgcu_grid* h) {
+    if (!h) return TGCU_OK;
+    Grid& g = h->g;
+    cudaSetDevice(g.device);
+    cudaDeviceSynchronize();
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(g.p[i]);
+        cudaFree(g.m[i]);
+        cudaFree(g.v[i]);
+    }
+    cudaFree(g.grad);
+    cudaFree(g.st);
+    cudaFreeHost(g.st_host);
+    cudaFree(g.bin_count);
+    cudaFree(g.bin_off);
+    cudaFree(g.bin_cursor);
+    cudaFree(g.binned);
+    cudaFree(g.partials);
+    cudaFree(g.d_trace);
+    cudaFreeHost(g.h_terms);
+    cudaFree(g.staging);
+    cudaFree(g.scratch_d);
+    for (auto e : g.prof_ev) cudaEventDestroy(e);
+    delete h;
+    return TGCU_OK;
+}
+
+int tgcu_grid_spec_of(const tgcu_grid* h, tgcu_grid_spec* out) {
+    *out = h->g.spec;
+    return TGCU_OK;
+}
+int64_t tgcu_grid_coeff_total(const tgcu_grid* h) { return h->g.NC; }
+float* tgcu_grid_coeffs(tgcu_grid* h) { return h->g.p[h->g.cur]; }
+float* tgcu_grid_grad(tgcu_grid* h) {
+    float* r = nullptr;
+    guard([&] {
+        set_device(h->g);
+        ensure_grad(h->g);
+        r = h->g.grad;
+    });
+    return r;
+}
+
+static void check_n(const Grid& g, int64_t n, const char* what) {
+    require(n == g.NC, std::string(what) + ": coefficient array has " + std::to_string(n) +
+                           " entries, expected " + std::to_string(g.NC));
+}
+
+// Sticky async error -> exception (with the committed state restored).
+static void raise_sticky(Grid& g) {
+    TGCU_CUDA(cudaMemcpy(g.st_host, g.st, sizeof(Status), cudaMemcpyDeviceToHost));
+    const Status& s = *g.st_host;
+    if (!s.error) return;
+    g.cur = s.good_idx;
+    g.t = s.good_t;
+    std::string msg;
+    if (s.error_kind == 1)
+        msg = "locate: NaN coordinate (sample " + std::to_string(s.error_index) + ") at stage 0 step " +
+              std::to_string(s.error_step);
+    else if (s.error_kind == 2)
+        msg = "run_schedule: non-finite loss at stage 0 step " + std::to_string(s.error_step);
+    else
+        msg = "adam_step: non-finite gradient at parameter index " + std::to_string(s.error_index) +
+              " (stage 0 step " + std::to_string(s.error_step) + ")";
+    // Clear so the grid is usable again (the reference object survives a throw).
+    Status clean = s;
+    clean.error = 0;
+    clean.error_kind = 0;
+    clean.nan_point = ULLONG_MAX;
+    clean.bad_grad = ULLONG_MAX;
+    TGCU_CUDA(cudaMemcpy(g.st, &clean, sizeof(Status), cudaMemcpyHostToDevice));
+    g.steps_launched = 0;
+    throw Error(s.error, msg);
+}
+
+// Per-call NaN point report for the stateless query/backprop calls.
+static void check_nan_points(Grid& g, cudaStream_t s) {
+    TGCU_CUDA(cudaMemcpyAsync(g.st_host, g.st, sizeof(Status), cudaMemcpyDeviceToHost, s));
+    TGCU_CUDA(cudaStreamSynchronize(s));
+    if (g.st_host->nan_point != ULLONG_MAX) {
+        const unsigned long long idx = g.st_host->nan_point;
+        const unsigned long long none = ULLONG_MAX;
+        TGCU_CUDA(cudaMemcpy(&g.st->nan_point, &none, sizeof(none), cudaMemcpyHostToDevice));
+        throw Error(TGCU_ERR_INVALID_ARGUMENT, "locate: NaN coordinate (point " + std::to_string(idx) + ")");
+    }
+}
+
+int tgcu_grid_upload_f64(tgcu_grid* h, const double* coeffs, int64_t n) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        check_n(g, n, "upload");
+        std::vector<float> tmp(n);
+        for (int64_t i = 0; i < n; ++i) tmp[i] = (float)coeffs[i];
+        TGCU_CUDA(cudaMemcpy(g.p[g.cur], tmp.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+    });
+}
+
+int tgcu_grid_download_f64(tgcu_grid* h, double* coeffs, int64_t n) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        check_n(g, n, "download");
+        raise_sticky(g);
+        std::vector<float> tmp(n);
+        TGCU_CUDA(cudaMemcpy(tmp.data(), g.p[g.cur], sizeof(float) * n, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i) coeffs[i] = tmp[i];
+    });
+}
+
+int tgcu_grid_upload_f32(tgcu_grid* h, const float* coeffs, int64_t n, int flags) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        check_n(g, n, "upload");
+        TGCU_CUDA(cudaMemcpy(g.p[g.cur], coeffs, sizeof(float) * n,
+                             (flags & TGCU_HOST) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice));
+    });
+}
+
+int tgcu_grid_download_f32(tgcu_grid* h, float* coeffs, int64_t n, int flags) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        check_n(g, n, "download");
+        raise_sticky(g);
+        TGCU_CUDA(cudaMemcpy(coeffs, g.p[g.cur], sizeof(float) * n,
+                             (flags & TGCU_HOST) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice));
+    });
+}
+
+int tgcu_grid_all_finite(tgcu_grid* h, int* out) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        unsigned long long* flag = nullptr;
+        TGCU_CUDA(cudaMalloc(&flag, sizeof(unsigned long long)));
+        const unsigned long long none = ULLONG_MAX;
+        TGCU_CUDA(cudaMemcpy(flag, &none, sizeof(none), cudaMemcpyHostToDevice));
+        launch_all_finite(g.p[g.cur], g.NC, flag, 0);
+        unsigned long long r = 0;
+        TGCU_CUDA(cudaMemcpy(&r, flag, sizeof(r), cudaMemcpyDeviceToHost));
+        cudaFree(flag);
+        *out = r == ULLONG_MAX ? 1 : 0;
+    });
+}
+
+int tgcu_eval(tgcu_grid* h, const float* pts, int64_t n, float* values, float* spatial_grad, int flags,
+              void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(n >= 0, "eval: negative point count");
+        if (n == 0) return;
+        cudaStream_t s = as_stream(stream);
+        const float* dp = pts;
+        float* dv = values;
+        float* dg = spatial_grad;
+        if (flags & TGCU_HOST) {
+            const int64_t need = n * 3 + n + (spatial_grad ? 3 * n : 0);
+            ensure_staging(g, need);
+            float* sp = g.staging;
+            dv = sp + 3 * n;
+            dg = spatial_grad ? dv + n : nullptr;
+            TGCU_CUDA(cudaMemcpyAsync(sp, pts, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, s));
+            dp = sp;
+        }
+        if (flags & TGCU_SORTED)
+            launch_eval_sorted(g, dp, n, dv, dg, s);
+        else
+            launch_eval_direct(g, dp, n, dv, dg, s);
+        if (flags & TGCU_HOST) {
+            TGCU_CUDA(cudaMemcpyAsync(values, dv, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+            if (spatial_grad)
+                TGCU_CUDA(cudaMemcpyAsync(spatial_grad, dg, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, s));
+        }
+        if (!(flags & TGCU_ASYNC) || (flags & TGCU_HOST)) check_nan_points(g, s);
+    });
+}
+
+int tgcu_sort_points(tgcu_grid* h, const float* pts, int64_t n, float* sorted_pts, int64_t* perm, void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        launch_sort_points(g, pts, n, sorted_pts, perm, as_stream(stream));
+    });
+}
+
+int tgcu_backprop(tgcu_grid* h, const float* pts, const float* upstream, const float* upstream_vec, int64_t n,
+                  float* grad, int flags, void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(grad != nullptr, "backprop: gradient buffer is NULL");
+        if (n <= 0) return;
+        cudaStream_t s = as_stream(stream);
+        const float *dp = pts, *du = upstream, *dv = upstream_vec;
+        if (flags & TGCU_HOST) {
+            ensure_staging(g, 7 * n);
+            float* sp = g.staging;
+            TGCU_CUDA(cudaMemcpyAsync(sp, pts, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, s));
+            dp = sp;
+            if (upstream) {
+                TGCU_CUDA(cudaMemcpyAsync(sp + 3 * n, upstream, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+                du = sp + 3 * n;
+            }
+            if (upstream_vec) {
+                TGCU_CUDA(cudaMemcpyAsync(sp + 4 * n, upstream_vec, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, s));
+                dv = sp + 4 * n;
+            }
+        }
+        launch_backprop(g, dp, du, dv, n, grad, s);
+        if (!(flags & TGCU_ASYNC)) check_nan_points(g, s);
+    });
+}
+
+int tgcu_grad_zero(tgcu_grid* h, float* grad, void* stream) {
+    return guard([&] {
+        set_device(h->g);
+        TGCU_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * h->g.NC, as_stream(stream)));
+    });
+}
+
+int tgcu_grad_download_f64(tgcu_grid* h, const float* grad, double* out, int64_t n) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        check_n(g, n, "grad_download");
+        if (!grad) {
+            ensure_grad(g);
+            grad = g.grad;
+        }
+        std::vector<float> tmp(n);
+        TGCU_CUDA(cudaMemcpy(tmp.data(), grad, sizeof(float) * n, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i) out[i] = tmp[i];
+    });
+}
+
+static double pair_count_of(const tgcu_grid_spec& s) {
+    double P = 0.0;
+    for (int a = 0; a < s.dim; ++a) {
+        double np = s.res[a] - 1;
+        for (int b = 0; b < s.dim; ++b)
+            if (b != a) np *= s.res[b];
+        P += np;
+    }
+    return P;
+}
+
+int tgcu_tv_loss(tgcu_grid* h, float* grad, double scale, double* out, void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        cudaStream_t s = as_stream(stream);
+        const double inv_norm = 1.0 / (pair_count_of(g.spec) * g.K);
+        launch_tv(g, g.p[g.cur], grad, 2.0 * scale * inv_norm, 1, s);
+        double sum = 0.0;
+        TGCU_CUDA(cudaMemcpyAsync(&sum, g.scratch_d + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+        TGCU_CUDA(cudaStreamSynchronize(s));
+        *out = sum * inv_norm;
+    });
+}
+
+int tgcu_total_loss(tgcu_grid* h, const float* samples, int64_t n, const tgcu_loss_config* cfg, float* grad,
+                    tgcu_loss_terms* out, int flags, void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(cfg != nullptr, "total_loss: NULL config");
+        // LossConfig::validate (sdf_loss.cpp:118-122) and the empty-batch check (:261).
+        require(cfg->lambda1 >= 0.0 && cfg->lambda2 >= 0.0, "LossConfig: lambda weights must be >= 0");
+        require(cfg->k > 0.0, "LossConfig: weight sharpness k must be > 0");
+        require(n > 0, "total_loss: empty batch");
+        cudaStream_t s = as_stream(stream);
+        const float4* ds = reinterpret_cast<const float4*>(samples);
+        if (flags & TGCU_HOST) {
+            ensure_staging(g, 4 * n);
+            TGCU_CUDA(cudaMemcpyAsync(g.staging, samples, sizeof(float) * 4 * n, cudaMemcpyHostToDevice, s));
+            ds = reinterpret_cast<const float4*>(g.staging);
+        }
+        launch_point_terms(g, ds, n, *cfg, grad, s);
+        double sums[4] = {0, 0, 0, 0};
+        TGCU_CUDA(cudaMemcpyAsync(sums, g.scratch_d, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        TGCU_CUDA(cudaStreamSynchronize(s));
+        check_nan_points(g, s);
+        tgcu_loss_terms t{};
+        t.fit = sums[0] / (double)n;
+        t.eik = cfg->lambda1 > 0.0 ? sums[1] / (double)n : 0.0;
+        if (cfg->use_tv) {
+            const double inv_norm = 1.0 / (pair_count_of(g.spec) * g.K);
+            const bool with_grad = cfg->lambda2 > 0.0 && grad;
+            launch_tv(g, g.p[g.cur], with_grad ? grad : nullptr, 2.0 * cfg->lambda2 * inv_norm, 1, s);
+            double tvs = 0.0;
+            TGCU_CUDA(cudaMemcpyAsync(&tvs, g.scratch_d + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+            TGCU_CUDA(cudaStreamSynchronize(s));
+            t.tv = tvs * inv_norm;
+        }
+        t.total = t.fit + cfg->lambda1 * t.eik + cfg->lambda2 * t.tv;
+        if (out) *out = t;
+    });
+}
+
+int tgcu_adam_reset(tgcu_grid* h, const tgcu_adam_config* cfg) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        raise_sticky(g);
+        if (cfg) g.adam = *cfg;
+        g.t = 0;
+        ensure_optimizer(g);
+        TGCU_CUDA(cudaMemset(g.m[g.cur], 0, sizeof(float) * g.NC));
+        TGCU_CUDA(cudaMemset(g.v[g.cur], 0, sizeof(float) * g.NC));
+    });
+}
+
+int tgcu_adam_get_t(const tgcu_grid* h, int64_t* t) {
+    *t = h->g.t;
+    return TGCU_OK;
+}
+
+int tgcu_adam_step(tgcu_grid* h, const float* grad, void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        cudaStream_t s = as_stream(stream);
+        require(grad != nullptr, "adam_step: NULL gradient");
+        ensure_optimizer(g);
+        launch_adam_check(g, grad, s);
+        TGCU_CUDA(cudaMemcpyAsync(g.st_host, g.st, sizeof(Status), cudaMemcpyDeviceToHost, s));
+        TGCU_CUDA(cudaStreamSynchronize(s));
+        if (g.st_host->bad_grad != ULLONG_MAX) {
+            const unsigned long long idx = g.st_host->bad_grad;
+            const unsigned long long none = ULLONG_MAX;
+            TGCU_CUDA(cudaMemcpy(&g.st->bad_grad, &none, sizeof(none), cudaMemcpyHostToDevice));
+            throw Error(TGCU_ERR_NUMERICAL, "adam_step: non-finite gradient at parameter index " + std::to_string(idx));
+        }
+        g.t += 1;
+        const double bc1 = 1.0 - std::pow(g.adam.beta1, (double)g.t);
+        const double bc2 = 1.0 - std::pow(g.adam.beta2, (double)g.t);
+        launch_adam_update(g, grad, 1.0 / bc1, 1.0 / bc2, s);
+        TGCU_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int tgcu_adam_download_f64(tgcu_grid* h, double* m, double* v, int64_t n) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        check_n(g, n, "adam_download");
+        ensure_optimizer(g);
+        raise_sticky(g);
+        std::vector<float> tmp(n);
+        TGCU_CUDA(cudaMemcpy(tmp.data(), g.m[g.cur], sizeof(float) * n, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i) m[i] = tmp[i];
+        TGCU_CUDA(cudaMemcpy(tmp.data(), g.v[g.cur], sizeof(float) * n, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i) v[i] = tmp[i];
+    });
+}
+
+int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_loss_config* cfg,
+                    tgcu_loss_terms* out, int flags, void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(cfg != nullptr, "total_loss: NULL config");
+        require(cfg->lambda1 >= 0.0 && cfg->lambda2 >= 0.0, "LossConfig: lambda weights must be >= 0");
+        require(cfg->k > 0.0, "LossConfig: weight sharpness k must be > 0");
+        require(n > 0, "total_loss: empty batch");
+        require(n <= (int64_t)INT_MAX / (1 << g.spec.dim), "train_step: batch too large");
+        cudaStream_t s = as_stream(stream);
+        const float4* ds = reinterpret_cast<const float4*>(samples);
+        if (flags & TGCU_HOST) {
+            ensure_staging(g, 4 * n);
+            TGCU_CUDA(cudaMemcpyAsync(g.staging, samples, sizeof(float) * 4 * n, cudaMemcpyHostToDevice, s));
+            ds = reinterpret_cast<const float4*>(g.staging);
+        }
+        ensure_optimizer(g);
+        const int64_t t_after = g.t + 1;
+        const double bc1 = 1.0 - std::pow(g.adam.beta1, (double)t_after);
+        const double bc2 = 1.0 - std::pow(g.adam.beta2, (double)t_after);
+        const int in_idx = g.cur;
+        float* gout = nullptr;
+        if (flags & TGCU_EXPORT_GRAD) {
+            ensure_grad(g);
+            gout = g.grad;
+        }
+        launch_train_step(g, ds, n, *cfg, in_idx, g.steps_launched, 1.0 / bc1, 1.0 / bc2, t_after, gout, s);
+        // Optimistic commit; a failed step is rolled back by raise_sticky().
+        g.cur = 1 - in_idx;
+        g.t = t_after;
+        g.steps_launched += 1;
+        const bool sync = !(flags & TGCU_ASYNC) || out != nullptr;
+        if (out) {
+            TGCU_CUDA(cudaMemcpyAsync(g.h_terms, g.d_trace + ((g.steps_launched - 1) % kTraceCap),
+                                      sizeof(tgcu_loss_terms), cudaMemcpyDeviceToHost, s));
+        }
+        if (sync) {
+            TGCU_CUDA(cudaStreamSynchronize(s));
+            raise_sticky(g);
+            if (out) *out = *g.h_terms;
+        }
+    });
+}
+
+int tgcu_sync(tgcu_grid* h, tgcu_loss_terms* last) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        TGCU_CUDA(cudaDeviceSynchronize());
+        raise_sticky(g);
+        if (last && g.steps_launched > 0)
+            TGCU_CUDA(cudaMemcpy(last, g.d_trace + ((g.steps_launched - 1) % kTraceCap), sizeof(tgcu_loss_terms),
+                                 cudaMemcpyDeviceToHost));
+    });
+}
+
+int tgcu_profile_begin(tgcu_grid* h) {
+    return guard([&] {
+        h->g.prof_on = true;
+        h->g.prof_used = 0;
+    });
+}
+
+int tgcu_profile_end(tgcu_grid* h, double* total_ms, int* launches) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        g.prof_on = false;
+        double tot = 0.0;
+        for (size_t i = 0; i + 1 < g.prof_used; i += 2) {
+            TGCU_CUDA(cudaEventSynchronize(g.prof_ev[i + 1]));
+            float ms = 0.f;
+            TGCU_CUDA(cudaEventElapsedTime(&ms, g.prof_ev[i], g.prof_ev[i + 1]));
+            tot += ms;
+        }
+        *total_ms = tot;
+        *launches = (int)(g.prof_used / 2);
+        g.prof_used = 0;
+    });
+}
+
+int tgcu_sample_uniform_device(int dim, uint64_t seed, int64_t n, double lo, double hi, float* out3,
+                               void* stream) {
+    return guard([&] {
+        require(n >= 0 && out3 != nullptr && (dim == 2 || dim == 3), "sample_uniform_device: bad arguments");
+        launch_hash_points(out3, n, dim, seed, lo, hi, as_stream(stream));
+    });
+}
+
+int tgcu_trace(tgcu_grid* h, tgcu_loss_terms* out, int count) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(count >= 0 && count <= kTraceCap && count <= g.steps_launched, "trace: bad count");
+        TGCU_CUDA(cudaDeviceSynchronize());
+        std::vector<tgcu_loss_terms> all(kTraceCap);
+        TGCU_CUDA(cudaMemcpy(all.data(), g.d_trace, sizeof(tgcu_loss_terms) * kTraceCap, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < count; ++i) out[i] = all[(g.steps_launched - count + i) % kTraceCap];
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,282 @@
+// Device-side TaylorGrid math shared by every kernel (sm_100a).
+//
+// Precision plan (SURVEY §7 "fp32 locate precision"): the cell search
+// (clamp, t = (x - origin)/h, floor, clamp, local = t - cell) runs in fp64 so
+// the cell index matches the reference's locate (grid_spec.cpp:45-69) bit for
+// bit; the per-axis weights/offsets are then rounded to fp32 and the Taylor
+// polynomials, blends and coefficient-gradient monomials run in fp32 FMA
+// chains. The per-point loss chain (weight, sign, eikonal norm) runs in fp64.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tgcu {
+
+template <int DIM, int ORDER>
+struct KOf {
+    static constexpr int value = ORDER == 0 ? 1 : (ORDER == 1 ? 1 + DIM : 1 + DIM + DIM * (DIM + 1) / 2);
+};
+
+// Geometry passed by value to every kernel.
+struct DevSpec {
+    int res[3];
+    double origin[3];
+    double hi[3];     // origin + extent (clamp_point, grid_spec.cpp:35-43)
+    double h[3];      // spacing = extent / (res - 1) (grid_spec.hpp:29)
+    double inv_h[3];  // RN(1 / h), as make_corners (taylor_grid.cpp:37)
+    float hf[3];
+    float inv_hf[3];
+    long long sy, sz;  // vertex strides (x fastest)
+};
+
+// Device-side status / error word of a grid (sticky across async calls).
+struct Status {
+    int error;                      // TGCU_* class of the first failure (0 = ok)
+    int error_kind;                 // 1 NaN point, 2 non-finite loss, 3 non-finite grad
+    long long error_step;           // step index of the failure
+    long long error_index;          // point / parameter index
+    int good_idx;                   // ping-pong buffer holding the last committed state
+    int pad0;
+    long long good_t;               // Adam t of the last committed state
+    unsigned long long nan_point;   // per-call min NaN point index (ULLONG_MAX = none)
+    unsigned long long bad_grad;    // per-step min non-finite grad index
+    unsigned long long overflow;    // bin overflow flag
+};
+
+// t = x / h correctly rounded via Markstein's final-correction step with a
+// correctly rounded reciprocal (checked against true division in
+// tests/test_oracle_cpu.py::test_markstein_division_matches_ieee).
+__device__ __forceinline__ double div_by_h(double x, double h, double inv_h) {
+    const double q = x * inv_h;
+    const double r = fma(-q, h, x);
+    return fma(r, inv_h, q);
+}
+
+// Per-axis locate: clamp, divide, floor, clamp cell to [0, res-2] (max
+// boundary -> last cell with local 1). Returns the cell; local in fp64.
+__device__ __forceinline__ int locate_axis(const DevSpec& s, int a, double x, double& local) {
+    const double lo = s.origin[a];
+    const double hi = s.hi[a];
+    const double p = x < lo ? lo : (x > hi ? hi : x);
+    const double t = div_by_h(p - lo, s.h[a], s.inv_h[a]);
+    int c = (int)floor(t);
+    const int max_cell = s.res[a] - 2;
+    c = c < 0 ? 0 : c;
+    c = c > max_cell ? max_cell : c;
+    local = t - (double)c;
+    return c;
+}
+
+// Per-axis fp32 factors of the 2 corner choices: s[bit], delta[bit].
+struct AxisF {
+    float s0, s1;  // 1 - local, local
+    float d0, d1;  // local * h, (local - 1) * h (world units, make_corners :59)
+};
+
+__device__ __forceinline__ AxisF axis_factors(const DevSpec& s, int a, double local) {
+    AxisF f;
+    f.s0 = (float)(1.0 - local);
+    f.s1 = (float)local;
+    f.d0 = (float)(local * s.h[a]);
+    f.d1 = (float)((local - 1.0) * s.h[a]);
+    return f;
+}
+
+// Corner geometry in fp32: weight w, dw/dx (world units) and delta.
+template <int DIM>
+struct Corner {
+    float w;
+    float dw[DIM];
+    float d[DIM];
+};
+
+template <int DIM>
+__device__ __forceinline__ Corner<DIM> corner_geom(const DevSpec& s, const AxisF* ax, int i) {
+    Corner<DIM> c;
+    float sv[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        const int bit = (i >> a) & 1;
+        sv[a] = bit ? ax[a].s1 : ax[a].s0;
+        c.d[a] = bit ? ax[a].d1 : ax[a].d0;
+    }
+    float w = sv[0];
+#pragma unroll
+    for (int a = 1; a < DIM; ++a) w *= sv[a];
+    c.w = w;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        float other = 1.0f;
+#pragma unroll
+        for (int b = 0; b < DIM; ++b)
+            if (b != a) other *= sv[b];
+        const int bit = (i >> a) & 1;
+        c.dw[a] = (bit ? s.inv_hf[a] : -s.inv_hf[a]) * other;
+    }
+    return c;
+}
+
+// Hessian pair tables (taylor_grid.cpp:14-15).
+template <int DIM>
+struct Pairs;
+template <>
+struct Pairs<2> {
+    static constexpr int n = 3;
+    __device__ static constexpr int j(int t) { return t == 2 ? 1 : 0; }
+    __device__ static constexpr int k(int t) { return t == 0 ? 0 : 1; }
+};
+template <>
+struct Pairs<3> {
+    static constexpr int n = 6;
+    __device__ static constexpr int j(int t) { return t < 3 ? 0 : (t < 5 ? 1 : 2); }
+    __device__ static constexpr int k(int t) { return t == 0 ? 0 : (t == 1 ? 1 : (t == 2 ? 2 : (t == 3 ? 1 : 2))); }
+};
+
+// Vectorised load of one K-coefficient block (8-byte aligned for even K,
+// 16-byte aligned when K % 4 == 0).
+template <int K, bool LDG>
+__device__ __forceinline__ void load_block(const float* __restrict__ p, float (&c)[K]) {
+    if constexpr (K % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) {
+            const float4 v = LDG ? __ldg(reinterpret_cast<const float4*>(p) + q)
+                                 : reinterpret_cast<const float4*>(p)[q];
+            c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
+        }
+    } else if constexpr (K % 2 == 0) {
+#pragma unroll
+        for (int q = 0; q < K / 2; ++q) {
+            const float2 v = LDG ? __ldg(reinterpret_cast<const float2*>(p) + q)
+                                 : reinterpret_cast<const float2*>(p)[q];
+            c[2 * q] = v.x; c[2 * q + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < K; ++q) c[q] = LDG ? __ldg(p + q) : p[q];
+    }
+}
+
+// Taylor polynomial T(delta) and dT/ddelta of one block (taylor_grid.cpp:68-98),
+// accumulated into f / grad with the multilinear weight (eval_impl :107-117).
+template <int DIM, int ORDER, bool GRAD, int K>
+__device__ __forceinline__ void blend_corner(const float (&c)[K], const Corner<DIM>& g, float& f,
+                                             float* fg) {
+    float T = c[0];
+    float gT[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) gT[a] = 0.0f;
+    if constexpr (ORDER >= 1) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            T = fmaf(c[1 + a], g.d[a], T);
+            gT[a] = c[1 + a];
+        }
+    }
+    if constexpr (ORDER >= 2) {
+#pragma unroll
+        for (int t = 0; t < Pairs<DIM>::n; ++t) {
+            const int j = Pairs<DIM>::j(t), k = Pairs<DIM>::k(t);
+            const float q = c[1 + DIM + t];
+            if (j == k) {
+                T = fmaf(0.5f * q * g.d[j], g.d[j], T);
+                gT[j] = fmaf(q, g.d[j], gT[j]);
+            } else {
+                T = fmaf(q * g.d[j], g.d[k], T);
+                gT[j] = fmaf(q, g.d[k], gT[j]);
+                gT[k] = fmaf(q, g.d[j], gT[k]);
+            }
+        }
+    }
+    f = fmaf(g.w, T, f);
+    if constexpr (GRAD) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) fg[a] = fmaf(g.dw[a], T, fmaf(g.w, gT[a], fg[a]));
+    }
+}
+
+// Coefficient-gradient contribution of one (point, corner):
+// alpha = u*w + gvec.dw, beta = w (accumulate_cell, taylor_grid.cpp:123-152).
+template <int DIM, int ORDER, int K>
+__device__ __forceinline__ void corner_grad(const Corner<DIM>& g, float u, const float* gv,
+                                            float (&G)[K]) {
+    float alpha = u * g.w;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) alpha = fmaf(gv[a], g.dw[a], alpha);
+    const float beta = g.w;
+    G[0] += alpha;
+    if constexpr (ORDER >= 1) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) G[1 + a] += fmaf(alpha, g.d[a], beta * gv[a]);
+    }
+    if constexpr (ORDER >= 2) {
+#pragma unroll
+        for (int t = 0; t < Pairs<DIM>::n; ++t) {
+            const int j = Pairs<DIM>::j(t), k = Pairs<DIM>::k(t);
+            if (j == k)
+                G[1 + DIM + t] += fmaf(alpha * 0.5f * g.d[j], g.d[j], beta * gv[j] * g.d[j]);
+            else
+                G[1 + DIM + t] += fmaf(alpha * g.d[j], g.d[k], beta * fmaf(gv[j], g.d[k], gv[k] * g.d[j]));
+        }
+    }
+}
+
+// Per-point loss chain in fp64 (point_terms_chunk, sdf_loss.cpp:51-74).
+struct LossDev {
+    double k;
+    double inv_n;       // 1 / global batch size
+    double eik_scale;   // lambda1 (0 disables the eikonal term)
+    int use_weighting;
+    int differentiate_weight;
+};
+
+__device__ __forceinline__ double sigmoid_d(double x) { return 1.0 / (1.0 + exp(-x)); }
+__device__ __forceinline__ double w_prime_d(double d, double k) { return 1.0 - fabs(2.0 * sigmoid_d(k * d) - 1.0); }
+
+template <int DIM, bool EIK>
+__device__ __forceinline__ void point_loss(const LossDev& L, float f, const float* fg, float gt,
+                                           double& recon, double& eik, float& u, float* gv) {
+    const double value = (double)f;
+    const double gtd = (double)gt;
+    const double resid = value - gtd;
+    double w = 1.0;
+    double wp_pred = 0.0, wp_gt = 0.0;
+    if (L.use_weighting) {
+        wp_pred = w_prime_d(value, L.k);
+        wp_gt = w_prime_d(gtd, L.k);
+        w = wp_pred < wp_gt ? wp_gt : wp_pred;
+    }
+    recon = w * fabs(resid);
+    const double sgn = resid > 0.0 ? 1.0 : (resid < 0.0 ? -1.0 : 0.0);
+    double up = L.inv_n * w * sgn;
+    if (L.use_weighting && L.differentiate_weight && wp_pred > wp_gt && value != 0.0) {
+        const double s = sigmoid_d(L.k * value);
+        const double ds = 2.0 * L.k * s * (1.0 - s);
+        up += L.inv_n * fabs(resid) * (value > 0.0 ? -ds : ds);
+    }
+    u = (float)up;
+    eik = 0.0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) gv[a] = 0.0f;
+    if constexpr (EIK) {
+        double n2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) n2 += (double)fg[a] * (double)fg[a];
+        const double n = sqrt(n2);
+        const double r = n - 1.0;
+        eik = r * r;
+        if (n > 0.0) {
+            const double sc = L.eik_scale * L.inv_n * 2.0 * r / n;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) gv[a] = (float)(sc * (double)fg[a]);
+        }
+    }
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace tgcu

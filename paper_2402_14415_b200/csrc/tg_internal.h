@@ -1,0 +1,125 @@
+// Host-side internals of libtgcu: the grid handle, error plumbing and the
+// kernel launchers each .cu file provides.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tgcu.h"
+#include "tg_device.cuh"
+
+namespace tgcu {
+
+// Exception carrying a TGCU_* status class; converted to a return code at the
+// C boundary (api.cu).
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void require(bool cond, const std::string& msg) {
+    if (!cond) throw Error(TGCU_ERR_INVALID_ARGUMENT, msg);
+}
+
+#define TGCU_CUDA(expr)                                                                         \
+    do {                                                                                        \
+        cudaError_t _e = (expr);                                                                \
+        if (_e != cudaSuccess)                                                                  \
+            throw ::tgcu::Error(TGCU_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+void count_launch(int n = 1);
+
+// Brick edge (vertices per axis) of the fused training kernel and the
+// brick-binned query.
+constexpr int kBrick3 = 8;
+constexpr int kBrick2 = 16;
+
+struct Grid {
+    tgcu_grid_spec spec{};
+    int K = 0;
+    int64_t V = 0;   // vertices
+    int64_t NC = 0;  // coefficients = V*K
+    int device = 0;
+    DevSpec ds{};
+
+    // Ping-pong parameter / moment buffers (fused step writes the other one).
+    float* p[2] = {nullptr, nullptr};
+    float* m[2] = {nullptr, nullptr};
+    float* v[2] = {nullptr, nullptr};
+    int cur = 0;
+    float* grad = nullptr;  // unfused-API gradient buffer (lazy)
+
+    tgcu_adam_config adam{0.003, 0.9, 0.999, 1e-8};
+    int64_t t = 0;              // AdamState::t (host mirror, optimistic under async)
+    int64_t steps_launched = 0; // fused steps issued
+
+    Status* st = nullptr;     // device status
+    Status* st_host = nullptr;  // pinned mirror
+
+    // Bricks of the fused step / binned query.
+    int brick[3] = {1, 1, 1};
+    int nb[3] = {1, 1, 1};
+    int64_t NB = 1;
+    int* bin_count = nullptr;   // NB + 1
+    int* bin_off = nullptr;     // NB + 1
+    int* bin_cursor = nullptr;  // NB
+    float4* binned = nullptr;
+    int64_t binned_cap = 0;     // points
+    double* partials = nullptr; // NB * 4
+    tgcu_loss_terms* d_trace = nullptr;  // kTraceCap
+    tgcu_loss_terms* h_terms = nullptr;  // pinned, 1
+    float* staging = nullptr;            // device staging for host inputs
+    int64_t staging_cap = 0;             // floats
+    double* scratch_d = nullptr;         // reductions (unfused path)
+    int64_t scratch_cap = 0;
+    // Live kernel timing (tgcu_profile_*): CUDA events recorded on the launch
+    // stream around the fused brick kernel.
+    bool prof_on = false;
+    std::vector<cudaEvent_t> prof_ev;  // pairs (start, end)
+    size_t prof_used = 0;
+};
+
+void prof_mark(Grid& g, cudaStream_t s, int which);
+
+constexpr int kTraceCap = 4096;
+
+void ensure_staging(Grid& g, int64_t floats);
+void ensure_bins(Grid& g, int64_t points);
+void ensure_scratch(Grid& g, int64_t doubles);
+void ensure_grad(Grid& g);
+void ensure_optimizer(Grid& g);
+
+// Launchers (query.cu / train.cu). All stream-ordered; no synchronisation.
+void launch_eval_direct(Grid& g, const float* pts, int64_t n, float* vals, float* grads, cudaStream_t s);
+void launch_eval_sorted(Grid& g, const float* pts, int64_t n, float* vals, float* grads, cudaStream_t s);
+void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, cudaStream_t s);
+void launch_backprop(Grid& g, const float* pts, const float* up, const float* upv, int64_t n, float* grad,
+                     cudaStream_t s);
+// Unfused total_loss pieces: point terms (atomic scatter) + TV; sums land in
+// g.scratch_d[0..2] = {recon, eik, tv_sum}.
+void launch_point_terms(Grid& g, const float4* samples, int64_t n, const tgcu_loss_config& cfg, float* grad,
+                        cudaStream_t s);
+void launch_tv(Grid& g, const float* coeffs, float* grad, double gscale, int want_value, cudaStream_t s);
+void launch_adam_check(Grid& g, const float* grad, cudaStream_t s);
+void launch_adam_update(Grid& g, const float* grad, double inv_bc1, double inv_bc2, cudaStream_t s);
+// Fused step: binning + brick kernel + finalize (train.cu).
+void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_loss_config& cfg, int in_idx,
+                       int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
+                       cudaStream_t s);
+void launch_f64_to_f32(const double* src, float* dst, int64_t n, cudaStream_t s);
+void launch_f32_to_f64(const float* src, double* dst, int64_t n, cudaStream_t s);
+void launch_all_finite(const float* src, int64_t n, unsigned long long* flag, cudaStream_t s);
+void launch_fill_f0(Grid& g, float* dst, float value, cudaStream_t s);
+void launch_hash_gaussian(float* dst, int64_t n, uint64_t seed, double sigma, cudaStream_t s);
+void launch_hash_points(float* out, int64_t n, int dim, uint64_t seed, double lo, double hi, cudaStream_t s);
+
+}  // namespace tgcu
+
+struct tgcu_grid {
+    tgcu::Grid g;
+};

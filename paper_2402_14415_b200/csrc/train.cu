@@ -1,0 +1,612 @@
+// Fused training step: zero grad → total_loss (recon + eikonal + TV) →
+// finite checks → Adam, i.e. one iteration of run_schedule
+// (schedule.cpp:66-92) / cmd_bench (tools/main.cpp:640-644), as one device
+// pipeline with the gradient never materialised in HBM.
+//
+// Design ("owner computes", SURVEY §8a K2+K3):
+//   The vertex grid is cut into bricks of B^D vertices (B = 8 in 3D, 16 in
+//   2D). The CTA of brick b owns its vertices' Adam state and needs every
+//   point whose cell touches an owned vertex: the cells [B*b-1, B*b+B-1] per
+//   axis. Points are binned by brick with a counting sort; a point lying in
+//   the last cell layer of a brick is also copied to the next brick (1..2^D
+//   copies, 1.42x on average for uniform points).
+//   Per CTA:
+//     1. stage the (B+2)^D vertex tile of the current parameters in smem
+//        (owned vertices + one-vertex halo: the cells' corners and the TV
+//        stencil neighbours);
+//     2. per chunk of points: forward eval from the tile (fp64 locate, fp32
+//        blend), the fp64 loss chain, then a counting sort of the chunk by
+//        cell in smem; each owned-vertex thread then gathers the
+//        contributions of the points in its 2^D incident cells into K
+//        register accumulators (no atomics anywhere);
+//     3. TV gradient from the tile stencil + Adam over the owned
+//        coefficients, reading m/v and writing p/m/v to the other ping-pong
+//        buffers (coalesced rows), plus the per-brick loss partials.
+//   A 1-CTA finalize kernel reduces the partials in a fixed order, applies the
+//   reference's error order (NaN point, non-finite loss, non-finite gradient)
+//   and commits the step by naming the new current buffer; a failed step
+//   leaves the old buffers current and makes every later step a no-op until
+//   the host reads the sticky error.
+#include <climits>
+
+#include "dispatch.cuh"
+#include "tg_internal.h"
+
+namespace tgcu {
+
+template <int DIM>
+struct BrickShape {
+    static constexpr int B = DIM == 3 ? kBrick3 : kBrick2;
+    static constexpr int T = B + 2;   // tile edge (vertices)
+    static constexpr int CE = B + 1;  // cells per axis touching owned vertices
+    static constexpr int NCELL = DIM == 3 ? CE * CE * CE : CE * CE;
+    static constexpr int TVN = DIM == 3 ? T * T * T : T * T;
+    static constexpr int NOWN = DIM == 3 ? B * B * B : B * B;
+    static constexpr int NT = NOWN;   // one thread per owned vertex
+    static constexpr int CH = NT;     // points per chunk
+    static constexpr int REC = 8;     // floats per point record
+};
+
+template <int DIM, int ORDER>
+constexpr size_t brick_smem_bytes() {
+    using S = BrickShape<DIM>;
+    constexpr int K = KOf<DIM, ORDER>::value;
+    constexpr size_t tile = sizeof(float) * S::TVN * K;
+    constexpr size_t pts = sizeof(float) * S::CH * S::REC + sizeof(int) * S::CH * 3;
+    constexpr size_t gs = sizeof(float) * S::NOWN * K;
+    constexpr size_t uni = pts > gs ? pts : gs;
+    constexpr size_t cells = sizeof(int) * S::NCELL * 2;
+    return tile + uni + cells;
+}
+
+struct BinArgs {
+    DevSpec s;
+    const float4* pts;
+    long long n;
+    int nb[3];
+    int* count;
+    int* cursor;
+    float4* binned;
+    Status* st;
+};
+
+// Bricks needing the point: per axis the brick of its cell and, for a cell in
+// the brick's last layer, the next brick too. Returns the count (0 = NaN).
+template <int DIM>
+__device__ __forceinline__ int point_bricks(const DevSpec& s, const int* nb, const float4& q, int* out) {
+    constexpr int B = BrickShape<DIM>::B;
+    const float pf[3] = {q.x, q.y, q.z};
+    int lo[3] = {0, 0, 0}, two[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        const double x = (double)pf[a];
+        if (isnan(x)) return 0;
+        double local;
+        const int c = locate_axis(s, a, x, local);
+        lo[a] = c / B;
+        two[a] = (c % B) == B - 1 ? 1 : 0;
+    }
+    int m = 0;
+    for (int dz = 0; dz <= (DIM == 3 ? two[2] : 0); ++dz)
+        for (int dy = 0; dy <= two[1]; ++dy)
+            for (int dx = 0; dx <= two[0]; ++dx)
+                out[m++] = ((DIM == 3 ? (lo[2] + dz) * nb[1] : 0) + lo[1] + dy) * nb[0] + lo[0] + dx;
+    return m;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_bin_count(BinArgs A) {
+    if (A.st->error) return;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < A.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        int br[8];
+        const int m = point_bricks<DIM>(A.s, A.nb, A.pts[i], br);
+        if (m == 0) atomicMin(&A.st->nan_point, (unsigned long long)i);
+        for (int k = 0; k < m; ++k) atomicAdd(&A.count[br[k]], 1);
+    }
+}
+
+// Exclusive scan of NB brick counts -> off[0..NB], cursor = off. One CTA.
+__global__ void __launch_bounds__(1024) k_bin_scan(const int* __restrict__ count, int* __restrict__ off,
+                                                   int* __restrict__ cursor, int NB, Status* st) {
+    if (st->error) return;
+    __shared__ int warp_tot[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = 0; base < NB; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const int c = i < NB ? count[i] : 0;
+        int x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int w = warp_tot[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            warp_tot[lane] = w;  // inclusive
+        }
+        __syncthreads();
+        const int excl = carry + (wid ? warp_tot[wid - 1] : 0) + x - c;
+        if (i < NB) {
+            off[i] = excl;
+            cursor[i] = excl;
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = excl + c;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) off[NB] = carry;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_bin_scatter(BinArgs A) {
+    if (A.st->error) return;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < A.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float4 q = A.pts[i];
+        int br[8];
+        const int m = point_bricks<DIM>(A.s, A.nb, q, br);
+        for (int k = 0; k < m; ++k) {
+            const int slot = atomicAdd(&A.cursor[br[k]], 1);
+            A.binned[slot] = q;
+        }
+    }
+}
+
+struct StepArgs {
+    DevSpec s;
+    const float* p_in;
+    float* p_out;
+    const float* m_in;
+    float* m_out;
+    const float* v_in;
+    float* v_out;
+    const float4* binned;
+    const int* off;
+    int nb[3];
+    LossDev L;
+    float tv_gscale;
+    int want_tv;
+    float lr, b1, b2, eps, inv_bc1, inv_bc2;
+    double* partials;  // NB x 4: recon, eik, tv, home points
+    Status* st;
+    float* grad_out;   // optional: full gradient (validation mode, TGCU_EXPORT_GRAD)
+};
+
+template <int NCELL, int NT>
+__device__ __forceinline__ void block_excl_scan(const int* __restrict__ cnt, int* __restrict__ start, int* warp_tot) {
+    constexpr int IT = (NCELL + NT - 1) / NT;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    int v[IT];
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+        const int i = t * IT + k;
+        v[k] = i < NCELL ? cnt[i] : 0;
+        sum += v[k];
+    }
+    int x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int w = lane < NT / 32 ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < NT / 32) warp_tot[lane] = w;
+    }
+    __syncthreads();
+    int excl = (wid ? warp_tot[wid - 1] : 0) + x - sum;
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+        const int i = t * IT + k;
+        if (i < NCELL) start[i] = excl;
+        excl += v[k];
+    }
+}
+
+template <int DIM, int ORDER, bool EIK>
+__global__ void __launch_bounds__(BrickShape<DIM>::NT, 1) k_brick_step(StepArgs A) {
+    using S = BrickShape<DIM>;
+    constexpr int K = KOf<DIM, ORDER>::value;
+    constexpr int B = S::B, T = S::T, CE = S::CE, NT = S::NT, CH = S::CH;
+    if (A.st->error) return;
+
+    extern __shared__ __align__(16) float smem[];
+    float* tile = smem;                               // TVN*K
+    float* uni = tile + S::TVN * K;                   // point records | Gs
+    float* rec = uni;                                 // CH*REC
+    int* cellof = reinterpret_cast<int*>(rec + CH * S::REC);
+    int* rankof = cellof + CH;
+    int* order = rankof + CH;
+    constexpr size_t uni_floats =
+        (CH * S::REC + CH * 3) > (S::NOWN * K) ? (CH * S::REC + CH * 3) : (S::NOWN * K);
+    int* cnt = reinterpret_cast<int*>(uni + uni_floats);
+    int* start = cnt + S::NCELL;
+    __shared__ int warp_tot[32];
+    __shared__ double red[3][NT / 32];
+
+    const int tid = threadIdx.x;
+    const int nbx = A.nb[0], nby = A.nb[1];
+    const int b = blockIdx.x;
+    const int bx = b % nbx;
+    const int by = (b / nbx) % nby;
+    const int bz = DIM == 3 ? b / (nbx * nby) : 0;
+    const int o[3] = {bx * B, by * B, bz * B};
+
+    // ---- 1. stage the parameter tile (vertices o-1 .. o+B per axis) ----
+    {
+        constexpr int ROW = T * K;
+        constexpr int ROWS = DIM == 3 ? T * T : T;
+        for (int e = tid; e < ROWS * ROW; e += NT) {
+            const int r = e / ROW, q = e - r * ROW;
+            const int tx = q / K, ch = q - tx * K;
+            const int ty = r % T, tz = r / T;
+            const int vx = o[0] - 1 + tx, vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
+            float val = 0.0f;
+            if (vx >= 0 && vx < A.s.res[0] && vy >= 0 && vy < A.s.res[1] &&
+                (DIM == 2 || (vz >= 0 && vz < A.s.res[2])))
+                val = A.p_in[((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + vx) * K + ch];
+            tile[e] = val;
+        }
+    }
+    __syncthreads();
+
+    // This thread's owned vertex.
+    const int lv[3] = {tid % B, (tid / B) % B, DIM == 3 ? tid / (B * B) : 0};
+    bool own_ok = true;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) own_ok &= (o[a] + lv[a]) < A.s.res[a];
+
+    float G[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) G[q] = 0.0f;
+    double recon_sum = 0.0, eik_sum = 0.0, home_pts = 0.0;
+
+    // ---- 2. points ----
+    const int p0 = A.off[b], p1 = A.off[b + 1];
+    for (int base = p0; base < p1; base += CH) {
+        const int m = min(CH, p1 - base);
+        for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
+        __syncthreads();
+        if (tid < m) {
+            const float4 q = A.binned[base + tid];
+            const float pf[3] = {q.x, q.y, q.z};
+            AxisF ax[DIM];
+            int tc[3] = {0, 0, 0};
+            float lf[3] = {0.f, 0.f, 0.f};
+            bool home = true;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                double local;
+                const int c = locate_axis(A.s, a, (double)pf[a], local);
+                ax[a] = axis_factors(A.s, a, local);
+                lf[a] = (float)local;
+                tc[a] = c - (o[a] - 1);  // in [0, B]
+                home &= tc[a] >= 1;
+            }
+            const int tb = DIM == 3 ? (tc[2] * T + tc[1]) * T + tc[0] : tc[1] * T + tc[0];
+            float f = 0.0f, fg[DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
+#pragma unroll
+            for (int c = 0; c < (1 << DIM); ++c) {
+                const int tv = tb + (c & 1) + ((c >> 1) & 1) * T + (DIM == 3 ? ((c >> 2) & 1) * T * T : 0);
+                float cb[K];
+                load_block<K, false>(tile + tv * K, cb);
+                blend_corner<DIM, ORDER, EIK>(cb, corner_geom<DIM>(A.s, ax, c), f, fg);
+            }
+            double recon, eik;
+            float u, gv[DIM];
+            point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
+            if (home) {
+                recon_sum += recon;
+                eik_sum += eik;
+                home_pts += 1.0;
+            }
+            const int ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
+            rankof[tid] = atomicAdd(&cnt[ec], 1);
+            cellof[tid] = ec;
+            float* r = rec + tid * S::REC;
+            r[0] = lf[0];
+            r[1] = lf[1];
+            r[2] = lf[2];
+            r[3] = u;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) r[4 + a] = a < DIM ? gv[a] : 0.0f;
+        }
+        __syncthreads();
+        block_excl_scan<S::NCELL, NT>(cnt, start, warp_tot);
+        __syncthreads();
+        if (tid < m) order[start[cellof[tid]] + rankof[tid]] = tid;
+        __syncthreads();
+        if (own_ok) {
+#pragma unroll
+            for (int c = 0; c < (1 << DIM); ++c) {
+                int ec = 0;
+                {
+                    int e3[3] = {0, 0, 0};
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) e3[a] = lv[a] + 1 - ((c >> a) & 1);
+                    ec = DIM == 3 ? (e3[2] * CE + e3[1]) * CE + e3[0] : e3[1] * CE + e3[0];
+                }
+                const int j0 = start[ec], j1 = j0 + cnt[ec];
+                for (int j = j0; j < j1; ++j) {
+                    const float* r = rec + order[j] * S::REC;
+                    AxisF ax[DIM];
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) {
+                        const float l = r[a];
+                        ax[a].s0 = 1.0f - l;
+                        ax[a].s1 = l;
+                        ax[a].d0 = l * A.s.hf[a];
+                        ax[a].d1 = (l - 1.0f) * A.s.hf[a];
+                    }
+                    float gv[DIM];
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) gv[a] = EIK ? r[4 + a] : 0.0f;
+                    corner_grad<DIM, ORDER, K>(corner_geom<DIM>(A.s, ax, c), r[3], gv, G);
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- 3. TV + Adam over the owned coefficients ----
+    float* Gs = uni;
+#pragma unroll
+    for (int q = 0; q < K; ++q) Gs[tid * K + q] = G[q];
+    __syncthreads();
+    double tv_sum = 0.0;
+    const int tstride[3] = {1, T, T * T};
+    for (int e = tid; e < S::NOWN * K; e += NT) {
+        const int v = e / K, ch = e - v * K;
+        const int l3[3] = {v % B, (v / B) % B, DIM == 3 ? v / (B * B) : 0};
+        int g3[3];
+        bool ok = true;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            g3[a] = o[a] + l3[a];
+            ok &= g3[a] < A.s.res[a];
+        }
+        if (!ok) continue;
+        const int tv = DIM == 3 ? ((l3[2] + 1) * T + (l3[1] + 1)) * T + (l3[0] + 1) : (l3[1] + 1) * T + (l3[0] + 1);
+        const float pv = tile[tv * K + ch];
+        float gt = 0.0f;
+        if (A.want_tv) {
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                if (g3[a] + 1 < A.s.res[a]) {
+                    const float d = tile[(tv + tstride[a]) * K + ch] - pv;
+                    tv_sum += (double)d * (double)d;
+                    gt -= d;
+                }
+                if (g3[a] >= 1) gt += pv - tile[(tv - tstride[a]) * K + ch];
+            }
+        }
+        const float gi = fmaf(A.tv_gscale, gt, Gs[e]);
+        const long long gidx =
+            ((DIM == 3 ? (long long)g3[2] * A.s.sz : 0LL) + (long long)g3[1] * A.s.sy + g3[0]) * K + ch;
+        if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)gidx);
+        if (A.grad_out) A.grad_out[gidx] = gi;
+        const float mi = fmaf(A.b1, A.m_in[gidx], (1.0f - A.b1) * gi);
+        const float vi = fmaf(A.b2, A.v_in[gidx], (1.0f - A.b2) * gi * gi);
+        A.m_out[gidx] = mi;
+        A.v_out[gidx] = vi;
+        A.p_out[gidx] = pv - A.lr * (mi * A.inv_bc1) / (sqrtf(vi * A.inv_bc2) + A.eps);
+    }
+
+    // ---- per-brick loss partials (fixed-order block reduction) ----
+    recon_sum = warp_sum_d(recon_sum);
+    eik_sum = warp_sum_d(eik_sum);
+    tv_sum = warp_sum_d(tv_sum);
+    home_pts = warp_sum_d(home_pts);
+    __shared__ double hp[NT / 32];
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = recon_sum;
+        red[1][tid >> 5] = eik_sum;
+        red[2][tid >> 5] = tv_sum;
+        hp[tid >> 5] = home_pts;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0.0, c = 0.0, d = 0.0, h = 0.0;
+        for (int k = 0; k < NT / 32; ++k) {
+            a += red[0][k];
+            c += red[1][k];
+            d += red[2][k];
+            h += hp[k];
+        }
+        A.partials[4 * b] = a;
+        A.partials[4 * b + 1] = c;
+        A.partials[4 * b + 2] = d;
+        A.partials[4 * b + 3] = h;
+    }
+}
+
+struct FinArgs {
+    const double* partials;
+    int NB;
+    double n;
+    double lambda1, lambda2, inv_norm;
+    int use_tv, want_eik;
+    Status* st;
+    tgcu_loss_terms* trace;
+    long long step;
+    int in_idx;
+    long long t_after;
+};
+
+__global__ void __launch_bounds__(1024) k_step_finalize(FinArgs F) {
+    __shared__ double red[3][32];
+    if (F.st->error) return;
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int i = threadIdx.x; i < F.NB; i += blockDim.x) {
+        a += F.partials[4 * i];
+        b += F.partials[4 * i + 1];
+        c += F.partials[4 * i + 2];
+    }
+    a = warp_sum_d(a);
+    b = warp_sum_d(b);
+    c = warp_sum_d(c);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = a;
+        red[1][threadIdx.x >> 5] = b;
+        red[2][threadIdx.x >> 5] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double recon = 0.0, eik = 0.0, tvs = 0.0;
+    for (int k = 0; k < 32; ++k) {
+        recon += red[0][k];
+        eik += red[1][k];
+        tvs += red[2][k];
+    }
+    tgcu_loss_terms t;
+    t.fit = recon / F.n;
+    t.eik = F.want_eik ? eik / F.n : 0.0;
+    t.tv = F.use_tv ? tvs * F.inv_norm : 0.0;
+    t.total = t.fit + F.lambda1 * t.eik + F.lambda2 * t.tv;
+    F.trace[F.step % kTraceCap] = t;
+    Status* st = F.st;
+    int err = 0, kind = 0;
+    long long idx = -1;
+    if (st->nan_point != ULLONG_MAX) {
+        err = TGCU_ERR_INVALID_ARGUMENT;
+        kind = 1;
+        idx = (long long)st->nan_point;
+    } else if (!isfinite(t.total)) {
+        err = TGCU_ERR_NUMERICAL;
+        kind = 2;
+    } else if (st->bad_grad != ULLONG_MAX) {
+        err = TGCU_ERR_NUMERICAL;
+        kind = 3;
+        idx = (long long)st->bad_grad;
+    }
+    if (err) {
+        st->error = err;
+        st->error_kind = kind;
+        st->error_step = F.step;
+        st->error_index = idx;
+        st->good_idx = F.in_idx;
+        st->good_t = F.t_after - 1;
+    } else {
+        st->good_idx = 1 - F.in_idx;
+        st->good_t = F.t_after;
+    }
+    st->nan_point = ULLONG_MAX;
+    st->bad_grad = ULLONG_MAX;
+}
+
+void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_loss_config& cfg, int in_idx,
+                       int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
+                       cudaStream_t s) {
+    ensure_bins(g, n);
+    BinArgs B;
+    B.s = g.ds;
+    B.pts = samples;
+    B.n = n;
+    for (int a = 0; a < 3; ++a) B.nb[a] = g.nb[a];
+    B.count = g.bin_count;
+    B.cursor = g.bin_cursor;
+    B.binned = g.binned;
+    B.st = g.st;
+    TGCU_CUDA(cudaMemsetAsync(g.bin_count, 0, sizeof(int) * g.NB, s));
+    const int pblocks = grid_blocks(n, 256, 148 * 16);
+    if (g.spec.dim == 3) k_bin_count<3><<<pblocks, 256, 0, s>>>(B);
+    else k_bin_count<2><<<pblocks, 256, 0, s>>>(B);
+    k_bin_scan<<<1, 1024, 0, s>>>(g.bin_count, g.bin_off, g.bin_cursor, (int)g.NB, g.st);
+    if (g.spec.dim == 3) k_bin_scatter<3><<<pblocks, 256, 0, s>>>(B);
+    else k_bin_scatter<2><<<pblocks, 256, 0, s>>>(B);
+
+    StepArgs A;
+    A.s = g.ds;
+    const int out_idx = 1 - in_idx;
+    A.p_in = g.p[in_idx];
+    A.p_out = g.p[out_idx];
+    A.m_in = g.m[in_idx];
+    A.m_out = g.m[out_idx];
+    A.v_in = g.v[in_idx];
+    A.v_out = g.v[out_idx];
+    A.binned = g.binned;
+    A.off = g.bin_off;
+    for (int a = 0; a < 3; ++a) A.nb[a] = g.nb[a];
+    A.L.k = cfg.k;
+    A.L.inv_n = 1.0 / (double)n;
+    A.L.eik_scale = cfg.lambda1;
+    A.L.use_weighting = cfg.use_weighting;
+    A.L.differentiate_weight = cfg.differentiate_weight;
+    // TV normaliser P*K (sdf_loss.cpp:161-170).
+    double P = 0.0;
+    for (int a = 0; a < g.spec.dim; ++a) {
+        double np = g.spec.res[a] - 1;
+        for (int b2 = 0; b2 < g.spec.dim; ++b2)
+            if (b2 != a) np *= g.spec.res[b2];
+        P += np;
+    }
+    const double inv_norm = 1.0 / (P * g.K);
+    A.want_tv = cfg.use_tv ? 1 : 0;
+    A.tv_gscale = (cfg.use_tv && cfg.lambda2 > 0.0) ? (float)(2.0 * cfg.lambda2 * inv_norm) : 0.0f;
+    A.lr = (float)g.adam.lr;
+    A.b1 = (float)g.adam.beta1;
+    A.b2 = (float)g.adam.beta2;
+    A.eps = (float)g.adam.eps;
+    A.inv_bc1 = (float)inv_bc1;
+    A.inv_bc2 = (float)inv_bc2;
+    A.partials = g.partials;
+    A.st = g.st;
+    A.grad_out = grad_out;
+    const bool eik = cfg.lambda1 > 0.0;
+    TGCU_DISPATCH(g.spec.dim, g.spec.order, {
+        constexpr size_t smem = brick_smem_bytes<DIM, ORDER>();
+        auto kern = eik ? k_brick_step<DIM, ORDER, true> : k_brick_step<DIM, ORDER, false>;
+        static bool configured = false;
+        if (!configured) {
+            TGCU_CUDA(cudaFuncSetAttribute(k_brick_step<DIM, ORDER, true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            TGCU_CUDA(cudaFuncSetAttribute(k_brick_step<DIM, ORDER, false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            configured = true;
+        }
+        if (g.prof_on) prof_mark(g, s, 0);
+        kern<<<(unsigned)g.NB, BrickShape<DIM>::NT, smem, s>>>(A);
+        if (g.prof_on) prof_mark(g, s, 1);
+    });
+
+    FinArgs F;
+    F.partials = g.partials;
+    F.NB = (int)g.NB;
+    F.n = (double)n;
+    F.lambda1 = cfg.lambda1;
+    F.lambda2 = cfg.lambda2;
+    F.inv_norm = inv_norm;
+    F.use_tv = cfg.use_tv;
+    F.want_eik = eik;
+    F.st = g.st;
+    F.trace = g.d_trace;
+    F.step = step;
+    F.in_idx = in_idx;
+    F.t_after = t_after;
+    k_step_finalize<<<1, 1024, 0, s>>>(F);
+    count_launch(5);
+    TGCU_CUDA(cudaGetLastError());
+}
+
+}  // namespace tgcu

@@ -1,0 +1,256 @@
+"""GPU parity of the CUDA path (through the C ABI) against the reference.
+
+Tolerances (BASELINE.json north_star), written per test:
+  forward values          |d| <= 1e-6 * max(1, |ref|)
+  spatial gradients       |d| <= 1e-5 * max(1, |ref|)   (scale 1/h; fp32 blend)
+  coefficient gradients   |d| <= 1e-5 * max(|ref|, floor), floor = 1e-3 * max|ref|
+                          (relative with an absolute floor, as rel_err in
+                          tests/support/oracles.hpp:20-22; accumulation order differs)
+  loss curve over N steps |d| <= 1e-4 * |ref|
+Indices (cells, vertex ids, NaN/bad-gradient indices) are exact.
+"""
+import numpy as np
+import pytest
+
+import paper_2402_14415_b200 as tg
+from conftest import load_golden
+from oracle.pyoracle import Loss, Spec
+
+pytestmark = pytest.mark.gpu
+
+
+def gspec(dim, res, order):
+    res = tuple(int(r) for r in res)
+    return tg.GridSpec(dim=dim, resolution=res if dim == 3 else res[:2] + (1,), order=order)
+
+
+def ospec(dim, res, order):
+    return Spec(dim=dim, res=tuple(int(r) for r in res), order=order)
+
+
+def assert_close(got, ref, rel, floor=1.0, what=""):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    tol = rel * np.maximum(np.abs(ref), floor)
+    bad = np.abs(got - ref) > tol
+    assert not bad.any(), (f"{what}: {bad.sum()} / {bad.size} out of tolerance; worst "
+                           f"{np.max(np.abs(got - ref) / tol):.3g}x tol")
+
+
+def grad_close(got, ref, rel=1e-5, what="grad"):
+    floor = 1e-3 * max(float(np.max(np.abs(ref))), 1e-30)
+    assert_close(got, ref, rel, floor, what)
+
+
+# ---- K1 forward -------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("order", [0, 1, 2])
+def test_eval_golden(dim, order):
+    z = load_golden("eval_backprop.npz")
+    k = f"d{dim}o{order}_"
+    g = tg.init_grid(gspec(dim, z[k + "res"], order))
+    g.coeffs = z[k + "coeffs"]
+    pts = z[k + "pts"]
+    vals, grads = tg.eval_with_spatial_gradient(g, pts)
+    assert_close(vals, z[k + "vals"], 1e-6, what="value")
+    assert_close(grads, z[k + "grads"][:, :dim], 1e-5, what="spatial grad")
+    assert np.array_equal(tg.eval(g, pts), vals)
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_eval_large_vs_oracle_and_sorted(oracle, order):
+    rng = np.random.default_rng(3 + order)
+    res = (65, 64, 63)
+    s = ospec(3, res, order)
+    c = (0.1 * rng.standard_normal(s.V * s.K)).astype(np.float32)
+    g = tg.init_grid(gspec(3, res, order))
+    g.set_coeffs_f32(c)
+    pts = rng.uniform(-1.02, 1.02, (20000, 3)).astype(np.float32)
+    vals = tg.eval(g, pts)
+    ref = oracle.eval(s, c.astype(np.float64), pts.astype(np.float64))
+    assert_close(vals, ref, 1e-6, what="value")
+    # brick-binned query on sorted points gives the same values
+    import torch
+    dp = torch.from_numpy(pts).cuda()
+    sp = torch.empty_like(dp)
+    perm = torch.empty(len(pts), dtype=torch.int64, device="cuda")
+    tg.sort_points(g, dp, sp, perm)
+    v2, g2 = tg.eval_with_spatial_gradient(g, sp, sorted_points=True)
+    v1, g1 = tg.eval_with_spatial_gradient(g, sp)
+    torch.cuda.synchronize()
+    assert torch.equal(v1, v2) or torch.allclose(v1, v2, rtol=0, atol=1e-7)
+    assert np.array_equal(np.sort(perm.cpu().numpy()), np.arange(len(pts)))
+    assert_close(v2.cpu().numpy(), ref[perm.cpu().numpy()], 1e-6, what="sorted value")
+
+
+def test_locate_edge_cases_and_nan():
+    # max-boundary -> last cell with local 1; out-of-domain clamps; NaN rejected
+    g = tg.init_grid(tg.GridSpec(dim=3, resolution=(3, 3, 3), origin=(0, 0, 0), extent=(1, 1, 1), order=0))
+    c = np.zeros(27)
+    c[26] = 1.0  # vertex (2,2,2)
+    g.coeffs = c
+    v = tg.eval(g, [[1.0, 1.0, 1.0], [5.0, 5.0, 5.0], [0.75, 0.75, 0.75], [0.0, 0.0, 0.0]])
+    assert v[0] == 1.0 and v[1] == 1.0 and v[2] == pytest.approx(0.125) and v[3] == 0.0
+    with pytest.raises(ValueError, match="NaN coordinate"):
+        tg.eval(g, [[0.5, float("nan"), 0.5]])
+
+
+# ---- backward ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("order", [0, 1, 2])
+def test_backprop_golden(dim, order):
+    z = load_golden("eval_backprop.npz")
+    k = f"d{dim}o{order}_"
+    g = tg.init_grid(gspec(dim, z[k + "res"], order))
+    g.coeffs = z[k + "coeffs"]
+    g.zero_grad()
+    tg.backprop_value_and_spatial(g, z[k + "pts"], z[k + "up"], z[k + "uv"][:, :dim])
+    grad_close(g.grad(), z[k + "bgrad"])
+
+
+def test_backprop_locality_80():
+    g = tg.init_grid(tg.GridSpec(dim=3, resolution=(5, 5, 5), order=2))
+    g.zero_grad()
+    tg.backprop_point(g, [[0.137, -0.295, 0.481]], [1.3])
+    assert int(np.count_nonzero(g.grad())) == 80
+
+
+# ---- losses -------------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("name,cfg", [("paper", tg.LossConfig()),
+                                      ("recon", tg.LossConfig(lambda1=0.0, use_tv=False)),
+                                      ("dw", tg.LossConfig(differentiate_weight=True))])
+def test_total_loss_golden_unfused_and_fused(dim, name, cfg):
+    z = load_golden("loss.npz")
+    k = f"d{dim}_{name}_"
+    spec = gspec(dim, z[k + "res"], 2)
+    g = tg.init_grid(spec)
+    g.coeffs = z[k + "coeffs"]
+    g.zero_grad()
+    terms = tg.total_loss(g, z[k + "samples"], cfg)
+    assert_close(terms.as_array(), z[k + "terms"], 1e-6, floor=1e-30, what="terms")
+    grad_close(g.grad(), z[k + "grad"], what="unfused grad")
+    # fused step: same loss terms (on the pre-step params) and the same full gradient
+    g2 = tg.init_grid(spec)
+    g2.coeffs = z[k + "coeffs"]
+    g2.adam_reset(tg.AdamConfig(lr=1e-2))
+    t2 = tg.train_step(g2, z[k + "samples"], cfg, export_grad=True)
+    assert_close(t2.as_array(), z[k + "terms"], 1e-6, floor=1e-30, what="fused terms")
+    grad_close(g2.grad(), z[k + "grad"], what="fused grad")
+
+
+def test_tv_golden():
+    z = load_golden("loss.npz")
+    for dim in (2, 3):
+        k = f"d{dim}_tv_"
+        g = tg.init_grid(gspec(dim, z[k + "res"], 2))
+        g.coeffs = z[k + "coeffs"]
+        g.zero_grad()
+        tv = tg.tv_loss(g, with_grad=True, scale=0.7)
+        assert tv == pytest.approx(z[k + "tv"][0], rel=1e-6)
+        grad_close(g.grad(), z[k + "grad"], what="tv grad")
+
+
+# ---- Adam + training trajectory ------------------------------------------------------------------
+
+
+def test_adam_golden_and_errors():
+    z = load_golden("train.npz")
+    n = len(z["adam_p0"])
+    g = tg.init_grid(tg.GridSpec(dim=2, resolution=(n, 1 + 1, 1), order=0))  # 2n coeffs
+    p0 = np.concatenate([z["adam_p0"], np.zeros(n)])
+    g.coeffs = p0
+    g.adam_reset(tg.AdamConfig(lr=0.01))
+    import torch
+    gbuf = torch.zeros(2 * n, dtype=torch.float32, device="cuda")
+    for k in range(len(z["adam_grads"])):
+        gbuf[:n] = torch.from_numpy(z["adam_grads"][k].astype(np.float32))
+        tg.adam_step(g, gbuf.data_ptr())
+        assert_close(g.coeffs[:n], z["adam_traj"][k], 1e-5, floor=1e-2, what=f"adam step {k}")
+    before = g.coeffs
+    gbuf[5] = float("nan")
+    with pytest.raises(tg.NumericalError, match="index 5"):
+        tg.adam_step(g, gbuf.data_ptr())
+    assert np.array_equal(g.coeffs, before)
+
+
+def test_training_trajectory_golden():
+    """30 fused steps (2D, order 2, zero init, paper loss, lr 1e-2) vs the reference loss curve."""
+    z = load_golden("train.npz")
+    g = tg.init_grid(gspec(2, z["train_res"], 2))
+    g.adam_reset(tg.AdamConfig(lr=1e-2))
+    terms = []
+    for b in z["train_batches"]:
+        terms.append(tg.train_step(g, b, tg.LossConfig()).as_array())
+    terms = np.array(terms)
+    assert_close(terms[:, 0], z["train_terms"][:, 0], 1e-4, floor=1e-30, what="loss curve")
+    assert_close(g.coeffs, z["train_final"], 1e-3, floor=1e-2, what="final coeffs")
+
+
+def test_async_trajectory_matches_sync():
+    z = load_golden("train.npz")
+    g1 = tg.init_grid(gspec(2, z["train_res"], 2))
+    g2 = tg.init_grid(gspec(2, z["train_res"], 2))
+    for g in (g1, g2):
+        g.adam_reset(tg.AdamConfig(lr=1e-2))
+    sync_terms = [tg.train_step(g1, b).as_array() for b in z["train_batches"]]
+    for b in z["train_batches"]:
+        tg.train_step(g2, b, asynchronous=True)
+    g2.sync()
+    assert np.array_equal(np.array(sync_terms), g2.trace(len(z["train_batches"])))
+    assert np.array_equal(g1.coeffs, g2.coeffs)
+
+
+def test_nonfinite_loss_aborts_and_keeps_params():
+    z = load_golden("train.npz")
+    g = tg.init_grid(gspec(2, z["train_res"], 2))
+    g.adam_reset(tg.AdamConfig(lr=1e-2))
+    for b in z["train_batches"][:3]:
+        tg.train_step(g, b)
+    before = g.coeffs
+    t_before = g.adam_t
+    bad = z["train_batches"][3].copy()
+    bad[17, 3] = np.nan  # NaN target -> non-finite loss
+    with pytest.raises(tg.NumericalError, match="non-finite loss at stage 0 step 3"):
+        tg.train_step(g, bad)
+    assert np.array_equal(g.coeffs, before) and g.adam_t == t_before
+    # async: the failing step and every later one are no-ops; sync reports it
+    for b in [z["train_batches"][4], bad, z["train_batches"][5]]:
+        tg.train_step(g, b, asynchronous=True)
+    with pytest.raises(tg.NumericalError, match="non-finite loss"):
+        g.sync()
+    nan_pt = z["train_batches"][6].copy()
+    nan_pt[3, 0] = np.nan
+    with pytest.raises(ValueError, match="NaN coordinate"):
+        tg.train_step(g, nan_pt)
+
+
+# ---- BASELINE-size properties --------------------------------------------------------------------
+
+
+def test_c2_scale_fused_gradient_vs_oracle(oracle):
+    """C2 shape (128^3, order 2, 2^20 points: 50% uniform, 50% near a sphere r=0.6):
+    fused gradient, loss terms and updated params vs the fp64 oracle, on a
+    random (non-zero) grid so every term is active."""
+    res = (128, 128, 128)
+    s = ospec(3, res, 2)
+    rng = np.random.default_rng(11)
+    c = (0.01 * rng.standard_normal(s.V * s.K)).astype(np.float32)
+    smp = tg.sample(tg.SHAPE_SPHERE, 3, 99, 1 << 20, near_frac=0.5, sigma=0.01, param0=0.6)
+    g = tg.init_grid(gspec(3, res, 2))
+    g.set_coeffs_f32(c)
+    g.adam_reset(tg.AdamConfig(lr=1e-2))
+    t = tg.train_step(g, smp, tg.LossConfig(), export_grad=True)
+    gref = np.zeros(s.V * s.K)
+    tref = oracle.total_loss(s, c.astype(np.float64), smp.astype(np.float64), Loss(), gref)
+    assert_close(t.as_array(), tref, 1e-5, floor=1e-30, what="terms")
+    grad_close(g.grad(), gref, what="C2 fused grad")
+    # first Adam step: p - lr * g / (|g| + eps) (bias-corrected), fp32 state
+    p1 = c.astype(np.float64) - 1e-2 * gref / (np.abs(gref) + 1e-8)
+    assert_close(g.coeffs, p1, 1e-6, floor=1.0 + 0 * p1, what="params after step")
