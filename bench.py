@@ -223,30 +223,40 @@ def query_leg(device, hbm_peak, reps=10):
     pts = torch.empty((n, 3), dtype=torch.float32, device=f"cuda:{device}")
     tg.sample_uniform_device(3, 4242, pts)
     spts = torch.empty_like(pts)
+    vals = torch.empty(n, dtype=torch.float32, device=pts.device)
     st = torch.cuda.current_stream()
     out = {}
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     U = count_unique_vertices(pts, res, 1)
+    offs = None
     for order in (1, 2):
         g = tg.init_grid(tg.GridSpec(dim=3, resolution=res, order=order),
                          tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.1, seed=7, memory_cap_bytes=1 << 40),
                          device=device)
         K = g.spec.coeffs_per_vertex()
-        if order == 1:
+        if offs is None:
+            offs = torch.empty(tg.query_brick_codes(g) + 1, dtype=torch.int64, device=pts.device)
             t0.record(st)
-            tg.sort_points(g, pts, spts)
+            tg.sort_points(g, pts, spts, None, offs)
             t1.record(st)
             torch.cuda.synchronize()
             out["sort_ms"] = t0.elapsed_time(t1)
         alg = n * (4 * 3 + 4) + U * K * 4
-        for mode, src, srt in (("unsorted", pts, False), ("sorted", spts, True)):
-            tg.eval(g, src, sorted_points=srt)  # warm-up
+
+        def run(mode):
+            if mode == "unsorted":
+                tg.eval_device(g, pts, vals, asynchronous=True)
+            else:
+                tg.eval_sorted(g, spts, offs, vals, asynchronous=True)
+
+        for mode in ("unsorted", "sorted"):
+            run(mode)  # warm-up
             torch.cuda.synchronize()
             t0.record(st)
             for _ in range(reps):
-                tg.eval(g, src, sorted_points=srt)
+                run(mode)
             t1.record(st)
             torch.cuda.synchronize()
             ms = t0.elapsed_time(t1) / reps
@@ -258,7 +268,7 @@ def query_leg(device, hbm_peak, reps=10):
     out["unique_vertices"] = U
     out["grid"] = list(res)
     out["algorithmic_bytes"] = "N*(4D+4) + U*K*4 (SURVEY 8d B_q)"
-    del pts, spts
+    del pts, spts, vals, offs
     torch.cuda.empty_cache()
     return out
 

@@ -133,11 +133,19 @@ int tgcu_grid_all_finite(tgcu_grid* g, int* out);
 int tgcu_eval(tgcu_grid* g, const float* pts, int64_t n, float* values, float* spatial_grad,
               int flags, void* stream);
 
-/* Morton/brick sort of query points for the brick-binned query
- * (eval with TGCU_SORTED). perm (nullable) receives the source index of each
- * output point. Device pointers only. */
+/* Morton/brick sort of query points for the brick-binned query: points are
+ * ordered by the Morton code of their cell's brick (8^3 / 16^2 cells), then
+ * by cell inside the brick. perm (nullable) receives the source index of each
+ * output point; brick_offsets (nullable, tgcu_query_brick_codes()+1 entries)
+ * the start of every brick's run. Device pointers only. */
 int tgcu_sort_points(tgcu_grid* g, const float* pts, int64_t n, float* sorted_pts, int64_t* perm,
-                     void* stream);
+                     int64_t* brick_offsets, void* stream);
+int64_t tgcu_query_brick_codes(const tgcu_grid* g);
+/* Brick-binned query of sorted points: one CTA per brick stages the brick's
+ * vertex tile in shared memory. brick_offsets from tgcu_sort_points, or NULL
+ * (then computed by one extra pass over the points). Device pointers. */
+int tgcu_eval_sorted(tgcu_grid* g, const float* sorted_pts, int64_t n, const int64_t* brick_offsets,
+                     float* values, float* spatial_grad, int flags, void* stream);
 
 /* backprop_value_and_spatial (taylor_grid.cpp:223-229), batched: adds
  * upstream[i]·∂f/∂c + upstream_vec[i]·∂∇f/∂c into grad (device, coeff_total

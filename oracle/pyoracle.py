@@ -102,6 +102,8 @@ class Oracle:
         L.tgo_adam_step.argtypes = [_D, _D, _D, _D, C.c_int64, _L] + [C.c_double] * 4
         L.tgo_multilinear_resample.argtypes = [C.POINTER(_TgoSpec), _D, C.c_int, _I, _D]
         L.tgo_coeff_count.argtypes = [C.c_int, C.c_int]
+        L.tgo_backprop_mass.argtypes = [C.POINTER(_TgoSpec), _D, C.c_double, _D, _D]
+        L.tgo_total_loss_mass.argtypes = [C.POINTER(_TgoSpec), _D, _D, C.c_int64, C.POINTER(_TgoLoss), _D]
         L.tgo_markstein_div.restype = C.c_double
         L.tgo_markstein_div.argtypes = [C.c_double] * 3
         self.L = L
@@ -147,6 +149,25 @@ class Oracle:
 
     def adaptive_weight(self, a, b, k):
         return self.L.tgo_adaptive_weight(a, b, k)
+
+    def backprop_mass(self, s: Spec, pts, upstream, upstream_vec):
+        sp = self._spec(s)
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        uv = np.ascontiguousarray(upstream_vec, dtype=np.float64).reshape(-1, 3)
+        mass = np.zeros(s.V * s.K)
+        for i in range(len(pts)):
+            self.L.tgo_backprop_mass(C.byref(sp), _dp(pts[i]), float(upstream[i]), _dp(uv[i]), _dp(mass))
+        return mass
+
+    def total_loss_mass(self, s: Spec, coeffs, samples, cfg: Loss):
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        samples = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 4)
+        lc = _TgoLoss(cfg.lambda1, cfg.lambda2, cfg.k, int(cfg.use_weighting), int(cfg.use_tv),
+                      int(cfg.differentiate_weight))
+        mass = np.zeros(s.V * s.K)
+        self.L.tgo_total_loss_mass(C.byref(self._spec(s)), _dp(coeffs), _dp(samples), len(samples),
+                                   C.byref(lc), _dp(mass))
+        return mass
 
     def tv_loss(self, s: Spec, coeffs, grad=None, scale=1.0):
         coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)

@@ -199,6 +199,48 @@ static void accumulate_cell(const tgo_spec* s, const corners_t* c, double upstre
     }
 }
 
+/* L1 mass of the same contributions (|alpha*phi| + |beta*g.dphi| per term):
+ * the scale against which reordering the fp additions can perturb a sum. Used
+ * by the GPU parity tests to bound accumulation-order error. */
+static void accumulate_cell_mass(const tgo_spec* s, const corners_t* c, double upstream,
+                                 const double gvec[3], double* mass) {
+    const int K = tgo_coeff_count(s->order, s->dim);
+    const int dim = s->dim;
+    for (int i = 0; i < c->count; ++i) {
+        double* g = mass + c->vid[i] * K;
+        const double* d = c->delta[i];
+        const double dot = gvec[0] * c->dw[i][0] + gvec[1] * c->dw[i][1] + gvec[2] * c->dw[i][2];
+        const double alpha = fabs(upstream * c->w[i]) + fabs(dot);
+        const double beta = fabs(c->w[i]);
+        g[0] += alpha;
+        if (s->order >= 1)
+            for (int a = 0; a < dim; ++a) g[1 + a] += fabs(alpha * d[a]) + fabs(beta * gvec[a]);
+        if (s->order >= 2) {
+            const int(*pairs)[2] = dim == 2 ? kPairs2 : kPairs3;
+            const int npairs = dim * (dim + 1) / 2;
+            double* q = g + 1 + dim;
+            for (int t = 0; t < npairs; ++t) {
+                const int j = pairs[t][0], k = pairs[t][1];
+                if (j == k)
+                    q[t] += fabs(alpha * 0.5 * d[j] * d[j]) + fabs(beta * gvec[j] * d[j]);
+                else
+                    q[t] += fabs(alpha * d[j] * d[k]) + fabs(beta * gvec[j] * d[k]) + fabs(beta * gvec[k] * d[j]);
+            }
+        }
+    }
+}
+
+void tgo_backprop_mass(const tgo_spec* s, const double p[3], double upstream, const double gvec[3],
+                       double* mass) {
+    int cell[3];
+    double local[3];
+    int64_t vid[8];
+    if (tgo_locate(s, p, cell, local, vid) != 0) return;
+    corners_t c;
+    make_corners(s, local, vid, &c);
+    accumulate_cell_mass(s, &c, upstream, gvec, mass);
+}
+
 void tgo_backprop(const tgo_spec* s, const double p[3], double upstream, const double gvec[3],
                   double* grad) {
     int cell[3];
@@ -315,7 +357,8 @@ double tgo_tv_loss(const tgo_spec* s, const double* coeffs, double* g, double sc
 /* point_terms_chunk, sequential (sdf_loss.cpp:37-85). */
 static void point_terms(const tgo_spec* s, const double* coeffs, const double* samples, int64_t n,
                         const tgo_loss_cfg* cfg, int want_eik, double recon_scale,
-                        double eik_scale, double* grad, double* recon_out, double* eik_out) {
+                        double eik_scale, double* grad, double* mass, double* recon_out,
+                        double* eik_out) {
     const double inv_n = 1.0 / (double)n;
     double recon = 0.0, eik = 0.0;
     for (int64_t i = 0; i < n; ++i) {
@@ -329,7 +372,7 @@ static void point_terms(const tgo_spec* s, const double* coeffs, const double* s
         recon += w * fabs(resid);
         double upstream = 0.0;
         double uvec[3] = {0.0, 0.0, 0.0};
-        if (grad) {
+        if (grad || mass) {
             upstream = recon_scale * inv_n * w * sign_of(resid);
             if (cfg->use_weighting && cfg->differentiate_weight) {
                 const double wp_pred = w_prime(value, cfg->k);
@@ -342,7 +385,7 @@ static void point_terms(const tgo_spec* s, const double* coeffs, const double* s
             const double nrm = sqrt(sg[0] * sg[0] + sg[1] * sg[1] + sg[2] * sg[2]);
             const double r = nrm - 1.0;
             eik += r * r;
-            if (grad && nrm > 0.0) {
+            if ((grad || mass) && nrm > 0.0) {
                 const double sc = eik_scale * inv_n * 2.0 * r / nrm;
                 uvec[0] = sc * sg[0];
                 uvec[1] = sc * sg[1];
@@ -350,6 +393,7 @@ static void point_terms(const tgo_spec* s, const double* coeffs, const double* s
             }
         }
         if (grad) tgo_backprop(s, p, upstream, uvec, grad);
+        if (mass) tgo_backprop_mass(s, p, upstream, uvec, mass);
     }
     *recon_out = recon;
     *eik_out = eik;
@@ -360,7 +404,7 @@ void tgo_total_loss(const tgo_spec* s, const double* coeffs, const double* sampl
     double fit = 0.0, eik = 0.0, tv = 0.0, recon_sum = 0.0, eik_sum = 0.0;
     const int want_eik = cfg->lambda1 > 0.0;
     point_terms(s, coeffs, samples, n, cfg, want_eik, 1.0, want_eik ? cfg->lambda1 : 0.0, grad,
-                &recon_sum, &eik_sum);
+                NULL, &recon_sum, &eik_sum);
     fit = recon_sum / (double)n;
     if (want_eik) eik = eik_sum / (double)n;
     if (cfg->use_tv && cfg->lambda2 > 0.0)
@@ -435,4 +479,42 @@ double tgo_markstein_div(double x, double h, double inv_h) {
     const double q = x * inv_h;
     const double r = fma(-q, h, x);
     return fma(r, inv_h, q);
+}
+
+/* L1 mass of every gradient contribution of tgo_total_loss (point terms and
+ * TV pair terms), per coefficient. Test helper for order-independent
+ * tolerances. */
+void tgo_total_loss_mass(const tgo_spec* s, const double* coeffs, const double* samples, int64_t n,
+                         const tgo_loss_cfg* cfg, double* mass) {
+    double r, e;
+    const int want_eik = cfg->lambda1 > 0.0;
+    point_terms(s, coeffs, samples, n, cfg, want_eik, 1.0, want_eik ? cfg->lambda1 : 0.0, NULL, mass,
+                &r, &e);
+    if (!(cfg->use_tv && cfg->lambda2 > 0.0)) return;
+    const int K = tgo_coeff_count(s->order, s->dim);
+    int64_t pair_count = 0;
+    for (int a = 0; a < s->dim; ++a) {
+        int64_t np = s->res[a] - 1;
+        for (int b = 0; b < s->dim; ++b)
+            if (b != a) np *= s->res[b];
+        pair_count += np;
+    }
+    const double gscale = 2.0 * cfg->lambda2 / ((double)pair_count * K);
+    const int rx = s->res[0], ry = s->res[1], rz = s->dim == 3 ? s->res[2] : 1;
+    const int64_t st[3] = {1, rx, (int64_t)rx * ry};
+    for (int z = 0; z < rz; ++z)
+        for (int y = 0; y < ry; ++y)
+            for (int x = 0; x < rx; ++x) {
+                const int co[3] = {x, y, z};
+                const int64_t v = z * st[2] + y * st[1] + x;
+                for (int a = 0; a < s->dim; ++a) {
+                    if (co[a] + 1 >= s->res[a]) continue;
+                    const int64_t u = v + st[a];
+                    for (int ch = 0; ch < K; ++ch) {
+                        const double d = fabs(gscale * (coeffs[u * K + ch] - coeffs[v * K + ch]));
+                        mass[v * K + ch] += d;
+                        mass[u * K + ch] += d;
+                    }
+                }
+            }
 }

@@ -112,7 +112,10 @@ def lib():
     L.tgcu_grid_download_f32.argtypes = [P, P, C.c_int64, C.c_int]
     L.tgcu_grid_all_finite.argtypes = [P, C.POINTER(C.c_int)]
     L.tgcu_eval.argtypes = [P, P, C.c_int64, P, P, C.c_int, P]
-    L.tgcu_sort_points.argtypes = [P, P, C.c_int64, P, P, P]
+    L.tgcu_sort_points.argtypes = [P, P, C.c_int64, P, P, P, P]
+    L.tgcu_query_brick_codes.argtypes = [P]
+    L.tgcu_query_brick_codes.restype = C.c_int64
+    L.tgcu_eval_sorted.argtypes = [P, P, C.c_int64, P, P, P, C.c_int, P]
     L.tgcu_backprop.argtypes = [P, P, P, P, C.c_int64, P, C.c_int, P]
     L.tgcu_grad_zero.argtypes = [P, P, P]
     L.tgcu_grad_download_f64.argtypes = [P, P, P, C.c_int64]
@@ -426,11 +429,39 @@ def _eval(grid, points, want_grad, sorted_points):
     return vals.astype(np.float64), (grads.astype(np.float64)[:, :grid.spec.dim] if want_grad else None)
 
 
-def sort_points(grid: TaylorGrid, points_dev, out_dev, perm_dev=None):
-    """Brick/Morton sort of device query points for the brick-binned query."""
+def query_brick_codes(grid: TaylorGrid) -> int:
+    return int(lib().tgcu_query_brick_codes(grid.handle))
+
+
+def sort_points(grid: TaylorGrid, points_dev, out_dev, perm_dev=None, offsets_dev=None):
+    """Brick/Morton sort of device query points for the brick-binned query.
+    offsets_dev: optional int64 CUDA tensor of query_brick_codes(grid)+1 entries."""
     import torch
     _check(lib().tgcu_sort_points(grid.handle, _ptr(points_dev), points_dev.shape[0], _ptr(out_dev),
-                                  _ptr(perm_dev), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+                                  _ptr(perm_dev), _ptr(offsets_dev),
+                                  C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
+
+def eval_device(grid: TaylorGrid, points_dev, values_dev, grads_dev=None, asynchronous: bool = False):
+    """Direct-gather query of device points into preallocated device outputs."""
+    import torch
+    _check(lib().tgcu_eval(grid.handle, _ptr(points_dev), points_dev.shape[0], _ptr(values_dev), _ptr(grads_dev),
+                           TGCU_ASYNC if asynchronous else 0,
+                           C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return values_dev
+
+
+def eval_sorted(grid: TaylorGrid, sorted_dev, offsets_dev=None, values_dev=None, grads_dev=None,
+                asynchronous: bool = False):
+    """Brick-binned query of sorted device points (tgcu_eval_sorted)."""
+    import torch
+    n = sorted_dev.shape[0]
+    if values_dev is None:
+        values_dev = torch.empty(n, dtype=torch.float32, device=sorted_dev.device)
+    _check(lib().tgcu_eval_sorted(grid.handle, _ptr(sorted_dev), n, _ptr(offsets_dev), _ptr(values_dev),
+                                  _ptr(grads_dev), TGCU_ASYNC if asynchronous else 0,
+                                  C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return values_dev
 
 
 # ---- backward ---------------------------------------------------------------

@@ -420,7 +420,7 @@ int tgcu_eval(tgcu_grid* h, const float* pts, int64_t n, float* values, float* s
             dp = sp;
         }
         if (flags & TGCU_SORTED)
-            launch_eval_sorted(g, dp, n, dv, dg, s);
+            launch_eval_sorted(g, dp, n, nullptr, dv, dg, s);
         else
             launch_eval_direct(g, dp, n, dv, dg, s);
         if (flags & TGCU_HOST) {
@@ -432,11 +432,27 @@ int tgcu_eval(tgcu_grid* h, const float* pts, int64_t n, float* values, float* s
     });
 }
 
-int tgcu_sort_points(tgcu_grid* h, const float* pts, int64_t n, float* sorted_pts, int64_t* perm, void* stream) {
+int tgcu_sort_points(tgcu_grid* h, const float* pts, int64_t n, float* sorted_pts, int64_t* perm,
+                     int64_t* brick_offsets, void* stream) {
     return guard([&] {
         Grid& g = h->g;
         set_device(g);
-        launch_sort_points(g, pts, n, sorted_pts, perm, as_stream(stream));
+        launch_sort_points(g, pts, n, sorted_pts, perm, brick_offsets, as_stream(stream));
+    });
+}
+
+int64_t tgcu_query_brick_codes(const tgcu_grid* h) { return query_brick_codes(h->g); }
+
+int tgcu_eval_sorted(tgcu_grid* h, const float* pts, int64_t n, const int64_t* brick_offsets, float* values,
+                     float* spatial_grad, int flags, void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(!(flags & TGCU_HOST), "eval_sorted: device pointers only");
+        if (n <= 0) return;
+        cudaStream_t s = as_stream(stream);
+        launch_eval_sorted(g, pts, n, brick_offsets, values, spatial_grad, s);
+        if (!(flags & TGCU_ASYNC)) check_nan_points(g, s);
     });
 }
 

@@ -160,7 +160,61 @@ __global__ void k_gather_points(const float* __restrict__ pts, const long long* 
 template <int DIM>
 constexpr int brick_log2() { return DIM == 3 ? 3 : 4; }
 
-void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, cudaStream_t s) {
+// Number of Morton brick codes of the query decomposition (pow2^DIM).
+int64_t query_brick_codes(const Grid& g) {
+    const int LB = g.spec.dim == 3 ? 3 : 4;
+    const int B = 1 << LB;
+    unsigned int pow2 = 1;
+    for (int a = 0; a < g.spec.dim; ++a) {
+        const int nb = (g.spec.res[a] - 1 + B - 1) / B;  // bricks of cells
+        while (pow2 < (unsigned)nb) pow2 <<= 1;
+    }
+    int64_t codes = 1;
+    for (int a = 0; a < g.spec.dim; ++a) codes *= pow2;
+    return codes;
+}
+
+// off[c] = first sorted index whose brick code >= c, for c in [0, codes].
+// Each i writes the codes in (code(i-1), code(i)]; the last point also writes
+// the tail up to `codes`.
+template <int DIM, int LB, bool FROM_KEYS>
+__global__ void k_brick_offsets(DevSpec s, const unsigned long long* __restrict__ keys, const float* __restrict__ pts,
+                                long long n, long long codes, long long* __restrict__ off) {
+    constexpr int SH = DIM * LB;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n;
+         i += (long long)gridDim.x * blockDim.x) {
+        long long prev = -1, cur = codes;
+        unsigned int kb;
+        if (i > 0) {
+            if (FROM_KEYS) prev = (long long)(keys[i - 1] >> SH);
+            else { point_key<DIM, LB>(s, pts + 3 * (i - 1), &kb); prev = kb; }
+        }
+        if (i < n) {
+            if (FROM_KEYS) cur = (long long)(keys[i] >> SH);
+            else { point_key<DIM, LB>(s, pts + 3 * i, &kb); cur = kb; }
+        }
+        for (long long c = prev + 1; c <= cur; ++c) off[c] = i;
+    }
+}
+
+void launch_brick_offsets(Grid& g, const unsigned long long* keys, const float* pts, int64_t n, int64_t* off,
+                          cudaStream_t s) {
+    const long long codes = query_brick_codes(g);
+    const int blocks = grid_blocks(n + 1, 256, 148 * 32);
+    long long* o = reinterpret_cast<long long*>(off);
+    if (g.spec.dim == 3) {
+        if (keys) k_brick_offsets<3, 3, true><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
+        else k_brick_offsets<3, 3, false><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
+    } else {
+        if (keys) k_brick_offsets<2, 4, true><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
+        else k_brick_offsets<2, 4, false><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
+    }
+    count_launch();
+    TGCU_CUDA(cudaGetLastError());
+}
+
+void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, int64_t* offsets,
+                        cudaStream_t s) {
     if (n <= 0) return;
     unsigned long long *keys = nullptr, *keys_out = nullptr;
     long long *idx = nullptr, *idx_out = nullptr;
@@ -176,22 +230,13 @@ void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_
         own_perm = true;
     }
     const int blocks = grid_blocks(n, 256, 148 * 32);
-    int end_bit = 0;
-    if (g.spec.dim == 3) {
-        k_point_keys<3, 3><<<blocks, 256, 0, s>>>(g.ds, pts, n, keys, idx);
-        int maxc = 1;
-        for (int a = 0; a < 3; ++a) maxc = std::max(maxc, g.spec.res[a] - 2);
-        int bits = 1;
-        while ((1 << bits) <= maxc) ++bits;
-        end_bit = 3 * bits;
-    } else {
-        k_point_keys<2, 4><<<blocks, 256, 0, s>>>(g.ds, pts, n, keys, idx);
-        int maxc = 1;
-        for (int a = 0; a < 2; ++a) maxc = std::max(maxc, g.spec.res[a] - 2);
-        int bits = 1;
-        while ((1 << bits) <= maxc) ++bits;
-        end_bit = 2 * bits;
-    }
+    int maxc = 1;
+    for (int a = 0; a < g.spec.dim; ++a) maxc = std::max(maxc, g.spec.res[a] - 2);
+    int bits = 1;
+    while ((1 << bits) <= maxc) ++bits;
+    const int end_bit = g.spec.dim * bits;
+    if (g.spec.dim == 3) k_point_keys<3, 3><<<blocks, 256, 0, s>>>(g.ds, pts, n, keys, idx);
+    else k_point_keys<2, 4><<<blocks, 256, 0, s>>>(g.ds, pts, n, keys, idx);
     count_launch();
     TGCU_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, keys_out, idx, idx_out, (int64_t)n, 0,
                                               end_bit, s));
@@ -200,6 +245,7 @@ void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_
                                               end_bit, s));
     k_gather_points<<<blocks, 256, 0, s>>>(pts, idx_out, n, out);
     count_launch();
+    if (offsets) launch_brick_offsets(g, keys_out, nullptr, n, offsets, s);
     TGCU_CUDA(cudaFreeAsync(temp, s));
     TGCU_CUDA(cudaFreeAsync(keys, s));
     TGCU_CUDA(cudaFreeAsync(keys_out, s));
@@ -208,60 +254,52 @@ void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_
     TGCU_CUDA(cudaGetLastError());
 }
 
-// One CTA per brick (in Morton order = blockIdx.x). Tile: (B+1)^DIM vertices.
+// One CTA per Morton brick code (blockIdx.x). The brick's (B+1)^DIM vertex
+// tile arrives in smem by cp.async (8-byte granules, zero-filled outside the
+// grid); its points are [off[code], off[code+1]) of the brick-sorted array.
 template <int DIM, int ORDER, bool GRAD, int LB>
 __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __restrict__ coeffs,
-                                                    const float* __restrict__ pts, long long n,
+                                                    const float* __restrict__ pts, const long long* __restrict__ off,
                                                     float* __restrict__ vals, float* __restrict__ grads,
-                                                    Status* st, int nbx, int nby, int nbz) {
+                                                    Status* st) {
     constexpr int K = KOf<DIM, ORDER>::value;
     constexpr int B = 1 << LB;
-    constexpr int T = B + 1;                        // tile edge in vertices
-    constexpr int TV = DIM == 3 ? T * T * T : T * T;  // tile vertices
-    extern __shared__ __align__(16) float tile[];   // TV * K
+    constexpr int T = B + 1;  // tile edge in vertices
+    constexpr int GR = (K % 2 == 0) ? 2 : 1;
+    extern __shared__ __align__(16) float tile[];  // T^DIM * K
 
-    // Decode this brick's coordinates from the Morton index.
     const unsigned int code = blockIdx.x;
+    const long long p0 = off[code], p1 = off[code + 1];
+    if (p0 >= p1) return;
     unsigned int b[3] = {0, 0, 0};
-    for (int bit = 0; bit < 21; ++bit) {
+#pragma unroll
+    for (int bit = 0; bit < 10; ++bit) {
 #pragma unroll
         for (int a = 0; a < DIM; ++a) b[a] |= ((code >> (bit * DIM + a)) & 1u) << bit;
     }
-    if ((int)b[0] >= nbx || (int)b[1] >= nby || (DIM == 3 && (int)b[2] >= nbz)) return;
-
-    // Binary search this brick's [lo, hi) range in the brick-sorted points.
-    __shared__ long long range[2];
-    if (threadIdx.x < 2) {
-        const unsigned int target = code + threadIdx.x;
-        long long lo = 0, hi = n;
-        while (lo < hi) {
-            const long long mid = (lo + hi) >> 1;
-            unsigned int kb;
-            point_key<DIM, LB>(s, pts + 3 * mid, &kb);
-            if (kb < target) lo = mid + 1; else hi = mid;
-        }
-        range[threadIdx.x] = lo;
-    }
-    __syncthreads();
-    const long long p0 = range[0], p1 = range[1];
-    if (p0 >= p1) return;
-
-    // Stage the vertex tile: rows of T vertices x K coefficients are contiguous.
     const int ox = b[0] * B, oy = b[1] * B, oz = DIM == 3 ? b[2] * B : 0;
-    constexpr int ROW = T * K;
-    const int rows = DIM == 3 ? T * T : T;
-    for (int e = threadIdx.x; e < rows * ROW; e += blockDim.x) {
-        const int r = e / ROW, q = e - r * ROW;
-        const int tx = q / K, ch = q - tx * K;
-        const int ty = r % T, tz = r / T;
-        const int vx = ox + tx, vy = oy + ty, vz = oz + tz;
-        float val = 0.0f;
-        if (vx < s.res[0] && vy < s.res[1] && (DIM == 2 || vz < s.res[2]))
-            val = __ldg(coeffs + ((long long)vz * s.sz + (long long)vy * s.sy + vx) * K + ch);
-        tile[e] = val;
+    {
+        constexpr int ROWG = T * K / GR;
+        constexpr int ROWS = DIM == 3 ? T * T : T;
+        for (int e = threadIdx.x; e < ROWS * ROWG; e += blockDim.x) {
+            const int r = e / ROWG, q = (e - r * ROWG) * GR;
+            const int tx = q / K;
+            const int ty = r % T, tz = r / T;
+            const int vx = ox + tx, vy = oy + ty, vz = oz + tz;
+            const bool ok = vx < s.res[0] && vy < s.res[1] && (DIM == 2 || vz < s.res[2]);
+            const long long gi = ok ? ((long long)vz * s.sz + (long long)vy * s.sy + vx) * K + (q - tx * K) : 0;
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(tile + r * T * K + q);
+            const int nb = ok ? 4 * GR : 0;
+            if constexpr (GR == 2)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(coeffs + gi), "r"(nb) : "memory");
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(coeffs + gi), "r"(nb) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
 
+    const int o3[3] = {ox, oy, oz};
     for (long long i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
         double x[DIM];
         bool nan = false;
@@ -279,7 +317,6 @@ __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __re
         }
         AxisF ax[DIM];
         int lc[3] = {0, 0, 0};
-        const int o3[3] = {ox, oy, oz};
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
             double local;
@@ -288,20 +325,16 @@ __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __re
             lc[a] = c - o3[a];
         }
         const int tbase = DIM == 3 ? (lc[2] * T + lc[1]) * T + lc[0] : lc[1] * T + lc[0];
-        float cb[1 << DIM][K];
-#pragma unroll
-        for (int c = 0; c < (1 << DIM); ++c) {
-            const int tv = tbase + (c & 1) + ((c >> 1) & 1) * T + (DIM == 3 ? ((c >> 2) & 1) * T * T : 0);
-            load_block<K, false>(tile + tv * K, cb[c]);
-        }
         float f = 0.0f;
         float fg[DIM];
 #pragma unroll
         for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
 #pragma unroll
         for (int c = 0; c < (1 << DIM); ++c) {
-            const Corner<DIM> g = corner_geom<DIM>(s, ax, c);
-            blend_corner<DIM, ORDER, GRAD>(cb[c], g, f, fg);
+            const int tv = tbase + (c & 1) + ((c >> 1) & 1) * T + (DIM == 3 ? ((c >> 2) & 1) * T * T : 0);
+            float cb[K];
+            load_block<K, false>(tile + tv * K, cb);
+            blend_corner<DIM, ORDER, GRAD>(cb, corner_geom<DIM>(s, ax, c), f, fg);
         }
         vals[i] = f;
         if (GRAD) {
@@ -309,11 +342,19 @@ __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __re
             for (int a = 0; a < 3; ++a) grads[3 * i + a] = a < DIM ? fg[a] : 0.0f;
         }
     }
-    (void)TV;
 }
 
-void launch_eval_sorted(Grid& g, const float* pts, int64_t n, float* vals, float* grads, cudaStream_t s) {
+void launch_eval_sorted(Grid& g, const float* pts, int64_t n, const int64_t* offsets, float* vals, float* grads,
+                        cudaStream_t s) {
     if (n <= 0) return;
+    const int64_t codes = query_brick_codes(g);
+    long long* tmp = nullptr;
+    if (!offsets) {  // points sorted but no offsets given: one boundary pass
+        TGCU_CUDA(cudaMallocAsync(&tmp, sizeof(long long) * (codes + 1), s));
+        launch_brick_offsets(g, nullptr, pts, n, reinterpret_cast<int64_t*>(tmp), s);
+        offsets = reinterpret_cast<const int64_t*>(tmp);
+    }
+    const long long* off = reinterpret_cast<const long long*>(offsets);
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
         constexpr int LB = brick_log2<DIM>();
         constexpr int B = 1 << LB;
@@ -321,20 +362,12 @@ void launch_eval_sorted(Grid& g, const float* pts, int64_t n, float* vals, float
         constexpr int T = B + 1;
         constexpr int TV = DIM == 3 ? T * T * T : T * T;
         const size_t smem = sizeof(float) * TV * K;
-        int nbv[3] = {1, 1, 1};
-        unsigned int pow2 = 1;
-        for (int a = 0; a < DIM; ++a) {
-            nbv[a] = (g.spec.res[a] - 1 + B - 1) / B;  // bricks of cells
-            while (pow2 < (unsigned)nbv[a]) pow2 <<= 1;
-        }
-        unsigned long long blocks = 1;
-        for (int a = 0; a < DIM; ++a) blocks *= pow2;
         auto kern = grads ? k_eval_brick<DIM, ORDER, true, LB> : k_eval_brick<DIM, ORDER, false, LB>;
         TGCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)blocks, 256, smem, s>>>(g.ds, g.p[g.cur], pts, n, vals, grads, g.st, nbv[0], nbv[1],
-                                                  nbv[2]);
+        kern<<<(unsigned)codes, 256, smem, s>>>(g.ds, g.p[g.cur], pts, off, vals, grads, g.st);
     });
     count_launch();
+    if (tmp) TGCU_CUDA(cudaFreeAsync(tmp, s));
     TGCU_CUDA(cudaGetLastError());
 }
 

@@ -96,8 +96,11 @@ void ensure_optimizer(Grid& g);
 
 // Launchers (query.cu / train.cu). All stream-ordered; no synchronisation.
 void launch_eval_direct(Grid& g, const float* pts, int64_t n, float* vals, float* grads, cudaStream_t s);
-void launch_eval_sorted(Grid& g, const float* pts, int64_t n, float* vals, float* grads, cudaStream_t s);
-void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, cudaStream_t s);
+void launch_eval_sorted(Grid& g, const float* pts, int64_t n, const int64_t* offsets, float* vals, float* grads,
+                        cudaStream_t s);
+void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, int64_t* offsets,
+                        cudaStream_t s);
+int64_t query_brick_codes(const Grid& g);
 void launch_backprop(Grid& g, const float* pts, const float* up, const float* upv, int64_t n, float* grad,
                      cudaStream_t s);
 // Unfused total_loss pieces: point terms (atomic scatter) + TV; sums land in

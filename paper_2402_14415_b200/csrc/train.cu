@@ -47,18 +47,6 @@ struct BrickShape {
     static constexpr int REC = 8;     // floats per point record
 };
 
-template <int DIM, int ORDER>
-constexpr size_t brick_smem_bytes() {
-    using S = BrickShape<DIM>;
-    constexpr int K = KOf<DIM, ORDER>::value;
-    constexpr size_t tile = sizeof(float) * S::TVN * K;
-    constexpr size_t pts = sizeof(float) * S::CH * S::REC + sizeof(int) * S::CH * 3;
-    constexpr size_t gs = sizeof(float) * S::NOWN * K;
-    constexpr size_t uni = pts > gs ? pts : gs;
-    constexpr size_t cells = sizeof(int) * S::NCELL * 2;
-    return tile + uni + cells;
-}
-
 struct BinArgs {
     DevSpec s;
     const float4* pts;
@@ -222,23 +210,50 @@ __device__ __forceinline__ void block_excl_scan(const int* __restrict__ cnt, int
     }
 }
 
-template <int DIM, int ORDER, bool EIK>
-__global__ void __launch_bounds__(BrickShape<DIM>::NT, 1) k_brick_step(StepArgs A) {
+// cp.async (LDGSTS) of GR floats (4 or 8 bytes); zero-fill when !valid.
+template <int GR>
+__device__ __forceinline__ void cp_async(float* smem_dst, const float* gsrc, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    const int n = valid ? 4 * GR : 0;
+    if constexpr (GR == 2)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(n) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gsrc), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int DIM, int ORDER>
+struct BrickSmem {
     using S = BrickShape<DIM>;
+    static constexpr int K = KOf<DIM, ORDER>::value;
+    static constexpr int tile = S::TVN * K;                         // floats
+    static constexpr int mv = 2 * S::NOWN * K;                      // m then v (prefetched)
+    static constexpr int pts = S::CH * S::REC + S::CH * 3;          // records + 3 int arrays
+    static constexpr int gs = S::NOWN * K;
+    static constexpr int uni = pts > gs ? pts : gs;
+    static constexpr size_t bytes = sizeof(float) * (tile + mv + uni) + sizeof(int) * S::NCELL * 2;
+};
+
+template <int DIM, int ORDER, bool EIK>
+__global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs A) {
+    using S = BrickShape<DIM>;
+    using L = BrickSmem<DIM, ORDER>;
     constexpr int K = KOf<DIM, ORDER>::value;
     constexpr int B = S::B, T = S::T, CE = S::CE, NT = S::NT, CH = S::CH;
+    constexpr int GR = (K % 2 == 0) ? 2 : 1;  // async-copy granule (floats)
     if (A.st->error) return;
 
     extern __shared__ __align__(16) float smem[];
-    float* tile = smem;                               // TVN*K
-    float* uni = tile + S::TVN * K;                   // point records | Gs
-    float* rec = uni;                                 // CH*REC
+    float* tile = smem;                 // TVN*K   current parameters + halo
+    float* mvs = tile + L::tile;        // 2*NOWN*K  m, v of the owned vertices
+    float* uni = mvs + L::mv;           // point records | Gs
+    float* rec = uni;                   // CH*REC
     int* cellof = reinterpret_cast<int*>(rec + CH * S::REC);
     int* rankof = cellof + CH;
     int* order = rankof + CH;
-    constexpr size_t uni_floats =
-        (CH * S::REC + CH * 3) > (S::NOWN * K) ? (CH * S::REC + CH * 3) : (S::NOWN * K);
-    int* cnt = reinterpret_cast<int*>(uni + uni_floats);
+    int* cnt = reinterpret_cast<int*>(uni + L::uni);
     int* start = cnt + S::NCELL;
     __shared__ int warp_tot[32];
     __shared__ double red[3][NT / 32];
@@ -251,21 +266,40 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 1) k_brick_step(StepArgs 
     const int bz = DIM == 3 ? b / (nbx * nby) : 0;
     const int o[3] = {bx * B, by * B, bz * B};
 
-    // ---- 1. stage the parameter tile (vertices o-1 .. o+B per axis) ----
+    // ---- 1. async staging: parameter tile (group 0), then the owned m/v rows
+    //         (group 1), which stay in flight through the whole point phase ----
     {
-        constexpr int ROW = T * K;
+        constexpr int ROWG = T * K / GR;  // granules per tile row
         constexpr int ROWS = DIM == 3 ? T * T : T;
-        for (int e = tid; e < ROWS * ROW; e += NT) {
-            const int r = e / ROW, q = e - r * ROW;
-            const int tx = q / K, ch = q - tx * K;
+        for (int e = tid; e < ROWS * ROWG; e += NT) {
+            const int r = e / ROWG, q = (e - r * ROWG) * GR;
+            const int tx = q / K;
             const int ty = r % T, tz = r / T;
             const int vx = o[0] - 1 + tx, vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
-            float val = 0.0f;
-            if (vx >= 0 && vx < A.s.res[0] && vy >= 0 && vy < A.s.res[1] &&
-                (DIM == 2 || (vz >= 0 && vz < A.s.res[2])))
-                val = A.p_in[((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + vx) * K + ch];
-            tile[e] = val;
+            const bool ok = vx >= 0 && vx < A.s.res[0] && vy >= 0 && vy < A.s.res[1] &&
+                            (DIM == 2 || (vz >= 0 && vz < A.s.res[2]));
+            const long long gi = ok ? ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + vx) * K +
+                                          (q - tx * K)
+                                    : 0;
+            cp_async<GR>(tile + r * T * K + q, A.p_in + gi, ok);
         }
+        cp_async_commit();
+        constexpr int OROWG = B * K / GR;  // granules per owned row
+        constexpr int OROWS = DIM == 3 ? B * B : B;
+        for (int e = tid; e < 2 * OROWS * OROWG; e += NT) {
+            const int which = e / (OROWS * OROWG);
+            const int e2 = e - which * OROWS * OROWG;
+            const int r = e2 / OROWG, q = (e2 - r * OROWG) * GR;
+            const int lx = q / K;
+            const int ly = r % B, lz = r / B;
+            const int vx = o[0] + lx, vy = o[1] + ly, vz = o[2] + lz;
+            const bool ok = vx < A.s.res[0] && vy < A.s.res[1] && (DIM == 2 || vz < A.s.res[2]);
+            const long long gi =
+                ok ? ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + vx) * K + (q - lx * K) : 0;
+            cp_async<GR>(mvs + which * S::NOWN * K + r * B * K + q, (which ? A.v_in : A.m_in) + gi, ok);
+        }
+        cp_async_commit();
+        cp_async_wait<1>();  // tile landed (m/v may still be in flight)
     }
     __syncthreads();
 
@@ -373,6 +407,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 1) k_brick_step(StepArgs 
     float* Gs = uni;
 #pragma unroll
     for (int q = 0; q < K; ++q) Gs[tid * K + q] = G[q];
+    cp_async_wait<0>();  // m/v rows landed
     __syncthreads();
     double tv_sum = 0.0;
     const int tstride[3] = {1, T, T * T};
@@ -406,8 +441,8 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 1) k_brick_step(StepArgs 
             ((DIM == 3 ? (long long)g3[2] * A.s.sz : 0LL) + (long long)g3[1] * A.s.sy + g3[0]) * K + ch;
         if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)gidx);
         if (A.grad_out) A.grad_out[gidx] = gi;
-        const float mi = fmaf(A.b1, A.m_in[gidx], (1.0f - A.b1) * gi);
-        const float vi = fmaf(A.b2, A.v_in[gidx], (1.0f - A.b2) * gi * gi);
+        const float mi = fmaf(A.b1, mvs[e], (1.0f - A.b1) * gi);
+        const float vi = fmaf(A.b2, mvs[S::NOWN * K + e], (1.0f - A.b2) * gi * gi);
         A.m_out[gidx] = mi;
         A.v_out[gidx] = vi;
         A.p_out[gidx] = pv - A.lr * (mi * A.inv_bc1) / (sqrtf(vi * A.inv_bc2) + A.eps);
@@ -575,7 +610,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     A.grad_out = grad_out;
     const bool eik = cfg.lambda1 > 0.0;
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
-        constexpr size_t smem = brick_smem_bytes<DIM, ORDER>();
+        constexpr size_t smem = BrickSmem<DIM, ORDER>::bytes;
         auto kern = eik ? k_brick_step<DIM, ORDER, true> : k_brick_step<DIM, ORDER, false>;
         static bool configured = false;
         if (!configured) {
