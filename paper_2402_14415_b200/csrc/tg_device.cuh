@@ -200,23 +200,32 @@ __device__ __forceinline__ void blend_corner(const float (&c)[K], const Corner<D
 template <int DIM, int ORDER, int K>
 __device__ __forceinline__ void corner_grad(const Corner<DIM>& g, float u, const float* gv,
                                             float (&G)[K]) {
+    // Factored form: with wg_a = w*g_a and a_j = alpha*d_j + wg_j,
+    //   d f1_a  = a_a
+    //   d q_jj  = d_j * (alpha/2 * d_j + wg_j)
+    //   d q_jk  = a_j * d_k + wg_k * d_j
     float alpha = u * g.w;
 #pragma unroll
     for (int a = 0; a < DIM; ++a) alpha = fmaf(gv[a], g.dw[a], alpha);
-    const float beta = g.w;
     G[0] += alpha;
     if constexpr (ORDER >= 1) {
+        float wg[DIM], aj[DIM];
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) G[1 + a] += fmaf(alpha, g.d[a], beta * gv[a]);
-    }
-    if constexpr (ORDER >= 2) {
+        for (int a = 0; a < DIM; ++a) {
+            wg[a] = g.w * gv[a];
+            aj[a] = fmaf(alpha, g.d[a], wg[a]);
+            G[1 + a] += aj[a];
+        }
+        if constexpr (ORDER >= 2) {
+            const float half = 0.5f * alpha;
 #pragma unroll
-        for (int t = 0; t < Pairs<DIM>::n; ++t) {
-            const int j = Pairs<DIM>::j(t), k = Pairs<DIM>::k(t);
-            if (j == k)
-                G[1 + DIM + t] += fmaf(alpha * 0.5f * g.d[j], g.d[j], beta * gv[j] * g.d[j]);
-            else
-                G[1 + DIM + t] += fmaf(alpha * g.d[j], g.d[k], beta * fmaf(gv[j], g.d[k], gv[k] * g.d[j]));
+            for (int t = 0; t < Pairs<DIM>::n; ++t) {
+                const int j = Pairs<DIM>::j(t), k = Pairs<DIM>::k(t);
+                if (j == k)
+                    G[1 + DIM + t] = fmaf(g.d[j], fmaf(half, g.d[j], wg[j]), G[1 + DIM + t]);
+                else
+                    G[1 + DIM + t] += fmaf(aj[j], g.d[k], wg[k] * g.d[j]);
+            }
         }
     }
 }

@@ -268,35 +268,43 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
 
     // ---- 1. async staging: parameter tile (group 0), then the owned m/v rows
     //         (group 1), which stay in flight through the whole point phase ----
+    // Warp-per-row: a row (fixed y, z) is contiguous in HBM; the row's address
+    // and validity are computed once, lanes walk its granules.
+    const int lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = NT / 32;
     {
         constexpr int ROWG = T * K / GR;  // granules per tile row
         constexpr int ROWS = DIM == 3 ? T * T : T;
-        for (int e = tid; e < ROWS * ROWG; e += NT) {
-            const int r = e / ROWG, q = (e - r * ROWG) * GR;
-            const int tx = q / K;
+        for (int r = warp; r < ROWS; r += NW) {
             const int ty = r % T, tz = r / T;
-            const int vx = o[0] - 1 + tx, vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
-            const bool ok = vx >= 0 && vx < A.s.res[0] && vy >= 0 && vy < A.s.res[1] &&
-                            (DIM == 2 || (vz >= 0 && vz < A.s.res[2]));
-            const long long gi = ok ? ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + vx) * K +
-                                          (q - tx * K)
-                                    : 0;
-            cp_async<GR>(tile + r * T * K + q, A.p_in + gi, ok);
+            const int vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
+            const bool row_ok = vy >= 0 && vy < A.s.res[1] && (DIM == 2 || (vz >= 0 && vz < A.s.res[2]));
+            const long long base =
+                ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + (o[0] - 1)) * K;
+            float* dst = tile + r * T * K;
+            for (int gq = lane; gq < ROWG; gq += 32) {
+                const int q = gq * GR;
+                const int vx = o[0] - 1 + q / K;
+                const bool ok = row_ok && vx >= 0 && vx < A.s.res[0];
+                cp_async<GR>(dst + q, ok ? A.p_in + base + q : A.p_in, ok);
+            }
         }
         cp_async_commit();
         constexpr int OROWG = B * K / GR;  // granules per owned row
         constexpr int OROWS = DIM == 3 ? B * B : B;
-        for (int e = tid; e < 2 * OROWS * OROWG; e += NT) {
-            const int which = e / (OROWS * OROWG);
-            const int e2 = e - which * OROWS * OROWG;
-            const int r = e2 / OROWG, q = (e2 - r * OROWG) * GR;
-            const int lx = q / K;
+        for (int t = warp; t < 2 * OROWS; t += NW) {
+            const int which = t / OROWS, r = t - which * OROWS;
             const int ly = r % B, lz = r / B;
-            const int vx = o[0] + lx, vy = o[1] + ly, vz = o[2] + lz;
-            const bool ok = vx < A.s.res[0] && vy < A.s.res[1] && (DIM == 2 || vz < A.s.res[2]);
-            const long long gi =
-                ok ? ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + vx) * K + (q - lx * K) : 0;
-            cp_async<GR>(mvs + which * S::NOWN * K + r * B * K + q, (which ? A.v_in : A.m_in) + gi, ok);
+            const int vy = o[1] + ly, vz = o[2] + lz;
+            const bool row_ok = vy < A.s.res[1] && (DIM == 2 || vz < A.s.res[2]);
+            const long long base = ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0]) * K;
+            const float* src = which ? A.v_in : A.m_in;
+            float* dst = mvs + which * S::NOWN * K + r * B * K;
+            for (int gq = lane; gq < OROWG; gq += 32) {
+                const int q = gq * GR;
+                const bool ok = row_ok && o[0] + q / K < A.s.res[0];
+                cp_async<GR>(dst + q, ok ? src + base + q : src, ok);
+            }
         }
         cp_async_commit();
         cp_async_wait<1>();  // tile landed (m/v may still be in flight)
@@ -410,42 +418,47 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
     cp_async_wait<0>();  // m/v rows landed
     __syncthreads();
     double tv_sum = 0.0;
-    const int tstride[3] = {1, T, T * T};
-    for (int e = tid; e < S::NOWN * K; e += NT) {
-        const int v = e / K, ch = e - v * K;
-        const int l3[3] = {v % B, (v / B) % B, DIM == 3 ? v / (B * B) : 0};
-        int g3[3];
-        bool ok = true;
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) {
-            g3[a] = o[a] + l3[a];
-            ok &= g3[a] < A.s.res[a];
-        }
-        if (!ok) continue;
-        const int tv = DIM == 3 ? ((l3[2] + 1) * T + (l3[1] + 1)) * T + (l3[0] + 1) : (l3[1] + 1) * T + (l3[0] + 1);
-        const float pv = tile[tv * K + ch];
-        float gt = 0.0f;
-        if (A.want_tv) {
-#pragma unroll
-            for (int a = 0; a < DIM; ++a) {
-                if (g3[a] + 1 < A.s.res[a]) {
-                    const float d = tile[(tv + tstride[a]) * K + ch] - pv;
-                    tv_sum += (double)d * (double)d;
-                    gt -= d;
+    const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
+    constexpr int OROWS = DIM == 3 ? B * B : B;
+    constexpr int ROWF = B * K;  // floats per owned row
+    for (int r = warp; r < OROWS; r += NW) {
+        const int ly = r % B, lz = r / B;
+        const int gy = o[1] + ly, gz = o[2] + lz;
+        if (gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
+        const long long rbase = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K;
+        const int trow = DIM == 3 ? ((lz + 1) * T + (ly + 1)) * T + 1 : (ly + 1) * T + 1;  // tile vertex of lx = 0
+        const bool ylo = gy >= 1, yhi = gy + 1 < A.s.res[1];
+        const bool zlo = DIM == 3 && gz >= 1, zhi = DIM == 3 && gz + 1 < A.s.res[2];
+        for (int j = lane; j < ROWF; j += 32) {
+            const int lx = j / K, ch = j - lx * K;
+            const int gx = o[0] + lx;
+            if (gx >= A.s.res[0]) continue;
+            const int e = r * ROWF + j;
+            const float* tp = tile + (trow + lx) * K + ch;
+            const float pv = *tp;
+            float gt = 0.0f;
+            if (A.want_tv) {
+                // TV pairs (v, v+e_a) owned here add to the sum; both pair
+                // ends' terms add to this vertex's gradient (sdf_loss.cpp:155-257).
+                if (gx + 1 < A.s.res[0]) { const float d = tp[K] - pv; tv_sum += (double)d * (double)d; gt -= d; }
+                if (gx >= 1) gt += pv - tp[-K];
+                if (yhi) { const float d = tp[T * K] - pv; tv_sum += (double)d * (double)d; gt -= d; }
+                if (ylo) gt += pv - tp[-T * K];
+                if (DIM == 3) {
+                    if (zhi) { const float d = tp[T * T * K] - pv; tv_sum += (double)d * (double)d; gt -= d; }
+                    if (zlo) gt += pv - tp[-T * T * K];
                 }
-                if (g3[a] >= 1) gt += pv - tile[(tv - tstride[a]) * K + ch];
             }
+            const float gi = fmaf(A.tv_gscale, gt, Gs[e]);
+            const long long gidx = rbase + j;
+            if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)gidx);
+            if (A.grad_out) A.grad_out[gidx] = gi;
+            const float mi = fmaf(A.b1, mvs[e], c1 * gi);
+            const float vi = fmaf(A.b2, mvs[S::NOWN * K + e], c2 * gi * gi);
+            A.m_out[gidx] = mi;
+            A.v_out[gidx] = vi;
+            A.p_out[gidx] = pv - lr_bc1 * mi * __frcp_rn(sqrtf(vi * A.inv_bc2) + A.eps);
         }
-        const float gi = fmaf(A.tv_gscale, gt, Gs[e]);
-        const long long gidx =
-            ((DIM == 3 ? (long long)g3[2] * A.s.sz : 0LL) + (long long)g3[1] * A.s.sy + g3[0]) * K + ch;
-        if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)gidx);
-        if (A.grad_out) A.grad_out[gidx] = gi;
-        const float mi = fmaf(A.b1, mvs[e], (1.0f - A.b1) * gi);
-        const float vi = fmaf(A.b2, mvs[S::NOWN * K + e], (1.0f - A.b2) * gi * gi);
-        A.m_out[gidx] = mi;
-        A.v_out[gidx] = vi;
-        A.p_out[gidx] = pv - A.lr * (mi * A.inv_bc1) / (sqrtf(vi * A.inv_bc2) + A.eps);
     }
 
     // ---- per-brick loss partials (fixed-order block reduction) ----
