@@ -224,16 +224,62 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// TMA bulk copies (cp.async.bulk) completing on an mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::
+            "r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ float fast_sqrt(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float fast_rcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Shared-memory plan of the fused brick kernel. Tile rows (fixed y, z) are
+// stored with a stride of TROWF floats and start SHF floats into the row, so
+// that a row's HBM source range can be fetched as one 16-byte-aligned TMA
+// bulk copy (the reference AoS layout puts vertex o-1 at an 8-byte offset
+// for K = 10).
 template <int DIM, int ORDER>
 struct BrickSmem {
     using S = BrickShape<DIM>;
     static constexpr int K = KOf<DIM, ORDER>::value;
-    static constexpr int tile = S::TVN * K;                         // floats
-    static constexpr int mv = 2 * S::NOWN * K;                      // m then v (prefetched)
-    static constexpr int pts = S::CH * S::REC + S::CH * 3;          // records + 3 int arrays
+    static constexpr int SHF = (4 - (K % 4)) % 4;
+    static constexpr int TROWF = ((S::T * K + SHF + 3) / 4) * 4;
+    static constexpr int TROWS = DIM == 3 ? S::T * S::T : S::T;
+    static constexpr int tile = TROWS * TROWF;                    // floats
+    static constexpr int mv = 2 * S::NOWN * K;                    // m then v (prefetched)
+    static constexpr int pts = S::CH * S::REC + S::CH * 2;        // sorted records + cell/rank
     static constexpr int gs = S::NOWN * K;
     static constexpr int uni = pts > gs ? pts : gs;
     static constexpr size_t bytes = sizeof(float) * (tile + mv + uni) + sizeof(int) * S::NCELL * 2;
+    // float offset of tile vertex (tx, ty, tz)
+    __device__ static constexpr int at(int tx, int ty, int tz) {
+        return (DIM == 3 ? (tz * S::T + ty) : ty) * TROWF + SHF + tx * K;
+    }
 };
 
 template <int DIM, int ORDER, bool EIK>
@@ -242,81 +288,126 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
     using L = BrickSmem<DIM, ORDER>;
     constexpr int K = KOf<DIM, ORDER>::value;
     constexpr int B = S::B, T = S::T, CE = S::CE, NT = S::NT, CH = S::CH;
-    constexpr int GR = (K % 2 == 0) ? 2 : 1;  // async-copy granule (floats)
+    constexpr int GR = (K % 2 == 0) ? 2 : 1;  // fallback async-copy granule (floats)
     if (A.st->error) return;
 
-    extern __shared__ __align__(16) float smem[];
-    float* tile = smem;                 // TVN*K   current parameters + halo
-    float* mvs = tile + L::tile;        // 2*NOWN*K  m, v of the owned vertices
-    float* uni = mvs + L::mv;           // point records | Gs
-    float* rec = uni;                   // CH*REC
-    int* cellof = reinterpret_cast<int*>(rec + CH * S::REC);
-    int* rankof = cellof + CH;
-    int* order = rankof + CH;
+    extern __shared__ __align__(128) float smem[];
+    float* tile = smem;                 // TROWS*TROWF  current parameters + halo
+    float* mvs = tile + L::tile;        // 2*NOWN*K     m, v of the owned vertices
+    float* uni = mvs + L::mv;           // sorted point records | Gs
+    float4* rec = reinterpret_cast<float4*>(uni);  // CH x 2 float4
     int* cnt = reinterpret_cast<int*>(uni + L::uni);
     int* start = cnt + S::NCELL;
     __shared__ int warp_tot[32];
-    __shared__ double red[3][NT / 32];
+    __shared__ double red[4][NT / 32];
+    __shared__ __align__(8) unsigned long long bars[2];
 
     const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = NT / 32;
     const int nbx = A.nb[0], nby = A.nb[1];
     const int b = blockIdx.x;
     const int bx = b % nbx;
     const int by = (b / nbx) % nby;
     const int bz = DIM == 3 ? b / (nbx * nby) : 0;
     const int o[3] = {bx * B, by * B, bz * B};
+    const float* __restrict__ p_in = A.p_in;
 
-    // ---- 1. async staging: parameter tile (group 0), then the owned m/v rows
-    //         (group 1), which stay in flight through the whole point phase ----
-    // Warp-per-row: a row (fixed y, z) is contiguous in HBM; the row's address
-    // and validity are computed once, lanes walk its granules.
-    const int lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = NT / 32;
-    {
-        constexpr int ROWG = T * K / GR;  // granules per tile row
-        constexpr int ROWS = DIM == 3 ? T * T : T;
-        for (int r = warp; r < ROWS; r += NW) {
-            const int ty = r % T, tz = r / T;
-            const int vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
-            const bool row_ok = vy >= 0 && vy < A.s.res[1] && (DIM == 2 || (vz >= 0 && vz < A.s.res[2]));
-            const long long base =
-                ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + (o[0] - 1)) * K;
-            float* dst = tile + r * T * K;
-            for (int gq = lane; gq < ROWG; gq += 32) {
-                const int q = gq * GR;
-                const int vx = o[0] - 1 + q / K;
-                const bool ok = row_ok && vx >= 0 && vx < A.s.res[0];
-                cp_async<GR>(dst + q, ok ? A.p_in + base + q : A.p_in, ok);
-            }
-        }
-        cp_async_commit();
-        constexpr int OROWG = B * K / GR;  // granules per owned row
-        constexpr int OROWS = DIM == 3 ? B * B : B;
-        for (int t = warp; t < 2 * OROWS; t += NW) {
-            const int which = t / OROWS, r = t - which * OROWS;
-            const int ly = r % B, lz = r / B;
-            const int vy = o[1] + ly, vz = o[2] + lz;
-            const bool row_ok = vy < A.s.res[1] && (DIM == 2 || vz < A.s.res[2]);
-            const long long base = ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0]) * K;
-            const float* src = which ? A.v_in : A.m_in;
-            float* dst = mvs + which * S::NOWN * K + r * B * K;
-            for (int gq = lane; gq < OROWG; gq += 32) {
-                const int q = gq * GR;
-                const bool ok = row_ok && o[0] + q / K < A.s.res[0];
-                cp_async<GR>(dst + q, ok ? src + base + q : src, ok);
-            }
-        }
-        cp_async_commit();
-        cp_async_wait<1>();  // tile landed (m/v may still be in flight)
+    // ---- 1. staging: one TMA bulk copy per HBM row (tile rows -> bars[0],
+    //         owned m/v rows -> bars[1], which stay in flight through the
+    //         point phase); rows that are not 16-byte aligned or would read
+    //         outside the array fall back to cp.async granules ----
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        mbar_fence_init();
     }
     __syncthreads();
+    const long long nc_bytes = (long long)A.s.res[0] * A.s.res[1] * (DIM == 3 ? A.s.res[2] : 1) * K * 4;
+    if (warp == 0) {
+        // tile rows (vertices o-1 .. o+B in x) -> bars[0]
+        constexpr unsigned TBYTES = ((L::SHF * 4 + T * K * 4 + 15) / 16) * 16;
+        unsigned tx_bytes = 0;
+        for (int r = lane; r < L::TROWS; r += 32) {
+            const int ty = DIM == 3 ? r % T : r, tz = DIM == 3 ? r / T : 0;
+            const int vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
+            if (vy < 0 || vy >= A.s.res[1] || (DIM == 3 && (vz < 0 || vz >= A.s.res[2]))) continue;
+            const long long first = ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0] - 1) * K * 4;
+            const long long src = first - L::SHF * 4;
+            if ((src & 15) == 0 && src >= 0 && src + TBYTES <= nc_bytes) tx_bytes += TBYTES;
+        }
+        constexpr unsigned OBYTES = B * K * 4;
+        unsigned mv_bytes = 0;
+        constexpr int OROWS = DIM == 3 ? B * B : B;
+        for (int r = lane; r < OROWS; r += 32) {
+            const int ly = r % B, lz = DIM == 3 ? r / B : 0;
+            const int vy = o[1] + ly, vz = o[2] + lz;
+            if (vy >= A.s.res[1] || (DIM == 3 && vz >= A.s.res[2])) continue;
+            const long long src = ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0]) * K * 4;
+            if ((src & 15) == 0 && o[0] + B <= A.s.res[0] && (OBYTES & 15) == 0) mv_bytes += 2 * OBYTES;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            tx_bytes += __shfl_xor_sync(0xffffffffu, tx_bytes, off);
+            mv_bytes += __shfl_xor_sync(0xffffffffu, mv_bytes, off);
+        }
+        if (lane == 0) {
+            mbar_expect_tx(&bars[0], tx_bytes);
+            mbar_expect_tx(&bars[1], mv_bytes);
+        }
+        __syncwarp();
+        for (int r = lane; r < L::TROWS; r += 32) {
+            const int ty = DIM == 3 ? r % T : r, tz = DIM == 3 ? r / T : 0;
+            const int vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
+            if (vy < 0 || vy >= A.s.res[1] || (DIM == 3 && (vz < 0 || vz >= A.s.res[2]))) continue;
+            const long long firstv = (DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0] - 1;
+            const long long src = firstv * K * 4 - L::SHF * 4;
+            float* dst = tile + r * L::TROWF;
+            if ((src & 15) == 0 && src >= 0 && src + TBYTES <= nc_bytes) {
+                bulk_g2s(dst, reinterpret_cast<const char*>(p_in) + src, TBYTES, &bars[0]);
+            } else {
+                for (int q = 0; q < T * K; q += GR) {
+                    const int vx = o[0] - 1 + q / K;
+                    const bool ok = vx >= 0 && vx < A.s.res[0];
+                    cp_async<GR>(dst + L::SHF + q, ok ? p_in + firstv * K + q : p_in, ok);
+                }
+            }
+        }
+        for (int r = lane; r < OROWS; r += 32) {
+            const int ly = r % B, lz = DIM == 3 ? r / B : 0;
+            const int vy = o[1] + ly, vz = o[2] + lz;
+            if (vy >= A.s.res[1] || (DIM == 3 && vz >= A.s.res[2])) continue;
+            const long long v0 = (DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0];
+            const long long src = v0 * K * 4;
+            float* dm = mvs + r * B * K;
+            float* dv = mvs + S::NOWN * K + r * B * K;
+            if ((src & 15) == 0 && o[0] + B <= A.s.res[0] && (OBYTES & 15) == 0) {
+                bulk_g2s(dm, reinterpret_cast<const char*>(A.m_in) + src, OBYTES, &bars[1]);
+                bulk_g2s(dv, reinterpret_cast<const char*>(A.v_in) + src, OBYTES, &bars[1]);
+            } else {
+                for (int q = 0; q < B * K; q += GR) {
+                    const bool ok = o[0] + q / K < A.s.res[0];
+                    cp_async<GR>(dm + q, ok ? A.m_in + v0 * K + q : A.m_in, ok);
+                    cp_async<GR>(dv + q, ok ? A.v_in + v0 * K + q : A.v_in, ok);
+                }
+            }
+        }
+        cp_async_commit();
+    }
+    mbar_wait(&bars[0], 0);
+    if (warp == 0) cp_async_wait<0>();  // fallback rows (rare: grid-edge bricks)
+    __syncthreads();
 
-    // This thread's owned vertex.
+    // This thread's owned vertex (phase 2b accumulates its gradient in registers).
     const int lv[3] = {tid % B, (tid / B) % B, DIM == 3 ? tid / (B * B) : 0};
     bool own_ok = true;
 #pragma unroll
     for (int a = 0; a < DIM; ++a) own_ok &= (o[a] + lv[a]) < A.s.res[a];
-
+    // Incident cell of corner c: ext-cell coords lv + 1 - bit(c); ec0 is corner 0's.
+    const int ec0 = DIM == 3 ? ((lv[2] + 1) * CE + lv[1] + 1) * CE + lv[0] + 1 : (lv[1] + 1) * CE + lv[0] + 1;
+    auto ecv = [&](int c) {
+        return ec0 - (c & 1) - ((c >> 1) & 1) * CE - (DIM == 3 ? ((c >> 2) & 1) * CE * CE : 0);
+    };
     float G[K];
 #pragma unroll
     for (int q = 0; q < K; ++q) G[q] = 0.0f;
@@ -328,6 +419,9 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
         const int m = min(CH, p1 - base);
         for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
         __syncthreads();
+        // 2a. forward from the tile, fp64 loss chain, cell rank
+        float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+        int ec = 0, rank = 0;
         if (tid < m) {
             const float4 q = A.binned[base + tid];
             const float pf[3] = {q.x, q.y, q.z};
@@ -344,15 +438,15 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
                 tc[a] = c - (o[a] - 1);  // in [0, B]
                 home &= tc[a] >= 1;
             }
-            const int tb = DIM == 3 ? (tc[2] * T + tc[1]) * T + tc[0] : tc[1] * T + tc[0];
             float f = 0.0f, fg[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
 #pragma unroll
             for (int c = 0; c < (1 << DIM); ++c) {
-                const int tv = tb + (c & 1) + ((c >> 1) & 1) * T + (DIM == 3 ? ((c >> 2) & 1) * T * T : 0);
                 float cb[K];
-                load_block<K, false>(tile + tv * K, cb);
+                load_block<K, false>(tile + L::at(tc[0] + (c & 1), tc[1] + ((c >> 1) & 1),
+                                                  DIM == 3 ? tc[2] + ((c >> 2) & 1) : 0),
+                                     cb);
                 blend_corner<DIM, ORDER, EIK>(cb, corner_geom<DIM>(A.s, ax, c), f, fg);
             }
             double recon, eik;
@@ -363,91 +457,120 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
                 eik_sum += eik;
                 home_pts += 1.0;
             }
-            const int ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
-            rankof[tid] = atomicAdd(&cnt[ec], 1);
-            cellof[tid] = ec;
-            float* r = rec + tid * S::REC;
-            r[0] = lf[0];
-            r[1] = lf[1];
-            r[2] = lf[2];
-            r[3] = u;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) r[4 + a] = a < DIM ? gv[a] : 0.0f;
+            ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
+            rank = atomicAdd(&cnt[ec], 1);
+            r0 = make_float4(lf[0], lf[1], lf[2], u);
+            r1 = make_float4(gv[0], DIM > 1 ? gv[1] : 0.f, DIM > 2 ? gv[DIM - 1] : 0.f, 0.f);
         }
         __syncthreads();
         block_excl_scan<S::NCELL, NT>(cnt, start, warp_tot);
         __syncthreads();
-        if (tid < m) order[start[cellof[tid]] + rankof[tid]] = tid;
+        if (tid < m) {  // records land in cell order
+            const int slot = start[ec] + rank;
+            rec[2 * slot] = r0;
+            rec[2 * slot + 1] = r1;
+        }
         __syncthreads();
+        // 2b. this vertex gathers its 2^D incident cells' points (flattened
+        //     loop: a thread's cost is its own total, not the per-corner max)
         if (own_ok) {
-#pragma unroll
-            for (int c = 0; c < (1 << DIM); ++c) {
-                int ec = 0;
-                {
-                    int e3[3] = {0, 0, 0};
-#pragma unroll
-                    for (int a = 0; a < DIM; ++a) e3[a] = lv[a] + 1 - ((c >> a) & 1);
-                    ec = DIM == 3 ? (e3[2] * CE + e3[1]) * CE + e3[0] : e3[1] * CE + e3[0];
+            int c = 0;
+            int j = start[ec0], jend = j + cnt[ec0];
+            while (true) {
+                while (j >= jend) {
+                    if (++c == (1 << DIM)) break;
+                    const int e = ecv(c);
+                    j = start[e];
+                    jend = j + cnt[e];
                 }
-                const int j0 = start[ec], j1 = j0 + cnt[ec];
-                for (int j = j0; j < j1; ++j) {
-                    const float* r = rec + order[j] * S::REC;
-                    AxisF ax[DIM];
+                if (c == (1 << DIM)) break;
+                const float4 a0 = rec[2 * j];
+                const float l3[3] = {a0.x, a0.y, a0.z};
+                Corner<DIM> cg;
+                float sv[DIM];
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    const bool bit = (c >> a) & 1;
+                    const float l = l3[a];
+                    sv[a] = bit ? l : 1.0f - l;
+                    cg.d[a] = (bit ? l - 1.0f : l) * A.s.hf[a];
+                }
+                cg.w = sv[0];
+#pragma unroll
+                for (int a = 1; a < DIM; ++a) cg.w *= sv[a];
+                if constexpr (EIK) {
 #pragma unroll
                     for (int a = 0; a < DIM; ++a) {
-                        const float l = r[a];
-                        ax[a].s0 = 1.0f - l;
-                        ax[a].s1 = l;
-                        ax[a].d0 = l * A.s.hf[a];
-                        ax[a].d1 = (l - 1.0f) * A.s.hf[a];
-                    }
-                    float gv[DIM];
+                        float other = 1.0f;
 #pragma unroll
-                    for (int a = 0; a < DIM; ++a) gv[a] = EIK ? r[4 + a] : 0.0f;
-                    corner_grad<DIM, ORDER, K>(corner_geom<DIM>(A.s, ax, c), r[3], gv, G);
+                        for (int bb = 0; bb < DIM; ++bb)
+                            if (bb != a) other *= sv[bb];
+                        cg.dw[a] = (((c >> a) & 1) ? A.s.inv_hf[a] : -A.s.inv_hf[a]) * other;
+                    }
+                    const float4 a1 = rec[2 * j + 1];
+                    const float gv[3] = {a1.x, a1.y, a1.z};
+                    float gvd[DIM];
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) gvd[a] = gv[a];
+                    corner_grad<DIM, ORDER, K>(cg, a0.w, gvd, G);
+                } else {
+                    float gvd[DIM];
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) {
+                        gvd[a] = 0.0f;
+                        cg.dw[a] = 0.0f;
+                    }
+                    corner_grad<DIM, ORDER, K>(cg, a0.w, gvd, G);
                 }
+                ++j;
             }
         }
         __syncthreads();
     }
 
-    // ---- 3. TV + Adam over the owned coefficients ----
+    // ---- 3. TV + Adam over the owned coefficients (warp per row) ----
     float* Gs = uni;
 #pragma unroll
     for (int q = 0; q < K; ++q) Gs[tid * K + q] = G[q];
-    cp_async_wait<0>();  // m/v rows landed
+    mbar_wait(&bars[1], 0);  // m/v rows landed (bulk); fallback granules were waited above
     __syncthreads();
     double tv_sum = 0.0;
     const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
+    float* __restrict__ p_out = A.p_out;
+    float* __restrict__ m_out = A.m_out;
+    float* __restrict__ v_out = A.v_out;
     constexpr int OROWS = DIM == 3 ? B * B : B;
     constexpr int ROWF = B * K;  // floats per owned row
+    constexpr int TY = L::TROWF, TZ = DIM == 3 ? T * L::TROWF : 0;  // tile strides
     for (int r = warp; r < OROWS; r += NW) {
-        const int ly = r % B, lz = r / B;
+        const int ly = r % B, lz = DIM == 3 ? r / B : 0;
         const int gy = o[1] + ly, gz = o[2] + lz;
         if (gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
         const long long rbase = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K;
-        const int trow = DIM == 3 ? ((lz + 1) * T + (ly + 1)) * T + 1 : (ly + 1) * T + 1;  // tile vertex of lx = 0
+        const float* trow = tile + L::at(1, ly + 1, DIM == 3 ? lz + 1 : 0);
         const bool ylo = gy >= 1, yhi = gy + 1 < A.s.res[1];
         const bool zlo = DIM == 3 && gz >= 1, zhi = DIM == 3 && gz + 1 < A.s.res[2];
         for (int j = lane; j < ROWF; j += 32) {
-            const int lx = j / K, ch = j - lx * K;
+            const int lx = j / K;
             const int gx = o[0] + lx;
             if (gx >= A.s.res[0]) continue;
             const int e = r * ROWF + j;
-            const float* tp = tile + (trow + lx) * K + ch;
+            const float* tp = trow + j;
             const float pv = *tp;
             float gt = 0.0f;
             if (A.want_tv) {
-                // TV pairs (v, v+e_a) owned here add to the sum; both pair
-                // ends' terms add to this vertex's gradient (sdf_loss.cpp:155-257).
-                if (gx + 1 < A.s.res[0]) { const float d = tp[K] - pv; tv_sum += (double)d * (double)d; gt -= d; }
+                // pairs (v, v+e_a) owned here feed the TV sum; both ends' terms
+                // feed this vertex's gradient (sdf_loss.cpp:155-257)
+                float sq = 0.0f;
+                if (gx + 1 < A.s.res[0]) { const float d = tp[K] - pv; sq = fmaf(d, d, sq); gt -= d; }
                 if (gx >= 1) gt += pv - tp[-K];
-                if (yhi) { const float d = tp[T * K] - pv; tv_sum += (double)d * (double)d; gt -= d; }
-                if (ylo) gt += pv - tp[-T * K];
+                if (yhi) { const float d = tp[TY] - pv; sq = fmaf(d, d, sq); gt -= d; }
+                if (ylo) gt += pv - tp[-TY];
                 if (DIM == 3) {
-                    if (zhi) { const float d = tp[T * T * K] - pv; tv_sum += (double)d * (double)d; gt -= d; }
-                    if (zlo) gt += pv - tp[-T * T * K];
+                    if (zhi) { const float d = tp[TZ] - pv; sq = fmaf(d, d, sq); gt -= d; }
+                    if (zlo) gt += pv - tp[-TZ];
                 }
+                tv_sum += (double)sq;
             }
             const float gi = fmaf(A.tv_gscale, gt, Gs[e]);
             const long long gidx = rbase + j;
@@ -455,9 +578,9 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
             if (A.grad_out) A.grad_out[gidx] = gi;
             const float mi = fmaf(A.b1, mvs[e], c1 * gi);
             const float vi = fmaf(A.b2, mvs[S::NOWN * K + e], c2 * gi * gi);
-            A.m_out[gidx] = mi;
-            A.v_out[gidx] = vi;
-            A.p_out[gidx] = pv - lr_bc1 * mi * __frcp_rn(sqrtf(vi * A.inv_bc2) + A.eps);
+            m_out[gidx] = mi;
+            v_out[gidx] = vi;
+            p_out[gidx] = pv - lr_bc1 * mi * fast_rcp(fast_sqrt(vi * A.inv_bc2) + A.eps);
         }
     }
 
@@ -466,26 +589,17 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
     eik_sum = warp_sum_d(eik_sum);
     tv_sum = warp_sum_d(tv_sum);
     home_pts = warp_sum_d(home_pts);
-    __shared__ double hp[NT / 32];
-    if ((tid & 31) == 0) {
-        red[0][tid >> 5] = recon_sum;
-        red[1][tid >> 5] = eik_sum;
-        red[2][tid >> 5] = tv_sum;
-        hp[tid >> 5] = home_pts;
+    if (lane == 0) {
+        red[0][warp] = recon_sum;
+        red[1][warp] = eik_sum;
+        red[2][warp] = tv_sum;
+        red[3][warp] = home_pts;
     }
     __syncthreads();
-    if (tid == 0) {
-        double a = 0.0, c = 0.0, d = 0.0, h = 0.0;
-        for (int k = 0; k < NT / 32; ++k) {
-            a += red[0][k];
-            c += red[1][k];
-            d += red[2][k];
-            h += hp[k];
-        }
-        A.partials[4 * b] = a;
-        A.partials[4 * b + 1] = c;
-        A.partials[4 * b + 2] = d;
-        A.partials[4 * b + 3] = h;
+    if (tid < 4) {
+        double acc = 0.0;
+        for (int k = 0; k < NW; ++k) acc += red[tid][k];
+        A.partials[4 * b + tid] = acc;
     }
 }
 
