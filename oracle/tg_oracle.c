@@ -393,7 +393,20 @@ static void point_terms(const tgo_spec* s, const double* coeffs, const double* s
             }
         }
         if (grad) tgo_backprop(s, p, upstream, uvec, grad);
-        if (mass) tgo_backprop_mass(s, p, upstream, uvec, mass);
+        if (mass) {
+            /* The eikonal upstream scales with (|grad f| - 1), which an fp32
+             * forward evaluates to ~1e-7 absolute: bound its sensitivity by
+             * using (|r| + 0.1) for the mass (0.1 * mass_rel covers that). */
+            double umass[3] = {0.0, 0.0, 0.0};
+            if (want_eik) {
+                const double nrm = sqrt(sg[0] * sg[0] + sg[1] * sg[1] + sg[2] * sg[2]);
+                if (nrm > 0.0) {
+                    const double sc = eik_scale * inv_n * 2.0 * (fabs(nrm - 1.0) + 0.1) / nrm;
+                    for (int a = 0; a < 3; ++a) umass[a] = fabs(sc * sg[a]);
+                }
+            }
+            tgo_backprop_mass(s, p, upstream, umass, mass);
+        }
     }
     *recon_out = recon;
     *eik_out = eik;

@@ -222,7 +222,7 @@ def test_async_trajectory_matches_sync():
     g2.sync()
     # the fused step bins points with atomics, so runs agree to rounding, not bitwise
     assert_close(g2.trace(len(z["train_batches"])), np.array(sync_terms), 1e-6, floor=1e-30, what="async trace")
-    assert_close(g2.coeffs, g1.coeffs, 1e-6, floor=1e-2, what="async coeffs")
+    assert_close(g2.coeffs, g1.coeffs, 1e-5, floor=1e-2, what="async coeffs")
 
 
 def test_nonfinite_loss_aborts_and_keeps_params():
