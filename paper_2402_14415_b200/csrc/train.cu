@@ -259,11 +259,11 @@ __device__ __forceinline__ float fast_rcp(float x) {
     return r;
 }
 
-// Shared-memory plan of the fused brick kernel (persistent, double-buffered).
+// Shared-memory plan of the fused brick kernel (one brick per CTA, 2 CTAs/SM).
 // Tile rows (fixed y, z) are stored with a stride of TROWF floats and start
 // SHF floats into the row, so that a row's HBM range is one 16-byte-aligned
 // TMA bulk copy (the reference AoS layout puts vertex o-1 at an 8-byte offset
-// for K = 10). Per buffer: tile + m/v rows of the owned vertices.
+// for K = 10).
 template <int DIM, int ORDER>
 struct BrickSmem {
     using S = BrickShape<DIM>;
@@ -273,35 +273,32 @@ struct BrickSmem {
     static constexpr int TROWS = DIM == 3 ? S::T * S::T : S::T;
     static constexpr int tile = TROWS * TROWF;                    // floats
     static constexpr int mv = 2 * S::NOWN * K;                    // m then v
-    static constexpr int buf = tile + mv;                         // one pipeline stage
     static constexpr int REC = ((3 * DIM + 1) + 1) / 2 * 2;       // s0[D] s1[D] u g[D] (even)
     static constexpr int pts = S::CH * REC;                       // cell-ordered records
     static constexpr int gs = S::NOWN * K;
     static constexpr int uni = pts > gs ? pts : gs;
-    static constexpr size_t bytes =
-        sizeof(float) * (2 * buf + uni) + sizeof(int) * (S::NCELL * 2 + S::NT + 64 * 2);
+    static constexpr size_t bytes = sizeof(float) * (tile + mv + uni) + sizeof(int) * (S::NCELL * 2 + S::NT + 64 * 2);
     // float offset of tile vertex (tx, ty, tz)
     __device__ static constexpr int at(int tx, int ty, int tz) {
         return (DIM == 3 ? (tz * S::T + ty) : ty) * TROWF + SHF + tx * K;
     }
 };
 
-// Issue the HBM->smem copies of brick `b` into one pipeline stage (warp 0).
+// Issue the HBM->smem copies of brick `b` (warp 0): one TMA bulk copy per
+// HBM row (tile rows -> bar_tile, owned m/v rows -> bar_mv); rows that are not
+// 16-byte aligned or would read outside the array fall back to cp.async.
 template <int DIM, int ORDER>
-__device__ __forceinline__ void stage_brick(const StepArgs& A, int b, float* tile, float* mvs,
+__device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, float* tile, float* mvs,
                                             unsigned long long* bar_tile, unsigned long long* bar_mv, int lane) {
     using S = BrickShape<DIM>;
     using L = BrickSmem<DIM, ORDER>;
     constexpr int K = L::K, B = S::B, T = S::T;
     constexpr int GR = (K % 2 == 0) ? 2 : 1;
-    const int nbx = A.nb[0], nby = A.nb[1];
-    const int o[3] = {(b % nbx) * B, ((b / nbx) % nby) * B, DIM == 3 ? (b / (nbx * nby)) * B : 0};
     const long long nc_bytes = (long long)A.s.res[0] * A.s.res[1] * (DIM == 3 ? A.s.res[2] : 1) * K * 4;
     constexpr unsigned TBYTES = ((L::SHF * 4 + T * K * 4 + 15) / 16) * 16;
     constexpr unsigned OBYTES = B * K * 4;
     constexpr int OROWS = DIM == 3 ? B * B : B;
     const bool mv_bulk_ok = (OBYTES % 16) == 0 && o[0] + B <= A.s.res[0];
-    // bytes the bulk copies will deliver (fallback rows use cp.async instead)
     unsigned tx_bytes = 0, mv_bytes = 0;
     for (int r = lane; r < L::TROWS; r += 32) {
         const int ty = DIM == 3 ? r % T : r, tz = DIM == 3 ? r / T : 0;
@@ -368,10 +365,8 @@ __device__ __forceinline__ void stage_brick(const StepArgs& A, int b, float* til
     cp_async_commit();
 }
 
-// Persistent: gridDim.x CTAs (one per SM) pull bricks from a work counter and
-// prefetch brick i+1 (TMA into the other stage) while computing brick i.
 template <int DIM, int ORDER, bool EIK>
-__global__ void __launch_bounds__(BrickShape<DIM>::NT, 1) k_brick_step(StepArgs A) {
+__global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs A) {
     using S = BrickShape<DIM>;
     using L = BrickSmem<DIM, ORDER>;
     constexpr int K = KOf<DIM, ORDER>::value;
@@ -380,8 +375,9 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 1) k_brick_step(StepArgs 
     if (A.st->error) return;
 
     extern __shared__ __align__(128) float smem[];
-    float* stage0 = smem;                         // 2 x (tile | m | v)
-    float* uni = smem + 2 * L::buf;               // cell-ordered records | Gs
+    float* tile = smem;                           // current parameters + halo
+    float* mvs = tile + L::tile;                  // m, v of the owned vertices
+    float* uni = mvs + L::mv;                     // cell-ordered records | Gs
     int* cnt = reinterpret_cast<int*>(uni + L::uni);
     int* start = cnt + S::NCELL;
     int* perm = start + S::NCELL;                 // thread -> owned vertex (load balance)
@@ -389,278 +385,282 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 1) k_brick_step(StepArgs 
     int* bstart = bhist + 64;
     __shared__ int warp_tot[32];
     __shared__ double red[4][NT / 32];
-    __shared__ __align__(8) unsigned long long bars[2][2];  // [stage][tile, mv]
-    __shared__ int s_brick[2];
+    __shared__ __align__(8) unsigned long long bars[2];  // tile, mv
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     constexpr int NW = NT / 32;
     const int nbx = A.nb[0], nby = A.nb[1];
-    const int NB = A.nb[0] * A.nb[1] * A.nb[2];
+    const int b = blockIdx.x;
+    const int o[3] = {(b % nbx) * B, ((b / nbx) % nby) * B, DIM == 3 ? (b / (nbx * nby)) * B : 0};
 
     if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&bars[i][0], 1);
-            mbar_init(&bars[i][1], 1);
-        }
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
         mbar_fence_init();
-        s_brick[0] = atomicAdd(A.work, 1);
     }
     __syncthreads();
-    int b = s_brick[0];
-    if (b < NB && warp == 0) stage_brick<DIM, ORDER>(A, b, stage0, stage0 + L::tile, &bars[0][0], &bars[0][1], lane);
+    if (warp == 0) {
+        stage_brick<DIM, ORDER>(A, o, tile, mvs, &bars[0], &bars[1], lane);
+        mbar_wait(&bars[0], 0);  // one warp waits; the others park at the barrier
+        cp_async_wait<0>();      // fallback rows (rare: grid-edge bricks)
+    }
+    __syncthreads();
 
-    double recon_sum = 0.0, eik_sum = 0.0, tv_sum = 0.0, home_pts = 0.0;
-    const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
-    float* __restrict__ p_out = A.p_out;
-    float* __restrict__ m_out = A.m_out;
-    float* __restrict__ v_out = A.v_out;
+    float G[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) G[q] = 0.0f;
+    double recon_sum = 0.0, eik_sum = 0.0, home_pts = 0.0;
+    int myv = tid;  // owned vertex of this thread; set per brick by the workload sort
 
-    for (int it = 0; b < NB; ++it) {
-        const int sidx = it & 1;
-        const unsigned phase = (it >> 1) & 1;
-        float* tile = stage0 + sidx * L::buf;
-        float* mvs = tile + L::tile;
-        // claim + prefetch the next brick into the other stage
-        if (tid == 0) s_brick[(it + 1) & 1] = atomicAdd(A.work, 1);
+    const int p0 = A.off[b], p1 = A.off[b + 1];
+    for (int base = p0; base < p1; base += CH) {
+        const int m = min(CH, p1 - base);
+        for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
+        if (base == p0 && tid < 64) bhist[tid] = 0;
         __syncthreads();
-        const int bnext = s_brick[(it + 1) & 1];
-        if (warp == 0) {
-            if (bnext < NB) {
-                float* t2 = stage0 + (sidx ^ 1) * L::buf;
-                stage_brick<DIM, ORDER>(A, bnext, t2, t2 + L::tile, &bars[sidx ^ 1][0], &bars[sidx ^ 1][1], lane);
-            } else {
-                cp_async_commit();  // empty group keeps wait_group<1> aligned
+        // 2a. forward from the tile, fp64 loss chain, cell rank
+        float rv[REC];
+        int ec = 0, rank = 0;
+        if (tid < m) {
+            const float4 q = A.binned[base + tid];
+            const float pf[3] = {q.x, q.y, q.z};
+            AxisF ax[DIM];
+            int tc[3] = {0, 0, 0};
+            bool home = true;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                double local;
+                const int c = locate_axis(A.s, a, (double)pf[a], local);
+                ax[a] = axis_factors(A.s, a, local);
+                tc[a] = c - (o[a] - 1);  // in [0, B]
+                home &= tc[a] >= 1;
             }
+            float f = 0.0f, fg[DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                float cb[K];
+                load_block<K, false>(tile + L::at(tc[0] + (c & 1), tc[1] + ((c >> 1) & 1),
+                                                  DIM == 3 ? tc[2] + ((c >> 2) & 1) : 0),
+                                     cb);
+                blend_corner<DIM, ORDER, EIK>(cb, corner_geom<DIM>(A.s, ax, c), f, fg);
+            }
+            double recon, eik;
+            float u, gv[DIM];
+            point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
+            if (home) {
+                recon_sum += recon;
+                eik_sum += eik;
+                home_pts += 1.0;
+            }
+            ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
+            rank = atomicAdd(&cnt[ec], 1);
+            // s0/s1 rounded from fp64 (1 - l must not be formed from a rounded l)
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                rv[a] = ax[a].s0;
+                rv[DIM + a] = ax[a].s1;
+                rv[2 * DIM + 1 + a] = gv[a];
+            }
+            rv[2 * DIM] = u;
+#pragma unroll
+            for (int k2 = 3 * DIM + 1; k2 < REC; ++k2) rv[k2] = 0.0f;
         }
-        const int o[3] = {(b % nbx) * B, ((b / nbx) % nby) * B, DIM == 3 ? (b / (nbx * nby)) * B : 0};
-
-        mbar_wait(&bars[sidx][0], phase);
-        if (warp == 0) cp_async_wait<1>();  // fallback rows of this stage (rare: grid-edge bricks)
         __syncthreads();
-
-        // thread -> owned vertex; rebalanced after the first chunk
-        int myv = tid;
-        float G[K];
+        block_excl_scan<S::NCELL, NT>(cnt, start, warp_tot);
+        __syncthreads();
+        if (tid < m) {  // records land in cell order
+            float2* dst = reinterpret_cast<float2*>(uni + (start[ec] + rank) * REC);
 #pragma unroll
-        for (int q = 0; q < K; ++q) G[q] = 0.0f;
-
-        const int p0 = A.off[b], p1 = A.off[b + 1];
-        for (int base = p0; base < p1; base += CH) {
-            const int m = min(CH, p1 - base);
-            for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
+            for (int k2 = 0; k2 < REC / 2; ++k2) dst[k2] = make_float2(rv[2 * k2], rv[2 * k2 + 1]);
+        }
+        if (base == p0) {
+            // Load balance: sort the owned vertices by their (first-chunk)
+            // workload into 64 buckets so a warp's lanes carry similar loads;
+            // the mapping then holds for the brick (points are in random order).
+            const int v = tid;
+            const int l3[3] = {v % B, (v / B) % B, DIM == 3 ? v / (B * B) : 0};
+            const int e0 = DIM == 3 ? ((l3[2] + 1) * CE + l3[1] + 1) * CE + l3[0] + 1 : (l3[1] + 1) * CE + l3[0] + 1;
+            int wl = 0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                wl += cnt[e0 - (c & 1) - ((c >> 1) & 1) * CE - (DIM == 3 ? ((c >> 2) & 1) * CE * CE : 0)];
+            const int bk = 63 - min(wl, 63);  // heavy first
+            const int r2 = atomicAdd(&bhist[bk], 1);
             __syncthreads();
-            // 2a. forward from the tile, fp64 loss chain, cell rank
-            float rv[REC];
-            int ec = 0, rank = 0;
-            if (tid < m) {
-                const float4 q = A.binned[base + tid];
-                const float pf[3] = {q.x, q.y, q.z};
-                AxisF ax[DIM];
-                int tc[3] = {0, 0, 0};
-                bool home = true;
+            if (warp == 0) {
+                const int h0 = bhist[lane], h1 = bhist[lane + 32];
+                int x0 = h0, x1 = h1;
 #pragma unroll
-                for (int a = 0; a < DIM; ++a) {
-                    double local;
-                    const int c = locate_axis(A.s, a, (double)pf[a], local);
-                    ax[a] = axis_factors(A.s, a, local);
-                    tc[a] = c - (o[a] - 1);  // in [0, B]
-                    home &= tc[a] >= 1;
-                }
-                float f = 0.0f, fg[DIM];
-#pragma unroll
-                for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    float cb[K];
-                    load_block<K, false>(tile + L::at(tc[0] + (c & 1), tc[1] + ((c >> 1) & 1),
-                                                      DIM == 3 ? tc[2] + ((c >> 2) & 1) : 0),
-                                         cb);
-                    blend_corner<DIM, ORDER, EIK>(cb, corner_geom<DIM>(A.s, ax, c), f, fg);
-                }
-                double recon, eik;
-                float u, gv[DIM];
-                point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
-                if (home) {
-                    recon_sum += recon;
-                    eik_sum += eik;
-                    home_pts += 1.0;
-                }
-                ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
-                rank = atomicAdd(&cnt[ec], 1);
-                // s0/s1 rounded from fp64 (1 - l must not be formed from a rounded l)
-#pragma unroll
-                for (int a = 0; a < DIM; ++a) {
-                    rv[a] = ax[a].s0;
-                    rv[DIM + a] = ax[a].s1;
-                    rv[2 * DIM + 1 + a] = gv[a];
-                }
-                rv[2 * DIM] = u;
-#pragma unroll
-                for (int k2 = 3 * DIM + 1; k2 < REC; ++k2) rv[k2] = 0.0f;
-            }
-            __syncthreads();
-            block_excl_scan<S::NCELL, NT>(cnt, start, warp_tot);
-            __syncthreads();
-            if (tid < m) {  // records land in cell order
-                float2* dst = reinterpret_cast<float2*>(uni + (start[ec] + rank) * REC);
-#pragma unroll
-                for (int k2 = 0; k2 < REC / 2; ++k2) dst[k2] = make_float2(rv[2 * k2], rv[2 * k2 + 1]);
-            }
-            if (base == p0 && p1 - p0 > CH) {
-                // Load balance for multi-chunk bricks: sort the owned vertices
-                // by their first-chunk workload (a representative sample) into
-                // 64 buckets, so a warp's lanes carry similar loads.
-                if (tid < 64) bhist[tid] = 0;
-                __syncthreads();
-                const int v = tid;
-                const int l3[3] = {v % B, (v / B) % B, DIM == 3 ? v / (B * B) : 0};
-                const int e0 = DIM == 3 ? ((l3[2] + 1) * CE + l3[1] + 1) * CE + l3[0] + 1 : (l3[1] + 1) * CE + l3[0] + 1;
-                int wl = 0;
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-                    wl += cnt[e0 - (c & 1) - ((c >> 1) & 1) * CE - (DIM == 3 ? ((c >> 2) & 1) * CE * CE : 0)];
-                const int bk = 63 - min(wl, 63);  // heavy first
-                const int r2 = atomicAdd(&bhist[bk], 1);
-                __syncthreads();
-                if (warp == 0) {
-                    int h0 = bhist[lane], h1 = bhist[lane + 32];
-                    int x0 = h0, x1 = h1;
-#pragma unroll
-                    for (int off = 1; off < 32; off <<= 1) {
-                        const int y0 = __shfl_up_sync(0xffffffffu, x0, off);
-                        const int y1 = __shfl_up_sync(0xffffffffu, x1, off);
-                        if (lane >= off) { x0 += y0; x1 += y1; }
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int y0 = __shfl_up_sync(0xffffffffu, x0, off);
+                    const int y1 = __shfl_up_sync(0xffffffffu, x1, off);
+                    if (lane >= off) {
+                        x0 += y0;
+                        x1 += y1;
                     }
-                    const int tot0 = __shfl_sync(0xffffffffu, x0, 31);
-                    bstart[lane] = x0 - h0;
-                    bstart[lane + 32] = tot0 + x1 - h1;
                 }
-                __syncthreads();
-                perm[bstart[bk] + r2] = v;
-                __syncthreads();
-                myv = perm[tid];
-            } else {
-                __syncthreads();
+                const int tot0 = __shfl_sync(0xffffffffu, x0, 31);
+                bstart[lane] = x0 - h0;
+                bstart[lane + 32] = tot0 + x1 - h1;
             }
-            // 2b. this thread's vertex gathers its 2^D incident cells' points
-            {
-                const int l3[3] = {myv % B, (myv / B) % B, DIM == 3 ? myv / (B * B) : 0};
-                bool own_ok = true;
+            __syncthreads();
+            perm[bstart[bk] + r2] = v;
+            __syncthreads();
+            myv = perm[tid];
+        } else {
+            __syncthreads();
+        }
+        // 2b. this thread's vertex gathers the points of its 2^D incident
+        //     cells, as one flattened loop over (corner, point)
+        {
+            const int l3[3] = {myv % B, (myv / B) % B, DIM == 3 ? myv / (B * B) : 0};
+            bool own_ok = true;
 #pragma unroll
-                for (int a = 0; a < DIM; ++a) own_ok &= (o[a] + l3[a]) < A.s.res[a];
-                const int e0 = DIM == 3 ? ((l3[2] + 1) * CE + l3[1] + 1) * CE + l3[0] + 1 : (l3[1] + 1) * CE + l3[0] + 1;
-                if (own_ok) {
-#pragma unroll 1
-                    for (int c = 0; c < NC; ++c) {
+            for (int a = 0; a < DIM; ++a) own_ok &= (o[a] + l3[a]) < A.s.res[a];
+            const int e0 = DIM == 3 ? ((l3[2] + 1) * CE + l3[1] + 1) * CE + l3[0] + 1 : (l3[1] + 1) * CE + l3[0] + 1;
+            int c = -1, j = 0, jend = 0;
+            int total = 0;
+            if (own_ok) {
+#pragma unroll
+                for (int cc = 0; cc < NC; ++cc)
+                    total += cnt[e0 - (cc & 1) - ((cc >> 1) & 1) * CE - (DIM == 3 ? ((cc >> 2) & 1) * CE * CE : 0)];
+            }
+            for (int k = 0; k < total; ++k) {
+                if (j == jend) {
+                    do {
+                        ++c;
                         const int e = e0 - (c & 1) - ((c >> 1) & 1) * CE - (DIM == 3 ? ((c >> 2) & 1) * CE * CE : 0);
-                        const int j1 = start[e] + cnt[e];
-                        bool bit[DIM];
-#pragma unroll
-                        for (int a = 0; a < DIM; ++a) bit[a] = (c >> a) & 1;
-                        for (int j = start[e]; j < j1; ++j) {
-                            const float2* rp = reinterpret_cast<const float2*>(uni + j * REC);
-                            float r[REC];
-#pragma unroll
-                            for (int k2 = 0; k2 < REC / 2; ++k2) {
-                                const float2 t2 = rp[k2];
-                                r[2 * k2] = t2.x;
-                                r[2 * k2 + 1] = t2.y;
-                            }
-                            Corner<DIM> cg;
-                            float sv[DIM];
-#pragma unroll
-                            for (int a = 0; a < DIM; ++a) {
-                                const float s0 = r[a], s1 = r[DIM + a];
-                                sv[a] = bit[a] ? s1 : s0;
-                                cg.d[a] = (bit[a] ? -s0 : s1) * A.s.hf[a];  // (l - bit) * h
-                            }
-                            cg.w = sv[0];
-#pragma unroll
-                            for (int a = 1; a < DIM; ++a) cg.w *= sv[a];
-                            float gvd[DIM];
-#pragma unroll
-                            for (int a = 0; a < DIM; ++a) {
-                                float other = 1.0f;
-#pragma unroll
-                                for (int bb = 0; bb < DIM; ++bb)
-                                    if (bb != a) other *= sv[bb];
-                                cg.dw[a] = EIK ? (bit[a] ? A.s.inv_hf[a] : -A.s.inv_hf[a]) * other : 0.0f;
-                                gvd[a] = EIK ? r[2 * DIM + 1 + a] : 0.0f;
-                            }
-                            corner_grad<DIM, ORDER, K>(cg, r[2 * DIM], gvd, G);
-                        }
-                    }
+                        j = start[e];
+                        jend = j + cnt[e];
+                    } while (j == jend);
                 }
-            }
-            __syncthreads();
-        }
-
-        // ---- 3. TV + Adam over the owned coefficients (warp per row) ----
-        float* Gs = uni;
+                const float2* rp = reinterpret_cast<const float2*>(uni + j * REC);
+                float r[REC];
 #pragma unroll
-        for (int q = 0; q < K; ++q) Gs[myv * K + q] = G[q];
-        mbar_wait(&bars[sidx][1], phase);  // m/v rows landed
+                for (int k2 = 0; k2 < REC / 2; ++k2) {
+                    const float2 t2 = rp[k2];
+                    r[2 * k2] = t2.x;
+                    r[2 * k2 + 1] = t2.y;
+                }
+                Corner<DIM> cg;
+                float sv[DIM];
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    const bool bit = (c >> a) & 1;
+                    const float s0 = r[a], s1 = r[DIM + a];
+                    sv[a] = bit ? s1 : s0;
+                    cg.d[a] = (bit ? -s0 : s1) * A.s.hf[a];  // (l - bit) * h
+                }
+                cg.w = sv[0];
+#pragma unroll
+                for (int a = 1; a < DIM; ++a) cg.w *= sv[a];
+                float gvd[DIM];
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    float other = 1.0f;
+#pragma unroll
+                    for (int bb = 0; bb < DIM; ++bb)
+                        if (bb != a) other *= sv[bb];
+                    cg.dw[a] = EIK ? (((c >> a) & 1) ? A.s.inv_hf[a] : -A.s.inv_hf[a]) * other : 0.0f;
+                    gvd[a] = EIK ? r[2 * DIM + 1 + a] : 0.0f;
+                }
+                corner_grad<DIM, ORDER, K>(cg, r[2 * DIM], gvd, G);
+                ++j;
+            }
+        }
         __syncthreads();
+    }
+
+    // ---- 3. TV + Adam over the owned coefficients (flat float2 items) ----
+    float* Gs = uni;
+#pragma unroll
+    for (int q = 0; q < K; ++q) Gs[myv * K + q] = G[q];
+    if (warp == 0) mbar_wait(&bars[1], 0);  // m/v rows landed
+    __syncthreads();
+    double tv_sum = 0.0;
+    {
+        const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
+        float* __restrict__ p_out = A.p_out;
+        float* __restrict__ m_out = A.m_out;
+        float* __restrict__ v_out = A.v_out;
         constexpr int OROWS = DIM == 3 ? B * B : B;
-        constexpr int ROWF = B * K;  // floats per owned row
-        constexpr int TY = L::TROWF, TZ = DIM == 3 ? T * L::TROWF : 0;  // tile strides
-        for (int r = warp; r < OROWS; r += NW) {
+        constexpr int ROWF = B * K;      // floats per owned row
+        constexpr int W = K % 2 == 0 ? 2 : 1;
+        constexpr int ROWI = ROWF / W;   // items per row
+        constexpr int TY = L::TROWF, TZ = DIM == 3 ? T * L::TROWF : 0;
+        for (int it = tid; it < OROWS * ROWI; it += NT) {
+            const int r = it / ROWI, j = (it - r * ROWI) * W;
             const int ly = r % B, lz = DIM == 3 ? r / B : 0;
             const int gy = o[1] + ly, gz = o[2] + lz;
-            if (gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
-            const long long rbase = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K;
-            const float* trow = tile + L::at(1, ly + 1, DIM == 3 ? lz + 1 : 0);
-            const bool ylo = gy >= 1, yhi = gy + 1 < A.s.res[1];
-            const bool zlo = DIM == 3 && gz >= 1, zhi = DIM == 3 && gz + 1 < A.s.res[2];
-            for (int j = lane; j < ROWF; j += 32) {
-                const int lx = j / K;
-                const int gx = o[0] + lx;
-                if (gx >= A.s.res[0]) continue;
-                const int e = r * ROWF + j;
-                const float* tp = trow + j;
-                const float pv = *tp;
-                float gt = 0.0f;
-                if (A.want_tv) {
-                    // pairs (v, v+e_a) owned here feed the TV sum; both ends'
-                    // terms feed this vertex's gradient (sdf_loss.cpp:155-257)
-                    float sq = 0.0f;
-                    if (gx + 1 < A.s.res[0]) { const float d = tp[K] - pv; sq = fmaf(d, d, sq); gt -= d; }
-                    if (gx >= 1) gt += pv - tp[-K];
-                    if (yhi) { const float d = tp[TY] - pv; sq = fmaf(d, d, sq); gt -= d; }
-                    if (ylo) gt += pv - tp[-TY];
-                    if (DIM == 3) {
-                        if (zhi) { const float d = tp[TZ] - pv; sq = fmaf(d, d, sq); gt -= d; }
-                        if (zlo) gt += pv - tp[-TZ];
+            const int lx = j / K;
+            const int gx = o[0] + lx;
+            if (gx >= A.s.res[0] || gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
+            const int e = r * ROWF + j;
+            const float* tp = tile + L::at(1 + lx, ly + 1, DIM == 3 ? lz + 1 : 0) + (j - lx * K);
+            float pv[W], gt[W];
+#pragma unroll
+            for (int w2 = 0; w2 < W; ++w2) {
+                pv[w2] = tp[w2];
+                gt[w2] = 0.0f;
+            }
+            if (A.want_tv) {
+                // pairs (v, v+e_a) owned here feed the TV sum; both ends'
+                // terms feed this vertex's gradient (sdf_loss.cpp:155-257)
+                const int offs[3] = {K, TY, TZ};
+                const bool hi3[3] = {gx + 1 < A.s.res[0], gy + 1 < A.s.res[1], DIM == 3 && gz + 1 < A.s.res[2]};
+                const bool lo3[3] = {gx >= 1, gy >= 1, DIM == 3 && gz >= 1};
+                float sq = 0.0f;
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+#pragma unroll
+                    for (int w2 = 0; w2 < W; ++w2) {
+                        if (hi3[a]) {
+                            const float d = tp[offs[a] + w2] - pv[w2];
+                            sq = fmaf(d, d, sq);
+                            gt[w2] -= d;
+                        }
+                        if (lo3[a]) gt[w2] += pv[w2] - tp[w2 - offs[a]];
                     }
-                    tv_sum += (double)sq;
                 }
-                const float gi = fmaf(A.tv_gscale, gt, Gs[e]);
-                const long long gidx = rbase + j;
-                if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)gidx);
-                if (A.grad_out) A.grad_out[gidx] = gi;
-                const float mi = fmaf(A.b1, mvs[e], c1 * gi);
-                const float vi = fmaf(A.b2, mvs[S::NOWN * K + e], c2 * gi * gi);
-                m_out[gidx] = mi;
-                v_out[gidx] = vi;
-                p_out[gidx] = pv - lr_bc1 * mi * fast_rcp(fast_sqrt(vi * A.inv_bc2) + A.eps);
+                tv_sum += (double)sq;
+            }
+            const long long gidx = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K + j;
+            float pn[W], mn[W], vn[W];
+#pragma unroll
+            for (int w2 = 0; w2 < W; ++w2) {
+                const float gi = fmaf(A.tv_gscale, gt[w2], Gs[e + w2]);
+                if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + w2));
+                if (A.grad_out) A.grad_out[gidx + w2] = gi;
+                mn[w2] = fmaf(A.b1, mvs[e + w2], c1 * gi);
+                vn[w2] = fmaf(A.b2, mvs[S::NOWN * K + e + w2], c2 * gi * gi);
+                pn[w2] = pv[w2] - lr_bc1 * mn[w2] * fast_rcp(fast_sqrt(vn[w2] * A.inv_bc2) + A.eps);
+            }
+            if constexpr (W == 2) {
+                *reinterpret_cast<float2*>(m_out + gidx) = make_float2(mn[0], mn[1]);
+                *reinterpret_cast<float2*>(v_out + gidx) = make_float2(vn[0], vn[1]);
+                *reinterpret_cast<float2*>(p_out + gidx) = make_float2(pn[0], pn[1]);
+            } else {
+                m_out[gidx] = mn[0];
+                v_out[gidx] = vn[0];
+                p_out[gidx] = pn[0];
             }
         }
-        __syncthreads();  // stage `sidx` and the records are free again
-        // per-brick loss partials (fixed-order block reduction)
-        {
-            const double v4[4] = {warp_sum_d(recon_sum), warp_sum_d(eik_sum), warp_sum_d(tv_sum), warp_sum_d(home_pts)};
-            if (lane == 0)
-                for (int k2 = 0; k2 < 4; ++k2) red[k2][warp] = v4[k2];
-            __syncthreads();
-            if (tid < 4) {
-                double acc = 0.0;
-                for (int k2 = 0; k2 < NW; ++k2) acc += red[tid][k2];
-                A.partials[4 * b + tid] = acc;
-            }
-            recon_sum = eik_sum = tv_sum = home_pts = 0.0;
+    }
+
+    // ---- per-brick loss partials (fixed-order block reduction) ----
+    {
+        const double v4[4] = {warp_sum_d(recon_sum), warp_sum_d(eik_sum), warp_sum_d(tv_sum), warp_sum_d(home_pts)};
+        if (lane == 0)
+            for (int k2 = 0; k2 < 4; ++k2) red[k2][warp] = v4[k2];
+        __syncthreads();
+        if (tid < 4) {
+            double acc = 0.0;
+            for (int k2 = 0; k2 < NW; ++k2) acc += red[tid][k2];
+            A.partials[4 * b + tid] = acc;
         }
-        b = bnext;
     }
 }
 
@@ -811,10 +811,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
             configured = true;
         }
         if (g.prof_on) prof_mark(g, s, 0);
-        int nsm = 148;
-        TGCU_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g.device));
-        const unsigned ctas = (unsigned)std::min<long long>(nsm, g.NB);
-        kern<<<ctas, BrickShape<DIM>::NT, smem, s>>>(A);
+        kern<<<(unsigned)g.NB, BrickShape<DIM>::NT, smem, s>>>(A);
         if (g.prof_on) prof_mark(g, s, 1);
     });
 
