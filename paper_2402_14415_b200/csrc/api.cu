@@ -79,6 +79,14 @@ void ensure_bins(Grid& g, int64_t points) {
     g.binned_cap = need;
 }
 
+void ensure_bin_hist(Grid& g, int64_t ints) {
+    if (g.bin_hist_cap >= ints) return;
+    if (g.bin_hist) TGCU_CUDA(cudaFree(g.bin_hist));
+    g.bin_hist = nullptr;
+    TGCU_CUDA(cudaMalloc(&g.bin_hist, sizeof(int) * ints));
+    g.bin_hist_cap = ints;
+}
+
 // Ping-pong parameters + Adam moments (both slots), zero moments.
 void ensure_optimizer(Grid& g) {
     if (g.m[0]) return;
@@ -269,6 +277,7 @@ int tgcu_grid_destroy(tgcu_grid* h) {
     cudaFree(g.bin_off);
     cudaFree(g.bin_cursor);
     cudaFree(g.binned);
+    cudaFree(g.bin_hist);
     cudaFree(g.partials);
     cudaFree(g.d_trace);
     cudaFreeHost(g.h_terms);

@@ -68,6 +68,8 @@ struct Grid {
     int* bin_count = nullptr;   // NB + 1
     int* bin_off = nullptr;     // NB + 1
     int* bin_cursor = nullptr;  // NB
+    int* bin_hist = nullptr;    // per-tile brick histograms (privatized binning)
+    int64_t bin_hist_cap = 0;
     float4* binned = nullptr;
     int64_t binned_cap = 0;     // points
     double* partials = nullptr; // NB * 4
@@ -90,6 +92,7 @@ constexpr int kTraceCap = 4096;
 
 void ensure_staging(Grid& g, int64_t floats);
 void ensure_bins(Grid& g, int64_t points);
+void ensure_bin_hist(Grid& g, int64_t ints);
 void ensure_scratch(Grid& g, int64_t doubles);
 void ensure_grad(Grid& g);
 void ensure_optimizer(Grid& g);

@@ -151,6 +151,71 @@ __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs A) {
     }
 }
 
+// ---- privatized binning (NB small enough for a shared-memory histogram) ----
+// Points are cut into tiles of kBinTile; CTA c builds the brick histogram of
+// tile c in shared memory (native int smem atomics) and stores it as row c of
+// H[ncta][NB]. A column scan turns H into per-(tile, brick) bases, the brick
+// totals are scanned into offsets, and the scatter kernel reserves slots with
+// shared-memory atomics only: no contended global atomics on hot bricks.
+constexpr int kBinTile = 4096;
+constexpr int kBinThreads = 512;
+constexpr int kBinSmemMax = 16384;  // bricks
+
+template <int DIM>
+__global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __restrict__ H, int NB) {
+    extern __shared__ int hist[];
+    if (A.st->error) return;
+    for (int i = threadIdx.x; i < NB; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const long long t0 = (long long)blockIdx.x * kBinTile;
+    const long long t1 = min(t0 + kBinTile, A.n);
+    for (long long i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+        int br[8];
+        const int m = point_bricks<DIM>(A.s, A.nb, A.pts[i], br);
+        if (m == 0) atomicMin(&A.st->nan_point, (unsigned long long)i);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < m) atomicAdd(&hist[br[k]], 1);
+    }
+    __syncthreads();
+    int* row = H + (long long)blockIdx.x * NB;
+    for (int i = threadIdx.x; i < NB; i += blockDim.x) row[i] = hist[i];
+}
+
+// Per brick: exclusive scan of H over tiles (in place) and the brick total.
+__global__ void k_bin_cols(int* __restrict__ H, int ncta, int NB, int* __restrict__ totals, Status* st) {
+    if (st->error) return;
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= NB) return;
+    int sum = 0;
+    for (int c = 0; c < ncta; ++c) {
+        const int v = H[(long long)c * NB + b];
+        H[(long long)c * NB + b] = sum;
+        sum += v;
+    }
+    totals[b] = sum;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kBinThreads) k_bin_scatter_tiles(BinArgs A, const int* __restrict__ H,
+                                                                   const int* __restrict__ off, int NB) {
+    extern __shared__ int cur[];
+    if (A.st->error) return;
+    const int* row = H + (long long)blockIdx.x * NB;
+    for (int i = threadIdx.x; i < NB; i += blockDim.x) cur[i] = off[i] + row[i];
+    __syncthreads();
+    const long long t0 = (long long)blockIdx.x * kBinTile;
+    const long long t1 = min(t0 + kBinTile, A.n);
+    for (long long i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+        const float4 q = A.pts[i];
+        int br[8];
+        const int m = point_bricks<DIM>(A.s, A.nb, q, br);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < m) A.binned[atomicAdd(&cur[br[k]], 1)] = q;
+    }
+}
+
 struct StepArgs {
     DevSpec s;
     const float* p_in;
@@ -521,21 +586,26 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
 #pragma unroll
             for (int a = 0; a < DIM; ++a) own_ok &= (o[a] + l3[a]) < A.s.res[a];
             const int e0 = DIM == 3 ? ((l3[2] + 1) * CE + l3[1] + 1) * CE + l3[0] + 1 : (l3[1] + 1) * CE + l3[0] + 1;
-            int c = -1, j = 0, jend = 0;
+            // non-empty incident cells as a bitmask; one flat loop over items,
+            // the next corner is found with ffs when a cell's run ends
+            unsigned mask = 0;
             int total = 0;
             if (own_ok) {
 #pragma unroll
-                for (int cc = 0; cc < NC; ++cc)
-                    total += cnt[e0 - (cc & 1) - ((cc >> 1) & 1) * CE - (DIM == 3 ? ((cc >> 2) & 1) * CE * CE : 0)];
+                for (int cc = 0; cc < NC; ++cc) {
+                    const int n = cnt[e0 - (cc & 1) - ((cc >> 1) & 1) * CE - (DIM == 3 ? ((cc >> 2) & 1) * CE * CE : 0)];
+                    total += n;
+                    mask |= (n > 0 ? 1u : 0u) << cc;
+                }
             }
+            int c = 0, j = 0, jend = 0;
             for (int k = 0; k < total; ++k) {
                 if (j == jend) {
-                    do {
-                        ++c;
-                        const int e = e0 - (c & 1) - ((c >> 1) & 1) * CE - (DIM == 3 ? ((c >> 2) & 1) * CE * CE : 0);
-                        j = start[e];
-                        jend = j + cnt[e];
-                    } while (j == jend);
+                    c = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const int e = e0 - (c & 1) - ((c >> 1) & 1) * CE - (DIM == 3 ? ((c >> 2) & 1) * CE * CE : 0);
+                    j = start[e];
+                    jend = j + cnt[e];
                 }
                 const float2* rp = reinterpret_cast<const float2*>(uni + j * REC);
                 float r[REC];
@@ -574,7 +644,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
         __syncthreads();
     }
 
-    // ---- 3. TV + Adam over the owned coefficients (flat float2 items) ----
+    // ---- 3. TV + Adam over the owned coefficients: thread per vertex ----
     float* Gs = uni;
 #pragma unroll
     for (int q = 0; q < K; ++q) Gs[myv * K + q] = G[q];
@@ -582,70 +652,83 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
     __syncthreads();
     double tv_sum = 0.0;
     {
-        const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
-        float* __restrict__ p_out = A.p_out;
-        float* __restrict__ m_out = A.m_out;
-        float* __restrict__ v_out = A.v_out;
-        constexpr int OROWS = DIM == 3 ? B * B : B;
-        constexpr int ROWF = B * K;      // floats per owned row
         constexpr int W = K % 2 == 0 ? 2 : 1;
-        constexpr int ROWI = ROWF / W;   // items per row
-        constexpr int TY = L::TROWF, TZ = DIM == 3 ? T * L::TROWF : 0;
-        for (int it = tid; it < OROWS * ROWI; it += NT) {
-            const int r = it / ROWI, j = (it - r * ROWI) * W;
-            const int ly = r % B, lz = DIM == 3 ? r / B : 0;
-            const int gy = o[1] + ly, gz = o[2] + lz;
-            const int lx = j / K;
-            const int gx = o[0] + lx;
-            if (gx >= A.s.res[0] || gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
-            const int e = r * ROWF + j;
-            const float* tp = tile + L::at(1 + lx, ly + 1, DIM == 3 ? lz + 1 : 0) + (j - lx * K);
-            float pv[W], gt[W];
+        const int v = tid;
+        const int l3[3] = {v % B, (v / B) % B, DIM == 3 ? v / (B * B) : 0};
+        const int g3[3] = {o[0] + l3[0], o[1] + l3[1], o[2] + l3[2]};
+        bool ok = true;
 #pragma unroll
-            for (int w2 = 0; w2 < W; ++w2) {
-                pv[w2] = tp[w2];
-                gt[w2] = 0.0f;
+        for (int a = 0; a < DIM; ++a) ok &= g3[a] < A.s.res[a];
+        if (ok) {
+            const float* tp = tile + L::at(1 + l3[0], 1 + l3[1], DIM == 3 ? 1 + l3[2] : 0);
+            float pv[K], gt[K];
+#pragma unroll
+            for (int q = 0; q < K; q += W) {
+                if constexpr (W == 2) {
+                    const float2 t2 = *reinterpret_cast<const float2*>(tp + q);
+                    pv[q] = t2.x;
+                    pv[q + 1] = t2.y;
+                } else {
+                    pv[q] = tp[q];
+                }
             }
+#pragma unroll
+            for (int q = 0; q < K; ++q) gt[q] = 0.0f;
             if (A.want_tv) {
                 // pairs (v, v+e_a) owned here feed the TV sum; both ends'
                 // terms feed this vertex's gradient (sdf_loss.cpp:155-257)
-                const int offs[3] = {K, TY, TZ};
-                const bool hi3[3] = {gx + 1 < A.s.res[0], gy + 1 < A.s.res[1], DIM == 3 && gz + 1 < A.s.res[2]};
-                const bool lo3[3] = {gx >= 1, gy >= 1, DIM == 3 && gz >= 1};
+                constexpr int offs[3] = {K, L::TROWF, DIM == 3 ? T * L::TROWF : 0};
                 float sq = 0.0f;
 #pragma unroll
                 for (int a = 0; a < DIM; ++a) {
+                    if (g3[a] + 1 < A.s.res[a]) {
 #pragma unroll
-                    for (int w2 = 0; w2 < W; ++w2) {
-                        if (hi3[a]) {
-                            const float d = tp[offs[a] + w2] - pv[w2];
+                        for (int q = 0; q < K; ++q) {
+                            const float d = tp[offs[a] + q] - pv[q];
                             sq = fmaf(d, d, sq);
-                            gt[w2] -= d;
+                            gt[q] -= d;
                         }
-                        if (lo3[a]) gt[w2] += pv[w2] - tp[w2 - offs[a]];
+                    }
+                    if (g3[a] >= 1) {
+#pragma unroll
+                        for (int q = 0; q < K; ++q) gt[q] += pv[q] - tp[q - offs[a]];
                     }
                 }
-                tv_sum += (double)sq;
+                tv_sum = (double)sq;
             }
-            const long long gidx = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K + j;
-            float pn[W], mn[W], vn[W];
+            const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
+            const long long gidx =
+                ((DIM == 3 ? (long long)g3[2] * A.s.sz : 0LL) + (long long)g3[1] * A.s.sy + g3[0]) * K;
+            const float* gs = Gs + v * K;
+            const float* mm = mvs + v * K;
+            const float* vv = mvs + S::NOWN * K + v * K;
+            float pn[K], mn[K], vn[K];
+            bool finite = true;
 #pragma unroll
-            for (int w2 = 0; w2 < W; ++w2) {
-                const float gi = fmaf(A.tv_gscale, gt[w2], Gs[e + w2]);
-                if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + w2));
-                if (A.grad_out) A.grad_out[gidx + w2] = gi;
-                mn[w2] = fmaf(A.b1, mvs[e + w2], c1 * gi);
-                vn[w2] = fmaf(A.b2, mvs[S::NOWN * K + e + w2], c2 * gi * gi);
-                pn[w2] = pv[w2] - lr_bc1 * mn[w2] * fast_rcp(fast_sqrt(vn[w2] * A.inv_bc2) + A.eps);
+            for (int q = 0; q < K; ++q) {
+                const float gi = fmaf(A.tv_gscale, gt[q], gs[q]);
+                finite &= isfinite(gi);
+                if (A.grad_out) A.grad_out[gidx + q] = gi;
+                mn[q] = fmaf(A.b1, mm[q], c1 * gi);
+                vn[q] = fmaf(A.b2, vv[q], c2 * gi * gi);
+                pn[q] = pv[q] - lr_bc1 * mn[q] * fast_rcp(fast_sqrt(vn[q] * A.inv_bc2) + A.eps);
             }
-            if constexpr (W == 2) {
-                *reinterpret_cast<float2*>(m_out + gidx) = make_float2(mn[0], mn[1]);
-                *reinterpret_cast<float2*>(v_out + gidx) = make_float2(vn[0], vn[1]);
-                *reinterpret_cast<float2*>(p_out + gidx) = make_float2(pn[0], pn[1]);
-            } else {
-                m_out[gidx] = mn[0];
-                v_out[gidx] = vn[0];
-                p_out[gidx] = pn[0];
+            if (!finite) {
+                for (int q = 0; q < K; ++q)
+                    if (!isfinite(fmaf(A.tv_gscale, gt[q], gs[q])))
+                        atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
+            }
+#pragma unroll
+            for (int q = 0; q < K; q += W) {
+                if constexpr (W == 2) {
+                    *reinterpret_cast<float2*>(A.m_out + gidx + q) = make_float2(mn[q], mn[q + 1]);
+                    *reinterpret_cast<float2*>(A.v_out + gidx + q) = make_float2(vn[q], vn[q + 1]);
+                    *reinterpret_cast<float2*>(A.p_out + gidx + q) = make_float2(pn[q], pn[q + 1]);
+                } else {
+                    A.m_out[gidx + q] = mn[q];
+                    A.v_out[gidx + q] = vn[q];
+                    A.p_out[gidx + q] = pn[q];
+                }
             }
         }
     }
@@ -751,13 +834,34 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     B.cursor = g.bin_cursor;
     B.binned = g.binned;
     B.st = g.st;
-    TGCU_CUDA(cudaMemsetAsync(g.bin_count, 0, sizeof(int) * (g.NB + 1), s));  // + work counter
-    const int pblocks = grid_blocks(n, 256, 148 * 16);
-    if (g.spec.dim == 3) k_bin_count<3><<<pblocks, 256, 0, s>>>(B);
-    else k_bin_count<2><<<pblocks, 256, 0, s>>>(B);
-    k_bin_scan<<<1, 1024, 0, s>>>(g.bin_count, g.bin_off, g.bin_cursor, (int)g.NB, g.st);
-    if (g.spec.dim == 3) k_bin_scatter<3><<<pblocks, 256, 0, s>>>(B);
-    else k_bin_scatter<2><<<pblocks, 256, 0, s>>>(B);
+    if (g.NB <= kBinSmemMax) {
+        const int ncta = (int)((n + kBinTile - 1) / kBinTile);
+        ensure_bin_hist(g, (int64_t)ncta * g.NB);
+        const size_t sm = sizeof(int) * g.NB;
+        if (g.spec.dim == 3) {
+            TGCU_CUDA(cudaFuncSetAttribute(k_bin_hist<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kBinSmemMax)));
+            TGCU_CUDA(cudaFuncSetAttribute(k_bin_scatter_tiles<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kBinSmemMax)));
+            k_bin_hist<3><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, (int)g.NB);
+        } else {
+            TGCU_CUDA(cudaFuncSetAttribute(k_bin_hist<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kBinSmemMax)));
+            TGCU_CUDA(cudaFuncSetAttribute(k_bin_scatter_tiles<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kBinSmemMax)));
+            k_bin_hist<2><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, (int)g.NB);
+        }
+        k_bin_cols<<<(unsigned)((g.NB + 255) / 256), 256, 0, s>>>(g.bin_hist, ncta, (int)g.NB, g.bin_count, g.st);
+        k_bin_scan<<<1, 1024, 0, s>>>(g.bin_count, g.bin_off, g.bin_cursor, (int)g.NB, g.st);
+        if (g.spec.dim == 3) k_bin_scatter_tiles<3><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_off, (int)g.NB);
+        else k_bin_scatter_tiles<2><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_off, (int)g.NB);
+        count_launch(4);
+    } else {
+        TGCU_CUDA(cudaMemsetAsync(g.bin_count, 0, sizeof(int) * g.NB, s));
+        const int pblocks = grid_blocks(n, 256, 148 * 16);
+        if (g.spec.dim == 3) k_bin_count<3><<<pblocks, 256, 0, s>>>(B);
+        else k_bin_count<2><<<pblocks, 256, 0, s>>>(B);
+        k_bin_scan<<<1, 1024, 0, s>>>(g.bin_count, g.bin_off, g.bin_cursor, (int)g.NB, g.st);
+        if (g.spec.dim == 3) k_bin_scatter<3><<<pblocks, 256, 0, s>>>(B);
+        else k_bin_scatter<2><<<pblocks, 256, 0, s>>>(B);
+        count_launch(3);
+    }
 
     StepArgs A;
     A.s = g.ds;
@@ -830,7 +934,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     F.in_idx = in_idx;
     F.t_after = t_after;
     k_step_finalize<<<1, 1024, 0, s>>>(F);
-    count_launch(5);
+    count_launch(2);
     TGCU_CUDA(cudaGetLastError());
 }
 
