@@ -96,9 +96,8 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs A) {
 
 // Exclusive scan of NB brick counts -> off[0..NB], cursor = off. One CTA.
 __global__ void __launch_bounds__(1024) k_bin_scan(const int* __restrict__ count, int* __restrict__ off,
-                                                   int* __restrict__ cursor, int NB, Status* st, int* work) {
+                                                   int* __restrict__ cursor, int NB, Status* st) {
     if (st->error) return;
-    if (threadIdx.x == 0 && work) *work = 0;  // brick counter of the persistent step kernel
     __shared__ int warp_tot[32];
     __shared__ int carry;
     if (threadIdx.x == 0) carry = 0;
@@ -183,30 +182,49 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __rest
     for (int i = threadIdx.x; i < NB; i += blockDim.x) row[i] = hist[i];
 }
 
-// Per brick (one warp per brick): exclusive scan of H over tiles (in place)
-// and the brick total.
-__global__ void k_bin_cols(int* __restrict__ H, int ncta, int NB, int* __restrict__ totals, Status* st) {
+// Per brick: exclusive scan of H over tiles (in place) and the brick total.
+// A CTA owns 32 bricks: it loads their H columns for all tiles with
+// coalesced 128-byte rows into smem, scans each column with one warp, and
+// writes them back.
+constexpr int kColBricks = 32;
+constexpr int kMaxBinTiles = 512;
+__global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta, int NB, int* __restrict__ totals,
+                                                  Status* st) {
+    extern __shared__ int col[];  // [ncta][kColBricks + 1]
     if (st->error) return;
-    const int b = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (b >= NB) return;
+    const int b0 = blockIdx.x * kColBricks;
+    const int nb = min(kColBricks, NB - b0);
+    constexpr int LD = kColBricks + 1;
+    for (int i = threadIdx.x; i < ncta * kColBricks; i += blockDim.x) {
+        const int c = i / kColBricks, j = i - c * kColBricks;
+        if (j < nb) col[c * LD + j] = H[(long long)c * NB + b0 + j];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int per = (ncta + 31) / 32;
-    const int c0 = min(lane * per, ncta), c1 = min(c0 + per, ncta);
-    int sum = 0;
-    for (int c = c0; c < c1; ++c) sum += H[(long long)c * NB + b];
-    int x = sum;
+    for (int j = warp; j < nb; j += blockDim.x / 32) {
+        const int c0 = min(lane * per, ncta), c1 = min(c0 + per, ncta);
+        int sum = 0;
+        for (int c = c0; c < c1; ++c) sum += col[c * LD + j];
+        int x = sum;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, off);
-        if (lane >= off) x += y;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, off);
+            if (lane >= off) x += y;
+        }
+        int run = x - sum;
+        for (int c = c0; c < c1; ++c) {
+            const int v = col[c * LD + j];
+            col[c * LD + j] = run;
+            run += v;
+        }
+        if (lane == 31) totals[b0 + j] = x;
     }
-    int run = x - sum;
-    for (int c = c0; c < c1; ++c) {
-        const int v = H[(long long)c * NB + b];
-        H[(long long)c * NB + b] = run;
-        run += v;
+    __syncthreads();
+    for (int i = threadIdx.x; i < ncta * kColBricks; i += blockDim.x) {
+        const int c = i / kColBricks, j = i - c * kColBricks;
+        if (j < nb) H[(long long)c * NB + b0 + j] = col[c * LD + j];
     }
-    if (lane == 31) totals[b] = x;
 }
 
 template <int DIM>
@@ -247,7 +265,6 @@ struct StepArgs {
     double* partials;  // NB x 4: recon, eik, tv, home points
     Status* st;
     float* grad_out;   // optional: full gradient (validation mode, TGCU_EXPORT_GRAD)
-    int* work;         // persistent-kernel brick counter (zeroed per step)
 };
 
 template <int NCELL, int NT>
@@ -337,13 +354,11 @@ __device__ __forceinline__ float fast_rcp(float x) {
     return r;
 }
 
-// Shared-memory plan of the fused brick kernel: persistent, 2 CTAs/SM, the
-// parameter tile double-buffered (the next brick's tile arrives by TMA while
-// the current one computes). Tile rows (fixed y, z) are stored with a stride
-// of TROWF floats and start SHF floats into the row, so that a row's HBM range
-// is one 16-byte-aligned TMA bulk copy (the reference AoS layout puts vertex
-// o-1 at an 8-byte offset for K = 10). The Adam moments are not staged: their
-// rows are bulk-prefetched into L2 and read by the epilogue.
+// Shared-memory plan of the fused brick kernel (one brick per CTA, 2 CTAs/SM).
+// Tile rows (fixed y, z) are stored with a stride of TROWF floats and start
+// SHF floats into the row, so that a row's HBM range is one 16-byte-aligned
+// TMA bulk copy (the reference AoS layout puts vertex o-1 at an 8-byte offset
+// for K = 10).
 template <int DIM, int ORDER>
 struct BrickSmem {
     using S = BrickShape<DIM>;
@@ -351,46 +366,35 @@ struct BrickSmem {
     static constexpr int SHF = (4 - (K % 4)) % 4;
     static constexpr int TROWF = ((S::T * K + SHF + 3) / 4) * 4;
     static constexpr int TROWS = DIM == 3 ? S::T * S::T : S::T;
-    static constexpr int tile_data = TROWS * TROWF;
-    static constexpr int tile = tile_data > 2 * S::NOWN * K ? tile_data : 2 * S::NOWN * K;  // per buffer
+    static constexpr int tile = TROWS * TROWF;                    // floats
+    static constexpr int mv = 2 * S::NOWN * K;                    // m then v
     static constexpr int REC = ((3 * DIM + 1) + 1) / 2 * 2;       // s0[D] s1[D] u g[D] (even)
     static constexpr int pts = S::CH * REC;                       // cell-ordered records
     static constexpr int gs = S::NOWN * K;
     static constexpr int uni = pts > gs ? pts : gs;
-    static_assert(tile >= 2 * gs, "tile buffer doubles as the m/v output staging");
-    static constexpr size_t bytes = sizeof(float) * (2 * tile + uni) + sizeof(int) * (S::NCELL * 2 + S::NT + 64 * 2);
+    static constexpr size_t bytes = sizeof(float) * (tile + mv + uni) + sizeof(int) * (S::NCELL * 2 + S::NT + 64 * 2);
     // float offset of tile vertex (tx, ty, tz)
     __device__ static constexpr int at(int tx, int ty, int tz) {
         return (DIM == 3 ? (tz * S::T + ty) : ty) * TROWF + SHF + tx * K;
     }
 };
 
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
-}
-
-template <int DIM>
-__device__ __forceinline__ void brick_origin(const StepArgs& A, int b, int* o) {
-    constexpr int B = BrickShape<DIM>::B;
-    const int nbx = A.nb[0], nby = A.nb[1];
-    o[0] = (b % nbx) * B;
-    o[1] = ((b / nbx) % nby) * B;
-    o[2] = DIM == 3 ? (b / (nbx * nby)) * B : 0;
-}
-
-// Warp 0: TMA the tile of brick b (one bulk copy per HBM row; unaligned or
-// out-of-array rows fall back to cp.async) and bulk-prefetch its m/v rows
-// into L2.
+// Issue the HBM->smem copies of brick `b` (warp 0): one TMA bulk copy per
+// HBM row (tile rows -> bar_tile, owned m/v rows -> bar_mv); rows that are not
+// 16-byte aligned or would read outside the array fall back to cp.async.
 template <int DIM, int ORDER>
-__device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, float* tile,
-                                            unsigned long long* bar_tile, int lane) {
+__device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, float* tile, float* mvs,
+                                            unsigned long long* bar_tile, unsigned long long* bar_mv, int lane) {
     using S = BrickShape<DIM>;
     using L = BrickSmem<DIM, ORDER>;
     constexpr int K = L::K, B = S::B, T = S::T;
     constexpr int GR = (K % 2 == 0) ? 2 : 1;
     const long long nc_bytes = (long long)A.s.res[0] * A.s.res[1] * (DIM == 3 ? A.s.res[2] : 1) * K * 4;
     constexpr unsigned TBYTES = ((L::SHF * 4 + T * K * 4 + 15) / 16) * 16;
-    unsigned tx_bytes = 0;
+    constexpr unsigned OBYTES = B * K * 4;
+    constexpr int OROWS = DIM == 3 ? B * B : B;
+    const bool mv_bulk_ok = (OBYTES % 16) == 0 && o[0] + B <= A.s.res[0];
+    unsigned tx_bytes = 0, mv_bytes = 0;
     for (int r = lane; r < L::TROWS; r += 32) {
         const int ty = DIM == 3 ? r % T : r, tz = DIM == 3 ? r / T : 0;
         const int vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
@@ -399,9 +403,22 @@ __device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, flo
             ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0] - 1) * K * 4 - L::SHF * 4;
         if ((src & 15) == 0 && src >= 0 && src + TBYTES <= nc_bytes) tx_bytes += TBYTES;
     }
+    for (int r = lane; r < OROWS; r += 32) {
+        const int ly = r % B, lz = DIM == 3 ? r / B : 0;
+        const int vy = o[1] + ly, vz = o[2] + lz;
+        if (vy >= A.s.res[1] || (DIM == 3 && vz >= A.s.res[2])) continue;
+        const long long src = ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0]) * K * 4;
+        if ((src & 15) == 0 && mv_bulk_ok) mv_bytes += 2 * OBYTES;
+    }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) tx_bytes += __shfl_xor_sync(0xffffffffu, tx_bytes, off);
-    if (lane == 0) mbar_expect_tx(bar_tile, tx_bytes);
+    for (int off = 16; off > 0; off >>= 1) {
+        tx_bytes += __shfl_xor_sync(0xffffffffu, tx_bytes, off);
+        mv_bytes += __shfl_xor_sync(0xffffffffu, mv_bytes, off);
+    }
+    if (lane == 0) {
+        mbar_expect_tx(bar_tile, tx_bytes);
+        mbar_expect_tx(bar_mv, mv_bytes);
+    }
     __syncwarp();
     const float* p_in = A.p_in;
     for (int r = lane; r < L::TROWS; r += 32) {
@@ -421,21 +438,26 @@ __device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, flo
             }
         }
     }
-    cp_async_commit();
-    // m/v rows of the owned vertices -> L2
-    constexpr int OROWS = DIM == 3 ? B * B : B;
-    const int nvx = min(B, A.s.res[0] - o[0]);
     for (int r = lane; r < OROWS; r += 32) {
         const int ly = r % B, lz = DIM == 3 ? r / B : 0;
         const int vy = o[1] + ly, vz = o[2] + lz;
         if (vy >= A.s.res[1] || (DIM == 3 && vz >= A.s.res[2])) continue;
-        const long long off = ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0]) * K * 4;
-        const unsigned bytes = (unsigned)(nvx * K * 4) & ~15u;
-        if ((off & 15) == 0 && bytes > 0) {
-            prefetch_l2(reinterpret_cast<const char*>(A.m_in) + off, bytes);
-            prefetch_l2(reinterpret_cast<const char*>(A.v_in) + off, bytes);
+        const long long v0 = (DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0];
+        const long long src = v0 * K * 4;
+        float* dm = mvs + r * B * K;
+        float* dv = mvs + S::NOWN * K + r * B * K;
+        if ((src & 15) == 0 && mv_bulk_ok) {
+            bulk_g2s(dm, reinterpret_cast<const char*>(A.m_in) + src, OBYTES, bar_mv);
+            bulk_g2s(dv, reinterpret_cast<const char*>(A.v_in) + src, OBYTES, bar_mv);
+        } else {
+            for (int q = 0; q < B * K; q += GR) {
+                const bool ok = o[0] + q / K < A.s.res[0];
+                cp_async<GR>(dm + q, ok ? A.m_in + v0 * K + q : A.m_in, ok);
+                cp_async<GR>(dv + q, ok ? A.v_in + v0 * K + q : A.v_in, ok);
+            }
         }
     }
+    cp_async_commit();
 }
 
 template <int DIM, int ORDER, bool EIK>
@@ -448,8 +470,9 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
     if (A.st->error) return;
 
     extern __shared__ __align__(128) float smem[];
-    float* tiles = smem;                          // 2 x tile
-    float* uni = smem + 2 * L::tile;              // cell-ordered records | Gs | p staging
+    float* tile = smem;                           // current parameters + halo
+    float* mvs = tile + L::tile;                  // m, v of the owned vertices
+    float* uni = mvs + L::mv;                     // cell-ordered records | Gs
     int* cnt = reinterpret_cast<int*>(uni + L::uni);
     int* start = cnt + S::NCELL;
     int* perm = start + S::NCELL;                 // thread -> owned vertex (load balance)
@@ -457,341 +480,287 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
     int* bstart = bhist + 64;
     __shared__ int warp_tot[32];
     __shared__ double red[4][NT / 32];
-    __shared__ __align__(8) unsigned long long bars[2];  // tile barrier per buffer
-    __shared__ int s_brick[2];
+    __shared__ __align__(8) unsigned long long bars[2];  // tile, mv
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     constexpr int NW = NT / 32;
-    const int NB = A.nb[0] * A.nb[1] * A.nb[2];
+    const int nbx = A.nb[0], nby = A.nb[1];
+    const int b = blockIdx.x;
+    const int o[3] = {(b % nbx) * B, ((b / nbx) % nby) * B, DIM == 3 ? (b / (nbx * nby)) * B : 0};
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         mbar_fence_init();
-        s_brick[0] = atomicAdd(A.work, 1);
     }
     __syncthreads();
-    int b = s_brick[0];
-    if (b < NB && warp == 0) {
-        int o0[3];
-        brick_origin<DIM>(A, b, o0);
-        stage_brick<DIM, ORDER>(A, o0, tiles, &bars[0], lane);
+    if (warp == 0) {
+        stage_brick<DIM, ORDER>(A, o, tile, mvs, &bars[0], &bars[1], lane);
+        mbar_wait(&bars[0], 0);  // one warp waits; the others park at the barrier
+        cp_async_wait<0>();      // fallback rows (rare: grid-edge bricks)
+    }
+    __syncthreads();
+
+    float G[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) G[q] = 0.0f;
+    double recon_sum = 0.0, eik_sum = 0.0, home_pts = 0.0;
+    int myv = tid;  // owned vertex of this thread; set per brick by the workload sort
+
+    const int p0 = A.off[b], p1 = A.off[b + 1];
+    for (int base = p0; base < p1; base += CH) {
+        const int m = min(CH, p1 - base);
+        for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
+        if (base == p0 && tid < 64) bhist[tid] = 0;
+        __syncthreads();
+        // 2a. forward from the tile, fp64 loss chain, cell rank
+        float rv[REC];
+        int ec = 0, rank = 0;
+        if (tid < m) {
+            const float4 q = A.binned[base + tid];
+            const float pf[3] = {q.x, q.y, q.z};
+            AxisF ax[DIM];
+            int tc[3] = {0, 0, 0};
+            bool home = true;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                double local;
+                const int c = locate_axis(A.s, a, (double)pf[a], local);
+                ax[a] = axis_factors(A.s, a, local);
+                tc[a] = c - (o[a] - 1);  // in [0, B]
+                home &= tc[a] >= 1;
+            }
+            float f = 0.0f, fg[DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                float cb[K];
+                load_block<K, false>(tile + L::at(tc[0] + (c & 1), tc[1] + ((c >> 1) & 1),
+                                                  DIM == 3 ? tc[2] + ((c >> 2) & 1) : 0),
+                                     cb);
+                blend_corner<DIM, ORDER, EIK>(cb, corner_geom<DIM>(A.s, ax, c), f, fg);
+            }
+            double recon, eik;
+            float u, gv[DIM];
+            point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
+            if (home) {
+                recon_sum += recon;
+                eik_sum += eik;
+                home_pts += 1.0;
+            }
+            ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
+            rank = atomicAdd(&cnt[ec], 1);
+            // s0/s1 rounded from fp64 (1 - l must not be formed from a rounded l)
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                rv[a] = ax[a].s0;
+                rv[DIM + a] = ax[a].s1;
+                rv[2 * DIM + 1 + a] = gv[a];
+            }
+            rv[2 * DIM] = u;
+#pragma unroll
+            for (int k2 = 3 * DIM + 1; k2 < REC; ++k2) rv[k2] = 0.0f;
+        }
+        __syncthreads();
+        block_excl_scan<S::NCELL, NT>(cnt, start, warp_tot);
+        __syncthreads();
+        if (tid < m) {  // records land in cell order
+            float2* dst = reinterpret_cast<float2*>(uni + (start[ec] + rank) * REC);
+#pragma unroll
+            for (int k2 = 0; k2 < REC / 2; ++k2) dst[k2] = make_float2(rv[2 * k2], rv[2 * k2 + 1]);
+        }
+        if (base == p0) {
+            // Load balance: sort the owned vertices by their (first-chunk)
+            // workload into 64 buckets so a warp's lanes carry similar loads;
+            // the mapping then holds for the brick (points are in random order).
+            const int v = tid;
+            const int l3[3] = {v % B, (v / B) % B, DIM == 3 ? v / (B * B) : 0};
+            const int e0 = DIM == 3 ? ((l3[2] + 1) * CE + l3[1] + 1) * CE + l3[0] + 1 : (l3[1] + 1) * CE + l3[0] + 1;
+            int wl = 0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                wl += cnt[e0 - (c & 1) - ((c >> 1) & 1) * CE - (DIM == 3 ? ((c >> 2) & 1) * CE * CE : 0)];
+            const int bk = 63 - min(wl, 63);  // heavy first
+            const int r2 = atomicAdd(&bhist[bk], 1);
+            __syncthreads();
+            if (warp == 0) {
+                const int h0 = bhist[lane], h1 = bhist[lane + 32];
+                int x0 = h0, x1 = h1;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int y0 = __shfl_up_sync(0xffffffffu, x0, off);
+                    const int y1 = __shfl_up_sync(0xffffffffu, x1, off);
+                    if (lane >= off) {
+                        x0 += y0;
+                        x1 += y1;
+                    }
+                }
+                const int tot0 = __shfl_sync(0xffffffffu, x0, 31);
+                bstart[lane] = x0 - h0;
+                bstart[lane + 32] = tot0 + x1 - h1;
+            }
+            __syncthreads();
+            perm[bstart[bk] + r2] = v;
+            __syncthreads();
+            myv = perm[tid];
+        } else {
+            __syncthreads();
+        }
+        // 2b. this thread's vertex gathers the points of its 2^D incident
+        //     cells, as one flattened loop over (corner, point)
+        {
+            const int l3[3] = {myv % B, (myv / B) % B, DIM == 3 ? myv / (B * B) : 0};
+            bool own_ok = true;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) own_ok &= (o[a] + l3[a]) < A.s.res[a];
+            const int e0 = DIM == 3 ? ((l3[2] + 1) * CE + l3[1] + 1) * CE + l3[0] + 1 : (l3[1] + 1) * CE + l3[0] + 1;
+            // non-empty incident cells as a bitmask; one flat loop over items,
+            // the next corner is found with ffs when a cell's run ends
+            unsigned mask = 0;
+            int total = 0;
+            if (own_ok) {
+#pragma unroll
+                for (int cc = 0; cc < NC; ++cc) {
+                    const int n = cnt[e0 - (cc & 1) - ((cc >> 1) & 1) * CE - (DIM == 3 ? ((cc >> 2) & 1) * CE * CE : 0)];
+                    total += n;
+                    mask |= (n > 0 ? 1u : 0u) << cc;
+                }
+            }
+            int c = 0, j = 0, jend = 0;
+            for (int k = 0; k < total; ++k) {
+                if (j == jend) {
+                    c = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const int e = e0 - (c & 1) - ((c >> 1) & 1) * CE - (DIM == 3 ? ((c >> 2) & 1) * CE * CE : 0);
+                    j = start[e];
+                    jend = j + cnt[e];
+                }
+                const float2* rp = reinterpret_cast<const float2*>(uni + j * REC);
+                float r[REC];
+#pragma unroll
+                for (int k2 = 0; k2 < REC / 2; ++k2) {
+                    const float2 t2 = rp[k2];
+                    r[2 * k2] = t2.x;
+                    r[2 * k2 + 1] = t2.y;
+                }
+                Corner<DIM> cg;
+                float sv[DIM];
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    const bool bit = (c >> a) & 1;
+                    const float s0 = r[a], s1 = r[DIM + a];
+                    sv[a] = bit ? s1 : s0;
+                    cg.d[a] = (bit ? -s0 : s1) * A.s.hf[a];  // (l - bit) * h
+                }
+                cg.w = sv[0];
+#pragma unroll
+                for (int a = 1; a < DIM; ++a) cg.w *= sv[a];
+                float gvd[DIM];
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    float other = 1.0f;
+#pragma unroll
+                    for (int bb = 0; bb < DIM; ++bb)
+                        if (bb != a) other *= sv[bb];
+                    cg.dw[a] = EIK ? (((c >> a) & 1) ? A.s.inv_hf[a] : -A.s.inv_hf[a]) * other : 0.0f;
+                    gvd[a] = EIK ? r[2 * DIM + 1 + a] : 0.0f;
+                }
+                corner_grad<DIM, ORDER, K>(cg, r[2 * DIM], gvd, G);
+                ++j;
+            }
+        }
+        __syncthreads();
     }
 
-    for (int it = 0; b < NB; ++it) {
-        const int sidx = it & 1;
-        float* tile = tiles + sidx * L::tile;
-        // claim the next brick and stage its tile into the other buffer
-        if (tid == 0) s_brick[(it + 1) & 1] = atomicAdd(A.work, 1);
-        __syncthreads();
-        const int bnext = s_brick[(it + 1) & 1];
-        int o[3];
-        brick_origin<DIM>(A, b, o);
-        if (warp == 0) {
-            if (bnext < NB) {
-                int on[3];
-                brick_origin<DIM>(A, bnext, on);
-                stage_brick<DIM, ORDER>(A, on, tiles + (sidx ^ 1) * L::tile, &bars[sidx ^ 1], lane);
-            } else {
-                cp_async_commit();  // empty group keeps wait_group<1> aligned
-            }
-            mbar_wait(&bars[sidx], (it >> 1) & 1);
-            cp_async_wait<1>();  // fallback rows of this brick (rare: grid-edge bricks)
-        }
-        __syncthreads();
-
-        float G[K];
+    // ---- 3. TV + Adam over the owned coefficients (flat float2 items) ----
+    float* Gs = uni;
 #pragma unroll
-        for (int q = 0; q < K; ++q) G[q] = 0.0f;
-        double recon_sum = 0.0, eik_sum = 0.0, home_pts = 0.0;
-        int myv = tid;
-
-        const int p0 = A.off[b], p1 = A.off[b + 1];
-        for (int base = p0; base < p1; base += CH) {
-            const int m = min(CH, p1 - base);
-            for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
-            if (base == p0 && tid < 64) bhist[tid] = 0;
-            __syncthreads();
-            // 2a. forward from the tile, fp64 loss chain, cell rank
-            float rv[REC];
-            int ec = 0, rank = 0;
-            if (tid < m) {
-                const float4 q = A.binned[base + tid];
-                const float pf[3] = {q.x, q.y, q.z};
-                AxisF ax[DIM];
-                int tc[3] = {0, 0, 0};
-                bool home = true;
+    for (int q = 0; q < K; ++q) Gs[myv * K + q] = G[q];
+    if (warp == 0) mbar_wait(&bars[1], 0);  // m/v rows landed
+    __syncthreads();
+    double tv_sum = 0.0;
+    {
+        const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
+        float* __restrict__ p_out = A.p_out;
+        float* __restrict__ m_out = A.m_out;
+        float* __restrict__ v_out = A.v_out;
+        constexpr int OROWS = DIM == 3 ? B * B : B;
+        constexpr int ROWF = B * K;      // floats per owned row
+        constexpr int W = K % 2 == 0 ? 2 : 1;
+        constexpr int ROWI = ROWF / W;   // items per row
+        constexpr int TY = L::TROWF, TZ = DIM == 3 ? T * L::TROWF : 0;
+        for (int it = tid; it < OROWS * ROWI; it += NT) {
+            const int r = it / ROWI, j = (it - r * ROWI) * W;
+            const int ly = r % B, lz = DIM == 3 ? r / B : 0;
+            const int gy = o[1] + ly, gz = o[2] + lz;
+            const int lx = j / K;
+            const int gx = o[0] + lx;
+            if (gx >= A.s.res[0] || gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
+            const int e = r * ROWF + j;
+            const float* tp = tile + L::at(1 + lx, ly + 1, DIM == 3 ? lz + 1 : 0) + (j - lx * K);
+            float pv[W], gt[W];
+#pragma unroll
+            for (int w2 = 0; w2 < W; ++w2) {
+                pv[w2] = tp[w2];
+                gt[w2] = 0.0f;
+            }
+            if (A.want_tv) {
+                // pairs (v, v+e_a) owned here feed the TV sum; both ends'
+                // terms feed this vertex's gradient (sdf_loss.cpp:155-257)
+                const int offs[3] = {K, TY, TZ};
+                const bool hi3[3] = {gx + 1 < A.s.res[0], gy + 1 < A.s.res[1], DIM == 3 && gz + 1 < A.s.res[2]};
+                const bool lo3[3] = {gx >= 1, gy >= 1, DIM == 3 && gz >= 1};
+                float sq = 0.0f;
 #pragma unroll
                 for (int a = 0; a < DIM; ++a) {
-                    double local;
-                    const int c = locate_axis(A.s, a, (double)pf[a], local);
-                    ax[a] = axis_factors(A.s, a, local);
-                    tc[a] = c - (o[a] - 1);  // in [0, B]
-                    home &= tc[a] >= 1;
-                }
-                float f = 0.0f, fg[DIM];
 #pragma unroll
-                for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    float cb[K];
-                    load_block<K, false>(tile + L::at(tc[0] + (c & 1), tc[1] + ((c >> 1) & 1),
-                                                      DIM == 3 ? tc[2] + ((c >> 2) & 1) : 0),
-                                         cb);
-                    blend_corner<DIM, ORDER, EIK>(cb, corner_geom<DIM>(A.s, ax, c), f, fg);
-                }
-                double recon, eik;
-                float u, gv[DIM];
-                point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
-                if (home) {
-                    recon_sum += recon;
-                    eik_sum += eik;
-                    home_pts += 1.0;
-                }
-                ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
-                rank = atomicAdd(&cnt[ec], 1);
-                // s0/s1 rounded from fp64 (1 - l must not be formed from a rounded l)
-#pragma unroll
-                for (int a = 0; a < DIM; ++a) {
-                    rv[a] = ax[a].s0;
-                    rv[DIM + a] = ax[a].s1;
-                    rv[2 * DIM + 1 + a] = gv[a];
-                }
-                rv[2 * DIM] = u;
-#pragma unroll
-                for (int k2 = 3 * DIM + 1; k2 < REC; ++k2) rv[k2] = 0.0f;
-            }
-            __syncthreads();
-            block_excl_scan<S::NCELL, NT>(cnt, start, warp_tot);
-            __syncthreads();
-            if (tid < m) {  // records land in cell order
-                float2* dst = reinterpret_cast<float2*>(uni + (start[ec] + rank) * REC);
-#pragma unroll
-                for (int k2 = 0; k2 < REC / 2; ++k2) dst[k2] = make_float2(rv[2 * k2], rv[2 * k2 + 1]);
-            }
-            if (base == p0) {
-                // Load balance: sort the owned vertices by their (first-chunk)
-                // workload into 64 buckets so a warp's lanes carry similar
-                // loads; the mapping holds for the brick (points are in random
-                // order within a bin).
-                const int v = tid;
-                const int l3[3] = {v % B, (v / B) % B, DIM == 3 ? v / (B * B) : 0};
-                const int e0 = DIM == 3 ? ((l3[2] + 1) * CE + l3[1] + 1) * CE + l3[0] + 1 : (l3[1] + 1) * CE + l3[0] + 1;
-                int wl = 0;
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-                    wl += cnt[e0 - (c & 1) - ((c >> 1) & 1) * CE - (DIM == 3 ? ((c >> 2) & 1) * CE * CE : 0)];
-                const int bk = 63 - min(wl, 63);  // heavy first
-                const int r2 = atomicAdd(&bhist[bk], 1);
-                __syncthreads();
-                if (warp == 0) {
-                    const int h0 = bhist[lane], h1 = bhist[lane + 32];
-                    int x0 = h0, x1 = h1;
-#pragma unroll
-                    for (int off = 1; off < 32; off <<= 1) {
-                        const int y0 = __shfl_up_sync(0xffffffffu, x0, off);
-                        const int y1 = __shfl_up_sync(0xffffffffu, x1, off);
-                        if (lane >= off) {
-                            x0 += y0;
-                            x1 += y1;
-                        }
-                    }
-                    const int tot0 = __shfl_sync(0xffffffffu, x0, 31);
-                    bstart[lane] = x0 - h0;
-                    bstart[lane + 32] = tot0 + x1 - h1;
-                }
-                __syncthreads();
-                perm[bstart[bk] + r2] = v;
-                __syncthreads();
-                myv = perm[tid];
-            } else {
-                __syncthreads();
-            }
-            // 2b. this thread's vertex gathers the points of its 2^D incident
-            //     cells, as one flattened loop over (corner, point)
-            {
-                const int l3[3] = {myv % B, (myv / B) % B, DIM == 3 ? myv / (B * B) : 0};
-                bool own_ok = true;
-#pragma unroll
-                for (int a = 0; a < DIM; ++a) own_ok &= (o[a] + l3[a]) < A.s.res[a];
-                const int e0 = DIM == 3 ? ((l3[2] + 1) * CE + l3[1] + 1) * CE + l3[0] + 1 : (l3[1] + 1) * CE + l3[0] + 1;
-                // non-empty incident cells as a bitmask; the next corner is
-                // found with ffs when a cell's run ends
-                unsigned mask = 0;
-                int total = 0;
-                if (own_ok) {
-#pragma unroll
-                    for (int cc = 0; cc < NC; ++cc) {
-                        const int n = cnt[e0 - (cc & 1) - ((cc >> 1) & 1) * CE - (DIM == 3 ? ((cc >> 2) & 1) * CE * CE : 0)];
-                        total += n;
-                        mask |= (n > 0 ? 1u : 0u) << cc;
-                    }
-                }
-                int c = 0, j = 0, jend = 0;
-                for (int k = 0; k < total; ++k) {
-                    if (j == jend) {
-                        c = __ffs(mask) - 1;
-                        mask &= mask - 1;
-                        const int e = e0 - (c & 1) - ((c >> 1) & 1) * CE - (DIM == 3 ? ((c >> 2) & 1) * CE * CE : 0);
-                        j = start[e];
-                        jend = j + cnt[e];
-                    }
-                    const float2* rp = reinterpret_cast<const float2*>(uni + j * REC);
-                    float r[REC];
-#pragma unroll
-                    for (int k2 = 0; k2 < REC / 2; ++k2) {
-                        const float2 t2 = rp[k2];
-                        r[2 * k2] = t2.x;
-                        r[2 * k2 + 1] = t2.y;
-                    }
-                    Corner<DIM> cg;
-                    float sv[DIM];
-#pragma unroll
-                    for (int a = 0; a < DIM; ++a) {
-                        const bool bit = (c >> a) & 1;
-                        const float s0 = r[a], s1 = r[DIM + a];
-                        sv[a] = bit ? s1 : s0;
-                        cg.d[a] = (bit ? -s0 : s1) * A.s.hf[a];  // (l - bit) * h
-                    }
-                    cg.w = sv[0];
-#pragma unroll
-                    for (int a = 1; a < DIM; ++a) cg.w *= sv[a];
-                    float gvd[DIM];
-#pragma unroll
-                    for (int a = 0; a < DIM; ++a) {
-                        float other = 1.0f;
-#pragma unroll
-                        for (int bb = 0; bb < DIM; ++bb)
-                            if (bb != a) other *= sv[bb];
-                        cg.dw[a] = EIK ? (((c >> a) & 1) ? A.s.inv_hf[a] : -A.s.inv_hf[a]) * other : 0.0f;
-                        gvd[a] = EIK ? r[2 * DIM + 1 + a] : 0.0f;
-                    }
-                    corner_grad<DIM, ORDER, K>(cg, r[2 * DIM], gvd, G);
-                    ++j;
-                }
-            }
-            __syncthreads();
-        }
-
-        // ---- 3. TV + Adam, thread per vertex; outputs staged in smem ----
-        float* Gs = uni;
-#pragma unroll
-        for (int q = 0; q < K; ++q) Gs[myv * K + q] = G[q];
-        __syncthreads();
-        double tv_sum = 0.0;
-        const int v = tid;
-        const int l3[3] = {v % B, (v / B) % B, DIM == 3 ? v / (B * B) : 0};
-        const int g3[3] = {o[0] + l3[0], o[1] + l3[1], o[2] + l3[2]};
-        bool vok = true;
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) vok &= g3[a] < A.s.res[a];
-        const long long gidx = ((DIM == 3 ? (long long)g3[2] * A.s.sz : 0LL) + (long long)g3[1] * A.s.sy + g3[0]) * K;
-        const float* tp = tile + L::at(1 + l3[0], 1 + l3[1], DIM == 3 ? 1 + l3[2] : 0);
-        // 3a. full gradient (points + TV stencil) in place in Gs
-        if (vok) {
-            constexpr int offs[3] = {K, L::TROWF, DIM == 3 ? T * L::TROWF : 0};
-            float sq = 0.0f;
-            bool finite = true;
-#pragma unroll
-            for (int q = 0; q < K; ++q) {
-                const float pv = tp[q];
-                float gt = 0.0f;
-                if (A.want_tv) {
-                    // pairs (v, v+e_a) owned here feed the TV sum; both ends'
-                    // terms feed this vertex's gradient (sdf_loss.cpp:155-257)
-#pragma unroll
-                    for (int a = 0; a < DIM; ++a) {
-                        if (g3[a] + 1 < A.s.res[a]) {
-                            const float d = tp[offs[a] + q] - pv;
+                    for (int w2 = 0; w2 < W; ++w2) {
+                        if (hi3[a]) {
+                            const float d = tp[offs[a] + w2] - pv[w2];
                             sq = fmaf(d, d, sq);
-                            gt -= d;
+                            gt[w2] -= d;
                         }
-                        if (g3[a] >= 1) gt += pv - tp[q - offs[a]];
+                        if (lo3[a]) gt[w2] += pv[w2] - tp[w2 - offs[a]];
                     }
                 }
-                const float gi = fmaf(A.tv_gscale, gt, Gs[v * K + q]);
-                Gs[v * K + q] = gi;
-                finite &= isfinite(gi);
-                if (A.grad_out) A.grad_out[gidx + q] = gi;
+                tv_sum += (double)sq;
             }
-            tv_sum = (double)sq;
-            if (!finite) {
-                for (int q = 0; q < K; ++q)
-                    if (!isfinite(Gs[v * K + q])) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
-            }
-        }
-        // 3b. own parameters into registers, then the tile becomes staging
-        float pv[K];
-        if (vok) {
+            const long long gidx = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K + j;
+            float pn[W], mn[W], vn[W];
 #pragma unroll
-            for (int q = 0; q < K; ++q) pv[q] = tp[q];
+            for (int w2 = 0; w2 < W; ++w2) {
+                const float gi = fmaf(A.tv_gscale, gt[w2], Gs[e + w2]);
+                if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + w2));
+                if (A.grad_out) A.grad_out[gidx + w2] = gi;
+                mn[w2] = fmaf(A.b1, mvs[e + w2], c1 * gi);
+                vn[w2] = fmaf(A.b2, mvs[S::NOWN * K + e + w2], c2 * gi * gi);
+                pn[w2] = pv[w2] - lr_bc1 * mn[w2] * fast_rcp(fast_sqrt(vn[w2] * A.inv_bc2) + A.eps);
+            }
+            if constexpr (W == 2) {
+                *reinterpret_cast<float2*>(m_out + gidx) = make_float2(mn[0], mn[1]);
+                *reinterpret_cast<float2*>(v_out + gidx) = make_float2(vn[0], vn[1]);
+                *reinterpret_cast<float2*>(p_out + gidx) = make_float2(pn[0], pn[1]);
+            } else {
+                m_out[gidx] = mn[0];
+                v_out[gidx] = vn[0];
+                p_out[gidx] = pn[0];
+            }
         }
+    }
+
+    // ---- per-brick loss partials (fixed-order block reduction) ----
+    {
+        const double v4[4] = {warp_sum_d(recon_sum), warp_sum_d(eik_sum), warp_sum_d(tv_sum), warp_sum_d(home_pts)};
+        if (lane == 0)
+            for (int k2 = 0; k2 < 4; ++k2) red[k2][warp] = v4[k2];
         __syncthreads();
-        // 3c. Adam (adam.cpp:36-55), fp32 state, host fp64 bias corrections;
-        //     moments read from L2 (bulk-prefetched with the tile)
-        if (vok) {
-            constexpr int W = K % 2 == 0 ? 2 : 1;
-            const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
-#pragma unroll
-            for (int q = 0; q < K; q += W) {
-                float mo[W], vo[W];
-                if constexpr (W == 2) {
-                    const float2 a2 = __ldg(reinterpret_cast<const float2*>(A.m_in + gidx + q));
-                    const float2 b2 = __ldg(reinterpret_cast<const float2*>(A.v_in + gidx + q));
-                    mo[0] = a2.x; mo[1] = a2.y;
-                    vo[0] = b2.x; vo[1] = b2.y;
-                } else {
-                    mo[0] = __ldg(A.m_in + gidx + q);
-                    vo[0] = __ldg(A.v_in + gidx + q);
-                }
-#pragma unroll
-                for (int w2 = 0; w2 < W; ++w2) {
-                    const float gi = Gs[v * K + q + w2];
-                    const float mn = fmaf(A.b1, mo[w2], c1 * gi);
-                    const float vn = fmaf(A.b2, vo[w2], c2 * gi * gi);
-                    uni[v * K + q + w2] = pv[q + w2] - lr_bc1 * mn * fast_rcp(fast_sqrt(vn * A.inv_bc2) + A.eps);
-                    tile[v * K + q + w2] = mn;
-                    tile[S::NOWN * K + v * K + q + w2] = vn;
-                }
-            }
+        if (tid < 4) {
+            double acc = 0.0;
+            for (int k2 = 0; k2 < NW; ++k2) acc += red[tid][k2];
+            A.partials[4 * b + tid] = acc;
         }
-        __syncthreads();
-        // coalesced row stores (warp per owned row, 16-byte vectors when aligned)
-        {
-            constexpr int OROWS = DIM == 3 ? B * B : B;
-            constexpr int ROWF = B * K;
-            const int nvx = min(B, A.s.res[0] - o[0]);
-            const int rowf = nvx * K;
-            for (int t = warp; t < 3 * OROWS; t += NW) {
-                const int which = t / OROWS, r = t - which * OROWS;
-                const int ly = r % B, lz = DIM == 3 ? r / B : 0;
-                const int gy = o[1] + ly, gz = o[2] + lz;
-                if (gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
-                const long long gb = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K;
-                const float* src = which == 0 ? uni + r * ROWF : tile + (which - 1) * S::NOWN * K + r * ROWF;
-                float* dst = which == 0 ? A.p_out + gb : (which == 1 ? A.m_out + gb : A.v_out + gb);
-                if ((gb & 3) == 0 && (rowf & 3) == 0) {
-                    for (int q = lane * 4; q < rowf; q += 128)
-                        *reinterpret_cast<float4*>(dst + q) = *reinterpret_cast<const float4*>(src + q);
-                } else {
-                    for (int q = lane; q < rowf; q += 32) dst[q] = src[q];
-                }
-            }
-        }
-        // per-brick loss partials (fixed-order block reduction)
-        {
-            const double v4[4] = {warp_sum_d(recon_sum), warp_sum_d(eik_sum), warp_sum_d(tv_sum), warp_sum_d(home_pts)};
-            if (lane == 0)
-                for (int k2 = 0; k2 < 4; ++k2) red[k2][warp] = v4[k2];
-            __syncthreads();
-            if (tid < 4) {
-                double acc = 0.0;
-                for (int k2 = 0; k2 < NW; ++k2) acc += red[tid][k2];
-                A.partials[4 * b + tid] = acc;
-            }
-        }
-        b = bnext;
     }
 }
 
@@ -882,8 +851,9 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     B.cursor = g.bin_cursor;
     B.binned = g.binned;
     B.st = g.st;
-    if (g.NB <= kBinSmemMax) {
-        const int ncta = (int)((n + kBinTile - 1) / kBinTile);
+    const int ncta_tiles = (int)((n + kBinTile - 1) / kBinTile);
+    if (g.NB <= kBinSmemMax && ncta_tiles <= kMaxBinTiles) {
+        const int ncta = ncta_tiles;
         ensure_bin_hist(g, (int64_t)ncta * g.NB);
         const size_t sm = sizeof(int) * g.NB;
         if (g.spec.dim == 3) {
@@ -895,8 +865,11 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
             TGCU_CUDA(cudaFuncSetAttribute(k_bin_scatter_tiles<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kBinSmemMax)));
             k_bin_hist<2><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, (int)g.NB);
         }
-        k_bin_cols<<<(unsigned)((g.NB * 32 + 255) / 256), 256, 0, s>>>(g.bin_hist, ncta, (int)g.NB, g.bin_count, g.st);
-        k_bin_scan<<<1, 1024, 0, s>>>(g.bin_count, g.bin_off, g.bin_cursor, (int)g.NB, g.st, g.bin_count + g.NB);
+        const size_t csm = sizeof(int) * ncta * (kColBricks + 1);
+        TGCU_CUDA(cudaFuncSetAttribute(k_bin_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int) * kMaxBinTiles * (kColBricks + 1))));
+        k_bin_cols<<<(unsigned)((g.NB + kColBricks - 1) / kColBricks), 256, csm, s>>>(g.bin_hist, ncta, (int)g.NB,
+                                                                                      g.bin_count, g.st);
+        k_bin_scan<<<1, 1024, 0, s>>>(g.bin_count, g.bin_off, g.bin_cursor, (int)g.NB, g.st);
         if (g.spec.dim == 3) k_bin_scatter_tiles<3><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_off, (int)g.NB);
         else k_bin_scatter_tiles<2><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_off, (int)g.NB);
         count_launch(4);
@@ -905,7 +878,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
         const int pblocks = grid_blocks(n, 256, 148 * 16);
         if (g.spec.dim == 3) k_bin_count<3><<<pblocks, 256, 0, s>>>(B);
         else k_bin_count<2><<<pblocks, 256, 0, s>>>(B);
-        k_bin_scan<<<1, 1024, 0, s>>>(g.bin_count, g.bin_off, g.bin_cursor, (int)g.NB, g.st, g.bin_count + g.NB);
+        k_bin_scan<<<1, 1024, 0, s>>>(g.bin_count, g.bin_off, g.bin_cursor, (int)g.NB, g.st);
         if (g.spec.dim == 3) k_bin_scatter<3><<<pblocks, 256, 0, s>>>(B);
         else k_bin_scatter<2><<<pblocks, 256, 0, s>>>(B);
         count_launch(3);
@@ -948,7 +921,6 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     A.partials = g.partials;
     A.st = g.st;
     A.grad_out = grad_out;
-    A.work = g.bin_count + g.NB;
     const bool eik = cfg.lambda1 > 0.0;
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
         constexpr size_t smem = BrickSmem<DIM, ORDER>::bytes;
@@ -963,10 +935,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
             configured = true;
         }
         if (g.prof_on) prof_mark(g, s, 0);
-        int nsm = 148;
-        TGCU_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g.device));
-        const unsigned ctas = (unsigned)std::min<long long>(2LL * nsm, g.NB);  // persistent, 2 per SM
-        kern<<<ctas, BrickShape<DIM>::NT, smem, s>>>(A);
+        kern<<<(unsigned)g.NB, BrickShape<DIM>::NT, smem, s>>>(A);
         if (g.prof_on) prof_mark(g, s, 1);
     });
 
