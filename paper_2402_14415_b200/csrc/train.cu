@@ -495,12 +495,9 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
         mbar_fence_init();
     }
     __syncthreads();
-    if (warp == 0) {
-        stage_brick<DIM, ORDER>(A, o, tile, mvs, &bars[0], &bars[1], lane);
-        mbar_wait(&bars[0], 0);  // one warp waits; the others park at the barrier
-        cp_async_wait<0>();      // fallback rows (rare: grid-edge bricks)
-    }
-    __syncthreads();
+    // The tile is waited for inside the first chunk, after the points have
+    // been loaded, located and counted (none of which needs it).
+    if (warp == 0) stage_brick<DIM, ORDER>(A, o, tile, mvs, &bars[0], &bars[1], lane);
 
     float G[K];
 #pragma unroll
@@ -514,23 +511,37 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
         for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
         if (base == p0 && tid < 64) bhist[tid] = 0;
         __syncthreads();
-        // 2a. forward from the tile, fp64 loss chain, cell rank
+        // 2a. locate + cell rank (no tile needed), then forward from the tile
+        //     and the fp64 loss chain
         float rv[REC];
         int ec = 0, rank = 0;
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        AxisF ax[DIM];
+        int tc[3] = {0, 0, 0};
         if (tid < m) {
-            const float4 q = A.binned[base + tid];
+            q = A.binned[base + tid];
             const float pf[3] = {q.x, q.y, q.z};
-            AxisF ax[DIM];
-            int tc[3] = {0, 0, 0};
-            bool home = true;
 #pragma unroll
             for (int a = 0; a < DIM; ++a) {
                 double local;
                 const int c = locate_axis(A.s, a, (double)pf[a], local);
                 ax[a] = axis_factors(A.s, a, local);
                 tc[a] = c - (o[a] - 1);  // in [0, B]
-                home &= tc[a] >= 1;
             }
+            ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
+            rank = atomicAdd(&cnt[ec], 1);
+        }
+        if (base == p0) {
+            if (warp == 0) {
+                mbar_wait(&bars[0], 0);  // one warp waits; the others park at the barrier
+                cp_async_wait<0>();      // fallback rows (rare: grid-edge bricks)
+            }
+            __syncthreads();
+        }
+        if (tid < m) {
+            bool home = true;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) home &= tc[a] >= 1;
             float f = 0.0f, fg[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
@@ -550,8 +561,6 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
                 eik_sum += eik;
                 home_pts += 1.0;
             }
-            ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
-            rank = atomicAdd(&cnt[ec], 1);
             // s0/s1 rounded from fp64 (1 - l must not be formed from a rounded l)
 #pragma unroll
             for (int a = 0; a < DIM; ++a) {
@@ -674,78 +683,100 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
         __syncthreads();
     }
 
-    // ---- 3. TV + Adam over the owned coefficients (flat float2 items) ----
+    // ---- 3. TV + Adam, thread per vertex; results staged in place ----
     float* Gs = uni;
 #pragma unroll
     for (int q = 0; q < K; ++q) Gs[myv * K + q] = G[q];
+    if (p0 == p1 && warp == 0) {  // brick without points: the tile was never waited for
+        mbar_wait(&bars[0], 0);
+        cp_async_wait<0>();
+    }
     if (warp == 0) mbar_wait(&bars[1], 0);  // m/v rows landed
     __syncthreads();
     double tv_sum = 0.0;
     {
-        const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
-        float* __restrict__ p_out = A.p_out;
-        float* __restrict__ m_out = A.m_out;
-        float* __restrict__ v_out = A.v_out;
-        constexpr int OROWS = DIM == 3 ? B * B : B;
-        constexpr int ROWF = B * K;      // floats per owned row
-        constexpr int W = K % 2 == 0 ? 2 : 1;
-        constexpr int ROWI = ROWF / W;   // items per row
-        constexpr int TY = L::TROWF, TZ = DIM == 3 ? T * L::TROWF : 0;
-        for (int it = tid; it < OROWS * ROWI; it += NT) {
-            const int r = it / ROWI, j = (it - r * ROWI) * W;
-            const int ly = r % B, lz = DIM == 3 ? r / B : 0;
-            const int gy = o[1] + ly, gz = o[2] + lz;
-            const int lx = j / K;
-            const int gx = o[0] + lx;
-            if (gx >= A.s.res[0] || gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
-            const int e = r * ROWF + j;
-            const float* tp = tile + L::at(1 + lx, ly + 1, DIM == 3 ? lz + 1 : 0) + (j - lx * K);
-            float pv[W], gt[W];
+        const int v = tid;
+        const int l3[3] = {v % B, (v / B) % B, DIM == 3 ? v / (B * B) : 0};
+        const int g3[3] = {o[0] + l3[0], o[1] + l3[1], o[2] + l3[2]};
+        bool vok = true;
 #pragma unroll
-            for (int w2 = 0; w2 < W; ++w2) {
-                pv[w2] = tp[w2];
-                gt[w2] = 0.0f;
-            }
-            if (A.want_tv) {
-                // pairs (v, v+e_a) owned here feed the TV sum; both ends'
-                // terms feed this vertex's gradient (sdf_loss.cpp:155-257)
-                const int offs[3] = {K, TY, TZ};
-                const bool hi3[3] = {gx + 1 < A.s.res[0], gy + 1 < A.s.res[1], DIM == 3 && gz + 1 < A.s.res[2]};
-                const bool lo3[3] = {gx >= 1, gy >= 1, DIM == 3 && gz >= 1};
-                float sq = 0.0f;
+        for (int a = 0; a < DIM; ++a) vok &= g3[a] < A.s.res[a];
+        if (vok) {
+            const long long gidx =
+                ((DIM == 3 ? (long long)g3[2] * A.s.sz : 0LL) + (long long)g3[1] * A.s.sy + g3[0]) * K;
+            const float* tp = tile + L::at(1 + l3[0], 1 + l3[1], DIM == 3 ? 1 + l3[2] : 0);
+            float* gs = Gs + v * K;
+            float* mm = mvs + v * K;
+            float* vv = mvs + S::NOWN * K + v * K;
+            constexpr int offs[3] = {K, L::TROWF, DIM == 3 ? T * L::TROWF : 0};
+            const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
+            float sq = 0.0f;
+            bool finite = true;
 #pragma unroll
-                for (int a = 0; a < DIM; ++a) {
+            for (int q = 0; q < K; ++q) {
+                const float pv = tp[q];
+                float gt = 0.0f;
+                if (A.want_tv) {
+                    // pairs (v, v+e_a) owned here feed the TV sum; both ends'
+                    // terms feed this vertex's gradient (sdf_loss.cpp:155-257)
 #pragma unroll
-                    for (int w2 = 0; w2 < W; ++w2) {
-                        if (hi3[a]) {
-                            const float d = tp[offs[a] + w2] - pv[w2];
+                    for (int a = 0; a < DIM; ++a) {
+                        if (g3[a] + 1 < A.s.res[a]) {
+                            const float d = tp[offs[a] + q] - pv;
                             sq = fmaf(d, d, sq);
-                            gt[w2] -= d;
+                            gt -= d;
                         }
-                        if (lo3[a]) gt[w2] += pv[w2] - tp[w2 - offs[a]];
+                        if (g3[a] >= 1) gt += pv - tp[q - offs[a]];
                     }
                 }
-                tv_sum += (double)sq;
+                const float gi = fmaf(A.tv_gscale, gt, gs[q]);
+                finite &= isfinite(gi);
+                if (A.grad_out) A.grad_out[gidx + q] = gi;
+                // Adam (adam.cpp:36-55), fp32 state, host fp64 bias corrections
+                const float mn = fmaf(A.b1, mm[q], c1 * gi);
+                const float vn = fmaf(A.b2, vv[q], c2 * gi * gi);
+                mm[q] = mn;
+                vv[q] = vn;
+                gs[q] = pv - lr_bc1 * mn * fast_rcp(fast_sqrt(vn * A.inv_bc2) + A.eps);
+                if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
             }
-            const long long gidx = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K + j;
-            float pn[W], mn[W], vn[W];
-#pragma unroll
-            for (int w2 = 0; w2 < W; ++w2) {
-                const float gi = fmaf(A.tv_gscale, gt[w2], Gs[e + w2]);
-                if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + w2));
-                if (A.grad_out) A.grad_out[gidx + w2] = gi;
-                mn[w2] = fmaf(A.b1, mvs[e + w2], c1 * gi);
-                vn[w2] = fmaf(A.b2, mvs[S::NOWN * K + e + w2], c2 * gi * gi);
-                pn[w2] = pv[w2] - lr_bc1 * mn[w2] * fast_rcp(fast_sqrt(vn[w2] * A.inv_bc2) + A.eps);
+            (void)finite;
+            tv_sum = (double)sq;
+        }
+    }
+    __syncthreads();
+    // coalesced copy-out of the staged rows (p from Gs, m and v from mvs)
+    {
+        constexpr int OROWS = DIM == 3 ? B * B : B;
+        constexpr int ROWF = B * K;
+        const int nvx = min(B, A.s.res[0] - o[0]);
+        const int rowf = nvx * K;
+        if (rowf == ROWF && (ROWF % 4) == 0 && ((A.s.sy * K) % 4) == 0 && ((o[0] * K) % 4) == 0) {
+            constexpr int RV = ROWF / 4;  // float4 per row
+            for (int i = tid; i < 3 * OROWS * RV; i += NT) {
+                const int which = i / (OROWS * RV);
+                const int i2 = i - which * OROWS * RV;
+                const int r = i2 / RV, c4 = i2 - r * RV;
+                const int ly = r % B, lz = DIM == 3 ? r / B : 0;
+                const int gy = o[1] + ly, gz = o[2] + lz;
+                if (gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
+                const long long gb = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K;
+                const float* src = (which == 0 ? uni : mvs + (which - 1) * S::NOWN * K) + r * ROWF + 4 * c4;
+                float* dst = (which == 0 ? A.p_out : (which == 1 ? A.m_out : A.v_out)) + gb + 4 * c4;
+                *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
             }
-            if constexpr (W == 2) {
-                *reinterpret_cast<float2*>(m_out + gidx) = make_float2(mn[0], mn[1]);
-                *reinterpret_cast<float2*>(v_out + gidx) = make_float2(vn[0], vn[1]);
-                *reinterpret_cast<float2*>(p_out + gidx) = make_float2(pn[0], pn[1]);
-            } else {
-                m_out[gidx] = mn[0];
-                v_out[gidx] = vn[0];
-                p_out[gidx] = pn[0];
+        } else {
+            for (int i = tid; i < 3 * OROWS * ROWF; i += NT) {
+                const int which = i / (OROWS * ROWF);
+                const int i2 = i - which * OROWS * ROWF;
+                const int r = i2 / ROWF, c1 = i2 - r * ROWF;
+                const int ly = r % B, lz = DIM == 3 ? r / B : 0;
+                const int gy = o[1] + ly, gz = o[2] + lz;
+                if (c1 >= rowf || gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
+                const long long gb = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K;
+                const float* src = (which == 0 ? uni : mvs + (which - 1) * S::NOWN * K) + r * ROWF + c1;
+                float* dst = (which == 0 ? A.p_out : (which == 1 ? A.m_out : A.v_out)) + gb + c1;
+                *dst = *src;
             }
         }
     }
