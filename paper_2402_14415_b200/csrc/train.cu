@@ -379,86 +379,85 @@ struct BrickSmem {
     }
 };
 
-// Issue the HBM->smem copies of brick `b` (warp 0): one TMA bulk copy per
-// HBM row (tile rows -> bar_tile, owned m/v rows -> bar_mv); rows that are not
-// 16-byte aligned or would read outside the array fall back to cp.async.
+// HBM->smem staging of a brick, one row per thread: tile rows (threads
+// [0, TROWS)) -> bar_tile, owned m/v rows (the next 2*OROWS threads) ->
+// bar_mv, each as one TMA bulk copy. Both barriers expect an arrival from
+// every thread (arrive.expect_tx with the thread's own byte count, 0 if it
+// has no row), so no reduction is needed. Rows that are not 16-byte aligned
+// or would read outside the array fall back to cp.async by the same thread.
 template <int DIM, int ORDER>
 __device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, float* tile, float* mvs,
-                                            unsigned long long* bar_tile, unsigned long long* bar_mv, int lane) {
+                                            unsigned long long* bar_tile, unsigned long long* bar_mv, int tid) {
     using S = BrickShape<DIM>;
     using L = BrickSmem<DIM, ORDER>;
     constexpr int K = L::K, B = S::B, T = S::T;
     constexpr int GR = (K % 2 == 0) ? 2 : 1;
-    const long long nc_bytes = (long long)A.s.res[0] * A.s.res[1] * (DIM == 3 ? A.s.res[2] : 1) * K * 4;
     constexpr unsigned TBYTES = ((L::SHF * 4 + T * K * 4 + 15) / 16) * 16;
     constexpr unsigned OBYTES = B * K * 4;
     constexpr int OROWS = DIM == 3 ? B * B : B;
-    const bool mv_bulk_ok = (OBYTES % 16) == 0 && o[0] + B <= A.s.res[0];
-    unsigned tx_bytes = 0, mv_bytes = 0;
-    for (int r = lane; r < L::TROWS; r += 32) {
+    static_assert(L::TROWS + 2 * OROWS <= S::NT, "one staging row per thread");
+    const long long nc_bytes = (long long)A.s.res[0] * A.s.res[1] * (DIM == 3 ? A.s.res[2] : 1) * K * 4;
+    unsigned tx_tile = 0, tx_mv = 0;
+    if (tid < L::TROWS) {
+        const int r = tid;
         const int ty = DIM == 3 ? r % T : r, tz = DIM == 3 ? r / T : 0;
         const int vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
-        if (vy < 0 || vy >= A.s.res[1] || (DIM == 3 && (vz < 0 || vz >= A.s.res[2]))) continue;
-        const long long src =
-            ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0] - 1) * K * 4 - L::SHF * 4;
-        if ((src & 15) == 0 && src >= 0 && src + TBYTES <= nc_bytes) tx_bytes += TBYTES;
-    }
-    for (int r = lane; r < OROWS; r += 32) {
+        if (vy >= 0 && vy < A.s.res[1] && (DIM == 2 || (vz >= 0 && vz < A.s.res[2]))) {
+            const long long firstv = (DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0] - 1;
+            const long long src = firstv * K * 4 - L::SHF * 4;
+            float* dst = tile + r * L::TROWF;
+            if ((src & 15) == 0 && src >= 0 && src + TBYTES <= nc_bytes) {
+                tx_tile = TBYTES;
+                mbar_expect_tx(bar_tile, TBYTES);
+                bulk_g2s(dst, reinterpret_cast<const char*>(A.p_in) + src, TBYTES, bar_tile);
+            } else {
+                mbar_expect_tx(bar_tile, 0);
+                for (int q = 0; q < T * K; q += GR) {
+                    const int vx = o[0] - 1 + q / K;
+                    const bool ok = vx >= 0 && vx < A.s.res[0];
+                    cp_async<GR>(dst + L::SHF + q, ok ? A.p_in + firstv * K + q : A.p_in, ok);
+                }
+            }
+        }
+    } else if (tid < L::TROWS + 2 * OROWS) {
+        const int t = tid - L::TROWS;
+        const int which = t / OROWS, r = t - which * OROWS;
         const int ly = r % B, lz = DIM == 3 ? r / B : 0;
         const int vy = o[1] + ly, vz = o[2] + lz;
-        if (vy >= A.s.res[1] || (DIM == 3 && vz >= A.s.res[2])) continue;
-        const long long src = ((DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0]) * K * 4;
-        if ((src & 15) == 0 && mv_bulk_ok) mv_bytes += 2 * OBYTES;
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        tx_bytes += __shfl_xor_sync(0xffffffffu, tx_bytes, off);
-        mv_bytes += __shfl_xor_sync(0xffffffffu, mv_bytes, off);
-    }
-    if (lane == 0) {
-        mbar_expect_tx(bar_tile, tx_bytes);
-        mbar_expect_tx(bar_mv, mv_bytes);
-    }
-    __syncwarp();
-    const float* p_in = A.p_in;
-    for (int r = lane; r < L::TROWS; r += 32) {
-        const int ty = DIM == 3 ? r % T : r, tz = DIM == 3 ? r / T : 0;
-        const int vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
-        if (vy < 0 || vy >= A.s.res[1] || (DIM == 3 && (vz < 0 || vz >= A.s.res[2]))) continue;
-        const long long firstv = (DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0] - 1;
-        const long long src = firstv * K * 4 - L::SHF * 4;
-        float* dst = tile + r * L::TROWF;
-        if ((src & 15) == 0 && src >= 0 && src + TBYTES <= nc_bytes) {
-            bulk_g2s(dst, reinterpret_cast<const char*>(p_in) + src, TBYTES, bar_tile);
-        } else {
-            for (int q = 0; q < T * K; q += GR) {
-                const int vx = o[0] - 1 + q / K;
-                const bool ok = vx >= 0 && vx < A.s.res[0];
-                cp_async<GR>(dst + L::SHF + q, ok ? p_in + firstv * K + q : p_in, ok);
+        if (vy < A.s.res[1] && (DIM == 2 || vz < A.s.res[2])) {
+            const long long v0 = (DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0];
+            const long long src = v0 * K * 4;
+            const float* gsrc = which ? A.v_in : A.m_in;
+            float* dst = mvs + which * S::NOWN * K + r * B * K;
+            if ((src & 15) == 0 && (OBYTES % 16) == 0 && o[0] + B <= A.s.res[0]) {
+                tx_mv = OBYTES;
+                mbar_expect_tx(bar_mv, OBYTES);
+                bulk_g2s(dst, reinterpret_cast<const char*>(gsrc) + src, OBYTES, bar_mv);
+            } else {
+                mbar_expect_tx(bar_mv, 0);
+                for (int q = 0; q < B * K; q += GR) {
+                    const bool ok = o[0] + q / K < A.s.res[0];
+                    cp_async<GR>(dst + q, ok ? gsrc + v0 * K + q : gsrc, ok);
+                }
             }
         }
     }
-    for (int r = lane; r < OROWS; r += 32) {
-        const int ly = r % B, lz = DIM == 3 ? r / B : 0;
-        const int vy = o[1] + ly, vz = o[2] + lz;
-        if (vy >= A.s.res[1] || (DIM == 3 && vz >= A.s.res[2])) continue;
-        const long long v0 = (DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0];
-        const long long src = v0 * K * 4;
-        float* dm = mvs + r * B * K;
-        float* dv = mvs + S::NOWN * K + r * B * K;
-        if ((src & 15) == 0 && mv_bulk_ok) {
-            bulk_g2s(dm, reinterpret_cast<const char*>(A.m_in) + src, OBYTES, bar_mv);
-            bulk_g2s(dv, reinterpret_cast<const char*>(A.v_in) + src, OBYTES, bar_mv);
-        } else {
-            for (int q = 0; q < B * K; q += GR) {
-                const bool ok = o[0] + q / K < A.s.res[0];
-                cp_async<GR>(dm + q, ok ? A.m_in + v0 * K + q : A.m_in, ok);
-                cp_async<GR>(dv + q, ok ? A.v_in + v0 * K + q : A.v_in, ok);
-            }
-        }
-    }
+    (void)tx_tile;
+    (void)tx_mv;
     cp_async_commit();
 }
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 
 template <int DIM, int ORDER, bool EIK>
 __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs A) {
@@ -490,14 +489,31 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
     const int o[3] = {(b % nbx) * B, ((b / nbx) % nby) * B, DIM == 3 ? (b / (nbx * nby)) * B : 0};
 
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        mbar_init(&bars[0], NT);
+        mbar_init(&bars[1], NT);
         mbar_fence_init();
     }
     __syncthreads();
     // The tile is waited for inside the first chunk, after the points have
     // been loaded, located and counted (none of which needs it).
-    if (warp == 0) stage_brick<DIM, ORDER>(A, o, tile, mvs, &bars[0], &bars[1], lane);
+    {
+        using LS = BrickSmem<DIM, ORDER>;
+        constexpr int OR = DIM == 3 ? B * B : B;
+        stage_brick<DIM, ORDER>(A, o, tile, mvs, &bars[0], &bars[1], tid);
+        // threads that did not arrive on a barrier (no row of it) arrive now
+        const bool tile_row = tid < LS::TROWS && [&] {
+            const int ty = DIM == 3 ? tid % T : tid, tz = DIM == 3 ? tid / T : 0;
+            const int vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
+            return vy >= 0 && vy < A.s.res[1] && (DIM == 2 || (vz >= 0 && vz < A.s.res[2]));
+        }();
+        const bool mv_row = tid >= LS::TROWS && tid < LS::TROWS + 2 * OR && [&] {
+            const int t = tid - LS::TROWS, r = t % OR;
+            const int ly = r % B, lz = DIM == 3 ? r / B : 0;
+            return o[1] + ly < A.s.res[1] && (DIM == 2 || o[2] + lz < A.s.res[2]);
+        }();
+        if (!tile_row) mbar_arrive(&bars[0]);
+        if (!mv_row) mbar_arrive(&bars[1]);
+    }
 
     float G[K];
 #pragma unroll
@@ -532,10 +548,8 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
             rank = atomicAdd(&cnt[ec], 1);
         }
         if (base == p0) {
-            if (warp == 0) {
-                mbar_wait(&bars[0], 0);  // one warp waits; the others park at the barrier
-                cp_async_wait<0>();      // fallback rows (rare: grid-edge bricks)
-            }
+            cp_async_wait<0>();  // own fallback rows (rare: grid-edge bricks)
+            if (warp == 0) mbar_wait(&bars[0], 0);  // one warp waits; the others park at the barrier
             __syncthreads();
         }
         if (tid < m) {
@@ -687,10 +701,8 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
     float* Gs = uni;
 #pragma unroll
     for (int q = 0; q < K; ++q) Gs[myv * K + q] = G[q];
-    if (p0 == p1 && warp == 0) {  // brick without points: the tile was never waited for
-        mbar_wait(&bars[0], 0);
-        cp_async_wait<0>();
-    }
+    cp_async_wait<0>();
+    if (p0 == p1 && warp == 0) mbar_wait(&bars[0], 0);  // brick without points: tile not yet waited for
     if (warp == 0) mbar_wait(&bars[1], 0);  // m/v rows landed
     __syncthreads();
     double tv_sum = 0.0;
@@ -745,38 +757,30 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
         }
     }
     __syncthreads();
-    // coalesced copy-out of the staged rows (p from Gs, m and v from mvs)
+    // copy-out of the staged rows (p from Gs, m and v from mvs): one TMA bulk
+    // store per row and array, issued by one thread each
     {
         constexpr int OROWS = DIM == 3 ? B * B : B;
         constexpr int ROWF = B * K;
         const int nvx = min(B, A.s.res[0] - o[0]);
         const int rowf = nvx * K;
-        if (rowf == ROWF && (ROWF % 4) == 0 && ((A.s.sy * K) % 4) == 0 && ((o[0] * K) % 4) == 0) {
-            constexpr int RV = ROWF / 4;  // float4 per row
-            for (int i = tid; i < 3 * OROWS * RV; i += NT) {
-                const int which = i / (OROWS * RV);
-                const int i2 = i - which * OROWS * RV;
-                const int r = i2 / RV, c4 = i2 - r * RV;
-                const int ly = r % B, lz = DIM == 3 ? r / B : 0;
-                const int gy = o[1] + ly, gz = o[2] + lz;
-                if (gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid < 3 * OROWS) {
+            const int which = tid / OROWS, r = tid - which * OROWS;
+            const int ly = r % B, lz = DIM == 3 ? r / B : 0;
+            const int gy = o[1] + ly, gz = o[2] + lz;
+            if (gy < A.s.res[1] && (DIM == 2 || gz < A.s.res[2])) {
                 const long long gb = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K;
-                const float* src = (which == 0 ? uni : mvs + (which - 1) * S::NOWN * K) + r * ROWF + 4 * c4;
-                float* dst = (which == 0 ? A.p_out : (which == 1 ? A.m_out : A.v_out)) + gb + 4 * c4;
-                *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
-            }
-        } else {
-            for (int i = tid; i < 3 * OROWS * ROWF; i += NT) {
-                const int which = i / (OROWS * ROWF);
-                const int i2 = i - which * OROWS * ROWF;
-                const int r = i2 / ROWF, c1 = i2 - r * ROWF;
-                const int ly = r % B, lz = DIM == 3 ? r / B : 0;
-                const int gy = o[1] + ly, gz = o[2] + lz;
-                if (c1 >= rowf || gy >= A.s.res[1] || (DIM == 3 && gz >= A.s.res[2])) continue;
-                const long long gb = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K;
-                const float* src = (which == 0 ? uni : mvs + (which - 1) * S::NOWN * K) + r * ROWF + c1;
-                float* dst = (which == 0 ? A.p_out : (which == 1 ? A.m_out : A.v_out)) + gb + c1;
-                *dst = *src;
+                const float* src = (which == 0 ? uni : mvs + (which - 1) * S::NOWN * K) + r * ROWF;
+                float* dst = (which == 0 ? A.p_out : (which == 1 ? A.m_out : A.v_out)) + gb;
+                if ((gb & 3) == 0 && (rowf & 3) == 0) {
+                    bulk_s2g(dst, src, (unsigned)rowf * 4);
+                    bulk_commit();
+                    bulk_wait_read0();  // smem must stay valid until read out
+                } else {
+                    for (int q = 0; q < rowf; ++q) dst[q] = src[q];
+                }
             }
         }
     }
