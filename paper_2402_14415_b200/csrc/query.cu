@@ -12,6 +12,7 @@
 
 #include "dispatch.cuh"
 #include "tg_internal.h"
+#include "tma.cuh"
 
 namespace tgcu {
 
@@ -266,7 +267,12 @@ __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __re
     constexpr int B = 1 << LB;
     constexpr int T = B + 1;  // tile edge in vertices
     constexpr int GR = (K % 2 == 0) ? 2 : 1;
-    extern __shared__ __align__(16) float tile[];  // T^DIM * K
+    // tile rows (fixed y, z) of T vertices, stride TROWF floats
+    constexpr int TROWF = ((T * K + 3) / 4) * 4;
+    constexpr int ROWS = DIM == 3 ? T * T : T;
+    constexpr unsigned RBYTES = ((T * K * 4 + 15) / 16) * 16;
+    extern __shared__ __align__(128) float tile[];  // ROWS * TROWF
+    __shared__ __align__(8) unsigned long long bar;
 
     const unsigned int code = blockIdx.x;
     const long long p0 = off[code], p1 = off[code + 1];
@@ -278,24 +284,41 @@ __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __re
         for (int a = 0; a < DIM; ++a) b[a] |= ((code >> (bit * DIM + a)) & 1u) << bit;
     }
     const int ox = b[0] * B, oy = b[1] * B, oz = DIM == 3 ? b[2] * B : 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, blockDim.x);
+        mbar_fence_init();
+    }
+    __syncthreads();
     {
-        constexpr int ROWG = T * K / GR;
-        constexpr int ROWS = DIM == 3 ? T * T : T;
-        for (int e = threadIdx.x; e < ROWS * ROWG; e += blockDim.x) {
-            const int r = e / ROWG, q = (e - r * ROWG) * GR;
-            const int tx = q / K;
-            const int ty = r % T, tz = r / T;
-            const int vx = ox + tx, vy = oy + ty, vz = oz + tz;
-            const bool ok = vx < s.res[0] && vy < s.res[1] && (DIM == 2 || vz < s.res[2]);
-            const long long gi = ok ? ((long long)vz * s.sz + (long long)vy * s.sy + vx) * K + (q - tx * K) : 0;
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(tile + r * T * K + q);
-            const int nb = ok ? 4 * GR : 0;
-            if constexpr (GR == 2)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(coeffs + gi), "r"(nb) : "memory");
-            else
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(coeffs + gi), "r"(nb) : "memory");
+        // one TMA bulk copy per row (thread r), cp.async fallback when the row
+        // is unaligned or runs past the array
+        const long long nc_bytes = (long long)s.res[0] * s.res[1] * (DIM == 3 ? s.res[2] : 1) * K * 4;
+        const int r = threadIdx.x;
+        bool arrived = false;
+        if (r < ROWS) {
+            const int ty = DIM == 3 ? r % T : r, tz = DIM == 3 ? r / T : 0;
+            const int vy = oy + ty, vz = oz + tz;
+            if (vy < s.res[1] && (DIM == 2 || vz < s.res[2])) {
+                const long long v0 = (DIM == 3 ? (long long)vz * s.sz : 0LL) + (long long)vy * s.sy + ox;
+                const long long src = v0 * K * 4;
+                float* dst = tile + r * TROWF;
+                if ((src & 15) == 0 && src + RBYTES <= nc_bytes) {
+                    mbar_expect_tx(&bar, RBYTES);
+                    bulk_g2s(dst, reinterpret_cast<const char*>(coeffs) + src, RBYTES, &bar);
+                } else {
+                    mbar_expect_tx(&bar, 0);
+                    for (int q = 0; q < T * K; q += GR) {
+                        const bool ok = ox + q / K < s.res[0];
+                        cp_async<GR>(dst + q, ok ? coeffs + v0 * K + q : coeffs, ok);
+                    }
+                }
+                arrived = true;
+            }
         }
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+        if (!arrived) mbar_arrive(&bar);
+        cp_async_commit();
+        cp_async_wait<0>();
+        if (threadIdx.x < 32) mbar_wait(&bar, 0);
     }
     __syncthreads();
 
@@ -324,16 +347,16 @@ __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __re
             ax[a] = axis_factors(s, a, local);
             lc[a] = c - o3[a];
         }
-        const int tbase = DIM == 3 ? (lc[2] * T + lc[1]) * T + lc[0] : lc[1] * T + lc[0];
+        const int tbase = (DIM == 3 ? lc[2] * T + lc[1] : lc[1]) * TROWF + lc[0] * K;
         float f = 0.0f;
         float fg[DIM];
 #pragma unroll
         for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
 #pragma unroll
         for (int c = 0; c < (1 << DIM); ++c) {
-            const int tv = tbase + (c & 1) + ((c >> 1) & 1) * T + (DIM == 3 ? ((c >> 2) & 1) * T * T : 0);
+            const int tv = tbase + (c & 1) * K + ((c >> 1) & 1) * TROWF + (DIM == 3 ? ((c >> 2) & 1) * T * TROWF : 0);
             float cb[K];
-            load_block<K, false>(tile + tv * K, cb);
+            load_block<K, false>(tile + tv, cb);
             blend_corner<DIM, ORDER, GRAD>(cb, corner_geom<DIM>(s, ax, c), f, fg);
         }
         vals[i] = f;
@@ -360,8 +383,8 @@ void launch_eval_sorted(Grid& g, const float* pts, int64_t n, const int64_t* off
         constexpr int B = 1 << LB;
         constexpr int K = KOf<DIM, ORDER>::value;
         constexpr int T = B + 1;
-        constexpr int TV = DIM == 3 ? T * T * T : T * T;
-        const size_t smem = sizeof(float) * TV * K;
+        constexpr int TROWF = ((T * K + 3) / 4) * 4;
+        const size_t smem = sizeof(float) * (DIM == 3 ? T * T : T) * TROWF;
         auto kern = grads ? k_eval_brick<DIM, ORDER, true, LB> : k_eval_brick<DIM, ORDER, false, LB>;
         TGCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<(unsigned)codes, 256, smem, s>>>(g.ds, g.p[g.cur], pts, off, vals, grads, g.st);
