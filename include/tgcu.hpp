@@ -1,0 +1,113 @@
+// tgcu.hpp — header-only C++ shim over the C ABI (tgcu.h) in the shape of the
+// reference's tg:: API (/root/reference/proj/core/include/taylorgrid/*.hpp),
+// so reference callers (run_schedule, cmd_bench, TrainProblem subclasses) can
+// drive the B200 path with the same names, argument meaning and exception
+// types (errors.hpp:9-34; std::invalid_argument for require_arg failures).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "tgcu.h"
+
+namespace tgcu {
+
+struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct IngestError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NumericalError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ResourceError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+// Status -> the reference's exception classes.
+inline void check(int rc) {
+    if (rc == TGCU_OK) return;
+    const std::string msg = tgcu_last_error();
+    switch (rc) {
+        case TGCU_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case TGCU_ERR_CONFIG: throw ConfigError(msg);
+        case TGCU_ERR_INGEST: throw IngestError(msg);
+        case TGCU_ERR_NUMERICAL: throw NumericalError(msg);
+        case TGCU_ERR_RESOURCE: throw ResourceError(msg);
+        default: throw CudaError(msg);
+    }
+}
+
+inline int coeff_count(int order, int dim) {
+    int k = 0;
+    check(tgcu_coeff_count(order, dim, &k));
+    return k;
+}
+
+// tg::LossTerms / tg::LossConfig / tg::AdamConfig equivalents.
+using LossTerms = tgcu_loss_terms;
+struct LossConfig {
+    double lambda1 = 1e-4, lambda2 = 2e-5, k = 50.0;
+    bool use_weighting = true, use_tv = true, differentiate_weight = false;
+    tgcu_loss_config c() const {
+        return {lambda1, lambda2, k, use_weighting ? 1 : 0, use_tv ? 1 : 0, differentiate_weight ? 1 : 0};
+    }
+};
+struct AdamConfig {
+    double lr = 0.003, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+};
+
+// A device-resident tg::TaylorGrid together with its AdamState.
+class Grid {
+public:
+    explicit Grid(const tgcu_grid_spec& spec, const tgcu_init_options* opts = nullptr, int device = 0) {
+        check(tgcu_grid_create(&spec, opts, device, &h_));
+    }
+    ~Grid() { tgcu_grid_destroy(h_); }
+    Grid(const Grid&) = delete;
+    Grid& operator=(const Grid&) = delete;
+    Grid(Grid&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+
+    tgcu_grid* handle() const { return h_; }
+    int64_t coeff_total() const { return tgcu_grid_coeff_total(h_); }
+
+    // TaylorGrid::coeffs in the reference layout (fp64 at the boundary).
+    std::vector<double> coeffs() const {
+        std::vector<double> c(static_cast<size_t>(coeff_total()));
+        check(tgcu_grid_download_f64(h_, c.data(), static_cast<int64_t>(c.size())));
+        return c;
+    }
+    void set_coeffs(std::span<const double> c) {
+        check(tgcu_grid_upload_f64(h_, c.data(), static_cast<int64_t>(c.size())));
+    }
+
+    // eval / eval_with_spatial_gradient, batched over host fp32 points (n x 3).
+    std::vector<float> eval(std::span<const float> pts, std::vector<float>* spatial_grad = nullptr) const {
+        const int64_t n = static_cast<int64_t>(pts.size() / 3);
+        std::vector<float> v(static_cast<size_t>(n));
+        if (spatial_grad) spatial_grad->assign(static_cast<size_t>(3 * n), 0.0f);
+        check(tgcu_eval(h_, pts.data(), n, v.data(), spatial_grad ? spatial_grad->data() : nullptr, TGCU_HOST,
+                        nullptr));
+        return v;
+    }
+
+    // AdamState::reset + config.
+    void adam_reset(const AdamConfig& a) {
+        const tgcu_adam_config c{a.lr, a.beta1, a.beta2, a.eps};
+        check(tgcu_adam_reset(h_, &c));
+    }
+
+    // One run_schedule step (schedule.cpp:66-92): zero grad, total_loss,
+    // finite-loss check, adam_step. samples: host n x 4 (x, y, z, gt).
+    LossTerms train_step(std::span<const float> samples, const LossConfig& cfg) {
+        const tgcu_loss_config c = cfg.c();
+        LossTerms t{};
+        check(tgcu_train_step(h_, samples.data(), static_cast<int64_t>(samples.size() / 4), &c, &t, TGCU_HOST,
+                              nullptr));
+        return t;
+    }
+
+private:
+    tgcu_grid* h_ = nullptr;
+};
+
+}  // namespace tgcu

@@ -1,0 +1,43 @@
+// C++ caller of the B200 path through include/tgcu.hpp, written the way a
+// reference tool would use it (cmd_bench-shaped loop, tools/main.cpp:639-644).
+// Built by __graft_entry__.build(); run by tests/test_cpp_shim.py on a GPU.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "tgcu.hpp"
+
+int main() {
+    tgcu_grid_spec gs{3, {24, 24, 24}, {-1, -1, -1}, {2, 2, 2}, 2};
+    tgcu::Grid g(gs);
+    g.adam_reset({1e-2, 0.9, 0.999, 1e-8});
+    const int n = 8192;
+    std::vector<float> smp(4 * n);
+    if (tgcu_sample(0, 3, 7, n, 0.5, 0.01, 0.6, smp.data()) != TGCU_OK) return 2;
+    tgcu::LossConfig lc;
+    double first = 0, last = 0;
+    for (int s = 0; s < 20; ++s) {
+        const auto t = g.train_step(smp, lc);
+        if (s == 0) first = t.total;
+        last = t.total;
+    }
+    std::vector<float> pts = {0.f, 0.f, 0.f, 0.6f, 0.f, 0.f};
+    std::vector<float> grad;
+    const auto v = g.eval(pts, &grad);
+    std::printf("loss %.6g -> %.6g, f(0)=%.4f f(0.6,0,0)=%.4f\n", first, last, v[0], v[1]);
+    if (!(last < first) || !std::isfinite(v[0])) return 3;
+    smp[4 * 5 + 3] = NAN;  // non-finite loss -> tg::NumericalError semantics
+    try {
+        g.train_step(smp, lc);
+        return 4;
+    } catch (const tgcu::NumericalError& e) {
+        std::printf("NumericalError: %s\n", e.what());
+    }
+    try {
+        tgcu::coeff_count(3, 3);
+        return 5;
+    } catch (const std::invalid_argument&) {
+    }
+    std::printf("shim ok\n");
+    return 0;
+}
