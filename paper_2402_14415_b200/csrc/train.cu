@@ -662,39 +662,77 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
             float* mm = mvs + v * K;
             float* vv = mvs + S::NOWN * K + v * K;
             constexpr int offs[3] = {K, L::TROWF, DIM == 3 ? T * L::TROWF : 0};
-            const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
-            float sq = 0.0f;
-            bool finite = true;
+            bool hi[DIM], lo[DIM];
 #pragma unroll
-            for (int q = 0; q < K; ++q) {
-                const float pv = tp[q];
-                float gt = 0.0f;
-                if (A.want_tv) {
-                    // pairs (v, v+e_a) owned here feed the TV sum; both ends'
-                    // terms feed this vertex's gradient (sdf_loss.cpp:155-257)
+            for (int a = 0; a < DIM; ++a) {
+                hi[a] = A.want_tv && g3[a] + 1 < A.s.res[a];
+                lo[a] = A.want_tv && g3[a] >= 1;
+            }
+            const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
+            if constexpr (K % 2 == 0) {
+                // channel pairs on the packed fp32x2 pipe (FFMA2 / FADD2 / FMUL2)
+                const float2 gsc = make_float2(A.tv_gscale, A.tv_gscale);
+                const float2 b1 = make_float2(A.b1, A.b1), b2 = make_float2(A.b2, A.b2);
+                const float2 cc1 = make_float2(c1, c1), cc2 = make_float2(c2, c2);
+                float2 sq2 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int q = 0; q < K; q += 2) {
+                    const float2 pv = *reinterpret_cast<const float2*>(tp + q);
+                    const float2 npv = make_float2(-pv.x, -pv.y);
+                    float2 gt = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int a = 0; a < DIM; ++a) {
-                        if (g3[a] + 1 < A.s.res[a]) {
+                        if (hi[a]) {  // pair (v, v+e_a): TV sum and -d
+                            const float2 d = __fadd2_rn(*reinterpret_cast<const float2*>(tp + offs[a] + q), npv);
+                            sq2 = __ffma2_rn(d, d, sq2);
+                            gt = __fadd2_rn(gt, make_float2(-d.x, -d.y));
+                        }
+                        if (lo[a]) {  // pair (v-e_a, v): +(pv - p_lo)
+                            const float2 pl = *reinterpret_cast<const float2*>(tp + q - offs[a]);
+                            gt = __fadd2_rn(gt, __fadd2_rn(pv, make_float2(-pl.x, -pl.y)));
+                        }
+                    }
+                    const float2 gi = __ffma2_rn(gsc, gt, *reinterpret_cast<const float2*>(gs + q));
+                    if (A.grad_out) *reinterpret_cast<float2*>(A.grad_out + gidx + q) = gi;
+                    if (!isfinite(gi.x)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
+                    if (!isfinite(gi.y)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q + 1));
+                    // Adam (adam.cpp:36-55), fp32 state, host fp64 bias corrections
+                    const float2 mn = __ffma2_rn(b1, *reinterpret_cast<const float2*>(mm + q), __fmul2_rn(cc1, gi));
+                    const float2 vn = __ffma2_rn(b2, *reinterpret_cast<const float2*>(vv + q),
+                                                 __fmul2_rn(cc2, __fmul2_rn(gi, gi)));
+                    *reinterpret_cast<float2*>(mm + q) = mn;
+                    *reinterpret_cast<float2*>(vv + q) = vn;
+                    const float2 stp = make_float2(lr_bc1 * mn.x * fast_rcp(fast_sqrt(vn.x * A.inv_bc2) + A.eps),
+                                                   lr_bc1 * mn.y * fast_rcp(fast_sqrt(vn.y * A.inv_bc2) + A.eps));
+                    *reinterpret_cast<float2*>(gs + q) = __fadd2_rn(pv, make_float2(-stp.x, -stp.y));
+                }
+                tv_sum = (double)(sq2.x + sq2.y);
+            } else {
+                float sq = 0.0f;
+#pragma unroll
+                for (int q = 0; q < K; ++q) {
+                    const float pv = tp[q];
+                    float gt = 0.0f;
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) {
+                        if (hi[a]) {
                             const float d = tp[offs[a] + q] - pv;
                             sq = fmaf(d, d, sq);
                             gt -= d;
                         }
-                        if (g3[a] >= 1) gt += pv - tp[q - offs[a]];
+                        if (lo[a]) gt += pv - tp[q - offs[a]];
                     }
+                    const float gi = fmaf(A.tv_gscale, gt, gs[q]);
+                    if (A.grad_out) A.grad_out[gidx + q] = gi;
+                    if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
+                    const float mn = fmaf(A.b1, mm[q], c1 * gi);
+                    const float vn = fmaf(A.b2, vv[q], c2 * gi * gi);
+                    mm[q] = mn;
+                    vv[q] = vn;
+                    gs[q] = pv - lr_bc1 * mn * fast_rcp(fast_sqrt(vn * A.inv_bc2) + A.eps);
                 }
-                const float gi = fmaf(A.tv_gscale, gt, gs[q]);
-                finite &= isfinite(gi);
-                if (A.grad_out) A.grad_out[gidx + q] = gi;
-                // Adam (adam.cpp:36-55), fp32 state, host fp64 bias corrections
-                const float mn = fmaf(A.b1, mm[q], c1 * gi);
-                const float vn = fmaf(A.b2, vv[q], c2 * gi * gi);
-                mm[q] = mn;
-                vv[q] = vn;
-                gs[q] = pv - lr_bc1 * mn * fast_rcp(fast_sqrt(vn * A.inv_bc2) + A.eps);
-                if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
+                tv_sum = (double)sq;
             }
-            (void)finite;
-            tv_sum = (double)sq;
         }
     }
     __syncthreads();
