@@ -79,12 +79,27 @@ void ensure_bins(Grid& g, int64_t points) {
     g.binned_cap = need;
 }
 
-void ensure_bin_hist(Grid& g, int64_t ints) {
-    if (g.bin_hist_cap >= ints) return;
-    if (g.bin_hist) TGCU_CUDA(cudaFree(g.bin_hist));
-    g.bin_hist = nullptr;
-    TGCU_CUDA(cudaMalloc(&g.bin_hist, sizeof(int) * ints));
-    g.bin_hist_cap = ints;
+void ensure_bin_hist(Grid& g, int64_t ints, int64_t points, int64_t chain_ctas) {
+    if (g.bin_hist_cap < ints) {
+        if (g.bin_hist) TGCU_CUDA(cudaFree(g.bin_hist));
+        g.bin_hist = nullptr;
+        TGCU_CUDA(cudaMalloc(&g.bin_hist, sizeof(int) * ints));
+        g.bin_hist_cap = ints;
+    }
+    if (g.bin_codes_cap < points) {
+        if (g.bin_codes) TGCU_CUDA(cudaFree(g.bin_codes));
+        g.bin_codes = nullptr;
+        TGCU_CUDA(cudaMalloc(&g.bin_codes, sizeof(int) * points));
+        g.bin_codes_cap = points;
+    }
+    if (g.bin_chain_cap < chain_ctas) {
+        if (g.bin_chain) TGCU_CUDA(cudaFree(g.bin_chain));
+        g.bin_chain = nullptr;
+        TGCU_CUDA(cudaMalloc(&g.bin_chain, sizeof(int) * 2 * chain_ctas));
+        TGCU_CUDA(cudaMemset(g.bin_chain, 0, sizeof(int) * 2 * chain_ctas));
+        g.bin_chain_cap = chain_ctas;
+        g.bin_epoch = 0;
+    }
 }
 
 // Ping-pong parameters + Adam moments (both slots), zero moments.
@@ -278,6 +293,8 @@ int tgcu_grid_destroy(tgcu_grid* h) {
     cudaFree(g.bin_cursor);
     cudaFree(g.binned);
     cudaFree(g.bin_hist);
+    cudaFree(g.bin_codes);
+    cudaFree(g.bin_chain);
     cudaFree(g.partials);
     cudaFree(g.d_trace);
     cudaFreeHost(g.h_terms);

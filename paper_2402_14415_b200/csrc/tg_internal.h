@@ -70,6 +70,11 @@ struct Grid {
     int* bin_cursor = nullptr;  // NB
     int* bin_hist = nullptr;    // per-tile brick histograms (privatized binning)
     int64_t bin_hist_cap = 0;
+    int* bin_codes = nullptr;   // per-point brick code
+    int64_t bin_codes_cap = 0;
+    int* bin_chain = nullptr;   // chained-scan flags/prefixes (2 ints per CTA)
+    int64_t bin_chain_cap = 0;
+    int bin_epoch = 0;
     float4* binned = nullptr;
     int64_t binned_cap = 0;     // points
     double* partials = nullptr; // NB * 4
@@ -92,7 +97,7 @@ constexpr int kTraceCap = 4096;
 
 void ensure_staging(Grid& g, int64_t floats);
 void ensure_bins(Grid& g, int64_t points);
-void ensure_bin_hist(Grid& g, int64_t ints);
+void ensure_bin_hist(Grid& g, int64_t ints, int64_t points, int64_t chain_ctas);
 void ensure_scratch(Grid& g, int64_t doubles);
 void ensure_grad(Grid& g);
 void ensure_optimizer(Grid& g);

@@ -154,64 +154,109 @@ __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs A) {
 
 // ---- privatized binning (NB small enough for a shared-memory histogram) ----
 // Points are cut into tiles of kBinTile; CTA c builds the brick histogram of
-// tile c in shared memory (native int smem atomics) and stores it as row c of
-// H[ncta][NB]. A column scan turns H into per-(tile, brick) bases, the brick
-// totals are scanned into offsets, and the scatter kernel reserves slots with
-// shared-memory atomics only: no contended global atomics on hot bricks.
+// tile c in shared memory (native int smem atomics), stores it as row c of
+// H[ncta][NB] and records every point's brick code (base brick | axis mask).
+// k_bin_cols turns H into per-(tile, brick) exclusive prefixes and computes
+// the brick offsets with a chained (in-order) scan across its CTAs; the
+// scatter reserves slots with shared-memory atomics only. No contended global
+// atomics on hot bricks, three launches.
 constexpr int kBinTile = 4096;
 constexpr int kBinThreads = 512;
+constexpr int kBinPer = kBinTile / kBinThreads;  // points per thread
 constexpr int kBinSmemMax = 16384;  // bricks
+constexpr int kColBricks = 32;
+constexpr int kMaxBinTiles = 512;
+
+// Base brick of the point and the per-axis "also next brick" mask (bit 28+a),
+// or -1 for a NaN coordinate.
+template <int DIM>
+__device__ __forceinline__ int point_brick_code(const DevSpec& s, const int* nb, const float4& q) {
+    constexpr int B = BrickShape<DIM>::B;
+    const float pf[3] = {q.x, q.y, q.z};
+    int lo[3] = {0, 0, 0}, mask = 0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        const double x = (double)pf[a];
+        if (isnan(x)) return -1;
+        double local;
+        const int c = locate_axis(s, a, x, local);
+        lo[a] = c / B;
+        mask |= ((c % B) == B - 1 ? 1 : 0) << a;
+    }
+    return (((DIM == 3 ? lo[2] * nb[1] : 0) + lo[1]) * nb[0] + lo[0]) | (mask << 28);
+}
 
 template <int DIM>
-__global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __restrict__ H, int NB) {
+__device__ __forceinline__ int code_bricks(int code, const int* nb, int* out) {
+    const int base = code & 0x0fffffff, mask = code >> 28;
+    int m = 0;
+    const int sy = nb[0], sz = nb[0] * nb[1];
+    for (int dz = 0; dz <= (DIM == 3 ? (mask >> 2) & 1 : 0); ++dz)
+        for (int dy = 0; dy <= ((mask >> 1) & 1); ++dy)
+            for (int dx = 0; dx <= (mask & 1); ++dx) out[m++] = base + dz * sz + dy * sy + dx;
+    return m;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __restrict__ H, int* __restrict__ codes,
+                                                          int NB) {
     extern __shared__ int hist[];
     if (A.st->error) return;
     for (int i = threadIdx.x; i < NB; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
     const long long t0 = (long long)blockIdx.x * kBinTile;
-    const long long t1 = min(t0 + kBinTile, A.n);
-    for (long long i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
-        int br[8];
-        const int m = point_bricks<DIM>(A.s, A.nb, A.pts[i], br);
-        if (m == 0) atomicMin(&A.st->nan_point, (unsigned long long)i);
+    float4 q[kBinPer];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (k < m) atomicAdd(&hist[br[k]], 1);
+    for (int k = 0; k < kBinPer; ++k) {  // all loads in flight first
+        const long long i = t0 + threadIdx.x + (long long)k * kBinThreads;
+        q[k] = i < A.n ? A.pts[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kBinPer; ++k) {
+        const long long i = t0 + threadIdx.x + (long long)k * kBinThreads;
+        if (i >= A.n) continue;
+        const int code = point_brick_code<DIM>(A.s, A.nb, q[k]);
+        codes[i] = code;
+        if (code < 0) {
+            atomicMin(&A.st->nan_point, (unsigned long long)i);
+            continue;
+        }
+        int br[8];
+        const int m = code_bricks<DIM>(code, A.nb, br);
+        for (int j = 0; j < m; ++j) atomicAdd(&hist[br[j]], 1);
     }
     __syncthreads();
     int* row = H + (long long)blockIdx.x * NB;
     for (int i = threadIdx.x; i < NB; i += blockDim.x) row[i] = hist[i];
 }
 
-// Per brick: exclusive scan of H over tiles (in place) and the brick total.
-// A CTA owns 32 bricks: it loads their H columns for all tiles with
-// coalesced 128-byte rows into smem, scans each column with one warp, and
-// writes them back.
-constexpr int kColBricks = 32;
-constexpr int kMaxBinTiles = 512;
-__global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta, int NB, int* __restrict__ totals,
-                                                  Status* st) {
+// H columns -> per-(tile, brick) exclusive prefixes (in place); brick totals
+// -> exclusive offsets off[0..NB] via a chained scan over the CTAs (all CTAs
+// are co-resident; CTA i waits for CTA i-1's inclusive prefix, tagged with
+// this launch's epoch).
+__global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta, int NB, int* __restrict__ off,
+                                                  int* __restrict__ chain, int epoch, Status* st) {
     extern __shared__ int col[];  // [ncta][kColBricks + 1]
+    __shared__ int tot[kColBricks];
+    __shared__ int carry;
     if (st->error) return;
     const int b0 = blockIdx.x * kColBricks;
     const int nb = min(kColBricks, NB - b0);
     constexpr int LD = kColBricks + 1;
-    for (int i = threadIdx.x; i < ncta * kColBricks; i += blockDim.x) {
-        const int c = i / kColBricks, j = i - c * kColBricks;
-        if (j < nb) col[c * LD + j] = H[(long long)c * NB + b0 + j];
-    }
-    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // warp w loads rows c = w, w+8, ... (lane = brick): coalesced 128-byte rows
+    for (int c = warp; c < ncta; c += 8) col[c * LD + lane] = lane < nb ? H[(long long)c * NB + b0 + lane] : 0;
+    __syncthreads();
     const int per = (ncta + 31) / 32;
-    for (int j = warp; j < nb; j += blockDim.x / 32) {
+    for (int j = warp; j < kColBricks; j += 8) {
         const int c0 = min(lane * per, ncta), c1 = min(c0 + per, ncta);
         int sum = 0;
         for (int c = c0; c < c1; ++c) sum += col[c * LD + j];
         int x = sum;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, off);
-            if (lane >= off) x += y;
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o2);
+            if (lane >= o2) x += y;
         }
         int run = x - sum;
         for (int c = c0; c < c1; ++c) {
@@ -219,32 +264,66 @@ __global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta,
             col[c * LD + j] = run;
             run += v;
         }
-        if (lane == 31) totals[b0 + j] = x;
+        if (lane == 31) tot[j] = x;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < ncta * kColBricks; i += blockDim.x) {
-        const int c = i / kColBricks, j = i - c * kColBricks;
-        if (j < nb) H[(long long)c * NB + b0 + j] = col[c * LD + j];
+    for (int c = warp; c < ncta; c += 8)
+        if (lane < nb) H[(long long)c * NB + b0 + lane] = col[c * LD + lane];
+    if (warp == 0) {
+        const int t = tot[lane];
+        int x = t;
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o2);
+            if (lane >= o2) x += y;
+        }
+        const int block_sum = __shfl_sync(0xffffffffu, x, 31);
+        if (lane == 0) {
+            int prev = 0;
+            if (blockIdx.x > 0) {
+                volatile int* ch = chain;
+                while (ch[2 * (blockIdx.x - 1)] != epoch) {
+                }
+                __threadfence();
+                prev = ch[2 * (blockIdx.x - 1) + 1];
+            }
+            chain[2 * blockIdx.x + 1] = prev + block_sum;
+            __threadfence();
+            atomicExch(&chain[2 * blockIdx.x], epoch);
+            carry = prev;
+        }
+        __syncwarp();
+        const int c0 = __shfl_sync(0xffffffffu, lane == 0 ? carry : 0, 0);
+        if (lane < nb) off[b0 + lane] = c0 + x - t;
+        if (blockIdx.x == gridDim.x - 1 && lane == 0) off[NB] = c0 + block_sum;
     }
 }
 
 template <int DIM>
 __global__ void __launch_bounds__(kBinThreads) k_bin_scatter_tiles(BinArgs A, const int* __restrict__ H,
+                                                                   const int* __restrict__ codes,
                                                                    const int* __restrict__ off, int NB) {
     extern __shared__ int cur[];
     if (A.st->error) return;
     const int* row = H + (long long)blockIdx.x * NB;
     for (int i = threadIdx.x; i < NB; i += blockDim.x) cur[i] = off[i] + row[i];
-    __syncthreads();
     const long long t0 = (long long)blockIdx.x * kBinTile;
-    const long long t1 = min(t0 + kBinTile, A.n);
-    for (long long i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
-        const float4 q = A.pts[i];
-        int br[8];
-        const int m = point_bricks<DIM>(A.s, A.nb, q, br);
+    float4 q[kBinPer];
+    int cd[kBinPer];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (k < m) A.binned[atomicAdd(&cur[br[k]], 1)] = q;
+    for (int k = 0; k < kBinPer; ++k) {
+        const long long i = t0 + threadIdx.x + (long long)k * kBinThreads;
+        const bool ok = i < A.n;
+        q[k] = ok ? A.pts[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        cd[k] = ok ? codes[i] : -1;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kBinPer; ++k) {
+        if (cd[k] < 0) continue;
+        int br[8];
+        const int m = code_bricks<DIM>(cd[k], A.nb, br);
+        for (int j = 0; j < m; ++j) A.binned[atomicAdd(&cur[br[j]], 1)] = q[k];
     }
 }
 
@@ -868,25 +947,29 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     const int ncta_tiles = (int)((n + kBinTile - 1) / kBinTile);
     if (g.NB <= kBinSmemMax && ncta_tiles <= kMaxBinTiles) {
         const int ncta = ncta_tiles;
-        ensure_bin_hist(g, (int64_t)ncta * g.NB);
+        ensure_bin_hist(g, (int64_t)ncta * g.NB, n, (g.NB + kColBricks - 1) / kColBricks);
         const size_t sm = sizeof(int) * g.NB;
-        if (g.spec.dim == 3) {
-            TGCU_CUDA(cudaFuncSetAttribute(k_bin_hist<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kBinSmemMax)));
-            TGCU_CUDA(cudaFuncSetAttribute(k_bin_scatter_tiles<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kBinSmemMax)));
-            k_bin_hist<3><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, (int)g.NB);
-        } else {
-            TGCU_CUDA(cudaFuncSetAttribute(k_bin_hist<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kBinSmemMax)));
-            TGCU_CUDA(cudaFuncSetAttribute(k_bin_scatter_tiles<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kBinSmemMax)));
-            k_bin_hist<2><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, (int)g.NB);
-        }
         const size_t csm = sizeof(int) * ncta * (kColBricks + 1);
-        TGCU_CUDA(cudaFuncSetAttribute(k_bin_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int) * kMaxBinTiles * (kColBricks + 1))));
-        k_bin_cols<<<(unsigned)((g.NB + kColBricks - 1) / kColBricks), 256, csm, s>>>(g.bin_hist, ncta, (int)g.NB,
-                                                                                      g.bin_count, g.st);
-        k_bin_scan<<<1, 1024, 0, s>>>(g.bin_count, g.bin_off, g.bin_cursor, (int)g.NB, g.st);
-        if (g.spec.dim == 3) k_bin_scatter_tiles<3><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_off, (int)g.NB);
-        else k_bin_scatter_tiles<2><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_off, (int)g.NB);
-        count_launch(4);
+        static bool attr = false;
+        if (!attr) {
+            TGCU_CUDA(cudaFuncSetAttribute(k_bin_hist<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBinSmemMax));
+            TGCU_CUDA(cudaFuncSetAttribute(k_bin_hist<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBinSmemMax));
+            TGCU_CUDA(cudaFuncSetAttribute(k_bin_scatter_tiles<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBinSmemMax));
+            TGCU_CUDA(cudaFuncSetAttribute(k_bin_scatter_tiles<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBinSmemMax));
+            TGCU_CUDA(cudaFuncSetAttribute(k_bin_cols, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(sizeof(int) * kMaxBinTiles * (kColBricks + 1))));
+            attr = true;
+        }
+        if (g.spec.dim == 3) k_bin_hist<3><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_codes, (int)g.NB);
+        else k_bin_hist<2><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_codes, (int)g.NB);
+        const int epoch = ++g.bin_epoch;
+        k_bin_cols<<<(unsigned)((g.NB + kColBricks - 1) / kColBricks), 256, csm, s>>>(
+            g.bin_hist, ncta, (int)g.NB, g.bin_off, g.bin_chain, epoch, g.st);
+        if (g.spec.dim == 3)
+            k_bin_scatter_tiles<3><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_codes, g.bin_off, (int)g.NB);
+        else
+            k_bin_scatter_tiles<2><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_codes, g.bin_off, (int)g.NB);
+        count_launch(3);
     } else {
         TGCU_CUDA(cudaMemsetAsync(g.bin_count, 0, sizeof(int) * g.NB, s));
         const int pblocks = grid_blocks(n, 256, 148 * 16);
