@@ -278,22 +278,25 @@ __global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta,
             if (lane >= o2) x += y;
         }
         const int block_sum = __shfl_sync(0xffffffffu, x, 31);
+        // publish this CTA's aggregate, then add up every predecessor's
+        // (all CTAs are co-resident and publish before looking back)
         if (lane == 0) {
-            int prev = 0;
-            if (blockIdx.x > 0) {
-                volatile int* ch = chain;
-                while (ch[2 * (blockIdx.x - 1)] != epoch) {
-                }
-                __threadfence();
-                prev = ch[2 * (blockIdx.x - 1) + 1];
-            }
-            chain[2 * blockIdx.x + 1] = prev + block_sum;
+            chain[2 * blockIdx.x + 1] = block_sum;
             __threadfence();
             atomicExch(&chain[2 * blockIdx.x], epoch);
-            carry = prev;
         }
-        __syncwarp();
-        const int c0 = __shfl_sync(0xffffffffu, lane == 0 ? carry : 0, 0);
+        int prev = 0;
+        volatile int* ch = chain;
+        for (int j = lane; j < (int)blockIdx.x; j += 32) {
+            while (ch[2 * j] != epoch) {
+            }
+            __threadfence();
+            prev += ch[2 * j + 1];
+        }
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) prev += __shfl_xor_sync(0xffffffffu, prev, o2);
+        (void)carry;
+        const int c0 = prev;
         if (lane < nb) off[b0 + lane] = c0 + x - t;
         if (blockIdx.x == gridDim.x - 1 && lane == 0) off[NB] = c0 + block_sum;
     }
