@@ -188,6 +188,32 @@ int tgcu_adam_download_f64(tgcu_grid* g, double* m, double* v, int64_t n);
  * TGCU_ASYNC; "stage 0 step k" / "index i" in the message). out may be NULL. */
 int tgcu_train_step(tgcu_grid* g, const float* samples, int64_t n, const tgcu_loss_config* cfg,
                     tgcu_loss_terms* out, int flags, void* stream);
+/* ---- multi-GPU z-slab training (owner computes) ----
+ * A slab grid holds the brick layers [zb_lo, zb_hi) (bricks of 8^3 vertices)
+ * of the global 3D spec: it owns (and Adam-updates) vertex planes
+ * [8*zb_lo, min(8*zb_hi, res_z)) and stores one extra halo plane below and
+ * above. Every rank is given the full global batch; its binning keeps the
+ * points whose cells touch its owned vertices (those in a slab-boundary cell
+ * layer go to both ranks). A step is
+ *   tgcu_slab_step_begin -> sum the 5 doubles at *partials over ranks
+ *   (recon, eik, tv, nan flag, bad-grad flag; e.g. NCCL all-reduce in place)
+ *   -> tgcu_slab_step_finish(reduced) -> exchange halo planes.
+ * Gradients are never exchanged: each is computed by its owner; after the
+ * commit each rank sends its boundary owned planes of the new parameters to
+ * its neighbours (tgcu_slab_halo). Slab grids are training-only. */
+int tgcu_grid_create_slab(const tgcu_grid_spec* global_spec, int zb_lo, int zb_hi, const tgcu_init_options* opts,
+                          int device, tgcu_grid** out);
+int tgcu_slab_info(const tgcu_grid* g, int* z_store_lo, int* z_store_n, int* z_own_lo, int* z_own_hi,
+                   int* brick_layers);
+int tgcu_slab_step_begin(tgcu_grid* g, const float* samples, int64_t n_global, const tgcu_loss_config* cfg,
+                         double** partials, int flags, void* stream);
+int tgcu_slab_step_finish(tgcu_grid* g, const double* reduced, tgcu_loss_terms* out, int flags, void* stream);
+/* Device pointers (current parameters) of the planes to send to / receive
+ * from the lower and upper neighbour (NULL at the grid boundary), and the
+ * plane size in floats. */
+int tgcu_slab_halo(tgcu_grid* g, float** send_lo, float** send_hi, float** recv_lo, float** recv_hi,
+                   int64_t* plane_floats);
+
 /* Wait for the grid's outstanding async work and report any sticky error.
  * If last_terms is not NULL it receives the most recent step's LossTerms. */
 int tgcu_sync(tgcu_grid* g, tgcu_loss_terms* last_terms);

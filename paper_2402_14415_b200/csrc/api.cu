@@ -187,7 +187,12 @@ int tgcu_coeff_count(int order, int dim, int* out) {
     });
 }
 
-int tgcu_grid_create(const tgcu_grid_spec* spec, const tgcu_init_options* opts_in, int device, tgcu_grid** out) {
+// init_grid for a full grid (zb_lo = zb_hi = -1) or for the z-slab of brick
+// layers [zb_lo, zb_hi) of the global spec (multi-GPU owner-computes
+// training): the slab stores vertex planes [8*zb_lo - 1, 8*zb_hi] clipped to
+// the grid (its owned planes plus one halo plane on each side).
+static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts_in, int device, int zb_lo,
+                       int zb_hi, tgcu_grid** out) {
     *out = nullptr;
     tgcu_grid* h = nullptr;
     const int rc = guard([&] {
@@ -198,8 +203,20 @@ int tgcu_grid_create(const tgcu_grid_spec* spec, const tgcu_init_options* opts_i
         tgcu_init_options opts{TGCU_INIT_ZEROS, 0.0, 1e-4, 0, 4ull << 30};
         if (opts_in) opts = *opts_in;
         const int K = coeff_count_of(s.order, s.dim);
-        int64_t V = 1;
-        for (int a = 0; a < s.dim; ++a) V *= s.res[a];
+        int64_t Vg = 1;
+        for (int a = 0; a < s.dim; ++a) Vg *= s.res[a];
+        const int B = s.dim == 3 ? kBrick3 : kBrick2;
+        const bool slab = zb_lo >= 0;
+        const int nbz_global = s.dim == 3 ? (s.res[2] + B - 1) / B : 1;
+        int zoff = 0, zstore = s.dim == 3 ? s.res[2] : 1;
+        if (slab) {
+            require(s.dim == 3, "slab grids need dim 3");
+            require(zb_lo < zb_hi && zb_hi <= nbz_global, "slab brick layers out of range");
+            zoff = std::max(0, B * zb_lo - 1);
+            const int zend = std::min(s.res[2], B * zb_hi + 1);
+            zstore = zend - zoff;
+        }
+        const int64_t V = (int64_t)s.res[0] * (s.dim == 3 ? (int64_t)s.res[1] * zstore : s.res[1]);
         const uint64_t bytes = (uint64_t)(V * K) * sizeof(double);
         if (bytes > opts.memory_cap_bytes)
             throw Error(TGCU_ERR_RESOURCE, "init_grid: " + std::to_string(bytes) + " bytes exceeds memory cap of " +
@@ -215,6 +232,7 @@ int tgcu_grid_create(const tgcu_grid_spec* spec, const tgcu_init_options* opts_i
         g.V = V;
         g.NC = V * K;
         g.device = device;
+        g.slab = slab;
         TGCU_CUDA(cudaSetDevice(device));
         DevSpec& d = g.ds;
         for (int a = 0; a < 3; ++a) {
@@ -229,6 +247,17 @@ int tgcu_grid_create(const tgcu_grid_spec* spec, const tgcu_init_options* opts_i
         }
         d.sy = s.res[0];
         d.sz = (long long)s.res[0] * (s.dim == 3 ? s.res[1] : 1);
+        d.zoff = zoff;
+        d.zstore = zstore;
+        // TV normaliser P*K of the global grid (sdf_loss.cpp:161-170).
+        double P = 0.0;
+        for (int a = 0; a < s.dim; ++a) {
+            double np = s.res[a] - 1;
+            for (int b2 = 0; b2 < s.dim; ++b2)
+                if (b2 != a) np *= s.res[b2];
+            P += np;
+        }
+        g.tv_inv_norm = 1.0 / (P * K);
         // Parameters now; the ping-pong copy and the Adam moments on first
         // optimiser use (ensure_optimizer), so query-only grids cost 4 B/coeff.
         TGCU_CUDA(cudaMalloc(&g.p[0], sizeof(float) * g.NC));
@@ -239,31 +268,38 @@ int tgcu_grid_create(const tgcu_grid_spec* spec, const tgcu_init_options* opts_i
         st0.bad_grad = ULLONG_MAX;
         TGCU_CUDA(cudaMemcpy(g.st, &st0, sizeof(Status), cudaMemcpyHostToDevice));
         // Brick decomposition (train.cu / query.cu).
-        const int B = s.dim == 3 ? kBrick3 : kBrick2;
         g.NB = 1;
+        g.zb_global = nbz_global;
         for (int a = 0; a < 3; ++a) {
             g.brick[a] = a < s.dim ? B : 1;
             g.nb[a] = a < s.dim ? (s.res[a] + B - 1) / B : 1;
-            g.NB *= g.nb[a];
         }
+        if (slab) {
+            g.zb0 = zb_lo;
+            g.nb[2] = zb_hi - zb_lo;
+        }
+        for (int a = 0; a < 3; ++a) g.NB *= g.nb[a];
         TGCU_CUDA(cudaMalloc(&g.bin_count, sizeof(int) * (g.NB + 1)));
         TGCU_CUDA(cudaMalloc(&g.bin_off, sizeof(int) * (g.NB + 1)));
         TGCU_CUDA(cudaMalloc(&g.bin_cursor, sizeof(int) * (g.NB + 1)));
         TGCU_CUDA(cudaMalloc(&g.partials, sizeof(double) * 4 * g.NB));
         TGCU_CUDA(cudaMalloc(&g.d_trace, sizeof(tgcu_loss_terms) * kTraceCap));
+        TGCU_CUDA(cudaMalloc(&g.slab_red, sizeof(double) * 8));
         TGCU_CUDA(cudaMallocHost(&g.h_terms, sizeof(tgcu_loss_terms)));
         // init_grid modes (taylor_grid.cpp:174-186).
         float* p = g.p[0];
         TGCU_CUDA(cudaMemset(p, 0, sizeof(float) * g.NC));
+        const int64_t goff = (int64_t)zoff * d.sz * K;  // this slab's first coefficient in the global order
         if (opts.mode == TGCU_INIT_CONSTANT) {
             launch_fill_f0(g, p, (float)opts.constant, 0);
         } else if (opts.mode == TGCU_INIT_SMALL_UNIFORM) {
             std::vector<float> hbuf(g.NC);
             HostRng r(opts.seed);
+            for (int64_t i = 0; i < goff; ++i) r.next();  // global stream, this slab's window
             for (int64_t i = 0; i < g.NC; ++i) hbuf[i] = (float)r.uniform(-opts.epsilon, opts.epsilon);
             TGCU_CUDA(cudaMemcpy(p, hbuf.data(), sizeof(float) * g.NC, cudaMemcpyHostToDevice));
         } else if (opts.mode == TGCU_INIT_HASH_GAUSSIAN) {
-            launch_hash_gaussian(p, g.NC, opts.seed, opts.epsilon, 0);
+            launch_hash_gaussian(p, g.NC, opts.seed, opts.epsilon, goff, 0);
         }
         TGCU_CUDA(cudaDeviceSynchronize());
     });
@@ -272,6 +308,31 @@ int tgcu_grid_create(const tgcu_grid_spec* spec, const tgcu_init_options* opts_i
         return rc;
     }
     *out = h;
+    return TGCU_OK;
+}
+
+int tgcu_grid_create(const tgcu_grid_spec* spec, const tgcu_init_options* opts_in, int device, tgcu_grid** out) {
+    return create_grid(spec, opts_in, device, -1, -1, out);
+}
+
+int tgcu_grid_create_slab(const tgcu_grid_spec* spec, int zb_lo, int zb_hi, const tgcu_init_options* opts,
+                          int device, tgcu_grid** out) {
+    if (zb_lo < 0) {
+        *out = nullptr;
+        return set_err(TGCU_ERR_INVALID_ARGUMENT, "tgcu_grid_create_slab: negative brick layer");
+    }
+    return create_grid(spec, opts, device, zb_lo, zb_hi, out);
+}
+
+int tgcu_slab_info(const tgcu_grid* h, int* z_store_lo, int* z_store_n, int* z_own_lo, int* z_own_hi,
+                   int* brick_layers) {
+    const Grid& g = h->g;
+    const int B = g.spec.dim == 3 ? kBrick3 : kBrick2;
+    if (z_store_lo) *z_store_lo = g.ds.zoff;
+    if (z_store_n) *z_store_n = g.ds.zstore;
+    if (z_own_lo) *z_own_lo = g.slab ? B * g.zb0 : 0;
+    if (z_own_hi) *z_own_hi = g.slab ? std::min(g.spec.res[2], B * (g.zb0 + g.nb[2])) : g.ds.zstore;
+    if (brick_layers) *brick_layers = g.zb_global;
     return TGCU_OK;
 }
 
@@ -297,6 +358,7 @@ int tgcu_grid_destroy(tgcu_grid* h) {
     cudaFree(g.bin_chain);
     cudaFree(g.partials);
     cudaFree(g.d_trace);
+    cudaFree(g.slab_red);
     cudaFreeHost(g.h_terms);
     cudaFree(g.staging);
     cudaFree(g.scratch_d);
@@ -680,7 +742,8 @@ int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
             ensure_grad(g);
             gout = g.grad;
         }
-        launch_train_step(g, ds, n, *cfg, in_idx, g.steps_launched, 1.0 / bc1, 1.0 / bc2, t_after, gout, s);
+        require(!g.slab, "train_step: slab grids step with tgcu_slab_step_begin/finish");
+        launch_train_step(g, ds, n, *cfg, in_idx, g.steps_launched, 1.0 / bc1, 1.0 / bc2, t_after, gout, nullptr, s);
         // Optimistic commit; a failed step is rolled back by raise_sticky().
         g.cur = 1 - in_idx;
         g.t = t_after;
@@ -695,6 +758,85 @@ int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
             raise_sticky(g);
             if (out) *out = *g.h_terms;
         }
+    });
+}
+
+int tgcu_slab_step_begin(tgcu_grid* h, const float* samples, int64_t n, const tgcu_loss_config* cfg,
+                         double** partials, int flags, void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(g.slab, "slab_step_begin: not a slab grid");
+        require(cfg != nullptr && partials != nullptr, "slab_step_begin: NULL argument");
+        require(cfg->lambda1 >= 0.0 && cfg->lambda2 >= 0.0, "LossConfig: lambda weights must be >= 0");
+        require(cfg->k > 0.0, "LossConfig: weight sharpness k must be > 0");
+        require(n > 0, "total_loss: empty batch");
+        cudaStream_t s = as_stream(stream);
+        ensure_optimizer(g);
+        const float4* ds = reinterpret_cast<const float4*>(samples);
+        if (flags & TGCU_HOST) {
+            ensure_staging(g, 4 * n);
+            TGCU_CUDA(cudaMemcpyAsync(g.staging, samples, sizeof(float) * 4 * n, cudaMemcpyHostToDevice, s));
+            ds = reinterpret_cast<const float4*>(g.staging);
+        }
+        const int64_t t_after = g.t + 1;
+        const double bc1 = 1.0 - std::pow(g.adam.beta1, (double)t_after);
+        const double bc2 = 1.0 - std::pow(g.adam.beta2, (double)t_after);
+        float* gout = nullptr;
+        if (flags & TGCU_EXPORT_GRAD) {
+            ensure_grad(g);
+            gout = g.grad;
+        }
+        g.slab_in_idx = g.cur;
+        g.slab_step = g.steps_launched;
+        g.slab_t_after = t_after;
+        g.slab_n = n;
+        g.slab_cfg = *cfg;
+        launch_train_step(g, ds, n, *cfg, g.cur, g.steps_launched, 1.0 / bc1, 1.0 / bc2, t_after, gout, g.slab_red, s);
+        *partials = g.slab_red;
+    });
+}
+
+int tgcu_slab_step_finish(tgcu_grid* h, const double* reduced, tgcu_loss_terms* out, int flags, void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(g.slab, "slab_step_finish: not a slab grid");
+        cudaStream_t s = as_stream(stream);
+        launch_slab_finish(g, reduced ? reduced : g.slab_red, g.slab_cfg, g.slab_in_idx, g.slab_step,
+                           g.slab_t_after, g.slab_n, s);
+        g.cur = 1 - g.slab_in_idx;
+        g.t = g.slab_t_after;
+        g.steps_launched += 1;
+        if (out) {
+            TGCU_CUDA(cudaMemcpyAsync(g.h_terms, g.d_trace + ((g.steps_launched - 1) % kTraceCap),
+                                      sizeof(tgcu_loss_terms), cudaMemcpyDeviceToHost, s));
+        }
+        if (!(flags & TGCU_ASYNC) || out) {
+            TGCU_CUDA(cudaStreamSynchronize(s));
+            raise_sticky(g);
+            if (out) *out = *g.h_terms;
+        }
+    });
+}
+
+int tgcu_slab_halo(tgcu_grid* h, float** send_lo, float** send_hi, float** recv_lo, float** recv_hi,
+                   int64_t* plane_floats) {
+    return guard([&] {
+        Grid& g = h->g;
+        require(g.slab, "slab_halo: not a slab grid");
+        const int B = kBrick3;
+        const int own_lo = B * g.zb0;
+        const int own_hi = std::min(g.spec.res[2], B * (g.zb0 + g.nb[2]));
+        const int64_t pf = g.ds.sz * g.K;
+        float* p = g.p[g.cur];
+        auto plane = [&](int z) { return p + (int64_t)(z - g.ds.zoff) * pf; };
+        const bool has_lo = own_lo > 0, has_hi = own_hi < g.spec.res[2];
+        *send_lo = has_lo ? plane(own_lo) : nullptr;
+        *recv_lo = has_lo ? plane(own_lo - 1) : nullptr;
+        *send_hi = has_hi ? plane(own_hi - 1) : nullptr;
+        *recv_hi = has_hi ? plane(own_hi) : nullptr;
+        *plane_floats = pf;
     });
 }
 

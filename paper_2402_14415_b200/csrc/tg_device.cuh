@@ -28,6 +28,8 @@ struct DevSpec {
     float hf[3];
     float inv_hf[3];
     long long sy, sz;  // vertex strides (x fastest)
+    int zoff;          // first z vertex plane stored (slab grids; 0 otherwise)
+    int zstore;        // z vertex planes stored
 };
 
 // Device-side status / error word of a grid (sticky across async calls).

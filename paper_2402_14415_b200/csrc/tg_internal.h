@@ -62,6 +62,16 @@ struct Grid {
     Status* st_host = nullptr;  // pinned mirror
 
     // Bricks of the fused step / binned query.
+    // Slab grids (multi-GPU z partition): brick layers [zb0, zb0 + nb[2]) of
+    // the global grid spec; stored vertex planes [ds.zoff, ds.zoff + ds.zstore).
+    bool slab = false;
+    int zb0 = 0;
+    int zb_global = 0;            // brick layers of the global grid
+    double tv_inv_norm = 0.0;     // 1 / (P*K) of the global grid
+    double* slab_red = nullptr;   // 8 doubles: local sums of the pending slab step
+    int slab_in_idx = 0;
+    int64_t slab_step = 0, slab_t_after = 0, slab_n = 0;
+    tgcu_loss_config slab_cfg{};
     int brick[3] = {1, 1, 1};
     int nb[3] = {1, 1, 1};
     int64_t NB = 1;
@@ -121,12 +131,14 @@ void launch_adam_update(Grid& g, const float* grad, double inv_bc1, double inv_b
 // Fused step: binning + brick kernel + finalize (train.cu).
 void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_loss_config& cfg, int in_idx,
                        int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
-                       cudaStream_t s);
+                       double* slab_out, cudaStream_t s);
+void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& cfg, int in_idx, int64_t step,
+                        int64_t t_after, int64_t n, cudaStream_t s);
 void launch_f64_to_f32(const double* src, float* dst, int64_t n, cudaStream_t s);
 void launch_f32_to_f64(const float* src, double* dst, int64_t n, cudaStream_t s);
 void launch_all_finite(const float* src, int64_t n, unsigned long long* flag, cudaStream_t s);
 void launch_fill_f0(Grid& g, float* dst, float value, cudaStream_t s);
-void launch_hash_gaussian(float* dst, int64_t n, uint64_t seed, double sigma, cudaStream_t s);
+void launch_hash_gaussian(float* dst, int64_t n, uint64_t seed, double sigma, int64_t goff, cudaStream_t s);
 void launch_hash_points(float* out, int64_t n, int dim, uint64_t seed, double lo, double hi, cudaStream_t s);
 
 }  // namespace tgcu

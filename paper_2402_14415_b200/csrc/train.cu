@@ -57,29 +57,42 @@ struct BinArgs {
     int* cursor;
     float4* binned;
     Status* st;
+    int zb0;  // first brick layer (slab grids)
 };
 
-// Bricks needing the point: per axis the brick of its cell and, for a cell in
-// the brick's last layer, the next brick too. Returns the count (0 = NaN).
+// Brick code of a point: its cell's brick coordinates (9 bits per axis) and
+// the per-axis "also the next brick" mask (bits 27..29), or -1 for a NaN
+// coordinate. Brick coordinates are global; code_bricks() maps them to this
+// grid's brick indices, dropping bricks outside a slab grid's layers.
 template <int DIM>
-__device__ __forceinline__ int point_bricks(const DevSpec& s, const int* nb, const float4& q, int* out) {
+__device__ __forceinline__ int point_brick_code(const DevSpec& s, const int* nb, const float4& q) {
     constexpr int B = BrickShape<DIM>::B;
     const float pf[3] = {q.x, q.y, q.z};
-    int lo[3] = {0, 0, 0}, two[3] = {0, 0, 0};
+    int lo[3] = {0, 0, 0}, mask = 0;
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
         const double x = (double)pf[a];
-        if (isnan(x)) return 0;
+        if (isnan(x)) return -1;
         double local;
         const int c = locate_axis(s, a, x, local);
         lo[a] = c / B;
-        two[a] = (c % B) == B - 1 ? 1 : 0;
+        mask |= ((c % B) == B - 1 ? 1 : 0) << a;
     }
+    (void)nb;
+    return lo[0] | (lo[1] << 9) | (lo[2] << 18) | (mask << 27);
+}
+
+template <int DIM>
+__device__ __forceinline__ int code_bricks(int code, const int* nb, int zb0, int* out) {
+    const int bx = code & 511, by = (code >> 9) & 511, bz = (code >> 18) & 511, mask = code >> 27;
     int m = 0;
-    for (int dz = 0; dz <= (DIM == 3 ? two[2] : 0); ++dz)
-        for (int dy = 0; dy <= two[1]; ++dy)
-            for (int dx = 0; dx <= two[0]; ++dx)
-                out[m++] = ((DIM == 3 ? (lo[2] + dz) * nb[1] : 0) + lo[1] + dy) * nb[0] + lo[0] + dx;
+    for (int dz = 0; dz <= (DIM == 3 ? (mask >> 2) & 1 : 0); ++dz) {
+        const int lz = bz + dz - zb0;
+        if (DIM == 3 && (lz < 0 || lz >= nb[2])) continue;
+        for (int dy = 0; dy <= ((mask >> 1) & 1); ++dy)
+            for (int dx = 0; dx <= (mask & 1); ++dx)
+                out[m++] = ((DIM == 3 ? lz * nb[1] : 0) + by + dy) * nb[0] + bx + dx;
+    }
     return m;
 }
 
@@ -88,9 +101,13 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs A) {
     if (A.st->error) return;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < A.n;
          i += (long long)gridDim.x * blockDim.x) {
+        const int code = point_brick_code<DIM>(A.s, A.nb, A.pts[i]);
+        if (code < 0) {
+            atomicMin(&A.st->nan_point, (unsigned long long)i);
+            continue;
+        }
         int br[8];
-        const int m = point_bricks<DIM>(A.s, A.nb, A.pts[i], br);
-        if (m == 0) atomicMin(&A.st->nan_point, (unsigned long long)i);
+        const int m = code_bricks<DIM>(code, A.nb, A.zb0, br);
         for (int k = 0; k < m; ++k) atomicAdd(&A.count[br[k]], 1);
     }
 }
@@ -143,8 +160,10 @@ __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs A) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < A.n;
          i += (long long)gridDim.x * blockDim.x) {
         const float4 q = A.pts[i];
+        const int code = point_brick_code<DIM>(A.s, A.nb, q);
+        if (code < 0) continue;
         int br[8];
-        const int m = point_bricks<DIM>(A.s, A.nb, q, br);
+        const int m = code_bricks<DIM>(code, A.nb, A.zb0, br);
         for (int k = 0; k < m; ++k) {
             const int slot = atomicAdd(&A.cursor[br[k]], 1);
             A.binned[slot] = q;
@@ -166,36 +185,6 @@ constexpr int kBinPer = kBinTile / kBinThreads;  // points per thread
 constexpr int kBinSmemMax = 16384;  // bricks
 constexpr int kColBricks = 32;
 constexpr int kMaxBinTiles = 512;
-
-// Base brick of the point and the per-axis "also next brick" mask (bit 28+a),
-// or -1 for a NaN coordinate.
-template <int DIM>
-__device__ __forceinline__ int point_brick_code(const DevSpec& s, const int* nb, const float4& q) {
-    constexpr int B = BrickShape<DIM>::B;
-    const float pf[3] = {q.x, q.y, q.z};
-    int lo[3] = {0, 0, 0}, mask = 0;
-#pragma unroll
-    for (int a = 0; a < DIM; ++a) {
-        const double x = (double)pf[a];
-        if (isnan(x)) return -1;
-        double local;
-        const int c = locate_axis(s, a, x, local);
-        lo[a] = c / B;
-        mask |= ((c % B) == B - 1 ? 1 : 0) << a;
-    }
-    return (((DIM == 3 ? lo[2] * nb[1] : 0) + lo[1]) * nb[0] + lo[0]) | (mask << 28);
-}
-
-template <int DIM>
-__device__ __forceinline__ int code_bricks(int code, const int* nb, int* out) {
-    const int base = code & 0x0fffffff, mask = code >> 28;
-    int m = 0;
-    const int sy = nb[0], sz = nb[0] * nb[1];
-    for (int dz = 0; dz <= (DIM == 3 ? (mask >> 2) & 1 : 0); ++dz)
-        for (int dy = 0; dy <= ((mask >> 1) & 1); ++dy)
-            for (int dx = 0; dx <= (mask & 1); ++dx) out[m++] = base + dz * sz + dy * sy + dx;
-    return m;
-}
 
 template <int DIM>
 __global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __restrict__ H, int* __restrict__ codes,
@@ -222,7 +211,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __rest
             continue;
         }
         int br[8];
-        const int m = code_bricks<DIM>(code, A.nb, br);
+        const int m = code_bricks<DIM>(code, A.nb, A.zb0, br);
         for (int j = 0; j < m; ++j) atomicAdd(&hist[br[j]], 1);
     }
     __syncthreads();
@@ -325,7 +314,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_scatter_tiles(BinArgs A, co
     for (int k = 0; k < kBinPer; ++k) {
         if (cd[k] < 0) continue;
         int br[8];
-        const int m = code_bricks<DIM>(cd[k], A.nb, br);
+        const int m = code_bricks<DIM>(cd[k], A.nb, A.zb0, br);
         for (int j = 0; j < m; ++j) A.binned[atomicAdd(&cur[br[j]], 1)] = q[k];
     }
 }
@@ -348,6 +337,7 @@ struct StepArgs {
     double* partials;  // NB x 4: recon, eik, tv, home points
     Status* st;
     float* grad_out;   // optional: full gradient (validation mode, TGCU_EXPORT_GRAD)
+    int zb0;           // first brick layer of this grid (slab grids; 0 otherwise)
 };
 
 template <int NCELL, int NT>
@@ -431,14 +421,14 @@ __device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, flo
     constexpr unsigned OBYTES = B * K * 4;
     constexpr int OROWS = DIM == 3 ? B * B : B;
     static_assert(L::TROWS + 2 * OROWS <= S::NT, "one staging row per thread");
-    const long long nc_bytes = (long long)A.s.res[0] * A.s.res[1] * (DIM == 3 ? A.s.res[2] : 1) * K * 4;
+    const long long nc_bytes = (long long)A.s.res[0] * A.s.res[1] * (DIM == 3 ? A.s.zstore : 1) * K * 4;
     unsigned tx_tile = 0, tx_mv = 0;
     if (tid < L::TROWS) {
         const int r = tid;
         const int ty = DIM == 3 ? r % T : r, tz = DIM == 3 ? r / T : 0;
         const int vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
         if (vy >= 0 && vy < A.s.res[1] && (DIM == 2 || (vz >= 0 && vz < A.s.res[2]))) {
-            const long long firstv = (DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0] - 1;
+            const long long firstv = (DIM == 3 ? (long long)(vz - A.s.zoff) * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0] - 1;
             const long long src = firstv * K * 4 - L::SHF * 4;
             float* dst = tile + r * L::TROWF;
             if ((src & 15) == 0 && src >= 0 && src + TBYTES <= nc_bytes) {
@@ -460,7 +450,7 @@ __device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, flo
         const int ly = r % B, lz = DIM == 3 ? r / B : 0;
         const int vy = o[1] + ly, vz = o[2] + lz;
         if (vy < A.s.res[1] && (DIM == 2 || vz < A.s.res[2])) {
-            const long long v0 = (DIM == 3 ? (long long)vz * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0];
+            const long long v0 = (DIM == 3 ? (long long)(vz - A.s.zoff) * A.s.sz : 0LL) + (long long)vy * A.s.sy + o[0];
             const long long src = v0 * K * 4;
             const float* gsrc = which ? A.v_in : A.m_in;
             float* dst = mvs + which * S::NOWN * K + r * B * K;
@@ -509,7 +499,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
     constexpr int NW = NT / 32;
     const int nbx = A.nb[0], nby = A.nb[1];
     const int b = blockIdx.x;
-    const int o[3] = {(b % nbx) * B, ((b / nbx) % nby) * B, DIM == 3 ? (b / (nbx * nby)) * B : 0};
+    const int o[3] = {(b % nbx) * B, ((b / nbx) % nby) * B, DIM == 3 ? (A.zb0 + b / (nbx * nby)) * B : 0};
 
     if (tid == 0) {
         mbar_init(&bars[0], NT);
@@ -738,7 +728,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
         for (int a = 0; a < DIM; ++a) vok &= g3[a] < A.s.res[a];
         if (vok) {
             const long long gidx =
-                ((DIM == 3 ? (long long)g3[2] * A.s.sz : 0LL) + (long long)g3[1] * A.s.sy + g3[0]) * K;
+                ((DIM == 3 ? (long long)(g3[2] - A.s.zoff) * A.s.sz : 0LL) + (long long)g3[1] * A.s.sy + g3[0]) * K;
             const float* tp = tile + L::at(1 + l3[0], 1 + l3[1], DIM == 3 ? 1 + l3[2] : 0);
             float* gs = Gs + v * K;
             float* mm = mvs + v * K;
@@ -832,7 +822,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
             const int ly = r % B, lz = DIM == 3 ? r / B : 0;
             const int gy = o[1] + ly, gz = o[2] + lz;
             if (gy < A.s.res[1] && (DIM == 2 || gz < A.s.res[2])) {
-                const long long gb = ((DIM == 3 ? (long long)gz * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K;
+                const long long gb = ((DIM == 3 ? (long long)(gz - A.s.zoff) * A.s.sz : 0LL) + (long long)gy * A.s.sy + o[0]) * K;
                 const float* src = (which == 0 ? uni : mvs + (which - 1) * S::NOWN * K) + r * ROWF;
                 float* dst = (which == 0 ? A.p_out : (which == 1 ? A.m_out : A.v_out)) + gb;
                 if ((gb & 3) == 0 && (rowf & 3) == 0) {
@@ -871,53 +861,74 @@ struct FinArgs {
     long long step;
     int in_idx;
     long long t_after;
+    double* slab_out;       // slab phase 1: write local {recon, eik, tv, has_nan, has_bad}, no commit
+    const double* reduced;  // slab phase 2: globally summed {recon, eik, tv, n_nan, n_bad}
 };
 
+// Reduce the per-brick partials in a fixed order, apply the reference's error
+// order (NaN point -> non-finite loss -> non-finite gradient) and commit.
 __global__ void __launch_bounds__(1024) k_step_finalize(FinArgs F) {
     __shared__ double red[3][32];
     if (F.st->error) return;
-    double a = 0.0, b = 0.0, c = 0.0;
-    for (int i = threadIdx.x; i < F.NB; i += blockDim.x) {
-        a += F.partials[4 * i];
-        b += F.partials[4 * i + 1];
-        c += F.partials[4 * i + 2];
-    }
-    a = warp_sum_d(a);
-    b = warp_sum_d(b);
-    c = warp_sum_d(c);
-    if ((threadIdx.x & 31) == 0) {
-        red[0][threadIdx.x >> 5] = a;
-        red[1][threadIdx.x >> 5] = b;
-        red[2][threadIdx.x >> 5] = c;
-    }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
     double recon = 0.0, eik = 0.0, tvs = 0.0;
-    for (int k = 0; k < 32; ++k) {
-        recon += red[0][k];
-        eik += red[1][k];
-        tvs += red[2][k];
+    if (!F.reduced) {
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int i = threadIdx.x; i < F.NB; i += blockDim.x) {
+            a += F.partials[4 * i];
+            b += F.partials[4 * i + 1];
+            c += F.partials[4 * i + 2];
+        }
+        a = warp_sum_d(a);
+        b = warp_sum_d(b);
+        c = warp_sum_d(c);
+        if ((threadIdx.x & 31) == 0) {
+            red[0][threadIdx.x >> 5] = a;
+            red[1][threadIdx.x >> 5] = b;
+            red[2][threadIdx.x >> 5] = c;
+        }
+        __syncthreads();
+        if (threadIdx.x != 0) return;
+        for (int k = 0; k < 32; ++k) {
+            recon += red[0][k];
+            eik += red[1][k];
+            tvs += red[2][k];
+        }
+    } else {
+        if (threadIdx.x != 0) return;
+        recon = F.reduced[0];
+        eik = F.reduced[1];
+        tvs = F.reduced[2];
     }
+    Status* st = F.st;
+    if (F.slab_out) {
+        F.slab_out[0] = recon;
+        F.slab_out[1] = eik;
+        F.slab_out[2] = tvs;
+        F.slab_out[3] = st->nan_point != ULLONG_MAX ? 1.0 : 0.0;
+        F.slab_out[4] = st->bad_grad != ULLONG_MAX ? 1.0 : 0.0;
+        return;
+    }
+    const bool any_nan = st->nan_point != ULLONG_MAX || (F.reduced && F.reduced[3] > 0.0);
+    const bool any_bad = st->bad_grad != ULLONG_MAX || (F.reduced && F.reduced[4] > 0.0);
     tgcu_loss_terms t;
     t.fit = recon / F.n;
     t.eik = F.want_eik ? eik / F.n : 0.0;
     t.tv = F.use_tv ? tvs * F.inv_norm : 0.0;
     t.total = t.fit + F.lambda1 * t.eik + F.lambda2 * t.tv;
     F.trace[F.step % kTraceCap] = t;
-    Status* st = F.st;
     int err = 0, kind = 0;
     long long idx = -1;
-    if (st->nan_point != ULLONG_MAX) {
+    if (any_nan) {
         err = TGCU_ERR_INVALID_ARGUMENT;
         kind = 1;
-        idx = (long long)st->nan_point;
+        idx = st->nan_point != ULLONG_MAX ? (long long)st->nan_point : -1;
     } else if (!isfinite(t.total)) {
         err = TGCU_ERR_NUMERICAL;
         kind = 2;
-    } else if (st->bad_grad != ULLONG_MAX) {
+    } else if (any_bad) {
         err = TGCU_ERR_NUMERICAL;
         kind = 3;
-        idx = (long long)st->bad_grad;
+        idx = st->bad_grad != ULLONG_MAX ? (long long)st->bad_grad : -1;
     }
     if (err) {
         st->error = err;
@@ -934,9 +945,31 @@ __global__ void __launch_bounds__(1024) k_step_finalize(FinArgs F) {
     st->bad_grad = ULLONG_MAX;
 }
 
+// Slab phase 2: commit with the globally reduced sums.
+void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& cfg, int in_idx, int64_t step,
+                        int64_t t_after, int64_t n, cudaStream_t s) {
+    FinArgs F{};
+    F.NB = (int)g.NB;
+    F.n = (double)n;
+    F.lambda1 = cfg.lambda1;
+    F.lambda2 = cfg.lambda2;
+    F.inv_norm = g.tv_inv_norm;
+    F.use_tv = cfg.use_tv;
+    F.want_eik = cfg.lambda1 > 0.0;
+    F.st = g.st;
+    F.trace = g.d_trace;
+    F.step = step;
+    F.in_idx = in_idx;
+    F.t_after = t_after;
+    F.reduced = reduced;
+    k_step_finalize<<<1, 32, 0, s>>>(F);
+    count_launch();
+    TGCU_CUDA(cudaGetLastError());
+}
+
 void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_loss_config& cfg, int in_idx,
                        int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
-                       cudaStream_t s) {
+                       double* slab_out, cudaStream_t s) {
     ensure_bins(g, n);
     BinArgs B;
     B.s = g.ds;
@@ -947,6 +980,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     B.cursor = g.bin_cursor;
     B.binned = g.binned;
     B.st = g.st;
+    B.zb0 = g.zb0;
     const int ncta_tiles = (int)((n + kBinTile - 1) / kBinTile);
     if (g.NB <= kBinSmemMax && ncta_tiles <= kMaxBinTiles) {
         const int ncta = ncta_tiles;
@@ -1001,15 +1035,8 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     A.L.eik_scale = cfg.lambda1;
     A.L.use_weighting = cfg.use_weighting;
     A.L.differentiate_weight = cfg.differentiate_weight;
-    // TV normaliser P*K (sdf_loss.cpp:161-170).
-    double P = 0.0;
-    for (int a = 0; a < g.spec.dim; ++a) {
-        double np = g.spec.res[a] - 1;
-        for (int b2 = 0; b2 < g.spec.dim; ++b2)
-            if (b2 != a) np *= g.spec.res[b2];
-        P += np;
-    }
-    const double inv_norm = 1.0 / (P * g.K);
+    // TV normaliser P*K over the global grid (sdf_loss.cpp:161-170).
+    const double inv_norm = g.tv_inv_norm;
     A.want_tv = cfg.use_tv ? 1 : 0;
     A.tv_gscale = (cfg.use_tv && cfg.lambda2 > 0.0) ? (float)(2.0 * cfg.lambda2 * inv_norm) : 0.0f;
     A.lr = (float)g.adam.lr;
@@ -1021,6 +1048,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     A.partials = g.partials;
     A.st = g.st;
     A.grad_out = grad_out;
+    A.zb0 = g.zb0;
     const bool eik = cfg.lambda1 > 0.0;
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
         constexpr size_t smem = BrickSmem<DIM, ORDER>::bytes;
@@ -1053,6 +1081,8 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     F.step = step;
     F.in_idx = in_idx;
     F.t_after = t_after;
+    F.slab_out = slab_out;
+    F.reduced = nullptr;
     k_step_finalize<<<1, 1024, 0, s>>>(F);
     count_launch(2);
     TGCU_CUDA(cudaGetLastError());

@@ -333,10 +333,12 @@ __device__ __forceinline__ double hash_uniform(unsigned long long seed, unsigned
     return (double)(splitmix64(seed * 0x2545F4914F6CDD1DULL + i) >> 11) * 0x1.0p-53;
 }
 
-__global__ void k_hash_gaussian(float* __restrict__ p, long long n, unsigned long long seed, float sigma) {
+__global__ void k_hash_gaussian(float* __restrict__ p, long long n, unsigned long long seed, float sigma,
+                                long long goff) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        double u1 = hash_uniform(seed, 2 * i);
-        const double u2 = hash_uniform(seed, 2 * i + 1);
+        const long long gi = i + goff;  // global coefficient index (slab grids)
+        double u1 = hash_uniform(seed, 2 * gi);
+        const double u2 = hash_uniform(seed, 2 * gi + 1);
         if (u1 <= 0.0) u1 = 0x1.0p-53;
         p[i] = sigma * (float)(sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
     }
@@ -351,8 +353,8 @@ __global__ void k_hash_points(float* __restrict__ out, long long n, int dim, uns
     }
 }
 
-void launch_hash_gaussian(float* dst, int64_t n, uint64_t seed, double sigma, cudaStream_t s) {
-    k_hash_gaussian<<<grid_blocks(n, 256, 148 * 64), 256, 0, s>>>(dst, n, seed, (float)sigma);
+void launch_hash_gaussian(float* dst, int64_t n, uint64_t seed, double sigma, int64_t goff, cudaStream_t s) {
+    k_hash_gaussian<<<grid_blocks(n, 256, 148 * 64), 256, 0, s>>>(dst, n, seed, (float)sigma, goff);
     count_launch();
     TGCU_CUDA(cudaGetLastError());
 }

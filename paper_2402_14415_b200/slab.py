@@ -1,0 +1,241 @@
+"""Multi-GPU z-slab training, owner computes.
+
+The global grid is cut into slabs of whole brick layers (bricks of 8^3
+vertices). Rank r owns the vertex planes of its brick layers and the Adam
+state of those vertices; it stores one halo plane below and above. Every rank
+is given the full global batch and keeps the points whose cells touch its
+owned vertices (a point in a slab-boundary cell layer is used by both ranks,
+exactly as a point in a brick-boundary cell layer is binned into both bricks
+on one GPU). Per step:
+
+    partials = slab.begin(batch)          # bin + fused brick kernel, local sums
+    all_reduce(partials)                  # {recon, eik, tv, nan flag, bad flag}
+    terms = slab.finish(partials)         # same commit decision on every rank
+    halo exchange of boundary parameter planes (send/recv with the neighbours)
+
+No gradient is exchanged: each gradient is computed by its owner. The loss
+scale 1/N and the TV normaliser P*K are global (sdf_loss.cpp:161-170), so the
+slab steps reproduce the single-grid step.
+
+The partition helpers are plain numpy so the CPU tests (gloo, world size 2)
+exercise the same rules with the oracle as compute engine.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import (TGCU_ASYNC, TGCU_HOST, AdamConfig, GridSpec, InitOptions, LossConfig, LossTerms, _check, _ptr, _Terms,
+               lib)
+
+BRICK = 8
+
+
+def brick_layers(res_z: int) -> int:
+    return (res_z + BRICK - 1) // BRICK
+
+
+def slab_ranges(nbz: int, world: int, weights: Optional[np.ndarray] = None) -> List[Tuple[int, int]]:
+    """Split nbz brick layers into `world` contiguous ranges. With per-layer
+    weights (e.g. point counts) the split balances weight + the dense work."""
+    if world > nbz:
+        raise ValueError(f"slab_ranges: {world} ranks for {nbz} brick layers")
+    if weights is None:
+        base, rem = divmod(nbz, world)
+        out, lo = [], 0
+        for r in range(world):
+            hi = lo + base + (1 if r < rem else 0)
+            out.append((lo, hi))
+            lo = hi
+        return out
+    w = np.asarray(weights, dtype=np.float64)
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    out, lo = [], 0
+    for r in range(world):
+        if r == world - 1:
+            hi = nbz
+        else:
+            target = cum[-1] * (r + 1) / world
+            hi = int(np.searchsorted(cum, target))
+            hi = max(hi, lo + 1)
+            hi = min(hi, nbz - (world - 1 - r))
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def owned_planes(res_z: int, zb_lo: int, zb_hi: int) -> Tuple[int, int]:
+    return BRICK * zb_lo, min(res_z, BRICK * zb_hi)
+
+
+def stored_planes(res_z: int, zb_lo: int, zb_hi: int) -> Tuple[int, int]:
+    return max(0, BRICK * zb_lo - 1), min(res_z, BRICK * zb_hi + 1)
+
+
+def point_cells_z(spec: GridSpec, z: np.ndarray) -> np.ndarray:
+    """The reference's locate rule on the z axis (grid_spec.cpp:45-69), fp64."""
+    lo = spec.origin[2]
+    hi = spec.origin[2] + spec.extent[2]
+    h = spec.extent[2] / (spec.resolution[2] - 1)
+    p = np.clip(np.asarray(z, dtype=np.float64), lo, hi)
+    c = np.floor((p - lo) / h).astype(np.int64)
+    return np.clip(c, 0, spec.resolution[2] - 2)
+
+
+def slab_point_mask(spec: GridSpec, points: np.ndarray, zb_lo: int, zb_hi: int) -> np.ndarray:
+    """Points whose cell touches a vertex owned by brick layers [zb_lo, zb_hi):
+    cells [8*zb_lo - 1, 8*zb_hi - 1] along z."""
+    c = point_cells_z(spec, np.asarray(points)[:, 2])
+    return (c >= BRICK * zb_lo - 1) & (c <= BRICK * zb_hi - 1)
+
+
+def home_point_mask(spec: GridSpec, points: np.ndarray, zb_lo: int, zb_hi: int) -> np.ndarray:
+    """Points whose loss terms this slab sums (cell's brick layer is its own)."""
+    c = point_cells_z(spec, np.asarray(points)[:, 2])
+    return (c >= BRICK * zb_lo) & (c <= BRICK * zb_hi - 1)
+
+
+class _CudaBuf:
+    """__cuda_array_interface__ view of a raw device pointer (torch.as_tensor)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def device_view(ptr: int, n: int, dtype: str = "<f4"):
+    import torch
+    return torch.as_tensor(_CudaBuf(ptr, n, dtype), device="cuda")
+
+
+class SlabGrid:
+    """Device handle of one slab (tgcu_grid_create_slab)."""
+
+    def __init__(self, spec: GridSpec, zb_lo: int, zb_hi: int, opts: Optional[InitOptions] = None, device: int = 0):
+        L = lib()
+        self.spec = spec
+        self.zb = (zb_lo, zb_hi)
+        o = opts or InitOptions()
+        from . import _Init
+        ci = _Init(int(o.mode), o.constant, o.epsilon, o.seed, o.memory_cap_bytes)
+        h = C.c_void_p()
+        _check(L.tgcu_grid_create_slab(C.byref(spec._c()), zb_lo, zb_hi, C.byref(ci), device, C.byref(h)))
+        self._h = h
+        info = [C.c_int() for _ in range(5)]
+        L.tgcu_slab_info(h, *[C.byref(x) for x in info])
+        self.z_store_lo, self.z_store_n, self.z_own_lo, self.z_own_hi, self.brick_layers = [x.value for x in info]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tgcu_grid_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def adam_reset(self, cfg: AdamConfig = AdamConfig()):
+        _check(lib().tgcu_adam_reset(self._h, C.byref(cfg._c())))
+
+    def coeff_total(self) -> int:
+        return int(lib().tgcu_grid_coeff_total(self._h))
+
+    def coeffs(self) -> np.ndarray:
+        out = np.empty(self.coeff_total())
+        _check(lib().tgcu_grid_download_f64(self._h, _ptr(out), out.size))
+        return out
+
+    def set_coeffs(self, values):
+        a = np.ascontiguousarray(values, dtype=np.float64).ravel()
+        _check(lib().tgcu_grid_upload_f64(self._h, _ptr(a), a.size))
+
+    def owned_coeffs(self) -> np.ndarray:
+        """Coefficients of the owned vertex planes (reference AoS layout)."""
+        K = self.spec.coeffs_per_vertex()
+        plane = self.spec.resolution[0] * self.spec.resolution[1] * K
+        c = self.coeffs()
+        a = (self.z_own_lo - self.z_store_lo) * plane
+        b = (self.z_own_hi - self.z_store_lo) * plane
+        return c[a:b]
+
+    def begin(self, samples, cfg: LossConfig, stream=None, export_grad=False) -> int:
+        """Phase 1; returns the device pointer of the 5 local partial sums."""
+        from . import TGCU_EXPORT_GRAD, _is_torch
+        flags = 0 if _is_torch(samples) else TGCU_HOST
+        if export_grad:
+            flags |= TGCU_EXPORT_GRAD
+        if not _is_torch(samples):
+            samples = np.ascontiguousarray(np.asarray(samples, dtype=np.float32)).reshape(-1, 4)
+        p = C.POINTER(C.c_double)()
+        _check(lib().tgcu_slab_step_begin(self._h, _ptr(samples), samples.shape[0], C.byref(cfg._c()),
+                                          C.byref(p), flags, C.c_void_p(stream) if stream else None))
+        return C.cast(p, C.c_void_p).value
+
+    def finish(self, reduced_ptr: Optional[int], asynchronous=False, stream=None) -> Optional[LossTerms]:
+        if asynchronous:
+            _check(lib().tgcu_slab_step_finish(self._h, C.c_void_p(reduced_ptr) if reduced_ptr else None, None,
+                                               TGCU_ASYNC, C.c_void_p(stream) if stream else None))
+            return None
+        t = _Terms()
+        _check(lib().tgcu_slab_step_finish(self._h, C.c_void_p(reduced_ptr) if reduced_ptr else None, C.byref(t), 0,
+                                           C.c_void_p(stream) if stream else None))
+        return LossTerms._from(t)
+
+    def halo(self):
+        """(send_lo, send_hi, recv_lo, recv_hi, plane_floats) device pointers (0 = none)."""
+        ptrs = [C.c_void_p() for _ in range(4)]
+        pf = C.c_int64()
+        _check(lib().tgcu_slab_halo(self._h, *[C.byref(x) for x in ptrs], C.byref(pf)))
+        return tuple((x.value or 0) for x in ptrs) + (pf.value,)
+
+    def sync(self) -> LossTerms:
+        t = _Terms()
+        _check(lib().tgcu_sync(self._h, C.byref(t)))
+        return LossTerms._from(t)
+
+
+class SlabTrainer:
+    """One rank of a torch.distributed (NCCL) slab-parallel training run."""
+
+    def __init__(self, spec: GridSpec, rank: int, world: int, adam: AdamConfig, device: int = 0,
+                 opts: Optional[InitOptions] = None, ranges=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.rank, self.world = rank, world
+        nbz = brick_layers(spec.resolution[2])
+        self.ranges = ranges or slab_ranges(nbz, world)
+        lo, hi = self.ranges[rank]
+        self.slab = SlabGrid(spec, lo, hi, opts, device)
+        self.slab.adam_reset(adam)
+        self.exchange()  # halo planes of the initial parameters
+
+    def exchange(self):
+        """Send owned boundary planes to the neighbours, receive their halo planes."""
+        dist = self.dist
+        s_lo, s_hi, r_lo, r_hi, pf = self.slab.halo()
+        ops = []
+        if s_lo:
+            ops.append(dist.P2POp(dist.isend, device_view(s_lo, pf), self.rank - 1))
+            ops.append(dist.P2POp(dist.irecv, device_view(r_lo, pf), self.rank - 1))
+        if s_hi:
+            ops.append(dist.P2POp(dist.isend, device_view(s_hi, pf), self.rank + 1))
+            ops.append(dist.P2POp(dist.irecv, device_view(r_hi, pf), self.rank + 1))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def step(self, samples_dev, cfg: LossConfig, stream=None, want_terms=False):
+        part = self.slab.begin(samples_dev, cfg, stream=stream)
+        t = device_view(part, 5, "<f8")
+        self.dist.all_reduce(t)
+        terms = self.slab.finish(part, asynchronous=not want_terms, stream=stream)
+        self.exchange()
+        return terms

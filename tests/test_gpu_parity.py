@@ -274,3 +274,44 @@ def test_c2_scale_fused_gradient_vs_oracle(oracle):
     # first Adam step: p - lr * g / (|g| + eps) (bias-corrected), fp32 state
     p1 = c.astype(np.float64) - 1e-2 * gref / (np.abs(gref) + 1e-8)
     assert_close(g.coeffs, p1, 1e-6, floor=1.0 + 0 * p1, what="params after step")
+
+
+# ---- multi-GPU slab path, two slabs emulated on one device ----------------------------------------
+
+
+def test_slab_two_on_one_gpu_matches_full_grid():
+    """Two z-slab grids driven like two ranks (sum of partials, commit, halo
+    exchange by device copies) reproduce the single-grid fused trajectory."""
+    from paper_2402_14415_b200.slab import SlabGrid, brick_layers, device_view, slab_ranges
+    res = (24, 20, 40)
+    spec = tg.GridSpec(dim=3, resolution=res, order=2)
+    init = tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.02, seed=3)
+    cfg = tg.LossConfig()
+    full = tg.init_grid(spec, init)
+    full.adam_reset(tg.AdamConfig(lr=1e-2))
+    ranges = slab_ranges(brick_layers(res[2]), 2)
+    slabs = [SlabGrid(spec, lo, hi, init) for lo, hi in ranges]
+    for sg in slabs:
+        sg.adam_reset(tg.AdamConfig(lr=1e-2))
+    K = spec.coeffs_per_vertex()
+    plane = res[0] * res[1] * K
+    c_full = full.coeffs
+    for sg in slabs:  # identical initial values, halo planes included
+        assert np.array_equal(sg.coeffs(), c_full[sg.z_store_lo * plane:(sg.z_store_lo + sg.z_store_n) * plane])
+    for step in range(6):
+        b = tg.sample(tg.SHAPE_SPHERE, 3, 500 + step, 20000, near_frac=0.5, sigma=0.01, param0=0.6)
+        tf = tg.train_step(full, b, cfg).as_array()
+        parts = [sg.begin(b, cfg) for sg in slabs]
+        views = [device_view(p, 5, "<f8") for p in parts]
+        tot = views[0] + views[1]
+        for v in views:
+            v.copy_(tot)
+        terms = [sg.finish(p).as_array() for sg, p in zip(slabs, parts)]
+        s0, s1 = slabs[0].halo(), slabs[1].halo()
+        pf = s0[4]
+        device_view(s1[2], pf).copy_(device_view(s0[1], pf))  # slab0 top owned plane -> slab1 lower halo
+        device_view(s0[3], pf).copy_(device_view(s1[0], pf))  # slab1 bottom owned plane -> slab0 upper halo
+        for t in terms:
+            assert_close(t, tf, 1e-6, floor=1e-30, what=f"slab terms step {step}")
+    owned = np.concatenate([sg.owned_coeffs() for sg in slabs])
+    assert_close(owned, full.coeffs, 1e-5, floor=1e-2, what="slab coefficients")
