@@ -217,25 +217,52 @@ class SlabTrainer:
         self.slab.adam_reset(adam)
         self.exchange()  # halo planes of the initial parameters
 
+    def _staged(self) -> bool:
+        # NCCL moves device memory directly; gloo (CPU tests, one shared GPU)
+        # goes through host copies.
+        return self.dist.get_backend() != "nccl"
+
     def exchange(self):
         """Send owned boundary planes to the neighbours, receive their halo planes."""
         dist = self.dist
         s_lo, s_hi, r_lo, r_hi, pf = self.slab.halo()
-        ops = []
+        staged = self._staged()
+        if staged:
+            import torch
+            torch.cuda.synchronize()
+        sends, recvs = [], []
         if s_lo:
-            ops.append(dist.P2POp(dist.isend, device_view(s_lo, pf), self.rank - 1))
-            ops.append(dist.P2POp(dist.irecv, device_view(r_lo, pf), self.rank - 1))
+            sends.append((device_view(s_lo, pf), self.rank - 1))
+            recvs.append((device_view(r_lo, pf), self.rank - 1))
         if s_hi:
-            ops.append(dist.P2POp(dist.isend, device_view(s_hi, pf), self.rank + 1))
-            ops.append(dist.P2POp(dist.irecv, device_view(r_hi, pf), self.rank + 1))
-        if ops:
+            sends.append((device_view(s_hi, pf), self.rank + 1))
+            recvs.append((device_view(r_hi, pf), self.rank + 1))
+        if not sends:
+            return
+        if staged:
+            sbuf = [(t.cpu(), peer) for t, peer in sends]
+            rbuf = [(t.cpu(), peer, t) for t, peer in recvs]
+            reqs = [dist.isend(t, peer) for t, peer in sbuf] + [dist.irecv(t, peer) for t, peer, _ in rbuf]
+            for r in reqs:
+                r.wait()
+            for t, _, dev in rbuf:
+                dev.copy_(t)
+        else:
+            ops = [dist.P2POp(dist.isend, t, p) for t, p in sends] + [dist.P2POp(dist.irecv, t, p) for t, p in recvs]
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
 
     def step(self, samples_dev, cfg: LossConfig, stream=None, want_terms=False):
         part = self.slab.begin(samples_dev, cfg, stream=stream)
         t = device_view(part, 5, "<f8")
-        self.dist.all_reduce(t)
+        if self._staged():
+            import torch
+            torch.cuda.synchronize()
+            h = t.cpu()
+            self.dist.all_reduce(h)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t)
         terms = self.slab.finish(part, asynchronous=not want_terms, stream=stream)
         self.exchange()
         return terms
