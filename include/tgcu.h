@@ -214,6 +214,10 @@ int tgcu_slab_step_finish(tgcu_grid* g, const double* reduced, tgcu_loss_terms* 
 int tgcu_slab_halo(tgcu_grid* g, float** send_lo, float** send_hi, float** recv_lo, float** recv_hi,
                    int64_t* plane_floats);
 
+/* Fused steps issued on this grid since creation or the last reported error;
+ * error messages of a failed step name it as "step <this index at launch>". */
+int tgcu_grid_steps_launched(const tgcu_grid* g, int64_t* n);
+
 /* Wait for the grid's outstanding async work and report any sticky error.
  * If last_terms is not NULL it receives the most recent step's LossTerms. */
 int tgcu_sync(tgcu_grid* g, tgcu_loss_terms* last_terms);
@@ -226,6 +230,58 @@ int tgcu_trace(tgcu_grid* g, tgcu_loss_terms* out, int count);
  * the summed device milliseconds and the number of timed launches. */
 int tgcu_profile_begin(tgcu_grid* g);
 int tgcu_profile_end(tgcu_grid* g, double* total_ms, int* launches);
+
+/* ---- stage transitions, lattice query, .tgrid I/O ---------- */
+
+/* multilinear_resample (taylor_grid.cpp:231-271): `channels` interleaved values
+ * per vertex of old_spec (n = vertex_count * channels floats) resampled onto
+ * new_res (per-axis vertex counts of the same origin/extent). Weights and
+ * accumulation in fp64 in the reference's order, rounded once to fp32. data /
+ * out are device pointers, or host with TGCU_HOST. */
+int tgcu_multilinear_resample(const tgcu_grid_spec* old_spec, const float* data, int64_t n, int channels,
+                              const int new_res[3], float* out, int flags, void* stream);
+
+/* upsample (taylor_grid.cpp:273-284) into an existing grid: dst must have
+ * src's dim, order, origin and extent, and res >= src's on every axis
+ * (TGCU_ERR_INVALID_ARGUMENT "upsample: resolution may not shrink (axis a)").
+ * dst's coefficients are replaced; its Adam state is the caller's to reset
+ * (run_schedule resets moments per stage, schedule.cpp:79). */
+int tgcu_grid_upsample(tgcu_grid* src, tgcu_grid* dst, int flags, void* stream);
+
+/* sample_grid_field (marching.cpp:53-58): eval on the lattice[0] x lattice[1]
+ * (x lattice[2] in 3D) points origin + extent * i / (lattice - 1) of the
+ * grid's own domain (ScalarField3::position, marching.hpp:21-24), x fastest.
+ * For dim 2 this is the CLI's sample_grid_field2 (tools/main.cpp:33-45).
+ * values: device (or host with TGCU_HOST) array of prod(lattice) floats. */
+int tgcu_sample_grid_field(tgcu_grid* g, const int lattice[3], float* values, int flags, void* stream);
+
+/* SdfProblem::compute's batch draw (sdf_fit.cpp:21-23) on device: n samples
+ * (x, y, z, gt) drawn with replacement from a device pool of pool_n samples,
+ * index = floor(u * pool_n), u from a counter hash of (seed, step, i) — a
+ * different stream from the reference's mt19937_64, same distribution. */
+int tgcu_draw_batch(const float* pool, int64_t pool_n, int64_t n, uint64_t seed, uint64_t step, float* out,
+                    void* stream);
+
+/* tg::Rng streams (rng.hpp:14-74, mt19937_64 + the reference's index()
+ * rejection mapping) as host handles, for drivers that need the reference's
+ * exact draw sequence: SdfProblem's batch indices (sdf_fit.cpp:22). */
+typedef struct tgcu_rng tgcu_rng;
+int tgcu_rng_create(uint64_t seed, tgcu_rng** out);
+void tgcu_rng_destroy(tgcu_rng* r);
+/* count draws of Rng::index(n) into out. */
+int tgcu_rng_index(tgcu_rng* r, uint64_t n, int64_t count, int64_t* out);
+/* fit_sdf's seeded Fisher-Yates order (sdf_fit.cpp:59-64); pass the
+ * reference's seed (options.seed ^ 0x5deece66d). */
+int tgcu_shuffle_order(uint64_t seed, int64_t n, uint32_t* order);
+
+/* .tgrid files (grid_io.cpp:36-111, layout grid_io.hpp:11-16). F64 writes the
+ * fp32 coefficients widened (exact); loading an F64 file narrows to fp32.
+ * File errors -> TGCU_ERR_INGEST with the reference's messages. */
+enum { TGCU_TGRID_F64 = 0, TGCU_TGRID_F32 = 1 };
+int tgcu_save_tgrid(tgcu_grid* g, const char* path, int precision);
+int tgcu_load_tgrid(const char* path, int device, tgcu_grid** out);
+/* tgrid_file_size (grid_io.cpp:36-40); -1 for an invalid spec. */
+int64_t tgcu_tgrid_file_size(const tgcu_grid_spec* spec, int precision);
 
 /* Number of kernels this library launched since the counter was reset. */
 int64_t tgcu_launch_count(void);

@@ -101,6 +101,7 @@ class Oracle:
         L.tgo_adam_step.restype = C.c_int64
         L.tgo_adam_step.argtypes = [_D, _D, _D, _D, C.c_int64, _L] + [C.c_double] * 4
         L.tgo_multilinear_resample.argtypes = [C.POINTER(_TgoSpec), _D, C.c_int, _I, _D]
+        L.tgo_sample_lattice.argtypes = [C.POINTER(_TgoSpec), _D, _I, _D]
         L.tgo_coeff_count.argtypes = [C.c_int, C.c_int]
         L.tgo_backprop_mass.argtypes = [C.POINTER(_TgoSpec), _D, C.c_double, _D, _D]
         L.tgo_total_loss_mass.argtypes = [C.POINTER(_TgoSpec), _D, _D, C.c_int64, C.POINTER(_TgoLoss), _D]
@@ -219,6 +220,68 @@ class Oracle:
         self.L.tgo_multilinear_resample(C.byref(self._spec(s)), _dp(data), channels, nr, _dp(out))
         return out
 
+    def sample_lattice(self, s: Spec, coeffs, lattice):
+        lt = (C.c_int * 3)(*[int(r) for r in (list(lattice) + [1, 1, 1])[:3]])
+        n = lt[0] * lt[1] * (lt[2] if s.dim == 3 else 1)
+        out = np.zeros(n)
+        self.L.tgo_sample_lattice(C.byref(self._spec(s)), _dp(np.ascontiguousarray(coeffs, dtype=np.float64)), lt,
+                                  _dp(out))
+        return out
+
+    def run_schedule(self, s: Spec, coeffs0, stages, batches, cfg: "Loss", lr=0.003, beta1=0.9, beta2=0.999,
+                     eps=1e-8):
+        """run_schedule (schedule.cpp:62-108): per stage upsample when the
+        resolution changes (taylor_grid.cpp:273-284), fresh Adam moments, then
+        the stage's steps; batches are consumed in order. stages = [(res, steps)].
+        Returns (final spec, coeffs, terms)."""
+        cur = Spec(s.dim, tuple(stages[0][0]), s.origin, s.extent, s.order)
+        c = np.array(coeffs0, dtype=np.float64)
+        terms, k = [], 0
+        for res, steps in stages:
+            res = tuple(res)
+            if any(res[a] != cur.res[a] for a in range(s.dim)):
+                c = self.resample(cur, c, cur.K, res)
+                cur = Spec(s.dim, res, s.origin, s.extent, s.order)
+            c, tr = self.train(cur, c, list(batches[k:k + steps]), cfg, lr, beta1, beta2, eps) if steps else (c, [])
+            terms.extend(list(tr))
+            k += steps
+        return cur, c, np.array(terms).reshape(-1, 4)
+
+
+def schedule_progressive(target, dim, total_steps):
+    """Schedule::progressive (schedule.cpp:27-54) restated: target/4, /2, /1
+    (floored at 4, capped at target), equal split, collapsed duplicates,
+    remainder to the last stage. Returns [(res tuple, steps)]."""
+    stages = []
+    for d in (4, 2, 1):
+        res = [2, 2, 2]  # Stage::resolution default {2, 2, 2} on unused axes
+        same_target = True
+        for a in range(dim):
+            res[a] = min(max(4, int(target[a]) // d), int(target[a]))
+            same_target &= res[a] == target[a]
+        res = tuple(res[:3])
+        if stages and all(res[a] == stages[-1][0][a] for a in range(dim)):
+            continue
+        stages.append([res, total_steps // 3])
+        if same_target:
+            break
+    stages[-1][1] += total_steps - sum(st for _, st in stages)
+    return [(r, st) for r, st in stages]
+
+
+def tgrid_bytes(s: Spec, coeffs, precision: int) -> bytes:
+    """save_tgrid's byte stream (grid_io.cpp:44-65, layout grid_io.hpp:11-16):
+    "TGRD" | u32 version 1 | u8 dim | u8 order | dim x u32 res | dim x f64
+    origin | dim x f64 extent | u8 precision (0 F64, 1 F32) | coefficients."""
+    import struct
+    out = b"TGRD" + struct.pack("<IBB", 1, s.dim, s.order)
+    out += struct.pack("<" + "I" * s.dim, *[int(r) for r in s.res[:s.dim]])
+    out += struct.pack("<" + "d" * s.dim, *[float(o) for o in s.origin[:s.dim]])
+    out += struct.pack("<" + "d" * s.dim, *[float(e) for e in s.extent[:s.dim]])
+    out += struct.pack("<B", precision)
+    c = np.asarray(coeffs, dtype=np.float64 if precision == 0 else np.float32)
+    return out + c.astype(c.dtype.newbyteorder("<")).tobytes()
+
 
 class Reference:
     """The reference's own code (oracle/_ref/libtgref.so)."""
@@ -249,6 +312,18 @@ class Reference:
         L.tgr_rng_uniform.argtypes = [C.c_uint64, C.c_int64, _D]
         L.tgr_rng_gaussian.argtypes = [C.c_uint64, C.c_int64, _D]
         L.tgr_upsample.argtypes = sp + [_D, _I, _D]
+        L.tgr_run_schedule.argtypes = [C.c_int, _D, _D, C.c_int, _D, C.c_int, _I, _I, _D, C.c_int64,
+                                       C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                                       C.c_double, C.c_double, C.c_double, C.c_double, _D, _D]
+        L.tgr_schedule_progressive.argtypes = [_I, C.c_int, C.c_int, _I, _I, _I]
+        L.tgr_sample_grid_field.argtypes = sp + [_D, _I, _D]
+        L.tgr_save_tgrid.argtypes = sp + [_D, C.c_char_p, C.c_int]
+        L.tgr_load_tgrid.argtypes = [C.c_char_p, _I, _D, _D, C.c_int64]
+        L.tgr_rng_index.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _L]
+        L.tgr_shuffle_order.argtypes = [C.c_uint64, C.c_int64, C.c_void_p]
+        L.tgr_trace_csv.argtypes = [C.c_int, _I, _I, _D, _D, C.c_char_p, C.c_char_p, C.c_int64]
+        L.tgr_fit_sdf.argtypes = sp + [_D, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
+                                       C.c_int, C.c_double, C.c_double, C.c_uint64, _D, _D, _D]
         self.L = L
 
     def _err(self, rc):
@@ -360,6 +435,94 @@ class Reference:
         out = np.zeros(n * s.K)
         self._err(self.L.tgr_upsample(*_spec_args(s), _dp(np.ascontiguousarray(coeffs, dtype=np.float64)), nr, _dp(out)))
         return out
+
+    def run_schedule(self, s: Spec, coeffs0, stages, batches, cfg, lr=0.003, beta1=0.9, beta2=0.999, eps=1e-8):
+        """tg::run_schedule with a TrainProblem feeding `batches` in order."""
+        ns = len(stages)
+        sr = np.array([list(r) + [1] * (3 - len(r)) for r, _ in stages], dtype=np.int32).ravel()
+        st = np.array([n for _, n in stages], dtype=np.int32)
+        fr = list(stages[-1][0])
+        nv = 1
+        for a in range(s.dim):
+            nv *= fr[a]
+        out = np.zeros(nv * s.K)
+        total = int(st.sum())
+        terms = np.zeros((total, 4))
+        b = np.ascontiguousarray(np.asarray(batches[:total], dtype=np.float64))
+        n = b.shape[1] if total else 0
+        org = np.array(list(s.origin) + [0.0] * 3, dtype=np.float64)[:3]
+        ext = np.array(list(s.extent) + [1.0] * 3, dtype=np.float64)[:3]
+        self._err(self.L.tgr_run_schedule(s.dim, _dp(org), _dp(ext), s.order,
+                                          _dp(np.ascontiguousarray(coeffs0, dtype=np.float64)), ns,
+                                          sr.ctypes.data_as(_I), st.ctypes.data_as(_I), _dp(b), n, cfg.lambda1,
+                                          cfg.lambda2, cfg.k, int(cfg.use_weighting), int(cfg.use_tv),
+                                          int(cfg.differentiate_weight), lr, beta1, beta2, eps, _dp(out),
+                                          _dp(terms)))
+        return out, terms
+
+    def fit_sdf(self, s: Spec, samples, total_steps, cfg, batch, lr=0.003, holdout_fraction=0.0, seed=1):
+        """tg::fit_sdf (default progressive plan); returns (coeffs at s.res, terms, report)."""
+        smp = np.ascontiguousarray(np.asarray(samples, dtype=np.float64)).reshape(-1, 4)
+        out = np.zeros(s.V * s.K)
+        terms = np.zeros((total_steps, 4))
+        rep = np.zeros(3)
+        self._err(self.L.tgr_fit_sdf(*_spec_args(s), _dp(smp), smp.shape[0], total_steps, batch, cfg.lambda1,
+                                     cfg.lambda2, cfg.k, int(cfg.use_weighting), int(cfg.use_tv), lr,
+                                     holdout_fraction, seed, _dp(out), _dp(terms), _dp(rep)))
+        return out, terms, {"holdout_mae": rep[0], "train_samples": int(rep[1]), "holdout_samples": int(rep[2])}
+
+    def rng_index(self, seed, n, count):
+        out = np.zeros(count, dtype=np.int64)
+        self.L.tgr_rng_index(seed, n, count, out.ctypes.data_as(_L))
+        return out
+
+    def shuffle_order(self, seed, n):
+        out = np.zeros(n, dtype=np.uint32)
+        self.L.tgr_shuffle_order(seed, n, out.ctypes.data_as(C.c_void_p))
+        return out
+
+    def trace_csv(self, steps, stages, res3, terms, wall_ms, label="recon"):
+        n = len(steps)
+        ss = np.ascontiguousarray(np.stack([steps, stages], 1).astype(np.int32))
+        rr = np.ascontiguousarray(np.asarray(res3, dtype=np.int32))
+        tt = np.ascontiguousarray(np.asarray(terms, dtype=np.float64))
+        ww = np.ascontiguousarray(np.asarray(wall_ms, dtype=np.float64))
+        buf = C.create_string_buffer(256 * (n + 1))
+        rc = self.L.tgr_trace_csv(n, ss.ctypes.data_as(_I), rr.ctypes.data_as(_I), _dp(tt), _dp(ww), label.encode(),
+                                  buf, len(buf))
+        assert rc == 0
+        return buf.value.decode()
+
+    def schedule_progressive(self, target, dim, total_steps):
+        t = (C.c_int * 3)(*[int(x) for x in (list(target) + [1, 1, 1])[:3]])
+        ns = C.c_int()
+        sr = (C.c_int * 9)()
+        st = (C.c_int * 3)()
+        self.L.tgr_schedule_progressive(t, dim, total_steps, C.byref(ns), sr, st)
+        return [(tuple(sr[3 * i:3 * i + 3]), st[i]) for i in range(ns.value)]
+
+    def sample_grid_field(self, s: Spec, coeffs, lattice):
+        lt = (C.c_int * 3)(*[int(r) for r in (list(lattice) + [1, 1, 1])[:3]])
+        n = lt[0] * lt[1] * (lt[2] if s.dim == 3 else 1)
+        out = np.zeros(n)
+        self._err(self.L.tgr_sample_grid_field(*_spec_args(s), _dp(np.ascontiguousarray(coeffs, dtype=np.float64)),
+                                               lt, _dp(out)))
+        return out
+
+    def save_tgrid(self, s: Spec, coeffs, path, precision=0):
+        self._err(self.L.tgr_save_tgrid(*_spec_args(s), _dp(np.ascontiguousarray(coeffs, dtype=np.float64)),
+                                        str(path).encode(), precision))
+
+    def load_tgrid(self, path):
+        sp = (C.c_int * 5)()
+        geo = (C.c_double * 6)()
+        rc = self.L.tgr_load_tgrid(str(path).encode(), sp, geo, None, 0)
+        if rc != 0:
+            raise OSError(self.L.tgr_last_error().decode())
+        s = Spec(sp[0], tuple(sp[2:5]), tuple(geo[0:3]), tuple(geo[3:6]), sp[1])
+        c = np.zeros(s.V * s.K)
+        self._err(self.L.tgr_load_tgrid(str(path).encode(), sp, geo, _dp(c), c.size))
+        return s, c
 
 
 def reference_available() -> bool:

@@ -17,9 +17,14 @@
 
 #include "taylorgrid/adam.hpp"
 #include "taylorgrid/errors.hpp"
+#include "taylorgrid/grid_io.hpp"
+#include "taylorgrid/marching.hpp"
 #include "taylorgrid/parallel.hpp"
 #include "taylorgrid/rng.hpp"
 #include "taylorgrid/sampling.hpp"
+#include "taylorgrid/schedule.hpp"
+#include "taylorgrid/sample_set.hpp"
+#include "taylorgrid/sdf_fit.hpp"
 #include "taylorgrid/sdf_loss.hpp"
 #include "taylorgrid/taylor_grid.hpp"
 
@@ -310,6 +315,205 @@ int tgr_upsample(int dim, const int* res, const double* origin, const double* ex
         const tg::TaylorGrid up = tg::upsample(grid, {new_res[0], new_res[1], new_res[2]});
         std::memcpy(out, up.coeffs.data(), up.coeffs.size() * sizeof(double));
         return 0;
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+// run_schedule (schedule.cpp:62-108) driven by a TrainProblem that feeds the
+// caller's batches in order (one n-sample batch per global step). stage_res is
+// nstages x 3, coeffs0 the grid at stage 0's resolution; out_coeffs receives the
+// final grid (final stage resolution), terms_out total_steps x 4.
+int tgr_run_schedule(int dim, const double* origin, const double* extent, int order,
+                     const double* coeffs0, int nstages, const int* stage_res, const int* stage_steps,
+                     const double* batches, int64_t n, double lambda1, double lambda2, double k,
+                     int use_weighting, int use_tv, int differentiate_weight, double lr, double beta1,
+                     double beta2, double eps, double* out_coeffs, double* terms_out) {
+    try {
+        class Feed final : public tg::TrainProblem {
+        public:
+            Feed(const double* b, int64_t n, int dim, tg::LossConfig c) : b_(b), n_(n), dim_(dim), cfg_(c) {}
+            tg::LossTerms compute(const tg::TaylorGrid& grid, std::span<double> grad) override {
+                const auto batch = make_batch(b_ + 4 * n_ * step_++, n_, dim_);
+                return tg::total_loss(grid, batch, cfg_, grad, 1);
+            }
+
+        private:
+            const double* b_;
+            int64_t n_;
+            int dim_;
+            tg::LossConfig cfg_;
+            int64_t step_ = 0;
+        };
+        tg::Schedule sch;
+        for (int s = 0; s < nstages; ++s)
+            sch.stages.push_back({{stage_res[3 * s], stage_res[3 * s + 1], stage_res[3 * s + 2]}, stage_steps[s]});
+        const auto spec = make_spec(dim, stage_res, origin, extent, order);
+        Feed feed(batches, n, dim, make_loss(lambda1, lambda2, k, use_weighting, use_tv, differentiate_weight));
+        const auto r = tg::run_schedule(feed, sch, make_grid(spec, coeffs0), tg::AdamConfig{lr, beta1, beta2, eps}, 1);
+        std::memcpy(out_coeffs, r.grid.coeffs.data(), r.grid.coeffs.size() * sizeof(double));
+        for (std::size_t i = 0; i < r.trace.size(); ++i) {
+            terms_out[4 * i] = r.trace[i].loss.total;
+            terms_out[4 * i + 1] = r.trace[i].loss.fit;
+            terms_out[4 * i + 2] = r.trace[i].loss.eik;
+            terms_out[4 * i + 3] = r.trace[i].loss.tv;
+        }
+        return 0;
+    } catch (const tg::NumericalError& e) {
+        return fail(e, 4);
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+// fit_sdf (sdf_fit.cpp:52-105) with the default progressive schedule over
+// total_steps, LossConfig batch_size = batch. samples n x 4 (x, y, z, gt).
+// out_coeffs: final grid (spec resolution); terms_out: total_steps x 4;
+// report_out: {holdout_mae, train_samples, holdout_samples}.
+int tgr_fit_sdf(int dim, const int* res, const double* origin, const double* extent, int order,
+                const double* samples, int64_t n, int total_steps, int batch, double lambda1, double lambda2,
+                double k, int use_weighting, int use_tv, double lr, double holdout_fraction, uint64_t seed,
+                double* out_coeffs, double* terms_out, double* report_out) {
+    try {
+        tg::SampleSet set;
+        set.dim = dim;
+        set.samples.resize(static_cast<std::size_t>(n));
+        for (int64_t i = 0; i < n; ++i) {
+            set.samples[i].point = {samples[4 * i], samples[4 * i + 1], dim == 3 ? samples[4 * i + 2] : 0.0};
+            set.samples[i].gt_sdf = samples[4 * i + 3];
+        }
+        tg::FitOptions opt;
+        opt.loss = make_loss(lambda1, lambda2, k, use_weighting, use_tv, 0);
+        opt.loss.batch_size = batch;
+        opt.adam.lr = lr;
+        opt.total_steps = total_steps;
+        opt.holdout_fraction = holdout_fraction;
+        opt.seed = seed;
+        opt.threads = 1;
+        const tg::FitResult r = tg::fit_sdf(set, make_spec(dim, res, origin, extent, order), opt);
+        std::memcpy(out_coeffs, r.grid.coeffs.data(), r.grid.coeffs.size() * sizeof(double));
+        for (std::size_t i = 0; i < r.trace.size(); ++i) {
+            terms_out[4 * i] = r.trace[i].loss.total;
+            terms_out[4 * i + 1] = r.trace[i].loss.fit;
+            terms_out[4 * i + 2] = r.trace[i].loss.eik;
+            terms_out[4 * i + 3] = r.trace[i].loss.tv;
+        }
+        report_out[0] = r.report.holdout_mae;
+        report_out[1] = static_cast<double>(r.report.train_samples);
+        report_out[2] = static_cast<double>(r.report.holdout_samples);
+        return 0;
+    } catch (const tg::NumericalError& e) {
+        return fail(e, 4);
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+// Rng::index stream (rng.hpp:27-35) and fit_sdf's seeded Fisher-Yates
+// (sdf_fit.cpp:59-64) with tg::Rng.
+int tgr_rng_index(uint64_t seed, uint64_t n, int64_t count, int64_t* out) {
+    tg::Rng r(seed);
+    for (int64_t i = 0; i < count; ++i) out[i] = static_cast<int64_t>(r.index(n));
+    return 0;
+}
+
+int tgr_shuffle_order(uint64_t seed, int64_t n, uint32_t* order) {
+    for (int64_t i = 0; i < n; ++i) order[i] = static_cast<uint32_t>(i);
+    tg::Rng shuffle_rng(seed);
+    for (std::size_t i = static_cast<std::size_t>(n); i > 1; --i) std::swap(order[i - 1], order[shuffle_rng.index(i)]);
+    return 0;
+}
+
+// trace_csv_string (schedule.cpp:110-120) of rows given as arrays.
+int tgr_trace_csv(int nrows, const int* step_stage, const int* res3, const double* terms, const double* wall_ms,
+                  const char* label, char* out, int64_t cap) {
+    std::vector<tg::TraceRow> rows(static_cast<std::size_t>(nrows));
+    for (int i = 0; i < nrows; ++i) {
+        rows[i].step = step_stage[2 * i];
+        rows[i].stage = step_stage[2 * i + 1];
+        rows[i].resolution = {res3[3 * i], res3[3 * i + 1], res3[3 * i + 2]};
+        rows[i].loss = {terms[4 * i], terms[4 * i + 1], terms[4 * i + 2], terms[4 * i + 3]};
+        rows[i].wall_ms = wall_ms[i];
+    }
+    const std::string s = tg::trace_csv_string(rows, label);
+    if (static_cast<int64_t>(s.size()) + 1 > cap) return -static_cast<int>(s.size() + 1);
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+}
+
+// Schedule::progressive (schedule.cpp:27-54): writes up to 3 stages.
+int tgr_schedule_progressive(const int* target, int dim, int total_steps, int* nstages, int* stage_res,
+                             int* stage_steps) {
+    const auto s = tg::Schedule::progressive({target[0], target[1], target[2]}, dim, total_steps);
+    *nstages = static_cast<int>(s.stages.size());
+    for (std::size_t i = 0; i < s.stages.size(); ++i) {
+        for (int a = 0; a < 3; ++a) stage_res[3 * i + a] = s.stages[i].resolution[a];
+        stage_steps[i] = s.stages[i].steps;
+    }
+    return 0;
+}
+
+// sample_grid_field (marching.cpp:53-58) for dim 3; for dim 2 the CLI's
+// sample_grid_field2 lattice (tools/main.cpp:33-45, position() of
+// marching.hpp:34-36) evaluated with the reference eval.
+int tgr_sample_grid_field(int dim, const int* res, const double* origin, const double* extent, int order,
+                          const double* coeffs, const int* lattice, double* out) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        const tg::TaylorGrid grid = make_grid(spec, coeffs);
+        if (dim == 3) {
+            const tg::ScalarField3 f = tg::sample_grid_field(grid, {lattice[0], lattice[1], lattice[2]}, 1);
+            std::memcpy(out, f.values.data(), f.values.size() * sizeof(double));
+        } else {
+            tg::ScalarField2 f;
+            f.res = {lattice[0], lattice[1]};
+            f.origin = {origin[0], origin[1]};
+            f.extent = {extent[0], extent[1]};
+            for (int y = 0; y < lattice[1]; ++y)
+                for (int x = 0; x < lattice[0]; ++x) {
+                    const auto p = f.position(x, y);
+                    out[static_cast<std::size_t>(y) * lattice[0] + x] = tg::eval(grid, {p[0], p[1], 0.0});
+                }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+// save_tgrid / load_tgrid (grid_io.cpp:36-111).
+int tgr_save_tgrid(int dim, const int* res, const double* origin, const double* extent, int order,
+                   const double* coeffs, const char* path, int precision) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        tg::save_tgrid(make_grid(spec, coeffs), path, static_cast<tg::StoragePrecision>(precision));
+        return 0;
+    } catch (const tg::IngestError& e) {
+        return fail(e, 3);
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+// Loads a file; spec_out = {dim, order, res[3]} as ints, geo_out = origin[3],
+// extent[3]; coeffs_out may be NULL (query the size first).
+int tgr_load_tgrid(const char* path, int* spec_out, double* geo_out, double* coeffs_out, int64_t cap) {
+    try {
+        const tg::TaylorGrid g = tg::load_tgrid(path);
+        spec_out[0] = g.spec.dim;
+        spec_out[1] = g.spec.order;
+        for (int a = 0; a < 3; ++a) {
+            spec_out[2 + a] = g.spec.resolution[a];
+            geo_out[a] = g.spec.origin[a];
+            geo_out[3 + a] = g.spec.extent[a];
+        }
+        if (coeffs_out) {
+            if (static_cast<int64_t>(g.coeffs.size()) > cap) throw std::invalid_argument("tgr_load_tgrid: cap");
+            std::memcpy(coeffs_out, g.coeffs.data(), g.coeffs.size() * sizeof(double));
+        }
+        return static_cast<int>(0);
+    } catch (const tg::IngestError& e) {
+        return fail(e, 3);
     } catch (const std::exception& e) {
         return fail(e, 1);
     }

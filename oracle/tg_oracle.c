@@ -485,6 +485,24 @@ void tgo_multilinear_resample(const tgo_spec* old_spec, const double* data, int 
     }
 }
 
+/* sample_grid_field (marching.cpp:53-58 via sample_field3 :30-51) for dim 3,
+ * and the CLI's 2D lattice sample_grid_field2 (tools/main.cpp:33-45): lattice
+ * point (x, y, z) sits at origin + extent * x / (n - 1) per axis
+ * (ScalarField3::position, marching.hpp:21-24), x fastest; values fp64. */
+void tgo_sample_lattice(const tgo_spec* s, const double* coeffs, const int lattice[3], double* out) {
+    const int nz = s->dim == 3 ? lattice[2] : 1;
+    int64_t idx = 0;
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < lattice[1]; ++y)
+            for (int x = 0; x < lattice[0]; ++x) {
+                double p[3];
+                p[0] = s->origin[0] + s->extent[0] * x / (lattice[0] - 1);
+                p[1] = s->origin[1] + s->extent[1] * y / (lattice[1] - 1);
+                p[2] = s->dim == 3 ? s->origin[2] + s->extent[2] * z / (lattice[2] - 1) : 0.0;
+                out[idx++] = tgo_eval(s, coeffs, p, NULL);
+            }
+}
+
 /* Test helper: the device locate's division t = x / h via Markstein's
  * correction with a correctly rounded reciprocal (tg_device.cuh div_by_h),
  * evaluated with C99 fma so the CPU test can compare it with IEEE division. */

@@ -25,7 +25,9 @@ __all__ = [
     "backprop_spatial_chain", "backprop_value_and_spatial", "adaptive_weight", "tv_loss",
     "total_loss", "adam_step", "train_step", "sample", "sample_uniform", "shape_sdf",
     "ConfigError", "IngestError", "NumericalError", "ResourceError", "CudaError", "lib",
-    "launch_count", "reset_launch_count", "LIB_PATH",
+    "launch_count", "reset_launch_count", "LIB_PATH", "upsample", "multilinear_resample", "ScalarField3",
+    "ScalarField2", "sample_grid_field", "sample_grid_field2", "StoragePrecision", "save_tgrid", "load_tgrid",
+    "tgrid_file_size", "draw_batch",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtgcu.so")
@@ -100,6 +102,7 @@ def lib():
     L.tgcu_coeff_count.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int)]
     L.tgcu_grid_create.argtypes = [C.POINTER(_Spec), C.POINTER(_Init), C.c_int, C.POINTER(P)]
     L.tgcu_grid_destroy.argtypes = [P]
+    L.tgcu_grid_spec_of.argtypes = [P, C.POINTER(_Spec)]
     L.tgcu_grid_coeff_total.argtypes = [P]
     L.tgcu_grid_coeff_total.restype = C.c_int64
     L.tgcu_grid_coeffs.argtypes = [P]
@@ -127,6 +130,7 @@ def lib():
     L.tgcu_adam_download_f64.argtypes = [P, P, P, C.c_int64]
     L.tgcu_train_step.argtypes = [P, P, C.c_int64, C.POINTER(_Loss), C.POINTER(_Terms), C.c_int, P]
     L.tgcu_sync.argtypes = [P, C.POINTER(_Terms)]
+    L.tgcu_grid_steps_launched.argtypes = [P, C.POINTER(C.c_int64)]
     L.tgcu_grid_create_slab.argtypes = [C.POINTER(_Spec), C.c_int, C.c_int, C.POINTER(_Init), C.c_int, C.POINTER(P)]
     L.tgcu_slab_info.argtypes = [P] + [C.POINTER(C.c_int)] * 5
     L.tgcu_slab_step_begin.argtypes = [P, P, C.c_int64, C.POINTER(_Loss), C.POINTER(C.POINTER(C.c_double)),
@@ -141,6 +145,18 @@ def lib():
     L.tgcu_sample_uniform.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_double, C.c_double, P]
     L.tgcu_sample_uniform_device.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_double, C.c_double, P, P]
     L.tgcu_shape_sdf.argtypes = [C.c_int, C.c_int, C.c_double, P, C.c_int64, P]
+    L.tgcu_multilinear_resample.argtypes = [C.POINTER(_Spec), P, C.c_int64, C.c_int, C.POINTER(C.c_int), P, C.c_int, P]
+    L.tgcu_grid_upsample.argtypes = [P, P, C.c_int, P]
+    L.tgcu_sample_grid_field.argtypes = [P, C.POINTER(C.c_int), P, C.c_int, P]
+    L.tgcu_draw_batch.argtypes = [P, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, P, P]
+    L.tgcu_save_tgrid.argtypes = [P, C.c_char_p, C.c_int]
+    L.tgcu_load_tgrid.argtypes = [C.c_char_p, C.c_int, C.POINTER(P)]
+    L.tgcu_tgrid_file_size.argtypes = [C.POINTER(_Spec), C.c_int]
+    L.tgcu_tgrid_file_size.restype = C.c_int64
+    L.tgcu_rng_create.argtypes = [C.c_uint64, C.POINTER(P)]
+    L.tgcu_rng_destroy.argtypes = [P]
+    L.tgcu_rng_index.argtypes = [P, C.c_uint64, C.c_int64, P]
+    L.tgcu_shuffle_order.argtypes = [C.c_uint64, C.c_int64, P]
     _lib = L
     return L
 
@@ -377,6 +393,12 @@ class TaylorGrid:
         _check(lib().tgcu_adam_download_f64(self._h, _ptr(m), _ptr(v), n))
         return m, v
 
+    @property
+    def steps_launched(self) -> int:
+        n = C.c_int64()
+        lib().tgcu_grid_steps_launched(self._h, C.byref(n))
+        return n.value
+
     def sync(self) -> LossTerms:
         t = _Terms()
         _check(lib().tgcu_sync(self._h, C.byref(t)))
@@ -594,3 +616,139 @@ def shape_sdf(shape: int, dim: int, param0: float, pts) -> np.ndarray:
     out = np.empty(p.shape[0])
     _check(lib().tgcu_shape_sdf(shape, dim, param0, _ptr(p), p.shape[0], _ptr(out)))
     return out
+
+
+# ---- stage transitions, lattice query, .tgrid I/O ---------------------
+
+
+def _res3(res, dim):
+    r = [int(x) for x in res] + [1] * 3
+    return (C.c_int * 3)(*r[:3])
+
+
+def upsample(grid: TaylorGrid, new_resolution) -> TaylorGrid:
+    """upsample (taylor_grid.cpp:273-284): a new device grid at new_resolution
+    (>= the old one per axis) holding the multilinear resample of the
+    coefficients. Raises ValueError "upsample: resolution may not shrink"."""
+    s = grid.spec
+    for a in range(s.dim):
+        if int(new_resolution[a]) < int(s.resolution[a]):
+            raise ValueError(f"upsample: resolution may not shrink (axis {a})")
+    res = tuple(int(new_resolution[a]) for a in range(s.dim)) + tuple(s.resolution[s.dim:])
+    ns = GridSpec(dim=s.dim, resolution=res, origin=tuple(s.origin), extent=tuple(s.extent), order=s.order)
+    out = TaylorGrid(ns, InitOptions(memory_cap_bytes=1 << 62), grid.device)
+    _check(lib().tgcu_grid_upsample(grid.handle, out.handle, 0, None))
+    return out
+
+
+def multilinear_resample(old_spec: GridSpec, data, channels: int, new_resolution) -> np.ndarray:
+    """multilinear_resample (taylor_grid.cpp:231-271) of host data (fp32 in/out)."""
+    a = np.ascontiguousarray(np.asarray(data, dtype=np.float32)).ravel()
+    nr = _res3(new_resolution, old_spec.dim)
+    nv = 1
+    for ax in range(old_spec.dim):
+        nv *= nr[ax]
+    out = np.empty(nv * channels, dtype=np.float32)
+    _check(lib().tgcu_multilinear_resample(C.byref(old_spec._c()), _ptr(a), a.size, channels, nr, _ptr(out),
+                                           TGCU_HOST, None))
+    return out
+
+
+@dataclass
+class ScalarField3:
+    """tg::ScalarField3 (marching.hpp:12-25): lattice values, x fastest."""
+    res: tuple
+    origin: tuple
+    extent: tuple
+    values: np.ndarray
+
+    def at(self, x: int, y: int, z: int) -> float:
+        return float(self.values[(z * self.res[1] + y) * self.res[0] + x])
+
+    def position(self, x: int, y: int, z: int):
+        return tuple(self.origin[a] + self.extent[a] * v / (self.res[a] - 1) for a, v in enumerate((x, y, z)))
+
+
+@dataclass
+class ScalarField2:
+    """tg::ScalarField2 (marching.hpp:27-37)."""
+    res: tuple
+    origin: tuple
+    extent: tuple
+    values: np.ndarray
+
+
+def _lattice(grid: TaylorGrid, lat, out=None, stream=None):
+    n = 1
+    for a in range(grid.spec.dim):
+        n *= int(lat[a])
+    if out is not None:  # device output tensor
+        _check(lib().tgcu_sample_grid_field(grid.handle, _res3(lat, grid.spec.dim), _ptr(out), 0,
+                                            C.c_void_p(stream) if stream else None))
+        return out
+    vals = np.empty(n, dtype=np.float32)
+    _check(lib().tgcu_sample_grid_field(grid.handle, _res3(lat, grid.spec.dim), _ptr(vals), TGCU_HOST, None))
+    return vals.astype(np.float64)
+
+
+def sample_grid_field(grid: TaylorGrid, res, out=None, stream=None):
+    """sample_grid_field (marching.cpp:53-58) -> ScalarField3; with `out` (a CUDA
+    float32 tensor of prod(res)) the values stay on the device."""
+    if grid.spec.dim != 3:
+        raise ValueError("sample_grid_field: needs a 3D grid")
+    for r in res[:3]:
+        if int(r) < 2:
+            raise ValueError("sample_field3: resolution must be >= 2 per axis")
+    v = _lattice(grid, res, out, stream)
+    if out is not None:
+        return v
+    return ScalarField3(tuple(int(r) for r in res[:3]), tuple(grid.spec.origin[:3]), tuple(grid.spec.extent[:3]), v)
+
+
+def sample_grid_field2(grid: TaylorGrid, nx: int, ny: int) -> ScalarField2:
+    """The CLI's 2D lattice (tools/main.cpp:33-45) -> ScalarField2."""
+    v = _lattice(grid, (nx, ny))
+    return ScalarField2((nx, ny), tuple(grid.spec.origin[:2]), tuple(grid.spec.extent[:2]), v)
+
+
+class StoragePrecision(IntEnum):
+    """tg::StoragePrecision (grid_io.hpp:9)."""
+    F64 = 0
+    F32 = 1
+
+
+def save_tgrid(grid: TaylorGrid, path, precision: StoragePrecision = StoragePrecision.F64) -> None:
+    """save_tgrid (grid_io.cpp:44-65)."""
+    _check(lib().tgcu_save_tgrid(grid.handle, os.fspath(path).encode(), int(precision)))
+
+
+def load_tgrid(path, device: int = 0) -> TaylorGrid:
+    """load_tgrid (grid_io.cpp:67-109) -> a device grid (F64 payloads narrowed to fp32)."""
+    h = C.c_void_p()
+    _check(lib().tgcu_load_tgrid(os.fspath(path).encode(), device, C.byref(h)))
+    cs = _Spec()
+    lib().tgcu_grid_spec_of(h, C.byref(cs))
+    spec = GridSpec(dim=cs.dim, resolution=tuple(cs.res[:cs.dim]), origin=tuple(cs.origin[:cs.dim]),
+                    extent=tuple(cs.extent[:cs.dim]), order=cs.order)
+    g = TaylorGrid.__new__(TaylorGrid)
+    g.spec, g._h, g.device = spec, h, device
+    return g
+
+
+def tgrid_file_size(spec: GridSpec, precision: StoragePrecision = StoragePrecision.F64) -> int:
+    """tgrid_file_size (grid_io.cpp:36-40)."""
+    n = int(lib().tgcu_tgrid_file_size(C.byref(spec._c()), int(precision)))
+    if n < 0:
+        raise ValueError("tgrid_file_size: invalid spec")
+    return n
+
+
+def draw_batch(pool_dev, n: int, seed: int, step: int, out_dev=None, stream=None):
+    """Device batch draw with replacement from a (pool_n, 4) CUDA float32 pool
+    (SdfProblem::compute, sdf_fit.cpp:21-23; hashed stream)."""
+    import torch
+    if out_dev is None:
+        out_dev = torch.empty((n, 4), dtype=torch.float32, device=pool_dev.device)
+    _check(lib().tgcu_draw_batch(_ptr(pool_dev), pool_dev.shape[0], n, seed, step, _ptr(out_dev),
+                                 C.c_void_p(stream) if stream else None))
+    return out_dev

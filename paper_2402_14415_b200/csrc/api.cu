@@ -14,30 +14,14 @@ namespace {
 thread_local std::string g_err;
 std::atomic<long long> g_launches{0};
 
+}  // namespace
+
+namespace tgcu {
+
 int set_err(int code, const std::string& m) {
     g_err = m;
     return code;
 }
-
-template <class F>
-int guard(F&& f) {
-    try {
-        f();
-        return TGCU_OK;
-    } catch (const tgcu::Error& e) {
-        return set_err(e.code, e.what());
-    } catch (const std::bad_alloc& e) {
-        return set_err(TGCU_ERR_RESOURCE, e.what());
-    } catch (const std::exception& e) {
-        return set_err(TGCU_ERR_CUDA, e.what());
-    }
-}
-
-cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
-
-}  // namespace
-
-namespace tgcu {
 
 void count_launch(int n) { g_launches += n; }
 
@@ -120,7 +104,26 @@ void ensure_grad(Grid& g) {
     TGCU_CUDA(cudaMemset(g.grad, 0, sizeof(float) * g.NC));
 }
 
-static void validate_spec(const tgcu_grid_spec& s) {
+DevSpec make_devspec(const tgcu_grid_spec& s) {
+    DevSpec d{};
+    for (int a = 0; a < 3; ++a) {
+        const bool act = a < s.dim;
+        d.res[a] = act ? s.res[a] : 1;
+        d.origin[a] = act ? s.origin[a] : 0.0;
+        d.hi[a] = act ? s.origin[a] + s.extent[a] : 0.0;
+        d.h[a] = act ? s.extent[a] / (s.res[a] - 1) : 1.0;
+        d.inv_h[a] = act ? 1.0 / d.h[a] : 0.0;
+        d.hf[a] = (float)d.h[a];
+        d.inv_hf[a] = (float)d.inv_h[a];
+    }
+    d.sy = s.res[0];
+    d.sz = (long long)s.res[0] * (s.dim == 3 ? s.res[1] : 1);
+    d.zoff = 0;
+    d.zstore = s.dim == 3 ? s.res[2] : 1;
+    return d;
+}
+
+void validate_spec(const tgcu_grid_spec& s) {
     // GridSpec::validate (grid_spec.cpp:21-33) + coeff_count ranges.
     require(s.dim == 2 || s.dim == 3, "coeff_count: dim must be 2 or 3, got " + std::to_string(s.dim));
     require(s.order >= 0 && s.order <= 2, "coeff_count: order must be in {0,1,2}, got " + std::to_string(s.order));
@@ -135,7 +138,7 @@ static void validate_spec(const tgcu_grid_spec& s) {
     }
 }
 
-static int coeff_count_of(int order, int dim) {
+int coeff_count_of(int order, int dim) {
     return order == 0 ? 1 : (order == 1 ? 1 + dim : 1 + dim + dim * (dim + 1) / 2);
 }
 
@@ -235,18 +238,7 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         g.slab = slab;
         TGCU_CUDA(cudaSetDevice(device));
         DevSpec& d = g.ds;
-        for (int a = 0; a < 3; ++a) {
-            const bool act = a < s.dim;
-            d.res[a] = act ? s.res[a] : 1;
-            d.origin[a] = act ? s.origin[a] : 0.0;
-            d.hi[a] = act ? s.origin[a] + s.extent[a] : 0.0;
-            d.h[a] = act ? s.extent[a] / (s.res[a] - 1) : 1.0;
-            d.inv_h[a] = act ? 1.0 / d.h[a] : 0.0;
-            d.hf[a] = (float)d.h[a];
-            d.inv_hf[a] = (float)d.inv_h[a];
-        }
-        d.sy = s.res[0];
-        d.sz = (long long)s.res[0] * (s.dim == 3 ? s.res[1] : 1);
+        d = make_devspec(s);
         d.zoff = zoff;
         d.zstore = zstore;
         // TV normaliser P*K of the global grid (sdf_loss.cpp:161-170).
@@ -669,6 +661,11 @@ int tgcu_adam_reset(tgcu_grid* h, const tgcu_adam_config* cfg) {
         TGCU_CUDA(cudaMemset(g.m[g.cur], 0, sizeof(float) * g.NC));
         TGCU_CUDA(cudaMemset(g.v[g.cur], 0, sizeof(float) * g.NC));
     });
+}
+
+int tgcu_grid_steps_launched(const tgcu_grid* h, int64_t* n) {
+    *n = h->g.steps_launched;
+    return TGCU_OK;
 }
 
 int tgcu_adam_get_t(const tgcu_grid* h, int64_t* t) {

@@ -21,7 +21,6 @@ __global__ void __launch_bounds__(256) k_eval_direct(DevSpec s, const float* __r
                                                      const float* __restrict__ pts, long long n,
                                                      float* __restrict__ vals, float* __restrict__ grads,
                                                      Status* st) {
-    constexpr int K = KOf<DIM, ORDER>::value;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         double x[DIM];
@@ -47,23 +46,8 @@ __global__ void __launch_bounds__(256) k_eval_direct(DevSpec s, const float* __r
             ax[a] = axis_factors(s, a, local);
             base += (long long)c * (a == 0 ? 1LL : (a == 1 ? s.sy : s.sz));
         }
-        // Issue every corner's loads before any math (8 independent gathers).
-        float cb[1 << DIM][K];
-#pragma unroll
-        for (int c = 0; c < (1 << DIM); ++c) {
-            const long long vid = base + (c & 1) + ((c >> 1) & 1) * s.sy + (DIM == 3 ? ((c >> 2) & 1) * s.sz : 0);
-            load_block<K, true>(coeffs + vid * K, cb[c]);
-        }
-        float f = 0.0f;
         float fg[DIM];
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
-#pragma unroll
-        for (int c = 0; c < (1 << DIM); ++c) {
-            const Corner<DIM> g = corner_geom<DIM>(s, ax, c);
-            blend_corner<DIM, ORDER, GRAD>(cb[c], g, f, fg);
-        }
-        vals[i] = f;
+        vals[i] = eval_cell<DIM, ORDER, GRAD>(s, coeffs, base, ax, fg);
         if (GRAD) {
 #pragma unroll
             for (int a = 0; a < 3; ++a) grads[3 * i + a] = a < DIM ? fg[a] : 0.0f;

@@ -231,6 +231,32 @@ int tgcu_sample_uniform(int dim, uint64_t seed, int64_t n, double lo, double hi,
     return TGCU_OK;
 }
 
+struct tgcu_rng {
+    Rng r;
+};
+
+int tgcu_rng_create(uint64_t seed, tgcu_rng** out) {
+    if (!out) return TGCU_ERR_INVALID_ARGUMENT;
+    *out = new tgcu_rng{Rng(seed)};
+    return TGCU_OK;
+}
+
+void tgcu_rng_destroy(tgcu_rng* r) { delete r; }
+
+int tgcu_rng_index(tgcu_rng* r, uint64_t n, int64_t count, int64_t* out) {
+    if (!r || !out || n == 0 || count < 0) return TGCU_ERR_INVALID_ARGUMENT;
+    for (int64_t i = 0; i < count; ++i) out[i] = static_cast<int64_t>(r->r.index(n));
+    return TGCU_OK;
+}
+
+int tgcu_shuffle_order(uint64_t seed, int64_t n, uint32_t* order) {
+    if (n < 0 || (n > 0 && !order)) return TGCU_ERR_INVALID_ARGUMENT;
+    for (int64_t i = 0; i < n; ++i) order[i] = static_cast<uint32_t>(i);
+    Rng rng(seed);
+    for (int64_t i = n; i > 1; --i) std::swap(order[i - 1], order[rng.index(static_cast<uint64_t>(i))]);
+    return TGCU_OK;
+}
+
 int tgcu_shape_sdf(int shape, int dim, double param0, const double* pts, int64_t n, double* out) {
     if (n < 0 || !pts || !out) return TGCU_ERR_INVALID_ARGUMENT;
     std::vector<Prim> prims;

@@ -197,6 +197,29 @@ __device__ __forceinline__ void blend_corner(const float (&c)[K], const Corner<D
     }
 }
 
+// Value (+ spatial gradient) of the cell whose corner-0 vertex is `base`:
+// issue all 2^D block gathers first, then blend (eval_impl, taylor_grid.cpp:100-119).
+template <int DIM, int ORDER, bool GRAD>
+__device__ __forceinline__ float eval_cell(const DevSpec& s, const float* __restrict__ coeffs, long long base,
+                                           const AxisF* ax, float* fg) {
+    constexpr int K = KOf<DIM, ORDER>::value;
+    float cb[1 << DIM][K];
+#pragma unroll
+    for (int c = 0; c < (1 << DIM); ++c) {
+        const long long vid = base + (c & 1) + ((c >> 1) & 1) * s.sy + (DIM == 3 ? ((c >> 2) & 1) * s.sz : 0);
+        load_block<K, true>(coeffs + vid * K, cb[c]);
+    }
+    float f = 0.0f;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < (1 << DIM); ++c) {
+        const Corner<DIM> g = corner_geom<DIM>(s, ax, c);
+        blend_corner<DIM, ORDER, GRAD>(cb[c], g, f, fg);
+    }
+    return f;
+}
+
 // Coefficient-gradient contribution of one (point, corner):
 // alpha = u*w + gvec.dw, beta = w (accumulate_cell, taylor_grid.cpp:123-152).
 template <int DIM, int ORDER, int K>

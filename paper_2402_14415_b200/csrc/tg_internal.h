@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <new>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -33,6 +34,32 @@ inline void require(bool cond, const std::string& msg) {
     } while (0)
 
 void count_launch(int n = 1);
+
+// C-boundary error plumbing (api.cu): records the thread-local message read by
+// tgcu_last_error() and returns the status code.
+int set_err(int code, const std::string& m);
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return TGCU_OK;
+    } catch (const Error& e) {
+        return set_err(e.code, e.what());
+    } catch (const std::bad_alloc& e) {
+        return set_err(TGCU_ERR_RESOURCE, e.what());
+    } catch (const std::exception& e) {
+        return set_err(TGCU_ERR_CUDA, e.what());
+    }
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// GridSpec::validate (grid_spec.cpp:21-33) + coeff_count ranges; throws Error.
+void validate_spec(const tgcu_grid_spec& s);
+int coeff_count_of(int order, int dim);
+// Device geometry of a full (non-slab) grid spec.
+DevSpec make_devspec(const tgcu_grid_spec& s);
 
 // Brick edge (vertices per axis) of the fused training kernel and the
 // brick-binned query.
@@ -140,6 +167,8 @@ void launch_all_finite(const float* src, int64_t n, unsigned long long* flag, cu
 void launch_fill_f0(Grid& g, float* dst, float value, cudaStream_t s);
 void launch_hash_gaussian(float* dst, int64_t n, uint64_t seed, double sigma, int64_t goff, cudaStream_t s);
 void launch_hash_points(float* out, int64_t n, int dim, uint64_t seed, double lo, double hi, cudaStream_t s);
+void launch_draw_batch(const float* pool, int64_t pool_n, int64_t n, uint64_t seed, uint64_t step, float* out,
+                       cudaStream_t s);
 
 }  // namespace tgcu
 

@@ -353,6 +353,28 @@ __global__ void k_hash_points(float* __restrict__ out, long long n, int dim, uns
     }
 }
 
+// SdfProblem batch draw (sdf_fit.cpp:21-23): n samples with replacement from
+// a device-resident pool; index = floor(u * pool_n) from a counter hash of
+// (seed, step, i) in place of the reference's mt19937_64 stream.
+__global__ void k_draw_batch(const float4* __restrict__ pool, long long pool_n, long long n,
+                             unsigned long long seed, unsigned long long step, float4* __restrict__ out) {
+    const unsigned long long key = splitmix64(seed ^ (step * 0xD1B54A32D192ED03ULL));
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        long long j = (long long)(hash_uniform(key, (unsigned long long)i) * (double)pool_n);
+        j = j < pool_n ? j : pool_n - 1;
+        out[i] = __ldg(pool + j);
+    }
+}
+
+void launch_draw_batch(const float* pool, int64_t pool_n, int64_t n, uint64_t seed, uint64_t step, float* out,
+                       cudaStream_t s) {
+    if (n <= 0) return;
+    k_draw_batch<<<grid_blocks(n, 256, 148 * 16), 256, 0, s>>>(reinterpret_cast<const float4*>(pool), pool_n, n, seed,
+                                                                step, reinterpret_cast<float4*>(out));
+    count_launch();
+    TGCU_CUDA(cudaGetLastError());
+}
+
 void launch_hash_gaussian(float* dst, int64_t n, uint64_t seed, double sigma, int64_t goff, cudaStream_t s) {
     k_hash_gaussian<<<grid_blocks(n, 256, 148 * 64), 256, 0, s>>>(dst, n, seed, (float)sigma, goff);
     count_launch();
