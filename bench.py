@@ -238,6 +238,8 @@ def query_leg(device, hbm_peak, reps=10):
         K = g.spec.coeffs_per_vertex()
         if offs is None:
             offs = torch.empty(tg.query_brick_codes(g) + 1, dtype=torch.int64, device=pts.device)
+            tg.sort_points(g, pts, spts, None, offs)  # warm-up: stream-pool growth, CUB module load
+            torch.cuda.synchronize()
             t0.record(st)
             tg.sort_points(g, pts, spts, None, offs)
             t1.record(st)

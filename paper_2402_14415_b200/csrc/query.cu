@@ -121,24 +121,26 @@ __device__ __forceinline__ unsigned long long point_key(const DevSpec& s, const 
     return (kb << (DIM * LB)) | kc;
 }
 
-template <int DIM, int LB>
-__global__ void k_point_keys(DevSpec s, const float* __restrict__ pts, long long n,
-                             unsigned long long* __restrict__ keys, long long* __restrict__ idx) {
+template <int DIM, int LB, class KeyT, class IdxT>
+__global__ void k_point_keys(DevSpec s, const float* __restrict__ pts, long long n, KeyT* __restrict__ keys,
+                             IdxT* __restrict__ idx) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        keys[i] = point_key<DIM, LB>(s, pts + 3 * i, nullptr);
-        idx[i] = i;
+        keys[i] = (KeyT)point_key<DIM, LB>(s, pts + 3 * i, nullptr);
+        idx[i] = (IdxT)i;
     }
 }
 
-__global__ void k_gather_points(const float* __restrict__ pts, const long long* __restrict__ idx, long long n,
-                                float* __restrict__ out) {
+template <class IdxT>
+__global__ void k_gather_points(const float* __restrict__ pts, const IdxT* __restrict__ idx, long long n,
+                                float* __restrict__ out, long long* __restrict__ perm) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        const long long j = idx[i];
+        const long long j = (long long)idx[i];
         out[3 * i] = pts[3 * j];
         out[3 * i + 1] = pts[3 * j + 1];
         out[3 * i + 2] = pts[3 * j + 2];
+        if (perm) perm[i] = j;
     }
 }
 
@@ -162,8 +164,8 @@ int64_t query_brick_codes(const Grid& g) {
 // off[c] = first sorted index whose brick code >= c, for c in [0, codes].
 // Each i writes the codes in (code(i-1), code(i)]; the last point also writes
 // the tail up to `codes`.
-template <int DIM, int LB, bool FROM_KEYS>
-__global__ void k_brick_offsets(DevSpec s, const unsigned long long* __restrict__ keys, const float* __restrict__ pts,
+template <int DIM, int LB, bool FROM_KEYS, class KeyT>
+__global__ void k_brick_offsets(DevSpec s, const KeyT* __restrict__ keys, const float* __restrict__ pts,
                                 long long n, long long codes, long long* __restrict__ off) {
     constexpr int SH = DIM * LB;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n;
@@ -182,61 +184,67 @@ __global__ void k_brick_offsets(DevSpec s, const unsigned long long* __restrict_
     }
 }
 
-void launch_brick_offsets(Grid& g, const unsigned long long* keys, const float* pts, int64_t n, int64_t* off,
-                          cudaStream_t s) {
+template <class KeyT>
+void launch_brick_offsets(Grid& g, const KeyT* keys, const float* pts, int64_t n, int64_t* off, cudaStream_t s) {
     const long long codes = query_brick_codes(g);
     const int blocks = grid_blocks(n + 1, 256, 148 * 32);
     long long* o = reinterpret_cast<long long*>(off);
     if (g.spec.dim == 3) {
-        if (keys) k_brick_offsets<3, 3, true><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
-        else k_brick_offsets<3, 3, false><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
+        if (keys) k_brick_offsets<3, 3, true, KeyT><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
+        else k_brick_offsets<3, 3, false, KeyT><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
     } else {
-        if (keys) k_brick_offsets<2, 4, true><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
-        else k_brick_offsets<2, 4, false><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
+        if (keys) k_brick_offsets<2, 4, true, KeyT><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
+        else k_brick_offsets<2, 4, false, KeyT><<<blocks, 256, 0, s>>>(g.ds, keys, pts, n, codes, o);
     }
     count_launch();
     TGCU_CUDA(cudaGetLastError());
 }
 
-void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, int64_t* offsets,
-                        cudaStream_t s) {
-    if (n <= 0) return;
-    unsigned long long *keys = nullptr, *keys_out = nullptr;
-    long long *idx = nullptr, *idx_out = nullptr;
+// Key = Morton(brick) : Morton(cell in brick), end_bit = D * ceil(log2(max cells)).
+// 32-bit keys and indices whenever they fit (halves the radix passes' bytes).
+template <class KeyT, class IdxT>
+static void sort_points_t(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, int64_t* offsets,
+                          int end_bit, cudaStream_t s) {
+    KeyT *keys = nullptr, *keys_out = nullptr;
+    IdxT *idx = nullptr, *idx_out = nullptr;
     void* temp = nullptr;
     size_t temp_bytes = 0;
-    TGCU_CUDA(cudaMallocAsync(&keys, n * 8, s));
-    TGCU_CUDA(cudaMallocAsync(&keys_out, n * 8, s));
-    TGCU_CUDA(cudaMallocAsync(&idx, n * 8, s));
-    idx_out = reinterpret_cast<long long*>(perm);
-    bool own_perm = false;
-    if (!idx_out) {
-        TGCU_CUDA(cudaMallocAsync(&idx_out, n * 8, s));
-        own_perm = true;
-    }
+    TGCU_CUDA(cudaMallocAsync(&keys, n * sizeof(KeyT), s));
+    TGCU_CUDA(cudaMallocAsync(&keys_out, n * sizeof(KeyT), s));
+    TGCU_CUDA(cudaMallocAsync(&idx, n * sizeof(IdxT), s));
+    TGCU_CUDA(cudaMallocAsync(&idx_out, n * sizeof(IdxT), s));
     const int blocks = grid_blocks(n, 256, 148 * 32);
-    int maxc = 1;
-    for (int a = 0; a < g.spec.dim; ++a) maxc = std::max(maxc, g.spec.res[a] - 2);
-    int bits = 1;
-    while ((1 << bits) <= maxc) ++bits;
-    const int end_bit = g.spec.dim * bits;
-    if (g.spec.dim == 3) k_point_keys<3, 3><<<blocks, 256, 0, s>>>(g.ds, pts, n, keys, idx);
-    else k_point_keys<2, 4><<<blocks, 256, 0, s>>>(g.ds, pts, n, keys, idx);
+    if (g.spec.dim == 3) k_point_keys<3, 3, KeyT, IdxT><<<blocks, 256, 0, s>>>(g.ds, pts, n, keys, idx);
+    else k_point_keys<2, 4, KeyT, IdxT><<<blocks, 256, 0, s>>>(g.ds, pts, n, keys, idx);
     count_launch();
     TGCU_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, keys_out, idx, idx_out, (int64_t)n, 0,
                                               end_bit, s));
     TGCU_CUDA(cudaMallocAsync(&temp, temp_bytes, s));
     TGCU_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_out, idx, idx_out, (int64_t)n, 0,
                                               end_bit, s));
-    k_gather_points<<<blocks, 256, 0, s>>>(pts, idx_out, n, out);
+    k_gather_points<IdxT><<<blocks, 256, 0, s>>>(pts, idx_out, n, out, reinterpret_cast<long long*>(perm));
     count_launch();
-    if (offsets) launch_brick_offsets(g, keys_out, nullptr, n, offsets, s);
+    if (offsets) launch_brick_offsets<KeyT>(g, keys_out, nullptr, n, offsets, s);
     TGCU_CUDA(cudaFreeAsync(temp, s));
     TGCU_CUDA(cudaFreeAsync(keys, s));
     TGCU_CUDA(cudaFreeAsync(keys_out, s));
     TGCU_CUDA(cudaFreeAsync(idx, s));
-    if (own_perm) TGCU_CUDA(cudaFreeAsync(idx_out, s));
+    TGCU_CUDA(cudaFreeAsync(idx_out, s));
     TGCU_CUDA(cudaGetLastError());
+}
+
+void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, int64_t* offsets,
+                        cudaStream_t s) {
+    if (n <= 0) return;
+    int maxc = 1;
+    for (int a = 0; a < g.spec.dim; ++a) maxc = std::max(maxc, g.spec.res[a] - 2);
+    int bits = 1;
+    while ((1 << bits) <= maxc) ++bits;
+    const int end_bit = g.spec.dim * bits;
+    if (end_bit <= 32 && n < (1LL << 31))
+        sort_points_t<unsigned int, unsigned int>(g, pts, n, out, perm, offsets, end_bit, s);
+    else
+        sort_points_t<unsigned long long, unsigned long long>(g, pts, n, out, perm, offsets, end_bit, s);
 }
 
 // One CTA per Morton brick code (blockIdx.x). The brick's (B+1)^DIM vertex
@@ -358,7 +366,7 @@ void launch_eval_sorted(Grid& g, const float* pts, int64_t n, const int64_t* off
     long long* tmp = nullptr;
     if (!offsets) {  // points sorted but no offsets given: one boundary pass
         TGCU_CUDA(cudaMallocAsync(&tmp, sizeof(long long) * (codes + 1), s));
-        launch_brick_offsets(g, nullptr, pts, n, reinterpret_cast<int64_t*>(tmp), s);
+        launch_brick_offsets<unsigned int>(g, nullptr, pts, n, reinterpret_cast<int64_t*>(tmp), s);
         offsets = reinterpret_cast<const int64_t*>(tmp);
     }
     const long long* off = reinterpret_cast<const long long*>(offsets);

@@ -69,64 +69,69 @@ __global__ void k_axis_table(DevSpec s, int dim, int3 n, int mode, double3 org, 
     }
 }
 
-// multilinear_resample: one thread per (new vertex, channel), so stores are
-// fully coalesced; weights and accumulation in fp64 in the reference's order
-// (w_i = prod_a s_a; dst = sum_i w_i * src_i), rounded once to fp32.
-template <int DIM>
-__global__ void __launch_bounds__(256) k_resample(const AxisLoc* __restrict__ loc, int3 n, long long sy_old,
-                                                  long long sz_old, const float* __restrict__ src, int C,
-                                                  float* __restrict__ dst, long long total) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const long long v = t / C;
-        const int ch = (int)(t - v * C);
-        const int x = (int)(v % n.x);
-        const long long yz = v / n.x;
-        const int y = (int)(yz % n.y);
-        const int z = DIM == 3 ? (int)(yz / n.y) : 0;
-        const AxisLoc lx = loc[x];
-        const AxisLoc ly = loc[n.x + y];
-        const AxisLoc lz = DIM == 3 ? loc[n.x + n.y + z] : AxisLoc{0, 0, 0.0};
-        const long long base = lx.cell + ly.cell * sy_old + (DIM == 3 ? lz.cell * sz_old : 0);
-        const double L[3] = {lx.local, ly.local, lz.local};
-        double acc = 0.0;
+// multilinear_resample: one thread per new vertex of one output row
+// (blockIdx.y = y, blockIdx.z = z). The 8 corner weights are formed once in
+// fp64 exactly as the reference does (w = ((1 * s_x) * s_y) * s_z with
+// s = bit ? local : 1 - local; 1 * s_x is exact, so the x*y partial products
+// are shared between corners) and reused for every channel; per channel the
+// accumulation dst = sum_i w_i * src_i runs in the reference's corner order
+// (0 + w_0 src_0 is exact, so the first term starts the sum), rounded once.
+template <int DIM, int C>
+__global__ void __launch_bounds__(128) k_resample(const AxisLoc* __restrict__ loc, int3 n, long long sy_old,
+                                                  long long sz_old, const float* __restrict__ src, int Crt,
+                                                  float* __restrict__ dst) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n.x) return;
+    const int NC = C > 0 ? C : Crt;
+    const int y = blockIdx.y, z = blockIdx.z;
+    const AxisLoc lx = loc[x];
+    const AxisLoc ly = loc[n.x + y];
+    const AxisLoc lz = DIM == 3 ? loc[n.x + n.y + z] : AxisLoc{0, 0, 0.0};
+    const long long base = lx.cell + ly.cell * sy_old + (DIM == 3 ? lz.cell * sz_old : 0);
+    const double sx[2] = {__dsub_rn(1.0, lx.local), lx.local};
+    const double sy[2] = {__dsub_rn(1.0, ly.local), ly.local};
+    const double sz[2] = {__dsub_rn(1.0, lz.local), lz.local};
+    double w[1 << DIM];
 #pragma unroll
-        for (int i = 0; i < (1 << DIM); ++i) {
-            double w = 1.0;
+    for (int i = 0; i < (1 << DIM); ++i) {
+        const double wxy = __dmul_rn(sx[i & 1], sy[(i >> 1) & 1]);
+        w[i] = DIM == 3 ? __dmul_rn(wxy, sz[(i >> 2) & 1]) : wxy;
+    }
+    const float* sp[1 << DIM];
 #pragma unroll
-            for (int a = 0; a < DIM; ++a) w = __dmul_rn(w, ((i >> a) & 1) ? L[a] : __dsub_rn(1.0, L[a]));
-            const long long vid =
-                base + (i & 1) + ((i >> 1) & 1) * sy_old + (DIM == 3 ? ((i >> 2) & 1) * sz_old : 0);
-            acc = __dadd_rn(acc, __dmul_rn(w, (double)__ldg(src + vid * C + ch)));
-        }
-        dst[t] = (float)acc;
+    for (int i = 0; i < (1 << DIM); ++i)
+        sp[i] = src + (base + (i & 1) + ((i >> 1) & 1) * sy_old + (DIM == 3 ? ((i >> 2) & 1) * sz_old : 0)) * NC;
+    float* dp = dst + (((long long)z * n.y + y) * n.x + x) * NC;
+#pragma unroll(C > 0 ? C : 1)
+    for (int ch = 0; ch < NC; ++ch) {
+        double acc = __dmul_rn(w[0], (double)__ldg(sp[0] + ch));
+#pragma unroll
+        for (int i = 1; i < (1 << DIM); ++i) acc = __dadd_rn(acc, __dmul_rn(w[i], (double)__ldg(sp[i] + ch)));
+        dp[ch] = (float)acc;
     }
 }
 
-// sample_grid_field: one thread per lattice point (x fastest, so a warp shares
-// cells and its block gathers hit L1); per-axis fp32 factors from the table.
+// sample_grid_field: one thread per lattice point of one lattice row (x
+// fastest, so a warp shares cells and its block gathers hit L1); per-axis fp32
+// factors from the table.
 template <int DIM, int ORDER>
 __global__ void __launch_bounds__(256) k_eval_lattice(DevSpec s, const float* __restrict__ coeffs,
                                                       const float4* __restrict__ fac, const int* __restrict__ cell,
-                                                      int3 n, float* __restrict__ vals, long long total) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int x = (int)(t % n.x);
-        const long long yz = t / n.x;
-        const int y = (int)(yz % n.y);
-        const int z = DIM == 3 ? (int)(yz / n.y) : 0;
-        const int idx[3] = {x, n.x + y, n.x + n.y + z};
-        AxisF ax[DIM];
-        long long base = 0;
+                                                      int3 n, float* __restrict__ vals) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n.x) return;
+    const int y = blockIdx.y, z = blockIdx.z;
+    const int idx[3] = {x, n.x + y, n.x + n.y + z};
+    AxisF ax[DIM];
+    long long base = 0;
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) {
-            const float4 f = __ldg(fac + idx[a]);
-            ax[a] = AxisF{f.x, f.y, f.z, f.w};
-            base += (long long)__ldg(cell + idx[a]) * (a == 0 ? 1LL : (a == 1 ? s.sy : s.sz));
-        }
-        float fg[DIM];
-        vals[t] = eval_cell<DIM, ORDER, false>(s, coeffs, base, ax, fg);
+    for (int a = 0; a < DIM; ++a) {
+        const float4 f = __ldg(fac + idx[a]);
+        ax[a] = AxisF{f.x, f.y, f.z, f.w};
+        base += (long long)__ldg(cell + idx[a]) * (a == 0 ? 1LL : (a == 1 ? s.sy : s.sz));
     }
+    float fg[DIM];
+    vals[((long long)z * n.y + y) * n.x + x] = eval_cell<DIM, ORDER, false>(s, coeffs, base, ax, fg);
 }
 
 namespace {
@@ -150,15 +155,23 @@ void resample_device(const tgcu_grid_spec& old_spec, const float* data, int C, c
     TGCU_CUDA(cudaMallocAsync(&loc, sizeof(AxisLoc) * na, st));
     k_axis_table<<<grid_blocks(na, 256), 256, 0, st>>>(s, dim, n, 0, org, ext, step, loc, nullptr, nullptr);
     count_launch();
-    const long long total = (long long)n.x * n.y * n.z * C;
-    if (total > 0) {
-        const int blocks = grid_blocks(total, 256, 148 * 16);
-        if (dim == 3)
-            k_resample<3><<<blocks, 256, 0, st>>>(loc, n, s.sy, s.sz, data, C, out, total);
-        else
-            k_resample<2><<<blocks, 256, 0, st>>>(loc, n, s.sy, s.sz, data, C, out, total);
-        count_launch();
+    require(n.y < 65536 && n.z < 65536, "multilinear_resample: resolution too large");
+    const int thr = std::min(128, (n.x + 31) / 32 * 32);
+    const dim3 blocks((n.x + thr - 1) / thr, n.y, n.z);
+#define TGCU_RS(DIMV, CV) k_resample<DIMV, CV><<<blocks, thr, 0, st>>>(loc, n, s.sy, s.sz, data, C, out)
+    if (dim == 3) {
+        if (C == 10) TGCU_RS(3, 10);
+        else if (C == 4) TGCU_RS(3, 4);
+        else if (C == 1) TGCU_RS(3, 1);
+        else TGCU_RS(3, 0);
+    } else {
+        if (C == 6) TGCU_RS(2, 6);
+        else if (C == 3) TGCU_RS(2, 3);
+        else if (C == 1) TGCU_RS(2, 1);
+        else TGCU_RS(2, 0);
     }
+#undef TGCU_RS
+    count_launch();
     TGCU_CUDA(cudaGetLastError());
     TGCU_CUDA(cudaFreeAsync(loc, st));
 }
@@ -271,9 +284,11 @@ int tgcu_sample_grid_field(tgcu_grid* h, const int lattice[3], float* values, in
         k_axis_table<<<grid_blocks(na, 256), 256, 0, st>>>(g.ds, dim, n, 1, org, ext, double3{1.0, 1.0, 1.0},
                                                            nullptr, fac, cell);
         count_launch();
+        require(n.y < 65536 && n.z < 65536, "sample_grid_field: lattice too large");
+        const int thr = std::min(256, (n.x + 31) / 32 * 32);
+        const dim3 blocks((n.x + thr - 1) / thr, n.y, n.z);
         TGCU_DISPATCH(dim, g.spec.order, {
-            k_eval_lattice<DIM, ORDER><<<grid_blocks(total, 256, 148 * 16), 256, 0, st>>>(g.ds, g.p[g.cur], fac,
-                                                                                         cell, n, dv, total);
+            k_eval_lattice<DIM, ORDER><<<blocks, thr, 0, st>>>(g.ds, g.p[g.cur], fac, cell, n, dv);
         });
         count_launch();
         TGCU_CUDA(cudaGetLastError());
