@@ -2,6 +2,7 @@
 // kernel launchers each .cu file provides.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (header only; the encoder is fetched through the runtime)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -121,6 +122,11 @@ struct Grid {
     int64_t staging_cap = 0;             // floats
     double* scratch_d = nullptr;         // reductions (unfused path)
     int64_t scratch_cap = 0;
+    // TMA tensor maps of the fused step (train.cu ensure_tmaps): per ping-pong
+    // slot, the parameter tile box (B+2)^D x K, and the owned box B^D x K of
+    // p, m and v. tm_state: 0 = not built, 1 = usable, -1 = layout not eligible.
+    CUtensorMap tm_tile[2], tm_own_p[2], tm_own_m[2], tm_own_v[2];
+    int tm_state = 0;
     // Live kernel timing (tgcu_profile_*): CUDA events recorded on the launch
     // stream around the fused brick kernel.
     bool prof_on = false;

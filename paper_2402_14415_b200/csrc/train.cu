@@ -27,6 +27,8 @@
 //   and commits the step by naming the new current buffer; a failed step
 //   leaves the old buffers current and makes every later step a no-op until
 //   the host reads the sticky error.
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
 #include <climits>
 
 #include "dispatch.cuh"
@@ -320,6 +322,10 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_scatter_tiles(BinArgs A, co
 }
 
 struct StepArgs {
+    // TMA tensor maps (use_tmap): parameter tile (load), owned boxes of
+    // p (store), m and v (load + store).
+    CUtensorMap tm_tile, tm_p_out, tm_m_in, tm_v_in, tm_m_out, tm_v_out;
+    int use_tmap;
     DevSpec s;
     const float* p_in;
     float* p_out;
@@ -381,23 +387,31 @@ __device__ __forceinline__ void block_excl_scan(const int* __restrict__ cnt, int
 
 // Shared-memory plan of the fused brick kernel (one brick per CTA, 2 CTAs/SM).
 // Tile rows (fixed y, z) are stored with a stride of TROWF floats and start
-// SHF floats into the row, so that a row's HBM range is one 16-byte-aligned
-// TMA bulk copy (the reference AoS layout puts vertex o-1 at an 8-byte offset
-// for K = 10).
+// SHF floats into the row, so that a row's HBM range begins 16-byte aligned
+// (the reference AoS layout puts vertex o-1 at an 8-byte offset for K = 10):
+// one TMA tensor box of TROWF x T [x T] floats, or one bulk copy per row.
+// Regions start on 128-byte boundaries (TMA tensor smem alignment).
 template <int DIM, int ORDER>
 struct BrickSmem {
     using S = BrickShape<DIM>;
     static constexpr int K = KOf<DIM, ORDER>::value;
     static constexpr int SHF = (4 - (K % 4)) % 4;
     static constexpr int TROWF = ((S::T * K + SHF + 3) / 4) * 4;
+    // TMA tensor boxes: the tile box is TROWF floats wide starting SHF floats
+    // before vertex o-1 (a 16-byte-aligned element offset, as o*K is), the
+    // owned boxes B*K floats from vertex o.
+    static constexpr bool TMAP = (S::B * K * 4) % 16 == 0 && TROWF <= 256;
     static constexpr int TROWS = DIM == 3 ? S::T * S::T : S::T;
-    static constexpr int tile = TROWS * TROWF;                    // floats
-    static constexpr int mv = 2 * S::NOWN * K;                    // m then v
+    static constexpr int r32(int x) { return (x + 31) / 32 * 32; }
+    static constexpr int tile = r32(TROWS * TROWF);               // floats
+    static constexpr int mv = r32(2 * S::NOWN * K);               // m then v
     static constexpr int REC = ((3 * DIM + 1) + 1) / 2 * 2;       // s0[D] s1[D] u g[D] (even)
     static constexpr int pts = S::CH * REC;                       // cell-ordered records
     static constexpr int gs = S::NOWN * K;
-    static constexpr int uni = pts > gs ? pts : gs;
+    static constexpr int uni = r32(pts > gs ? pts : gs);
     static constexpr size_t bytes = sizeof(float) * (tile + mv + uni) + sizeof(int) * (S::NCELL * 2 + S::NT + 64 * 2);
+    static constexpr unsigned tile_box_bytes = TROWS * TROWF * 4;  // TROWF x T [x T] floats
+    static constexpr unsigned own_box_bytes = S::NOWN * K * 4;
     // float offset of tile vertex (tx, ty, tz)
     __device__ static constexpr int at(int tx, int ty, int tz) {
         return (DIM == 3 ? (tz * S::T + ty) : ty) * TROWF + SHF + tx * K;
@@ -473,7 +487,7 @@ __device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, flo
 }
 
 template <int DIM, int ORDER, bool EIK>
-__global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs A) {
+__global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __grid_constant__ StepArgs A) {
     using S = BrickShape<DIM>;
     using L = BrickSmem<DIM, ORDER>;
     constexpr int K = KOf<DIM, ORDER>::value;
@@ -497,19 +511,37 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     constexpr int NW = NT / 32;
-    const int nbx = A.nb[0], nby = A.nb[1];
-    const int b = blockIdx.x;
-    const int o[3] = {(b % nbx) * B, ((b / nbx) % nby) * B, DIM == 3 ? (A.zb0 + b / (nbx * nby)) * B : 0};
+    // grid = (nb_x, nb_y, nb_z): brick coordinates without integer division
+    const int b = ((int)blockIdx.z * A.nb[1] + (int)blockIdx.y) * A.nb[0] + (int)blockIdx.x;
+    const int o[3] = {(int)blockIdx.x * B, (int)blockIdx.y * B, DIM == 3 ? (A.zb0 + (int)blockIdx.z) * B : 0};
+    const int zrel = o[2] - A.s.zoff;  // first owned plane in the stored planes
+    const bool tmap = L::TMAP && A.use_tmap;
 
     if (tid == 0) {
-        mbar_init(&bars[0], NT);
-        mbar_init(&bars[1], NT);
+        mbar_init(&bars[0], tmap ? 1 : NT);
+        mbar_init(&bars[1], tmap ? 1 : NT);
         mbar_fence_init();
     }
     __syncthreads();
     // The tile is waited for inside the first chunk, after the points have
     // been loaded, located and counted (none of which needs it).
-    {
+    if (tmap) {
+        // one elected thread: the (B+2)^D tile (out-of-grid vertices zero
+        // filled) and the owned m, v boxes, each one TMA tensor copy
+        if (tid == 0) {
+            mbar_expect_tx(&bars[0], L::tile_box_bytes);
+            mbar_expect_tx(&bars[1], 2 * L::own_box_bytes);
+            if constexpr (DIM == 3) {
+                tma_load_3d(tile, &A.tm_tile, &bars[0], (o[0] - 1) * K - L::SHF, o[1] - 1, zrel - 1);
+                tma_load_3d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1], zrel);
+                tma_load_3d(mvs + S::NOWN * K, &A.tm_v_in, &bars[1], o[0] * K, o[1], zrel);
+            } else {
+                tma_load_2d(tile, &A.tm_tile, &bars[0], (o[0] - 1) * K - L::SHF, o[1] - 1);
+                tma_load_2d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1]);
+                tma_load_2d(mvs + S::NOWN * K, &A.tm_v_in, &bars[1], o[0] * K, o[1]);
+            }
+        }
+    } else {
         using LS = BrickSmem<DIM, ORDER>;
         constexpr int OR = DIM == 3 ? B * B : B;
         stage_brick<DIM, ORDER>(A, o, tile, mvs, &bars[0], &bars[1], tid);
@@ -808,15 +840,29 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
         }
     }
     __syncthreads();
-    // copy-out of the staged rows (p from Gs, m and v from mvs): one TMA bulk
-    // store per row and array, issued by one thread each
-    {
+    // copy-out of the staged results (p from Gs, m and v from mvs): three TMA
+    // tensor box stores (out-of-grid vertices dropped), or one bulk store per
+    // row and array, issued by one thread each
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tmap) {
+        if (tid == 0) {
+            if constexpr (DIM == 3) {
+                tma_store_3d(&A.tm_p_out, uni, o[0] * K, o[1], zrel);
+                tma_store_3d(&A.tm_m_out, mvs, o[0] * K, o[1], zrel);
+                tma_store_3d(&A.tm_v_out, mvs + S::NOWN * K, o[0] * K, o[1], zrel);
+            } else {
+                tma_store_2d(&A.tm_p_out, uni, o[0] * K, o[1]);
+                tma_store_2d(&A.tm_m_out, mvs, o[0] * K, o[1]);
+                tma_store_2d(&A.tm_v_out, mvs + S::NOWN * K, o[0] * K, o[1]);
+            }
+            bulk_commit();
+        }
+    } else {
         constexpr int OROWS = DIM == 3 ? B * B : B;
         constexpr int ROWF = B * K;
         const int nvx = min(B, A.s.res[0] - o[0]);
         const int rowf = nvx * K;
-        fence_proxy_async_smem();
-        __syncthreads();
         if (tid < 3 * OROWS) {
             const int which = tid / OROWS, r = tid - which * OROWS;
             const int ly = r % B, lz = DIM == 3 ? r / B : 0;
@@ -848,6 +894,8 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(StepArgs 
             A.partials[4 * b + tid] = acc;
         }
     }
+    // the CTA's shared memory must outlive the TMA stores' reads
+    if (tmap && tid == 0) bulk_wait_read0();
 }
 
 struct FinArgs {
@@ -945,6 +993,55 @@ __global__ void __launch_bounds__(1024) k_step_finalize(FinArgs F) {
     st->bad_grad = ULLONG_MAX;
 }
 
+// ---- TMA tensor maps of the fused step --------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        TGCU_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw Error(TGCU_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// A (rows = K * res_x floats) x res_y [x zstore] view of one coefficient-layout
+// buffer with a box of box_x floats x box_yz rows [x box_yz planes].
+static bool encode_grid_map(CUtensorMap* m, const Grid& g, const float* base, unsigned box_x, unsigned box_yz) {
+    const int dim = g.spec.dim;
+    const cuuint64_t row = (cuuint64_t)g.ds.res[0] * g.K;
+    cuuint64_t gdim[3] = {row, (cuuint64_t)g.ds.res[1], (cuuint64_t)g.ds.zstore};
+    cuuint64_t gstr[2] = {row * 4, row * 4 * (cuuint64_t)g.ds.res[1]};
+    cuuint32_t box[3] = {box_x, box_yz, box_yz};
+    cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)dim,
+                                            const_cast<float*>(base), gdim, gstr, box, es,
+                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// Build the 8 maps once the ping-pong buffers exist. Eligible when the
+// compile-time tile layout is dense (BrickSmem::TMAP) and a grid row of K*res_x
+// floats is a multiple of 16 bytes (tensor-map stride rule); otherwise the
+// kernel stages per row.
+static void ensure_tmaps(Grid& g, bool layout_ok, unsigned tile_row_floats) {
+    if (g.tm_state != 0) return;
+    g.tm_state = -1;
+    if (!layout_ok || ((int64_t)g.ds.res[0] * g.K * 4) % 16 != 0) return;
+    const int B = g.spec.dim == 3 ? kBrick3 : kBrick2;
+    const unsigned T = (unsigned)B + 2;
+    bool ok = true;
+    for (int i = 0; i < 2; ++i) {
+        ok = ok && encode_grid_map(&g.tm_tile[i], g, g.p[i], tile_row_floats, T);
+        ok = ok && encode_grid_map(&g.tm_own_p[i], g, g.p[i], (unsigned)B * g.K, (unsigned)B);
+        ok = ok && encode_grid_map(&g.tm_own_m[i], g, g.m[i], (unsigned)B * g.K, (unsigned)B);
+        ok = ok && encode_grid_map(&g.tm_own_v[i], g, g.v[i], (unsigned)B * g.K, (unsigned)B);
+    }
+    if (ok) g.tm_state = 1;
+}
+
 // Slab phase 2: commit with the globally reduced sums.
 void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& cfg, int in_idx, int64_t step,
                         int64_t t_after, int64_t n, cudaStream_t s) {
@@ -1018,7 +1115,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
         count_launch(3);
     }
 
-    StepArgs A;
+    StepArgs A{};
     A.s = g.ds;
     const int out_idx = 1 - in_idx;
     A.p_in = g.p[in_idx];
@@ -1050,6 +1147,18 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     A.grad_out = grad_out;
     A.zb0 = g.zb0;
     const bool eik = cfg.lambda1 > 0.0;
+    TGCU_DISPATCH(g.spec.dim, g.spec.order,
+                  { ensure_tmaps(g, BrickSmem<DIM, ORDER>::TMAP, BrickSmem<DIM, ORDER>::TROWF); });
+    A.use_tmap = g.tm_state == 1 ? 1 : 0;
+    if (A.use_tmap) {
+        A.tm_tile = g.tm_tile[in_idx];
+        A.tm_m_in = g.tm_own_m[in_idx];
+        A.tm_v_in = g.tm_own_v[in_idx];
+        A.tm_p_out = g.tm_own_p[out_idx];
+        A.tm_m_out = g.tm_own_m[out_idx];
+        A.tm_v_out = g.tm_own_v[out_idx];
+    }
+    const dim3 bgrid((unsigned)g.nb[0], (unsigned)g.nb[1], (unsigned)g.nb[2]);
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
         constexpr size_t smem = BrickSmem<DIM, ORDER>::bytes;
         static_assert(BrickSmem<DIM, ORDER>::bytes <= 227 * 1024, "brick smem");
@@ -1063,7 +1172,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
             configured = true;
         }
         if (g.prof_on) prof_mark(g, s, 0);
-        kern<<<(unsigned)g.NB, BrickShape<DIM>::NT, smem, s>>>(A);
+        kern<<<bgrid, BrickShape<DIM>::NT, smem, s>>>(A);
         if (g.prof_on) prof_mark(g, s, 1);
     });
 
