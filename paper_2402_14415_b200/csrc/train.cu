@@ -235,8 +235,22 @@ __global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta,
     const int nb = min(kColBricks, NB - b0);
     constexpr int LD = kColBricks + 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // warp w loads rows c = w, w+8, ... (lane = brick): coalesced 128-byte rows
-    for (int c = warp; c < ncta; c += 8) col[c * LD + lane] = lane < nb ? H[(long long)c * NB + b0 + lane] : 0;
+    // warp w loads rows c = w, w+8, ... (lane = brick): coalesced 128-byte rows,
+    // 8 loads in flight per warp before the shared stores
+    constexpr int U = 8;
+    for (int cb = warp; cb < ncta; cb += 8 * U) {
+        int v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c = cb + 8 * u;
+            v[u] = (c < ncta && lane < nb) ? H[(long long)c * NB + b0 + lane] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c = cb + 8 * u;
+            if (c < ncta) col[c * LD + lane] = v[u];
+        }
+    }
     __syncthreads();
     const int per = (ncta + 31) / 32;
     for (int j = warp; j < kColBricks; j += 8) {
