@@ -346,15 +346,22 @@ def main():
         ms_step = ms_total / args.steps
 
         # ---- e2e: host (pinned) samples in, LossTerms out, every step -------------
+        # Single GPU: the pipelined C-ABI host path (TGCU_HOST|TGCU_ASYNC): each
+        # step's H2D copy runs on the library's copy stream under the previous
+        # step's kernels and each step's LossTerms are copied back to pinned
+        # host memory. Slabs (N > 1): host samples, synchronous steps.
         pinned = [torch.from_numpy(b).pin_memory() for b in host_batches]
         ne = max(3, min(args.e2e_steps, args.steps))
+        e2e_async = ws == 1
         for i in range(3):
-            step(pinned[i % NBATCH].numpy(), asynchronous=False)
+            step(pinned[i % NBATCH].numpy(), asynchronous=e2e_async)
+        g.sync()
         torch.cuda.synchronize()
         barrier(ws)
         t0 = time.perf_counter()
         for i in range(ne):
-            step(pinned[i % NBATCH].numpy(), asynchronous=False)  # H2D inside, D2H of LossTerms
+            step(pinned[i % NBATCH].numpy(), asynchronous=e2e_async)  # H2D inside, D2H of LossTerms
+        e2e_last = g.sync()
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - t0, ws)
         barrier(ws)
@@ -385,7 +392,10 @@ def main():
                      "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_step,
                      "step_frac_survey_bytes": survey_bytes / (ms_step * 1e-3) / 1e9 / hbm_peak},
         "e2e": {"value": NPTS * ne / e2e_s, "unit": "points/s", "h2d_bytes_per_step": NPTS * 16 * ws,
-                "d2h_bytes_per_step": 32, "api": "tgcu_train_step(TGCU_HOST) + LossTerms readback per step"},
+                "d2h_bytes_per_step": 32,
+                "api": ("tgcu_train_step(TGCU_HOST|TGCU_ASYNC): pipelined H2D on a copy stream, per-step LossTerms "
+                        "D2H to pinned memory" if ws == 1 else "SlabTrainer.step with host samples, synchronous"),
+                "loss_last": e2e_last.total},
         "gpu_launches": int(launches),
         "clocks": clk,
         "loss_last": last.total,

@@ -185,7 +185,11 @@ int tgcu_adam_download_f64(tgcu_grid* g, double* m, double* v, int64_t n);
  * fused brick kernel → finalize). The gradient never touches HBM. On a
  * non-finite loss or gradient the step is not committed (params, moments and
  * t stay as before) and TGCU_ERR_NUMERICAL is returned (sticky under
- * TGCU_ASYNC; "stage 0 step k" / "index i" in the message). out may be NULL. */
+ * TGCU_ASYNC; "stage 0 step k" / "index i" in the message). out may be NULL.
+ * TGCU_HOST | TGCU_ASYNC with out == NULL pipelines host input: the samples are
+ * copied on an internal copy stream into one of two device slots while the
+ * previous step computes, and the step's LossTerms are copied back to pinned
+ * host memory; the host array must stay valid until tgcu_sync(). */
 int tgcu_train_step(tgcu_grid* g, const float* samples, int64_t n, const tgcu_loss_config* cfg,
                     tgcu_loss_terms* out, int flags, void* stream);
 /* ---- multi-GPU z-slab training (owner computes) ----

@@ -46,6 +46,25 @@ void ensure_staging(Grid& g, int64_t floats) {
     g.staging_cap = floats;
 }
 
+void ensure_pipeline(Grid& g, int64_t floats) {
+    if (!g.cstream) {
+        TGCU_CUDA(cudaStreamCreateWithFlags(&g.cstream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            TGCU_CUDA(cudaEventCreateWithFlags(&g.ev_ready[i], cudaEventDisableTiming));
+            TGCU_CUDA(cudaEventCreateWithFlags(&g.ev_free[i], cudaEventDisableTiming));
+        }
+        TGCU_CUDA(cudaMallocHost(&g.h_ring, sizeof(tgcu_loss_terms) * kTraceCap));
+    }
+    if (g.pstage_cap >= floats) return;
+    TGCU_CUDA(cudaDeviceSynchronize());  // slots may be in flight
+    for (int i = 0; i < 2; ++i) {
+        if (g.pstage[i]) TGCU_CUDA(cudaFree(g.pstage[i]));
+        g.pstage[i] = nullptr;
+        TGCU_CUDA(cudaMalloc(&g.pstage[i], sizeof(float) * floats));
+    }
+    g.pstage_cap = floats;
+}
+
 void ensure_scratch(Grid& g, int64_t doubles) {
     if (g.scratch_cap >= doubles) return;
     if (g.scratch_d) TGCU_CUDA(cudaFree(g.scratch_d));
@@ -354,6 +373,13 @@ int tgcu_grid_destroy(tgcu_grid* h) {
     cudaFreeHost(g.h_terms);
     cudaFree(g.staging);
     cudaFree(g.scratch_d);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(g.pstage[i]);
+        if (g.ev_ready[i]) cudaEventDestroy(g.ev_ready[i]);
+        if (g.ev_free[i]) cudaEventDestroy(g.ev_free[i]);
+    }
+    if (g.cstream) cudaStreamDestroy(g.cstream);
+    cudaFreeHost(g.h_ring);
     for (auto e : g.prof_ev) cudaEventDestroy(e);
     delete h;
     return TGCU_OK;
@@ -724,7 +750,21 @@ int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
         require(n <= (int64_t)INT_MAX / (1 << g.spec.dim), "train_step: batch too large");
         cudaStream_t s = as_stream(stream);
         const float4* ds = reinterpret_cast<const float4*>(samples);
-        if (flags & TGCU_HOST) {
+        // Pipelined host input: the copy of this step's samples runs on the
+        // copy stream into the free slot while earlier steps compute.
+        const bool pipe = (flags & TGCU_HOST) && (flags & TGCU_ASYNC) && out == nullptr;
+        int slot = 0;
+        if (pipe) {
+            ensure_pipeline(g, 4 * n);
+            slot = g.pipe_slot;
+            g.pipe_slot ^= 1;
+            TGCU_CUDA(cudaStreamWaitEvent(g.cstream, g.ev_free[slot], 0));
+            TGCU_CUDA(cudaMemcpyAsync(g.pstage[slot], samples, sizeof(float) * 4 * n, cudaMemcpyHostToDevice,
+                                      g.cstream));
+            TGCU_CUDA(cudaEventRecord(g.ev_ready[slot], g.cstream));
+            TGCU_CUDA(cudaStreamWaitEvent(s, g.ev_ready[slot], 0));
+            ds = reinterpret_cast<const float4*>(g.pstage[slot]);
+        } else if (flags & TGCU_HOST) {
             ensure_staging(g, 4 * n);
             TGCU_CUDA(cudaMemcpyAsync(g.staging, samples, sizeof(float) * 4 * n, cudaMemcpyHostToDevice, s));
             ds = reinterpret_cast<const float4*>(g.staging);
@@ -745,6 +785,11 @@ int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
         g.cur = 1 - in_idx;
         g.t = t_after;
         g.steps_launched += 1;
+        if (pipe) {
+            TGCU_CUDA(cudaEventRecord(g.ev_free[slot], s));  // slot consumed (binning read it)
+            const int64_t r = (g.steps_launched - 1) % kTraceCap;  // this step's LossTerms -> pinned ring
+            TGCU_CUDA(cudaMemcpyAsync(g.h_ring + r, g.d_trace + r, sizeof(tgcu_loss_terms), cudaMemcpyDeviceToHost, s));
+        }
         const bool sync = !(flags & TGCU_ASYNC) || out != nullptr;
         if (out) {
             TGCU_CUDA(cudaMemcpyAsync(g.h_terms, g.d_trace + ((g.steps_launched - 1) % kTraceCap),

@@ -120,6 +120,15 @@ struct Grid {
     tgcu_loss_terms* h_terms = nullptr;  // pinned, 1
     float* staging = nullptr;            // device staging for host inputs
     int64_t staging_cap = 0;             // floats
+    // Pipelined host inputs (TGCU_HOST | TGCU_ASYNC train steps): a copy
+    // stream filling two device slots, ordered against the compute stream by
+    // events, and a pinned ring receiving each step's LossTerms.
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    float* pstage[2] = {nullptr, nullptr};
+    int64_t pstage_cap = 0;              // floats per slot
+    int pipe_slot = 0;
+    tgcu_loss_terms* h_ring = nullptr;   // pinned, kTraceCap
     double* scratch_d = nullptr;         // reductions (unfused path)
     int64_t scratch_cap = 0;
     // TMA tensor maps of the fused step (train.cu ensure_tmaps): per ping-pong
@@ -139,6 +148,7 @@ void prof_mark(Grid& g, cudaStream_t s, int which);
 constexpr int kTraceCap = 4096;
 
 void ensure_staging(Grid& g, int64_t floats);
+void ensure_pipeline(Grid& g, int64_t floats);
 void ensure_bins(Grid& g, int64_t points);
 void ensure_bin_hist(Grid& g, int64_t ints, int64_t points, int64_t chain_ctas);
 void ensure_scratch(Grid& g, int64_t doubles);
