@@ -247,11 +247,15 @@ void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_
         sort_points_t<unsigned long long, unsigned long long>(g, pts, n, out, perm, offsets, end_bit, s);
 }
 
-// One CTA per Morton brick code (blockIdx.x). The brick's (B+1)^DIM vertex
-// tile arrives in smem by cp.async (8-byte granules, zero-filled outside the
-// grid); its points are [off[code], off[code+1]) of the brick-sorted array.
+// One CTA per brick of B^D cells (launch grid = bricks per axis); its points
+// are [off[code], off[code+1]) of the brick-sorted array, code = Morton(brick).
+// The brick's (B+1)^D vertex tile arrives by one TMA tensor box load
+// (out-of-grid vertices zero-filled), or by one bulk copy per row when the
+// grid layout cannot take a tensor map. Each thread loads and locates its first
+// point before waiting for the tile, so the two latencies overlap.
 template <int DIM, int ORDER, bool GRAD, int LB>
-__global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __restrict__ coeffs,
+__global__ void __launch_bounds__(256) k_eval_brick(const __grid_constant__ CUtensorMap tmap, int use_tmap,
+                                                    DevSpec s, const float* __restrict__ coeffs,
                                                     const float* __restrict__ pts, const long long* __restrict__ off,
                                                     float* __restrict__ vals, float* __restrict__ grads,
                                                     Status* st) {
@@ -259,29 +263,31 @@ __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __re
     constexpr int B = 1 << LB;
     constexpr int T = B + 1;  // tile edge in vertices
     constexpr int GR = (K % 2 == 0) ? 2 : 1;
-    // tile rows (fixed y, z) of T vertices, stride TROWF floats
+    // tile rows (fixed y, z) of T vertices, stride TROWF floats (16-byte multiple)
     constexpr int TROWF = ((T * K + 3) / 4) * 4;
     constexpr int ROWS = DIM == 3 ? T * T : T;
     constexpr unsigned RBYTES = ((T * K * 4 + 15) / 16) * 16;
     extern __shared__ __align__(128) float tile[];  // ROWS * TROWF
     __shared__ __align__(8) unsigned long long bar;
 
-    const unsigned int code = blockIdx.x;
+    const int ox = (int)blockIdx.x * B, oy = (int)blockIdx.y * B, oz = DIM == 3 ? (int)blockIdx.z * B : 0;
+    const unsigned int code = DIM == 3 ? (unsigned int)(spread3(blockIdx.x) | (spread3(blockIdx.y) << 1) |
+                                                        (spread3(blockIdx.z) << 2))
+                                       : (unsigned int)(spread2(blockIdx.x) | (spread2(blockIdx.y) << 1));
     const long long p0 = off[code], p1 = off[code + 1];
     if (p0 >= p1) return;
-    unsigned int b[3] = {0, 0, 0};
-#pragma unroll
-    for (int bit = 0; bit < 10; ++bit) {
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) b[a] |= ((code >> (bit * DIM + a)) & 1u) << bit;
-    }
-    const int ox = b[0] * B, oy = b[1] * B, oz = DIM == 3 ? b[2] * B : 0;
+    const bool tm = use_tmap != 0;
     if (threadIdx.x == 0) {
-        mbar_init(&bar, blockDim.x);
+        mbar_init(&bar, tm ? 1 : blockDim.x);
         mbar_fence_init();
+        if (tm) {
+            mbar_expect_tx(&bar, (unsigned)(ROWS * TROWF * 4));
+            if constexpr (DIM == 3) tma_load_3d(tile, &tmap, &bar, ox * K, oy, oz);
+            else tma_load_2d(tile, &tmap, &bar, ox * K, oy);
+        }
     }
-    __syncthreads();
-    {
+    if (!tm) {
+        __syncthreads();  // barrier initialised before the per-row arrivals
         // one TMA bulk copy per row (thread r), cp.async fallback when the row
         // is unaligned or runs past the array
         const long long nc_bytes = (long long)s.res[0] * s.res[1] * (DIM == 3 ? s.res[2] : 1) * K * 4;
@@ -309,13 +315,11 @@ __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __re
         }
         if (!arrived) mbar_arrive(&bar);
         cp_async_commit();
-        cp_async_wait<0>();
-        if (threadIdx.x < 32) mbar_wait(&bar, 0);
     }
-    __syncthreads();
 
     const int o3[3] = {ox, oy, oz};
-    for (long long i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
+    // locate of point i: cell-relative tile offset and per-axis factors (false for NaN)
+    auto prepare = [&](long long i, AxisF* ax, int& tbase) -> bool {
         double x[DIM];
         bool nan = false;
 #pragma unroll
@@ -328,9 +332,8 @@ __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __re
             vals[i] = __int_as_float(0x7fc00000);
             if (GRAD)
                 for (int a = 0; a < 3; ++a) grads[3 * i + a] = __int_as_float(0x7fc00000);
-            continue;
+            return false;
         }
-        AxisF ax[DIM];
         int lc[3] = {0, 0, 0};
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
@@ -339,7 +342,10 @@ __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __re
             ax[a] = axis_factors(s, a, local);
             lc[a] = c - o3[a];
         }
-        const int tbase = (DIM == 3 ? lc[2] * T + lc[1] : lc[1]) * TROWF + lc[0] * K;
+        tbase = (DIM == 3 ? lc[2] * T + lc[1] : lc[1]) * TROWF + lc[0] * K;
+        return true;
+    };
+    auto evaluate = [&](long long i, const AxisF* ax, int tbase) {
         float f = 0.0f;
         float fg[DIM];
 #pragma unroll
@@ -356,7 +362,37 @@ __global__ void __launch_bounds__(256) k_eval_brick(DevSpec s, const float* __re
 #pragma unroll
             for (int a = 0; a < 3; ++a) grads[3 * i + a] = a < DIM ? fg[a] : 0.0f;
         }
+    };
+
+    // first point: load + locate while the tile is in flight
+    long long i = p0 + threadIdx.x;
+    AxisF ax[DIM];
+    int tbase = 0;
+    bool ok = i < p1 && prepare(i, ax, tbase);
+    if (!tm) cp_async_wait<0>();
+    if (threadIdx.x < 32) mbar_wait(&bar, 0);
+    __syncthreads();
+    if (ok) evaluate(i, ax, tbase);
+    for (i += blockDim.x; i < p1; i += blockDim.x) {
+        if (prepare(i, ax, tbase)) evaluate(i, ax, tbase);
     }
+}
+
+// Query tile tensor maps (box (B+1) vertices padded to 16 bytes x (B+1) [x (B+1)]).
+static bool ensure_query_tmaps(Grid& g, unsigned box_x, unsigned T) {
+    if (g.tmq_state == 0) {
+        g.tmq_state = -1;
+        if (((int64_t)g.ds.res[0] * g.K * 4) % 16 == 0 && box_x <= 256 && !g.slab) {
+            bool ok = encode_grid_map(&g.tm_query[0], g, g.p[0], box_x, T);
+            if (g.p[1]) ok = ok && encode_grid_map(&g.tm_query[1], g, g.p[1], box_x, T);
+            if (ok) g.tmq_state = g.p[1] ? 2 : 1;  // maps built for 1 or 2 buffers
+        }
+    }
+    if (g.tmq_state == 1 && g.p[1]) {  // optimiser buffers appeared since
+        if (!encode_grid_map(&g.tm_query[1], g, g.p[1], box_x, T)) return false;
+        g.tmq_state = 2;
+    }
+    return g.tmq_state >= 1 && (g.cur == 0 || g.tmq_state == 2);
 }
 
 void launch_eval_sorted(Grid& g, const float* pts, int64_t n, const int64_t* offsets, float* vals, float* grads,
@@ -377,9 +413,14 @@ void launch_eval_sorted(Grid& g, const float* pts, int64_t n, const int64_t* off
         constexpr int T = B + 1;
         constexpr int TROWF = ((T * K + 3) / 4) * 4;
         const size_t smem = sizeof(float) * (DIM == 3 ? T * T : T) * TROWF;
+        const bool use_tm = ensure_query_tmaps(g, TROWF, T);
+        CUtensorMap map{};
+        if (use_tm) map = g.tm_query[g.cur];
+        dim3 grid(1, 1, 1);
+        for (int a = 0; a < DIM; ++a) (&grid.x)[a] = (unsigned)((g.spec.res[a] - 1 + B - 1) / B);
         auto kern = grads ? k_eval_brick<DIM, ORDER, true, LB> : k_eval_brick<DIM, ORDER, false, LB>;
         TGCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)codes, 256, smem, s>>>(g.ds, g.p[g.cur], pts, off, vals, grads, g.st);
+        kern<<<grid, 256, smem, s>>>(map, use_tm ? 1 : 0, g.ds, g.p[g.cur], pts, off, vals, grads, g.st);
     });
     count_launch();
     if (tmp) TGCU_CUDA(cudaFreeAsync(tmp, s));

@@ -136,6 +136,9 @@ struct Grid {
     // p, m and v. tm_state: 0 = not built, 1 = usable, -1 = layout not eligible.
     CUtensorMap tm_tile[2], tm_own_p[2], tm_own_m[2], tm_own_v[2];
     int tm_state = 0;
+    // Query tile boxes ((B+1)^D vertices) over p[0], p[1] (query.cu).
+    CUtensorMap tm_query[2];
+    int tmq_state = 0;
     // Live kernel timing (tgcu_profile_*): CUDA events recorded on the launch
     // stream around the fused brick kernel.
     bool prof_on = false;
@@ -147,6 +150,9 @@ void prof_mark(Grid& g, cudaStream_t s, int which);
 
 constexpr int kTraceCap = 4096;
 
+// TMA tensor map over a coefficient-layout buffer: rows of K*res_x floats x
+// res_y [x stored z planes], box box_x floats x box_yz [x box_yz] (train.cu).
+bool encode_grid_map(CUtensorMap* m, const Grid& g, const float* base, unsigned box_x, unsigned box_yz);
 void ensure_staging(Grid& g, int64_t floats);
 void ensure_pipeline(Grid& g, int64_t floats);
 void ensure_bins(Grid& g, int64_t points);

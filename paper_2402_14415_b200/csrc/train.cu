@@ -1022,7 +1022,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // A (rows = K * res_x floats) x res_y [x zstore] view of one coefficient-layout
 // buffer with a box of box_x floats x box_yz rows [x box_yz planes].
-static bool encode_grid_map(CUtensorMap* m, const Grid& g, const float* base, unsigned box_x, unsigned box_yz) {
+bool encode_grid_map(CUtensorMap* m, const Grid& g, const float* base, unsigned box_x, unsigned box_yz) {
     const int dim = g.spec.dim;
     const cuuint64_t row = (cuuint64_t)g.ds.res[0] * g.K;
     cuuint64_t gdim[3] = {row, (cuuint64_t)g.ds.res[1], (cuuint64_t)g.ds.zstore};
