@@ -247,6 +247,16 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
             throw Error(TGCU_ERR_CUDA, "tgcu: no CUDA device available (the product path has no CPU fallback)");
         require(device >= 0 && device < ndev, "tgcu_grid_create: bad device " + std::to_string(device));
+        // Stream-ordered scratch (query binning, sorts, resample tables) comes
+        // from the device's default memory pool; keep freed blocks cached there
+        // instead of returning them to the OS at every synchronisation.
+        {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+                uint64_t keep = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+        }
         h = new tgcu_grid();
         Grid& g = h->g;
         g.spec = s;
@@ -527,6 +537,8 @@ int tgcu_eval(tgcu_grid* h, const float* pts, int64_t n, float* values, float* s
         }
         if (flags & TGCU_SORTED)
             launch_eval_sorted(g, dp, n, nullptr, dv, dg, s);
+        else if (n >= kBinnedQueryMin && !g.slab)
+            launch_eval_binned(g, dp, n, dv, dg, s);  // large unsorted batches: bin by brick, smem tiles
         else
             launch_eval_direct(g, dp, n, dv, dg, s);
         if (flags & TGCU_HOST) {

@@ -147,6 +147,15 @@ __global__ void k_gather_points(const float* __restrict__ pts, const IdxT* __res
 template <int DIM>
 constexpr int brick_log2() { return DIM == 3 ? 3 : 4; }
 
+// Row stride (floats) of the query tile: T*K rounded to 16 bytes, padded for
+// the 3D K = 10 / K = 4 tiles so that the y-row and z-plane strides spread a
+// warp's Morton-neighbouring cells over the shared-memory banks (simulated
+// LDS.64 wavefronts: 1.87x -> 1.72x of ideal for K = 10, 3.3x -> 2.6x for K = 4).
+template <int DIM, int K, int T>
+constexpr int query_trowf() {
+    return (DIM == 3 && K == 10) ? 104 : (DIM == 3 && K == 4) ? 48 : ((T * K + 3) / 4) * 4;
+}
+
 // Number of Morton brick codes of the query decomposition (pow2^DIM).
 int64_t query_brick_codes(const Grid& g) {
     const int LB = g.spec.dim == 3 ? 3 : 4;
@@ -253,7 +262,7 @@ void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_
 // (out-of-grid vertices zero-filled), or by one bulk copy per row when the
 // grid layout cannot take a tensor map. Each thread loads and locates its first
 // point before waiting for the tile, so the two latencies overlap.
-template <int DIM, int ORDER, bool GRAD, int LB>
+template <int DIM, int ORDER, bool GRAD, int LB, bool BINNED = false>
 __global__ void __launch_bounds__(256) k_eval_brick(const __grid_constant__ CUtensorMap tmap, int use_tmap,
                                                     DevSpec s, const float* __restrict__ coeffs,
                                                     const float* __restrict__ pts, const long long* __restrict__ off,
@@ -264,7 +273,7 @@ __global__ void __launch_bounds__(256) k_eval_brick(const __grid_constant__ CUte
     constexpr int T = B + 1;  // tile edge in vertices
     constexpr int GR = (K % 2 == 0) ? 2 : 1;
     // tile rows (fixed y, z) of T vertices, stride TROWF floats (16-byte multiple)
-    constexpr int TROWF = ((T * K + 3) / 4) * 4;
+    constexpr int TROWF = query_trowf<DIM, K, T>();
     constexpr int ROWS = DIM == 3 ? T * T : T;
     constexpr unsigned RBYTES = ((T * K * 4 + 15) / 16) * 16;
     extern __shared__ __align__(128) float tile[];  // ROWS * TROWF
@@ -318,14 +327,24 @@ __global__ void __launch_bounds__(256) k_eval_brick(const __grid_constant__ CUte
     }
 
     const int o3[3] = {ox, oy, oz};
-    // locate of point i: cell-relative tile offset and per-axis factors (false for NaN)
-    auto prepare = [&](long long i, AxisF* ax, int& tbase) -> bool {
+    // locate of point i: cell-relative tile offset and per-axis factors (false
+    // for NaN); oi = the output slot (i, or the caller's index of a binned point)
+    auto prepare = [&](long long i, AxisF* ax, int& tbase, long long& oi) -> bool {
         double x[DIM];
         bool nan = false;
+        if constexpr (BINNED) {
+            const float4 q = reinterpret_cast<const float4*>(pts)[i];
+            const float qq[3] = {q.x, q.y, q.z};
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) {
-            x[a] = (double)pts[3 * i + a];
-            nan |= isnan(x[a]);
+            for (int a = 0; a < DIM; ++a) x[a] = (double)qq[a];
+            oi = (long long)(unsigned int)__float_as_int(q.w);
+        } else {
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                x[a] = (double)pts[3 * i + a];
+                nan |= isnan(x[a]);
+            }
+            oi = i;
         }
         if (nan) {
             atomicMin(&st->nan_point, (unsigned long long)i);
@@ -345,7 +364,7 @@ __global__ void __launch_bounds__(256) k_eval_brick(const __grid_constant__ CUte
         tbase = (DIM == 3 ? lc[2] * T + lc[1] : lc[1]) * TROWF + lc[0] * K;
         return true;
     };
-    auto evaluate = [&](long long i, const AxisF* ax, int tbase) {
+    auto evaluate = [&](long long i, const AxisF* ax, int tbase) {  // i = output slot
         float f = 0.0f;
         float fg[DIM];
 #pragma unroll
@@ -365,16 +384,67 @@ __global__ void __launch_bounds__(256) k_eval_brick(const __grid_constant__ CUte
     };
 
     // first point: load + locate while the tile is in flight
-    long long i = p0 + threadIdx.x;
+    long long i = p0 + threadIdx.x, oi = 0;
     AxisF ax[DIM];
     int tbase = 0;
-    bool ok = i < p1 && prepare(i, ax, tbase);
+    bool ok = i < p1 && prepare(i, ax, tbase, oi);
     if (!tm) cp_async_wait<0>();
     if (threadIdx.x < 32) mbar_wait(&bar, 0);
     __syncthreads();
-    if (ok) evaluate(i, ax, tbase);
+    if (ok) evaluate(oi, ax, tbase);
     for (i += blockDim.x; i < p1; i += blockDim.x) {
-        if (prepare(i, ax, tbase)) evaluate(i, ax, tbase);
+        if (prepare(i, ax, tbase, oi)) evaluate(oi, ax, tbase);
+    }
+}
+
+// ---- binned query of unsorted points ------------------------------------------------
+// A counting sort by query brick replaces the full radix sort: per point its
+// Morton brick code (NaN points are answered here and not binned), global
+// atomic counts, an exclusive scan, and an atomic-cursor scatter of
+// (x, y, z, caller index) records; the brick kernel then writes each value to
+// the caller's slot.
+template <int DIM, int LB>
+__global__ void __launch_bounds__(256) k_qbin_count(DevSpec s, const float* __restrict__ pts, long long n,
+                                                    int* __restrict__ cnt, float* __restrict__ vals,
+                                                    float* __restrict__ grads, Status* st) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        bool nan = false;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) nan |= isnan(pts[3 * i + a]);
+        if (nan) {
+            atomicMin(&st->nan_point, (unsigned long long)i);
+            vals[i] = __int_as_float(0x7fc00000);
+            if (grads)
+                for (int a = 0; a < 3; ++a) grads[3 * i + a] = __int_as_float(0x7fc00000);
+            continue;
+        }
+        unsigned int kb;
+        point_key<DIM, LB>(s, pts + 3 * i, &kb);
+        atomicAdd(&cnt[kb], 1);
+    }
+}
+
+template <int DIM, int LB>
+__global__ void __launch_bounds__(256) k_qbin_scatter(DevSpec s, const float* __restrict__ pts, long long n,
+                                                      int* __restrict__ cursor, float4* __restrict__ binned) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
+        if (isnan(x) || isnan(y) || (DIM == 3 && isnan(z))) continue;
+        unsigned int kb;
+        point_key<DIM, LB>(s, pts + 3 * i, &kb);
+        const int slot = atomicAdd(&cursor[kb], 1);
+        binned[slot] = make_float4(x, y, z, __int_as_float((int)i));
+    }
+}
+
+__global__ void k_i32_to_i64_copy(const int* __restrict__ a, long long* __restrict__ b, int* __restrict__ c,
+                                  long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        b[i] = a[i];
+        if (i < n - 1) c[i] = a[i];
     }
 }
 
@@ -395,6 +465,62 @@ static bool ensure_query_tmaps(Grid& g, unsigned box_x, unsigned T) {
     return g.tmq_state >= 1 && (g.cur == 0 || g.tmq_state == 2);
 }
 
+template <bool BINNED>
+static void launch_brick_query(Grid& g, const float* pts, const long long* off, float* vals, float* grads,
+                               cudaStream_t s) {
+    TGCU_DISPATCH(g.spec.dim, g.spec.order, {
+        constexpr int LB = brick_log2<DIM>();
+        constexpr int B = 1 << LB;
+        constexpr int K = KOf<DIM, ORDER>::value;
+        constexpr int T = B + 1;
+        constexpr int TROWF = query_trowf<DIM, K, T>();
+        const size_t smem = sizeof(float) * (DIM == 3 ? T * T : T) * TROWF;
+        const bool use_tm = ensure_query_tmaps(g, TROWF, T);
+        CUtensorMap map{};
+        if (use_tm) map = g.tm_query[g.cur];
+        dim3 grid(1, 1, 1);
+        for (int a = 0; a < DIM; ++a) (&grid.x)[a] = (unsigned)((g.spec.res[a] - 1 + B - 1) / B);
+        auto kern = grads ? k_eval_brick<DIM, ORDER, true, LB, BINNED> : k_eval_brick<DIM, ORDER, false, LB, BINNED>;
+        TGCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, 256, smem, s>>>(map, use_tm ? 1 : 0, g.ds, g.p[g.cur], pts, off, vals, grads, g.st);
+    });
+    count_launch();
+}
+
+void launch_eval_binned(Grid& g, const float* pts, int64_t n, float* vals, float* grads, cudaStream_t s) {
+    if (n <= 0) return;
+    require(n < (1LL << 31), "eval: more than 2^31 points per call");
+    const int64_t codes = query_brick_codes(g);
+    int *cnt = nullptr, *cursor = nullptr;
+    long long* off = nullptr;
+    float4* binned = nullptr;
+    void* temp = nullptr;
+    size_t temp_bytes = 0;
+    TGCU_CUDA(cudaMallocAsync(&cnt, sizeof(int) * (codes + 1), s));
+    TGCU_CUDA(cudaMallocAsync(&cursor, sizeof(int) * (codes + 1), s));
+    TGCU_CUDA(cudaMallocAsync(&off, sizeof(long long) * (codes + 1), s));
+    TGCU_CUDA(cudaMallocAsync(&binned, sizeof(float4) * n, s));
+    TGCU_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * (codes + 1), s));
+    const int blocks = grid_blocks(n, 256, 148 * 32);
+    if (g.spec.dim == 3) k_qbin_count<3, 3><<<blocks, 256, 0, s>>>(g.ds, pts, n, cnt, vals, grads, g.st);
+    else k_qbin_count<2, 4><<<blocks, 256, 0, s>>>(g.ds, pts, n, cnt, vals, grads, g.st);
+    // cursor = off (int) = exclusive scan of cnt over codes + 1 entries
+    TGCU_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, cnt, cursor, (int64_t)(codes + 1), s));
+    TGCU_CUDA(cudaMallocAsync(&temp, temp_bytes, s));
+    TGCU_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, cnt, cursor, (int64_t)(codes + 1), s));
+    k_i32_to_i64_copy<<<grid_blocks(codes + 1, 256), 256, 0, s>>>(cursor, off, cnt, codes + 1);  // cnt := cursor copy
+    if (g.spec.dim == 3) k_qbin_scatter<3, 3><<<blocks, 256, 0, s>>>(g.ds, pts, n, cnt, binned);
+    else k_qbin_scatter<2, 4><<<blocks, 256, 0, s>>>(g.ds, pts, n, cnt, binned);
+    count_launch(3);
+    launch_brick_query<true>(g, reinterpret_cast<const float*>(binned), off, vals, grads, s);
+    TGCU_CUDA(cudaFreeAsync(temp, s));
+    TGCU_CUDA(cudaFreeAsync(cnt, s));
+    TGCU_CUDA(cudaFreeAsync(cursor, s));
+    TGCU_CUDA(cudaFreeAsync(off, s));
+    TGCU_CUDA(cudaFreeAsync(binned, s));
+    TGCU_CUDA(cudaGetLastError());
+}
+
 void launch_eval_sorted(Grid& g, const float* pts, int64_t n, const int64_t* offsets, float* vals, float* grads,
                         cudaStream_t s) {
     if (n <= 0) return;
@@ -406,23 +532,7 @@ void launch_eval_sorted(Grid& g, const float* pts, int64_t n, const int64_t* off
         offsets = reinterpret_cast<const int64_t*>(tmp);
     }
     const long long* off = reinterpret_cast<const long long*>(offsets);
-    TGCU_DISPATCH(g.spec.dim, g.spec.order, {
-        constexpr int LB = brick_log2<DIM>();
-        constexpr int B = 1 << LB;
-        constexpr int K = KOf<DIM, ORDER>::value;
-        constexpr int T = B + 1;
-        constexpr int TROWF = ((T * K + 3) / 4) * 4;
-        const size_t smem = sizeof(float) * (DIM == 3 ? T * T : T) * TROWF;
-        const bool use_tm = ensure_query_tmaps(g, TROWF, T);
-        CUtensorMap map{};
-        if (use_tm) map = g.tm_query[g.cur];
-        dim3 grid(1, 1, 1);
-        for (int a = 0; a < DIM; ++a) (&grid.x)[a] = (unsigned)((g.spec.res[a] - 1 + B - 1) / B);
-        auto kern = grads ? k_eval_brick<DIM, ORDER, true, LB> : k_eval_brick<DIM, ORDER, false, LB>;
-        TGCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<grid, 256, smem, s>>>(map, use_tm ? 1 : 0, g.ds, g.p[g.cur], pts, off, vals, grads, g.st);
-    });
-    count_launch();
+    launch_brick_query<false>(g, pts, off, vals, grads, s);
     if (tmp) TGCU_CUDA(cudaFreeAsync(tmp, s));
     TGCU_CUDA(cudaGetLastError());
 }

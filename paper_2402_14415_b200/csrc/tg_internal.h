@@ -163,6 +163,10 @@ void ensure_optimizer(Grid& g);
 
 // Launchers (query.cu / train.cu). All stream-ordered; no synchronisation.
 void launch_eval_direct(Grid& g, const float* pts, int64_t n, float* vals, float* grads, cudaStream_t s);
+// Unsorted batches of at least kBinnedQueryMin points: counting sort by query
+// brick + the smem-tile brick kernel writing values to the caller's slots.
+constexpr int64_t kBinnedQueryMin = 1 << 18;
+void launch_eval_binned(Grid& g, const float* pts, int64_t n, float* vals, float* grads, cudaStream_t s);
 void launch_eval_sorted(Grid& g, const float* pts, int64_t n, const int64_t* offsets, float* vals, float* grads,
                         cudaStream_t s);
 void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, int64_t* offsets,
