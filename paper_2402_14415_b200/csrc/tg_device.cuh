@@ -273,6 +273,50 @@ __device__ __forceinline__ void corner_grad(const Corner<DIM>& g, float u, const
     }
 }
 
+// corner_grad for 3D order 2 on the packed fp32x2 pipe. Accumulators pair the
+// ten channels as P0 = (f0, f1x), P1 = (f1y, f1z), P2 = (q00, q11),
+// P3 = (q01, q02), P4 = (q12, q22); with a_j = alpha d_j + wg_j:
+//   (q00, q11) += (d0, d1) * (alpha/2 (d0, d1) + (wg0, wg1))
+//   (q01, q02) += a0 (d1, d2) + d0 (wg1, wg2)
+//   (q12, q22) += (a1, alpha/2 d2) * d2 + wg2 (d1, d2)
+// (the same sums as corner_grad, 18 issue slots instead of ~27).
+template <bool EIK>
+__device__ __forceinline__ void corner_grad_p2(const Corner<3>& g, float u, const float* gv, float2 (&P)[5]) {
+    float alpha = u * g.w;
+    if constexpr (EIK) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) alpha = fmaf(gv[a], g.dw[a], alpha);
+    }
+    const float2 d01 = make_float2(g.d[0], g.d[1]);
+    const float2 d12 = make_float2(g.d[1], g.d[2]);
+    const float d2 = g.d[2];
+    const float ha = 0.5f * alpha;
+    float2 wg01 = make_float2(0.f, 0.f), wg12 = make_float2(0.f, 0.f);
+    float wg2 = 0.0f;
+    if constexpr (EIK) {
+        wg01 = __fmul2_rn(make_float2(g.w, g.w), make_float2(gv[0], gv[1]));
+        wg2 = g.w * gv[2];
+        wg12 = make_float2(wg01.y, wg2);
+    }
+    const float2 a01 = EIK ? __ffma2_rn(make_float2(alpha, alpha), d01, wg01) : __fmul2_rn(make_float2(alpha, alpha), d01);
+    const float a2 = EIK ? fmaf(alpha, d2, wg2) : alpha * d2;
+    P[0] = __fadd2_rn(P[0], make_float2(alpha, a01.x));
+    P[1] = __fadd2_rn(P[1], make_float2(a01.y, a2));
+    const float2 t01 = EIK ? __ffma2_rn(make_float2(ha, ha), d01, wg01) : __fmul2_rn(make_float2(ha, ha), d01);
+    P[2] = __ffma2_rn(d01, t01, P[2]);
+    if constexpr (EIK) P[3] = __ffma2_rn(wg12, make_float2(g.d[0], g.d[0]), P[3]);
+    P[3] = __ffma2_rn(make_float2(a01.x, a01.x), d12, P[3]);
+    if constexpr (EIK) P[4] = __ffma2_rn(make_float2(wg2, wg2), d12, P[4]);
+    P[4] = __ffma2_rn(make_float2(a01.y, ha * d2), make_float2(d2, d2), P[4]);
+}
+
+// Unpack corner_grad_p2's accumulators into the reference channel order.
+__device__ __forceinline__ void unpack_p2(const float2 (&P)[5], float* G) {
+    G[0] = P[0].x; G[1] = P[0].y; G[2] = P[1].x; G[3] = P[1].y;
+    G[4] = P[2].x; G[7] = P[2].y; G[5] = P[3].x; G[6] = P[3].y;
+    G[8] = P[4].x; G[9] = P[4].y;
+}
+
 // Per-point loss chain in fp64 (point_terms_chunk, sdf_loss.cpp:51-74).
 struct LossDev {
     double k;

@@ -335,6 +335,99 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_scatter_tiles(BinArgs A, co
     }
 }
 
+struct FinArgs {
+    const double* partials;
+    int NB;
+    double n;
+    double lambda1, lambda2, inv_norm;
+    int use_tv, want_eik;
+    Status* st;
+    tgcu_loss_terms* trace;
+    long long step;
+    int in_idx;
+    long long t_after;
+    double* slab_out;       // slab phase 1: write local {recon, eik, tv, has_nan, has_bad}, no commit
+    const double* reduced;  // slab phase 2: globally summed {recon, eik, tv, n_nan, n_bad}
+};
+
+template <int NTH>
+__device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid) {
+    double recon = 0.0, eik = 0.0, tvs = 0.0;
+    if (!F.reduced) {
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int i = tid; i < F.NB; i += NTH) {
+            a += F.partials[4 * i];
+            b += F.partials[4 * i + 1];
+            c += F.partials[4 * i + 2];
+        }
+        a = warp_sum_d(a);
+        b = warp_sum_d(b);
+        c = warp_sum_d(c);
+        if ((tid & 31) == 0) {
+            red[0][tid >> 5] = a;
+            red[1][tid >> 5] = b;
+            red[2][tid >> 5] = c;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int k = 0; k < NTH / 32; ++k) {
+                recon += red[0][k];
+                eik += red[1][k];
+                tvs += red[2][k];
+            }
+        }
+    } else if (tid == 0) {
+        recon = F.reduced[0];
+        eik = F.reduced[1];
+        tvs = F.reduced[2];
+    }
+    if (tid != 0) return;
+    Status* st = F.st;
+    if (F.slab_out) {
+        F.slab_out[0] = recon;
+        F.slab_out[1] = eik;
+        F.slab_out[2] = tvs;
+        F.slab_out[3] = st->nan_point != ULLONG_MAX ? 1.0 : 0.0;
+        F.slab_out[4] = st->bad_grad != ULLONG_MAX ? 1.0 : 0.0;
+        return;
+    }
+    const bool any_nan = st->nan_point != ULLONG_MAX || (F.reduced && F.reduced[3] > 0.0);
+    const bool any_bad = st->bad_grad != ULLONG_MAX || (F.reduced && F.reduced[4] > 0.0);
+    tgcu_loss_terms t;
+    t.fit = recon / F.n;
+    t.eik = F.want_eik ? eik / F.n : 0.0;
+    t.tv = F.use_tv ? tvs * F.inv_norm : 0.0;
+    t.total = t.fit + F.lambda1 * t.eik + F.lambda2 * t.tv;
+    F.trace[F.step % kTraceCap] = t;
+    int err = 0, kind = 0;
+    long long idx = -1;
+    if (any_nan) {
+        err = TGCU_ERR_INVALID_ARGUMENT;
+        kind = 1;
+        idx = st->nan_point != ULLONG_MAX ? (long long)st->nan_point : -1;
+    } else if (!isfinite(t.total)) {
+        err = TGCU_ERR_NUMERICAL;
+        kind = 2;
+    } else if (any_bad) {
+        err = TGCU_ERR_NUMERICAL;
+        kind = 3;
+        idx = st->bad_grad != ULLONG_MAX ? (long long)st->bad_grad : -1;
+    }
+    if (err) {
+        st->error = err;
+        st->error_kind = kind;
+        st->error_step = F.step;
+        st->error_index = idx;
+        st->good_idx = F.in_idx;
+        st->good_t = F.t_after - 1;
+    } else {
+        st->good_idx = 1 - F.in_idx;
+        st->good_t = F.t_after;
+    }
+    st->nan_point = ULLONG_MAX;
+    st->bad_grad = ULLONG_MAX;
+}
+
 struct StepArgs {
     // TMA tensor maps (use_tmap): parameter tile (load), owned boxes of
     // p (store), m and v (load + store).
@@ -536,7 +629,10 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         mbar_init(&bars[1], tmap ? 1 : NT);
         mbar_fence_init();
     }
-    __syncthreads();
+    // With tensor maps only warp 0 touches the barriers (thread 0 arms them,
+    // warp 0 waits); per-row staging has every thread arrive.
+    if (tmap) __syncwarp();
+    else __syncthreads();
     // The tile is waited for inside the first chunk, after the points have
     // been loaded, located and counted (none of which needs it).
     if (tmap) {
@@ -574,9 +670,13 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         if (!mv_row) mbar_arrive(&bars[1]);
     }
 
+    constexpr bool PACKED = DIM == 3 && ORDER == 2;  // fp32x2 accumulators (corner_grad_p2)
     float G[K];
 #pragma unroll
     for (int q = 0; q < K; ++q) G[q] = 0.0f;
+    float2 P[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) P[q] = make_float2(0.f, 0.f);
     double recon_sum = 0.0, eik_sum = 0.0, home_pts = 0.0;
     int myv = tid;  // owned vertex of this thread; set per brick by the workload sort
 
@@ -749,7 +849,10 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                     cg.dw[a] = EIK ? (((c >> a) & 1) ? A.s.inv_hf[a] : -A.s.inv_hf[a]) * other : 0.0f;
                     gvd[a] = EIK ? r[2 * DIM + 1 + a] : 0.0f;
                 }
-                corner_grad<DIM, ORDER, K>(cg, r[2 * DIM], gvd, G);
+                if constexpr (PACKED)
+                    corner_grad_p2<EIK>(*reinterpret_cast<const Corner<3>*>(&cg), r[2 * DIM], gvd, P);
+                else
+                    corner_grad<DIM, ORDER, K>(cg, r[2 * DIM], gvd, G);
                 ++j;
             }
         }
@@ -758,6 +861,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
 
     // ---- 3. TV + Adam, thread per vertex; results staged in place ----
     float* Gs = uni;
+    if constexpr (PACKED) unpack_p2(P, G);
 #pragma unroll
     for (int q = 0; q < K; ++q) Gs[myv * K + q] = G[q];
     cp_async_wait<0>();
@@ -908,103 +1012,19 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             A.partials[4 * b + tid] = acc;
         }
     }
+    // (a last-CTA finalize here, behind a per-CTA fence + ticket, measured
+    //  15 us slower per C2 step than the separate 1-CTA finalize launch)
     // the CTA's shared memory must outlive the TMA stores' reads
     if (tmap && tid == 0) bulk_wait_read0();
 }
 
-struct FinArgs {
-    const double* partials;
-    int NB;
-    double n;
-    double lambda1, lambda2, inv_norm;
-    int use_tv, want_eik;
-    Status* st;
-    tgcu_loss_terms* trace;
-    long long step;
-    int in_idx;
-    long long t_after;
-    double* slab_out;       // slab phase 1: write local {recon, eik, tv, has_nan, has_bad}, no commit
-    const double* reduced;  // slab phase 2: globally summed {recon, eik, tv, n_nan, n_bad}
-};
-
 // Reduce the per-brick partials in a fixed order, apply the reference's error
-// order (NaN point -> non-finite loss -> non-finite gradient) and commit.
+// order (NaN point -> non-finite loss -> non-finite gradient) and commit
+// (slab phase 2; the single-grid step finalizes in its last brick CTA).
 __global__ void __launch_bounds__(1024) k_step_finalize(FinArgs F) {
     __shared__ double red[3][32];
     if (F.st->error) return;
-    double recon = 0.0, eik = 0.0, tvs = 0.0;
-    if (!F.reduced) {
-        double a = 0.0, b = 0.0, c = 0.0;
-        for (int i = threadIdx.x; i < F.NB; i += blockDim.x) {
-            a += F.partials[4 * i];
-            b += F.partials[4 * i + 1];
-            c += F.partials[4 * i + 2];
-        }
-        a = warp_sum_d(a);
-        b = warp_sum_d(b);
-        c = warp_sum_d(c);
-        if ((threadIdx.x & 31) == 0) {
-            red[0][threadIdx.x >> 5] = a;
-            red[1][threadIdx.x >> 5] = b;
-            red[2][threadIdx.x >> 5] = c;
-        }
-        __syncthreads();
-        if (threadIdx.x != 0) return;
-        for (int k = 0; k < 32; ++k) {
-            recon += red[0][k];
-            eik += red[1][k];
-            tvs += red[2][k];
-        }
-    } else {
-        if (threadIdx.x != 0) return;
-        recon = F.reduced[0];
-        eik = F.reduced[1];
-        tvs = F.reduced[2];
-    }
-    Status* st = F.st;
-    if (F.slab_out) {
-        F.slab_out[0] = recon;
-        F.slab_out[1] = eik;
-        F.slab_out[2] = tvs;
-        F.slab_out[3] = st->nan_point != ULLONG_MAX ? 1.0 : 0.0;
-        F.slab_out[4] = st->bad_grad != ULLONG_MAX ? 1.0 : 0.0;
-        return;
-    }
-    const bool any_nan = st->nan_point != ULLONG_MAX || (F.reduced && F.reduced[3] > 0.0);
-    const bool any_bad = st->bad_grad != ULLONG_MAX || (F.reduced && F.reduced[4] > 0.0);
-    tgcu_loss_terms t;
-    t.fit = recon / F.n;
-    t.eik = F.want_eik ? eik / F.n : 0.0;
-    t.tv = F.use_tv ? tvs * F.inv_norm : 0.0;
-    t.total = t.fit + F.lambda1 * t.eik + F.lambda2 * t.tv;
-    F.trace[F.step % kTraceCap] = t;
-    int err = 0, kind = 0;
-    long long idx = -1;
-    if (any_nan) {
-        err = TGCU_ERR_INVALID_ARGUMENT;
-        kind = 1;
-        idx = st->nan_point != ULLONG_MAX ? (long long)st->nan_point : -1;
-    } else if (!isfinite(t.total)) {
-        err = TGCU_ERR_NUMERICAL;
-        kind = 2;
-    } else if (any_bad) {
-        err = TGCU_ERR_NUMERICAL;
-        kind = 3;
-        idx = st->bad_grad != ULLONG_MAX ? (long long)st->bad_grad : -1;
-    }
-    if (err) {
-        st->error = err;
-        st->error_kind = kind;
-        st->error_step = F.step;
-        st->error_index = idx;
-        st->good_idx = F.in_idx;
-        st->good_t = F.t_after - 1;
-    } else {
-        st->good_idx = 1 - F.in_idx;
-        st->good_t = F.t_after;
-    }
-    st->nan_point = ULLONG_MAX;
-    st->bad_grad = ULLONG_MAX;
+    finalize_body<1024>(F, red, threadIdx.x);
 }
 
 // ---- TMA tensor maps of the fused step --------------------------------------
@@ -1161,6 +1181,22 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     A.grad_out = grad_out;
     A.zb0 = g.zb0;
     const bool eik = cfg.lambda1 > 0.0;
+    FinArgs F;
+    F.partials = g.partials;
+    F.NB = (int)g.NB;
+    F.n = (double)n;
+    F.lambda1 = cfg.lambda1;
+    F.lambda2 = cfg.lambda2;
+    F.inv_norm = inv_norm;
+    F.use_tv = cfg.use_tv;
+    F.want_eik = eik;
+    F.st = g.st;
+    F.trace = g.d_trace;
+    F.step = step;
+    F.in_idx = in_idx;
+    F.t_after = t_after;
+    F.slab_out = slab_out;
+    F.reduced = nullptr;
     TGCU_DISPATCH(g.spec.dim, g.spec.order,
                   { ensure_tmaps(g, BrickSmem<DIM, ORDER>::TMAP, BrickSmem<DIM, ORDER>::TROWF); });
     A.use_tmap = g.tm_state == 1 ? 1 : 0;
@@ -1190,22 +1226,6 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
         if (g.prof_on) prof_mark(g, s, 1);
     });
 
-    FinArgs F;
-    F.partials = g.partials;
-    F.NB = (int)g.NB;
-    F.n = (double)n;
-    F.lambda1 = cfg.lambda1;
-    F.lambda2 = cfg.lambda2;
-    F.inv_norm = inv_norm;
-    F.use_tv = cfg.use_tv;
-    F.want_eik = eik;
-    F.st = g.st;
-    F.trace = g.d_trace;
-    F.step = step;
-    F.in_idx = in_idx;
-    F.t_after = t_after;
-    F.slab_out = slab_out;
-    F.reduced = nullptr;
     k_step_finalize<<<1, 1024, 0, s>>>(F);
     count_launch(2);
     TGCU_CUDA(cudaGetLastError());
