@@ -278,6 +278,29 @@ int tgcu_rng_index(tgcu_rng* r, uint64_t n, int64_t count, int64_t* out);
  * reference's seed (options.seed ^ 0x5deece66d). */
 int tgcu_shuffle_order(uint64_t seed, int64_t n, uint32_t* order);
 
+/* ---- radiance density chain (volume_render.cpp:61-276, sh.cpp:43-107) ---- */
+enum { TGCU_DENSITY_SHIFTED_SOFTPLUS = 0, TGCU_DENSITY_CLAMP_RELU = 1 };
+/* tg::RenderOptions (volume_render.hpp:17-24) without stratified jitter. */
+typedef struct {
+    int n_samples;          /* 1..1024 samples per ray, t_i = near + i (far - near) / n */
+    int activation;         /* TGCU_DENSITY_* (apply_activation, volume_render.cpp:19-28) */
+    double softplus_shift;  /* default -10 */
+    double background[3];   /* default (1, 1, 1) */
+} tgcu_render_options;
+/* photometric_loss (volume_render.cpp:210-276) / render_ray (:194-208),
+ * batched: the density is `density` (3D TaylorGrid, current parameters); the
+ * color an SH grid (tg::SHColorGrid, sh.hpp:19-29) of geometry sh_spec, degree
+ * 0..2, coefficients sh_coeffs (vertex-major, [R basis | G basis | B basis]).
+ * rays: n x 8 floats (origin xyz, unit direction xyz, near, far), 16-byte
+ * aligned; gt: n x 3 or NULL (render only). Outputs (each may be NULL): colors
+ * n x 3, residual transmittance n, loss = mean squared RGB error; gradients
+ * accumulate (+=) into grad_density (coeff_total) and grad_sh (SH coeffs).
+ * Device pointers, or host with TGCU_HOST. A NaN ray -> INVALID_ARGUMENT. */
+int tgcu_photometric_loss(tgcu_grid* density, const tgcu_grid_spec* sh_spec, int sh_degree, const float* sh_coeffs,
+                          const float* rays, const float* gt, int64_t n, const tgcu_render_options* opts,
+                          float* colors, float* residual, float* grad_density, float* grad_sh, double* loss,
+                          int flags, void* stream);
+
 /* .tgrid files (grid_io.cpp:36-111, layout grid_io.hpp:11-16). F64 writes the
  * fp32 coefficients widened (exact); loading an F64 file narrows to fp32.
  * File errors -> TGCU_ERR_INGEST with the reference's messages. */

@@ -102,6 +102,9 @@ class Oracle:
         L.tgo_adam_step.argtypes = [_D, _D, _D, _D, C.c_int64, _L] + [C.c_double] * 4
         L.tgo_multilinear_resample.argtypes = [C.POINTER(_TgoSpec), _D, C.c_int, _I, _D]
         L.tgo_sample_lattice.argtypes = [C.POINTER(_TgoSpec), _D, _I, _D]
+        L.tgo_photometric_loss.restype = C.c_double
+        L.tgo_photometric_loss.argtypes = [C.POINTER(_TgoSpec), _D, C.POINTER(_TgoSpec), C.c_int, _D, C.c_int64,
+                                           _D, _D, _D, _D, _D, C.c_int, C.c_int, C.c_double, _D, _D, _D, _D, _D]
         L.tgo_coeff_count.argtypes = [C.c_int, C.c_int]
         L.tgo_backprop_mass.argtypes = [C.POINTER(_TgoSpec), _D, C.c_double, _D, _D]
         L.tgo_total_loss_mass.argtypes = [C.POINTER(_TgoSpec), _D, _D, C.c_int64, C.POINTER(_TgoLoss), _D]
@@ -228,6 +231,25 @@ class Oracle:
                                   _dp(out))
         return out
 
+    def photometric_loss(self, ds: Spec, dc, ss: Spec, deg, sc, rays, n_samples=64, activation=0, shift=-10.0,
+                         bg=(1.0, 1.0, 1.0), want_grad=False, render=False):
+        """forward_ray / backward_ray / photometric_loss restated (no jitter).
+        rays = dict(origins, dirs, near, far[, gt]). Returns dict(loss, grad_density,
+        grad_sh, colors, residual)."""
+        n = len(rays["near"])
+        f = lambda a: np.ascontiguousarray(np.asarray(a, dtype=np.float64))  # noqa: E731
+        o, d, nr, fr = f(rays["origins"]), f(rays["dirs"]), f(rays["near"]), f(rays["far"])
+        gt = f(rays["gt"]) if rays.get("gt") is not None else None
+        B = (deg + 1) ** 2
+        gd = np.zeros(ds.V * ds.K) if want_grad else None
+        gs = np.zeros(ss.V * 3 * B) if want_grad else None
+        col = np.zeros((n, 3)) if render else None
+        res = np.zeros(n) if render else None
+        loss = self.L.tgo_photometric_loss(C.byref(self._spec(ds)), _dp(f(dc)), C.byref(self._spec(ss)), deg,
+                                           _dp(f(sc)), n, _dp(o), _dp(d), _dp(nr), _dp(fr), _dp(gt), n_samples,
+                                           activation, shift, _dp(f(bg)), _dp(gd), _dp(gs), _dp(col), _dp(res))
+        return dict(loss=loss, grad_density=gd, grad_sh=gs, colors=col, residual=res)
+
     def run_schedule(self, s: Spec, coeffs0, stages, batches, cfg: "Loss", lr=0.003, beta1=0.9, beta2=0.999,
                      eps=1e-8):
         """run_schedule (schedule.cpp:62-108): per stage upsample when the
@@ -322,6 +344,8 @@ class Reference:
         L.tgr_rng_index.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _L]
         L.tgr_shuffle_order.argtypes = [C.c_uint64, C.c_int64, C.c_void_p]
         L.tgr_trace_csv.argtypes = [C.c_int, _I, _I, _D, _D, C.c_char_p, C.c_char_p, C.c_int64]
+        L.tgr_photometric_loss.argtypes = sp + [_D, _I, _D, _D, C.c_int, _D, C.c_int64, _D, _D, _D, _D, _D,
+                                                C.c_int, C.c_int, C.c_double, _D, _D, _D, _D, _D, _D]
         L.tgr_fit_sdf.argtypes = sp + [_D, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
                                        C.c_int, C.c_double, C.c_double, C.c_uint64, _D, _D, _D]
         self.L = L
@@ -492,6 +516,29 @@ class Reference:
                                   buf, len(buf))
         assert rc == 0
         return buf.value.decode()
+
+    def photometric_loss(self, ds: Spec, dc, ss: Spec, deg, sc, rays, n_samples=64, activation=0, shift=-10.0,
+                         bg=(1.0, 1.0, 1.0), want_grad=False, render=False):
+        """tg::photometric_loss / render_ray (threads 1, no jitter)."""
+        n = len(rays["near"])
+        f = lambda a: np.ascontiguousarray(np.asarray(a, dtype=np.float64))  # noqa: E731
+        o, d, nr, fr = f(rays["origins"]), f(rays["dirs"]), f(rays["near"]), f(rays["far"])
+        gt = f(rays["gt"]) if rays.get("gt") is not None else None
+        B = (deg + 1) ** 2
+        gd = np.zeros(ds.V * ds.K) if want_grad else None
+        gs = np.zeros(ss.V * 3 * B) if want_grad else None
+        col = np.zeros((n, 3)) if render else None
+        res = np.zeros(n) if render else None
+        loss = C.c_double(0.0)
+        sres = (C.c_int * 3)(*[int(x) for x in ss.res])
+        sorg = f(list(ss.origin))
+        sext = f(list(ss.extent))
+        self._err(self.L.tgr_photometric_loss(*_spec_args(ds), _dp(f(dc)), sres, _dp(sorg), _dp(sext), deg,
+                                              _dp(f(sc)), n, _dp(o), _dp(d), _dp(nr), _dp(fr), _dp(gt), n_samples,
+                                              activation, shift, _dp(f(bg)), _dp(gd), _dp(gs), _dp(col), _dp(res),
+                                              C.byref(loss)))
+        return dict(loss=loss.value if gt is not None else 0.0, grad_density=gd, grad_sh=gs, colors=col,
+                    residual=res)
 
     def schedule_progressive(self, target, dim, total_steps):
         t = (C.c_int * 3)(*[int(x) for x in (list(target) + [1, 1, 1])[:3]])

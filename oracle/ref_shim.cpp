@@ -27,6 +27,7 @@
 #include "taylorgrid/sdf_fit.hpp"
 #include "taylorgrid/sdf_loss.hpp"
 #include "taylorgrid/taylor_grid.hpp"
+#include "taylorgrid/volume_render.hpp"
 
 namespace {
 
@@ -439,6 +440,53 @@ int tgr_trace_csv(int nrows, const int* step_stage, const int* res3, const doubl
     if (static_cast<int64_t>(s.size()) + 1 > cap) return -static_cast<int>(s.size() + 1);
     std::memcpy(out, s.c_str(), s.size() + 1);
     return 0;
+}
+
+// photometric_loss / render_ray (volume_render.cpp:194-276) on a density
+// TaylorGrid and an SHColorGrid (sh.hpp:19-29). gt may be NULL (render only:
+// colors_out / residual_out via render_ray); grads may be NULL.
+int tgr_photometric_loss(int dim, const int* res, const double* origin, const double* extent, int order,
+                         const double* dcoeffs, const int* sh_res, const double* sh_origin, const double* sh_extent,
+                         int sh_degree, const double* sh_coeffs, int64_t nrays, const double* origins,
+                         const double* dirs, const double* near_, const double* far_, const double* gt,
+                         int n_samples, int activation, double shift, const double* bg, double* grad_density,
+                         double* grad_sh, double* colors_out, double* residual_out, double* loss_out) {
+    try {
+        const tg::TaylorGrid dg = make_grid(make_spec(dim, res, origin, extent, order), dcoeffs);
+        tg::SHColorGrid sg = tg::init_sh_grid(make_spec(3, sh_res, sh_origin, sh_extent, 0), sh_degree);
+        std::memcpy(sg.coeffs.data(), sh_coeffs, sg.coeffs.size() * sizeof(double));
+        tg::RenderOptions opt;
+        opt.n_samples = n_samples;
+        opt.activation = activation == 0 ? tg::DensityActivation::ShiftedSoftplus : tg::DensityActivation::ClampRelu;
+        opt.softplus_shift = shift;
+        opt.background = {bg[0], bg[1], bg[2]};
+        tg::RayBatch batch;
+        for (int64_t r = 0; r < nrays; ++r) {
+            batch.origins.push_back({origins[3 * r], origins[3 * r + 1], origins[3 * r + 2]});
+            batch.directions.push_back({dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]});
+            batch.near.push_back(near_[r]);
+            batch.far.push_back(far_[r]);
+            if (gt) batch.gt_colors.push_back({gt[3 * r], gt[3 * r + 1], gt[3 * r + 2]});
+        }
+        if (colors_out || residual_out) {
+            for (int64_t r = 0; r < nrays; ++r) {
+                const tg::RayRenderResult rr = tg::render_ray(dg, sg, batch.origins[r], batch.directions[r],
+                                                              near_[r], far_[r], opt, static_cast<uint64_t>(r));
+                if (colors_out)
+                    for (int c = 0; c < 3; ++c) colors_out[3 * r + c] = rr.color[c];
+                if (residual_out) residual_out[r] = rr.residual_transmittance;
+            }
+        }
+        if (gt) {
+            std::span<double> gd, gs;
+            if (grad_density) gd = std::span<double>(grad_density, dg.coeffs.size());
+            if (grad_sh) gs = std::span<double>(grad_sh, sg.coeffs.size());
+            *loss_out = tg::photometric_loss(dg, sg, batch, opt, gd, gs, 1);
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
 }
 
 // Schedule::progressive (schedule.cpp:27-54): writes up to 3 stages.

@@ -9,6 +9,7 @@
 #include "tg_oracle.h"
 
 #include <math.h>
+#include <stdlib.h>
 #include <stddef.h>
 #include <string.h>
 
@@ -501,6 +502,176 @@ void tgo_sample_lattice(const tgo_spec* s, const double* coeffs, const int latti
                 p[2] = s->dim == 3 ? s->origin[2] + s->extent[2] * z / (lattice[2] - 1) : 0.0;
                 out[idx++] = tgo_eval(s, coeffs, p, NULL);
             }
+}
+
+/* ---- radiance chain ------------------------------------------
+ * sh_basis (sh.cpp:43-60), the SH color of SHColorGrid (sh.cpp:71-107),
+ * forward_ray / backward_ray (volume_render.cpp:61-187) without jitter, and
+ * photometric_loss (volume_render.cpp:210-276) run sequentially. */
+#define TGO_MAX_SAMPLES 1024
+void tgo_sh_basis(int degree, const double dir[3], double* out) {
+    out[0] = 0.28209479177387814;
+    if (degree < 1) return;
+    const double x = dir[0], y = dir[1], z = dir[2];
+    const double c1 = 0.4886025119029199;
+    out[1] = -c1 * y;
+    out[2] = c1 * z;
+    out[3] = -c1 * x;
+    if (degree < 2) return;
+    out[4] = 1.0925484305920792 * x * y;
+    out[5] = -1.0925484305920792 * y * z;
+    out[6] = 0.31539156525252005 * (2.0 * z * z - x * x - y * y);
+    out[7] = -1.0925484305920792 * x * z;
+    out[8] = 0.5462742152960396 * (x * x - y * y);
+}
+
+static double sigm(double x) { return 1.0 / (1.0 + exp(-x)); }
+static double softplus_(double x) { return x > 30.0 ? x : log1p(exp(x)); }
+
+/* apply_activation (volume_render.cpp:19-28): 0 = shifted softplus, 1 = clamp relu */
+static double activation(double raw, int act, double shift, double* deriv) {
+    if (act == 0) {
+        const double z = raw + shift;
+        if (deriv) *deriv = sigm(z);
+        return softplus_(z);
+    }
+    if (deriv) *deriv = raw > 0.0 ? 1.0 : 0.0;
+    return raw > 0.0 ? raw : 0.0;
+}
+
+typedef struct {
+    double t[TGO_MAX_SAMPLES], delta[TGO_MAX_SAMPLES], sigma[TGO_MAX_SAMPLES], act_deriv[TGO_MAX_SAMPLES];
+    double trans_step[TGO_MAX_SAMPLES], weight[TGO_MAX_SAMPLES];
+    double point[TGO_MAX_SAMPLES][3], color[TGO_MAX_SAMPLES][3];
+    int64_t sh_vid[TGO_MAX_SAMPLES][8];
+    double sh_w[TGO_MAX_SAMPLES][8];
+} ray_ws;
+
+/* forward_ray (volume_render.cpp:61-128); returns the residual transmittance. */
+static double forward_ray(const tgo_spec* ds, const double* dc, const tgo_spec* ss, int deg, const double* sc,
+                          const double o[3], const double dir[3], double near_, double far_, int n, int act,
+                          double shift, const double bg[3], ray_ws* ws, double color_out[3]) {
+    const double span = far_ - near_;
+    const double bin = span / n;
+    for (int i = 0; i < n; ++i) ws->t[i] = near_ + i * bin;
+    for (int i = 0; i + 1 < n; ++i) ws->delta[i] = ws->t[i + 1] - ws->t[i];
+    ws->delta[n - 1] = far_ - ws->t[n - 1];
+    const int B = (deg + 1) * (deg + 1), C = 3 * B;
+    double basis[9];
+    tgo_sh_basis(deg, dir, basis);
+    double col[3] = {0.0, 0.0, 0.0};
+    double transmittance = 1.0;
+    for (int i = 0; i < n; ++i) {
+        double x[3];
+        for (int a = 0; a < 3; ++a) x[a] = o[a] + ws->t[i] * dir[a];
+        for (int a = 0; a < 3; ++a) ws->point[i][a] = x[a];
+        const double raw = tgo_eval(ds, dc, x, NULL);
+        ws->sigma[i] = activation(raw, act, shift, &ws->act_deriv[i]);
+        int cell[3];
+        double local[3];
+        int64_t vid[8];
+        tgo_locate(ss, x, cell, local, vid);
+        const int corners = 1 << ss->dim;
+        double pre[3] = {0.0, 0.0, 0.0};
+        for (int c = 0; c < corners; ++c) {
+            double w = 1.0;
+            for (int a = 0; a < ss->dim; ++a) {
+                const int bit = (c >> a) & 1;
+                w *= bit ? local[a] : 1.0 - local[a];
+            }
+            ws->sh_w[i][c] = w;
+            ws->sh_vid[i][c] = vid[c];
+            const double* block = sc + vid[c] * C;
+            for (int ch = 0; ch < 3; ++ch) {
+                double acc = 0.0;
+                const double* k = block + ch * B;
+                for (int b = 0; b < B; ++b) acc += k[b] * basis[b];
+                pre[ch] += w * acc;
+            }
+        }
+        for (int ch = 0; ch < 3; ++ch) ws->color[i][ch] = sigm(pre[ch]);
+        const double step = exp(-ws->sigma[i] * ws->delta[i]);
+        ws->trans_step[i] = step;
+        const double w = transmittance * (1.0 - step);
+        ws->weight[i] = w;
+        for (int ch = 0; ch < 3; ++ch) col[ch] += w * ws->color[i][ch];
+        transmittance *= step;
+    }
+    for (int ch = 0; ch < 3; ++ch) color_out[ch] = col[ch] + transmittance * bg[ch];
+    return transmittance;
+}
+
+/* backward_ray (volume_render.cpp:131-187). */
+static void backward_ray(const tgo_spec* ds, const tgo_spec* ss, int deg, const double dir[3], int n, const double bg[3],
+                         double residual, const double dl_dcolor[3], ray_ws* ws, double* gd, double* gsh) {
+    const int B = (deg + 1) * (deg + 1), C = 3 * B;
+    double basis[9];
+    tgo_sh_basis(deg, dir, basis);
+    double suffix[3] = {residual * bg[0], residual * bg[1], residual * bg[2]};
+    double run = 1.0;
+    for (int i = 0; i < n; ++i) {
+        run *= ws->trans_step[i];
+        ws->t[i] = run; /* T_{i+1} */
+    }
+    const double zero[3] = {0.0, 0.0, 0.0};
+    for (int i = n - 1; i >= 0; --i) {
+        const double t_next = ws->t[i];
+        if (gd) {
+            double dl_dsigma = 0.0;
+            for (int ch = 0; ch < 3; ++ch)
+                dl_dsigma += dl_dcolor[ch] * ws->delta[i] * (t_next * ws->color[i][ch] - suffix[ch]);
+            const double dl_draw = dl_dsigma * ws->act_deriv[i];
+            if (dl_draw != 0.0) tgo_backprop(ds, ws->point[i], dl_draw, zero, gd);
+        }
+        if (gsh) {
+            for (int ch = 0; ch < 3; ++ch) {
+                const double c = ws->color[i][ch];
+                const double dl_dpre = dl_dcolor[ch] * ws->weight[i] * c * (1.0 - c);
+                if (dl_dpre == 0.0) continue;
+                for (int corner = 0; corner < (1 << ss->dim); ++corner) {
+                    const double f = ws->sh_w[i][corner] * dl_dpre;
+                    double* k = gsh + ws->sh_vid[i][corner] * C + ch * B;
+                    for (int b = 0; b < B; ++b) k[b] += f * basis[b];
+                }
+            }
+        }
+        for (int ch = 0; ch < 3; ++ch) suffix[ch] += ws->weight[i] * ws->color[i][ch];
+    }
+}
+
+/* photometric_loss (volume_render.cpp:210-245, threads = 1) and render_ray
+ * (:194-208). rays: origins/dirs n x 3, near/far n, gt n x 3 (NULL: render
+ * only). colors_out n x 3 and residual_out n may be NULL; gd/gsh gradient
+ * accumulators (NULL: none). Returns the mean squared error (0 without gt). */
+double tgo_photometric_loss(const tgo_spec* ds, const double* dc, const tgo_spec* ss, int deg, const double* sc,
+                            int64_t nrays, const double* origins, const double* dirs, const double* near_,
+                            const double* far_, const double* gt, int n_samples, int act, double shift,
+                            const double bg[3], double* gd, double* gsh, double* colors_out, double* residual_out) {
+    ray_ws* ws = (ray_ws*)malloc(sizeof(ray_ws));
+    const double inv_n = 1.0 / (double)nrays;
+    double sum = 0.0;
+    for (int64_t r = 0; r < nrays; ++r) {
+        double col[3];
+        const double resid = forward_ray(ds, dc, ss, deg, sc, origins + 3 * r, dirs + 3 * r, near_[r], far_[r],
+                                         n_samples, act, shift, bg, ws, col);
+        if (colors_out)
+            for (int ch = 0; ch < 3; ++ch) colors_out[3 * r + ch] = col[ch];
+        if (residual_out) residual_out[r] = resid;
+        if (!gt) continue;
+        double err[3], e2 = 0.0;
+        for (int ch = 0; ch < 3; ++ch) {
+            err[ch] = col[ch] - gt[3 * r + ch];
+            e2 += err[ch] * err[ch];
+        }
+        sum += e2;
+        if (gd || gsh) {
+            double g[3];
+            for (int ch = 0; ch < 3; ++ch) g[ch] = (2.0 * inv_n) * err[ch];
+            backward_ray(ds, ss, deg, dirs + 3 * r, n_samples, bg, resid, g, ws, gd, gsh);
+        }
+    }
+    free(ws);
+    return sum * inv_n;
 }
 
 /* Test helper: the device locate's division t = x / h via Markstein's

@@ -191,6 +191,9 @@ void launch_f64_to_f32(const double* src, float* dst, int64_t n, cudaStream_t s)
 void launch_f32_to_f64(const float* src, double* dst, int64_t n, cudaStream_t s);
 void launch_all_finite(const float* src, int64_t n, unsigned long long* flag, cudaStream_t s);
 void launch_fill_f0(Grid& g, float* dst, float value, cudaStream_t s);
+void launch_rays(Grid& g, const DevSpec& ss, int deg, const float* scoeffs, const float* rays, const float* gt,
+                 int64_t n, const tgcu_render_options& o, float* colors, float* resid, float* gd, float* gsh,
+                 double* ray_err, double* loss, cudaStream_t s);
 void launch_hash_gaussian(float* dst, int64_t n, uint64_t seed, double sigma, int64_t goff, cudaStream_t s);
 void launch_hash_points(float* out, int64_t n, int dim, uint64_t seed, double lo, double hi, cudaStream_t s);
 void launch_draw_batch(const float* pool, int64_t pool_n, int64_t n, uint64_t seed, uint64_t step, float* out,

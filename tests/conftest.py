@@ -38,13 +38,14 @@ def assert_trajectory_close(got, ref, lr, steps, rel=1e-5, floor=1e-2, max_frac=
     """Two runs of the same training trajectory that differ only in fp32
     summation order (the fused step bins and ranks points with atomics). Adam
     normalises each update, so a coefficient whose gradient is rounding noise
-    can move by up to ~lr per step either way: require all but `max_frac` of
-    the coefficients within rel * max(|ref|, floor) and every one within
-    2 * lr * steps."""
+    can move by up to ~lr per step either way: require all but max(3,
+    max_frac * size) of the coefficients within rel * max(|ref|, floor) and
+    every one within 2 * lr * steps."""
     import numpy as np
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     d = np.abs(got - ref)
     bad = d > rel * np.maximum(np.abs(ref), floor)
-    assert bad.mean() <= max_frac, f"{what}: {bad.sum()}/{bad.size} beyond {rel:g} rel (max {d.max():.3g})"
+    allowed = max(3, int(max_frac * bad.size))  # a handful of noise-gradient coefficients, even in tiny grids
+    assert bad.sum() <= allowed, f"{what}: {bad.sum()}/{bad.size} beyond {rel:g} rel (max {d.max():.3g})"
     assert d.max() <= 2.0 * lr * steps, f"{what}: max |d| {d.max():.3g} > 2*lr*steps"

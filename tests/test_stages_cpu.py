@@ -125,3 +125,20 @@ def test_live_reference_stage_rows(reference, oracle):
     c = rng.normal(0, 0.3, s.V * s.K)
     assert np.array_equal(oracle.resample(s, c, s.K, (9, 5, 11)), reference.upsample(s, c, (9, 5, 11)))
     assert np.array_equal(oracle.sample_lattice(s, c, (7, 3, 10)), reference.sample_grid_field(s, c, (7, 3, 10)))
+
+
+@pytest.mark.parametrize("case", ["soft64", "soft100", "relu64"])
+def test_oracle_radiance_golden(oracle, case):
+    """forward_ray / backward_ray / photometric_loss restated == the reference."""
+    z = load_golden("radiance.npz")
+    p = case + "_"
+    act, ns, order, deg = (int(x) for x in z[p + "meta"])
+    ds = Spec(3, tuple(int(r) for r in z[p + "dres"]), order=order)
+    ss = Spec(3, tuple(int(r) for r in z[p + "sres"]), order=0, origin=tuple(z[p + "sorg"]),
+              extent=tuple(z[p + "sext"]))
+    rays = dict(origins=z[p + "o"], dirs=z[p + "d"], near=z[p + "near"], far=z[p + "far"], gt=z[p + "gt"])
+    r = oracle.photometric_loss(ds, z[p + "dc"], ss, deg, z[p + "sc"], rays, n_samples=ns, activation=act,
+                                want_grad=True, render=True)
+    assert r["loss"] == z[p + "loss"][0]
+    assert np.array_equal(r["grad_density"], z[p + "gd"]) and np.array_equal(r["grad_sh"], z[p + "gs"])
+    assert np.array_equal(r["colors"], z[p + "colors"]) and np.array_equal(r["residual"], z[p + "resid"])
