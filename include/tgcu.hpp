@@ -106,8 +106,51 @@ public:
         return t;
     }
 
+    tgcu_grid_spec spec() const {
+        tgcu_grid_spec s{};
+        tgcu_grid_spec_of(h_, &s);
+        return s;
+    }
+
+    // sample_grid_field (marching.cpp:53-58): values on an n0 x n1 x n2 lattice
+    // of the grid's domain, x fastest.
+    std::vector<float> sample_grid_field(const std::array<int, 3>& lattice) const {
+        const size_t n = static_cast<size_t>(lattice[0]) * lattice[1] * (spec().dim == 3 ? lattice[2] : 1);
+        std::vector<float> v(n);
+        check(tgcu_sample_grid_field(h_, lattice.data(), v.data(), TGCU_HOST, nullptr));
+        return v;
+    }
+
+    // save_tgrid (grid_io.cpp:44-65); precision TGCU_TGRID_F64 / _F32.
+    void save_tgrid(const char* path, int precision = TGCU_TGRID_F64) const {
+        check(tgcu_save_tgrid(h_, path, precision));
+    }
+
+    static Grid adopt(tgcu_grid* h) {
+        Grid g;
+        g.h_ = h;
+        return g;
+    }
+
 private:
+    Grid() = default;
     tgcu_grid* h_ = nullptr;
 };
+
+// upsample (taylor_grid.cpp:273-284): a new grid at new_res.
+inline Grid upsample(const Grid& g, const std::array<int, 3>& new_res) {
+    tgcu_grid_spec s = g.spec();
+    for (int a = 0; a < 3; ++a) s.res[a] = new_res[a];
+    Grid out(s);
+    check(tgcu_grid_upsample(g.handle(), out.handle(), 0, nullptr));
+    return out;
+}
+
+// load_tgrid (grid_io.cpp:67-109).
+inline Grid load_tgrid(const char* path, int device = 0) {
+    tgcu_grid* h = nullptr;
+    check(tgcu_load_tgrid(path, device, &h));
+    return Grid::adopt(h);
+}
 
 }  // namespace tgcu

@@ -38,6 +38,20 @@ int main() {
         return 5;
     } catch (const std::invalid_argument&) {
     }
+    // progressive stage change, lattice extraction, .tgrid round trip
+    tgcu::Grid up = tgcu::upsample(g, {48, 48, 48});
+    const auto lat = up.sample_grid_field({9, 9, 9});
+    if (lat.size() != 729 || !std::isfinite(lat[364])) return 6;
+    up.save_tgrid("/tmp/tgcu_shim_test.tgrid");
+    tgcu::Grid back = tgcu::load_tgrid("/tmp/tgcu_shim_test.tgrid");
+    if (back.coeffs() != up.coeffs()) return 7;
+    try {
+        tgcu::load_tgrid("/tmp/does_not_exist.tgrid");
+        return 8;
+    } catch (const tgcu::IngestError& e) {
+        std::printf("IngestError: %s\n", e.what());
+    }
+    std::printf("upsample + lattice + tgrid ok (f(centre) %.4f)\n", lat[364]);
     std::printf("shim ok\n");
     return 0;
 }
