@@ -155,6 +155,14 @@ template <int DIM, int K, int T>
 constexpr int query_trowf() {
     return (DIM == 3 && K == 10) ? 104 : (DIM == 3 && K == 4) ? 48 : ((T * K + 3) / 4) * 4;
 }
+#ifndef QMINB_SMALL
+#define QMINB_SMALL 8
+#endif
+// Resident CTAs per SM the register budget is sized for: the tile of a K = 10
+// brick (33.7 KB) allows 6, smaller tiles 8 (measured: 5 -> 6 CTAs took the
+// 512^3 order-2 sorted query from 53 % to 59 % of the HBM roofline).
+template <int K>
+constexpr int query_min_blocks() { return K >= 10 ? 6 : QMINB_SMALL; }
 
 // Number of Morton brick codes of the query decomposition (pow2^DIM).
 int64_t query_brick_codes(const Grid& g) {
@@ -263,7 +271,7 @@ void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_
 // grid layout cannot take a tensor map. Each thread loads and locates its first
 // point before waiting for the tile, so the two latencies overlap.
 template <int DIM, int ORDER, bool GRAD, int LB, bool BINNED = false>
-__global__ void __launch_bounds__(256) k_eval_brick(const __grid_constant__ CUtensorMap tmap, int use_tmap,
+__global__ void __launch_bounds__(256, query_min_blocks<KOf<DIM, ORDER>::value>()) k_eval_brick(const __grid_constant__ CUtensorMap tmap, int use_tmap,
                                                     DevSpec s, const float* __restrict__ coeffs,
                                                     const float* __restrict__ pts, const long long* __restrict__ off,
                                                     float* __restrict__ vals, float* __restrict__ grads,
