@@ -171,6 +171,27 @@ double tgo_eval(const tgo_spec* s, const double* coeffs, const double p[3], doub
     return value;
 }
 
+/* Test helper for the gradient tolerance: per axis, the L1 size of the terms
+ * whose sum is the spatial gradient (sum_i |dw_i,a T_i| + |w_i gT_i,a|). An
+ * fp32 forward resolves grad f only to ~eps32 times this, which on fine grids
+ * (dw ~ 1/h) is far larger than |grad f| itself. */
+static void eval_grad_l1(const tgo_spec* s, const double* coeffs, const double p[3], double l1[3]) {
+    int cell[3];
+    double local[3];
+    int64_t vid[8];
+    l1[0] = l1[1] = l1[2] = 0.0;
+    if (tgo_locate(s, p, cell, local, vid) != 0) return;
+    corners_t c;
+    make_corners(s, local, vid, &c);
+    const int K = tgo_coeff_count(s->order, s->dim);
+    for (int i = 0; i < c.count; ++i) {
+        const double* b = coeffs + c.vid[i] * K;
+        double tg[3];
+        const double tv = taylor_poly(b, s->order, s->dim, c.delta[i], tg);
+        for (int a = 0; a < s->dim; ++a) l1[a] += fabs(c.dw[i][a] * tv) + fabs(c.w[i] * tg[a]);
+    }
+}
+
 /* accumulate_cell (taylor_grid.cpp:123-152). */
 static void accumulate_cell(const tgo_spec* s, const corners_t* c, double upstream,
                             const double gvec[3], double* grad) {
@@ -398,12 +419,18 @@ static void point_terms(const tgo_spec* s, const double* coeffs, const double* s
             /* The eikonal upstream scales with (|grad f| - 1), which an fp32
              * forward evaluates to ~1e-7 absolute: bound its sensitivity by
              * using (|r| + 0.1) for the mass (0.1 * mass_rel covers that). */
+            /* The fp32 forward also resolves grad f only to ~16 eps32 times
+             * the L1 size of its terms (eval_grad_l1: 2^D corners, each a
+             * chain of ~2K FMAs): add 0.25 (= 16 eps32 / mass_rel) of that
+             * size per axis. */
             double umass[3] = {0.0, 0.0, 0.0};
             if (want_eik) {
                 const double nrm = sqrt(sg[0] * sg[0] + sg[1] * sg[1] + sg[2] * sg[2]);
                 if (nrm > 0.0) {
+                    double l1[3];
+                    eval_grad_l1(s, coeffs, p, l1);
                     const double sc = eik_scale * inv_n * 2.0 * (fabs(nrm - 1.0) + 0.1) / nrm;
-                    for (int a = 0; a < 3; ++a) umass[a] = fabs(sc * sg[a]);
+                    for (int a = 0; a < 3; ++a) umass[a] = fabs(sc) * (fabs(sg[a]) + 0.25 * l1[a]);
                 }
             }
             tgo_backprop_mass(s, p, upstream, umass, mass);

@@ -381,3 +381,76 @@ def test_binned_unsorted_query_matches_direct(oracle, order):
     pts[[7, 100003]] = np.nan
     with pytest.raises(ValueError, match="point 7"):
         tg.eval(g, pts)
+
+
+@pytest.mark.parametrize("dim,res", [(2, (37, 29)), (3, (19, 12, 26))])
+@pytest.mark.parametrize("order", [0, 1, 2])
+@pytest.mark.parametrize("name,cfg", [("paper", tg.LossConfig()), ("recon", tg.LossConfig(lambda1=0.0, use_tv=False)),
+                                      ("dw", tg.LossConfig(differentiate_weight=True, lambda1=3e-3))])
+def test_fused_step_all_orders_vs_oracle(oracle, dim, res, order, name, cfg):
+    """Fused step (binning, brick kernel with edge bricks, finalize) for every
+    order and dimension: loss terms, full gradient and the first Adam update
+    against the fp64 oracle; resolutions not multiples of the brick edge."""
+    rng = np.random.default_rng(1000 + 10 * order + dim)
+    r3 = tuple(res) + ((1,) if dim == 2 else ())
+    s = ospec(dim, r3, order)
+    c = (0.2 * rng.standard_normal(s.V * s.K)).astype(np.float32).astype(np.float64)
+    n = 5000
+    pts = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    pts[:50] = np.float32(1.0)            # max boundary -> last cell, local 1 (several bricks' boundary)
+    pts[50:100, 0] = np.float32(-1.0)
+    if dim == 2:
+        pts[:, 2] = 0.0
+    gt = (np.linalg.norm(pts[:, :dim], axis=1) - 0.5).astype(np.float32)
+    smp = np.concatenate([pts, gt[:, None]], 1).astype(np.float64)
+    loss = Loss(cfg.lambda1, cfg.lambda2, cfg.k, cfg.use_weighting, cfg.use_tv, cfg.differentiate_weight)
+    gref = np.zeros(s.V * s.K)
+    tref = oracle.total_loss(s, c, smp, loss, gref)
+    mass = oracle.total_loss_mass(s, c, smp, loss)
+    g = tg.init_grid(gspec(dim, r3, order))
+    g.coeffs = c
+    g.adam_reset(tg.AdamConfig(lr=1e-2))
+    t = tg.train_step(g, smp, cfg, export_grad=True)
+    assert_close(t.as_array(), tref, 1e-6, floor=1e-30, what="fused terms")
+    grad_close(g.grad(), gref, mass, what="fused grad")
+    p1 = c - 1e-2 * gref / (np.abs(gref) + 1e-8)  # first Adam step (bias-corrected)
+    ok = np.abs(gref) > 1e-3 * (np.abs(gref).max() + 1e-30)  # away from sign-ambiguous tiny gradients
+    assert_close(g.coeffs[ok], p1[ok], 1e-6, floor=1.0, what="params after step")
+
+
+@pytest.mark.parametrize("case", ["many_points", "many_bricks"])
+def test_global_binning_path_vs_oracle(oracle, case):
+    """Batches of more than 2^21 points, or grids of more than 16384 bricks
+    (C3 / C5 scale), bin with global atomics instead of the privatized
+    shared-memory histograms: same loss terms and gradient as the oracle."""
+    rng = np.random.default_rng(77)
+    if case == "many_points":
+        res, order, n = (48, 44, 40), 2, 3 * (1 << 20)
+    else:
+        res, order, n = (256, 256, 256), 1, 200000   # 32^3 = 32768 bricks
+    s = ospec(3, res, order)
+    c = (0.05 * rng.standard_normal(s.V * s.K)).astype(np.float32).astype(np.float64)
+    smp = tg.sample(tg.SHAPE_SPHERE, 3, 321, n, near_frac=0.5, sigma=0.01, param0=0.6).astype(np.float64)
+    cfg = tg.LossConfig()
+    gref = np.zeros(s.V * s.K)
+    tref = oracle.total_loss(s, c, smp, Loss(), gref)
+    mass = oracle.total_loss_mass(s, c, smp, Loss())
+    g = tg.init_grid(gspec(3, res, order))
+    g.coeffs = c
+    g.adam_reset(tg.AdamConfig(lr=1e-2))
+    t = tg.train_step(g, smp, cfg, export_grad=True)
+    assert_close(t.as_array(), tref, 1e-6, floor=1e-30, what="terms")
+    grad_close(g.grad(), gref, mass, what="grad")
+
+
+def test_empty_and_degenerate_inputs():
+    g = tg.init_grid(tg.GridSpec(dim=3, resolution=(9, 9, 9), order=2))
+    g.adam_reset(tg.AdamConfig())
+    assert tg.eval(g, np.zeros((0, 3))).shape == (0,)
+    with pytest.raises(ValueError, match="empty batch"):
+        tg.train_step(g, np.zeros((0, 4)))
+    assert g.adam_t == 0
+    # a batch whose points all sit in one cell / on one vertex
+    one = np.tile(np.array([[0.125, -0.25, 0.5, 0.1]], np.float32), (4096, 1))
+    t = tg.train_step(g, one)
+    assert np.isfinite(t.total) and g.adam_t == 1
