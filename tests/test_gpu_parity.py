@@ -288,17 +288,18 @@ def test_c2_scale_fused_gradient_vs_oracle(oracle):
 # ---- multi-GPU slab path, two slabs emulated on one device ----------------------------------------
 
 
-def test_slab_two_on_one_gpu_matches_full_grid():
-    """Two z-slab grids driven like two ranks (sum of partials, commit, halo
-    exchange by device copies) reproduce the single-grid fused trajectory."""
+@pytest.mark.parametrize("nslab,res", [(2, (24, 20, 40)), (3, (21, 18, 43))])
+def test_slab_two_on_one_gpu_matches_full_grid(nslab, res):
+    """z-slab grids driven like ranks (sum of partials, commit, halo exchange
+    by device copies) reproduce the single-grid fused trajectory; with three
+    slabs the middle one exchanges both halo planes."""
     from paper_2402_14415_b200.slab import SlabGrid, brick_layers, device_view, slab_ranges
-    res = (24, 20, 40)
     spec = tg.GridSpec(dim=3, resolution=res, order=2)
     init = tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.02, seed=3)
     cfg = tg.LossConfig()
     full = tg.init_grid(spec, init)
     full.adam_reset(tg.AdamConfig(lr=1e-2))
-    ranges = slab_ranges(brick_layers(res[2]), 2)
+    ranges = slab_ranges(brick_layers(res[2]), nslab)
     slabs = [SlabGrid(spec, lo, hi, init) for lo, hi in ranges]
     for sg in slabs:
         sg.adam_reset(tg.AdamConfig(lr=1e-2))
@@ -312,14 +313,18 @@ def test_slab_two_on_one_gpu_matches_full_grid():
         tf = tg.train_step(full, b, cfg).as_array()
         parts = [sg.begin(b, cfg) for sg in slabs]
         views = [device_view(p, 5, "<f8") for p in parts]
-        tot = views[0] + views[1]
+        tot = views[0].clone()
+        for v in views[1:]:
+            tot += v
         for v in views:
             v.copy_(tot)
         terms = [sg.finish(p).as_array() for sg, p in zip(slabs, parts)]
-        s0, s1 = slabs[0].halo(), slabs[1].halo()
-        pf = s0[4]
-        device_view(s1[2], pf).copy_(device_view(s0[1], pf))  # slab0 top owned plane -> slab1 lower halo
-        device_view(s0[3], pf).copy_(device_view(s1[0], pf))  # slab1 bottom owned plane -> slab0 upper halo
+        halos = [sg.halo() for sg in slabs]
+        for r in range(nslab - 1):  # slab r's top owned plane <-> slab r+1's bottom owned plane
+            lo, hi = halos[r], halos[r + 1]
+            pf = lo[4]
+            device_view(hi[2], pf).copy_(device_view(lo[1], pf))
+            device_view(lo[3], pf).copy_(device_view(hi[0], pf))
         for t in terms:
             assert_close(t, tf, 1e-6, floor=1e-30, what=f"slab terms step {step}")
     owned = np.concatenate([sg.owned_coeffs() for sg in slabs])
