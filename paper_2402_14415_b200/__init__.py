@@ -153,6 +153,9 @@ def lib():
     L.tgcu_load_tgrid.argtypes = [C.c_char_p, C.c_int, C.POINTER(P)]
     L.tgcu_tgrid_file_size.argtypes = [C.POINTER(_Spec), C.c_int]
     L.tgcu_tgrid_file_size.restype = C.c_int64
+    # tgcu_render_options is declared in radiance.py (_RO); the pointer is passed as void*
+    L.tgcu_photometric_loss.argtypes = [P, C.POINTER(_Spec), C.c_int, P, P, P, C.c_int64, P, P, P, P, P,
+                                        C.POINTER(C.c_double), C.c_int, P]
     L.tgcu_rng_create.argtypes = [C.c_uint64, C.POINTER(P)]
     L.tgcu_rng_destroy.argtypes = [P]
     L.tgcu_rng_index.argtypes = [P, C.c_uint64, C.c_int64, P]

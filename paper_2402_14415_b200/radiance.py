@@ -94,9 +94,6 @@ def make_rays(origins, dirs, near, far) -> np.ndarray:
 def _call(density: TaylorGrid, sh: SHColorGrid, rays, gt, opts: RenderOptions, want_colors: bool,
           want_grad: bool):
     L = lib()
-    L.tgcu_photometric_loss.argtypes = [C.c_void_p, C.POINTER(_Spec), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
-                                        C.c_int64, C.POINTER(_RO), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                        C.POINTER(C.c_double), C.c_int, C.c_void_p]
     r = np.ascontiguousarray(np.asarray(rays, dtype=np.float32)).reshape(-1, 8)
     n = r.shape[0]
     g = None if gt is None else np.ascontiguousarray(np.asarray(gt, dtype=np.float32)).reshape(-1, 3)
@@ -109,8 +106,8 @@ def _call(density: TaylorGrid, sh: SHColorGrid, rays, gt, opts: RenderOptions, w
              (C.c_double * 3)(*[float(b) for b in opts.background]))
     loss = C.c_double(0.0)
     _check(L.tgcu_photometric_loss(density.handle, C.byref(sh.spec._c()), sh.degree, _ptr(shc), _ptr(r), _ptr(g), n,
-                                   C.byref(ro), _ptr(cols), _ptr(res), _ptr(gd), _ptr(gs), C.byref(loss), TGCU_HOST,
-                                   None))
+                                   C.cast(C.pointer(ro), C.c_void_p), _ptr(cols), _ptr(res), _ptr(gd), _ptr(gs),
+                                   C.byref(loss), TGCU_HOST, None))
     return loss.value, cols, res, gd, gs
 
 

@@ -63,7 +63,8 @@ def throughput():
 
     def run(grad):
         tg._check(L.tgcu_photometric_loss(g.handle, C.byref(spec), deg, C.c_void_p(shc.data_ptr()),
-                                          C.c_void_p(rays.data_ptr()), C.c_void_p(gt.data_ptr()), n, C.byref(ro),
+                                          C.c_void_p(rays.data_ptr()), C.c_void_p(gt.data_ptr()), n,
+                                          C.cast(C.pointer(ro), C.c_void_p),
                                           None, None, C.c_void_p(gd.data_ptr()) if grad else None,
                                           C.c_void_p(gs.data_ptr()) if grad else None, C.byref(loss), 0, None))
     for grad in (False, True):
@@ -78,5 +79,6 @@ def throughput():
 
 
 if __name__ == "__main__":
-    margins()
+    if "--no-margins" not in sys.argv:
+        margins()
     throughput()
