@@ -106,12 +106,18 @@ class ClockSampler:
 
 
 def dist_setup():
+    """One process per GPU (torchrun env). The device is bound before the
+    process group so NCCL initialises on it. TGCU_DIST_BACKEND=gloo (tests
+    only) runs the same flow with host-staged collectives, ranks wrapping onto
+    the available devices."""
+    import torch
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("TGCU_DIST_BACKEND", "nccl"))
     return ws, rank, local
 
 
@@ -126,7 +132,8 @@ def max_over_ranks(x, ws):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -373,7 +380,12 @@ def main():
     clk = clocks.summary()
     value = NPTS * args.steps / (ms_total * 1e-3)  # whole job: one global batch per step
     kern_ms = brick_ms / max(brick_n, 1)
-    kern_bytes = 24 * VK + 16 * NPTS  # p r+w, m r+w, v r+w (fp32) + each point once
+    if ws == 1:
+        vk_local, pts_local = VK, NPTS
+    else:  # this rank's kernel: its owned vertex planes, ~1/N of the points
+        vk_local = (g.z_own_hi - g.z_own_lo) * RES[0] * RES[1] * K
+        pts_local = NPTS // ws
+    kern_bytes = 24 * vk_local + 16 * pts_local  # p r+w, m r+w, v r+w (fp32) + each point once
     achieved = kern_bytes / (kern_ms * 1e-3) / 1e9
     survey_bytes = NPTS * 16 + 3 * VK * 4 + 32 * VK  # SURVEY 8d B_t with U ~= V (unfused accounting)
     line = {
@@ -388,7 +400,8 @@ def main():
                      "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic_from_profile(),
                      "algorithmic_bytes_per_launch": kern_bytes,
-                     "algorithmic_bytes_def": "24 B/coeff (p,m,v read+write fp32; grad never stored) + 16 B/point",
+                     "algorithmic_bytes_def": "24 B/coeff (p,m,v read+write fp32; grad never stored) + 16 B/point"
+                                              + ("" if ws == 1 else " (rank 0's owned slab, N/ranks points)"),
                      "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_step,
                      "step_frac_survey_bytes": survey_bytes / (ms_step * 1e-3) / 1e9 / hbm_peak},
         "e2e": {"value": NPTS * ne / e2e_s, "unit": "points/s", "h2d_bytes_per_step": NPTS * 16 * ws,

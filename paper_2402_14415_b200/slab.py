@@ -201,6 +201,15 @@ class SlabGrid:
         _check(lib().tgcu_sync(self._h, C.byref(t)))
         return LossTerms._from(t)
 
+    def profile_begin(self):
+        _check(lib().tgcu_profile_begin(self._h))
+
+    def profile_end(self):
+        """(summed brick-kernel device ms, launches) since profile_begin."""
+        ms, n = C.c_double(), C.c_int()
+        _check(lib().tgcu_profile_end(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
 
 class SlabTrainer:
     """One rank of a torch.distributed (NCCL) slab-parallel training run."""
