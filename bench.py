@@ -324,8 +324,15 @@ def main():
         trainer = SlabTrainer(spec, rank, ws, tg.AdamConfig(lr=LR), device=dev)
         g = trainer.slab
 
+        # data sharded by owner up front (outside the timed region): each rank
+        # holds the points whose cells touch its slab; the loss keeps the
+        # global 1/N (SURVEY 8e "bins points to their owning GPU")
+        local_host = [trainer.local_points(b) for b in host_batches]
+        dev_batches = [torch.from_numpy(b).to(f"cuda:{dev}") for b in local_host]
+        host_batches = local_host
+
         def step(batch, asynchronous=True):
-            return trainer.step(batch, cfg, stream=sp, want_terms=not asynchronous)
+            return trainer.step(batch, cfg, stream=sp, want_terms=not asynchronous, n_global=NPTS)
 
     for i in range(args.warmup):
         step(dev_batches[i % NBATCH])
@@ -404,7 +411,8 @@ def main():
                                               + ("" if ws == 1 else " (rank 0's owned slab, N/ranks points)"),
                      "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_step,
                      "step_frac_survey_bytes": survey_bytes / (ms_step * 1e-3) / 1e9 / hbm_peak},
-        "e2e": {"value": NPTS * ne / e2e_s, "unit": "points/s", "h2d_bytes_per_step": NPTS * 16 * ws,
+        "e2e": {"value": NPTS * ne / e2e_s, "unit": "points/s",
+                "h2d_bytes_per_step": int(16 * ws * sum(b.shape[0] for b in host_batches) / len(host_batches)),
                 "d2h_bytes_per_step": 32,
                 "api": ("tgcu_train_step(TGCU_HOST|TGCU_ASYNC): pipelined H2D on a copy stream, per-step LossTerms "
                         "D2H to pinned memory" if ws == 1 else "SlabTrainer.step with host samples, synchronous"),

@@ -196,9 +196,9 @@ int tgcu_train_step(tgcu_grid* g, const float* samples, int64_t n, const tgcu_lo
  * A slab grid holds the brick layers [zb_lo, zb_hi) (bricks of 8^3 vertices)
  * of the global 3D spec: it owns (and Adam-updates) vertex planes
  * [8*zb_lo, min(8*zb_hi, res_z)) and stores one extra halo plane below and
- * above. Every rank is given the full global batch; its binning keeps the
- * points whose cells touch its owned vertices (those in a slab-boundary cell
- * layer go to both ranks). A step is
+ * above. A rank reads either the full global batch or only the points whose
+ * cells touch its owned vertices (those in a slab-boundary cell layer belong
+ * to both ranks); its binning keeps exactly those. A step is
  *   tgcu_slab_step_begin -> sum the 5 doubles at *partials over ranks
  *   (recon, eik, tv, nan flag, bad-grad flag; e.g. NCCL all-reduce in place)
  *   -> tgcu_slab_step_finish(reduced) -> exchange halo planes.
@@ -209,8 +209,12 @@ int tgcu_grid_create_slab(const tgcu_grid_spec* global_spec, int zb_lo, int zb_h
                           int device, tgcu_grid** out);
 int tgcu_slab_info(const tgcu_grid* g, int* z_store_lo, int* z_store_n, int* z_own_lo, int* z_own_hi,
                    int* brick_layers);
-int tgcu_slab_step_begin(tgcu_grid* g, const float* samples, int64_t n_global, const tgcu_loss_config* cfg,
-                         double** partials, int flags, void* stream);
+/* samples: the n points this rank reads (the full global batch, or only the
+ * points whose cells touch this slab's owned planes — slab.py
+ * slab_point_mask); n_global: the global batch size for the loss scale 1/N
+ * (<= 0: n). */
+int tgcu_slab_step_begin(tgcu_grid* g, const float* samples, int64_t n, int64_t n_global,
+                         const tgcu_loss_config* cfg, double** partials, int flags, void* stream);
 int tgcu_slab_step_finish(tgcu_grid* g, const double* reduced, tgcu_loss_terms* out, int flags, void* stream);
 /* Device pointers (current parameters) of the planes to send to / receive
  * from the lower and upper neighbour (NULL at the grid boundary), and the

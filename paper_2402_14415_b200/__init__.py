@@ -133,8 +133,8 @@ def lib():
     L.tgcu_grid_steps_launched.argtypes = [P, C.POINTER(C.c_int64)]
     L.tgcu_grid_create_slab.argtypes = [C.POINTER(_Spec), C.c_int, C.c_int, C.POINTER(_Init), C.c_int, C.POINTER(P)]
     L.tgcu_slab_info.argtypes = [P] + [C.POINTER(C.c_int)] * 5
-    L.tgcu_slab_step_begin.argtypes = [P, P, C.c_int64, C.POINTER(_Loss), C.POINTER(C.POINTER(C.c_double)),
-                                       C.c_int, P]
+    L.tgcu_slab_step_begin.argtypes = [P, P, C.c_int64, C.c_int64, C.POINTER(_Loss),
+                                       C.POINTER(C.POINTER(C.c_double)), C.c_int, P]
     L.tgcu_slab_step_finish.argtypes = [P, P, C.POINTER(_Terms), C.c_int, P]
     L.tgcu_slab_halo.argtypes = [P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(C.c_int64)]
     L.tgcu_trace.argtypes = [P, C.POINTER(_Terms), C.c_int]

@@ -792,7 +792,8 @@ int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
             gout = g.grad;
         }
         require(!g.slab, "train_step: slab grids step with tgcu_slab_step_begin/finish");
-        launch_train_step(g, ds, n, *cfg, in_idx, g.steps_launched, 1.0 / bc1, 1.0 / bc2, t_after, gout, nullptr, s);
+        launch_train_step(g, ds, n, n, *cfg, in_idx, g.steps_launched, 1.0 / bc1, 1.0 / bc2, t_after, gout, nullptr,
+                          s);
         // Optimistic commit; a failed step is rolled back by raise_sticky().
         g.cur = 1 - in_idx;
         g.t = t_after;
@@ -815,8 +816,8 @@ int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
     });
 }
 
-int tgcu_slab_step_begin(tgcu_grid* h, const float* samples, int64_t n, const tgcu_loss_config* cfg,
-                         double** partials, int flags, void* stream) {
+int tgcu_slab_step_begin(tgcu_grid* h, const float* samples, int64_t n, int64_t n_global,
+                         const tgcu_loss_config* cfg, double** partials, int flags, void* stream) {
     return guard([&] {
         Grid& g = h->g;
         set_device(g);
@@ -844,9 +845,12 @@ int tgcu_slab_step_begin(tgcu_grid* h, const float* samples, int64_t n, const tg
         g.slab_in_idx = g.cur;
         g.slab_step = g.steps_launched;
         g.slab_t_after = t_after;
-        g.slab_n = n;
+        const int64_t nn = n_global > 0 ? n_global : n;
+        require(nn >= n, "slab_step_begin: n_global smaller than the local batch");
+        g.slab_n = nn;
         g.slab_cfg = *cfg;
-        launch_train_step(g, ds, n, *cfg, g.cur, g.steps_launched, 1.0 / bc1, 1.0 / bc2, t_after, gout, g.slab_red, s);
+        launch_train_step(g, ds, n, nn, *cfg, g.cur, g.steps_launched, 1.0 / bc1, 1.0 / bc2, t_after, gout,
+                          g.slab_red, s);
         *partials = g.slab_red;
     });
 }

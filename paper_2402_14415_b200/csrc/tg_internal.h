@@ -182,7 +182,8 @@ void launch_tv(Grid& g, const float* coeffs, float* grad, double gscale, int wan
 void launch_adam_check(Grid& g, const float* grad, cudaStream_t s);
 void launch_adam_update(Grid& g, const float* grad, double inv_bc1, double inv_bc2, cudaStream_t s);
 // Fused step: binning + brick kernel + finalize (train.cu).
-void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_loss_config& cfg, int in_idx,
+void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
+                       int in_idx,
                        int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
                        double* slab_out, cudaStream_t s);
 void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& cfg, int in_idx, int64_t step,

@@ -1098,7 +1098,8 @@ void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& 
     TGCU_CUDA(cudaGetLastError());
 }
 
-void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_loss_config& cfg, int in_idx,
+void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
+                       int in_idx,
                        int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
                        double* slab_out, cudaStream_t s) {
     ensure_bins(g, n);
@@ -1162,7 +1163,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     A.off = g.bin_off;
     for (int a = 0; a < 3; ++a) A.nb[a] = g.nb[a];
     A.L.k = cfg.k;
-    A.L.inv_n = 1.0 / (double)n;
+    A.L.inv_n = 1.0 / (double)n_norm;  // the global batch size (slab ranks may read a subset)
     A.L.eik_scale = cfg.lambda1;
     A.L.use_weighting = cfg.use_weighting;
     A.L.differentiate_weight = cfg.differentiate_weight;
@@ -1184,7 +1185,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, const tgcu_los
     FinArgs F;
     F.partials = g.partials;
     F.NB = (int)g.NB;
-    F.n = (double)n;
+    F.n = (double)n_norm;
     F.lambda1 = cfg.lambda1;
     F.lambda2 = cfg.lambda2;
     F.inv_norm = inv_norm;

@@ -6,7 +6,8 @@ state of those vertices; it stores one halo plane below and above. Every rank
 is given the full global batch and keeps the points whose cells touch its
 owned vertices (a point in a slab-boundary cell layer is used by both ranks,
 exactly as a point in a brick-boundary cell layer is binned into both bricks
-on one GPU). Per step:
+on one GPU; with `local_points` the batch can be sharded to the ranks up
+front, the loss still normalised by the global batch size). Per step:
 
     partials = slab.begin(batch)          # bin + fused brick kernel, local sums
     all_reduce(partials)                  # {recon, eik, tv, nan flag, bad flag}
@@ -166,8 +167,10 @@ class SlabGrid:
         b = (self.z_own_hi - self.z_store_lo) * plane
         return c[a:b]
 
-    def begin(self, samples, cfg: LossConfig, stream=None, export_grad=False) -> int:
-        """Phase 1; returns the device pointer of the 5 local partial sums."""
+    def begin(self, samples, cfg: LossConfig, stream=None, export_grad=False, n_global: int = 0) -> int:
+        """Phase 1; returns the device pointer of the 5 local partial sums.
+        samples: the full global batch, or only this slab's points
+        (slab_point_mask) with n_global = the global batch size."""
         from . import TGCU_EXPORT_GRAD, _is_torch
         flags = 0 if _is_torch(samples) else TGCU_HOST
         if export_grad:
@@ -175,7 +178,7 @@ class SlabGrid:
         if not _is_torch(samples):
             samples = np.ascontiguousarray(np.asarray(samples, dtype=np.float32)).reshape(-1, 4)
         p = C.POINTER(C.c_double)()
-        _check(lib().tgcu_slab_step_begin(self._h, _ptr(samples), samples.shape[0], C.byref(cfg._c()),
+        _check(lib().tgcu_slab_step_begin(self._h, _ptr(samples), samples.shape[0], int(n_global), C.byref(cfg._c()),
                                           C.byref(p), flags, C.c_void_p(stream) if stream else None))
         return C.cast(p, C.c_void_p).value
 
@@ -261,8 +264,17 @@ class SlabTrainer:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
 
-    def step(self, samples_dev, cfg: LossConfig, stream=None, want_terms=False):
-        part = self.slab.begin(samples_dev, cfg, stream=stream)
+    def local_points(self, samples):
+        """The points of a global batch this rank's slab needs (host numpy):
+        cells touching its owned vertex planes (the reference cell rule)."""
+        lo, hi = self.ranges[self.rank]
+        a = np.asarray(samples)
+        return np.ascontiguousarray(a[slab_point_mask(self.slab.spec, a.astype(np.float64), lo, hi)])
+
+    def step(self, samples_dev, cfg: LossConfig, stream=None, want_terms=False, n_global: int = 0):
+        """One step. samples_dev: the global batch, or this rank's local_points
+        with n_global = the global batch size."""
+        part = self.slab.begin(samples_dev, cfg, stream=stream, n_global=n_global)
         t = device_view(part, 5, "<f8")
         if self._staged():
             import torch

@@ -288,12 +288,14 @@ def test_c2_scale_fused_gradient_vs_oracle(oracle):
 # ---- multi-GPU slab path, two slabs emulated on one device ----------------------------------------
 
 
-@pytest.mark.parametrize("nslab,res", [(2, (24, 20, 40)), (3, (21, 18, 43))])
-def test_slab_two_on_one_gpu_matches_full_grid(nslab, res):
+@pytest.mark.parametrize("nslab,res,sharded", [(2, (24, 20, 40), False), (3, (21, 18, 43), False),
+                                               (3, (21, 18, 43), True)])
+def test_slab_two_on_one_gpu_matches_full_grid(nslab, res, sharded):
     """z-slab grids driven like ranks (sum of partials, commit, halo exchange
     by device copies) reproduce the single-grid fused trajectory; with three
-    slabs the middle one exchanges both halo planes."""
-    from paper_2402_14415_b200.slab import SlabGrid, brick_layers, device_view, slab_ranges
+    slabs the middle one exchanges both halo planes; sharded: each slab reads
+    only its own points (slab_point_mask) with the global batch size."""
+    from paper_2402_14415_b200.slab import SlabGrid, brick_layers, device_view, slab_point_mask, slab_ranges
     spec = tg.GridSpec(dim=3, resolution=res, order=2)
     init = tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.02, seed=3)
     cfg = tg.LossConfig()
@@ -311,7 +313,11 @@ def test_slab_two_on_one_gpu_matches_full_grid(nslab, res):
     for step in range(6):
         b = tg.sample(tg.SHAPE_SPHERE, 3, 500 + step, 20000, near_frac=0.5, sigma=0.01, param0=0.6)
         tf = tg.train_step(full, b, cfg).as_array()
-        parts = [sg.begin(b, cfg) for sg in slabs]
+        if sharded:
+            parts = [sg.begin(np.ascontiguousarray(b[slab_point_mask(spec, b.astype(np.float64), *rg)]), cfg,
+                              n_global=len(b)) for sg, rg in zip(slabs, ranges)]
+        else:
+            parts = [sg.begin(b, cfg) for sg in slabs]
         views = [device_view(p, 5, "<f8") for p in parts]
         tot = views[0].clone()
         for v in views[1:]:
