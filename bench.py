@@ -138,6 +138,38 @@ def max_over_ranks(x, ws):
     return float(t.item())
 
 
+def make_stacked_batches(ws, seed0, n=NPTS, count=NBATCH):
+    """Weak scaling: N copies of the C2 problem stacked along z, one per rank's
+    slab of 128 vertex planes (C2 spacing h = 2/127). Slab r's points are a C2
+    batch (50 % uniform, 50 % near its sphere of radius 0.6) shifted by
+    128 r h, its uniform half stretched over the slab's full thickness so the
+    shared boundary cell layers get points; gt = the exact distance to the
+    union of the spheres (nearest of slabs r-1, r, r+1), from the fp32
+    coordinates."""
+    import numpy as np
+    import paper_2402_14415_b200 as tg
+    h = 2.0 / (RES[2] - 1)
+    th = RES[2] * h
+    n_uni = n - int(np.floor(n * 0.5))
+    out = []
+    for i in range(count):
+        parts = []
+        for r in range(ws):
+            b = tg.sample(tg.SHAPE_SPHERE, 3, seed0 + 7919 * r + i, n, near_frac=0.5, sigma=0.01,
+                          param0=0.6).astype(np.float64)
+            b[:n_uni, 2] = -1.0 + (b[:n_uni, 2] + 1.0) * (th / 2.0)
+            b[:, 2] += 128 * r * h
+            p = b[:, :3].astype(np.float32).astype(np.float64)
+            gt = np.full(n, np.inf)
+            for k in (r - 1, r, r + 1):
+                if 0 <= k < ws:
+                    c = np.array([0.0, 0.0, 128 * k * h])
+                    gt = np.minimum(gt, np.linalg.norm(p - c, axis=1) - 0.6)
+            parts.append(np.concatenate([p, gt[:, None]], 1).astype(np.float32))
+        out.append(np.ascontiguousarray(np.concatenate(parts)))
+    return out
+
+
 def make_batches(seed0, n=NPTS, count=NBATCH):
     import paper_2402_14415_b200 as tg
     return [tg.sample(tg.SHAPE_SPHERE, 3, seed0 + i, n, near_frac=0.5, sigma=0.01, param0=0.6) for i in range(count)]
@@ -181,21 +213,28 @@ def run_reference(args):
         return
     import paper_2402_14415_b200 as tg  # host sampler only (same inputs as our arm)
     R = Reference()
-    threads = max(1, min(os.cpu_count() or 1, 64))
-    s = Spec(dim=3, res=RES, order=ORDER)
-    batches = [b.astype(np.float64) for b in make_batches(1000, count=2)]
+    # our arm's config: C2 (N = 1) or N stacked C2 slabs (weak scaling, N > 1)
+    res = (RES[0], RES[1], RES[2] * ws)
+    s = Spec(dim=3, res=res, order=ORDER, extent=(2.0, 2.0, (res[2] - 1) * 2.0 / (RES[2] - 1)))
+    npts = NPTS * ws
+    # the reference keeps a dense fp64 gradient copy per thread: cap threads at ~16 GB of copies
+    threads = max(1, min(os.cpu_count() or 1, 64, int(16e9 // (8 * s.V * s.K))))
+    batches = [b.astype(np.float64) for b in
+               (make_batches(1000, count=2) if ws == 1 else make_stacked_batches(ws, 1000, count=2))]
     # warm-up + probe one step, then a bounded number of timed steps (~60 s of CPU work)
     _, _, t1 = R.train(s, np.zeros(s.V * s.K), np.array(batches[:1]), Loss(), lr=LR, threads=threads)
     steps = int(max(1, min(args.steps, 60.0 // max(t1, 1e-3))))
     seq = np.array([batches[i % len(batches)] for i in range(steps)])
     _, terms, secs = R.train(s, np.zeros(s.V * s.K), seq, Loss(), lr=LR, threads=threads)
-    v = steps * NPTS / secs
-    sample = f"{steps} full C2 steps ({steps * NPTS} points), threads={threads} (bounded sample of --steps {args.steps})"
+    v = steps * npts / secs
+    sample = (f"{steps} full steps of the arm's config ({steps * npts} points), threads={threads} "
+              f"(bounded sample of --steps {args.steps})")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "points/s", "n_gpus": args.gpus,
         "steps": steps, "warmup": 1, "ms_per_step": 1e3 * secs / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded sphere samples)",
-        "config": {"workload": WORKLOAD, "grid": list(RES), "order": ORDER, "points_per_step": NPTS},
+        "config": {"workload": WORKLOAD if ws == 1 else f"C2 per GPU, {ws} C2 slabs stacked in z; " + WORKLOAD,
+                   "grid": list(res), "order": ORDER, "points_per_step": npts},
         "cpu_baseline": {"value": v, "unit": "points/s", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "loss_last": float(terms[-1, 0]),
@@ -303,11 +342,16 @@ def main():
     dev = local
     hbm_peak, peak_src = peaks()
 
-    spec = tg.GridSpec(dim=3, resolution=RES, order=ORDER)
+    # N = 1: C2. N > 1: weak scaling, N C2 slabs stacked in z (make_stacked_batches).
+    res = (RES[0], RES[1], RES[2] * ws)
+    spec = tg.GridSpec(dim=3, resolution=res, order=ORDER,
+                       extent=(2.0, 2.0, (res[2] - 1) * 2.0 / (RES[2] - 1)))
     K = spec.coeffs_per_vertex()
     VK = spec.coeff_total()
     cfg = tg.LossConfig()  # paper defaults
-    host_batches = make_batches(1000)  # every rank sees the same global batches
+    npts_global = NPTS * ws
+    # every rank builds the same seeded global batches
+    host_batches = make_batches(1000) if ws == 1 else make_stacked_batches(ws, 1000)
     dev_batches = [torch.from_numpy(b).to(f"cuda:{dev}") for b in host_batches]
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
@@ -318,8 +362,8 @@ def main():
         def step(batch, asynchronous=True):
             return tg.train_step(g, batch, cfg, asynchronous=asynchronous, stream=None if not asynchronous else sp)
     else:
-        # strong scaling: the C2 grid cut into z-slabs of brick layers, one per
-        # rank (owner computes; NCCL all-reduce of loss partials + halo planes)
+        # weak scaling: rank r owns the r-th stacked C2 slab (16 brick layers;
+        # owner computes; NCCL all-reduce of loss partials + halo planes)
         from paper_2402_14415_b200.slab import SlabTrainer
         trainer = SlabTrainer(spec, rank, ws, tg.AdamConfig(lr=LR), device=dev)
         g = trainer.slab
@@ -332,7 +376,7 @@ def main():
         host_batches = local_host
 
         def step(batch, asynchronous=True):
-            return trainer.step(batch, cfg, stream=sp, want_terms=not asynchronous, n_global=NPTS)
+            return trainer.step(batch, cfg, stream=sp, want_terms=not asynchronous, n_global=npts_global)
 
     for i in range(args.warmup):
         step(dev_batches[i % NBATCH])
@@ -385,23 +429,27 @@ def main():
             q = query_leg(dev, hbm_peak)
 
     clk = clocks.summary()
-    value = NPTS * args.steps / (ms_total * 1e-3)  # whole job: one global batch per step
+    value = npts_global * args.steps / (ms_total * 1e-3)  # whole job: one global batch per step
     kern_ms = brick_ms / max(brick_n, 1)
     if ws == 1:
         vk_local, pts_local = VK, NPTS
-    else:  # this rank's kernel: its owned vertex planes, ~1/N of the points
+    else:  # this rank's kernel: its owned vertex planes and its local points
         vk_local = (g.z_own_hi - g.z_own_lo) * RES[0] * RES[1] * K
-        pts_local = NPTS // ws
+        pts_local = int(sum(b.shape[0] for b in host_batches) / len(host_batches))
     kern_bytes = 24 * vk_local + 16 * pts_local  # p r+w, m r+w, v r+w (fp32) + each point once
     achieved = kern_bytes / (kern_ms * 1e-3) / 1e9
-    survey_bytes = NPTS * 16 + 3 * VK * 4 + 32 * VK  # SURVEY 8d B_t with U ~= V (unfused accounting)
+    survey_bytes = npts_global * 16 + 3 * VK * 4 + 32 * VK  # SURVEY 8d B_t with U ~= V (unfused accounting)
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: seeded sphere samples (reference Rng mappings), 4 distinct batches cycled",
-        "config": {"workload": WORKLOAD, "grid": list(RES), "order": ORDER, "points_per_step": NPTS,
-                   "parallelism": f"z-slab x{ws} (owner computes, NCCL halo)" if ws > 1 else "single GPU",
+        "config": {"workload": WORKLOAD if ws == 1 else
+                   (f"C2 per GPU, weak scaling: {ws} C2 slabs stacked in z (grid 128x128x{128 * ws}, "
+                    f"{ws} x 2^20 points/step, sphere per slab, owner-sharded batch); " + WORKLOAD),
+                   "grid": list(res), "order": ORDER, "points_per_step": npts_global,
+                   "parallelism": f"z-slab x{ws} (owner computes, NCCL all-reduce + halo planes)" if ws > 1
+                   else "single GPU",
                    "l2": "no flush: every step streams p,m,v (503 MB) + points, > 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": "k_brick_step<3,2,true> (fused loss+backward+TV+Adam)",
                      "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
@@ -411,7 +459,7 @@ def main():
                                               + ("" if ws == 1 else " (rank 0's owned slab, N/ranks points)"),
                      "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_step,
                      "step_frac_survey_bytes": survey_bytes / (ms_step * 1e-3) / 1e9 / hbm_peak},
-        "e2e": {"value": NPTS * ne / e2e_s, "unit": "points/s",
+        "e2e": {"value": npts_global * ne / e2e_s, "unit": "points/s",
                 "h2d_bytes_per_step": int(16 * ws * sum(b.shape[0] for b in host_batches) / len(host_batches)),
                 "d2h_bytes_per_step": 32,
                 "api": ("tgcu_train_step(TGCU_HOST|TGCU_ASYNC): pipelined H2D on a copy stream, per-step LossTerms "
