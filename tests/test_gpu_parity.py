@@ -37,8 +37,7 @@ def assert_close(got, ref, rel, floor=1.0, what=""):
     bad = np.abs(got - ref) > tol
     w = int(np.argmax(np.abs(got - ref) / tol))
     assert not bad.any(), (f"{what}: {bad.sum()} / {bad.size} out of tolerance; worst "
-                           f"{np.max(np.abs(got - ref) / tol):.3g}x tol at {w} (channel {w % 10}): "
-                           f"got {got[w]:.6g} ref {ref[w]:.6g} mass {np.asarray(mass).ravel()[w]:.3g}")
+                           f"{np.max(np.abs(got - ref) / tol):.3g}x tol at {w}: got {got[w]:.8g} ref {ref[w]:.8g}")
 
 
 def grad_close(got, ref, mass, rel=1e-5, mass_rel=4e-6, what="grad"):
@@ -53,7 +52,7 @@ def grad_close(got, ref, mass, rel=1e-5, mass_rel=4e-6, what="grad"):
     bad = np.abs(got - ref) > tol
     w = int(np.argmax(np.abs(got - ref) / tol))
     assert not bad.any(), (f"{what}: {bad.sum()} / {bad.size} out of tolerance; worst "
-                           f"{np.max(np.abs(got - ref) / tol):.3g}x tol at {w} (channel {w % 10}): "
+                           f"{np.max(np.abs(got - ref) / tol):.3g}x tol at index {w}: "
                            f"got {got[w]:.6g} ref {ref[w]:.6g} mass {np.asarray(mass).ravel()[w]:.3g}")
 
 
@@ -465,3 +464,42 @@ def test_empty_and_degenerate_inputs():
     one = np.tile(np.array([[0.125, -0.25, 0.5, 0.1]], np.float32), (4096, 1))
     t = tg.train_step(g, one)
     assert np.isfinite(t.total) and g.adam_t == 1
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("TGCU_RANDOM_CASES", "12"))))
+def test_fused_step_random_configs(oracle, seed):
+    """Seeded random sweep: dimension, order, resolution (2..41 per axis, so
+    single-cell axes and partial bricks), batch size (1..20000, below and
+    above the 512-point chunk), loss switches and learning rate — fused step
+    vs the fp64 oracle (terms, gradient, first Adam update)."""
+    rng = np.random.default_rng(9000 + seed)
+    dim = int(rng.choice([2, 3]))
+    order = int(rng.integers(0, 3))
+    res = tuple(int(r) for r in rng.integers(2, 42, dim)) + ((1,) if dim == 2 else ())
+    n = int(rng.choice([1, 7, 513, int(rng.integers(1, 20001))]))
+    cfg = tg.LossConfig(lambda1=float(rng.choice([0.0, 1e-4, 1e-2])), lambda2=float(rng.choice([0.0, 2e-5, 1e-3])),
+                        k=float(rng.choice([5.0, 50.0])), use_weighting=bool(rng.integers(0, 2)),
+                        use_tv=bool(rng.integers(0, 2)), differentiate_weight=bool(rng.integers(0, 2)))
+    lr = float(rng.choice([1e-3, 1e-2]))
+    s = ospec(dim, res, order)
+    c = (0.2 * rng.standard_normal(s.V * s.K)).astype(np.float32).astype(np.float64)
+    pts = rng.uniform(-1.1, 1.1, (n, 3)).astype(np.float32)
+    if dim == 2:
+        pts[:, 2] = 0.0
+    gt = rng.uniform(-0.5, 0.5, n).astype(np.float32)
+    smp = np.concatenate([pts, gt[:, None]], 1).astype(np.float64)
+    loss = Loss(cfg.lambda1, cfg.lambda2, cfg.k, cfg.use_weighting, cfg.use_tv, cfg.differentiate_weight)
+    gref = np.zeros(s.V * s.K)
+    tref = oracle.total_loss(s, c, smp, loss, gref)
+    mass = oracle.total_loss_mass(s, c, smp, loss)
+    g = tg.init_grid(gspec(dim, res, order))
+    g.coeffs = c
+    g.adam_reset(tg.AdamConfig(lr=lr))
+    t = tg.train_step(g, smp, cfg, export_grad=True)
+    # loss terms 1e-5: a batch of one point gets no averaging, and its eikonal
+    # term (|grad f| - 1)^2 carries the fp32 forward error of grad f directly
+    assert_close(t.as_array(), tref, 1e-5, floor=1e-30, what=f"terms {dim}D o{order} {res} n={n} {cfg}")
+    grad_close(g.grad(), gref, mass, what=f"grad {dim}D o{order} {res} n={n}")
+    p1 = c - lr * gref / (np.abs(gref) + 1e-8)
+    ok = np.abs(gref) > 1e-3 * (np.abs(gref).max() + 1e-30)
+    assert_close(g.coeffs[ok], p1[ok], 1e-6, floor=1.0, what="params after step")
