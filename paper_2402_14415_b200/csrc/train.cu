@@ -593,6 +593,26 @@ __device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, flo
     cp_async_commit();
 }
 
+#ifdef TGCU_PHASE_TIMING
+// Instrumented build only (tools/phase_timing.py): per CTA, thread 0's
+// %globaltimer at the kernel's phase boundaries.
+constexpr int kPhaseSlots = 10;
+__device__ unsigned long long g_phase[32768 * kPhaseSlots];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TGCU_PT(var) \
+    unsigned long long var = 0; \
+    if (threadIdx.x == 0) var = gtimer();
+#define TGCU_PT_SET(var) \
+    if (threadIdx.x == 0) var = gtimer();
+#else
+#define TGCU_PT(var)
+#define TGCU_PT_SET(var)
+#endif
+
 template <int DIM, int ORDER, bool EIK>
 __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __grid_constant__ StepArgs A) {
     using S = BrickShape<DIM>;
@@ -600,7 +620,11 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     constexpr int K = KOf<DIM, ORDER>::value;
     constexpr int B = S::B, T = S::T, CE = S::CE, NT = S::NT, CH = S::CH, REC = L::REC;
     constexpr int NC = 1 << DIM;
-    if (A.st->error) return;
+    // brick index and its point range, loaded together with the error flag
+    const int b = ((int)blockIdx.z * A.nb[1] + (int)blockIdx.y) * A.nb[0] + (int)blockIdx.x;
+    const int err = A.st->error;
+    const int p0 = A.off[b], p1 = A.off[b + 1];
+    if (err) return;
 
     extern __shared__ __align__(128) float smem[];
     float* tile = smem;                           // current parameters + halo
@@ -618,8 +642,11 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     constexpr int NW = NT / 32;
+    TGCU_PT(pt_start)
+#ifdef TGCU_PHASE_TIMING
+    unsigned long long pt_tile = 0, pt_2a = 0, pt_scan = 0, pt_bal = 0, pt_2b = 0, pt_x;
+#endif
     // grid = (nb_x, nb_y, nb_z): brick coordinates without integer division
-    const int b = ((int)blockIdx.z * A.nb[1] + (int)blockIdx.y) * A.nb[0] + (int)blockIdx.x;
     const int o[3] = {(int)blockIdx.x * B, (int)blockIdx.y * B, DIM == 3 ? (A.zb0 + (int)blockIdx.z) * B : 0};
     const int zrel = o[2] - A.s.zoff;  // first owned plane in the stored planes
     const bool tmap = L::TMAP && A.use_tmap;
@@ -680,15 +707,15 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     double recon_sum = 0.0, eik_sum = 0.0, home_pts = 0.0;
     int myv = tid;  // owned vertex of this thread; set per brick by the workload sort
 
-    const int p0 = A.off[b], p1 = A.off[b + 1];
     for (int base = p0; base < p1; base += CH) {
         const int m = min(CH, p1 - base);
         for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
         if (base == p0 && tid < 64) bhist[tid] = 0;
         __syncthreads();
-        // 2a. locate + cell rank (no tile needed), then forward from the tile
-        //     and the fp64 loss chain
-        float rv[REC];
+        // 2a. locate + cell rank, the chunk's counting sort by cell and (first
+        //     chunk) the workload balance need no parameters: they run while
+        //     the tile is still in flight. Then the forward from the tile and
+        //     the fp64 loss chain write each record straight to its cell slot.
         int ec = 0, rank = 0;
         float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
         AxisF ax[DIM];
@@ -706,53 +733,21 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
             rank = atomicAdd(&cnt[ec], 1);
         }
-        if (base == p0) {
-            cp_async_wait<0>();  // own fallback rows (rare: grid-edge bricks)
-            if (warp == 0) mbar_wait(&bars[0], 0);  // one warp waits; the others park at the barrier
-            __syncthreads();
-        }
-        if (tid < m) {
-            bool home = true;
-#pragma unroll
-            for (int a = 0; a < DIM; ++a) home &= tc[a] >= 1;
-            float f = 0.0f, fg[DIM];
-#pragma unroll
-            for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                float cb[K];
-                load_block<K, false>(tile + L::at(tc[0] + (c & 1), tc[1] + ((c >> 1) & 1),
-                                                  DIM == 3 ? tc[2] + ((c >> 2) & 1) : 0),
-                                     cb);
-                blend_corner<DIM, ORDER, EIK>(cb, corner_geom<DIM>(A.s, ax, c), f, fg);
-            }
-            double recon, eik;
-            float u, gv[DIM];
-            point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
-            if (home) {
-                recon_sum += recon;
-                eik_sum += eik;
-                home_pts += 1.0;
-            }
-            // s0/s1 rounded from fp64 (1 - l must not be formed from a rounded l)
-#pragma unroll
-            for (int a = 0; a < DIM; ++a) {
-                rv[a] = ax[a].s0;
-                rv[DIM + a] = ax[a].s1;
-                rv[2 * DIM + 1 + a] = gv[a];
-            }
-            rv[2 * DIM] = u;
-#pragma unroll
-            for (int k2 = 3 * DIM + 1; k2 < REC; ++k2) rv[k2] = 0.0f;
-        }
+#ifdef TGCU_PHASE_TIMING
+        unsigned long long pt_c0 = 0;
+        TGCU_PT_SET(pt_c0)
+#endif
         __syncthreads();
+#ifdef TGCU_PHASE_TIMING
+        const unsigned long long pt_s0 = pt_c0;
+#endif
         block_excl_scan<S::NCELL, NT>(cnt, start, warp_tot);
         __syncthreads();
-        if (tid < m) {  // records land in cell order
-            float2* dst = reinterpret_cast<float2*>(uni + (start[ec] + rank) * REC);
-#pragma unroll
-            for (int k2 = 0; k2 < REC / 2; ++k2) dst[k2] = make_float2(rv[2 * k2], rv[2 * k2 + 1]);
-        }
+#ifdef TGCU_PHASE_TIMING
+        TGCU_PT_SET(pt_x)
+        if (tid == 0) pt_scan += pt_x - pt_s0;
+        const unsigned long long pt_b0 = pt_x;
+#endif
         if (base == p0) {
             // Load balance: sort the owned vertices by their (first-chunk)
             // workload into 64 buckets so a warp's lanes carry similar loads;
@@ -785,11 +780,66 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             }
             __syncthreads();
             perm[bstart[bk] + r2] = v;
+            cp_async_wait<0>();  // own fallback rows (rare: grid-edge bricks)
+            if (warp == 0) mbar_wait(&bars[0], 0);  // one warp waits for the tile; the others park here
             __syncthreads();
             myv = perm[tid];
-        } else {
-            __syncthreads();
+#ifdef TGCU_PHASE_TIMING
+            TGCU_PT_SET(pt_tile)
+#endif
         }
+#ifdef TGCU_PHASE_TIMING
+        TGCU_PT_SET(pt_x)
+        if (tid == 0) pt_bal += pt_x - pt_b0;
+        const unsigned long long pt_f0 = pt_x;
+#endif
+        if (tid < m) {
+            bool home = true;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) home &= tc[a] >= 1;
+            float f = 0.0f, fg[DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                float cb[K];
+                load_block<K, false>(tile + L::at(tc[0] + (c & 1), tc[1] + ((c >> 1) & 1),
+                                                  DIM == 3 ? tc[2] + ((c >> 2) & 1) : 0),
+                                     cb);
+                blend_corner<DIM, ORDER, EIK>(cb, corner_geom<DIM>(A.s, ax, c), f, fg);
+            }
+            double recon, eik;
+            float u, gv[DIM];
+            point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
+            if (home) {
+                recon_sum += recon;
+                eik_sum += eik;
+                home_pts += 1.0;
+            }
+            // record: s0/s1 rounded from fp64 (1 - l must not be formed from a
+            // rounded l), u, g; lands in cell order
+            float rv[REC];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                rv[a] = ax[a].s0;
+                rv[DIM + a] = ax[a].s1;
+                rv[2 * DIM + 1 + a] = gv[a];
+            }
+            rv[2 * DIM] = u;
+#pragma unroll
+            for (int k2 = 3 * DIM + 1; k2 < REC; ++k2) rv[k2] = 0.0f;
+            float2* dst = reinterpret_cast<float2*>(uni + (start[ec] + rank) * REC);
+#pragma unroll
+            for (int k2 = 0; k2 < REC / 2; ++k2) dst[k2] = make_float2(rv[2 * k2], rv[2 * k2 + 1]);
+        }
+        __syncthreads();  // records visible
+#ifdef TGCU_PHASE_TIMING
+        TGCU_PT_SET(pt_x)
+        if (tid == 0) pt_2a += pt_x - pt_f0;
+#endif
+#ifdef TGCU_PHASE_TIMING
+        const unsigned long long pt_g0 = pt_x;
+#endif
         // 2b. this thread's vertex gathers the points of its 2^D incident
         //     cells, as one flattened loop over (corner, point)
         {
@@ -857,7 +907,12 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             }
         }
         __syncthreads();
+#ifdef TGCU_PHASE_TIMING
+        TGCU_PT_SET(pt_x)
+        if (tid == 0) pt_2b += pt_x - pt_g0;
+#endif
     }
+    TGCU_PT(pt_epi)
 
     // ---- 3. TV + Adam, thread per vertex; results staged in place ----
     float* Gs = uni;
@@ -1012,6 +1067,21 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             A.partials[4 * b + tid] = acc;
         }
     }
+#ifdef TGCU_PHASE_TIMING
+    if (tid == 0) {
+        unsigned long long* ph = g_phase + (unsigned long long)b * kPhaseSlots;
+        ph[0] = pt_start;
+        ph[1] = pt_tile;
+        ph[2] = pt_2a;
+        ph[3] = pt_scan;
+        ph[4] = pt_bal;
+        ph[5] = pt_2b;
+        ph[6] = pt_epi;
+        ph[7] = gtimer();
+        ph[8] = (unsigned long long)(p1 - p0);
+        ph[9] = 0;
+    }
+#endif
     // (a last-CTA finalize here, behind a per-CTA fence + ticket, measured
     //  15 us slower per C2 step than the separate 1-CTA finalize launch)
     // the CTA's shared memory must outlive the TMA stores' reads
@@ -1233,3 +1303,12 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
 }
 
 }  // namespace tgcu
+
+#ifdef TGCU_PHASE_TIMING
+extern "C" int tgcu_phase_dump(unsigned long long* out, int ncta) {
+    return cudaMemcpyFromSymbol(out, tgcu::g_phase, sizeof(unsigned long long) * ncta * tgcu::kPhaseSlots) ==
+                   cudaSuccess
+               ? 0
+               : 6;
+}
+#endif
