@@ -613,7 +613,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TGCU_PT_SET(var)
 #endif
 
-template <int DIM, int ORDER, bool EIK>
+template <int DIM, int ORDER, bool EIK, bool EXPORT>
 __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __grid_constant__ StepArgs A) {
     using S = BrickShape<DIM>;
     using L = BrickSmem<DIM, ORDER>;
@@ -952,8 +952,9 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                 const float2 b1 = make_float2(A.b1, A.b1), b2 = make_float2(A.b2, A.b2);
                 const float2 cc1 = make_float2(c1, c1), cc2 = make_float2(c2, c2);
                 float2 sq2 = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int q = 0; q < K; q += 2) {
+                // TV gradient + point gradient of channel pair q (the TV sum
+                // accumulates into *sq when given)
+                auto grad_pair = [&](int q, float2* sq) -> float2 {
                     const float2 pv = *reinterpret_cast<const float2*>(tp + q);
                     const float2 npv = make_float2(-pv.x, -pv.y);
                     float2 gt = make_float2(0.f, 0.f);
@@ -961,7 +962,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                     for (int a = 0; a < DIM; ++a) {
                         if (hi[a]) {  // pair (v, v+e_a): TV sum and -d
                             const float2 d = __fadd2_rn(*reinterpret_cast<const float2*>(tp + offs[a] + q), npv);
-                            sq2 = __ffma2_rn(d, d, sq2);
+                            if (sq) *sq = __ffma2_rn(d, d, *sq);
                             gt = __fadd2_rn(gt, make_float2(-d.x, -d.y));
                         }
                         if (lo[a]) {  // pair (v-e_a, v): +(pv - p_lo)
@@ -969,10 +970,19 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                             gt = __fadd2_rn(gt, __fadd2_rn(pv, make_float2(-pl.x, -pl.y)));
                         }
                     }
-                    const float2 gi = __ffma2_rn(gsc, gt, *reinterpret_cast<const float2*>(gs + q));
-                    if (A.grad_out) *reinterpret_cast<float2*>(A.grad_out + gidx + q) = gi;
-                    if (!isfinite(gi.x)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
-                    if (!isfinite(gi.y)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q + 1));
+                    return __ffma2_rn(gsc, gt, *reinterpret_cast<const float2*>(gs + q));
+                };
+                // one finiteness test per vertex (a NaN / inf in any channel
+                // makes the sum non-finite); the channel scan runs only then
+                float2 gsum = make_float2(0.f, 0.f);
+                float2 gkeep[K / 2];
+#pragma unroll
+                for (int q = 0; q < K; q += 2) {
+                    const float2 pv = *reinterpret_cast<const float2*>(tp + q);
+                    const float2 gi = grad_pair(q, &sq2);
+                    gkeep[q / 2] = gi;
+                    gsum = __fadd2_rn(gsum, gi);
+                    if constexpr (EXPORT) *reinterpret_cast<float2*>(A.grad_out + gidx + q) = gi;
                     // Adam (adam.cpp:36-55), fp32 state, host fp64 bias corrections
                     const float2 mn = __ffma2_rn(b1, *reinterpret_cast<const float2*>(mm + q), __fmul2_rn(cc1, gi));
                     const float2 vn = __ffma2_rn(b2, *reinterpret_cast<const float2*>(vv + q),
@@ -982,6 +992,14 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                     const float2 stp = make_float2(lr_bc1 * mn.x * fast_rcp(fast_sqrt(vn.x * A.inv_bc2) + A.eps),
                                                    lr_bc1 * mn.y * fast_rcp(fast_sqrt(vn.y * A.inv_bc2) + A.eps));
                     *reinterpret_cast<float2*>(gs + q) = __fadd2_rn(pv, make_float2(-stp.x, -stp.y));
+                }
+                if (!isfinite(gsum.x + gsum.y)) {  // rare: name the first bad channel
+#pragma unroll
+                    for (int q = 0; q < K; q += 2) {
+                        const float2 gi = gkeep[q / 2];
+                        if (!isfinite(gi.x)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
+                        if (!isfinite(gi.y)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q + 1));
+                    }
                 }
                 tv_sum = (double)(sq2.x + sq2.y);
             } else {
@@ -1000,7 +1018,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                         if (lo[a]) gt += pv - tp[q - offs[a]];
                     }
                     const float gi = fmaf(A.tv_gscale, gt, gs[q]);
-                    if (A.grad_out) A.grad_out[gidx + q] = gi;
+                    if constexpr (EXPORT) A.grad_out[gidx + q] = gi;
                     if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
                     const float mn = fmaf(A.b1, mm[q], c1 * gi);
                     const float vn = fmaf(A.b2, vv[q], c2 * gi * gi);
@@ -1283,13 +1301,13 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
         constexpr size_t smem = BrickSmem<DIM, ORDER>::bytes;
         static_assert(BrickSmem<DIM, ORDER>::bytes <= 227 * 1024, "brick smem");
-        auto kern = eik ? k_brick_step<DIM, ORDER, true> : k_brick_step<DIM, ORDER, false>;
+        auto kern = grad_out ? (eik ? k_brick_step<DIM, ORDER, true, true> : k_brick_step<DIM, ORDER, false, true>)
+                             : (eik ? k_brick_step<DIM, ORDER, true, false> : k_brick_step<DIM, ORDER, false, false>);
         static bool configured = false;
         if (!configured) {
-            TGCU_CUDA(cudaFuncSetAttribute(k_brick_step<DIM, ORDER, true>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            TGCU_CUDA(cudaFuncSetAttribute(k_brick_step<DIM, ORDER, false>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            for (auto k : {k_brick_step<DIM, ORDER, true, true>, k_brick_step<DIM, ORDER, false, true>,
+                           k_brick_step<DIM, ORDER, true, false>, k_brick_step<DIM, ORDER, false, false>})
+                TGCU_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             configured = true;
         }
         if (g.prof_on) prof_mark(g, s, 0);
