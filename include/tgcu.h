@@ -236,6 +236,10 @@ int tgcu_trace(tgcu_grid* g, tgcu_loss_terms* out, int count);
 /* Live timing of the fused brick kernel: CUDA events recorded on the launch
  * stream around every k_brick_step launch between begin and end; end returns
  * the summed device milliseconds and the number of timed launches. */
+/* Diagnostics: enable = 1 starts recording events at the boundaries of each
+ * fused step (synchronising after each step); enable = 0 stops and returns the
+ * mean ms of {brick histogram, column pass, scatter, brick kernel, finalize}. */
+int tgcu_step_breakdown(tgcu_grid* g, int enable, double* mean_ms5, int* steps);
 int tgcu_profile_begin(tgcu_grid* g);
 int tgcu_profile_end(tgcu_grid* g, double* total_ms, int* launches);
 

@@ -38,6 +38,21 @@ void prof_mark(Grid& g, cudaStream_t s, int which) {
     TGCU_CUDA(cudaEventRecord(g.prof_ev[g.prof_used++], s));
 }
 
+void bd_mark(Grid& g, cudaStream_t s, int i) {
+    if (!g.bd_ev[i]) TGCU_CUDA(cudaEventCreate(&g.bd_ev[i]));
+    TGCU_CUDA(cudaEventRecord(g.bd_ev[i], s));
+}
+
+void bd_collect(Grid& g) {
+    TGCU_CUDA(cudaEventSynchronize(g.bd_ev[5]));
+    for (int i = 0; i < 5; ++i) {
+        float ms = 0.f;
+        TGCU_CUDA(cudaEventElapsedTime(&ms, g.bd_ev[i], g.bd_ev[i + 1]));
+        g.bd_sum[i] += ms;
+    }
+    ++g.bd_steps;
+}
+
 void ensure_staging(Grid& g, int64_t floats) {
     if (g.staging_cap >= floats) return;
     if (g.staging) TGCU_CUDA(cudaFree(g.staging));
@@ -914,6 +929,22 @@ int tgcu_profile_begin(tgcu_grid* h) {
     return guard([&] {
         h->g.prof_on = true;
         h->g.prof_used = 0;
+    });
+}
+
+int tgcu_step_breakdown(tgcu_grid* h, int enable, double* mean_ms5, int* steps) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        if (enable) {
+            g.bd_on = true;
+            for (double& x : g.bd_sum) x = 0.0;
+            g.bd_steps = 0;
+            return;
+        }
+        g.bd_on = false;
+        for (int i = 0; i < 5; ++i) mean_ms5[i] = g.bd_steps ? g.bd_sum[i] / g.bd_steps : 0.0;
+        if (steps) *steps = g.bd_steps;
     });
 }
 

@@ -144,9 +144,17 @@ struct Grid {
     bool prof_on = false;
     std::vector<cudaEvent_t> prof_ev;  // pairs (start, end)
     size_t prof_used = 0;
+    // Step breakdown (tgcu_step_breakdown, diagnostics): events at the
+    // boundaries of one fused step, summed per segment after each step.
+    bool bd_on = false;
+    cudaEvent_t bd_ev[6] = {};
+    double bd_sum[5] = {0, 0, 0, 0, 0};
+    int bd_steps = 0;
 };
 
 void prof_mark(Grid& g, cudaStream_t s, int which);
+void bd_mark(Grid& g, cudaStream_t s, int i);  // step breakdown boundary i (0..5)
+void bd_collect(Grid& g);                       // after a step: add its segment times
 
 constexpr int kTraceCap = 4096;
 

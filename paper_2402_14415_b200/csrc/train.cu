@@ -1202,6 +1202,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     B.st = g.st;
     B.zb0 = g.zb0;
     const int ncta_tiles = (int)((n + kBinTile - 1) / kBinTile);
+    if (g.bd_on) bd_mark(g, s, 0);
     if (g.NB <= kBinSmemMax && ncta_tiles <= kMaxBinTiles) {
         const int ncta = ncta_tiles;
         ensure_bin_hist(g, (int64_t)ncta * g.NB, n, (g.NB + kColBricks - 1) / kColBricks);
@@ -1219,9 +1220,11 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         }
         if (g.spec.dim == 3) k_bin_hist<3><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_codes, (int)g.NB);
         else k_bin_hist<2><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_codes, (int)g.NB);
+        if (g.bd_on) bd_mark(g, s, 1);
         const int epoch = ++g.bin_epoch;
         k_bin_cols<<<(unsigned)((g.NB + kColBricks - 1) / kColBricks), 256, csm, s>>>(
             g.bin_hist, ncta, (int)g.NB, g.bin_off, g.bin_chain, epoch, g.st);
+        if (g.bd_on) bd_mark(g, s, 2);
         if (g.spec.dim == 3)
             k_bin_scatter_tiles<3><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_codes, g.bin_off, (int)g.NB);
         else
@@ -1311,13 +1314,19 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
             configured = true;
         }
         if (g.prof_on) prof_mark(g, s, 0);
+        if (g.bd_on) bd_mark(g, s, 3);
         kern<<<bgrid, BrickShape<DIM>::NT, smem, s>>>(A);
+        if (g.bd_on) bd_mark(g, s, 4);
         if (g.prof_on) prof_mark(g, s, 1);
     });
 
     k_step_finalize<<<1, 1024, 0, s>>>(F);
     count_launch(2);
     TGCU_CUDA(cudaGetLastError());
+    if (g.bd_on) {
+        bd_mark(g, s, 5);
+        bd_collect(g);
+    }
 }
 
 }  // namespace tgcu
