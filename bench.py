@@ -360,7 +360,10 @@ def main():
         g.adam_reset(tg.AdamConfig(lr=LR))
 
         def step(batch, asynchronous=True):
-            return tg.train_step(g, batch, cfg, asynchronous=asynchronous, stream=None if not asynchronous else sp)
+            # device batches are uploaded and synchronized before use: input_ready
+            # lets each step's binning overlap the previous brick kernel
+            return tg.train_step(g, batch, cfg, asynchronous=asynchronous, stream=None if not asynchronous else sp,
+                                 input_ready=True)
     else:
         # weak scaling: rank r owns the r-th stacked C2 slab (16 brick layers;
         # owner computes; NCCL all-reduce of loss partials + halo planes)
@@ -376,7 +379,8 @@ def main():
         host_batches = local_host
 
         def step(batch, asynchronous=True):
-            return trainer.step(batch, cfg, stream=sp, want_terms=not asynchronous, n_global=npts_global)
+            return trainer.step(batch, cfg, stream=sp, want_terms=not asynchronous, n_global=npts_global,
+                                input_ready=True)
 
     for i in range(args.warmup):
         step(dev_batches[i % NBATCH])

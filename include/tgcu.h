@@ -44,8 +44,12 @@ enum {
     TGCU_HOST = 1,   /* point / value pointers are host memory */
     TGCU_ASYNC = 2,  /* do not synchronize; errors become sticky */
     TGCU_SORTED = 4,      /* eval: points are sorted by tgcu_sort_points (brick-binned query) */
-    TGCU_EXPORT_GRAD = 8  /* train_step: also write the full gradient to the grid grad buffer
+    TGCU_EXPORT_GRAD = 8, /* train_step: also write the full gradient to the grid grad buffer
                              (validation mode; the fused path otherwise never stores it) */
+    TGCU_INPUT_READY = 16 /* train_step / slab_step_begin with device samples: the caller
+                             guarantees the samples are complete (no pending writes on any
+                             stream), so the step's point binning need not wait for earlier
+                             work on `stream` and overlaps the previous step's brick kernel */
 };
 
 /* tg::GridSpec (grid_spec.hpp:19-24). */
@@ -189,7 +193,11 @@ int tgcu_adam_download_f64(tgcu_grid* g, double* m, double* v, int64_t n);
  * TGCU_HOST | TGCU_ASYNC with out == NULL pipelines host input: the samples are
  * copied on an internal copy stream into one of two device slots while the
  * previous step computes, and the step's LossTerms are copied back to pinned
- * host memory; the host array must stay valid until tgcu_sync(). */
+ * host memory; the host array must stay valid until tgcu_sync().
+ * Point binning runs on an internal stream into one of two bin sets, so the
+ * binning of step i+1 overlaps step i's brick kernel when its input is known
+ * complete (pipelined host input, or TGCU_INPUT_READY); otherwise it is
+ * ordered after all earlier work on `stream`. */
 int tgcu_train_step(tgcu_grid* g, const float* samples, int64_t n, const tgcu_loss_config* cfg,
                     tgcu_loss_terms* out, int flags, void* stream);
 /* ---- multi-GPU z-slab training (owner computes) ----

@@ -57,7 +57,7 @@ class CudaError(RuntimeError):
 
 _ERR = {1: ValueError, 2: ConfigError, 3: IngestError, 4: NumericalError, 5: ResourceError, 6: CudaError}
 
-TGCU_HOST, TGCU_ASYNC, TGCU_SORTED, TGCU_EXPORT_GRAD = 1, 2, 4, 8
+TGCU_HOST, TGCU_ASYNC, TGCU_SORTED, TGCU_EXPORT_GRAD, TGCU_INPUT_READY = 1, 2, 4, 8, 16
 
 # ---- C structs ----------------------------------------------------------------
 
@@ -289,6 +289,18 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
+def _dev_f32(t, cols: int, what: str):
+    """A device tensor passed straight to the C ABI: contiguous fp32 CUDA (n, cols)."""
+    import torch
+    if t.dtype != torch.float32:
+        raise TypeError(f"{what}: device array must be float32, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{what}: torch tensor must live on a CUDA device")
+    if t.dim() != 2 or t.shape[1] != cols or not t.is_contiguous():
+        raise ValueError(f"{what}: expected a contiguous (n, {cols}) tensor, got shape {tuple(t.shape)}")
+    return t
+
+
 def _ptr(x):
     if x is None:
         return None
@@ -446,6 +458,7 @@ def _eval(grid, points, want_grad, sorted_points):
     flags = TGCU_SORTED if sorted_points else 0
     if _is_torch(points):
         import torch
+        _dev_f32(points, 3, "eval")
         n = points.shape[0]
         vals = torch.empty(n, dtype=torch.float32, device=points.device)
         grads = torch.empty((n, 3), dtype=torch.float32, device=points.device) if want_grad else None
@@ -468,6 +481,7 @@ def sort_points(grid: TaylorGrid, points_dev, out_dev, perm_dev=None, offsets_de
     """Brick/Morton sort of device query points for the brick-binned query.
     offsets_dev: optional int64 CUDA tensor of query_brick_codes(grid)+1 entries."""
     import torch
+    _dev_f32(points_dev, 3, "sort_points")
     _check(lib().tgcu_sort_points(grid.handle, _ptr(points_dev), points_dev.shape[0], _ptr(out_dev),
                                   _ptr(perm_dev), _ptr(offsets_dev),
                                   C.c_void_p(torch.cuda.current_stream().cuda_stream)))
@@ -548,7 +562,7 @@ def tv_loss(grid: TaylorGrid, with_grad: bool = False, scale: float = 1.0) -> fl
 
 def _samples(samples):
     if _is_torch(samples):
-        return samples, 0
+        return _dev_f32(samples, 4, "samples"), 0
     a = np.ascontiguousarray(np.asarray(samples, dtype=np.float32)).reshape(-1, 4)
     return a, TGCU_HOST
 
@@ -571,13 +585,17 @@ def adam_step(grid: TaylorGrid, grad_ptr: Optional[int] = None):
 
 
 def train_step(grid: TaylorGrid, samples, cfg: LossConfig = LossConfig(), asynchronous: bool = False,
-               stream=None, export_grad: bool = False) -> Optional[LossTerms]:
+               stream=None, export_grad: bool = False, input_ready: bool = False) -> Optional[LossTerms]:
     """One fused step: zero grad → total_loss → finite check → adam_step
     (schedule.cpp:66-92). Returns the LossTerms (None when asynchronous).
-    export_grad also stores the full gradient in the grid grad buffer (validation)."""
+    export_grad also stores the full gradient in the grid grad buffer (validation).
+    input_ready (device samples): the caller guarantees the samples are complete,
+    so the step's binning overlaps the previous step's brick kernel."""
     s, flags = _samples(samples)
     if export_grad:
         flags |= TGCU_EXPORT_GRAD
+    if input_ready and not flags & TGCU_HOST:
+        flags |= TGCU_INPUT_READY
     if asynchronous:
         flags |= TGCU_ASYNC
         _check(lib().tgcu_train_step(grid.handle, _ptr(s), s.shape[0], C.byref(cfg._c()), None, flags,

@@ -88,13 +88,23 @@ void ensure_scratch(Grid& g, int64_t doubles) {
     g.scratch_cap = doubles;
 }
 
-void ensure_bins(Grid& g, int64_t points) {
+void ensure_bins(Grid& g, int set, int64_t points) {
     const int64_t need = points << g.spec.dim;  // worst case 2^D copies per point
-    if (g.binned_cap >= need) return;
-    if (g.binned) TGCU_CUDA(cudaFree(g.binned));
-    g.binned = nullptr;
-    TGCU_CUDA(cudaMalloc(&g.binned, sizeof(float4) * need));
-    g.binned_cap = need;
+    if (g.binned_cap[set] >= need) return;
+    if (g.binned[set]) TGCU_CUDA(cudaFree(g.binned[set]));  // (cudaFree waits for the device)
+    g.binned[set] = nullptr;
+    TGCU_CUDA(cudaMalloc(&g.binned[set], sizeof(float4) * need));
+    g.binned_cap[set] = need;
+}
+
+void ensure_bin_stream(Grid& g) {
+    if (g.bstream) return;
+    TGCU_CUDA(cudaStreamCreateWithFlags(&g.bstream, cudaStreamNonBlocking));
+    TGCU_CUDA(cudaEventCreateWithFlags(&g.ev_in, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+        TGCU_CUDA(cudaEventCreateWithFlags(&g.ev_bdone[i], cudaEventDisableTiming));
+        TGCU_CUDA(cudaEventCreateWithFlags(&g.ev_bfree[i], cudaEventDisableTiming));
+    }
 }
 
 void ensure_bin_hist(Grid& g, int64_t ints, int64_t points, int64_t chain_ctas) {
@@ -302,6 +312,7 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         Status st0{};
         st0.nan_point = ULLONG_MAX;
         st0.bad_grad = ULLONG_MAX;
+        st0.nan_bin[0] = st0.nan_bin[1] = ULLONG_MAX;
         TGCU_CUDA(cudaMemcpy(g.st, &st0, sizeof(Status), cudaMemcpyHostToDevice));
         // Brick decomposition (train.cu / query.cu).
         g.NB = 1;
@@ -316,7 +327,7 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         }
         for (int a = 0; a < 3; ++a) g.NB *= g.nb[a];
         TGCU_CUDA(cudaMalloc(&g.bin_count, sizeof(int) * (g.NB + 1)));
-        TGCU_CUDA(cudaMalloc(&g.bin_off, sizeof(int) * (g.NB + 1)));
+        for (int i = 0; i < 2; ++i) TGCU_CUDA(cudaMalloc(&g.bin_off[i], sizeof(int) * (g.NB + 1)));
         TGCU_CUDA(cudaMalloc(&g.bin_cursor, sizeof(int) * (g.NB + 1)));
         TGCU_CUDA(cudaMalloc(&g.partials, sizeof(double) * 4 * g.NB));
         TGCU_CUDA(cudaMalloc(&g.d_trace, sizeof(tgcu_loss_terms) * kTraceCap));
@@ -386,9 +397,15 @@ int tgcu_grid_destroy(tgcu_grid* h) {
     cudaFree(g.st);
     cudaFreeHost(g.st_host);
     cudaFree(g.bin_count);
-    cudaFree(g.bin_off);
     cudaFree(g.bin_cursor);
-    cudaFree(g.binned);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(g.bin_off[i]);
+        cudaFree(g.binned[i]);
+        if (g.ev_bdone[i]) cudaEventDestroy(g.ev_bdone[i]);
+        if (g.ev_bfree[i]) cudaEventDestroy(g.ev_bfree[i]);
+    }
+    if (g.ev_in) cudaEventDestroy(g.ev_in);
+    if (g.bstream) cudaStreamDestroy(g.bstream);
     cudaFree(g.bin_hist);
     cudaFree(g.bin_codes);
     cudaFree(g.bin_chain);
@@ -453,6 +470,7 @@ static void raise_sticky(Grid& g) {
     clean.error_kind = 0;
     clean.nan_point = ULLONG_MAX;
     clean.bad_grad = ULLONG_MAX;
+    clean.nan_bin[0] = clean.nan_bin[1] = ULLONG_MAX;
     TGCU_CUDA(cudaMemcpy(g.st, &clean, sizeof(Status), cudaMemcpyHostToDevice));
     g.steps_launched = 0;
     throw Error(s.error, msg);
@@ -780,21 +798,26 @@ int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
         // Pipelined host input: the copy of this step's samples runs on the
         // copy stream into the free slot while earlier steps compute.
         const bool pipe = (flags & TGCU_HOST) && (flags & TGCU_ASYNC) && out == nullptr;
-        int slot = 0;
+        BinInput bin_in;
+        bin_in.ready = (flags & TGCU_INPUT_READY) != 0;
         if (pipe) {
+            // The copy stream fills the slot, the binning stream reads it; the
+            // caller's stream only sees binned points.
             ensure_pipeline(g, 4 * n);
-            slot = g.pipe_slot;
+            const int slot = g.pipe_slot;
             g.pipe_slot ^= 1;
             TGCU_CUDA(cudaStreamWaitEvent(g.cstream, g.ev_free[slot], 0));
             TGCU_CUDA(cudaMemcpyAsync(g.pstage[slot], samples, sizeof(float) * 4 * n, cudaMemcpyHostToDevice,
                                       g.cstream));
             TGCU_CUDA(cudaEventRecord(g.ev_ready[slot], g.cstream));
-            TGCU_CUDA(cudaStreamWaitEvent(s, g.ev_ready[slot], 0));
+            bin_in.wait = g.ev_ready[slot];
+            bin_in.consumed = g.ev_free[slot];
             ds = reinterpret_cast<const float4*>(g.pstage[slot]);
         } else if (flags & TGCU_HOST) {
             ensure_staging(g, 4 * n);
             TGCU_CUDA(cudaMemcpyAsync(g.staging, samples, sizeof(float) * 4 * n, cudaMemcpyHostToDevice, s));
             ds = reinterpret_cast<const float4*>(g.staging);
+            bin_in.ready = false;  // ordered after the copy on s
         }
         ensure_optimizer(g);
         const int64_t t_after = g.t + 1;
@@ -808,13 +831,12 @@ int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
         }
         require(!g.slab, "train_step: slab grids step with tgcu_slab_step_begin/finish");
         launch_train_step(g, ds, n, n, *cfg, in_idx, g.steps_launched, 1.0 / bc1, 1.0 / bc2, t_after, gout, nullptr,
-                          s);
+                          bin_in, s);
         // Optimistic commit; a failed step is rolled back by raise_sticky().
         g.cur = 1 - in_idx;
         g.t = t_after;
         g.steps_launched += 1;
         if (pipe) {
-            TGCU_CUDA(cudaEventRecord(g.ev_free[slot], s));  // slot consumed (binning read it)
             const int64_t r = (g.steps_launched - 1) % kTraceCap;  // this step's LossTerms -> pinned ring
             TGCU_CUDA(cudaMemcpyAsync(g.h_ring + r, g.d_trace + r, sizeof(tgcu_loss_terms), cudaMemcpyDeviceToHost, s));
         }
@@ -844,10 +866,13 @@ int tgcu_slab_step_begin(tgcu_grid* h, const float* samples, int64_t n, int64_t 
         cudaStream_t s = as_stream(stream);
         ensure_optimizer(g);
         const float4* ds = reinterpret_cast<const float4*>(samples);
+        BinInput bin_in;
+        bin_in.ready = (flags & TGCU_INPUT_READY) != 0;
         if (flags & TGCU_HOST) {
             ensure_staging(g, 4 * n);
             TGCU_CUDA(cudaMemcpyAsync(g.staging, samples, sizeof(float) * 4 * n, cudaMemcpyHostToDevice, s));
             ds = reinterpret_cast<const float4*>(g.staging);
+            bin_in.ready = false;
         }
         const int64_t t_after = g.t + 1;
         const double bc1 = 1.0 - std::pow(g.adam.beta1, (double)t_after);
@@ -865,7 +890,7 @@ int tgcu_slab_step_begin(tgcu_grid* h, const float* samples, int64_t n, int64_t 
         g.slab_n = nn;
         g.slab_cfg = *cfg;
         launch_train_step(g, ds, n, nn, *cfg, g.cur, g.steps_launched, 1.0 / bc1, 1.0 / bc2, t_after, gout,
-                          g.slab_red, s);
+                          g.slab_red, bin_in, s);
         *partials = g.slab_red;
     });
 }

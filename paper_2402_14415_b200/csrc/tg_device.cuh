@@ -44,6 +44,8 @@ struct Status {
     unsigned long long nan_point;   // per-call min NaN point index (ULLONG_MAX = none)
     unsigned long long bad_grad;    // per-step min non-finite grad index
     unsigned long long overflow;    // bin overflow flag
+    unsigned long long nan_bin[2];  // fused step: min NaN sample index found by the
+                                    // binning of bin set k (ULLONG_MAX = none)
 };
 
 // t = x / h correctly rounded via Markstein's final-correction step with a

@@ -103,9 +103,14 @@ struct Grid {
     int brick[3] = {1, 1, 1};
     int nb[3] = {1, 1, 1};
     int64_t NB = 1;
-    int* bin_count = nullptr;   // NB + 1
-    int* bin_off = nullptr;     // NB + 1
-    int* bin_cursor = nullptr;  // NB
+    // Point binning of the fused step. Two bin sets (offsets + binned
+    // points) alternate between steps so the binning of step i+1 can run on
+    // the binning stream while step i's brick kernel still reads set i&1;
+    // the histogram / code / chain scratch is only touched by binning
+    // kernels, which are serial on that stream.
+    int* bin_count = nullptr;   // NB + 1 (fallback binning)
+    int* bin_off[2] = {nullptr, nullptr};  // NB + 1 per set
+    int* bin_cursor = nullptr;  // NB (fallback binning)
     int* bin_hist = nullptr;    // per-tile brick histograms (privatized binning)
     int64_t bin_hist_cap = 0;
     int* bin_codes = nullptr;   // per-point brick code
@@ -113,8 +118,13 @@ struct Grid {
     int* bin_chain = nullptr;   // chained-scan flags/prefixes (2 ints per CTA)
     int64_t bin_chain_cap = 0;
     int bin_epoch = 0;
-    float4* binned = nullptr;
-    int64_t binned_cap = 0;     // points
+    float4* binned[2] = {nullptr, nullptr};
+    int64_t binned_cap[2] = {0, 0};  // points
+    int bin_set = 0;                 // set of the next step
+    int slab_set = 0;                // set of the pending slab step
+    cudaStream_t bstream = nullptr;  // binning stream
+    cudaEvent_t ev_in = nullptr;     // caller stream -> binning stream (input order)
+    cudaEvent_t ev_bdone[2] = {nullptr, nullptr}, ev_bfree[2] = {nullptr, nullptr};
     double* partials = nullptr; // NB * 4
     tgcu_loss_terms* d_trace = nullptr;  // kTraceCap
     tgcu_loss_terms* h_terms = nullptr;  // pinned, 1
@@ -163,7 +173,8 @@ constexpr int kTraceCap = 4096;
 bool encode_grid_map(CUtensorMap* m, const Grid& g, const float* base, unsigned box_x, unsigned box_yz);
 void ensure_staging(Grid& g, int64_t floats);
 void ensure_pipeline(Grid& g, int64_t floats);
-void ensure_bins(Grid& g, int64_t points);
+void ensure_bins(Grid& g, int set, int64_t points);
+void ensure_bin_stream(Grid& g);
 void ensure_bin_hist(Grid& g, int64_t ints, int64_t points, int64_t chain_ctas);
 void ensure_scratch(Grid& g, int64_t doubles);
 void ensure_grad(Grid& g);
@@ -189,11 +200,22 @@ void launch_point_terms(Grid& g, const float4* samples, int64_t n, const tgcu_lo
 void launch_tv(Grid& g, const float* coeffs, float* grad, double gscale, int want_value, cudaStream_t s);
 void launch_adam_check(Grid& g, const float* grad, cudaStream_t s);
 void launch_adam_update(Grid& g, const float* grad, double inv_bc1, double inv_bc2, cudaStream_t s);
-// Fused step: binning + brick kernel + finalize (train.cu).
+// How the binning stream orders its reads of a step's samples:
+//  wait     - an event marking the samples complete (pipelined host copy), or
+//  ready    - the caller asserts the samples are complete (TGCU_INPUT_READY),
+//  neither  - after all work issued so far on the caller's stream.
+// consumed (optional) is recorded once binning has read the samples.
+struct BinInput {
+    cudaEvent_t wait = nullptr;
+    bool ready = false;
+    cudaEvent_t consumed = nullptr;
+};
+// Fused step: binning (binning stream) + brick kernel + finalize (caller's
+// stream) (train.cu).
 void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
                        int in_idx,
                        int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
-                       double* slab_out, cudaStream_t s);
+                       double* slab_out, const BinInput& in, cudaStream_t s);
 void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& cfg, int in_idx, int64_t step,
                         int64_t t_after, int64_t n, cudaStream_t s);
 void launch_f64_to_f32(const double* src, float* dst, int64_t n, cudaStream_t s);

@@ -58,7 +58,7 @@ struct BinArgs {
     int* count;
     int* cursor;
     float4* binned;
-    Status* st;
+    unsigned long long* nan;  // the bin set's NaN slot (Status::nan_bin)
     int zb0;  // first brick layer (slab grids)
 };
 
@@ -100,12 +100,11 @@ __device__ __forceinline__ int code_bricks(int code, const int* nb, int zb0, int
 
 template <int DIM>
 __global__ void __launch_bounds__(256) k_bin_count(BinArgs A) {
-    if (A.st->error) return;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < A.n;
          i += (long long)gridDim.x * blockDim.x) {
         const int code = point_brick_code<DIM>(A.s, A.nb, A.pts[i]);
         if (code < 0) {
-            atomicMin(&A.st->nan_point, (unsigned long long)i);
+            atomicMin(A.nan, (unsigned long long)i);
             continue;
         }
         int br[8];
@@ -116,8 +115,7 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs A) {
 
 // Exclusive scan of NB brick counts -> off[0..NB], cursor = off. One CTA.
 __global__ void __launch_bounds__(1024) k_bin_scan(const int* __restrict__ count, int* __restrict__ off,
-                                                   int* __restrict__ cursor, int NB, Status* st) {
-    if (st->error) return;
+                                                   int* __restrict__ cursor, int NB) {
     __shared__ int warp_tot[32];
     __shared__ int carry;
     if (threadIdx.x == 0) carry = 0;
@@ -158,7 +156,6 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const int* __restrict__ count
 
 template <int DIM>
 __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs A) {
-    if (A.st->error) return;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < A.n;
          i += (long long)gridDim.x * blockDim.x) {
         const float4 q = A.pts[i];
@@ -192,7 +189,6 @@ template <int DIM>
 __global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __restrict__ H, int* __restrict__ codes,
                                                           int NB) {
     extern __shared__ int hist[];
-    if (A.st->error) return;
     for (int i = threadIdx.x; i < NB; i += blockDim.x) hist[i] = 0;
     const long long t0 = (long long)blockIdx.x * kBinTile;
     float4 q[kBinPer];
@@ -209,7 +205,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __rest
         const int code = point_brick_code<DIM>(A.s, A.nb, q[k]);
         codes[i] = code;
         if (code < 0) {
-            atomicMin(&A.st->nan_point, (unsigned long long)i);
+            atomicMin(A.nan, (unsigned long long)i);
             continue;
         }
         int br[8];
@@ -226,11 +222,10 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __rest
 // are co-resident; CTA i waits for CTA i-1's inclusive prefix, tagged with
 // this launch's epoch).
 __global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta, int NB, int* __restrict__ off,
-                                                  int* __restrict__ chain, int epoch, Status* st) {
+                                                  int* __restrict__ chain, int epoch) {
     extern __shared__ int col[];  // [ncta][kColBricks + 1]
     __shared__ int tot[kColBricks];
     __shared__ int carry;
-    if (st->error) return;
     const int b0 = blockIdx.x * kColBricks;
     const int nb = min(kColBricks, NB - b0);
     constexpr int LD = kColBricks + 1;
@@ -312,7 +307,6 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_scatter_tiles(BinArgs A, co
                                                                    const int* __restrict__ codes,
                                                                    const int* __restrict__ off, int NB) {
     extern __shared__ int cur[];
-    if (A.st->error) return;
     const int* row = H + (long long)blockIdx.x * NB;
     for (int i = threadIdx.x; i < NB; i += blockDim.x) cur[i] = off[i] + row[i];
     const long long t0 = (long long)blockIdx.x * kBinTile;
@@ -342,6 +336,7 @@ struct FinArgs {
     double lambda1, lambda2, inv_norm;
     int use_tv, want_eik;
     Status* st;
+    unsigned long long* nan;  // NaN slot of the step's bin set
     tgcu_loss_terms* trace;
     long long step;
     int in_idx;
@@ -387,11 +382,12 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
         F.slab_out[0] = recon;
         F.slab_out[1] = eik;
         F.slab_out[2] = tvs;
-        F.slab_out[3] = st->nan_point != ULLONG_MAX ? 1.0 : 0.0;
+        F.slab_out[3] = *F.nan != ULLONG_MAX ? 1.0 : 0.0;
         F.slab_out[4] = st->bad_grad != ULLONG_MAX ? 1.0 : 0.0;
         return;
     }
-    const bool any_nan = st->nan_point != ULLONG_MAX || (F.reduced && F.reduced[3] > 0.0);
+    const unsigned long long nanp = *F.nan;
+    const bool any_nan = nanp != ULLONG_MAX || (F.reduced && F.reduced[3] > 0.0);
     const bool any_bad = st->bad_grad != ULLONG_MAX || (F.reduced && F.reduced[4] > 0.0);
     tgcu_loss_terms t;
     t.fit = recon / F.n;
@@ -404,7 +400,7 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
     if (any_nan) {
         err = TGCU_ERR_INVALID_ARGUMENT;
         kind = 1;
-        idx = st->nan_point != ULLONG_MAX ? (long long)st->nan_point : -1;
+        idx = nanp != ULLONG_MAX ? (long long)nanp : -1;
     } else if (!isfinite(t.total)) {
         err = TGCU_ERR_NUMERICAL;
         kind = 2;
@@ -424,7 +420,7 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
         st->good_idx = 1 - F.in_idx;
         st->good_t = F.t_after;
     }
-    st->nan_point = ULLONG_MAX;
+    *F.nan = ULLONG_MAX;
     st->bad_grad = ULLONG_MAX;
 }
 
@@ -1108,7 +1104,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
 
 // Reduce the per-brick partials in a fixed order, apply the reference's error
 // order (NaN point -> non-finite loss -> non-finite gradient) and commit
-// (slab phase 2; the single-grid step finalizes in its last brick CTA).
+// (after the brick kernel; slab grids: phase 2, with the globally reduced sums).
 __global__ void __launch_bounds__(1024) k_step_finalize(FinArgs F) {
     __shared__ double red[3][32];
     if (F.st->error) return;
@@ -1176,6 +1172,7 @@ void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& 
     F.use_tv = cfg.use_tv;
     F.want_eik = cfg.lambda1 > 0.0;
     F.st = g.st;
+    F.nan = &g.st->nan_bin[g.slab_set];
     F.trace = g.d_trace;
     F.step = step;
     F.in_idx = in_idx;
@@ -1189,8 +1186,24 @@ void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& 
 void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
                        int in_idx,
                        int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
-                       double* slab_out, cudaStream_t s) {
-    ensure_bins(g, n);
+                       double* slab_out, const BinInput& in, cudaStream_t s) {
+    // Binning runs on the binning stream into bin set k; the brick kernel
+    // (caller's stream) waits for it and releases the set when done, so the
+    // binning of the next step overlaps this step's brick kernel whenever its
+    // input order allows (BinInput).
+    ensure_bin_stream(g);
+    const int k = g.bin_set;
+    g.bin_set ^= 1;
+    if (slab_out) g.slab_set = k;
+    ensure_bins(g, k, n);
+    cudaStream_t bs = g.bstream;
+    if (in.wait) {
+        TGCU_CUDA(cudaStreamWaitEvent(bs, in.wait, 0));
+    } else if (!in.ready) {
+        TGCU_CUDA(cudaEventRecord(g.ev_in, s));
+        TGCU_CUDA(cudaStreamWaitEvent(bs, g.ev_in, 0));
+    }
+    TGCU_CUDA(cudaStreamWaitEvent(bs, g.ev_bfree[k], 0));  // brick kernel of step i-2 done with set k
     BinArgs B;
     B.s = g.ds;
     B.pts = samples;
@@ -1198,11 +1211,12 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     for (int a = 0; a < 3; ++a) B.nb[a] = g.nb[a];
     B.count = g.bin_count;
     B.cursor = g.bin_cursor;
-    B.binned = g.binned;
-    B.st = g.st;
+    B.binned = g.binned[k];
+    B.nan = &g.st->nan_bin[k];
     B.zb0 = g.zb0;
+    int* const off = g.bin_off[k];
     const int ncta_tiles = (int)((n + kBinTile - 1) / kBinTile);
-    if (g.bd_on) bd_mark(g, s, 0);
+    if (g.bd_on) bd_mark(g, bs, 0);
     if (g.NB <= kBinSmemMax && ncta_tiles <= kMaxBinTiles) {
         const int ncta = ncta_tiles;
         ensure_bin_hist(g, (int64_t)ncta * g.NB, n, (g.NB + kColBricks - 1) / kColBricks);
@@ -1218,28 +1232,34 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
                                            (int)(sizeof(int) * kMaxBinTiles * (kColBricks + 1))));
             attr = true;
         }
-        if (g.spec.dim == 3) k_bin_hist<3><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_codes, (int)g.NB);
-        else k_bin_hist<2><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_codes, (int)g.NB);
-        if (g.bd_on) bd_mark(g, s, 1);
+        if (g.spec.dim == 3) k_bin_hist<3><<<ncta, kBinThreads, sm, bs>>>(B, g.bin_hist, g.bin_codes, (int)g.NB);
+        else k_bin_hist<2><<<ncta, kBinThreads, sm, bs>>>(B, g.bin_hist, g.bin_codes, (int)g.NB);
+        if (g.bd_on) bd_mark(g, bs, 1);
         const int epoch = ++g.bin_epoch;
-        k_bin_cols<<<(unsigned)((g.NB + kColBricks - 1) / kColBricks), 256, csm, s>>>(
-            g.bin_hist, ncta, (int)g.NB, g.bin_off, g.bin_chain, epoch, g.st);
-        if (g.bd_on) bd_mark(g, s, 2);
+        k_bin_cols<<<(unsigned)((g.NB + kColBricks - 1) / kColBricks), 256, csm, bs>>>(
+            g.bin_hist, ncta, (int)g.NB, off, g.bin_chain, epoch);
+        if (g.bd_on) bd_mark(g, bs, 2);
         if (g.spec.dim == 3)
-            k_bin_scatter_tiles<3><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_codes, g.bin_off, (int)g.NB);
+            k_bin_scatter_tiles<3><<<ncta, kBinThreads, sm, bs>>>(B, g.bin_hist, g.bin_codes, off, (int)g.NB);
         else
-            k_bin_scatter_tiles<2><<<ncta, kBinThreads, sm, s>>>(B, g.bin_hist, g.bin_codes, g.bin_off, (int)g.NB);
+            k_bin_scatter_tiles<2><<<ncta, kBinThreads, sm, bs>>>(B, g.bin_hist, g.bin_codes, off, (int)g.NB);
         count_launch(3);
     } else {
-        TGCU_CUDA(cudaMemsetAsync(g.bin_count, 0, sizeof(int) * g.NB, s));
+        if (g.bd_on) bd_mark(g, bs, 1);
+        TGCU_CUDA(cudaMemsetAsync(g.bin_count, 0, sizeof(int) * g.NB, bs));
         const int pblocks = grid_blocks(n, 256, 148 * 16);
-        if (g.spec.dim == 3) k_bin_count<3><<<pblocks, 256, 0, s>>>(B);
-        else k_bin_count<2><<<pblocks, 256, 0, s>>>(B);
-        k_bin_scan<<<1, 1024, 0, s>>>(g.bin_count, g.bin_off, g.bin_cursor, (int)g.NB, g.st);
-        if (g.spec.dim == 3) k_bin_scatter<3><<<pblocks, 256, 0, s>>>(B);
-        else k_bin_scatter<2><<<pblocks, 256, 0, s>>>(B);
+        if (g.spec.dim == 3) k_bin_count<3><<<pblocks, 256, 0, bs>>>(B);
+        else k_bin_count<2><<<pblocks, 256, 0, bs>>>(B);
+        k_bin_scan<<<1, 1024, 0, bs>>>(g.bin_count, off, g.bin_cursor, (int)g.NB);
+        if (g.bd_on) bd_mark(g, bs, 2);
+        if (g.spec.dim == 3) k_bin_scatter<3><<<pblocks, 256, 0, bs>>>(B);
+        else k_bin_scatter<2><<<pblocks, 256, 0, bs>>>(B);
         count_launch(3);
     }
+    TGCU_CUDA(cudaGetLastError());
+    if (in.consumed) TGCU_CUDA(cudaEventRecord(in.consumed, bs));
+    TGCU_CUDA(cudaEventRecord(g.ev_bdone[k], bs));
+    TGCU_CUDA(cudaStreamWaitEvent(s, g.ev_bdone[k], 0));
 
     StepArgs A{};
     A.s = g.ds;
@@ -1250,8 +1270,8 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     A.m_out = g.m[out_idx];
     A.v_in = g.v[in_idx];
     A.v_out = g.v[out_idx];
-    A.binned = g.binned;
-    A.off = g.bin_off;
+    A.binned = g.binned[k];
+    A.off = off;
     for (int a = 0; a < 3; ++a) A.nb[a] = g.nb[a];
     A.L.k = cfg.k;
     A.L.inv_n = 1.0 / (double)n_norm;  // the global batch size (slab ranks may read a subset)
@@ -1283,6 +1303,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     F.use_tv = cfg.use_tv;
     F.want_eik = eik;
     F.st = g.st;
+    F.nan = &g.st->nan_bin[k];
     F.trace = g.d_trace;
     F.step = step;
     F.in_idx = in_idx;
@@ -1316,6 +1337,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         if (g.prof_on) prof_mark(g, s, 0);
         if (g.bd_on) bd_mark(g, s, 3);
         kern<<<bgrid, BrickShape<DIM>::NT, smem, s>>>(A);
+        TGCU_CUDA(cudaEventRecord(g.ev_bfree[k], s));
         if (g.bd_on) bd_mark(g, s, 4);
         if (g.prof_on) prof_mark(g, s, 1);
     });

@@ -167,14 +167,20 @@ class SlabGrid:
         b = (self.z_own_hi - self.z_store_lo) * plane
         return c[a:b]
 
-    def begin(self, samples, cfg: LossConfig, stream=None, export_grad=False, n_global: int = 0) -> int:
+    def begin(self, samples, cfg: LossConfig, stream=None, export_grad=False, n_global: int = 0,
+              input_ready: bool = False) -> int:
         """Phase 1; returns the device pointer of the 5 local partial sums.
         samples: the full global batch, or only this slab's points
-        (slab_point_mask) with n_global = the global batch size."""
-        from . import TGCU_EXPORT_GRAD, _is_torch
+        (slab_point_mask) with n_global = the global batch size.
+        input_ready: see train_step (device samples known complete)."""
+        from . import TGCU_EXPORT_GRAD, TGCU_INPUT_READY, _dev_f32, _is_torch
         flags = 0 if _is_torch(samples) else TGCU_HOST
+        if flags == 0:
+            _dev_f32(samples, 4, "slab samples")
         if export_grad:
             flags |= TGCU_EXPORT_GRAD
+        if input_ready and not flags & TGCU_HOST:
+            flags |= TGCU_INPUT_READY
         if not _is_torch(samples):
             samples = np.ascontiguousarray(np.asarray(samples, dtype=np.float32)).reshape(-1, 4)
         p = C.POINTER(C.c_double)()
@@ -271,10 +277,11 @@ class SlabTrainer:
         a = np.asarray(samples)
         return np.ascontiguousarray(a[slab_point_mask(self.slab.spec, a.astype(np.float64), lo, hi)])
 
-    def step(self, samples_dev, cfg: LossConfig, stream=None, want_terms=False, n_global: int = 0):
+    def step(self, samples_dev, cfg: LossConfig, stream=None, want_terms=False, n_global: int = 0,
+             input_ready: bool = False):
         """One step. samples_dev: the global batch, or this rank's local_points
         with n_global = the global batch size."""
-        part = self.slab.begin(samples_dev, cfg, stream=stream, n_global=n_global)
+        part = self.slab.begin(samples_dev, cfg, stream=stream, n_global=n_global, input_ready=input_ready)
         t = device_view(part, 5, "<f8")
         if self._staged():
             import torch

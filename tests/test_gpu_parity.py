@@ -31,9 +31,9 @@ def ospec(dim, res, order):
 
 
 def assert_close(got, ref, rel, floor=1.0, what=""):
-    got = np.asarray(got, dtype=np.float64)
-    ref = np.asarray(ref, dtype=np.float64)
-    tol = rel * np.maximum(np.abs(ref), floor)
+    got = np.asarray(got, dtype=np.float64).ravel()
+    ref = np.asarray(ref, dtype=np.float64).ravel()
+    tol = rel * np.maximum(np.abs(ref), np.asarray(floor, dtype=np.float64).ravel())
     bad = np.abs(got - ref) > tol
     w = int(np.argmax(np.abs(got - ref) / tol))
     assert not bad.any(), (f"{what}: {bad.sum()} / {bad.size} out of tolerance; worst "
@@ -255,6 +255,56 @@ def test_nonfinite_loss_aborts_and_keeps_params():
     nan_pt[3, 0] = np.nan
     with pytest.raises(ValueError, match="NaN coordinate"):
         tg.train_step(g, nan_pt)
+
+
+def test_overlapped_binning_trajectory_and_nan_step():
+    """Binning of step i+1 on the binning stream (input_ready device batches,
+    pipelined host batches, mixed with stream-ordered steps) overlaps step i's
+    brick kernel: same trajectory as synchronous steps, and a NaN sample is
+    reported for its own step (per-bin-set NaN slot) with that step's input
+    state kept."""
+    import torch
+    z = load_golden("train.npz")
+    spec = gspec(2, z["train_res"], 2)
+    batches = list(z["train_batches"])
+    g1, g2 = tg.init_grid(spec), tg.init_grid(spec)
+    for g in (g1, g2):
+        g.adam_reset(tg.AdamConfig(lr=1e-2))
+    sync_terms = [tg.train_step(g1, b).as_array() for b in batches]
+    dev = [torch.from_numpy(b.astype(np.float32)).cuda() for b in batches]
+    torch.cuda.synchronize()
+    with pytest.raises(TypeError, match="float32"):
+        tg.train_step(g2, dev[0].double())
+    for i in range(len(batches)):
+        if i % 3 == 0:
+            tg.train_step(g2, dev[i], asynchronous=True, input_ready=True)
+        elif i % 3 == 1:
+            tg.train_step(g2, np.ascontiguousarray(batches[i]), asynchronous=True)  # pipelined host copy
+        else:
+            tg.train_step(g2, dev[i], asynchronous=True)  # ordered after the stream
+    g2.sync()
+    assert_close(g2.trace(len(batches)), np.array(sync_terms), 1e-6, floor=1e-30, what="overlapped trace")
+    assert_trajectory_close(g2.coeffs, g1.coeffs, 1e-2, len(batches), what="overlapped coeffs")
+
+    g3 = tg.init_grid(spec)
+    g3.adam_reset(tg.AdamConfig(lr=1e-2))
+    for b in dev[:2]:
+        tg.train_step(g3, b)
+    ref = g3.coeffs
+    bad = dev[2].clone()
+    bad[5, 1] = float("nan")
+    torch.cuda.synchronize()
+    seq = [bad, dev[3], dev[4], dev[5]]
+    for b in seq:
+        tg.train_step(g3, b, asynchronous=True, input_ready=True)
+    with pytest.raises(ValueError, match=r"NaN coordinate \(sample 5\) at stage 0 step 2"):
+        g3.sync()
+    assert np.array_equal(g3.coeffs, ref) and g3.adam_t == 2
+    # usable again: the remaining steps match a clean grid's
+    for b in dev[3:6]:
+        tg.train_step(g3, b, asynchronous=True, input_ready=True)
+    g3.sync()
+    assert np.all(np.isfinite(g3.coeffs))
 
 
 # ---- BASELINE-size properties --------------------------------------------------------------------
