@@ -592,7 +592,7 @@ __device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, flo
 #ifdef TGCU_PHASE_TIMING
 // Instrumented build only (tools/phase_timing.py): per CTA, thread 0's
 // %globaltimer at the kernel's phase boundaries.
-constexpr int kPhaseSlots = 10;
+constexpr int kPhaseSlots = 12;
 __device__ unsigned long long g_phase[32768 * kPhaseSlots];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -919,6 +919,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     if (p0 == p1 && warp == 0) mbar_wait(&bars[0], 0);  // brick without points: tile not yet waited for
     if (warp == 0) mbar_wait(&bars[1], 0);  // m/v rows landed
     __syncthreads();
+    TGCU_PT(pt_e1)
     double tv_sum = 0.0;
     {
         const int v = tid;
@@ -1027,6 +1028,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         }
     }
     __syncthreads();
+    TGCU_PT(pt_e2)
     // copy-out of the staged results (p from Gs, m and v from mvs): three TMA
     // tensor box stores (out-of-grid vertices dropped), or one bulk store per
     // row and array, issued by one thread each
@@ -1093,7 +1095,9 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         ph[6] = pt_epi;
         ph[7] = gtimer();
         ph[8] = (unsigned long long)(p1 - p0);
-        ph[9] = 0;
+        ph[9] = pt_e1;
+        ph[10] = pt_e2;
+        ph[11] = 0;
     }
 #endif
     // (a last-CTA finalize here, behind a per-CTA fence + ticket, measured

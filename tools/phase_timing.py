@@ -30,12 +30,12 @@ def main():
         tg.train_step(g, batches[i % 4], asynchronous=True)
     g.sync()
     nb = 16 ** 3
-    ph = np.zeros(nb * 10, dtype=np.uint64)
+    ph = np.zeros(nb * 12, dtype=np.uint64)
     L = tg.lib()
     L.tgcu_phase_dump.argtypes = [C.c_void_p, C.c_int]
     assert L.tgcu_phase_dump(ph.ctypes.data_as(C.c_void_p), nb) == 0
-    ph = ph.reshape(nb, 10).astype(np.float64)
-    start, tile, a2, scan, bal, b2, epi, end, npts = (ph[:, i] for i in range(9))
+    ph = ph.reshape(nb, 12).astype(np.float64)
+    start, tile, a2, scan, bal, b2, epi, end, npts, e1, e2 = (ph[:, i] for i in range(11))
     t0 = start.min()
     dur = end - start
     span = end.max() - t0
@@ -51,6 +51,8 @@ def main():
         print(f"  {name:38s} {v.sum() / tot * 100:5.1f} %   mean {v.mean() / 1e3:6.2f} us")
     other = tot - (tilew.sum() + (a2 - tilew).sum() + scan.sum() + bal.sum() + b2.sum() + epid.sum())
     print(f"  {'other (setup, chunk starts)':38s} {other / tot * 100:5.1f} %")
+    print(f"  epilogue split: G store + m/v wait {(e1 - epi).mean() / 1e3:.2f} us, TV + Adam {(e2 - e1).mean() / 1e3:.2f} us, "
+          f"store issue + partials + drain {(end - e2).mean() / 1e3:.2f} us")
     chunks = np.ceil(npts / 512)
     for c in sorted(set(chunks.astype(int))):
         sel = chunks == c
