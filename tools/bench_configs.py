@@ -79,6 +79,7 @@ def run(name, steps, warmup):
             "sigma": cfg["sigma"], "ms_per_step": ms, "points_per_s": N / (ms * 1e-3),
             "brick_kernel_ms": kms / max(kn, 1), "survey_bytes_per_step": bt,
             "step_frac_survey_bytes": bt / (ms * 1e-3) / 1e9 / peak,
+            "kernel_frac_survey_bytes": bt / (kms / max(kn, 1) * 1e-3) / 1e9 / peak,
             "kernel_frac_our_bytes": ours / (kms / max(kn, 1) * 1e-3) / 1e9 / peak, "peak_gbs": peak,
             "loss_last": last.total, "steps": steps}
 
