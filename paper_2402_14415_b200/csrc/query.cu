@@ -153,7 +153,17 @@ constexpr int brick_log2() { return DIM == 3 ? 3 : 4; }
 // LDS.64 wavefronts: 1.87x -> 1.72x of ideal for K = 10, 3.3x -> 2.6x for K = 4).
 template <int DIM, int K, int T>
 constexpr int query_trowf() {
-    return (DIM == 3 && K == 10) ? 104 : (DIM == 3 && K == 4) ? 48 : ((T * K + 3) / 4) * 4;
+    return (DIM == 3 && K == 10) ? 100 : (DIM == 3 && K == 4) ? 48 : ((T * K + 3) / 4) * 4;
+}
+// Rows per tile plane (3D). Tensor boxes land densely, so with T rows the
+// plane pitch T * TROWF is congruent to the row pitch modulo the 32 banks for
+// any 16-byte-multiple TROWF, and a cell's y and z corners collide. For K = 10
+// the box carries one extra row per plane (pitch 10 x 100 floats: the bank
+// model tools/bank_model.py gives 4.28 instead of 4.58 wavefronts per 64-bit
+// corner load; 6 CTAs still fit per SM).
+template <int DIM, int K, int T>
+constexpr int query_plane_rows() {
+    return (DIM == 3 && K == 10) ? T + 1 : T;
 }
 #ifndef QMINB_SMALL
 #define QMINB_SMALL 8
@@ -282,7 +292,8 @@ __global__ void __launch_bounds__(256, query_min_blocks<KOf<DIM, ORDER>::value>(
     constexpr int GR = (K % 2 == 0) ? 2 : 1;
     // tile rows (fixed y, z) of T vertices, stride TROWF floats (16-byte multiple)
     constexpr int TROWF = query_trowf<DIM, K, T>();
-    constexpr int ROWS = DIM == 3 ? T * T : T;
+    constexpr int PR = query_plane_rows<DIM, K, T>();  // rows per plane (3D)
+    constexpr int ROWS = DIM == 3 ? T * PR : T;
     constexpr unsigned RBYTES = ((T * K * 4 + 15) / 16) * 16;
     extern __shared__ __align__(128) float tile[];  // ROWS * TROWF
     __shared__ __align__(8) unsigned long long bar;
@@ -310,8 +321,8 @@ __global__ void __launch_bounds__(256, query_min_blocks<KOf<DIM, ORDER>::value>(
         const long long nc_bytes = (long long)s.res[0] * s.res[1] * (DIM == 3 ? s.res[2] : 1) * K * 4;
         const int r = threadIdx.x;
         bool arrived = false;
-        if (r < ROWS) {
-            const int ty = DIM == 3 ? r % T : r, tz = DIM == 3 ? r / T : 0;
+        if (r < ROWS && (DIM == 2 || r % PR < T)) {
+            const int ty = DIM == 3 ? r % PR : r, tz = DIM == 3 ? r / PR : 0;
             const int vy = oy + ty, vz = oz + tz;
             if (vy < s.res[1] && (DIM == 2 || vz < s.res[2])) {
                 const long long v0 = (DIM == 3 ? (long long)vz * s.sz : 0LL) + (long long)vy * s.sy + ox;
@@ -369,7 +380,7 @@ __global__ void __launch_bounds__(256, query_min_blocks<KOf<DIM, ORDER>::value>(
             ax[a] = axis_factors(s, a, local);
             lc[a] = c - o3[a];
         }
-        tbase = (DIM == 3 ? lc[2] * T + lc[1] : lc[1]) * TROWF + lc[0] * K;
+        tbase = (DIM == 3 ? lc[2] * PR + lc[1] : lc[1]) * TROWF + lc[0] * K;
         return true;
     };
     auto evaluate = [&](long long i, const AxisF* ax, int tbase) {  // i = output slot
@@ -379,7 +390,7 @@ __global__ void __launch_bounds__(256, query_min_blocks<KOf<DIM, ORDER>::value>(
         for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
 #pragma unroll
         for (int c = 0; c < (1 << DIM); ++c) {
-            const int tv = tbase + (c & 1) * K + ((c >> 1) & 1) * TROWF + (DIM == 3 ? ((c >> 2) & 1) * T * TROWF : 0);
+            const int tv = tbase + (c & 1) * K + ((c >> 1) & 1) * TROWF + (DIM == 3 ? ((c >> 2) & 1) * PR * TROWF : 0);
             float cb[K];
             load_block<K, false>(tile + tv, cb);
             blend_corner<DIM, ORDER, GRAD>(cb, corner_geom<DIM>(s, ax, c), f, fg);
@@ -457,17 +468,17 @@ __global__ void k_i32_to_i64_copy(const int* __restrict__ a, long long* __restri
 }
 
 // Query tile tensor maps (box (B+1) vertices padded to 16 bytes x (B+1) [x (B+1)]).
-static bool ensure_query_tmaps(Grid& g, unsigned box_x, unsigned T) {
+static bool ensure_query_tmaps(Grid& g, unsigned box_x, unsigned box_y, unsigned T) {
     if (g.tmq_state == 0) {
         g.tmq_state = -1;
         if (((int64_t)g.ds.res[0] * g.K * 4) % 16 == 0 && box_x <= 256 && !g.slab) {
-            bool ok = encode_grid_map(&g.tm_query[0], g, g.p[0], box_x, T);
-            if (g.p[1]) ok = ok && encode_grid_map(&g.tm_query[1], g, g.p[1], box_x, T);
+            bool ok = encode_grid_map(&g.tm_query[0], g, g.p[0], box_x, box_y, T);
+            if (g.p[1]) ok = ok && encode_grid_map(&g.tm_query[1], g, g.p[1], box_x, box_y, T);
             if (ok) g.tmq_state = g.p[1] ? 2 : 1;  // maps built for 1 or 2 buffers
         }
     }
     if (g.tmq_state == 1 && g.p[1]) {  // optimiser buffers appeared since
-        if (!encode_grid_map(&g.tm_query[1], g, g.p[1], box_x, T)) return false;
+        if (!encode_grid_map(&g.tm_query[1], g, g.p[1], box_x, box_y, T)) return false;
         g.tmq_state = 2;
     }
     return g.tmq_state >= 1 && (g.cur == 0 || g.tmq_state == 2);
@@ -482,8 +493,9 @@ static void launch_brick_query(Grid& g, const float* pts, const long long* off, 
         constexpr int K = KOf<DIM, ORDER>::value;
         constexpr int T = B + 1;
         constexpr int TROWF = query_trowf<DIM, K, T>();
-        const size_t smem = sizeof(float) * (DIM == 3 ? T * T : T) * TROWF;
-        const bool use_tm = ensure_query_tmaps(g, TROWF, T);
+        constexpr int PR = query_plane_rows<DIM, K, T>();
+        const size_t smem = sizeof(float) * (DIM == 3 ? T * PR : T) * TROWF;
+        const bool use_tm = ensure_query_tmaps(g, TROWF, PR, T);
         CUtensorMap map{};
         if (use_tm) map = g.tm_query[g.cur];
         dim3 grid(1, 1, 1);

@@ -169,8 +169,9 @@ void bd_collect(Grid& g);                       // after a step: add its segment
 constexpr int kTraceCap = 4096;
 
 // TMA tensor map over a coefficient-layout buffer: rows of K*res_x floats x
-// res_y [x stored z planes], box box_x floats x box_yz [x box_yz] (train.cu).
-bool encode_grid_map(CUtensorMap* m, const Grid& g, const float* base, unsigned box_x, unsigned box_yz);
+// res_y [x stored z planes], box box_x floats x box_y [x box_z, default box_y] (train.cu).
+bool encode_grid_map(CUtensorMap* m, const Grid& g, const float* base, unsigned box_x, unsigned box_y,
+                     unsigned box_z = 0);
 void ensure_staging(Grid& g, int64_t floats);
 void ensure_pipeline(Grid& g, int64_t floats);
 void ensure_bins(Grid& g, int set, int64_t points);

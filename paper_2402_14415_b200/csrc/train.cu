@@ -1130,12 +1130,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // A (rows = K * res_x floats) x res_y [x zstore] view of one coefficient-layout
 // buffer with a box of box_x floats x box_yz rows [x box_yz planes].
-bool encode_grid_map(CUtensorMap* m, const Grid& g, const float* base, unsigned box_x, unsigned box_yz) {
+bool encode_grid_map(CUtensorMap* m, const Grid& g, const float* base, unsigned box_x, unsigned box_y,
+                     unsigned box_z) {
     const int dim = g.spec.dim;
     const cuuint64_t row = (cuuint64_t)g.ds.res[0] * g.K;
     cuuint64_t gdim[3] = {row, (cuuint64_t)g.ds.res[1], (cuuint64_t)g.ds.zstore};
     cuuint64_t gstr[2] = {row * 4, row * 4 * (cuuint64_t)g.ds.res[1]};
-    cuuint32_t box[3] = {box_x, box_yz, box_yz};
+    cuuint32_t box[3] = {box_x, box_y, box_z ? box_z : box_y};
     cuuint32_t es[3] = {1, 1, 1};
     const CUresult r = tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)dim,
                                             const_cast<float*>(base), gdim, gstr, box, es,
