@@ -449,10 +449,14 @@ struct StepArgs {
     int zb0;           // first brick layer of this grid (slab grids; 0 otherwise)
 };
 
+// Cell runs of a chunk's records: every cell gets the contiguous slot range
+// [start, start + cnt). The runs need not be in cell order (a vertex walks its
+// cells by index), so each warp scans its cells with shuffles and reserves
+// its range with one shared-memory atomic: no block-wide barrier inside.
 template <int NCELL, int NT>
-__device__ __forceinline__ void block_excl_scan(const int* __restrict__ cnt, int* __restrict__ start, int* warp_tot) {
+__device__ __forceinline__ void cell_runs(const int* __restrict__ cnt, int* __restrict__ start, int* total) {
     constexpr int IT = (NCELL + NT - 1) / NT;
-    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int t = threadIdx.x, lane = t & 31;
     int v[IT];
     int sum = 0;
 #pragma unroll
@@ -467,19 +471,10 @@ __device__ __forceinline__ void block_excl_scan(const int* __restrict__ cnt, int
         const int y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    if (lane == 31) warp_tot[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        int w = lane < NT / 32 ? warp_tot[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
-        }
-        if (lane < NT / 32) warp_tot[lane] = w;
-    }
-    __syncthreads();
-    int excl = (wid ? warp_tot[wid - 1] : 0) + x - sum;
+    int base = 0;
+    if (lane == 31 && x > 0) base = atomicAdd(total, x);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int excl = base + x - sum;
 #pragma unroll
     for (int k = 0; k < IT; ++k) {
         const int i = t * IT + k;
@@ -631,7 +626,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     int* perm = start + S::NCELL;                 // thread -> owned vertex (load balance)
     int* bhist = perm + NT;                       // 64 workload buckets
     int* bstart = bhist + 64;
-    __shared__ int warp_tot[32];
+    __shared__ int run_total;
     __shared__ double red[4][NT / 32];
     __shared__ __align__(8) unsigned long long bars[2];  // tile, mv
 
@@ -707,6 +702,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         const int m = min(CH, p1 - base);
         for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
         if (base == p0 && tid < 64) bhist[tid] = 0;
+        if (tid == 0) run_total = 0;
         __syncthreads();
         // 2a. locate + cell rank, the chunk's counting sort by cell and (first
         //     chunk) the workload balance need no parameters: they run while
@@ -737,7 +733,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
 #ifdef TGCU_PHASE_TIMING
         const unsigned long long pt_s0 = pt_c0;
 #endif
-        block_excl_scan<S::NCELL, NT>(cnt, start, warp_tot);
+        cell_runs<S::NCELL, NT>(cnt, start, &run_total);
         __syncthreads();
 #ifdef TGCU_PHASE_TIMING
         TGCU_PT_SET(pt_x)
