@@ -230,6 +230,34 @@ int tgcu_slab_step_finish(tgcu_grid* g, const double* reduced, tgcu_loss_terms* 
 int tgcu_slab_halo(tgcu_grid* g, float** send_lo, float** send_hi, float** recv_lo, float** recv_hi,
                    int64_t* plane_floats);
 
+/* Fused halo (peer stores over NVLink): the brick kernel of the slab's lowest
+ * and highest owned planes also writes those planes' new parameters straight
+ * into the lower / upper neighbour's halo plane of the same ping-pong slot,
+ * so no halo exchange follows the step. The per-step reduction of the partials
+ * orders the neighbours (a rank's next step starts after every rank's brick
+ * kernel has finished), and a rolled-back step leaves both sides' committed
+ * slots untouched. Setup, once per run (slab.py SlabTrainer):
+ *   tgcu_slab_ipc_export on every rank -> exchange the 144-byte blobs ->
+ *   tgcu_slab_ipc_import(side 0, lower neighbour's blob),
+ *   tgcu_slab_ipc_import(side 1, upper neighbour's blob) ->
+ *   tgcu_slab_peer_probe(0) on every rank, barrier, tgcu_slab_peer_probe(1)
+ *   (verifies the neighbours' writes landed); any failure -> keep exchanging.
+ * blob: cudaIpcMemHandle_t of p[0] and p[1] (2 x 64 bytes), then the byte
+ * offsets of this slab's lower and upper halo plane within them (2 x int64). */
+int tgcu_slab_ipc_export(tgcu_grid* g, void* blob144);
+int tgcu_slab_ipc_import(tgcu_grid* g, int side, const void* blob144);
+/* Same-process form (one device hosting several slabs, tests): dst_lo[i] /
+ * dst_hi[i] = the neighbour's halo plane in its slot-i parameters (NULL: no
+ * neighbour on that side). */
+int tgcu_slab_set_peer_planes(tgcu_grid* g, float* const dst_lo[2], float* const dst_hi[2]);
+/* This slab's own halo planes (lower, upper; NULL at the grid boundary) in
+ * parameter slots 0 and 1 — what a same-process neighbour passes above. */
+int tgcu_slab_halo_slots(tgcu_grid* g, float* recv_lo[2], float* recv_hi[2]);
+/* phase 0: write a probe pattern into the neighbours' halo planes of the
+ * inactive slot; phase 1: check the neighbours' patterns in this slab's halo
+ * planes (*ok = 1 when both sides match). Synchronous. */
+int tgcu_slab_peer_probe(tgcu_grid* g, int phase, int* ok);
+
 /* Fused steps issued on this grid since creation or the last reported error;
  * error messages of a failed step name it as "step <this index at launch>". */
 int tgcu_grid_steps_launched(const tgcu_grid* g, int64_t* n);

@@ -137,6 +137,11 @@ def lib():
                                        C.POINTER(C.POINTER(C.c_double)), C.c_int, P]
     L.tgcu_slab_step_finish.argtypes = [P, P, C.POINTER(_Terms), C.c_int, P]
     L.tgcu_slab_halo.argtypes = [P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(C.c_int64)]
+    L.tgcu_slab_ipc_export.argtypes = [P, P]
+    L.tgcu_slab_ipc_import.argtypes = [P, C.c_int, P]
+    L.tgcu_slab_set_peer_planes.argtypes = [P, C.POINTER(P), C.POINTER(P)]
+    L.tgcu_slab_peer_probe.argtypes = [P, C.c_int, C.POINTER(C.c_int)]
+    L.tgcu_slab_halo_slots.argtypes = [P, C.POINTER(P), C.POINTER(P)]
     L.tgcu_trace.argtypes = [P, C.POINTER(_Terms), C.c_int]
     L.tgcu_launch_count.restype = C.c_int64
     L.tgcu_profile_begin.argtypes = [P]

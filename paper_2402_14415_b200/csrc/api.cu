@@ -422,6 +422,7 @@ int tgcu_grid_destroy(tgcu_grid* h) {
     }
     if (g.cstream) cudaStreamDestroy(g.cstream);
     cudaFreeHost(g.h_ring);
+    for (void* b : g.ipc_open) cudaIpcCloseMemHandle(b);
     for (auto e : g.prof_ev) cudaEventDestroy(e);
     delete h;
     return TGCU_OK;
@@ -935,6 +936,128 @@ int tgcu_slab_halo(tgcu_grid* h, float** send_lo, float** send_hi, float** recv_
         *send_hi = has_hi ? plane(own_hi - 1) : nullptr;
         *recv_hi = has_hi ? plane(own_hi) : nullptr;
         *plane_floats = pf;
+    });
+}
+
+namespace {
+// Owned-plane range and halo-plane byte offsets of a slab grid.
+struct SlabPlanes {
+    int own_lo, own_hi;
+    bool has_lo, has_hi;
+    int64_t pf;  // floats per plane
+};
+SlabPlanes slab_planes(const tgcu::Grid& g) {
+    SlabPlanes p;
+    p.own_lo = tgcu::kBrick3 * g.zb0;
+    p.own_hi = std::min(g.spec.res[2], tgcu::kBrick3 * (g.zb0 + g.nb[2]));
+    p.has_lo = p.own_lo > 0;
+    p.has_hi = p.own_hi < g.spec.res[2];
+    p.pf = g.ds.sz * g.K;
+    return p;
+}
+
+__global__ void k_fill_value(float* __restrict__ p, int64_t n, float v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+}  // namespace
+
+int tgcu_slab_ipc_export(tgcu_grid* h, void* blob) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(g.slab, "slab_ipc_export: not a slab grid");
+        require(blob != nullptr, "slab_ipc_export: NULL blob");
+        ensure_optimizer(g);
+        unsigned char* b = static_cast<unsigned char*>(blob);
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        for (int i = 0; i < 2; ++i)
+            TGCU_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(b + 64 * i), g.p[i]));
+        const SlabPlanes sp = slab_planes(g);
+        const int64_t off_lo = sp.has_lo ? (int64_t)(sp.own_lo - 1 - g.ds.zoff) * sp.pf * 4 : -1;
+        const int64_t off_hi = sp.has_hi ? (int64_t)(sp.own_hi - g.ds.zoff) * sp.pf * 4 : -1;
+        std::memcpy(b + 128, &off_lo, 8);
+        std::memcpy(b + 136, &off_hi, 8);
+    });
+}
+
+int tgcu_slab_ipc_import(tgcu_grid* h, int side, const void* blob) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(g.slab, "slab_ipc_import: not a slab grid");
+        require(blob != nullptr && (side == 0 || side == 1), "slab_ipc_import: bad argument");
+        const SlabPlanes sp = slab_planes(g);
+        require(side == 0 ? sp.has_lo : sp.has_hi, "slab_ipc_import: no neighbour on that side");
+        const unsigned char* b = static_cast<const unsigned char*>(blob);
+        int64_t off = -1;
+        // my lowest owned plane is the lower neighbour's upper halo and vice versa
+        std::memcpy(&off, b + (side == 0 ? 136 : 128), 8);
+        require(off >= 0, "slab_ipc_import: the neighbour has no halo plane facing this slab");
+        for (int i = 0; i < 2; ++i) {
+            cudaIpcMemHandle_t hd;
+            std::memcpy(&hd, b + 64 * i, sizeof(hd));
+            void* base = nullptr;
+            TGCU_CUDA(cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess));
+            g.ipc_open.push_back(base);
+            float* dst = reinterpret_cast<float*>(static_cast<char*>(base) + off);
+            (side == 0 ? g.peer_lo : g.peer_hi)[i] = dst;
+        }
+    });
+}
+
+int tgcu_slab_set_peer_planes(tgcu_grid* h, float* const dst_lo[2], float* const dst_hi[2]) {
+    return guard([&] {
+        Grid& g = h->g;
+        require(g.slab, "slab_set_peer_planes: not a slab grid");
+        for (int i = 0; i < 2; ++i) {
+            g.peer_lo[i] = dst_lo ? dst_lo[i] : nullptr;
+            g.peer_hi[i] = dst_hi ? dst_hi[i] : nullptr;
+        }
+    });
+}
+
+int tgcu_slab_halo_slots(tgcu_grid* h, float* recv_lo[2], float* recv_hi[2]) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(g.slab && recv_lo && recv_hi, "slab_halo_slots: bad argument");
+        ensure_optimizer(g);
+        const SlabPlanes sp = slab_planes(g);
+        for (int i = 0; i < 2; ++i) {
+            recv_lo[i] = sp.has_lo ? g.p[i] + (int64_t)(sp.own_lo - 1 - g.ds.zoff) * sp.pf : nullptr;
+            recv_hi[i] = sp.has_hi ? g.p[i] + (int64_t)(sp.own_hi - g.ds.zoff) * sp.pf : nullptr;
+        }
+    });
+}
+
+int tgcu_slab_peer_probe(tgcu_grid* h, int phase, int* ok) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(g.slab && ok != nullptr, "slab_peer_probe: bad argument");
+        ensure_optimizer(g);
+        const SlabPlanes sp = slab_planes(g);
+        const int j = 1 - g.cur;  // the slot the next step writes
+        *ok = 1;
+        if (phase == 0) {
+            // my lowest / highest owned plane index, as the neighbours will see it
+            if (g.peer_lo[j]) k_fill_value<<<64, 256>>>(g.peer_lo[j], sp.pf, (float)sp.own_lo);
+            if (g.peer_hi[j]) k_fill_value<<<64, 256>>>(g.peer_hi[j], sp.pf, (float)(sp.own_hi - 1));
+            TGCU_CUDA(cudaGetLastError());
+            TGCU_CUDA(cudaDeviceSynchronize());
+            return;
+        }
+        std::vector<float> plane(sp.pf);
+        auto check = [&](int z) {
+            TGCU_CUDA(cudaMemcpy(plane.data(), g.p[j] + (int64_t)(z - g.ds.zoff) * sp.pf, sizeof(float) * sp.pf,
+                                 cudaMemcpyDeviceToHost));
+            for (float v : plane)
+                if (v != (float)z) return false;
+            return true;
+        };
+        if (sp.has_lo && !check(sp.own_lo - 1)) *ok = 0;
+        if (sp.has_hi && !check(sp.own_hi)) *ok = 0;
     });
 }
 

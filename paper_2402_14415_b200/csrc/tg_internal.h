@@ -98,6 +98,11 @@ struct Grid {
     double tv_inv_norm = 0.0;     // 1 / (P*K) of the global grid
     double* slab_red = nullptr;   // 8 doubles: local sums of the pending slab step
     int slab_in_idx = 0;
+    // Fused halo (tgcu_slab_ipc_import / tgcu_slab_set_peer_planes): the
+    // neighbours' halo planes, per ping-pong slot, written by the brick kernel.
+    float* peer_lo[2] = {nullptr, nullptr};
+    float* peer_hi[2] = {nullptr, nullptr};
+    std::vector<void*> ipc_open;  // bases opened with cudaIpcOpenMemHandle
     int64_t slab_step = 0, slab_t_after = 0, slab_n = 0;
     tgcu_loss_config slab_cfg{};
     int brick[3] = {1, 1, 1};

@@ -447,6 +447,12 @@ struct StepArgs {
     Status* st;
     float* grad_out;   // optional: full gradient (validation mode, TGCU_EXPORT_GRAD)
     int zb0;           // first brick layer of this grid (slab grids; 0 otherwise)
+    // fused halo (slab grids): the neighbours' halo planes in the out slot;
+    // the lowest owned plane is local z 0 of brick layer zb0, the highest is
+    // local z peer_hi_lz of brick layer peer_hi_zb
+    float* peer_lo;
+    float* peer_hi;
+    int peer_hi_zb, peer_hi_lz;
 };
 
 // Cell runs of a chunk's records: every cell gets the contiguous slot range
@@ -1030,6 +1036,26 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     // row and array, issued by one thread each
     fence_proxy_async_smem();
     __syncthreads();
+    if constexpr (DIM == 3) {
+        // fused halo: a slab-boundary plane's new parameters go straight into
+        // the neighbour's halo plane (peer memory over NVLink), row by row
+        const int bz = (int)blockIdx.z + A.zb0;
+        const bool lo = A.peer_lo && bz == A.zb0, hi = A.peer_hi && bz == A.peer_hi_zb;
+        if (lo || hi) {
+            const int nvx = min(B, A.s.res[0] - o[0]);
+            const int rowf = nvx * K;
+            auto put_plane = [&](float* dst, int lz) {
+                for (int i = tid; i < B * rowf; i += NT) {
+                    const int ly = i / rowf, q = i - ly * rowf;
+                    if (o[1] + ly < A.s.res[1])
+                        dst[((long long)(o[1] + ly) * A.s.res[0] + o[0]) * K + q] = uni[(lz * B + ly) * B * K + q];
+                }
+            };
+            if (lo) put_plane(A.peer_lo, 0);
+            if (hi) put_plane(A.peer_hi, A.peer_hi_lz);
+            __threadfence_system();
+        }
+    }
     if (tmap) {
         if (tid == 0) {
             if constexpr (DIM == 3) {
@@ -1293,6 +1319,13 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     A.st = g.st;
     A.grad_out = grad_out;
     A.zb0 = g.zb0;
+    A.peer_lo = g.peer_lo[out_idx];
+    A.peer_hi = g.peer_hi[out_idx];
+    {
+        const int own_hi = std::min(g.spec.res[2], kBrick3 * (g.zb0 + g.nb[2]));
+        A.peer_hi_zb = (own_hi - 1) / kBrick3;
+        A.peer_hi_lz = (own_hi - 1) % kBrick3;
+    }
     const bool eik = cfg.lambda1 > 0.0;
     FinArgs F;
     F.partials = g.partials;

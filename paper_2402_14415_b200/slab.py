@@ -14,6 +14,13 @@ front, the loss still normalised by the global batch size). Per step:
     terms = slab.finish(partials)         # same commit decision on every rank
     halo exchange of boundary parameter planes (send/recv with the neighbours)
 
+With the fused halo (SlabTrainer default when every rank can open its
+neighbours' parameter buffers through CUDA IPC, i.e. NVLink peers or one
+shared device) the exchange disappears: the brick kernel of each boundary
+brick layer also stores the new boundary plane into the neighbour's halo
+plane of the same ping-pong slot, and the all-reduce of the partials is the
+only collective per step.
+
 No gradient is exchanged: each gradient is computed by its owner. The loss
 scale 1/N and the TV normaliser P*K are global (sdf_loss.cpp:161-170), so the
 slab steps reproduce the single-grid step.
@@ -210,6 +217,35 @@ class SlabGrid:
         _check(lib().tgcu_sync(self._h, C.byref(t)))
         return LossTerms._from(t)
 
+    # ---- fused halo: the brick kernel writes boundary planes into the neighbours ----
+    def ipc_export(self) -> bytes:
+        """144-byte blob: IPC handles of both parameter slots + halo plane offsets."""
+        buf = (C.c_ubyte * 144)()
+        _check(lib().tgcu_slab_ipc_export(self._h, C.cast(buf, C.c_void_p)))
+        return bytes(buf)
+
+    def ipc_import(self, side: int, blob: bytes):
+        """side 0: the lower neighbour's blob, side 1: the upper neighbour's."""
+        buf = (C.c_ubyte * 144).from_buffer_copy(blob)
+        _check(lib().tgcu_slab_ipc_import(self._h, int(side), C.cast(buf, C.c_void_p)))
+
+    def halo_slots(self) -> Tuple[Tuple[int, int], Tuple[int, int]]:
+        """This slab's (lower, upper) halo plane addresses, each as (slot 0, slot 1); 0 = none."""
+        lo, hi = (C.c_void_p * 2)(), (C.c_void_p * 2)()
+        _check(lib().tgcu_slab_halo_slots(self._h, lo, hi))
+        return (lo[0] or 0, lo[1] or 0), (hi[0] or 0, hi[1] or 0)
+
+    def set_peer_planes(self, dst_lo: Tuple[int, int], dst_hi: Tuple[int, int]):
+        """Same-device neighbours (tests): their halo plane addresses per slot."""
+        lo = (C.c_void_p * 2)(*[C.c_void_p(x or None) for x in dst_lo])
+        hi = (C.c_void_p * 2)(*[C.c_void_p(x or None) for x in dst_hi])
+        _check(lib().tgcu_slab_set_peer_planes(self._h, lo, hi))
+
+    def peer_probe(self, phase: int) -> bool:
+        ok = C.c_int(0)
+        _check(lib().tgcu_slab_peer_probe(self._h, int(phase), C.byref(ok)))
+        return bool(ok.value)
+
     def profile_begin(self):
         _check(lib().tgcu_profile_begin(self._h))
 
@@ -234,6 +270,46 @@ class SlabTrainer:
         self.slab = SlabGrid(spec, lo, hi, opts, device)
         self.slab.adam_reset(adam)
         self.exchange()  # halo planes of the initial parameters
+        self.fused_halo = self._setup_fused_halo()
+
+    def _all_ok(self, ok: bool) -> bool:
+        import torch
+        dev = "cpu" if self._staged() else "cuda"
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+        return bool(int(t.item()))
+
+    def _setup_fused_halo(self) -> bool:
+        """Peer-memory halo (tgcu_slab_ipc_export/import): the brick kernel of a
+        boundary brick layer writes the new boundary plane straight into the
+        neighbour's halo plane, so no exchange follows a step. Every rank
+        must succeed (IPC open + a probe round trip) or all keep exchanging.
+        TGCU_FUSED_HALO=0 disables it."""
+        import os
+        if self.world == 1 or os.environ.get("TGCU_FUSED_HALO", "1") == "0":
+            return False
+        ok = True
+        try:
+            blob = self.slab.ipc_export()
+        except Exception:
+            blob, ok = b"", False
+        blobs = [None] * self.world
+        self.dist.all_gather_object(blobs, blob)
+        try:
+            if ok and self.rank > 0:
+                self.slab.ipc_import(0, blobs[self.rank - 1])
+            if ok and self.rank < self.world - 1:
+                self.slab.ipc_import(1, blobs[self.rank + 1])
+        except Exception:
+            ok = False
+        ok = self._all_ok(ok)
+        if ok:
+            self.slab.peer_probe(0)
+            self.dist.barrier()
+            ok = self._all_ok(self.slab.peer_probe(1))
+        if not ok:
+            self.slab.set_peer_planes((0, 0), (0, 0))
+        return ok
 
     def _staged(self) -> bool:
         # NCCL moves device memory directly; gloo (CPU tests, one shared GPU)
@@ -292,5 +368,6 @@ class SlabTrainer:
         else:
             self.dist.all_reduce(t)
         terms = self.slab.finish(part, asynchronous=not want_terms, stream=stream)
-        self.exchange()
+        if not self.fused_halo:
+            self.exchange()
         return terms

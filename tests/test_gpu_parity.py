@@ -337,13 +337,17 @@ def test_c2_scale_fused_gradient_vs_oracle(oracle):
 # ---- multi-GPU slab path, two slabs emulated on one device ----------------------------------------
 
 
-@pytest.mark.parametrize("nslab,res,sharded", [(2, (24, 20, 40), False), (3, (21, 18, 43), False),
-                                               (3, (21, 18, 43), True)])
-def test_slab_two_on_one_gpu_matches_full_grid(nslab, res, sharded):
+@pytest.mark.parametrize("nslab,res,sharded,fused", [(2, (24, 20, 40), False, False), (3, (21, 18, 43), False, False),
+                                                     (3, (21, 18, 43), True, False), (3, (21, 18, 43), True, True),
+                                                     (2, (24, 20, 40), False, True)])
+def test_slab_two_on_one_gpu_matches_full_grid(nslab, res, sharded, fused):
     """z-slab grids driven like ranks (sum of partials, commit, halo exchange
     by device copies) reproduce the single-grid fused trajectory; with three
     slabs the middle one exchanges both halo planes; sharded: each slab reads
-    only its own points (slab_point_mask) with the global batch size."""
+    only its own points (slab_point_mask) with the global batch size; fused:
+    no exchange — the brick kernel writes the boundary planes into the
+    neighbours' halo planes (tgcu_slab_set_peer_planes, the same-device form
+    of the NVLink peer stores), checked first by the peer probe."""
     from paper_2402_14415_b200.slab import SlabGrid, brick_layers, device_view, slab_point_mask, slab_ranges
     spec = tg.GridSpec(dim=3, resolution=res, order=2)
     init = tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.02, seed=3)
@@ -359,6 +363,15 @@ def test_slab_two_on_one_gpu_matches_full_grid(nslab, res, sharded):
     c_full = full.coeffs
     for sg in slabs:  # identical initial values, halo planes included
         assert np.array_equal(sg.coeffs(), c_full[sg.z_store_lo * plane:(sg.z_store_lo + sg.z_store_n) * plane])
+    if fused:
+        slots = [sg.halo_slots() for sg in slabs]  # ((lo0, lo1), (hi0, hi1))
+        for r, sg in enumerate(slabs):
+            dst_lo = slots[r - 1][1] if r > 0 else (0, 0)          # lower neighbour's upper halo
+            dst_hi = slots[r + 1][0] if r < nslab - 1 else (0, 0)  # upper neighbour's lower halo
+            sg.set_peer_planes(dst_lo, dst_hi)
+        for sg in slabs:
+            sg.peer_probe(0)
+        assert all(sg.peer_probe(1) for sg in slabs)
     for step in range(6):
         b = tg.sample(tg.SHAPE_SPHERE, 3, 500 + step, 20000, near_frac=0.5, sigma=0.01, param0=0.6)
         tf = tg.train_step(full, b, cfg).as_array()
@@ -375,7 +388,7 @@ def test_slab_two_on_one_gpu_matches_full_grid(nslab, res, sharded):
             v.copy_(tot)
         terms = [sg.finish(p).as_array() for sg, p in zip(slabs, parts)]
         halos = [sg.halo() for sg in slabs]
-        for r in range(nslab - 1):  # slab r's top owned plane <-> slab r+1's bottom owned plane
+        for r in range(nslab - 1 if not fused else 0):  # slab r's top owned plane <-> slab r+1's bottom owned plane
             lo, hi = halos[r], halos[r + 1]
             pf = lo[4]
             device_view(hi[2], pf).copy_(device_view(lo[1], pf))
@@ -384,6 +397,17 @@ def test_slab_two_on_one_gpu_matches_full_grid(nslab, res, sharded):
             assert_close(t, tf, 1e-6, floor=1e-30, what=f"slab terms step {step}")
     owned = np.concatenate([sg.owned_coeffs() for sg in slabs])
     assert_trajectory_close(owned, full.coeffs, 1e-2, 6, what="slab coefficients")
+    # the halo planes hold exactly the neighbours' committed boundary planes
+    cs = [sg.coeffs() for sg in slabs]
+    for r in range(1, nslab):
+        lo_sg, hi_sg = slabs[r - 1], slabs[r]
+        z = hi_sg.z_own_lo - 1  # lower slab's top owned plane = upper slab's lower halo
+        a = (z - lo_sg.z_store_lo) * plane
+        assert np.array_equal(cs[r][:plane], cs[r - 1][a:a + plane])
+        z = lo_sg.z_own_hi      # upper slab's bottom owned plane = lower slab's upper halo
+        a = (z - hi_sg.z_store_lo) * plane
+        b = (z - lo_sg.z_store_lo) * plane
+        assert np.array_equal(cs[r - 1][b:b + plane], cs[r][a:a + plane])
 
 
 def test_pipelined_host_steps_match_device_steps():

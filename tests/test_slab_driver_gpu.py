@@ -2,7 +2,10 @@
 
 One GPU is available here, so both ranks run in separate processes on cuda:0
 over gloo (host-staged all-reduce / halo exchange); no kernel of one rank waits
-on the other's. The gathered owned slabs must reproduce a single-grid run.
+on the other's. The gathered owned slabs must reproduce a single-grid run,
+with the halo exchanged after each step or written by the brick kernel into
+the neighbour's buffers (fused halo through CUDA IPC, which two processes on
+one device support as NVLink peers do).
 """
 import os
 import socket
@@ -32,9 +35,10 @@ def _batches():
             for i in range(STEPS)]
 
 
-def _rank(rank, world, port, outdir):
+def _rank(rank, world, port, outdir, fused):
     import sys
     sys.path.insert(0, ROOT)
+    os.environ["TGCU_FUSED_HALO"] = "1" if fused else "0"
     import torch
     import torch.distributed as dist
     import paper_2402_14415_b200 as tg
@@ -48,14 +52,18 @@ def _rank(rank, world, port, outdir):
     for b in _batches():
         terms.append(tr.step(torch.from_numpy(b).cuda(), tg.LossConfig(), want_terms=True).as_array())
     np.save(os.path.join(outdir, f"own{rank}.npy"), tr.slab.owned_coeffs())
+    np.save(os.path.join(outdir, f"fused{rank}.npy"), np.array([tr.fused_halo]))
     np.save(os.path.join(outdir, f"terms{rank}.npy"), np.array(terms))
     dist.destroy_process_group()
 
 
-def test_slab_trainer_two_ranks_match_single_grid(tmp_path):
+@pytest.mark.parametrize("fused", [False, True])
+def test_slab_trainer_two_ranks_match_single_grid(tmp_path, fused):
     import torch.multiprocessing as mp
     import paper_2402_14415_b200 as tg
-    mp.spawn(_rank, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_rank, args=(2, _port(), str(tmp_path), fused), nprocs=2, join=True)
+    for r in range(2):
+        assert bool(np.load(tmp_path / f"fused{r}.npy")[0]) == fused
     spec = tg.GridSpec(dim=3, resolution=RES, order=2)
     g = tg.init_grid(spec, tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.02, seed=11))
     g.adam_reset(tg.AdamConfig(lr=1e-2))
