@@ -274,18 +274,35 @@ void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_
         sort_points_t<unsigned long long, unsigned long long>(g, pts, n, out, perm, offsets, end_bit, s);
 }
 
+// Where a brick's points come from (k_eval_brick SRC): brick-sorted points
+// (SRC 0: pts xyz, off = brick offsets by Morton code), binned points (SRC 1:
+// pts = float4 x, y, z, caller index), or a lattice (SRC 2: per-axis factor /
+// cell tables of the lattice coordinates and, per brick coordinate, the
+// lattice index range [x, y) whose cells lie in it).
+struct QuerySrc {
+    const float* pts = nullptr;
+    const long long* off = nullptr;
+    const float4* fac = nullptr;
+    const int* cell = nullptr;
+    const int2* rng = nullptr;
+    int3 n{1, 1, 1};     // lattice size
+    int nb[3] = {1, 1, 1};  // bricks per axis (rng offsets)
+};
+
 // One CTA per brick of B^D cells (launch grid = bricks per axis); its points
-// are [off[code], off[code+1]) of the brick-sorted array, code = Morton(brick).
+// are [off[code], off[code+1]) of the brick-sorted array, code = Morton(brick)
+// (or the lattice points whose cells lie in the brick).
 // The brick's (B+1)^D vertex tile arrives by one TMA tensor box load
 // (out-of-grid vertices zero-filled), or by one bulk copy per row when the
 // grid layout cannot take a tensor map. Each thread loads and locates its first
 // point before waiting for the tile, so the two latencies overlap.
-template <int DIM, int ORDER, bool GRAD, int LB, bool BINNED = false>
+template <int DIM, int ORDER, bool GRAD, int LB, int SRC = 0>
 __global__ void __launch_bounds__(256, query_min_blocks<KOf<DIM, ORDER>::value>()) k_eval_brick(const __grid_constant__ CUtensorMap tmap, int use_tmap,
-                                                    DevSpec s, const float* __restrict__ coeffs,
-                                                    const float* __restrict__ pts, const long long* __restrict__ off,
+                                                    DevSpec s, const float* __restrict__ coeffs, const QuerySrc Q,
                                                     float* __restrict__ vals, float* __restrict__ grads,
                                                     Status* st) {
+    constexpr bool BINNED = SRC == 1, LATTICE = SRC == 2;
+    const float* __restrict__ pts = Q.pts;
     constexpr int K = KOf<DIM, ORDER>::value;
     constexpr int B = 1 << LB;
     constexpr int T = B + 1;  // tile edge in vertices
@@ -302,7 +319,22 @@ __global__ void __launch_bounds__(256, query_min_blocks<KOf<DIM, ORDER>::value>(
     const unsigned int code = DIM == 3 ? (unsigned int)(spread3(blockIdx.x) | (spread3(blockIdx.y) << 1) |
                                                         (spread3(blockIdx.z) << 2))
                                        : (unsigned int)(spread2(blockIdx.x) | (spread2(blockIdx.y) << 1));
-    const long long p0 = off[code], p1 = off[code + 1];
+    long long p0, p1;
+    int2 lr[3] = {{0, 1}, {0, 1}, {0, 1}};  // lattice index range per axis
+    if constexpr (LATTICE) {
+        const int bc[3] = {(int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z};
+        long long cnt = 1;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            lr[a] = Q.rng[(a > 0 ? Q.nb[0] : 0) + (a > 1 ? Q.nb[1] : 0) + bc[a]];
+            cnt *= max(0, lr[a].y - lr[a].x);
+        }
+        p0 = 0;
+        p1 = cnt;
+    } else {
+        p0 = Q.off[code];
+        p1 = Q.off[code + 1];
+    }
     if (p0 >= p1) return;
     const bool tm = use_tmap != 0;
     if (threadIdx.x == 0) {
@@ -349,6 +381,23 @@ __global__ void __launch_bounds__(256, query_min_blocks<KOf<DIM, ORDER>::value>(
     // locate of point i: cell-relative tile offset and per-axis factors (false
     // for NaN); oi = the output slot (i, or the caller's index of a binned point)
     auto prepare = [&](long long i, AxisF* ax, int& tbase, long long& oi) -> bool {
+        if constexpr (LATTICE) {
+            // lattice point (X, Y, Z): per-axis factors and cells from the tables
+            const int nx = lr[0].y - lr[0].x, ny = lr[1].y - lr[1].x;
+            const int li = (int)i;
+            const int X = lr[0].x + li % nx, Y = lr[1].x + (li / nx) % ny, Z = lr[2].x + li / (nx * ny);
+            const int idx[3] = {X, Q.n.x + Y, Q.n.x + Q.n.y + Z};
+            int lc[3] = {0, 0, 0};
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                const float4 f = __ldg(Q.fac + idx[a]);
+                ax[a] = AxisF{f.x, f.y, f.z, f.w};
+                lc[a] = __ldg(Q.cell + idx[a]) - o3[a];
+            }
+            oi = DIM == 3 ? ((long long)Z * Q.n.y + Y) * Q.n.x + X : (long long)Y * Q.n.x + X;
+            tbase = (DIM == 3 ? lc[2] * PR + lc[1] : lc[1]) * TROWF + lc[0] * K;
+            return true;
+        }
         double x[DIM];
         bool nan = false;
         if constexpr (BINNED) {
@@ -484,9 +533,8 @@ static bool ensure_query_tmaps(Grid& g, unsigned box_x, unsigned box_y, unsigned
     return g.tmq_state >= 1 && (g.cur == 0 || g.tmq_state == 2);
 }
 
-template <bool BINNED>
-static void launch_brick_query(Grid& g, const float* pts, const long long* off, float* vals, float* grads,
-                               cudaStream_t s) {
+template <int SRC>
+static void launch_brick_query(Grid& g, const QuerySrc& Q, float* vals, float* grads, cudaStream_t s) {
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
         constexpr int LB = brick_log2<DIM>();
         constexpr int B = 1 << LB;
@@ -500,9 +548,9 @@ static void launch_brick_query(Grid& g, const float* pts, const long long* off, 
         if (use_tm) map = g.tm_query[g.cur];
         dim3 grid(1, 1, 1);
         for (int a = 0; a < DIM; ++a) (&grid.x)[a] = (unsigned)((g.spec.res[a] - 1 + B - 1) / B);
-        auto kern = grads ? k_eval_brick<DIM, ORDER, true, LB, BINNED> : k_eval_brick<DIM, ORDER, false, LB, BINNED>;
+        auto kern = grads ? k_eval_brick<DIM, ORDER, true, LB, SRC> : k_eval_brick<DIM, ORDER, false, LB, SRC>;
         TGCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<grid, 256, smem, s>>>(map, use_tm ? 1 : 0, g.ds, g.p[g.cur], pts, off, vals, grads, g.st);
+        kern<<<grid, 256, smem, s>>>(map, use_tm ? 1 : 0, g.ds, g.p[g.cur], Q, vals, grads, g.st);
     });
     count_launch();
 }
@@ -532,7 +580,10 @@ void launch_eval_binned(Grid& g, const float* pts, int64_t n, float* vals, float
     if (g.spec.dim == 3) k_qbin_scatter<3, 3><<<blocks, 256, 0, s>>>(g.ds, pts, n, cnt, binned);
     else k_qbin_scatter<2, 4><<<blocks, 256, 0, s>>>(g.ds, pts, n, cnt, binned);
     count_launch(3);
-    launch_brick_query<true>(g, reinterpret_cast<const float*>(binned), off, vals, grads, s);
+    QuerySrc Q;
+    Q.pts = reinterpret_cast<const float*>(binned);
+    Q.off = off;
+    launch_brick_query<1>(g, Q, vals, grads, s);
     TGCU_CUDA(cudaFreeAsync(temp, s));
     TGCU_CUDA(cudaFreeAsync(cnt, s));
     TGCU_CUDA(cudaFreeAsync(cursor, s));
@@ -552,9 +603,62 @@ void launch_eval_sorted(Grid& g, const float* pts, int64_t n, const int64_t* off
         offsets = reinterpret_cast<const int64_t*>(tmp);
     }
     const long long* off = reinterpret_cast<const long long*>(offsets);
-    launch_brick_query<false>(g, pts, off, vals, grads, s);
+    QuerySrc Q;
+    Q.pts = pts;
+    Q.off = off;
+    launch_brick_query<0>(g, Q, vals, grads, s);
     if (tmp) TGCU_CUDA(cudaFreeAsync(tmp, s));
     TGCU_CUDA(cudaGetLastError());
+}
+
+// ---- lattice query on the brick tiles -------------------------------------------
+// Lattice index range of every brick coordinate along each axis: the cells of
+// a lattice axis are non-decreasing, so the indices of one brick are a run.
+__global__ void k_lattice_ranges(const int* __restrict__ cell, int3 n, int dim, int lb, int nb0, int nb1,
+                                 int2* __restrict__ rng) {
+    const int na = n.x + (dim > 1 ? n.y : 0) + (dim > 2 ? n.z : 0);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < na; j += gridDim.x * blockDim.x) {
+        const int a = j < n.x ? 0 : (j < n.x + n.y ? 1 : 2);
+        const int first = a == 0 ? 0 : (a == 1 ? n.x : n.x + n.y);
+        const int len = a == 0 ? n.x : (a == 1 ? n.y : n.z);
+        const int i = j - first;
+        const int roff = a == 0 ? 0 : (a == 1 ? nb0 : nb0 + nb1);
+        const int b = cell[j] >> lb;
+        if (i == 0 || (cell[j - 1] >> lb) != b) rng[roff + b].x = i;
+        if (i == len - 1 || (cell[j + 1] >> lb) != b) rng[roff + b].y = i + 1;
+    }
+}
+
+bool launch_eval_lattice_brick(Grid& g, const float4* fac, const int* cell, int3 n, float* vals, cudaStream_t s) {
+    const int dim = g.spec.dim;
+    const int LB = dim == 3 ? 3 : 4;
+    const int B = 1 << LB;
+    int nb[3] = {1, 1, 1};
+    int64_t bricks = 1;
+    for (int a = 0; a < dim; ++a) {
+        nb[a] = (g.spec.res[a] - 1 + B - 1) / B;
+        bricks *= nb[a];
+    }
+    const int64_t pts = (int64_t)n.x * n.y * n.z;
+    // a tile per brick pays off when the bricks hold enough lattice points
+    if (pts < bricks * 128 || pts >= (1LL << 31)) return false;
+    const int nrng = nb[0] + nb[1] + nb[2];
+    int2* rng = nullptr;
+    TGCU_CUDA(cudaMallocAsync(&rng, sizeof(int2) * nrng, s));
+    TGCU_CUDA(cudaMemsetAsync(rng, 0, sizeof(int2) * nrng, s));
+    const int na = n.x + (dim > 1 ? n.y : 0) + (dim > 2 ? n.z : 0);
+    k_lattice_ranges<<<grid_blocks(na, 256), 256, 0, s>>>(cell, n, dim, LB, nb[0], nb[1], rng);
+    count_launch();
+    QuerySrc Q;
+    Q.fac = fac;
+    Q.cell = cell;
+    Q.rng = rng;
+    Q.n = n;
+    for (int a = 0; a < 3; ++a) Q.nb[a] = nb[a];
+    launch_brick_query<2>(g, Q, vals, nullptr, s);
+    TGCU_CUDA(cudaFreeAsync(rng, s));
+    TGCU_CUDA(cudaGetLastError());
+    return true;
 }
 
 }  // namespace tgcu

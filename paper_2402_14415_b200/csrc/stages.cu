@@ -285,12 +285,17 @@ int tgcu_sample_grid_field(tgcu_grid* h, const int lattice[3], float* values, in
                                                            nullptr, fac, cell);
         count_launch();
         require(n.y < 65536 && n.z < 65536, "sample_grid_field: lattice too large");
-        const int thr = std::min(256, (n.x + 31) / 32 * 32);
-        const dim3 blocks((n.x + thr - 1) / thr, n.y, n.z);
-        TGCU_DISPATCH(dim, g.spec.order, {
-            k_eval_lattice<DIM, ORDER><<<blocks, thr, 0, st>>>(g.ds, g.p[g.cur], fac, cell, n, dv);
-        });
-        count_launch();
+        // dense lattices: one CTA per grid brick evaluates its lattice points
+        // from the brick's shared-memory tile (query.cu); sparse ones: a
+        // thread per lattice point reading the corner blocks through L1/L2
+        if (!launch_eval_lattice_brick(g, fac, cell, n, dv, st)) {
+            const int thr = std::min(256, (n.x + 31) / 32 * 32);
+            const dim3 blocks((n.x + thr - 1) / thr, n.y, n.z);
+            TGCU_DISPATCH(dim, g.spec.order, {
+                k_eval_lattice<DIM, ORDER><<<blocks, thr, 0, st>>>(g.ds, g.p[g.cur], fac, cell, n, dv);
+            });
+            count_launch();
+        }
         TGCU_CUDA(cudaGetLastError());
         if (flags & TGCU_HOST)
             TGCU_CUDA(cudaMemcpyAsync(values, dv, sizeof(float) * total, cudaMemcpyDeviceToHost, st));

@@ -192,6 +192,10 @@ void launch_eval_direct(Grid& g, const float* pts, int64_t n, float* vals, float
 // brick + the smem-tile brick kernel writing values to the caller's slots.
 constexpr int64_t kBinnedQueryMin = 1 << 18;
 void launch_eval_binned(Grid& g, const float* pts, int64_t n, float* vals, float* grads, cudaStream_t s);
+// Lattice values on the brick tiles when the lattice is dense enough (about
+// >= 128 points per brick); false = not taken (caller uses the row kernel).
+// fac / cell: per-axis tables of k_axis_table (stages.cu), n: lattice size.
+bool launch_eval_lattice_brick(Grid& g, const float4* fac, const int* cell, int3 n, float* vals, cudaStream_t s);
 void launch_eval_sorted(Grid& g, const float* pts, int64_t n, const int64_t* offsets, float* vals, float* grads,
                         cudaStream_t s);
 void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, int64_t* offsets,

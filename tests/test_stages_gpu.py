@@ -111,6 +111,28 @@ def test_sample_grid_field_golden(oracle, z, case):
     assert_close(f.values, z[f"lat_{case}_vals"], 1e-6, what="lattice values")
 
 
+@pytest.mark.parametrize("dim,res,order,lat", [
+    (3, (40, 33, 29), 2, (97, 64, 51)),     # dense: brick tiles
+    (3, (17, 26, 12), 1, (120, 7, 60)),     # dense, one thin axis
+    (3, (50, 41, 37), 2, (9, 13, 6)),       # sparse: a thread per lattice point
+    (3, (33, 33, 33), 2, (33, 33, 33)),     # lattice on the vertices
+    (2, (70, 45), 2, (300, 211)),           # 2D dense
+    (2, (64, 64), 1, (5, 7)),               # 2D sparse
+])
+def test_sample_grid_field_brick_and_row_paths(oracle, dim, res, order, lat):
+    """Both lattice kernels (brick tiles for dense lattices, a thread per value
+    for sparse ones) against the oracle's sample_lattice."""
+    rng = np.random.default_rng(sum(res) + order)
+    s = Spec(dim=dim, res=res, order=order)
+    c = rng.normal(0, 0.2, s.V * s.K).astype(np.float32).astype(np.float64)
+    g = grid_from(dim, s.res, order, c)
+    if dim == 3:
+        got = tg.sample_grid_field(g, lat).values
+    else:
+        got = tg.sample_grid_field2(g, lat[0], lat[1]).values
+    assert_close(got, oracle.sample_lattice(s, c, lat), 1e-6, what="lattice values")
+
+
 def test_sample_grid_field_device_and_errors(oracle):
     import torch
     rng = np.random.default_rng(5)
