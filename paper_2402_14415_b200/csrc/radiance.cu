@@ -43,6 +43,42 @@ struct RayArgs {
     Status* st;
 };
 
+// Vector float reductions into L2 (red.global.add.v2/.v4.f32, sm_90+): one
+// L2 atomic per 8 / 16 bytes instead of one per float. red_block adds N
+// consecutive floats, choosing v4 / v2 / scalar pieces from the destination's
+// alignment (the K- and 3B-float vertex blocks sit at any 4-byte offset).
+__device__ __forceinline__ void red_v2(float* p, float a, float b) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void red_v4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+template <int N, int I, int OFF>
+__device__ __forceinline__ void red_rec(float* d, const float* v) {
+    if constexpr (I < N) {
+        constexpr int pos = (OFF + I) & 3;  // float position of d + I within its 16-byte line
+        if constexpr (pos == 0 && I + 4 <= N) {
+            red_v4(d + I, v[I], v[I + 1], v[I + 2], v[I + 3]);
+            red_rec<N, I + 4, OFF>(d, v);
+        } else if constexpr ((pos & 1) == 0 && I + 2 <= N) {
+            red_v2(d + I, v[I], v[I + 1]);
+            red_rec<N, I + 2, OFF>(d, v);
+        } else {
+            atomicAdd(d + I, v[I]);
+            red_rec<N, I + 1, OFF>(d, v);
+        }
+    }
+}
+template <int N>
+__device__ __forceinline__ void red_block(float* d, const float* v) {
+    switch ((reinterpret_cast<uintptr_t>(d) >> 2) & 3) {
+        case 0: red_rec<N, 0, 0>(d, v); break;
+        case 1: red_rec<N, 0, 1>(d, v); break;
+        case 2: red_rec<N, 0, 2>(d, v); break;
+        default: red_rec<N, 0, 3>(d, v); break;
+    }
+}
+
 __device__ __forceinline__ double sigmoid_dd(double x) { return 1.0 / (1.0 + exp(-x)); }
 
 template <int DEG>
@@ -268,24 +304,32 @@ __global__ void __launch_bounds__(256) k_rays(RayArgs A) {
                         for (int q = 0; q < K; ++q) G[q] = 0.0f;
                         corner_grad<3, ORDER, K>(corner_geom<3>(A.ds, ax, cc), (float)dl_draw, gv, G);
                         const long long vid = base + (cc & 1) + ((cc >> 1) & 1) * A.ds.sy + ((cc >> 2) & 1) * A.ds.sz;
-#pragma unroll
-                        for (int q = 0; q < K; ++q) atomicAdd(A.gd + vid * K + q, G[q]);
+                        red_block<K>(A.gd + vid * K, G);
                     }
                 }
             }
             if (A.gsh) {
+                double dl_dpre[3];
+                bool any = false;
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
                     const double c = s.color[ch];
-                    const double dl_dpre = g[ch] * w * c * (1.0 - c);
-                    if (dl_dpre == 0.0) continue;
+                    dl_dpre[ch] = g[ch] * w * c * (1.0 - c);
+                    any |= dl_dpre[ch] != 0.0;
+                }
+                if (any) {
+                    // the corner's whole 3B-float SH block in one vector reduction
 #pragma unroll
                     for (int cc = 0; cc < 8; ++cc) {
-                        const double f = s.shw[cc] * dl_dpre;
                         const long long vid = s.shv + (cc & 1) + ((cc >> 1) & 1) * A.ss.sy + ((cc >> 2) & 1) * A.ss.sz;
-                        float* k = A.gsh + vid * C + ch * B;
+                        float gb[C];
 #pragma unroll
-                        for (int b = 0; b < B; ++b) atomicAdd(k + b, (float)(f * basis[b]));
+                        for (int ch = 0; ch < 3; ++ch) {
+                            const double f = s.shw[cc] * dl_dpre[ch];
+#pragma unroll
+                            for (int b = 0; b < B; ++b) gb[ch * B + b] = (float)(f * basis[b]);
+                        }
+                        red_block<C>(A.gsh + vid * C, gb);
                     }
                 }
             }
