@@ -319,6 +319,42 @@ __device__ __forceinline__ void unpack_p2(const float2 (&P)[5], float* G) {
     G[8] = P[4].x; G[9] = P[4].y;
 }
 
+// Vector float reductions into L2 (red.global.add.v2/.v4.f32, sm_90+): one
+// L2 atomic per 8 / 16 bytes instead of one per float. red_block adds N
+// consecutive floats, choosing v4 / v2 / scalar pieces from the destination's
+// alignment (the K- and 3B-float vertex blocks sit at any 4-byte offset).
+__device__ __forceinline__ void red_v2(float* p, float a, float b) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void red_v4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+template <int N, int I, int OFF>
+__device__ __forceinline__ void red_rec(float* d, const float* v) {
+    if constexpr (I < N) {
+        constexpr int pos = (OFF + I) & 3;  // float position of d + I within its 16-byte line
+        if constexpr (pos == 0 && I + 4 <= N) {
+            red_v4(d + I, v[I], v[I + 1], v[I + 2], v[I + 3]);
+            red_rec<N, I + 4, OFF>(d, v);
+        } else if constexpr ((pos & 1) == 0 && I + 2 <= N) {
+            red_v2(d + I, v[I], v[I + 1]);
+            red_rec<N, I + 2, OFF>(d, v);
+        } else {
+            atomicAdd(d + I, v[I]);
+            red_rec<N, I + 1, OFF>(d, v);
+        }
+    }
+}
+template <int N>
+__device__ __forceinline__ void red_block(float* d, const float* v) {
+    switch ((reinterpret_cast<uintptr_t>(d) >> 2) & 3) {
+        case 0: red_rec<N, 0, 0>(d, v); break;
+        case 1: red_rec<N, 0, 1>(d, v); break;
+        case 2: red_rec<N, 0, 2>(d, v); break;
+        default: red_rec<N, 0, 3>(d, v); break;
+    }
+}
+
 // Per-point loss chain in fp64 (point_terms_chunk, sdf_loss.cpp:51-74).
 struct LossDev {
     double k;

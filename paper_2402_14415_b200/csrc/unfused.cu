@@ -8,8 +8,8 @@
 
 namespace tgcu {
 
-// Scatter-add of one point's 2^D*K coefficient gradients with native fp32
-// reductions (REDG.E.ADD.F32).
+// Scatter-add of one point's 2^D*K coefficient gradients with vector fp32
+// reductions (red_block: REDG.E.ADD.F32x4 / x2 / scalar by alignment).
 template <int DIM, int ORDER>
 __device__ __forceinline__ void scatter_point(const DevSpec& s, const AxisF* ax, long long base, float u,
                                               const float* gv, float* __restrict__ grad) {
@@ -22,9 +22,7 @@ __device__ __forceinline__ void scatter_point(const DevSpec& s, const AxisF* ax,
         for (int q = 0; q < K; ++q) G[q] = 0.0f;
         corner_grad<DIM, ORDER, K>(g, u, gv, G);
         const long long vid = base + (c & 1) + ((c >> 1) & 1) * s.sy + (DIM == 3 ? ((c >> 2) & 1) * s.sz : 0);
-        float* dst = grad + vid * K;
-#pragma unroll
-        for (int q = 0; q < K; ++q) atomicAdd(dst + q, G[q]);
+        red_block<K>(grad + vid * K, G);
     }
 }
 
