@@ -198,12 +198,17 @@ def unique_vertices(pts, res, zlo=0, zhi=None):
     return int(np.unique(np.concatenate(ids)).size)
 
 
-def traffic_from_profile():
+def traffic_from_profile(key="dram_bytes_per_launch"):
+    """The fused kernel's DRAM bytes per launch (or its L2 hit rate) from the
+    committed ncu capture (profiles/ncu_traffic.json, tools/ncu_traffic.py)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("k_brick_step", {}).get("dram_bytes_per_launch")
+        if key == "dram_bytes_per_launch":
+            return d.get("k_brick_step", {}).get(key)
+        ks = [v for k, v in d.get("kernels", {}).items() if k.startswith("k_brick_step")]
+        return ks[-1].get(key) if ks else None
     except Exception:
         return None
 
@@ -282,23 +287,29 @@ def count_unique_vertices(pts_dev, res, order_K):
     return int(mark.sum().item())
 
 
-def query_leg(device, hbm_peak, reps=10):
+def query_leg(device, hbm_peak, reps=10, ws=1, rank=0):
     """C4: 512^3 forward-only query, orders 1 and 2, 2^26 uniform points,
-    unsorted (direct gather) and brick-sorted (smem tile) kernels."""
+    unsorted (binned inside the call) and brick-sorted (smem tile) kernels.
+    With N ranks the grid is replicated and the points sharded (rank r takes
+    the r-th contiguous N-th of the same seeded set; no collective); times are
+    the max over ranks, throughput = all points / that time."""
     import torch
     import paper_2402_14415_b200 as tg
     res = (512, 512, 512)
     n = 1 << 26
-    pts = torch.empty((n, 3), dtype=torch.float32, device=f"cuda:{device}")
-    tg.sample_uniform_device(3, 4242, pts)
+    full = torch.empty((n, 3), dtype=torch.float32, device=f"cuda:{device}")
+    tg.sample_uniform_device(3, 4242, full)
+    m = n // ws
+    pts = full[rank * m:(rank + 1) * m] if ws > 1 else full
     spts = torch.empty_like(pts)
-    vals = torch.empty(n, dtype=torch.float32, device=pts.device)
+    vals = torch.empty(pts.shape[0], dtype=torch.float32, device=pts.device)
     st = torch.cuda.current_stream()
     out = {}
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    U = count_unique_vertices(pts, res, 1)
+    U = count_unique_vertices(full, res, 1)
+    del full
     offs = None
     for order in (1, 2):
         g = tg.init_grid(tg.GridSpec(dim=3, resolution=res, order=order),
@@ -313,7 +324,7 @@ def query_leg(device, hbm_peak, reps=10):
             tg.sort_points(g, pts, spts, None, offs)
             t1.record(st)
             torch.cuda.synchronize()
-            out["sort_ms"] = t0.elapsed_time(t1)
+            out["sort_ms"] = max_over_ranks(t0.elapsed_time(t1), ws)
         alg = n * (4 * 3 + 4) + U * K * 4
 
         def run(mode):
@@ -325,17 +336,19 @@ def query_leg(device, hbm_peak, reps=10):
         for mode in ("unsorted", "sorted"):
             run(mode)  # warm-up
             torch.cuda.synchronize()
+            barrier(ws)
             t0.record(st)
             for _ in range(reps):
                 run(mode)
             t1.record(st)
             torch.cuda.synchronize()
-            ms = t0.elapsed_time(t1) / reps
+            ms = max_over_ranks(t0.elapsed_time(t1) / reps, ws)
             gbs = alg / (ms * 1e-3) / 1e9
             out[f"o{order}_{mode}"] = {"gpts_per_s": n / (ms * 1e-3) / 1e9, "ms": ms, "achieved_gbs": gbs,
                                       "frac": gbs / hbm_peak}
         g.close()
     out["points"] = n
+    out["sharding"] = f"grid replicated, points sharded over {ws} rank(s)" if ws > 1 else "single GPU"
     out["unique_vertices"] = U
     out["grid"] = list(res)
     out["algorithmic_bytes"] = "N*(4D+4) + U*K*4 (SURVEY 8d B_q)"
@@ -453,12 +466,17 @@ def main():
         barrier(ws)
 
         q = None
-        if not args.no_query and rank == 0 and ws == 1:
-            q = query_leg(dev, hbm_peak)
+        if not args.no_query:
+            q = query_leg(dev, hbm_peak, ws=ws, rank=rank)
 
     clk = clocks.summary()
     value = npts_global * args.steps / (ms_total * 1e-3)  # whole job: one global batch per step
     kern_ms = brick_ms / max(brick_n, 1)
+    per_rank_ms = [kern_ms]
+    if ws > 1:  # per-GPU load imbalance of the fused kernel (report imbalance)
+        import torch.distributed as dist
+        per_rank_ms = [None] * ws
+        dist.all_gather_object(per_rank_ms, kern_ms)
     if ws == 1:
         vk_local, pts_local = VK, NPTS
     else:  # this rank's kernel: its owned vertex planes and its local points
@@ -486,10 +504,13 @@ def main():
                    "grid": list(res), "order": ORDER, "points_per_step": npts_global,
                    "parallelism": f"z-slab x{ws} (owner computes, NCCL all-reduce + halo planes)" if ws > 1
                    else "single GPU",
-                   "l2": "no flush: every step streams p,m,v (503 MB) + points, > 126 MB L2"},
+                   "l2": f"no flush: every step streams p,m,v ({24 * vk_local / 1e6:.0f} MB per GPU) + points, > the "
+                         f"{torch.cuda.get_device_properties(dev).L2_cache_size / 2**20:.0f} MiB L2 "
+                         f"(cudaDevAttrL2CacheSize)"},
         "roofline": {"bound": "hbm", "kernel": "k_brick_step<3,2,true> (fused loss+backward+TV+Adam)",
                      "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic_from_profile(),
+                     "frac_nominal_8tbs": achieved / 8000.0, "l2_hit_pct": traffic_from_profile("l2_hit_pct"),
                      "algorithmic_bytes_per_launch": bt_local,
                      "algorithmic_bytes_def": "SURVEY 8d B_t = N*(4D+4) + 3*U*K*4 + 8*V*K*4 with U = unique vertices "
                                               "touched, counted exactly per batch (mean over the batches)"
@@ -512,6 +533,11 @@ def main():
         "clocks": clk,
         "loss_last": last.total,
     }
+    if ws > 1:
+        line["per_rank_kernel_ms"] = per_rank_ms
+        line["kernel_imbalance_max_over_mean"] = max(per_rank_ms) / (sum(per_rank_ms) / ws)
+        line["halo"] = ("fused: boundary planes stored into the neighbours' halo by the brick kernel (peer memory)"
+                        if getattr(trainer, "fused_halo", False) else "NCCL send/recv of the boundary planes")
     if q is not None:
         line["query"] = q
     if rank == 0 and ws == 1 and not args.no_configs:
