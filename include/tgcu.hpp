@@ -106,6 +106,22 @@ public:
         return t;
     }
 
+    // Pipelined form of train_step (the cmd_bench loop at full speed): the
+    // host batch is copied on the library's copy stream while earlier steps
+    // compute, nothing synchronises; `samples` must stay valid until sync().
+    // Errors surface from sync() with the grid rolled back to the last
+    // committed step (NumericalError / std::invalid_argument as above).
+    void train_step_async(std::span<const float> samples, const LossConfig& cfg) {
+        const tgcu_loss_config c = cfg.c();
+        check(tgcu_train_step(h_, samples.data(), static_cast<int64_t>(samples.size() / 4), &c, nullptr,
+                              TGCU_HOST | TGCU_ASYNC, nullptr));
+    }
+    LossTerms sync() {
+        LossTerms t{};
+        check(tgcu_sync(h_, &t));
+        return t;
+    }
+
     tgcu_grid_spec spec() const {
         tgcu_grid_spec s{};
         tgcu_grid_spec_of(h_, &s);

@@ -21,6 +21,11 @@ int main() {
         if (s == 0) first = t.total;
         last = t.total;
     }
+    // pipelined host steps continue the same trajectory
+    for (int s = 0; s < 10; ++s) g.train_step_async(smp, lc);
+    const auto ta = g.sync();
+    if (!(ta.total < first) || !std::isfinite(ta.total)) return 9;
+    last = ta.total;
     std::vector<float> pts = {0.f, 0.f, 0.f, 0.6f, 0.f, 0.f};
     std::vector<float> grad;
     const auto v = g.eval(pts, &grad);
