@@ -350,10 +350,15 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
     double recon = 0.0, eik = 0.0, tvs = 0.0;
     if (!F.reduced) {
         double a = 0.0, b = 0.0, c = 0.0;
+        // 16-byte loads, unrolled so a thread's loads are all in flight
+        // before its (fixed-order) sums
+        const double2* P2 = reinterpret_cast<const double2*>(F.partials);
+#pragma unroll 4
         for (int i = tid; i < F.NB; i += NTH) {
-            a += F.partials[4 * i];
-            b += F.partials[4 * i + 1];
-            c += F.partials[4 * i + 2];
+            const double2 x = __ldg(P2 + 2 * i), y = __ldg(P2 + 2 * i + 1);
+            a += x.x;
+            b += x.y;
+            c += y.x;
         }
         a = warp_sum_d(a);
         b = warp_sum_d(b);
