@@ -21,15 +21,22 @@ tg.LIB_PATH = os.path.abspath(sys.argv[1])
 
 def main():
     import torch
-    spec = tg.GridSpec(dim=3, resolution=(128,) * 3, order=2)
+    # argv[2] = "c3": 256^3, 2^21 points of the 64-primitive SDF (50 % near, sigma 0.01); default C2
+    c3 = len(sys.argv) > 2 and sys.argv[2] == "c3"
+    res = 256 if c3 else 128
+    spec = tg.GridSpec(dim=3, resolution=(res,) * 3, order=2)
     g = tg.init_grid(spec)
     g.adam_reset(tg.AdamConfig(lr=1e-2))
-    batches = [torch.from_numpy(tg.sample(tg.SHAPE_SPHERE, 3, 1000 + i, 1 << 20, near_frac=0.5, sigma=0.01,
-                                          param0=0.6)).cuda() for i in range(4)]
+    if c3:
+        host = [tg.sample(tg.SHAPE_PRIMS, 3, 500 + i, 1 << 21, near_frac=0.5, sigma=0.01, param0=42) for i in range(2)]
+    else:
+        host = [tg.sample(tg.SHAPE_SPHERE, 3, 1000 + i, 1 << 20, near_frac=0.5, sigma=0.01, param0=0.6)
+                for i in range(4)]
+    batches = [torch.from_numpy(h).cuda() for h in host]
     for i in range(40):
-        tg.train_step(g, batches[i % 4], asynchronous=True)
+        tg.train_step(g, batches[i % len(batches)], asynchronous=True)
     g.sync()
-    nb = 16 ** 3
+    nb = (res // 8) ** 3
     ph = np.zeros(nb * 12, dtype=np.uint64)
     L = tg.lib()
     L.tgcu_phase_dump.argtypes = [C.c_void_p, C.c_int]
