@@ -29,6 +29,7 @@
 //   the host reads the sticky error.
 #include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 
+#include <atomic>
 #include <climits>
 
 #include "dispatch.cuh"
@@ -1254,15 +1255,17 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         ensure_bin_hist(g, (int64_t)ncta * g.NB, n, (g.NB + kColBricks - 1) / kColBricks);
         const size_t sm = sizeof(int) * g.NB;
         const size_t csm = sizeof(int) * ncta * (kColBricks + 1);
-        static bool attr = false;
-        if (!attr) {
+        // function attributes are per device: set them once for each device used
+        static std::atomic<unsigned long long> attr_devs{0};
+        const unsigned long long dbit = 1ull << (g.device & 63);
+        if (!(attr_devs.load() & dbit)) {
             TGCU_CUDA(cudaFuncSetAttribute(k_bin_hist<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBinSmemMax));
             TGCU_CUDA(cudaFuncSetAttribute(k_bin_hist<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBinSmemMax));
             TGCU_CUDA(cudaFuncSetAttribute(k_bin_scatter_tiles<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBinSmemMax));
             TGCU_CUDA(cudaFuncSetAttribute(k_bin_scatter_tiles<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBinSmemMax));
             TGCU_CUDA(cudaFuncSetAttribute(k_bin_cols, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(sizeof(int) * kMaxBinTiles * (kColBricks + 1))));
-            attr = true;
+            attr_devs.fetch_or(dbit);
         }
         if (g.spec.dim == 3) k_bin_hist<3><<<ncta, kBinThreads, sm, bs>>>(B, g.bin_hist, g.bin_codes, (int)g.NB);
         else k_bin_hist<2><<<ncta, kBinThreads, sm, bs>>>(B, g.bin_hist, g.bin_codes, (int)g.NB);
@@ -1366,12 +1369,13 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         static_assert(BrickSmem<DIM, ORDER>::bytes <= 227 * 1024, "brick smem");
         auto kern = grad_out ? (eik ? k_brick_step<DIM, ORDER, true, true> : k_brick_step<DIM, ORDER, false, true>)
                              : (eik ? k_brick_step<DIM, ORDER, true, false> : k_brick_step<DIM, ORDER, false, false>);
-        static bool configured = false;
-        if (!configured) {
+        static std::atomic<unsigned long long> configured_devs{0};
+        const unsigned long long cbit = 1ull << (g.device & 63);
+        if (!(configured_devs.load() & cbit)) {
             for (auto k : {k_brick_step<DIM, ORDER, true, true>, k_brick_step<DIM, ORDER, false, true>,
                            k_brick_step<DIM, ORDER, true, false>, k_brick_step<DIM, ORDER, false, false>})
                 TGCU_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            configured = true;
+            configured_devs.fetch_or(cbit);
         }
         if (g.prof_on) prof_mark(g, s, 0);
         if (g.bd_on) bd_mark(g, s, 3);
