@@ -277,6 +277,9 @@ int tgcu_trace(tgcu_grid* g, tgcu_loss_terms* out, int count);
  * mean ms of {brick histogram, column pass, scatter, brick kernel, finalize}. */
 int tgcu_step_breakdown(tgcu_grid* g, int enable, double* mean_ms5, int* steps);
 int tgcu_profile_begin(tgcu_grid* g);
+/* Time only every `every`-th fused brick launch (events around a launch cost
+ * the stream ~3 us each); tgcu_profile_end then reports the sampled launches. */
+int tgcu_profile_every(tgcu_grid* g, int every);
 int tgcu_profile_end(tgcu_grid* g, double* total_ms, int* launches);
 
 /* ---- stage transitions, lattice query, .tgrid I/O ---------- */

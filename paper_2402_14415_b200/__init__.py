@@ -145,6 +145,7 @@ def lib():
     L.tgcu_trace.argtypes = [P, C.POINTER(_Terms), C.c_int]
     L.tgcu_launch_count.restype = C.c_int64
     L.tgcu_profile_begin.argtypes = [P]
+    L.tgcu_profile_every.argtypes = [P, C.c_int]
     L.tgcu_profile_end.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_int)]
     L.tgcu_sample.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int64, C.c_double, C.c_double, C.c_double, P]
     L.tgcu_sample_uniform.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_double, C.c_double, P]
@@ -424,7 +425,9 @@ class TaylorGrid:
         _check(lib().tgcu_sync(self._h, C.byref(t)))
         return LossTerms._from(t)
 
-    def profile_begin(self):
+    def profile_begin(self, every: int = 1):
+        """Time the fused brick launches (every `every`-th one) until profile_end."""
+        _check(lib().tgcu_profile_every(self._h, int(every)))
         _check(lib().tgcu_profile_begin(self._h))
 
     def profile_end(self):

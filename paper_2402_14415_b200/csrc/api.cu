@@ -1096,6 +1096,13 @@ int tgcu_step_breakdown(tgcu_grid* h, int enable, double* mean_ms5, int* steps) 
     });
 }
 
+int tgcu_profile_every(tgcu_grid* h, int every) {
+    return guard([&] {
+        require(every >= 1, "profile_every: must be >= 1");
+        h->g.prof_every = every;
+    });
+}
+
 int tgcu_profile_end(tgcu_grid* h, double* total_ms, int* launches) {
     return guard([&] {
         Grid& g = h->g;

@@ -157,6 +157,8 @@ struct Grid {
     // Live kernel timing (tgcu_profile_*): CUDA events recorded on the launch
     // stream around the fused brick kernel.
     bool prof_on = false;
+    int prof_every = 1;          // time every n-th brick launch
+    bool prof_this = false;      // the current launch is timed
     std::vector<cudaEvent_t> prof_ev;  // pairs (start, end)
     size_t prof_used = 0;
     // Step breakdown (tgcu_step_breakdown, diagnostics): events at the

@@ -1377,12 +1377,13 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
                 TGCU_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             configured_devs.fetch_or(cbit);
         }
-        if (g.prof_on) prof_mark(g, s, 0);
+        g.prof_this = g.prof_on && (g.steps_launched % g.prof_every) == 0;
+        if (g.prof_this) prof_mark(g, s, 0);
         if (g.bd_on) bd_mark(g, s, 3);
         kern<<<bgrid, BrickShape<DIM>::NT, smem, s>>>(A);
         TGCU_CUDA(cudaEventRecord(g.ev_bfree[k], s));
         if (g.bd_on) bd_mark(g, s, 4);
-        if (g.prof_on) prof_mark(g, s, 1);
+        if (g.prof_this) prof_mark(g, s, 1);
     });
 
     k_step_finalize<<<1, 1024, 0, s>>>(F);

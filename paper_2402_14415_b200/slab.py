@@ -246,7 +246,8 @@ class SlabGrid:
         _check(lib().tgcu_slab_peer_probe(self._h, int(phase), C.byref(ok)))
         return bool(ok.value)
 
-    def profile_begin(self):
+    def profile_begin(self, every: int = 1):
+        _check(lib().tgcu_profile_every(self._h, int(every)))
         _check(lib().tgcu_profile_begin(self._h))
 
     def profile_end(self):
