@@ -439,7 +439,7 @@ def main():
         l0 = tg.launch_count()
         # the brick kernel is timed live on every 8th step: event pairs around
         # every launch would cost the stream ~6 us per step
-        g.profile_begin(every=8)
+        g.profile_begin(every=8 if args.steps >= 64 else 1)
         ev0.record(stream)
         for i in range(args.steps):
             step(dev_batches[i % NBATCH])

@@ -85,6 +85,16 @@ __device__ __forceinline__ unsigned long long spread3(unsigned long long x) {
     x = (x | x << 2) & 0x1249249249249249ULL;
     return x;
 }
+// 32-bit spread of a 10-bit value (brick coordinates: at most 512 bricks per
+// axis), a third of the 64-bit version's instructions.
+__device__ __forceinline__ unsigned int spread3_10(unsigned int x) {
+    x &= 0x3ffu;
+    x = (x | x << 16) & 0x030000ffu;
+    x = (x | x << 8) & 0x0300f00fu;
+    x = (x | x << 4) & 0x030c30c3u;
+    x = (x | x << 2) & 0x09249249u;
+    return x;
+}
 __device__ __forceinline__ unsigned long long spread2(unsigned long long x) {
     x &= 0xffffffffULL;
     x = (x | x << 16) & 0x0000ffff0000ffffULL;
@@ -316,8 +326,8 @@ __global__ void __launch_bounds__(256, query_min_blocks<KOf<DIM, ORDER>::value>(
     __shared__ __align__(8) unsigned long long bar;
 
     const int ox = (int)blockIdx.x * B, oy = (int)blockIdx.y * B, oz = DIM == 3 ? (int)blockIdx.z * B : 0;
-    const unsigned int code = DIM == 3 ? (unsigned int)(spread3(blockIdx.x) | (spread3(blockIdx.y) << 1) |
-                                                        (spread3(blockIdx.z) << 2))
+    const unsigned int code = DIM == 3 ? (spread3_10(blockIdx.x) | (spread3_10(blockIdx.y) << 1) |
+                                          (spread3_10(blockIdx.z) << 2))
                                        : (unsigned int)(spread2(blockIdx.x) | (spread2(blockIdx.y) << 1));
     long long p0, p1;
     int2 lr[3] = {{0, 1}, {0, 1}, {0, 1}};  // lattice index range per axis
