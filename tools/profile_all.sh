@@ -21,6 +21,10 @@ python tools/prof_query.py --order 2 --reps 1 > $OUT/pa_query.log 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k "regex:k_eval_brick<.int.3, .int.2, .bool.0, .int.3, .int.0>" -c 1 -o $OUT/query_o2_$TAG -f \
     python tools/prof_query.py --order 2 --reps 1 > $OUT/pa_ncu_query.log 2>&1
+python tools/prof_query.py --order 1 --reps 1 > $OUT/pa_query1.log 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k "regex:k_eval_brick<.int.3, .int.1, .bool.0, .int.3, .int.0>" -c 1 -o $OUT/query_o1_$TAG -f \
+    python tools/prof_query.py --order 1 --reps 1 > $OUT/pa_ncu_query1.log 2>&1
 python tools/prof_radiance.py --no-margins > $OUT/pa_rays.log 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_rays<.int.2, .int.2, .bool.1>" \
     -c 1 -o $OUT/rays_$TAG -f python tools/prof_radiance.py --no-margins > $OUT/pa_ncu_rays.log 2>&1
