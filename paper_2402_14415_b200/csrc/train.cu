@@ -14,14 +14,17 @@
 //     1. stage the (B+2)^D vertex tile of the current parameters in smem
 //        (owned vertices + one-vertex halo: the cells' corners and the TV
 //        stencil neighbours);
-//     2. per chunk of points: forward eval from the tile (fp64 locate, fp32
-//        blend), the fp64 loss chain, then a counting sort of the chunk by
-//        cell in smem; each owned-vertex thread then gathers the
-//        contributions of the points in its 2^D incident cells into K
-//        register accumulators (no atomics anywhere);
+//     2. per chunk of points: fp64 locate and a counting sort of the chunk
+//        by cell in smem (cell runs reserved per warp), then the forward eval
+//        from the tile (fp32 blend) and the loss chain, each point's record
+//        written straight into its cell's run; each owned-vertex thread then
+//        gathers the contributions of the points in its 2^D incident cells
+//        into K register accumulators (no global atomics);
 //     3. TV gradient from the tile stencil + Adam over the owned
 //        coefficients, reading m/v and writing p/m/v to the other ping-pong
 //        buffers (coalesced rows), plus the per-brick loss partials.
+//   The binning of a step runs on a library stream into one of two bin sets,
+//   so it overlaps the previous step's brick kernel (launch_train_step).
 //   A 1-CTA finalize kernel reduces the partials in a fixed order, applies the
 //   reference's error order (NaN point, non-finite loss, non-finite gradient)
 //   and commits the step by naming the new current buffer; a failed step
