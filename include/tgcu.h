@@ -220,7 +220,8 @@ int tgcu_slab_info(const tgcu_grid* g, int* z_store_lo, int* z_store_n, int* z_o
 /* samples: the n points this rank reads (the full global batch, or only the
  * points whose cells touch this slab's owned planes — slab.py
  * slab_point_mask); n_global: the global batch size for the loss scale 1/N
- * (<= 0: n). */
+ * (<= 0: n). n may be 0 when n_global > 0 (a slab holding none of the
+ * batch's points still applies TV and Adam to its vertices). */
 int tgcu_slab_step_begin(tgcu_grid* g, const float* samples, int64_t n, int64_t n_global,
                          const tgcu_loss_config* cfg, double** partials, int flags, void* stream);
 int tgcu_slab_step_finish(tgcu_grid* g, const double* reduced, tgcu_loss_terms* out, int flags, void* stream);

@@ -863,7 +863,8 @@ int tgcu_slab_step_begin(tgcu_grid* h, const float* samples, int64_t n, int64_t 
         require(cfg != nullptr && partials != nullptr, "slab_step_begin: NULL argument");
         require(cfg->lambda1 >= 0.0 && cfg->lambda2 >= 0.0, "LossConfig: lambda weights must be >= 0");
         require(cfg->k > 0.0, "LossConfig: weight sharpness k must be > 0");
-        require(n > 0, "total_loss: empty batch");
+        // a rank may hold no points of a (non-empty) global batch: TV + Adam only
+        require(n >= 0 && (n > 0 || n_global > 0), "total_loss: empty batch");
         cudaStream_t s = as_stream(stream);
         ensure_optimizer(g);
         const float4* ds = reinterpret_cast<const float4*>(samples);

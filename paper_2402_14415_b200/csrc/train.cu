@@ -1253,7 +1253,14 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     int* const off = g.bin_off[k];
     const int ncta_tiles = (int)((n + kBinTile - 1) / kBinTile);
     if (g.bd_on) bd_mark(g, bs, 0);
-    if (g.NB <= kBinSmemMax && ncta_tiles <= kMaxBinTiles) {
+    if (n == 0) {
+        // a slab rank with no local points: every brick empty (TV + Adam only)
+        TGCU_CUDA(cudaMemsetAsync(off, 0, sizeof(int) * (g.NB + 1), bs));
+        if (g.bd_on) {
+            bd_mark(g, bs, 1);
+            bd_mark(g, bs, 2);
+        }
+    } else if (g.NB <= kBinSmemMax && ncta_tiles <= kMaxBinTiles) {
         const int ncta = ncta_tiles;
         ensure_bin_hist(g, (int64_t)ncta * g.NB, n, (g.NB + kColBricks - 1) / kColBricks);
         const size_t sm = sizeof(int) * g.NB;

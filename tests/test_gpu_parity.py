@@ -410,6 +410,44 @@ def test_slab_two_on_one_gpu_matches_full_grid(nslab, res, sharded, fused):
         assert np.array_equal(cs[r - 1][b:b + plane], cs[r][a:a + plane])
 
 
+def test_slab_with_no_local_points_matches_full_grid():
+    """A slab whose cells hold none of the batch's points (all points below
+    it) still takes its TV + Adam step: n = 0 local points with the global
+    batch size, against the full-grid trajectory."""
+    from paper_2402_14415_b200.slab import SlabGrid, brick_layers, device_view, slab_point_mask, slab_ranges
+    res = (24, 20, 40)
+    spec = tg.GridSpec(dim=3, resolution=res, order=2)
+    init = tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.02, seed=5)
+    cfg = tg.LossConfig()
+    full = tg.init_grid(spec, init)
+    full.adam_reset(tg.AdamConfig(lr=1e-2))
+    ranges = slab_ranges(brick_layers(res[2]), 2)
+    slabs = [SlabGrid(spec, lo, hi, init) for lo, hi in ranges]
+    for sg in slabs:
+        sg.adam_reset(tg.AdamConfig(lr=1e-2))
+    K = spec.coeffs_per_vertex()
+    plane = res[0] * res[1] * K
+    for step in range(4):
+        b = tg.sample(tg.SHAPE_SPHERE, 3, 700 + step, 5000, near_frac=0.0)
+        b[:, 2] = -1.0 + (b[:, 2] + 1.0) * 0.3   # z in [-1, -0.4]: only the lower slab's cells
+        tf = tg.train_step(full, b, cfg).as_array()
+        local = [np.ascontiguousarray(b[slab_point_mask(spec, b.astype(np.float64), *rg)]) for rg in ranges]
+        assert len(local[1]) == 0
+        parts = [sg.begin(lp, cfg, n_global=len(b)) for sg, lp in zip(slabs, local)]
+        views = [device_view(p, 5, "<f8") for p in parts]
+        tot = views[0].clone() + views[1]
+        for v in views:
+            v.copy_(tot)
+        terms = [sg.finish(p).as_array() for sg, p in zip(slabs, parts)]
+        lo, hi = slabs[0].halo(), slabs[1].halo()
+        device_view(hi[2], lo[4]).copy_(device_view(lo[1], lo[4]))
+        device_view(lo[3], lo[4]).copy_(device_view(hi[0], lo[4]))
+        for t in terms:
+            assert_close(t, tf, 1e-6, floor=1e-30, what=f"terms step {step}")
+    owned = np.concatenate([sg.owned_coeffs() for sg in slabs])
+    assert_trajectory_close(owned, full.coeffs, 1e-2, 4, what="slab coefficients")
+
+
 def test_pipelined_host_steps_match_device_steps():
     """TGCU_HOST|TGCU_ASYNC (copy-stream pipelined host input) gives the same
     trajectory as device-resident async steps; host arrays alternate slots."""
