@@ -550,12 +550,13 @@ def main():
     if q is not None:
         line["query"] = q
     if rank == 0 and ws == 1 and not args.no_configs:
-        # BASELINE configs C3 (256^3, 2^21 pts) and C5 (512^3, 2^23 pts, 90% near-surface) on this GPU:
+        # BASELINE configs C1 (2D 128^2, parity config), C3 (256^3, 2^21 pts) and C5 (512^3, 2^23 pts,
+        # 90% near-surface) on this GPU:
         # step time and fraction of the HBM roofline (tools/bench_configs.py)
         sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
         import bench_configs
         with ClockSampler(dev) as cclk:
-            line["larger_configs"] = [bench_configs.run(c, 30, 5) for c in ("c3", "c5")]
+            line["larger_configs"] = [bench_configs.run(c, 30, 5) for c in ("c1", "c3", "c5")]
         line["larger_configs_clocks"] = cclk.summary()
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(host_batches)

@@ -17,6 +17,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 CONFIGS = {
+    "c1": dict(res=128, points=1 << 16, near=0.0, sigma=0.01, lr=1e-2, dim=2),
     "c3": dict(res=256, points=1 << 21, near=0.5, sigma=0.01, lr=1e-2),
     "c5": dict(res=512, points=1 << 23, near=0.9, sigma=0.005, lr=5e-3),
 }
@@ -43,11 +44,15 @@ def run(name, steps, warmup):
     import paper_2402_14415_b200 as tg
     cfg = CONFIGS[name]
     res = cfg["res"]
-    spec = tg.GridSpec(dim=3, resolution=(res,) * 3, order=2)
+    dim = cfg.get("dim", 3)
+    spec = tg.GridSpec(dim=dim, resolution=(res,) * dim + ((1,) if dim == 2 else ()), order=2)
     g = tg.init_grid(spec, tg.InitOptions(memory_cap_bytes=1 << 40))
     g.adam_reset(tg.AdamConfig(lr=cfg["lr"]))
-    host = [tg.sample(tg.SHAPE_PRIMS, 3, 500 + i, cfg["points"], near_frac=cfg["near"], sigma=cfg["sigma"],
-                      param0=42) for i in range(2)]
+    if dim == 2:  # C1: circle r=0.5 union box, uniform points (sampling.cpp C1 restatement)
+        host = [tg.sample(tg.SHAPE_C1_2D, 2, 500 + i, cfg["points"]) for i in range(2)]
+    else:
+        host = [tg.sample(tg.SHAPE_PRIMS, 3, 500 + i, cfg["points"], near_frac=cfg["near"], sigma=cfg["sigma"],
+                          param0=42) for i in range(2)]
     dev = [torch.from_numpy(b).cuda() for b in host]
     torch.cuda.synchronize()
     lc = tg.LossConfig()
@@ -65,17 +70,18 @@ def run(name, steps, warmup):
     last = g.sync()
     ms = e0.elapsed_time(e1) / steps
     K = spec.coeffs_per_vertex()
-    V = res ** 3
+    V = res ** dim
     N = cfg["points"]
-    UK = np.mean([unique_vertex_coeffs(b, res, K) for b in host])
-    bt = N * 16 + 3 * UK * 4 + 32 * V * K
+    # 2D: U ~= V (uniform points on 127^2 cells); 3D: counted exactly
+    UK = V * K if dim == 2 else np.mean([unique_vertex_coeffs(b, res, K) for b in host])
+    bt = N * (4 * dim + 4) + 3 * UK * 4 + 32 * V * K
     ours = 24 * V * K + 16 * N
     peak = 6549.1
     try:
         peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"]
     except Exception:
         pass
-    return {"config": name, "grid": [res] * 3, "order": 2, "points_per_step": N, "near_frac": cfg["near"],
+    return {"config": name, "grid": [res] * dim, "order": 2, "points_per_step": N, "near_frac": cfg["near"],
             "sigma": cfg["sigma"], "ms_per_step": ms, "points_per_s": N / (ms * 1e-3),
             "brick_kernel_ms": kms / max(kn, 1), "survey_bytes_per_step": bt,
             "step_frac_survey_bytes": bt / (ms * 1e-3) / 1e9 / peak,
