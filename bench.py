@@ -233,8 +233,16 @@ def cpu_baseline(batches, steps_cap=2):
 def run_reference(args):
     """--impl reference: the reference CPU implementation on the same config."""
     ws, rank, _ = dist_setup()
-    if rank != 0:
-        return
+    try:
+        if rank == 0:
+            _run_reference_rank0(args, ws)
+    finally:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+def _run_reference_rank0(args, ws):
     from oracle.pyoracle import Loss, Reference, Spec, reference_available
     if not reference_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtgref.so not built"}))
