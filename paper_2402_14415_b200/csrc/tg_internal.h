@@ -115,6 +115,7 @@ struct Grid {
     // kernels, which are serial on that stream.
     int* bin_count = nullptr;   // NB + 1 (fallback binning)
     int* bin_off[2] = {nullptr, nullptr};  // NB + 1 per set
+    int* brick_order[2] = {nullptr, nullptr};  // NB per set: launch order of the bricks
     int* bin_cursor = nullptr;  // NB (fallback binning)
     int* bin_hist = nullptr;    // per-tile brick histograms (privatized binning)
     int64_t bin_hist_cap = 0;

@@ -117,9 +117,33 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs A) {
     }
 }
 
+// Launch order of the bricks: those with more than one chunk of points first
+// (they take 4-7x as long, so the kernel should not end on one), the rest
+// after them. ord[NB], ord[NB + 1] count the two classes (zeroed per step);
+// one atomic per warp and class.
+__device__ __forceinline__ void place_brick(int brick, bool valid, int count, int ch, int NB, int* __restrict__ ord) {
+    const int lane = threadIdx.x & 31;
+    const bool heavy = valid && count > ch, light = valid && count <= ch;
+    const unsigned mh = __ballot_sync(0xffffffffu, heavy), ml = __ballot_sync(0xffffffffu, light);
+    int bh = 0, bl = 0;
+    if (lane == 0) {
+        if (mh) bh = atomicAdd(&ord[NB], __popc(mh));
+        if (ml) bl = atomicAdd(&ord[NB + 1], __popc(ml));
+    }
+    bh = __shfl_sync(0xffffffffu, bh, 0);
+    bl = __shfl_sync(0xffffffffu, bl, 0);
+    const unsigned lt = (1u << lane) - 1u;
+    if (heavy) ord[bh + __popc(mh & lt)] = brick;
+    if (light) ord[NB - 1 - (bl + __popc(ml & lt))] = brick;
+}
+
+__global__ void k_identity_order(int* __restrict__ ord, int NB) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < NB; b += gridDim.x * blockDim.x) ord[b] = b;
+}
+
 // Exclusive scan of NB brick counts -> off[0..NB], cursor = off. One CTA.
 __global__ void __launch_bounds__(1024) k_bin_scan(const int* __restrict__ count, int* __restrict__ off,
-                                                   int* __restrict__ cursor, int NB) {
+                                                   int* __restrict__ cursor, int NB, int ch, int* __restrict__ ord) {
     __shared__ int warp_tot[32];
     __shared__ int carry;
     if (threadIdx.x == 0) carry = 0;
@@ -151,6 +175,7 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const int* __restrict__ count
             off[i] = excl;
             cursor[i] = excl;
         }
+        place_brick(i, i < NB, c, ch, NB, ord);
         __syncthreads();
         if (threadIdx.x == blockDim.x - 1) carry = excl + c;
         __syncthreads();
@@ -226,7 +251,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __rest
 // are co-resident; CTA i waits for CTA i-1's inclusive prefix, tagged with
 // this launch's epoch).
 __global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta, int NB, int* __restrict__ off,
-                                                  int* __restrict__ chain, int epoch) {
+                                                  int* __restrict__ chain, int epoch, int chunk, int* __restrict__ ord) {
     extern __shared__ int col[];  // [ncta][kColBricks + 1]
     __shared__ int tot[kColBricks];
     __shared__ int carry;
@@ -303,6 +328,7 @@ __global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta,
         const int c0 = prev;
         if (lane < nb) off[b0 + lane] = c0 + x - t;
         if (blockIdx.x == gridDim.x - 1 && lane == 0) off[NB] = c0 + block_sum;
+        place_brick(b0 + lane, lane < nb, t, chunk, NB, ord);
     }
 }
 
@@ -462,6 +488,7 @@ struct StepArgs {
     float* peer_lo;
     float* peer_hi;
     int peer_hi_zb, peer_hi_lz;
+    const int* order;  // launch order of the bricks (1D grid): most chunks first
 };
 
 // Cell runs of a chunk's records: every cell gets the contiguous slot range
@@ -627,7 +654,10 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     constexpr int B = S::B, T = S::T, CE = S::CE, NT = S::NT, CH = S::CH, REC = L::REC;
     constexpr int NC = 1 << DIM;
     // brick index and its point range, loaded together with the error flag
-    const int b = ((int)blockIdx.z * A.nb[1] + (int)blockIdx.y) * A.nb[0] + (int)blockIdx.x;
+    // brick of this CTA: the launch order puts the multi-chunk bricks first so
+    // the kernel does not end on a long surface brick
+    const int b = A.order[blockIdx.x];
+    const int bcx = b % A.nb[0], bcy = (b / A.nb[0]) % A.nb[1], bcz = b / (A.nb[0] * A.nb[1]);
     const int err = A.st->error;
     const int p0 = A.off[b], p1 = A.off[b + 1];
     if (err) return;
@@ -653,7 +683,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     unsigned long long pt_tile = 0, pt_2a = 0, pt_scan = 0, pt_bal = 0, pt_2b = 0, pt_x;
 #endif
     // grid = (nb_x, nb_y, nb_z): brick coordinates without integer division
-    const int o[3] = {(int)blockIdx.x * B, (int)blockIdx.y * B, DIM == 3 ? (A.zb0 + (int)blockIdx.z) * B : 0};
+    const int o[3] = {bcx * B, bcy * B, DIM == 3 ? (A.zb0 + bcz) * B : 0};
     const int zrel = o[2] - A.s.zoff;  // first owned plane in the stored planes
     const bool tmap = L::TMAP && A.use_tmap;
 
@@ -1048,7 +1078,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     if constexpr (DIM == 3) {
         // fused halo: a slab-boundary plane's new parameters go straight into
         // the neighbour's halo plane (peer memory over NVLink), row by row
-        const int bz = (int)blockIdx.z + A.zb0;
+        const int bz = bcz + A.zb0;
         const bool lo = A.peer_lo && bz == A.zb0, hi = A.peer_hi && bz == A.peer_hi_zb;
         if (lo || hi) {
             const int nvx = min(B, A.s.res[0] - o[0]);
@@ -1251,11 +1281,15 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     B.nan = &g.st->nan_bin[k];
     B.zb0 = g.zb0;
     int* const off = g.bin_off[k];
+    int* const ord = g.brick_order[k];  // NB entries + 2 class counters
+    const int ch = g.spec.dim == 3 ? BrickShape<3>::CH : BrickShape<2>::CH;
+    TGCU_CUDA(cudaMemsetAsync(ord + g.NB, 0, 2 * sizeof(int), bs));
     const int ncta_tiles = (int)((n + kBinTile - 1) / kBinTile);
     if (g.bd_on) bd_mark(g, bs, 0);
     if (n == 0) {
         // a slab rank with no local points: every brick empty (TV + Adam only)
         TGCU_CUDA(cudaMemsetAsync(off, 0, sizeof(int) * (g.NB + 1), bs));
+        k_identity_order<<<grid_blocks(g.NB, 256), 256, 0, bs>>>(ord, (int)g.NB);
         if (g.bd_on) {
             bd_mark(g, bs, 1);
             bd_mark(g, bs, 2);
@@ -1282,7 +1316,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         if (g.bd_on) bd_mark(g, bs, 1);
         const int epoch = ++g.bin_epoch;
         k_bin_cols<<<(unsigned)((g.NB + kColBricks - 1) / kColBricks), 256, csm, bs>>>(
-            g.bin_hist, ncta, (int)g.NB, off, g.bin_chain, epoch);
+            g.bin_hist, ncta, (int)g.NB, off, g.bin_chain, epoch, ch, ord);
         if (g.bd_on) bd_mark(g, bs, 2);
         if (g.spec.dim == 3)
             k_bin_scatter_tiles<3><<<ncta, kBinThreads, sm, bs>>>(B, g.bin_hist, g.bin_codes, off, (int)g.NB);
@@ -1295,7 +1329,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         const int pblocks = grid_blocks(n, 256, 148 * 16);
         if (g.spec.dim == 3) k_bin_count<3><<<pblocks, 256, 0, bs>>>(B);
         else k_bin_count<2><<<pblocks, 256, 0, bs>>>(B);
-        k_bin_scan<<<1, 1024, 0, bs>>>(g.bin_count, off, g.bin_cursor, (int)g.NB);
+        k_bin_scan<<<1, 1024, 0, bs>>>(g.bin_count, off, g.bin_cursor, (int)g.NB, ch, ord);
         if (g.bd_on) bd_mark(g, bs, 2);
         if (g.spec.dim == 3) k_bin_scatter<3><<<pblocks, 256, 0, bs>>>(B);
         else k_bin_scatter<2><<<pblocks, 256, 0, bs>>>(B);
@@ -1337,6 +1371,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     A.st = g.st;
     A.grad_out = grad_out;
     A.zb0 = g.zb0;
+    A.order = g.brick_order[k];
     A.peer_lo = g.peer_lo[out_idx];
     A.peer_hi = g.peer_hi[out_idx];
     {
@@ -1373,7 +1408,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         A.tm_m_out = g.tm_own_m[out_idx];
         A.tm_v_out = g.tm_own_v[out_idx];
     }
-    const dim3 bgrid((unsigned)g.nb[0], (unsigned)g.nb[1], (unsigned)g.nb[2]);
+    const dim3 bgrid((unsigned)g.NB);
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
         constexpr size_t smem = BrickSmem<DIM, ORDER>::bytes;
         static_assert(BrickSmem<DIM, ORDER>::bytes <= 227 * 1024, "brick smem");
