@@ -78,7 +78,8 @@ typedef struct {
 } tgcu_init_options;
 
 /* tg::LossConfig (sdf_loss.hpp:15-25). batch_size is the caller's n;
- * the eikonal points are the batch itself (EikonalPointSource::ReuseBatch). */
+ * the eikonal points are the batch itself (EikonalPointSource::ReuseBatch)
+ * except through tgcu_train_step_fresh_eik (FreshUniform). */
 typedef struct {
     double lambda1;
     double lambda2;
@@ -200,6 +201,14 @@ int tgcu_adam_download_f64(tgcu_grid* g, double* m, double* v, int64_t n);
  * ordered after all earlier work on `stream`. */
 int tgcu_train_step(tgcu_grid* g, const float* samples, int64_t n, const tgcu_loss_config* cfg,
                     tgcu_loss_terms* out, int flags, void* stream);
+/* tgcu_train_step with EikonalPointSource::FreshUniform (sdf_loss.cpp:274-283):
+ * the reconstruction term on the batch, the eikonal term on eik_points (n x 3
+ * floats: the n points the reference draws per step with
+ * rng->uniform_in_box(origin, domain_max), tgcu_rng_uniform_box), each
+ * normalised by n; TV and Adam as tgcu_train_step. Host or device arrays per
+ * TGCU_HOST; not pipelined. lambda1 == 0 draws nothing (plain train step). */
+int tgcu_train_step_fresh_eik(tgcu_grid* g, const float* samples, int64_t n, const float* eik_points,
+                              const tgcu_loss_config* cfg, tgcu_loss_terms* out, int flags, void* stream);
 /* ---- multi-GPU z-slab training (owner computes) ----
  * A slab grid holds the brick layers [zb_lo, zb_hi) (bricks of 8^3 vertices)
  * of the global 3D spec: it owns (and Adam-updates) vertex planes
@@ -322,6 +331,9 @@ int tgcu_rng_create(uint64_t seed, tgcu_rng** out);
 void tgcu_rng_destroy(tgcu_rng* r);
 /* count draws of Rng::index(n) into out. */
 int tgcu_rng_index(tgcu_rng* r, uint64_t n, int64_t count, int64_t* out);
+/* Rng::uniform_in_box (rng.hpp:53-57): count points, axes 0..dim-1 drawn in
+ * order from [lo, hi), z = 0 in 2D, into out3 (count x 3 doubles). */
+int tgcu_rng_uniform_box(tgcu_rng* r, int dim, const double* lo, const double* hi, int64_t count, double* out3);
 /* fit_sdf's seeded Fisher-Yates order (sdf_fit.cpp:59-64); pass the
  * reference's seed (options.seed ^ 0x5deece66d). */
 int tgcu_shuffle_order(uint64_t seed, int64_t n, uint32_t* order);

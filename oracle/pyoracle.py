@@ -325,6 +325,9 @@ class Reference:
         L.tgr_total_loss.argtypes = sp + [_D, _D, C.c_int64, C.c_double, C.c_double, C.c_double,
                                           C.c_int, C.c_int, C.c_int, _D, C.c_int, _D]
         L.tgr_adam_step.argtypes = [_D, _D, _D, _D, C.c_int64, _L] + [C.c_double] * 4 + [C.c_int]
+        L.tgr_total_loss_fresh.argtypes = sp + [_D, _D, C.c_int64, C.c_double, C.c_double, C.c_double,
+                                                C.c_int, C.c_int, C.c_int, C.c_uint64, _D, C.c_int, _D]
+        L.tgr_eikonal_loss.argtypes = sp + [_D, _D, C.c_int64, C.c_double, _D, _D]
         L.tgr_train.argtypes = sp + [_D, _D, C.c_int64, C.c_int, C.c_double, C.c_double, C.c_double,
                                      C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                      C.c_double, C.c_int, _D, _D]
@@ -414,6 +417,25 @@ class Reference:
                                         int(cfg.use_tv), int(cfg.differentiate_weight), _dp(grad),
                                         threads, _dp(terms)))
         return terms
+
+    def total_loss_fresh(self, s: Spec, coeffs, samples, cfg: Loss, seed: int, grad=None, threads=1):
+        """total_loss with EikonalPointSource::FreshUniform and tg::Rng(seed)."""
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        samples = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 4)
+        terms = np.zeros(4)
+        self._err(self.L.tgr_total_loss_fresh(*_spec_args(s), _dp(coeffs), _dp(samples), len(samples),
+                                              cfg.lambda1, cfg.lambda2, cfg.k, int(cfg.use_weighting),
+                                              int(cfg.use_tv), int(cfg.differentiate_weight), int(seed), _dp(grad),
+                                              threads, _dp(terms)))
+        return terms
+
+    def eikonal_loss(self, s: Spec, coeffs, pts, scale, grad=None):
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        out = C.c_double()
+        self._err(self.L.tgr_eikonal_loss(*_spec_args(s), _dp(coeffs), _dp(pts), len(pts), scale, _dp(grad),
+                                          C.byref(out)))
+        return out.value
 
     def adam_step(self, p, g, m, v, t, lr=0.003, beta1=0.9, beta2=0.999, eps=1e-8, threads=1):
         tt = C.c_int64(t)

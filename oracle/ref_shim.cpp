@@ -193,6 +193,51 @@ int tgr_total_loss(int dim, const int* res, const double* origin, const double* 
     }
 }
 
+// total_loss with EikonalPointSource::FreshUniform and tg::Rng(seed)
+// (sdf_loss.cpp:274-283): the reference draws its own eikonal points.
+int tgr_total_loss_fresh(int dim, const int* res, const double* origin, const double* extent, int order,
+                         const double* coeffs, const double* samples, int64_t n, double lambda1,
+                         double lambda2, double k, int use_weighting, int use_tv, int differentiate_weight,
+                         uint64_t seed, double* grad, int threads, double* terms) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        const tg::TaylorGrid grid = make_grid(spec, coeffs);
+        const auto batch = make_batch(samples, n, dim);
+        auto cfg = make_loss(lambda1, lambda2, k, use_weighting, use_tv, differentiate_weight);
+        cfg.eikonal_point_source = tg::EikonalPointSource::FreshUniform;
+        std::span<double> g;
+        if (grad) g = std::span<double>(grad, grid.coeffs.size());
+        tg::Rng rng(seed);
+        const tg::LossTerms t = tg::total_loss(grid, batch, cfg, g, threads, &rng);
+        terms[0] = t.total;
+        terms[1] = t.fit;
+        terms[2] = t.eik;
+        terms[3] = t.tv;
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, 1);
+    } catch (const std::exception& e) {
+        return fail(e, 4);
+    }
+}
+
+// eikonal_loss (sdf_loss.cpp:137-153) on caller points (n x 3).
+int tgr_eikonal_loss(int dim, const int* res, const double* origin, const double* extent, int order,
+                     const double* coeffs, const double* pts, int64_t n, double scale, double* grad, double* out) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        const tg::TaylorGrid grid = make_grid(spec, coeffs);
+        std::vector<tg::Vec3> p(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) p[i] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+        std::span<double> g;
+        if (grad) g = std::span<double>(grad, grid.coeffs.size());
+        *out = tg::eikonal_loss(grid, p, g, scale);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
 // adam_step on caller arrays; returns 0, or 4 with the NumericalError text.
 int tgr_adam_step(double* p, const double* g, double* m, double* v, int64_t n, int64_t* t, double lr,
                   double beta1, double beta2, double eps, int threads) {

@@ -165,6 +165,8 @@ def lib():
     L.tgcu_rng_create.argtypes = [C.c_uint64, C.POINTER(P)]
     L.tgcu_rng_destroy.argtypes = [P]
     L.tgcu_rng_index.argtypes = [P, C.c_uint64, C.c_int64, P]
+    L.tgcu_rng_uniform_box.argtypes = [P, C.c_int, P, P, C.c_int64, P]
+    L.tgcu_train_step_fresh_eik.argtypes = [P, P, C.c_int64, P, C.POINTER(_Loss), C.POINTER(_Terms), C.c_int, P]
     L.tgcu_shuffle_order.argtypes = [C.c_uint64, C.c_int64, P]
     _lib = L
     return L
@@ -246,7 +248,9 @@ class InitOptions:
 
 @dataclass
 class LossConfig:
-    """tg::LossConfig (sdf_loss.hpp:15-25); reuse-batch eikonal points."""
+    """tg::LossConfig (sdf_loss.hpp:15-25). eikonal_point_source: the batch
+    itself (ReuseBatch, default) or |batch| fresh uniform points drawn from the
+    step's Rng (FreshUniform, sdf_loss.cpp:274-283)."""
     lambda1: float = 1e-4
     lambda2: float = 2e-5
     k: float = 50.0
@@ -254,10 +258,45 @@ class LossConfig:
     use_tv: bool = True
     batch_size: int = 8192
     differentiate_weight: bool = False
+    eikonal_point_source: int = 0  # EikonalPointSource
 
     def _c(self) -> _Loss:
         return _Loss(self.lambda1, self.lambda2, self.k, int(self.use_weighting), int(self.use_tv),
                      int(self.differentiate_weight))
+
+
+class EikonalPointSource(IntEnum):
+    """tg::EikonalPointSource (sdf_loss.hpp:13)."""
+    ReuseBatch = 0
+    FreshUniform = 1
+
+
+class Rng:
+    """tg::Rng (rng.hpp:14-74) on the host: mt19937_64, the reference's
+    index / uniform_in_box draws (same streams as the reference)."""
+
+    def __init__(self, seed: int):
+        h = C.c_void_p()
+        _check(lib().tgcu_rng_create(int(seed), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().tgcu_rng_destroy(self._h)
+            self._h = None
+
+    def index(self, n: int, count: int) -> np.ndarray:
+        out = np.empty(int(count), dtype=np.int64)
+        _check(lib().tgcu_rng_index(self._h, int(n), int(count), _ptr(out)))
+        return out
+
+    def uniform_in_box(self, dim: int, lo, hi, count: int) -> np.ndarray:
+        """count points (count x 3, fp64; z = 0 in 2D)."""
+        lo3 = np.ascontiguousarray(np.asarray(list(lo) + [0.0] * 3, dtype=np.float64)[:3])
+        hi3 = np.ascontiguousarray(np.asarray(list(hi) + [0.0] * 3, dtype=np.float64)[:3])
+        out = np.empty((int(count), 3), dtype=np.float64)
+        _check(lib().tgcu_rng_uniform_box(self._h, int(dim), _ptr(lo3), _ptr(hi3), int(count), _ptr(out)))
+        return out
 
 
 @dataclass
@@ -593,7 +632,8 @@ def adam_step(grid: TaylorGrid, grad_ptr: Optional[int] = None):
 
 
 def train_step(grid: TaylorGrid, samples, cfg: LossConfig = LossConfig(), asynchronous: bool = False,
-               stream=None, export_grad: bool = False, input_ready: bool = False) -> Optional[LossTerms]:
+               stream=None, export_grad: bool = False, input_ready: bool = False,
+               rng: Optional["Rng"] = None) -> Optional[LossTerms]:
     """One fused step: zero grad → total_loss → finite check → adam_step
     (schedule.cpp:66-92). Returns the LossTerms (None when asynchronous).
     export_grad also stores the full gradient in the grid grad buffer (validation).
@@ -602,6 +642,22 @@ def train_step(grid: TaylorGrid, samples, cfg: LossConfig = LossConfig(), asynch
     s, flags = _samples(samples)
     if export_grad:
         flags |= TGCU_EXPORT_GRAD
+    if cfg.eikonal_point_source == EikonalPointSource.FreshUniform and cfg.lambda1 > 0.0:
+        # total_loss draws |batch| points with rng->uniform_in_box(origin, domain_max)
+        if rng is None:
+            raise ValueError("total_loss: fresh-uniform eikonal points need an rng")
+        sp = grid.spec
+        hi = [sp.origin[a] + sp.extent[a] for a in range(3)]
+        eik = rng.uniform_in_box(sp.dim, sp.origin, hi, s.shape[0]).astype(np.float32)
+        if not flags & TGCU_HOST:
+            import torch
+            eik = torch.from_numpy(eik).to(s.device)
+        ef = flags | (TGCU_ASYNC if asynchronous else 0)
+        t = _Terms()
+        _check(lib().tgcu_train_step_fresh_eik(grid.handle, _ptr(s), s.shape[0], _ptr(eik), C.byref(cfg._c()),
+                                               None if asynchronous else C.byref(t), ef,
+                                               C.c_void_p(stream) if stream else None))
+        return None if asynchronous else LossTerms._from(t)
     if input_ready and not flags & TGCU_HOST:
         flags |= TGCU_INPUT_READY
     if asynchronous:

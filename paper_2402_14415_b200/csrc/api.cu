@@ -868,6 +868,65 @@ int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
     });
 }
 
+int tgcu_train_step_fresh_eik(tgcu_grid* h, const float* samples, int64_t n, const float* eik_points,
+                              const tgcu_loss_config* cfg, tgcu_loss_terms* out, int flags, void* stream) {
+    if (cfg && cfg->lambda1 <= 0.0)  // no eikonal term: the reference draws no points
+        return tgcu_train_step(h, samples, n, cfg, out, flags & ~TGCU_INPUT_READY, stream);
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(cfg != nullptr, "total_loss: NULL config");
+        require(cfg->lambda1 >= 0.0 && cfg->lambda2 >= 0.0, "LossConfig: lambda weights must be >= 0");
+        require(cfg->k > 0.0, "LossConfig: weight sharpness k must be > 0");
+        require(n > 0, "total_loss: empty batch");
+        require(eik_points != nullptr, "total_loss: fresh-uniform eikonal points need an rng");
+        require(2 * n <= (int64_t)INT_MAX / (1 << g.spec.dim), "train_step: batch too large");
+        require(!g.slab, "train_step: slab grids step with tgcu_slab_step_begin/finish");
+        cudaStream_t s = as_stream(stream);
+        // point list = the batch (recon only) followed by the eikonal points
+        // (eikonal only, gt = kEikMark), staged on the caller's stream
+        ensure_staging(g, 8 * n);
+        float4* st4 = reinterpret_cast<float4*>(g.staging);
+        const cudaMemcpyKind kind = (flags & TGCU_HOST) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        TGCU_CUDA(cudaMemcpyAsync(st4, samples, sizeof(float) * 4 * n, kind, s));
+        const float* e3 = eik_points;
+        float* tmp = nullptr;
+        if (flags & TGCU_HOST) {
+            TGCU_CUDA(cudaMallocAsync(&tmp, sizeof(float) * 3 * n, s));
+            TGCU_CUDA(cudaMemcpyAsync(tmp, eik_points, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, s));
+            e3 = tmp;
+        }
+        launch_pack_eik(e3, n, st4 + n, s);
+        if (tmp) TGCU_CUDA(cudaFreeAsync(tmp, s));
+        ensure_optimizer(g);
+        const int64_t t_after = g.t + 1;
+        const double bc1 = 1.0 - std::pow(g.adam.beta1, (double)t_after);
+        const double bc2 = 1.0 - std::pow(g.adam.beta2, (double)t_after);
+        const int in_idx = g.cur;
+        float* gout = nullptr;
+        if (flags & TGCU_EXPORT_GRAD) {
+            ensure_grad(g);
+            gout = g.grad;
+        }
+        BinInput bin_in;  // ordered after the staging on s
+        launch_train_step(g, st4, 2 * n, n, *cfg, in_idx, g.steps_launched, 1.0 / bc1, 1.0 / bc2, t_after, gout,
+                          nullptr, bin_in, s, true);
+        g.cur = 1 - in_idx;
+        g.t = t_after;
+        g.steps_launched += 1;
+        const bool sync = !(flags & TGCU_ASYNC) || out != nullptr;
+        if (out) {
+            TGCU_CUDA(cudaMemcpyAsync(g.h_terms, g.d_trace + ((g.steps_launched - 1) % kTraceCap),
+                                      sizeof(tgcu_loss_terms), cudaMemcpyDeviceToHost, s));
+        }
+        if (sync) {
+            TGCU_CUDA(cudaStreamSynchronize(s));
+            raise_sticky(g);
+            if (out) *out = *g.h_terms;
+        }
+    });
+}
+
 int tgcu_slab_step_begin(tgcu_grid* h, const float* samples, int64_t n, int64_t n_global,
                          const tgcu_loss_config* cfg, double** partials, int flags, void* stream) {
     return guard([&] {

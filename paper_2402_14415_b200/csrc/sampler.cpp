@@ -249,6 +249,14 @@ int tgcu_rng_index(tgcu_rng* r, uint64_t n, int64_t count, int64_t* out) {
     return TGCU_OK;
 }
 
+int tgcu_rng_uniform_box(tgcu_rng* r, int dim, const double* lo, const double* hi, int64_t count, double* out3) {
+    if (!r || !lo || !hi || !out3 || count < 0 || (dim != 2 && dim != 3)) return TGCU_ERR_INVALID_ARGUMENT;
+    for (int64_t i = 0; i < count; ++i) {  // Rng::uniform_in_box (rng.hpp:53-57): axes in order, z = 0 in 2D
+        for (int a = 0; a < 3; ++a) out3[3 * i + a] = a < dim ? r->r.uniform(lo[a], hi[a]) : 0.0;
+    }
+    return TGCU_OK;
+}
+
 int tgcu_shuffle_order(uint64_t seed, int64_t n, uint32_t* order) {
     if (n < 0 || (n > 0 && !order)) return TGCU_ERR_INVALID_ARGUMENT;
     for (int64_t i = 0; i < n; ++i) order[i] = static_cast<uint32_t>(i);

@@ -362,7 +362,13 @@ struct LossDev {
     double eik_scale;   // lambda1 (0 disables the eikonal term)
     int use_weighting;
     int differentiate_weight;
+    int fresh_eik;      // EikonalPointSource::FreshUniform: batch points carry recon only,
+                        // points whose gt is kEikMark carry the eikonal term only
 };
+
+// gt of a fresh-uniform eikonal point (a quiet NaN with a payload no fp64->fp32
+// conversion of a user value produces; a user NaN gt stays 0x7fc00000).
+constexpr unsigned kEikMark = 0x7fc0e1c5u;
 
 // Adaptive weight w'(d) = 1 - |2 sigmoid(k d) - 1| (sdf_loss.cpp:15-27) in the
 // cancellation-free form 2e / (1 + e), e = exp(-k|d|), evaluated in fp32: it
@@ -377,8 +383,9 @@ __device__ __forceinline__ float w_prime_f(double d, double k, float& e) {
 template <int DIM, bool EIK>
 __device__ __forceinline__ void point_loss(const LossDev& L, float f, const float* fg, float gt,
                                            double& recon, double& eik, float& u, float* gv) {
+    const bool eik_point = L.fresh_eik && __float_as_uint(gt) == kEikMark;
     const double value = (double)f;
-    const double gtd = (double)gt;
+    const double gtd = eik_point ? 0.0 : (double)gt;
     const double resid = value - gtd;
     double w = 1.0;
     float wp_pred = 0.0f, wp_gt = 0.0f, e_pred = 0.0f, e_gt;
@@ -396,11 +403,12 @@ __device__ __forceinline__ void point_loss(const LossDev& L, float f, const floa
         const double ds = 2.0 * L.k * (double)(e_pred * r1 * r1);
         up += L.inv_n * fabs(resid) * (value > 0.0 ? -ds : ds);
     }
-    u = (float)up;
+    u = eik_point ? 0.0f : (float)up;
+    if (eik_point) recon = 0.0;
     eik = 0.0;
 #pragma unroll
     for (int a = 0; a < DIM; ++a) gv[a] = 0.0f;
-    if constexpr (EIK) {
+    if (EIK && (!L.fresh_eik || eik_point)) {
         double n2 = 0.0;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) n2 += (double)fg[a] * (double)fg[a];

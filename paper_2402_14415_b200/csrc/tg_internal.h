@@ -228,7 +228,10 @@ struct BinInput {
 void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
                        int in_idx,
                        int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
-                       double* slab_out, const BinInput& in, cudaStream_t s);
+                       double* slab_out, const BinInput& in, cudaStream_t s, bool fresh_eik = false);
+// Fresh-uniform eikonal points (n x 3 floats, device) -> float4 records with
+// gt = kEikMark (tg_device.cuh), for the fused step's point list.
+void launch_pack_eik(const float* p3, int64_t n, float4* dst, cudaStream_t s);
 void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& cfg, int in_idx, int64_t step,
                         int64_t t_after, int64_t n, cudaStream_t s);
 void launch_f64_to_f32(const double* src, float* dst, int64_t n, cudaStream_t s);

@@ -1226,6 +1226,17 @@ static void ensure_tmaps(Grid& g, bool layout_ok, unsigned tile_row_floats) {
     if (ok) g.tm_state = 1;
 }
 
+__global__ void k_pack_eik(const float* __restrict__ p3, long long n, float4* __restrict__ dst) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = make_float4(p3[3 * i], p3[3 * i + 1], p3[3 * i + 2], __uint_as_float(kEikMark));
+}
+
+void launch_pack_eik(const float* p3, int64_t n, float4* dst, cudaStream_t s) {
+    k_pack_eik<<<grid_blocks(n, 256), 256, 0, s>>>(p3, n, dst);
+    count_launch();
+    TGCU_CUDA(cudaGetLastError());
+}
+
 // Slab phase 2: commit with the globally reduced sums.
 void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& cfg, int in_idx, int64_t step,
                         int64_t t_after, int64_t n, cudaStream_t s) {
@@ -1252,7 +1263,7 @@ void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& 
 void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
                        int in_idx,
                        int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
-                       double* slab_out, const BinInput& in, cudaStream_t s) {
+                       double* slab_out, const BinInput& in, cudaStream_t s, bool fresh_eik) {
     // Binning runs on the binning stream into bin set k; the brick kernel
     // (caller's stream) waits for it and releases the set when done, so the
     // binning of the next step overlaps this step's brick kernel whenever its
@@ -1357,6 +1368,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     A.L.eik_scale = cfg.lambda1;
     A.L.use_weighting = cfg.use_weighting;
     A.L.differentiate_weight = cfg.differentiate_weight;
+    A.L.fresh_eik = fresh_eik ? 1 : 0;
     // TV normaliser P*K over the global grid (sdf_loss.cpp:161-170).
     const double inv_norm = g.tv_inv_norm;
     A.want_tv = cfg.use_tv ? 1 : 0;

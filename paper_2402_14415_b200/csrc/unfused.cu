@@ -183,6 +183,7 @@ void launch_point_terms(Grid& g, const float4* samples, int64_t n, const tgcu_lo
     L.eik_scale = cfg.lambda1;
     L.use_weighting = cfg.use_weighting;
     L.differentiate_weight = cfg.differentiate_weight;
+    L.fresh_eik = 0;
     const bool eik = cfg.lambda1 > 0.0;
     double* partials = g.scratch_d + 8;
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {

@@ -29,7 +29,7 @@ from typing import Callable, List, Optional, Sequence
 
 import numpy as np
 
-from . import (AdamConfig, GridSpec, InitOptions, LossConfig, LossTerms, NumericalError, TaylorGrid, _check,
+from . import (AdamConfig, GridSpec, InitOptions, LossConfig, LossTerms, NumericalError, Rng, TaylorGrid, _check,
                _ptr, adam_step, draw_batch, eval as tg_eval, init_grid, lib, train_step, upsample)
 
 __all__ = ["Stage", "Schedule", "TraceRow", "ScheduleResult", "TrainProblem", "BatchProblem", "SdfProblem",
@@ -118,7 +118,8 @@ class TrainProblem:
         raise NotImplementedError
 
     def compute(self, grid: TaylorGrid, step: int = 0, asynchronous: bool = False) -> Optional[LossTerms]:
-        return train_step(grid, self.batch(grid, step), self.loss, asynchronous=asynchronous)
+        return train_step(grid, self.batch(grid, step), self.loss, asynchronous=asynchronous,
+                          rng=getattr(self, "rng", None))
 
     def on_stage_start(self, grid: TaylorGrid, stage: int) -> None:
         pass
@@ -152,24 +153,17 @@ class SdfProblem(TrainProblem):
         self.seed = seed
         self.exact = exact_stream
         if exact_stream:
-            h = C.c_void_p()
-            _check(lib().tgcu_rng_create(seed, C.byref(h)))
-            self._rng = h
-            self._idx = np.empty(self.n, dtype=np.int64)
+            # one stream for the batch draws and (FreshUniform) the eikonal
+            # points, in the reference's order (sdf_fit.cpp:21-24)
+            self.rng = Rng(seed)
         else:
             import torch
             self.pool = torch.from_numpy(self.train).to(f"cuda:{device}")
             self.out = torch.empty((self.n, 4), dtype=torch.float32, device=self.pool.device)
 
-    def __del__(self):
-        if getattr(self, "_rng", None):
-            lib().tgcu_rng_destroy(self._rng)
-            self._rng = None
-
     def batch(self, grid, step):
         if self.exact:
-            _check(lib().tgcu_rng_index(self._rng, self.train.shape[0], self.n, _ptr(self._idx)))
-            return self.train[self._idx]
+            return self.train[self.rng.index(self.train.shape[0], self.n)]
         import torch
         return draw_batch(self.pool, self.n, self.seed, step, self.out,
                           stream=torch.cuda.current_stream().cuda_stream)

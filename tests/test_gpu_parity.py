@@ -448,6 +448,47 @@ def test_slab_with_no_local_points_matches_full_grid():
     assert_trajectory_close(owned, full.coeffs, 1e-2, 4, what="slab coefficients")
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+def test_fused_step_fresh_uniform_eikonal(oracle, reference, dim):
+    """LossConfig(eikonal_point_source=FreshUniform): the fused step takes the
+    reconstruction term on the batch and the eikonal term on |batch| points
+    drawn from the step's Rng (reference order). Checked against the
+    reference's recon-only total_loss + eikonal_loss on the same fp32 points
+    (test_oracle_cpu pins that decomposition to the reference's FreshUniform
+    code): terms, full gradient, first Adam update; the same Rng stream is
+    consumed; no rng is an error."""
+    rng = np.random.default_rng(60 + dim)
+    res = (21, 18, 17) if dim == 3 else (40, 33)
+    s = ospec(dim, res, 2)
+    c = (0.05 * rng.standard_normal(s.V * s.K)).astype(np.float32).astype(np.float64)
+    n = 3000
+    pts = rng.uniform(-1.0, 1.0, (n, 3)).astype(np.float32)
+    if dim == 2:
+        pts[:, 2] = 0.0
+    smp = np.concatenate([pts, rng.uniform(-0.4, 0.4, (n, 1)).astype(np.float32)], 1).astype(np.float64)
+    cfg = tg.LossConfig(lambda1=1e-2, lambda2=1e-3, eikonal_point_source=tg.EikonalPointSource.FreshUniform)
+    g = tg.init_grid(gspec(dim, res, 2))
+    g.coeffs = c
+    g.adam_reset(tg.AdamConfig(lr=1e-2))
+    with pytest.raises(ValueError, match="need an rng"):
+        tg.train_step(g, smp, cfg)
+    seed = 77
+    t = tg.train_step(g, smp, cfg, export_grad=True, rng=tg.Rng(seed))
+    eik_pts = tg.Rng(seed).uniform_in_box(dim, [-1.0] * 3, [1.0] * 3, n).astype(np.float32).astype(np.float64)
+    gref = np.zeros(s.V * s.K)
+    t_fit = reference.total_loss(s, c, smp, Loss(lambda1=0.0, lambda2=cfg.lambda2), gref)
+    eik = reference.eikonal_loss(s, c, eik_pts, cfg.lambda1, gref)
+    tref = np.array([t_fit[1] + cfg.lambda1 * eik + cfg.lambda2 * t_fit[3], t_fit[1], eik, t_fit[3]])
+    assert_close(t.as_array(), tref, 1e-6, floor=1e-30, what="fresh-uniform terms")
+    eik_smp = np.concatenate([eik_pts, np.zeros((n, 1))], 1)
+    mass = (oracle.total_loss_mass(s, c, smp, Loss(lambda1=0.0, lambda2=cfg.lambda2))
+            + oracle.total_loss_mass(s, c, eik_smp, Loss(lambda1=cfg.lambda1, lambda2=0.0, use_tv=False)))
+    grad_close(g.grad(), gref, mass, what="fresh-uniform grad")
+    p1 = c - 1e-2 * gref / (np.abs(gref) + 1e-8)
+    ok = np.abs(gref) > 1e-3 * (np.abs(gref).max() + 1e-30)
+    assert_close(g.coeffs[ok], p1[ok], 1e-6, floor=1.0, what="params after step")
+
+
 def test_pipelined_host_steps_match_device_steps():
     """TGCU_HOST|TGCU_ASYNC (copy-stream pipelined host input) gives the same
     trajectory as device-resident async steps; host arrays alternate slots."""

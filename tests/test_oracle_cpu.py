@@ -377,3 +377,30 @@ def test_markstein_division_matches_ieee(oracle):
                 if L.tgo_markstein_div(num, h, inv_h) != num / h:
                     bad += 1
     assert bad == 0
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_fresh_uniform_eikonal_decomposition(reference, dim):
+    """EikonalPointSource::FreshUniform (sdf_loss.cpp:274-283) = the recon-only
+    total_loss on the batch + lambda1 * eikonal_loss on |batch| points that
+    tg::Rng(seed).uniform_in_box draws; the library's tgcu_rng_uniform_box
+    (tg.Rng) reproduces the reference's own draws."""
+    import paper_2402_14415_b200 as tg
+    rng = np.random.default_rng(40 + dim)
+    s = Spec(dim=dim, res=(9, 8, 7) if dim == 3 else (12, 10), order=2)
+    c = rng.uniform(-0.3, 0.3, s.V * s.K)
+    pts = rng.uniform(-1.0, 1.0, (300, 3))
+    if dim == 2:
+        pts[:, 2] = 0.0
+    smp = np.concatenate([pts, rng.uniform(-0.4, 0.4, (300, 1))], 1)
+    cfg = Loss(lambda1=1e-2, lambda2=1e-3)
+    seed = 1234
+    g_ref = np.zeros(s.V * s.K)
+    t_ref = reference.total_loss_fresh(s, c, smp, cfg, seed, g_ref)
+    eik_pts = tg.Rng(seed).uniform_in_box(dim, [-1.0] * 3, [1.0] * 3, len(smp))
+    g = np.zeros(s.V * s.K)
+    t_fit = reference.total_loss(s, c, smp, Loss(lambda1=0.0, lambda2=cfg.lambda2), g)
+    eik = reference.eikonal_loss(s, c, eik_pts, cfg.lambda1, g)
+    total = t_fit[1] + cfg.lambda1 * eik + cfg.lambda2 * t_fit[3]
+    np.testing.assert_allclose([total, t_fit[1], eik, t_fit[3]], t_ref, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(g, g_ref, rtol=1e-10, atol=1e-14 * np.abs(g_ref).max())
