@@ -350,7 +350,7 @@ class Reference:
         L.tgr_photometric_loss.argtypes = sp + [_D, _I, _D, _D, C.c_int, _D, C.c_int64, _D, _D, _D, _D, _D,
                                                 C.c_int, C.c_int, C.c_double, _D, _D, _D, _D, _D, _D]
         L.tgr_fit_sdf.argtypes = sp + [_D, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
-                                       C.c_int, C.c_double, C.c_double, C.c_uint64, _D, _D, _D]
+                                       C.c_int, C.c_double, C.c_double, C.c_uint64, _D, _D, _D, C.c_int]
         self.L = L
 
     def _err(self, rc):
@@ -506,7 +506,8 @@ class Reference:
                                           _dp(terms)))
         return out, terms
 
-    def fit_sdf(self, s: Spec, samples, total_steps, cfg, batch, lr=0.003, holdout_fraction=0.0, seed=1):
+    def fit_sdf(self, s: Spec, samples, total_steps, cfg, batch, lr=0.003, holdout_fraction=0.0, seed=1,
+                eik_fresh=False):
         """tg::fit_sdf (default progressive plan); returns (coeffs at s.res, terms, report)."""
         smp = np.ascontiguousarray(np.asarray(samples, dtype=np.float64)).reshape(-1, 4)
         out = np.zeros(s.V * s.K)
@@ -514,7 +515,7 @@ class Reference:
         rep = np.zeros(3)
         self._err(self.L.tgr_fit_sdf(*_spec_args(s), _dp(smp), smp.shape[0], total_steps, batch, cfg.lambda1,
                                      cfg.lambda2, cfg.k, int(cfg.use_weighting), int(cfg.use_tv), lr,
-                                     holdout_fraction, seed, _dp(out), _dp(terms), _dp(rep)))
+                                     holdout_fraction, seed, _dp(out), _dp(terms), _dp(rep), int(eik_fresh)))
         return out, terms, {"holdout_mae": rep[0], "train_samples": int(rep[1]), "holdout_samples": int(rep[2])}
 
     def rng_index(self, seed, n, count):

@@ -419,7 +419,7 @@ int tgr_run_schedule(int dim, const double* origin, const double* extent, int or
 int tgr_fit_sdf(int dim, const int* res, const double* origin, const double* extent, int order,
                 const double* samples, int64_t n, int total_steps, int batch, double lambda1, double lambda2,
                 double k, int use_weighting, int use_tv, double lr, double holdout_fraction, uint64_t seed,
-                double* out_coeffs, double* terms_out, double* report_out) {
+                double* out_coeffs, double* terms_out, double* report_out, int eik_fresh) {
     try {
         tg::SampleSet set;
         set.dim = dim;
@@ -430,6 +430,7 @@ int tgr_fit_sdf(int dim, const int* res, const double* origin, const double* ext
         }
         tg::FitOptions opt;
         opt.loss = make_loss(lambda1, lambda2, k, use_weighting, use_tv, 0);
+        if (eik_fresh) opt.loss.eikonal_point_source = tg::EikonalPointSource::FreshUniform;
         opt.loss.batch_size = batch;
         opt.adam.lr = lr;
         opt.total_steps = total_steps;

@@ -146,17 +146,16 @@ class SdfProblem(TrainProblem):
     device-resident pool (tgcu_draw_batch; hashed stream, same distribution)."""
 
     def __init__(self, train: np.ndarray, loss: LossConfig, seed: int, exact_stream: bool = False, device: int = 0):
-        import ctypes as C
         self.loss = loss
         self.train = np.ascontiguousarray(np.asarray(train, dtype=np.float32)).reshape(-1, 4)
         self.n = min(int(loss.batch_size), self.train.shape[0])
         self.seed = seed
         self.exact = exact_stream
-        if exact_stream:
-            # one stream for the batch draws and (FreshUniform) the eikonal
-            # points, in the reference's order (sdf_fit.cpp:21-24)
-            self.rng = Rng(seed)
-        else:
+        # the reference Rng: with exact_stream one stream serves the batch
+        # draws and (FreshUniform) the eikonal points, in the reference's order
+        # (sdf_fit.cpp:21-24); with device draws it serves the eikonal points
+        self.rng = Rng(seed)
+        if not exact_stream:
             import torch
             self.pool = torch.from_numpy(self.train).to(f"cuda:{device}")
             self.out = torch.empty((self.n, 4), dtype=torch.float32, device=self.pool.device)

@@ -236,6 +236,30 @@ def test_fit_sdf_reference_stream_golden(z, name):
     assert abs(r.report.holdout_mae - rep[0]) <= 1e-5 * max(1.0, rep[0])
 
 
+@pytest.mark.parametrize("name", ["d3", "d2"])
+def test_fit_sdf_fresh_uniform_eikonal_vs_reference(z, reference, name):
+    """fit_sdf with EikonalPointSource::FreshUniform and the reference stream:
+    every step draws its batch indices and then its |batch| eikonal points from
+    the one Rng, as the reference's SdfProblem does; loss curve against the
+    reference fit_sdf run live on the same samples."""
+    from oracle.pyoracle import Loss, Spec
+    dim = 3 if name == "d3" else 2
+    res = tuple(int(r) for r in z[f"fit_{name}_res"])[:dim]
+    smp = z[f"fit_{name}_samples"]
+    lc = tg.LossConfig(batch_size=64, lambda1=1e-2, eikonal_point_source=tg.EikonalPointSource.FreshUniform)
+    opts = FitOptions(loss=lc, adam=tg.AdamConfig(lr=1e-2), total_steps=30, holdout_fraction=0.1, seed=3,
+                      exact_stream=True, asynchronous=False)
+    r = fit_sdf(smp, tg.GridSpec(dim=dim, resolution=res, order=2), opts)
+    _, ref_terms, rep = reference.fit_sdf(Spec(dim=dim, res=res, order=2),
+                                          np.asarray(smp, dtype=np.float32).astype(np.float64), 30,
+                                          Loss(lambda1=1e-2), 64, lr=1e-2, holdout_fraction=0.1, seed=3,
+                                          eik_fresh=True)
+    assert (r.report.train_samples, r.report.holdout_samples) == (rep["train_samples"], rep["holdout_samples"])
+    terms = np.array([t.loss.as_array() for t in r.trace])
+    assert_close(terms[:, 0], ref_terms[:, 0], 1e-4, floor=1e-30, what="fresh-uniform fit loss curve")
+    assert_close(terms[:, 2], ref_terms[:, 2], 1e-4, floor=1e-30, what="fresh-uniform eikonal curve")
+
+
 def test_fit_sdf_device_stream_trains():
     """Default device batch draw: progressive 3-stage fit of a sphere converges."""
     smp = tg.sample(tg.SHAPE_SPHERE, 3, 7, 200000, near_frac=0.5, sigma=0.01, param0=0.6)
