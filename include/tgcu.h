@@ -167,6 +167,14 @@ int tgcu_grad_zero(tgcu_grid* g, float* grad, void* stream);
 int tgcu_grad_download_f64(tgcu_grid* g, const float* grad, double* out, int64_t n);
 
 /* tv_loss (sdf_loss.cpp:155-257). grad may be NULL (value only). */
+/* recon_loss (sdf_loss.cpp:130-135): mean weighted L1 residual of the batch;
+ * with grad (device, coefficient layout) the gradient times `scale` is added
+ * into it. eikonal_loss (sdf_loss.cpp:137-153): mean (|grad f| - 1)^2 over
+ * n points (n x 3 floats), gradient times `scale` added into grad. */
+int tgcu_recon_loss(tgcu_grid* g, const float* samples, int64_t n, const tgcu_loss_config* cfg, double scale,
+                    float* grad, double* out, int flags, void* stream);
+int tgcu_eikonal_loss(tgcu_grid* g, const float* points, int64_t n, double scale, float* grad, double* out,
+                      int flags, void* stream);
 int tgcu_tv_loss(tgcu_grid* g, float* grad, double scale, double* out, void* stream);
 
 /* total_loss (sdf_loss.cpp:259-292), reuse-batch eikonal: samples n×4

@@ -166,6 +166,8 @@ def lib():
     L.tgcu_rng_destroy.argtypes = [P]
     L.tgcu_rng_index.argtypes = [P, C.c_uint64, C.c_int64, P]
     L.tgcu_rng_uniform_box.argtypes = [P, C.c_int, P, P, C.c_int64, P]
+    L.tgcu_recon_loss.argtypes = [P, P, C.c_int64, C.POINTER(_Loss), C.c_double, P, C.POINTER(C.c_double), C.c_int, P]
+    L.tgcu_eikonal_loss.argtypes = [P, P, C.c_int64, C.c_double, P, C.POINTER(C.c_double), C.c_int, P]
     L.tgcu_train_step_fresh_eik.argtypes = [P, P, C.c_int64, P, C.POINTER(_Loss), C.POINTER(_Terms), C.c_int, P]
     L.tgcu_shuffle_order.argtypes = [C.c_uint64, C.c_int64, P]
     _lib = L
@@ -622,6 +624,31 @@ def total_loss(grid: TaylorGrid, samples, cfg: LossConfig = LossConfig(), with_g
     gp = C.c_void_p(grid.grad_ptr()) if with_grad else None
     _check(lib().tgcu_total_loss(grid.handle, _ptr(s), s.shape[0], C.byref(cfg._c()), gp, C.byref(t), flags, None))
     return LossTerms._from(t)
+
+
+def recon_loss(grid: TaylorGrid, samples, cfg: LossConfig = LossConfig(), scale: float = 1.0,
+               with_grad: bool = True) -> float:
+    """recon_loss (sdf_loss.cpp:130-135): mean weighted L1 residual; with_grad
+    adds scale x its gradient into the grid-owned gradient buffer."""
+    s, flags = _samples(samples)
+    out = C.c_double()
+    gp = C.c_void_p(grid.grad_ptr()) if with_grad else None
+    _check(lib().tgcu_recon_loss(grid.handle, _ptr(s), s.shape[0], C.byref(cfg._c()), float(scale), gp,
+                                 C.byref(out), flags, None))
+    return out.value
+
+
+def eikonal_loss(grid: TaylorGrid, points, scale: float = 1.0, with_grad: bool = True) -> float:
+    """eikonal_loss (sdf_loss.cpp:137-153): mean (|grad f| - 1)^2 over the
+    points (n, 3); with_grad adds scale x its gradient into the grid buffer."""
+    if _is_torch(points):
+        p, flags = _dev_f32(points, 3, "eikonal_loss"), 0
+    else:
+        p, flags = _host_f32(points, 3), TGCU_HOST
+    out = C.c_double()
+    gp = C.c_void_p(grid.grad_ptr()) if with_grad else None
+    _check(lib().tgcu_eikonal_loss(grid.handle, _ptr(p), p.shape[0], float(scale), gp, C.byref(out), flags, None))
+    return out.value
 
 
 def adam_step(grid: TaylorGrid, grad_ptr: Optional[int] = None):

@@ -736,6 +736,64 @@ int tgcu_total_loss(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
     });
 }
 
+int tgcu_recon_loss(tgcu_grid* h, const float* samples, int64_t n, const tgcu_loss_config* cfg, double scale,
+                    float* grad, double* out, int flags, void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(cfg != nullptr && out != nullptr, "recon_loss: NULL argument");
+        require(cfg->lambda1 >= 0.0 && cfg->lambda2 >= 0.0, "LossConfig: lambda weights must be >= 0");
+        require(cfg->k > 0.0, "LossConfig: weight sharpness k must be > 0");
+        require(n > 0, "recon_loss: empty batch");
+        cudaStream_t s = as_stream(stream);
+        const float4* ds = reinterpret_cast<const float4*>(samples);
+        if (flags & TGCU_HOST) {
+            ensure_staging(g, 4 * n);
+            TGCU_CUDA(cudaMemcpyAsync(g.staging, samples, sizeof(float) * 4 * n, cudaMemcpyHostToDevice, s));
+            ds = reinterpret_cast<const float4*>(g.staging);
+        }
+        tgcu_loss_config c = *cfg;
+        c.lambda1 = 0.0;  // point_terms<false> (sdf_loss.cpp:133)
+        launch_point_terms(g, ds, n, c, grad, s, scale);
+        double sums[2] = {0, 0};
+        TGCU_CUDA(cudaMemcpyAsync(sums, g.scratch_d, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        TGCU_CUDA(cudaStreamSynchronize(s));
+        check_nan_points(g, s);
+        *out = sums[0] / (double)n;
+    });
+}
+
+int tgcu_eikonal_loss(tgcu_grid* h, const float* points, int64_t n, double scale, float* grad, double* out,
+                      int flags, void* stream) {
+    return guard([&] {
+        Grid& g = h->g;
+        set_device(g);
+        require(out != nullptr, "eikonal_loss: NULL argument");
+        require(n > 0, "eikonal_loss: empty point set");
+        cudaStream_t s = as_stream(stream);
+        ensure_staging(g, 4 * n);
+        float4* st4 = reinterpret_cast<float4*>(g.staging);
+        const float* p3 = points;
+        float* tmp = nullptr;
+        if (flags & TGCU_HOST) {
+            TGCU_CUDA(cudaMallocAsync(&tmp, sizeof(float) * 3 * n, s));
+            TGCU_CUDA(cudaMemcpyAsync(tmp, points, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, s));
+            p3 = tmp;
+        }
+        launch_pack_eik(p3, n, st4, s);
+        if (tmp) TGCU_CUDA(cudaFreeAsync(tmp, s));
+        tgcu_loss_config c{};
+        c.lambda1 = scale;
+        c.k = 1.0;
+        launch_point_terms(g, st4, n, c, grad, s, 1.0, true);
+        double sums[2] = {0, 0};
+        TGCU_CUDA(cudaMemcpyAsync(sums, g.scratch_d, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        TGCU_CUDA(cudaStreamSynchronize(s));
+        check_nan_points(g, s);
+        *out = sums[1] / (double)n;
+    });
+}
+
 int tgcu_adam_reset(tgcu_grid* h, const tgcu_adam_config* cfg) {
     return guard([&] {
         Grid& g = h->g;

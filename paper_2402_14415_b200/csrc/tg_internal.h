@@ -209,7 +209,8 @@ void launch_backprop(Grid& g, const float* pts, const float* up, const float* up
 // Unfused total_loss pieces: point terms (atomic scatter) + TV; sums land in
 // g.scratch_d[0..2] = {recon, eik, tv_sum}.
 void launch_point_terms(Grid& g, const float4* samples, int64_t n, const tgcu_loss_config& cfg, float* grad,
-                        cudaStream_t s);
+                        cudaStream_t s,
+                        double upstream_scale = 1.0, bool eik_points = false);
 void launch_tv(Grid& g, const float* coeffs, float* grad, double gscale, int want_value, cudaStream_t s);
 void launch_adam_check(Grid& g, const float* grad, cudaStream_t s);
 void launch_adam_update(Grid& g, const float* grad, double inv_bc1, double inv_bc2, cudaStream_t s);

@@ -174,17 +174,17 @@ __global__ void k_reduce_pairs(const double* __restrict__ partials, int nblk, do
 }
 
 void launch_point_terms(Grid& g, const float4* samples, int64_t n, const tgcu_loss_config& cfg, float* grad,
-                        cudaStream_t s) {
+                        cudaStream_t s, double upstream_scale, bool eik_points) {
     const int blocks = grid_blocks(n, 256, 148 * 8);
     ensure_scratch(g, 2 * (int64_t)blocks + 8);
     LossDev L;
     L.k = cfg.k;
-    L.inv_n = 1.0 / (double)n;
+    L.inv_n = upstream_scale / (double)n;  // recon_loss's scale (sdf_loss.cpp:130-135)
     L.eik_scale = cfg.lambda1;
     L.use_weighting = cfg.use_weighting;
     L.differentiate_weight = cfg.differentiate_weight;
-    L.fresh_eik = 0;
-    const bool eik = cfg.lambda1 > 0.0;
+    L.fresh_eik = eik_points ? 1 : 0;  // eikonal_loss: marked points, eikonal term only
+    const bool eik = cfg.lambda1 > 0.0 || eik_points;
     double* partials = g.scratch_d + 8;
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
         if (eik)

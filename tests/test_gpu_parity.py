@@ -489,6 +489,44 @@ def test_fused_step_fresh_uniform_eikonal(oracle, reference, dim):
     assert_close(g.coeffs[ok], p1[ok], 1e-6, floor=1.0, what="params after step")
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+def test_recon_and_eikonal_loss_standalone(oracle, reference, dim):
+    """recon_loss / eikonal_loss (sdf_loss.cpp:130-153) with their scale on the
+    gradient, against the reference (values 1e-6, gradients within the
+    accumulation-order bound), and the errors for empty inputs."""
+    rng = np.random.default_rng(80 + dim)
+    res = (19, 16, 14) if dim == 3 else (30, 27)
+    s = ospec(dim, res, 2)
+    c = (0.1 * rng.standard_normal(s.V * s.K)).astype(np.float32).astype(np.float64)
+    n = 4000
+    pts = rng.uniform(-1.0, 1.0, (n, 3)).astype(np.float32)
+    if dim == 2:
+        pts[:, 2] = 0.0
+    smp = np.concatenate([pts, rng.uniform(-0.4, 0.4, (n, 1)).astype(np.float32)], 1).astype(np.float64)
+    g = tg.init_grid(gspec(dim, res, 2))
+    g.coeffs = c
+    cfg = tg.LossConfig()
+    g.zero_grad()
+    v = tg.recon_loss(g, smp, cfg, scale=2.5)
+    gref = np.zeros(s.V * s.K)
+    tref = reference.total_loss(s, c, smp, Loss(lambda1=0.0, use_tv=False), gref)
+    assert_close(v, tref[1], 1e-6, floor=1e-30, what="recon_loss")
+    mass = oracle.total_loss_mass(s, c, smp, Loss(lambda1=0.0, use_tv=False))
+    grad_close(g.grad(), 2.5 * gref, 2.5 * mass, what="recon_loss grad")
+    g.zero_grad()
+    e = tg.eikonal_loss(g, pts.astype(np.float64), scale=0.3)
+    gref = np.zeros(s.V * s.K)
+    eref = reference.eikonal_loss(s, c, pts.astype(np.float64), 0.3, gref)
+    assert_close(e, eref, 1e-6, floor=1e-30, what="eikonal_loss")
+    emass = oracle.total_loss_mass(s, c, np.concatenate([pts, np.zeros((n, 1))], 1).astype(np.float64),
+                                   Loss(lambda1=0.3, use_tv=False))
+    grad_close(g.grad(), gref, emass, what="eikonal_loss grad")
+    with pytest.raises(ValueError, match="recon_loss: empty batch"):
+        tg.recon_loss(g, np.zeros((0, 4)), cfg)
+    with pytest.raises(ValueError, match="eikonal_loss: empty point set"):
+        tg.eikonal_loss(g, np.zeros((0, 3)))
+
+
 def test_pipelined_host_steps_match_device_steps():
     """TGCU_HOST|TGCU_ASYNC (copy-stream pipelined host input) gives the same
     trajectory as device-resident async steps; host arrays alternate slots."""
