@@ -381,7 +381,7 @@ def main():
     ap.add_argument("--no-query", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C3 / C5 step timings")
-    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--e2e-steps", type=int, default=500)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -469,7 +469,7 @@ def main():
         pinned = [torch.from_numpy(b).pin_memory() for b in host_batches]
         ne = max(3, min(args.e2e_steps, args.steps))
         e2e_async = ws == 1
-        for i in range(3):
+        for i in range(2 * NBATCH):  # every pinned buffer through the copy path twice
             step(pinned[i % NBATCH].numpy(), asynchronous=e2e_async)
         g.sync()
         torch.cuda.synchronize()

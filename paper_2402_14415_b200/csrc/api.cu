@@ -65,9 +65,11 @@ void ensure_staging(Grid& g, int64_t floats) {
 void ensure_pipeline(Grid& g, int64_t floats) {
     if (!g.cstream) {
         TGCU_CUDA(cudaStreamCreateWithFlags(&g.cstream, cudaStreamNonBlocking));
+        TGCU_CUDA(cudaStreamCreateWithFlags(&g.cstream2, cudaStreamNonBlocking));
         for (int i = 0; i < 2; ++i) {
             TGCU_CUDA(cudaEventCreateWithFlags(&g.ev_ready[i], cudaEventDisableTiming));
             TGCU_CUDA(cudaEventCreateWithFlags(&g.ev_free[i], cudaEventDisableTiming));
+            TGCU_CUDA(cudaEventCreateWithFlags(&g.ev_half[i], cudaEventDisableTiming));
         }
         TGCU_CUDA(cudaMallocHost(&g.h_ring, sizeof(tgcu_loss_terms) * kTraceCap));
     }
@@ -433,8 +435,10 @@ int tgcu_grid_destroy(tgcu_grid* h) {
         cudaFree(g.pstage[i]);
         if (g.ev_ready[i]) cudaEventDestroy(g.ev_ready[i]);
         if (g.ev_free[i]) cudaEventDestroy(g.ev_free[i]);
+        if (g.ev_half[i]) cudaEventDestroy(g.ev_half[i]);
     }
     if (g.cstream) cudaStreamDestroy(g.cstream);
+    if (g.cstream2) cudaStreamDestroy(g.cstream2);
     cudaFreeHost(g.h_ring);
     for (void* b : g.ipc_open) cudaIpcCloseMemHandle(b);
     for (auto e : g.prof_ev) cudaEventDestroy(e);
@@ -879,9 +883,16 @@ int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
             ensure_pipeline(g, 4 * n);
             const int slot = g.pipe_slot;
             g.pipe_slot ^= 1;
+            // the two halves on two copy streams, joined on the first
+            const int64_t h1 = n / 2;
             TGCU_CUDA(cudaStreamWaitEvent(g.cstream, g.ev_free[slot], 0));
-            TGCU_CUDA(cudaMemcpyAsync(g.pstage[slot], samples, sizeof(float) * 4 * n, cudaMemcpyHostToDevice,
+            TGCU_CUDA(cudaStreamWaitEvent(g.cstream2, g.ev_free[slot], 0));
+            TGCU_CUDA(cudaMemcpyAsync(g.pstage[slot], samples, sizeof(float) * 4 * h1, cudaMemcpyHostToDevice,
                                       g.cstream));
+            TGCU_CUDA(cudaMemcpyAsync(g.pstage[slot] + 4 * h1, samples + 4 * h1, sizeof(float) * 4 * (n - h1),
+                                      cudaMemcpyHostToDevice, g.cstream2));
+            TGCU_CUDA(cudaEventRecord(g.ev_half[slot], g.cstream2));
+            TGCU_CUDA(cudaStreamWaitEvent(g.cstream, g.ev_half[slot], 0));
             TGCU_CUDA(cudaEventRecord(g.ev_ready[slot], g.cstream));
             bin_in.wait = g.ev_ready[slot];
             bin_in.consumed = g.ev_free[slot];

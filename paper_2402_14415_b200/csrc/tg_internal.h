@@ -139,8 +139,12 @@ struct Grid {
     // Pipelined host inputs (TGCU_HOST | TGCU_ASYNC train steps): a copy
     // stream filling two device slots, ordered against the compute stream by
     // events, and a pinned ring receiving each step's LossTerms.
-    cudaStream_t cstream = nullptr;
+    // Two copy streams, each moving half of a step's samples: one pinned H2D
+    // copy gets 25-42 GB/s depending on the box, two concurrent halves ~54
+    // GB/s (tools/h2d_bw.py).
+    cudaStream_t cstream = nullptr, cstream2 = nullptr;
     cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    cudaEvent_t ev_half[2] = {nullptr, nullptr};
     float* pstage[2] = {nullptr, nullptr};
     int64_t pstage_cap = 0;              // floats per slot
     int pipe_slot = 0;
