@@ -6,8 +6,23 @@ import time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 
 
+def gpu_local_cpus(dev=0):
+    """CPUs on the GPU's NUMA node (NVML CPU affinity mask)."""
+    import pynvml
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+    words = pynvml.nvmlDeviceGetCpuAffinity(h, 64)
+    cpus = [64 * w + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1]
+    pynvml.nvmlShutdown()
+    return cpus
+
+
 def main():
     import torch
+    if "--affinity" in sys.argv:
+        cpus = gpu_local_cpus()
+        os.sched_setaffinity(0, cpus)
+        print(f"bound to {len(cpus)} GPU-local cpus")
     import paper_2402_14415_b200 as tg
     spec = tg.GridSpec(dim=3, resolution=(128,) * 3, order=2)
     g = tg.init_grid(spec)
