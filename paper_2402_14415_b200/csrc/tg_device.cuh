@@ -379,6 +379,12 @@ __device__ __forceinline__ float w_prime_f(double d, double k, float& e) {
     e = expf(-(float)(k * fabs(d)));
     return 2.0f * e * __frcp_rn(1.0f + e);
 }
+// The reference's fp64 expression, for near ties only: which of w'(f) and
+// w'(gt) is larger selects the differentiate_weight term, so a near tie is
+// decided exactly as the reference decides it.
+__device__ __forceinline__ double w_prime_d(double d, double k) {
+    return 1.0 - fabs(2.0 * (1.0 / (1.0 + exp(-(k * d)))) - 1.0);
+}
 
 template <int DIM, bool EIK>
 __device__ __forceinline__ void point_loss(const LossDev& L, float f, const float* fg, float gt,
@@ -389,15 +395,22 @@ __device__ __forceinline__ void point_loss(const LossDev& L, float f, const floa
     const double resid = value - gtd;
     double w = 1.0;
     float wp_pred = 0.0f, wp_gt = 0.0f, e_pred = 0.0f, e_gt;
+    bool pred_wins = false;
     if (L.use_weighting) {
         wp_pred = w_prime_f(value, L.k, e_pred);
         wp_gt = w_prime_f(gtd, L.k, e_gt);
-        w = (double)(wp_pred < wp_gt ? wp_gt : wp_pred);
+        pred_wins = wp_pred > wp_gt;
+        w = (double)(pred_wins ? wp_pred : wp_gt);
+        if (fabsf(wp_pred - wp_gt) <= 1e-5f * fmaxf(wp_pred, wp_gt)) {  // rare: decide in fp64
+            const double dp = w_prime_d(value, L.k), dg = w_prime_d(gtd, L.k);
+            pred_wins = dp > dg;
+            w = dp < dg ? dg : dp;
+        }
     }
     recon = w * fabs(resid);
     const double sgn = resid > 0.0 ? 1.0 : (resid < 0.0 ? -1.0 : 0.0);
     double up = L.inv_n * w * sgn;
-    if (L.use_weighting && L.differentiate_weight && wp_pred > wp_gt && value != 0.0) {
+    if (L.use_weighting && L.differentiate_weight && pred_wins && value != 0.0) {
         // dw'/dd = -sign(d) 2k s(1-s), s = sigmoid(k d); s(1-s) = e / (1+e)^2
         const float r1 = __frcp_rn(1.0f + e_pred);
         const double ds = 2.0 * L.k * (double)(e_pred * r1 * r1);
