@@ -646,7 +646,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TGCU_PT_SET(var)
 #endif
 
-template <int DIM, int ORDER, bool EIK, bool EXPORT>
+// Bricks with at most this many points take the unsorted gather (one warp
+// of points; each vertex scans them). Compiled in (TINYOK) only for the
+// variant launched on sparse batches (under 64 point copies per brick on
+// average, e.g. C5): its branches cost the dense C2 step ~1.4 %.
+constexpr int kTiny = 32;
+
+template <int DIM, int ORDER, bool EIK, bool EXPORT, bool TINYOK>
 __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __grid_constant__ StepArgs A) {
     using S = BrickShape<DIM>;
     using L = BrickSmem<DIM, ORDER>;
@@ -743,12 +749,18 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     double recon_sum = 0.0, eik_sum = 0.0, home_pts = 0.0;
     int myv = tid;  // owned vertex of this thread; set per brick by the workload sort
 
+    // Tiny bricks (at most kTiny points, one chunk): no counting sort. Records
+    // stay in point order with each point's cell in start[]; every vertex
+    // scans the few points for its incident cells (3 barriers instead of 8).
+    const bool tiny = TINYOK && (p1 - p0) <= kTiny;
     for (int base = p0; base < p1; base += CH) {
         const int m = min(CH, p1 - base);
-        for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
-        if (base == p0 && tid < 64) bhist[tid] = 0;
-        if (tid == 0) run_total = 0;
-        __syncthreads();
+        if (!tiny) {
+            for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
+            if (base == p0 && tid < 64) bhist[tid] = 0;
+            if (tid == 0) run_total = 0;
+            __syncthreads();
+        }
         // 2a. locate + cell rank, the chunk's counting sort by cell and (first
         //     chunk) the workload balance need no parameters: they run while
         //     the tile is still in flight. Then the forward from the tile and
@@ -768,24 +780,34 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                 tc[a] = c - (o[a] - 1);  // in [0, B]
             }
             ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
-            rank = atomicAdd(&cnt[ec], 1);
+            if (tiny) start[tid] = tc[0] | (tc[1] << 8) | (tc[2] << 16);
+            else rank = atomicAdd(&cnt[ec], 1);
         }
 #ifdef TGCU_PHASE_TIMING
         unsigned long long pt_c0 = 0;
         TGCU_PT_SET(pt_c0)
 #endif
-        __syncthreads();
+        if (!tiny) {
+            __syncthreads();
+            cell_runs<S::NCELL, NT>(cnt, start, &run_total);
+            __syncthreads();
+        }
 #ifdef TGCU_PHASE_TIMING
         const unsigned long long pt_s0 = pt_c0;
 #endif
-        cell_runs<S::NCELL, NT>(cnt, start, &run_total);
-        __syncthreads();
 #ifdef TGCU_PHASE_TIMING
         TGCU_PT_SET(pt_x)
         if (tid == 0) pt_scan += pt_x - pt_s0;
         const unsigned long long pt_b0 = pt_x;
 #endif
-        if (base == p0) {
+        if (base == p0 && tiny) {
+            cp_async_wait<0>();
+            if (warp == 0) mbar_wait(&bars[0], 0);
+            __syncthreads();  // tile and the points' cells (start[]) visible
+#ifdef TGCU_PHASE_TIMING
+            TGCU_PT_SET(pt_tile)
+#endif
+        } else if (base == p0) {
             // Load balance: sort the owned vertices by their (first-chunk)
             // workload into 64 buckets so a warp's lanes carry similar loads;
             // the mapping then holds for the brick (points are in random order).
@@ -865,7 +887,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             rv[2 * DIM] = u;
 #pragma unroll
             for (int k2 = 3 * DIM + 1; k2 < REC; ++k2) rv[k2] = 0.0f;
-            float2* dst = reinterpret_cast<float2*>(uni + (start[ec] + rank) * REC);
+            float2* dst = reinterpret_cast<float2*>(uni + (tiny ? tid : start[ec] + rank) * REC);
 #pragma unroll
             for (int k2 = 0; k2 < REC / 2; ++k2) dst[k2] = make_float2(rv[2 * k2], rv[2 * k2 + 1]);
         }
@@ -877,6 +899,55 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
 #ifdef TGCU_PHASE_TIMING
         const unsigned long long pt_g0 = pt_x;
 #endif
+        if (tiny) {
+            // 2b (tiny bricks): each vertex scans the m points for its cells
+            const int v = tid;
+            const int l3[3] = {v % B, (v / B) % B, DIM == 3 ? v / (B * B) : 0};
+            bool own_ok = true;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) own_ok &= (o[a] + l3[a]) < A.s.res[a];
+            for (int j = 0; own_ok && j < m; ++j) {
+                const int pc = start[j];
+                const int bx = l3[0] + 1 - (pc & 255), by = l3[1] + 1 - ((pc >> 8) & 255);
+                const int bz = DIM == 3 ? l3[2] + 1 - (pc >> 16) : 0;
+                if ((unsigned)bx > 1u || (unsigned)by > 1u || (unsigned)bz > 1u) continue;
+                const int c = bx | (by << 1) | (bz << 2);
+                const float2* rp = reinterpret_cast<const float2*>(uni + j * REC);
+                float r[REC];
+#pragma unroll
+                for (int k2 = 0; k2 < REC / 2; ++k2) {
+                    const float2 t2 = rp[k2];
+                    r[2 * k2] = t2.x;
+                    r[2 * k2 + 1] = t2.y;
+                }
+                Corner<DIM> cg;
+                float sv[DIM];
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    const bool bit = (c >> a) & 1;
+                    const float s0 = r[a], s1 = r[DIM + a];
+                    sv[a] = bit ? s1 : s0;
+                    cg.d[a] = (bit ? -s0 : s1) * A.s.hf[a];
+                }
+                cg.w = sv[0];
+#pragma unroll
+                for (int a = 1; a < DIM; ++a) cg.w *= sv[a];
+                float gvd[DIM];
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    float other = 1.0f;
+#pragma unroll
+                    for (int bb = 0; bb < DIM; ++bb)
+                        if (bb != a) other *= sv[bb];
+                    cg.dw[a] = EIK ? (((c >> a) & 1) ? A.s.inv_hf[a] : -A.s.inv_hf[a]) * other : 0.0f;
+                    gvd[a] = EIK ? r[2 * DIM + 1 + a] : 0.0f;
+                }
+                if constexpr (PACKED)
+                    corner_grad_p2<EIK>(*reinterpret_cast<const Corner<3>*>(&cg), r[2 * DIM], gvd, P);
+                else
+                    corner_grad<DIM, ORDER, K>(cg, r[2 * DIM], gvd, G);
+            }
+        } else
         // 2b. this thread's vertex gathers the points of its 2^D incident
         //     cells, as one flattened loop over (corner, point)
         {
@@ -1424,13 +1495,22 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
         constexpr size_t smem = BrickSmem<DIM, ORDER>::bytes;
         static_assert(BrickSmem<DIM, ORDER>::bytes <= 227 * 1024, "brick smem");
-        auto kern = grad_out ? (eik ? k_brick_step<DIM, ORDER, true, true> : k_brick_step<DIM, ORDER, false, true>)
-                             : (eik ? k_brick_step<DIM, ORDER, true, false> : k_brick_step<DIM, ORDER, false, false>);
+        // sparse batches (few point copies per brick on average) take the
+        // variant with the tiny-brick path compiled in
+        const bool sparse = (double)n * (DIM == 3 ? 1.42 : 1.13) < 64.0 * (double)g.NB;
+        auto pick = [&](auto k_t, auto k_f) { return sparse ? k_t : k_f; };
+        auto kern = grad_out
+            ? (eik ? pick(k_brick_step<DIM, ORDER, true, true, true>, k_brick_step<DIM, ORDER, true, true, false>)
+                   : pick(k_brick_step<DIM, ORDER, false, true, true>, k_brick_step<DIM, ORDER, false, true, false>))
+            : (eik ? pick(k_brick_step<DIM, ORDER, true, false, true>, k_brick_step<DIM, ORDER, true, false, false>)
+                   : pick(k_brick_step<DIM, ORDER, false, false, true>, k_brick_step<DIM, ORDER, false, false, false>));
         static std::atomic<unsigned long long> configured_devs{0};
         const unsigned long long cbit = 1ull << (g.device & 63);
         if (!(configured_devs.load() & cbit)) {
-            for (auto k : {k_brick_step<DIM, ORDER, true, true>, k_brick_step<DIM, ORDER, false, true>,
-                           k_brick_step<DIM, ORDER, true, false>, k_brick_step<DIM, ORDER, false, false>})
+            for (auto k : {k_brick_step<DIM, ORDER, true, true, true>, k_brick_step<DIM, ORDER, false, true, true>,
+                           k_brick_step<DIM, ORDER, true, false, true>, k_brick_step<DIM, ORDER, false, false, true>,
+                           k_brick_step<DIM, ORDER, true, true, false>, k_brick_step<DIM, ORDER, false, true, false>,
+                           k_brick_step<DIM, ORDER, true, false, false>, k_brick_step<DIM, ORDER, false, false, false>})
                 TGCU_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             configured_devs.fetch_or(cbit);
         }
