@@ -1,4 +1,6 @@
 #!/bin/bash
+# Put the two builds at tools/ab/libtgcu_old.so and tools/ab/libtgcu_new.so first (gitignored);
+# the script overwrites paper_2402_14415_b200/libtgcu.so on the box it runs on.
 # A/B of two libtgcu builds on one box: bench step time, alternating.
 for i in 1 2 3; do
   for v in old new; do
