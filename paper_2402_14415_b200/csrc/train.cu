@@ -807,6 +807,14 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
 #ifdef TGCU_PHASE_TIMING
             TGCU_PT_SET(pt_tile)
 #endif
+        } else if (base == p0 && p1 - p0 <= CH) {
+            // single-chunk brick: identity mapping, just the tile wait
+            cp_async_wait<0>();
+            if (warp == 0) mbar_wait(&bars[0], 0);
+            __syncthreads();
+#ifdef TGCU_PHASE_TIMING
+            TGCU_PT_SET(pt_tile)
+#endif
         } else if (base == p0) {
             // Load balance: sort the owned vertices by their (first-chunk)
             // workload into 64 buckets so a warp's lanes carry similar loads;
