@@ -202,7 +202,9 @@ int tgcu_adam_download_f64(tgcu_grid* g, double* m, double* v, int64_t n);
  * TGCU_HOST | TGCU_ASYNC with out == NULL pipelines host input: the samples are
  * copied on an internal copy stream into one of two device slots while the
  * previous step computes, and the step's LossTerms are copied back to pinned
- * host memory; the host array must stay valid until tgcu_sync().
+ * host memory; the host array must stay valid and unmodified until
+ * tgcu_sync() (its copy may still be in flight: do not refill one buffer for
+ * consecutive steps).
  * Point binning runs on an internal stream into one of two bin sets, so the
  * binning of step i+1 overlaps step i's brick kernel when its input is known
  * complete (pipelined host input, or TGCU_INPUT_READY); otherwise it is

@@ -108,7 +108,9 @@ public:
 
     // Pipelined form of train_step (the cmd_bench loop at full speed): the
     // host batch is copied on the library's copy stream while earlier steps
-    // compute, nothing synchronises; `samples` must stay valid until sync().
+    // compute, nothing synchronises; `samples` must stay valid and
+    // unmodified until sync(): the copy may still be in flight, so refilling
+    // the same buffer for the next step corrupts it (cycle >= 2 buffers).
     // Errors surface from sync() with the grid rolled back to the last
     // committed step (NumericalError / std::invalid_argument as above).
     void train_step_async(std::span<const float> samples, const LossConfig& cfg) {

@@ -332,6 +332,7 @@ class Reference:
                                      C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                      C.c_double, C.c_int, _D, _D]
         L.tgr_eval_timed.argtypes = sp + [_D, _D, C.c_int64, _D, C.c_int, _D]
+        L.tgr_query_bench.argtypes = sp + [C.c_double, C.c_uint64, _D, C.c_int64, _D, C.c_int, _D]
         L.tgr_sample_sphere.argtypes = [C.c_double, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_double,
                                         C.c_uint64, _D]
         L.tgr_rng_uniform.argtypes = [C.c_uint64, C.c_int64, _D]
@@ -391,6 +392,16 @@ class Reference:
                                         threads, C.byref(secs)))
         return vals, secs.value
 
+    def query_bench(self, s: Spec, pts, threads, epsilon=0.1, seed=7):
+        """init_grid(SmallUniform) inside the reference, then parallel_for + eval
+        over pts; returns (values, seconds of the eval loop)."""
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        vals = np.empty(len(pts))
+        secs = C.c_double()
+        self._err(self.L.tgr_query_bench(*_spec_args(s), epsilon, seed, _dp(pts), len(pts), _dp(vals), threads,
+                                         C.byref(secs)))
+        return vals, secs.value
+
     def backprop(self, s: Spec, coeffs, pts, upstream, upstream_vec, grad):
         coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
         pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
@@ -445,8 +456,10 @@ class Reference:
 
     def train(self, s: Spec, coeffs, batches, cfg: Loss, lr, beta1=0.9, beta2=0.999, eps=1e-8,
               threads=1):
-        """Returns (final coeffs, per-step terms (steps×4), seconds in the step loop)."""
-        p = np.array(coeffs, dtype=np.float64)
+        """Returns (final coeffs, per-step terms (steps×4), seconds in the step loop).
+        coeffs None: the reference's zero init inside the library (no host copy;
+        the returned coeffs are None)."""
+        p = None if coeffs is None else np.array(coeffs, dtype=np.float64)
         batches = np.ascontiguousarray(batches, dtype=np.float64)
         steps, n = batches.shape[0], batches.shape[1]
         terms = np.zeros((steps, 4))

@@ -51,8 +51,8 @@ tg::GridSpec make_spec(int dim, const int* res, const double* origin, const doub
 tg::TaylorGrid make_grid(const tg::GridSpec& spec, const double* coeffs) {
     tg::InitOptions opts;
     opts.memory_cap_bytes = ~0ull;
-    tg::TaylorGrid g = tg::init_grid(spec, opts);
-    std::memcpy(g.coeffs.data(), coeffs, g.coeffs.size() * sizeof(double));
+    tg::TaylorGrid g = tg::init_grid(spec, opts);  // coeffs == nullptr: InitMode::Zeros
+    if (coeffs) std::memcpy(g.coeffs.data(), coeffs, g.coeffs.size() * sizeof(double));
     return g;
 }
 
@@ -293,7 +293,7 @@ int tgr_train(int dim, const int* res, const double* origin, const double* exten
                 terms_out[4 * s + 3] = t.tv;
             }
         }
-        std::memcpy(coeffs, grid.coeffs.data(), grid.coeffs.size() * sizeof(double));
+        if (coeffs) std::memcpy(coeffs, grid.coeffs.data(), grid.coeffs.size() * sizeof(double));
         if (seconds_out) *seconds_out = secs;
         return 0;
     } catch (const tg::NumericalError& e) {
@@ -311,6 +311,33 @@ int tgr_eval_timed(int dim, const int* res, const double* origin, const double* 
     try {
         const auto spec = make_spec(dim, res, origin, extent, order);
         const tg::TaylorGrid grid = make_grid(spec, coeffs);
+        const auto t0 = std::chrono::steady_clock::now();
+        tg::parallel_for(n, threads, [&](int64_t b, int64_t e, int) {
+            for (int64_t i = b; i < e; ++i) vals[i] = tg::eval(grid, {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]});
+        });
+        *seconds_out = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
+// Query throughput of the reference on a grid it initialises itself
+// (init_grid, InitMode::SmallUniform with the given epsilon and seed,
+// taylor_grid.cpp:162-188; memory cap lifted): parallel_for + eval over the
+// points. For the large BASELINE query grids (512^3), where passing fp64
+// coefficients from the caller would need a second multi-GB copy.
+int tgr_query_bench(int dim, const int* res, const double* origin, const double* extent, int order,
+                    double epsilon, uint64_t seed, const double* pts, int64_t n, double* vals, int threads,
+                    double* seconds_out) {
+    try {
+        const auto spec = make_spec(dim, res, origin, extent, order);
+        tg::InitOptions opts;
+        opts.mode = tg::InitMode::SmallUniform;
+        opts.epsilon = epsilon;
+        opts.seed = seed;
+        opts.memory_cap_bytes = ~0ull;
+        const tg::TaylorGrid grid = tg::init_grid(spec, opts);
         const auto t0 = std::chrono::steady_clock::now();
         tg::parallel_for(n, threads, [&](int64_t b, int64_t e, int) {
             for (int64_t i = b; i < e; ++i) vals[i] = tg::eval(grid, {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]});

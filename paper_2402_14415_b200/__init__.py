@@ -665,7 +665,13 @@ def train_step(grid: TaylorGrid, samples, cfg: LossConfig = LossConfig(), asynch
     (schedule.cpp:66-92). Returns the LossTerms (None when asynchronous).
     export_grad also stores the full gradient in the grid grad buffer (validation).
     input_ready (device samples): the caller guarantees the samples are complete,
-    so the step's binning overlaps the previous step's brick kernel."""
+    so the step's binning overlaps the previous step's brick kernel.
+    asynchronous=True with a host array: the copy to the device is queued on
+    the library's copy stream and runs while earlier steps compute, so the
+    array must stay alive AND unmodified until sync() (or until a later step
+    is known to have consumed it): refilling one pinned buffer every step
+    would overwrite samples whose copy is still in flight. Cycle through
+    at least two buffers and sync() before reusing one."""
     s, flags = _samples(samples)
     if export_grad:
         flags |= TGCU_EXPORT_GRAD

@@ -135,8 +135,9 @@ void ensure_bin_hist(Grid& g, int64_t ints, int64_t points, int64_t chain_ctas) 
     if (g.bin_chain_cap < chain_ctas) {
         if (g.bin_chain) TGCU_CUDA(cudaFree(g.bin_chain));
         g.bin_chain = nullptr;
-        TGCU_CUDA(cudaMalloc(&g.bin_chain, sizeof(int) * 2 * chain_ctas));
-        TGCU_CUDA(cudaMemset(g.bin_chain, 0, sizeof(int) * 2 * chain_ctas));
+        // 2 ints per CTA + the 64-bit ticket counter of k_bin_cols
+        TGCU_CUDA(cudaMalloc(&g.bin_chain, sizeof(int) * (2 * chain_ctas + 2)));
+        TGCU_CUDA(cudaMemset(g.bin_chain, 0, sizeof(int) * (2 * chain_ctas + 2)));
         g.bin_chain_cap = chain_ctas;
         g.bin_epoch = 0;
     }
@@ -280,6 +281,19 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         if (bytes > opts.memory_cap_bytes)
             throw Error(TGCU_ERR_RESOURCE, "init_grid: " + std::to_string(bytes) + " bytes exceeds memory cap of " +
                                                std::to_string(opts.memory_cap_bytes));
+        // Brick codes of the point binning (train.cu point_brick_code) pack the
+        // x, y, z brick coordinates into 27 bits, each axis as wide as the
+        // grid needs.
+        int code_sh[2];
+        {
+            auto bits = [](int n) { return n <= 1 ? 0 : 32 - __builtin_clz((unsigned)(n - 1)); };
+            const int bx = bits((s.res[0] + B - 1) / B), by = bits((s.res[1] + B - 1) / B), bz = bits(nbz_global);
+            if (bx + by + bz > 27)
+                throw Error(TGCU_ERR_RESOURCE, "init_grid: " + std::to_string(bx + by + bz) +
+                                                   " bits of brick coordinates exceed the 27-bit brick code");
+            code_sh[0] = bx;
+            code_sh[1] = bx + by;
+        }
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
             throw Error(TGCU_ERR_CUDA, "tgcu: no CUDA device available (the product path has no CPU fallback)");
@@ -329,6 +343,8 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         // Brick decomposition (train.cu / query.cu).
         g.NB = 1;
         g.zb_global = nbz_global;
+        g.code_sh[0] = code_sh[0];
+        g.code_sh[1] = code_sh[1];
         for (int a = 0; a < 3; ++a) {
             g.brick[a] = a < s.dim ? B : 1;
             g.nb[a] = a < s.dim ? (s.res[a] + B - 1) / B : 1;

@@ -330,6 +330,13 @@ int tgcu_save_tgrid(tgcu_grid* h, const char* path, int precision) {
         Grid& g = h->g;
         require(!g.slab, "save_tgrid: slab grids are not supported");
         require(precision == TGCU_TGRID_F64 || precision == TGCU_TGRID_F32, "save_tgrid: unknown precision");
+        // Commit any pending async step first (sticky errors surface here,
+        // before the file is created: a failed step leaves no partial file).
+        {
+            tgcu_loss_terms t;
+            const int rc = tgcu_sync(h, &t);
+            if (rc != TGCU_OK) throw Error(rc, tgcu_last_error());
+        }
         std::ofstream os(path, std::ios::binary);
         if (!os) throw Error(TGCU_ERR_INGEST, std::string("tgrid: cannot open for writing: ") + path);
         const tgcu_grid_spec& s = g.spec;
@@ -341,12 +348,6 @@ int tgcu_save_tgrid(tgcu_grid* h, const char* path, int precision) {
         for (int a = 0; a < s.dim; ++a) write_pod(os, s.origin[a]);
         for (int a = 0; a < s.dim; ++a) write_pod(os, s.extent[a]);
         write_pod(os, static_cast<uint8_t>(precision));
-        // Commit any pending async step first (sticky errors surface here).
-        {
-            tgcu_loss_terms t;
-            const int rc = tgcu_sync(h, &t);
-            if (rc != TGCU_OK) throw Error(rc, tgcu_last_error());
-        }
         TGCU_CUDA(cudaSetDevice(g.device));
         std::vector<float> buf((size_t)std::min<int64_t>(g.NC, kIoChunk));
         std::vector<double> wide(precision == TGCU_TGRID_F64 ? buf.size() : 0);

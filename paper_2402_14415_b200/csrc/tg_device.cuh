@@ -217,6 +217,68 @@ __device__ __forceinline__ void blend_corner(const float (&c)[K], const Corner<D
     }
 }
 
+// fp64 forward of the training path (the loss chain's input). The per-point
+// loss scalars amplify the forward error: the adaptive weight
+// w'(f) ~ 2 exp(-k|f|) turns an error e in f into a relative error k*e of the
+// point's upstream factor (k = 50), and the eikonal factor 2(n - 1)/n turns
+// an error in grad f into a relative error e/|n - 1|. The training kernels
+// therefore blend in fp64, as make_corners / taylor_poly / eval_impl do
+// (taylor_grid.cpp:29-119), on the fp32 coefficients upcast: the oracle and
+// this forward then agree to fp64 rounding and only the fp32 storage of the
+// records and the gradient sums remain.
+template <int DIM, int ORDER, bool GRAD>
+__device__ __forceinline__ void blend_corner_d(const float* __restrict__ c, const DevSpec& s, const double* local,
+                                               int i, double& f, double* fg) {
+    // c: the vertex's K coefficients (shared memory or global), read where
+    // used so that only a few fp64 temporaries are live at a time
+    double sv[DIM], d[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        const int bit = (i >> a) & 1;
+        sv[a] = bit ? local[a] : 1.0 - local[a];
+        d[a] = (local[a] - (double)bit) * s.h[a];
+    }
+    auto H = [&](int j, int k) -> double {
+        const int lo = j < k ? j : k, hi = j < k ? k : j;
+        const int t = lo * DIM - lo * (lo - 1) / 2 + (hi - lo);
+        return (double)c[1 + DIM + t];
+    };
+    double T = (double)c[0];
+    if constexpr (ORDER == 1) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) T = fma((double)c[1 + a], d[a], T);
+    } else if constexpr (ORDER == 2) {
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) {
+            double aj = fma(H(j, j), 0.5 * d[j], (double)c[1 + j]);
+#pragma unroll
+            for (int k = j + 1; k < DIM; ++k) aj = fma(H(j, k), d[k], aj);
+            T = fma(d[j], aj, T);
+        }
+    }
+    double w = sv[0];
+#pragma unroll
+    for (int a = 1; a < DIM; ++a) w *= sv[a];
+    f = fma(w, T, f);
+    if constexpr (GRAD) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            double gTa = 0.0;  // dT/ddelta_a = f1_a + sum_k H_ak delta_k
+            if constexpr (ORDER >= 1) gTa = (double)c[1 + a];
+            if constexpr (ORDER == 2) {
+#pragma unroll
+                for (int k = 0; k < DIM; ++k) gTa = fma(H(a, k), d[k], gTa);
+            }
+            double other = 1.0;
+#pragma unroll
+            for (int b = 0; b < DIM; ++b)
+                if (b != a) other *= sv[b];
+            const double dw = (((i >> a) & 1) ? s.inv_h[a] : -s.inv_h[a]) * other;
+            fg[a] = fma(dw, T, fma(w, gTa, fg[a]));
+        }
+    }
+}
+
 // Value (+ spatial gradient) of the cell whose corner-0 vertex is `base`:
 // issue all 2^D block gathers first, then blend (eval_impl, taylor_grid.cpp:100-119).
 template <int DIM, int ORDER, bool GRAD>
@@ -376,7 +438,12 @@ constexpr unsigned kEikMark = 0x7fc0e1c5u;
 // would lose 1 - |...| to cancellation) at a fraction of the cost of an fp64
 // exp + divide.
 __device__ __forceinline__ float w_prime_f(double d, double k, float& e) {
-    e = expf(-(float)(k * fabs(d)));
+    // exp(-x) with x = k|d| in fp64: expf of the fp32-rounded argument times
+    // exp(-(x - xf)) ~ 1 - (x - xf), so the argument's rounding (up to
+    // 2^-24 x, i.e. 3e-6 relative at k|d| = 50) does not reach e
+    const double x = k * fabs(d);
+    const float xf = (float)x;
+    e = expf(-xf) * (1.0f - (float)(x - (double)xf));
     return 2.0f * e * __frcp_rn(1.0f + e);
 }
 // The reference's fp64 expression, for near ties only: which of w'(f) and
@@ -386,8 +453,8 @@ __device__ __forceinline__ double w_prime_d(double d, double k) {
     return 1.0 - fabs(2.0 * (1.0 / (1.0 + exp(-(k * d)))) - 1.0);
 }
 
-template <int DIM, bool EIK>
-__device__ __forceinline__ void point_loss(const LossDev& L, float f, const float* fg, float gt,
+template <int DIM, bool EIK, typename FT>
+__device__ __forceinline__ void point_loss(const LossDev& L, FT f, const FT* fg, float gt,
                                            double& recon, double& eik, float& u, float* gv) {
     const bool eik_point = L.fresh_eik && __float_as_uint(gt) == kEikMark;
     const double value = (double)f;

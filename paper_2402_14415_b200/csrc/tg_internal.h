@@ -95,6 +95,7 @@ struct Grid {
     bool slab = false;
     int zb0 = 0;
     int zb_global = 0;            // brick layers of the global grid
+    int code_sh[2] = {0, 0};      // bit offsets of y / z in a binning brick code
     double tv_inv_norm = 0.0;     // 1 / (P*K) of the global grid
     double* slab_red = nullptr;   // 8 doubles: local sums of the pending slab step
     int slab_in_idx = 0;

@@ -64,14 +64,17 @@ struct BinArgs {
     float4* binned;
     unsigned long long* nan;  // the bin set's NaN slot (Status::nan_bin)
     int zb0;  // first brick layer (slab grids)
+    int sh1, sh2;  // bit offsets of the y and z brick coordinates in a brick code (brick_code_shifts)
 };
 
-// Brick code of a point: its cell's brick coordinates (9 bits per axis) and
-// the per-axis "also the next brick" mask (bits 27..29), or -1 for a NaN
+// Brick code of a point: its cell's brick coordinates (x in bits [0, sh1),
+// y in [sh1, sh2), z from sh2 up; widths sized per grid by brick_code_shifts
+// so any grid whose brick count fits 2^27 packs without overlap) and the
+// per-axis "also the next brick" mask (bits 27..29), or -1 for a NaN
 // coordinate. Brick coordinates are global; code_bricks() maps them to this
 // grid's brick indices, dropping bricks outside a slab grid's layers.
 template <int DIM>
-__device__ __forceinline__ int point_brick_code(const DevSpec& s, const int* nb, const float4& q) {
+__device__ __forceinline__ int point_brick_code(const DevSpec& s, const BinArgs& A, const float4& q) {
     constexpr int B = BrickShape<DIM>::B;
     const float pf[3] = {q.x, q.y, q.z};
     int lo[3] = {0, 0, 0}, mask = 0;
@@ -84,13 +87,15 @@ __device__ __forceinline__ int point_brick_code(const DevSpec& s, const int* nb,
         lo[a] = c / B;
         mask |= ((c % B) == B - 1 ? 1 : 0) << a;
     }
-    (void)nb;
-    return lo[0] | (lo[1] << 9) | (lo[2] << 18) | (mask << 27);
+    return lo[0] | (lo[1] << A.sh1) | (lo[2] << A.sh2) | (mask << 27);
 }
 
 template <int DIM>
-__device__ __forceinline__ int code_bricks(int code, const int* nb, int zb0, int* out) {
-    const int bx = code & 511, by = (code >> 9) & 511, bz = (code >> 18) & 511, mask = code >> 27;
+__device__ __forceinline__ int code_bricks(int code, const BinArgs& A, int* out) {
+    const int* nb = A.nb;
+    const int zb0 = A.zb0;
+    const int bx = code & ((1 << A.sh1) - 1), by = (code >> A.sh1) & ((1 << (A.sh2 - A.sh1)) - 1),
+              bz = (code >> A.sh2) & ((1 << (27 - A.sh2)) - 1), mask = code >> 27;
     int m = 0;
     for (int dz = 0; dz <= (DIM == 3 ? (mask >> 2) & 1 : 0); ++dz) {
         const int lz = bz + dz - zb0;
@@ -106,13 +111,13 @@ template <int DIM>
 __global__ void __launch_bounds__(256) k_bin_count(BinArgs A) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < A.n;
          i += (long long)gridDim.x * blockDim.x) {
-        const int code = point_brick_code<DIM>(A.s, A.nb, A.pts[i]);
+        const int code = point_brick_code<DIM>(A.s, A, A.pts[i]);
         if (code < 0) {
             atomicMin(A.nan, (unsigned long long)i);
             continue;
         }
         int br[8];
-        const int m = code_bricks<DIM>(code, A.nb, A.zb0, br);
+        const int m = code_bricks<DIM>(code, A, br);
         for (int k = 0; k < m; ++k) atomicAdd(&A.count[br[k]], 1);
     }
 }
@@ -188,10 +193,10 @@ __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs A) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < A.n;
          i += (long long)gridDim.x * blockDim.x) {
         const float4 q = A.pts[i];
-        const int code = point_brick_code<DIM>(A.s, A.nb, q);
+        const int code = point_brick_code<DIM>(A.s, A, q);
         if (code < 0) continue;
         int br[8];
-        const int m = code_bricks<DIM>(code, A.nb, A.zb0, br);
+        const int m = code_bricks<DIM>(code, A, br);
         for (int k = 0; k < m; ++k) {
             const int slot = atomicAdd(&A.cursor[br[k]], 1);
             A.binned[slot] = q;
@@ -231,14 +236,14 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __rest
     for (int k = 0; k < kBinPer; ++k) {
         const long long i = t0 + threadIdx.x + (long long)k * kBinThreads;
         if (i >= A.n) continue;
-        const int code = point_brick_code<DIM>(A.s, A.nb, q[k]);
+        const int code = point_brick_code<DIM>(A.s, A, q[k]);
         codes[i] = code;
         if (code < 0) {
             atomicMin(A.nan, (unsigned long long)i);
             continue;
         }
         int br[8];
-        const int m = code_bricks<DIM>(code, A.nb, A.zb0, br);
+        const int m = code_bricks<DIM>(code, A, br);
         for (int j = 0; j < m; ++j) atomicAdd(&hist[br[j]], 1);
     }
     __syncthreads();
@@ -247,15 +252,25 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_hist(BinArgs A, int* __rest
 }
 
 // H columns -> per-(tile, brick) exclusive prefixes (in place); brick totals
-// -> exclusive offsets off[0..NB] via a chained scan over the CTAs (all CTAs
-// are co-resident; CTA i waits for CTA i-1's inclusive prefix, tagged with
-// this launch's epoch).
+// -> exclusive offsets off[0..NB] via a chained scan over the CTAs: CTA i
+// publishes its aggregate, then waits for those of CTAs 0..i-1 (tagged with
+// this launch's epoch). Not all CTAs need be co-resident (up to 512 CTAs of
+// up to 67.5 KB of shared memory, possibly sharing the SMs with a brick
+// kernel), and the CUDA model does not promise in-order dispatch, so the
+// index i is a ticket taken from a launch-spanning 64-bit counter at the
+// start of the CTA (ticket mod gridDim.x): a CTA only ever waits for CTAs
+// that started before it, which are resident and make progress.
 __global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta, int NB, int* __restrict__ off,
-                                                  int* __restrict__ chain, int epoch, int chunk, int* __restrict__ ord) {
+                                                  int* __restrict__ chain, unsigned long long* __restrict__ ticket,
+                                                  int epoch, int chunk, int* __restrict__ ord) {
     extern __shared__ int col[];  // [ncta][kColBricks + 1]
     __shared__ int tot[kColBricks];
     __shared__ int carry;
-    const int b0 = blockIdx.x * kColBricks;
+    __shared__ int tile_s;
+    if (threadIdx.x == 0) tile_s = (int)(atomicAdd(ticket, 1ull) % gridDim.x);
+    __syncthreads();
+    const int tile = tile_s;
+    const int b0 = tile * kColBricks;
     const int nb = min(kColBricks, NB - b0);
     constexpr int LD = kColBricks + 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -308,15 +323,15 @@ __global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta,
         }
         const int block_sum = __shfl_sync(0xffffffffu, x, 31);
         // publish this CTA's aggregate, then add up every predecessor's
-        // (all CTAs are co-resident and publish before looking back)
+        // (predecessors hold earlier tickets: already running)
         if (lane == 0) {
-            chain[2 * blockIdx.x + 1] = block_sum;
+            chain[2 * tile + 1] = block_sum;
             __threadfence();
-            atomicExch(&chain[2 * blockIdx.x], epoch);
+            atomicExch(&chain[2 * tile], epoch);
         }
         int prev = 0;
         volatile int* ch = chain;
-        for (int j = lane; j < (int)blockIdx.x; j += 32) {
+        for (int j = lane; j < tile; j += 32) {
             while (ch[2 * j] != epoch) {
             }
             __threadfence();
@@ -327,7 +342,7 @@ __global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta,
         (void)carry;
         const int c0 = prev;
         if (lane < nb) off[b0 + lane] = c0 + x - t;
-        if (blockIdx.x == gridDim.x - 1 && lane == 0) off[NB] = c0 + block_sum;
+        if (tile == (int)gridDim.x - 1 && lane == 0) off[NB] = c0 + block_sum;
         place_brick(b0 + lane, lane < nb, t, chunk, NB, ord);
     }
 }
@@ -354,7 +369,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_scatter_tiles(BinArgs A, co
     for (int k = 0; k < kBinPer; ++k) {
         if (cd[k] < 0) continue;
         int br[8];
-        const int m = code_bricks<DIM>(cd[k], A.nb, A.zb0, br);
+        const int m = code_bricks<DIM>(cd[k], A, br);
         for (int j = 0; j < m; ++j) A.binned[atomicAdd(&cur[br[j]], 1)] = q[k];
     }
 }
@@ -746,7 +761,8 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     float2 P[5];
 #pragma unroll
     for (int q = 0; q < 5; ++q) P[q] = make_float2(0.f, 0.f);
-    double recon_sum = 0.0, eik_sum = 0.0, home_pts = 0.0;
+    double recon_sum = 0.0, eik_sum = 0.0;
+    int home_pts = 0;
     int myv = tid;  // owned vertex of this thread; set per brick by the workload sort
 
     // Tiny bricks (at most kTiny points, one chunk): no counting sort. Records
@@ -767,16 +783,14 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         //     the fp64 loss chain write each record straight to its cell slot.
         int ec = 0, rank = 0;
         float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-        AxisF ax[DIM];
+        double lc[DIM];
         int tc[3] = {0, 0, 0};
         if (tid < m) {
             q = A.binned[base + tid];
             const float pf[3] = {q.x, q.y, q.z};
 #pragma unroll
             for (int a = 0; a < DIM; ++a) {
-                double local;
-                const int c = locate_axis(A.s, a, (double)pf[a], local);
-                ax[a] = axis_factors(A.s, a, local);
+                const int c = locate_axis(A.s, a, (double)pf[a], lc[a]);
                 tc[a] = c - (o[a] - 1);  // in [0, B]
             }
             ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
@@ -864,24 +878,27 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             bool home = true;
 #pragma unroll
             for (int a = 0; a < DIM; ++a) home &= tc[a] >= 1;
-            float f = 0.0f, fg[DIM];
+            // fp64 forward (blend_corner_d): the loss chain amplifies forward errors
+            double f = 0.0, fg[DIM];
 #pragma unroll
-            for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                float cb[K];
-                load_block<K, false>(tile + L::at(tc[0] + (c & 1), tc[1] + ((c >> 1) & 1),
-                                                  DIM == 3 ? tc[2] + ((c >> 2) & 1) : 0),
-                                     cb);
-                blend_corner<DIM, ORDER, EIK>(cb, corner_geom<DIM>(A.s, ax, c), f, fg);
-            }
+            for (int a = 0; a < DIM; ++a) fg[a] = 0.0;
+            // corners one at a time: the fp64 temporaries of one corner live at
+            // once (the vertex accumulators hold registers across the chunk loop)
+#pragma unroll 1
+            for (int c = 0; c < NC; ++c)
+                blend_corner_d<DIM, ORDER, EIK>(tile + L::at(tc[0] + (c & 1), tc[1] + ((c >> 1) & 1),
+                                                             DIM == 3 ? tc[2] + ((c >> 2) & 1) : 0),
+                                                A.s, lc, c, f, fg);
             double recon, eik;
             float u, gv[DIM];
             point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
+            AxisF ax[DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) ax[a] = axis_factors(A.s, a, lc[a]);
             if (home) {
                 recon_sum += recon;
                 eik_sum += eik;
-                home_pts += 1.0;
+                ++home_pts;
             }
             // record: s0/s1 rounded from fp64 (1 - l must not be formed from a
             // rounded l), u, g; lands in cell order
@@ -1213,7 +1230,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
 
     // ---- per-brick loss partials (fixed-order block reduction) ----
     {
-        const double v4[4] = {warp_sum_d(recon_sum), warp_sum_d(eik_sum), warp_sum_d(tv_sum), warp_sum_d(home_pts)};
+        const double v4[4] = {warp_sum_d(recon_sum), warp_sum_d(eik_sum), warp_sum_d(tv_sum), warp_sum_d((double)home_pts)};
         if (lane == 0)
             for (int k2 = 0; k2 < 4; ++k2) red[k2][warp] = v4[k2];
         __syncthreads();
@@ -1370,6 +1387,8 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     B.binned = g.binned[k];
     B.nan = &g.st->nan_bin[k];
     B.zb0 = g.zb0;
+    B.sh1 = g.code_sh[0];
+    B.sh2 = g.code_sh[1];
     int* const off = g.bin_off[k];
     int* const ord = g.brick_order[k];  // NB entries + 2 class counters
     const int ch = g.spec.dim == 3 ? BrickShape<3>::CH : BrickShape<2>::CH;
@@ -1406,7 +1425,8 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         if (g.bd_on) bd_mark(g, bs, 1);
         const int epoch = ++g.bin_epoch;
         k_bin_cols<<<(unsigned)((g.NB + kColBricks - 1) / kColBricks), 256, csm, bs>>>(
-            g.bin_hist, ncta, (int)g.NB, off, g.bin_chain, epoch, ch, ord);
+            g.bin_hist, ncta, (int)g.NB, off, g.bin_chain,
+            reinterpret_cast<unsigned long long*>(g.bin_chain + 2 * g.bin_chain_cap), epoch, ch, ord);
         if (g.bd_on) bd_mark(g, bs, 2);
         if (g.spec.dim == 3)
             k_bin_scatter_tiles<3><<<ncta, kBinThreads, sm, bs>>>(B, g.bin_hist, g.bin_codes, off, (int)g.NB);

@@ -100,12 +100,12 @@ __global__ void __launch_bounds__(256) k_point_terms(DevSpec s, const float* __r
             continue;
         }
         AxisF ax[DIM];
+        double lc[DIM];
         long long base = 0;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
-            double local;
-            const int c = locate_axis(s, a, x[a], local);
-            ax[a] = axis_factors(s, a, local);
+            const int c = locate_axis(s, a, x[a], lc[a]);
+            ax[a] = axis_factors(s, a, lc[a]);
             base += (long long)c * (a == 0 ? 1LL : (a == 1 ? s.sy : s.sz));
         }
         float cb[1 << DIM][K];
@@ -114,11 +114,11 @@ __global__ void __launch_bounds__(256) k_point_terms(DevSpec s, const float* __r
             const long long vid = base + (c & 1) + ((c >> 1) & 1) * s.sy + (DIM == 3 ? ((c >> 2) & 1) * s.sz : 0);
             load_block<K, true>(coeffs + vid * K, cb[c]);
         }
-        float f = 0.0f, fg[DIM];
+        double f = 0.0, fg[DIM];  // fp64 forward, as the fused step (blend_corner_d)
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
+        for (int a = 0; a < DIM; ++a) fg[a] = 0.0;
 #pragma unroll
-        for (int c = 0; c < (1 << DIM); ++c) blend_corner<DIM, ORDER, EIK>(cb[c], corner_geom<DIM>(s, ax, c), f, fg);
+        for (int c = 0; c < (1 << DIM); ++c) blend_corner_d<DIM, ORDER, EIK>(cb[c], s, lc, c, f, fg);
         double recon, eik;
         float u, gv[DIM];
         point_loss<DIM, EIK>(L, f, fg, q.w, recon, eik, u, gv);
