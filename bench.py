@@ -241,8 +241,8 @@ def ref_train_sample(wl, batches, steps, threads=None):
     R = Reference()
     s = Spec(dim=3, res=(W["res"],) * 3, order=2)
     threads = threads or ref_train_threads(W["res"])
-    seq = np.array([batches[i % len(batches)] for i in range(steps)], dtype=np.float64)
-    _, terms, secs = R.train(s, None, seq, Loss(), lr=W["lr"], threads=threads)
+    _, terms, secs = R.train(s, None, np.array(batches, dtype=np.float64), Loss(), lr=W["lr"], threads=threads,
+                             steps=steps)
     return secs, terms, threads
 
 

@@ -278,6 +278,44 @@ int tgcu_slab_halo_slots(tgcu_grid* g, float* recv_lo[2], float* recv_hi[2]);
  * planes (*ok = 1 when both sides match). Synchronous. */
 int tgcu_slab_peer_probe(tgcu_grid* g, int phase, int* ok);
 
+/* ---- communicator of a multi-GPU job (comm.cu; no PyTorch / MPI) ----------
+ * One process per GPU. Rank 0 listens on addr:port and every other rank
+ * connects (a TCP star that carries the bootstrap and the host-side
+ * collectives). backend TGCU_COMM_NCCL: the slab step's all-reduce and halo
+ * send/recv run as NCCL collectives on the step's stream (libnccl.so.2 is
+ * loaded at run time); TGCU_COMM_HOST: the same collectives staged through
+ * host memory over the star (tests, ranks sharing a device). Host
+ * reductions combine the ranks in rank order (identical bits everywhere). */
+enum { TGCU_COMM_NCCL = 0, TGCU_COMM_HOST = 1 };
+typedef struct tgcu_comm tgcu_comm;
+int tgcu_comm_create(const char* addr, int port, int rank, int nranks, int device, int backend, tgcu_comm** out);
+int tgcu_comm_destroy(tgcu_comm* c);
+int tgcu_comm_info(const tgcu_comm* c, int* rank, int* nranks, int* backend);
+int tgcu_comm_barrier(tgcu_comm* c);
+/* In-place reduction of n host doubles over the ranks: op 0 sum, 1 max, 2 min. */
+int tgcu_comm_allreduce_host(tgcu_comm* c, double* buf, int n, int op);
+/* out (nranks x bytes, rank order) receives every rank's `bytes` bytes. */
+int tgcu_comm_allgather_host(tgcu_comm* c, const void* in, int64_t bytes, void* out);
+
+/* Routed host point-to-point (collective: every rank calls it): send nsend
+ * buffers to ranks dst[i]; receive nrecv buffers from ranks src[j] (sizes
+ * must match; several messages from one rank arrive in send order). */
+int tgcu_comm_exchange_host(tgcu_comm* c, int nsend, const int* dst, const void* const* sbuf, const int64_t* sbytes,
+                            int nrecv, const int* src, void* const* rbuf, const int64_t* rbytes);
+
+/* Attach a slab grid to the job: checks that the ranks' slabs tile the grid
+ * in rank order, exchanges the initial halo planes, and (fused_halo != 0)
+ * sets up the peer-memory halo (IPC handles over the star + probe round trip,
+ * all ranks or none). *fused_out = 1 when the fused halo is active. */
+int tgcu_slab_connect(tgcu_grid* g, tgcu_comm* c, int fused_halo, int* fused_out);
+/* One slab training step over the attached communicator:
+ * tgcu_slab_step_begin -> all-reduce of the 5 partials -> tgcu_slab_step_finish
+ * -> halo planes (unless fused). Same flags / out semantics as
+ * tgcu_train_step (TGCU_ASYNC with out == NULL: stream-ordered, no host sync
+ * on the NCCL backend). */
+int tgcu_slab_train_step(tgcu_grid* g, const float* samples, int64_t n, int64_t n_global,
+                         const tgcu_loss_config* cfg, tgcu_loss_terms* out, int flags, void* stream);
+
 /* Fused steps issued on this grid since creation or the last reported error;
  * error messages of a failed step name it as "step <this index at launch>". */
 int tgcu_grid_steps_launched(const tgcu_grid* g, int64_t* n);

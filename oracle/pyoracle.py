@@ -91,6 +91,7 @@ class Oracle:
         L = C.CDLL(path)
         L.tgo_eval.restype = C.c_double
         L.tgo_eval.argtypes = [C.POINTER(_TgoSpec), _D, _D, _D]
+        L.tgo_eval_batch_f32.argtypes = [C.POINTER(_TgoSpec), C.c_void_p, _D, C.c_int64, _D, _D]
         L.tgo_locate.argtypes = [C.POINTER(_TgoSpec), _D, _I, _D, _L]
         L.tgo_backprop.argtypes = [C.POINTER(_TgoSpec), _D, C.c_double, _D, _D]
         L.tgo_adaptive_weight.restype = C.c_double
@@ -141,6 +142,17 @@ class Oracle:
             vals[i] = self.L.tgo_eval(C.byref(sp), _dp(coeffs), _dp(pts[i]), g3 if want_grad else None)
             if want_grad:
                 grads[i] = list(g3)
+        return (vals, grads) if want_grad else vals
+
+    def eval_f32(self, s: Spec, coeffs32, pts, want_grad=False):
+        """eval on fp32-stored coefficients (upcast exactly), batched in C."""
+        sp = self._spec(s)
+        c = np.ascontiguousarray(coeffs32, dtype=np.float32)
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        vals = np.empty(len(pts))
+        grads = np.zeros((len(pts), 3)) if want_grad else None
+        self.L.tgo_eval_batch_f32(C.byref(sp), c.ctypes.data_as(C.c_void_p), _dp(pts), len(pts), _dp(vals),
+                                  _dp(grads))
         return (vals, grads) if want_grad else vals
 
     def backprop(self, s: Spec, pts, upstream, upstream_vec, grad):
@@ -328,7 +340,7 @@ class Reference:
         L.tgr_total_loss_fresh.argtypes = sp + [_D, _D, C.c_int64, C.c_double, C.c_double, C.c_double,
                                                 C.c_int, C.c_int, C.c_int, C.c_uint64, _D, C.c_int, _D]
         L.tgr_eikonal_loss.argtypes = sp + [_D, _D, C.c_int64, C.c_double, _D, _D]
-        L.tgr_train.argtypes = sp + [_D, _D, C.c_int64, C.c_int, C.c_double, C.c_double, C.c_double,
+        L.tgr_train.argtypes = sp + [_D, _D, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                      C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                      C.c_double, C.c_int, _D, _D]
         L.tgr_eval_timed.argtypes = sp + [_D, _D, C.c_int64, _D, C.c_int, _D]
@@ -455,16 +467,18 @@ class Reference:
         return tt.value
 
     def train(self, s: Spec, coeffs, batches, cfg: Loss, lr, beta1=0.9, beta2=0.999, eps=1e-8,
-              threads=1):
+              threads=1, steps=None):
         """Returns (final coeffs, per-step terms (steps×4), seconds in the step loop).
         coeffs None: the reference's zero init inside the library (no host copy;
-        the returned coeffs are None)."""
+        the returned coeffs are None). steps (default: one per batch): step i
+        uses batch i % len(batches)."""
         p = None if coeffs is None else np.array(coeffs, dtype=np.float64)
         batches = np.ascontiguousarray(batches, dtype=np.float64)
-        steps, n = batches.shape[0], batches.shape[1]
+        nb, n = batches.shape[0], batches.shape[1]
+        steps = nb if steps is None else int(steps)
         terms = np.zeros((steps, 4))
         secs = C.c_double()
-        self._err(self.L.tgr_train(*_spec_args(s), _dp(p), _dp(batches), n, steps, cfg.lambda1,
+        self._err(self.L.tgr_train(*_spec_args(s), _dp(p), _dp(batches), n, nb, steps, cfg.lambda1,
                                    cfg.lambda2, cfg.k, int(cfg.use_weighting), int(cfg.use_tv),
                                    int(cfg.differentiate_weight), lr, beta1, beta2, eps, threads,
                                    _dp(terms), C.byref(secs)))

@@ -264,7 +264,7 @@ int tgr_adam_step(double* p, const double* g, double* m, double* v, int64_t n, i
 // supplied by the caller (steps × n × 4). coeffs is updated in place; the
 // per-step LossTerms go to terms_out (steps × 4).
 int tgr_train(int dim, const int* res, const double* origin, const double* extent, int order,
-              double* coeffs, const double* batches, int64_t n, int steps, double lambda1,
+              double* coeffs, const double* batches, int64_t n, int nbatch, int steps, double lambda1,
               double lambda2, double k, int use_weighting, int use_tv, int differentiate_weight,
               double lr, double beta1, double beta2, double eps, int threads, double* terms_out,
               double* seconds_out) {
@@ -276,7 +276,8 @@ int tgr_train(int dim, const int* res, const double* origin, const double* exten
         std::vector<double> grad(grid.coeffs.size());
         double secs = 0.0;
         for (int s = 0; s < steps; ++s) {
-            const auto batch = make_batch(batches + 4 * n * static_cast<int64_t>(s), n, dim);
+            // step s uses batch s % nbatch (a long run cycles a few stored batches)
+            const auto batch = make_batch(batches + 4 * n * static_cast<int64_t>(s % nbatch), n, dim);
             const auto t0 = std::chrono::steady_clock::now();
             std::fill(grad.begin(), grad.end(), 0.0);
             const tg::LossTerms t = tg::total_loss(grid, batch, cfg, grad, threads);

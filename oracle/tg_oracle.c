@@ -171,6 +171,41 @@ double tgo_eval(const tgo_spec* s, const double* coeffs, const double p[3], doub
     return value;
 }
 
+/* tgo_eval over fp32-stored coefficients (each upcast exactly before use, so
+ * the arithmetic is tgo_eval's on the same values), batched: lets a parity
+ * test evaluate the oracle on a multi-GB fp32 device grid downloaded as is
+ * (BASELINE C4, 512^3) without a second fp64 copy. */
+void tgo_eval_batch_f32(const tgo_spec* s, const float* coeffs, const double* pts, int64_t n, double* vals,
+                        double* grads) {
+    const int K = tgo_coeff_count(s->order, s->dim);
+    for (int64_t q = 0; q < n; ++q) {
+        const double* p = pts + 3 * q;
+        int cell[3];
+        double local[3];
+        int64_t vid[8];
+        if (tgo_locate(s, p, cell, local, vid) != 0) {
+            vals[q] = NAN;
+            continue;
+        }
+        corners_t c;
+        make_corners(s, local, vid, &c);
+        double value = 0.0;
+        double g[3] = {0.0, 0.0, 0.0};
+        for (int i = 0; i < c.count; ++i) {
+            double b[10];
+            for (int k = 0; k < K; ++k) b[k] = (double)coeffs[c.vid[i] * K + k];
+            double tg[3];
+            const double tv = taylor_poly(b, s->order, s->dim, c.delta[i], grads ? tg : NULL);
+            value += c.w[i] * tv;
+            if (grads)
+                for (int a = 0; a < s->dim; ++a) g[a] += c.dw[i][a] * tv + c.w[i] * tg[a];
+        }
+        vals[q] = value;
+        if (grads)
+            for (int a = 0; a < 3; ++a) grads[3 * q + a] = g[a];
+    }
+}
+
 /* Test helper for the gradient tolerance: per axis, the L1 size of the terms
  * whose sum is the spatial gradient (sum_i |dw_i,a T_i| + |w_i gT_i,a|). An
  * fp32 forward resolves grad f only to ~eps32 times this, which on fine grids
@@ -392,15 +427,19 @@ static void point_terms(const tgo_spec* s, const double* coeffs, const double* s
         const double resid = value - gt;
         const double w = cfg->use_weighting ? tgo_adaptive_weight(value, gt, cfg->k) : 1.0;
         recon += w * fabs(resid);
-        double upstream = 0.0;
+        double upstream = 0.0, upstream_l1 = 0.0;
         double uvec[3] = {0.0, 0.0, 0.0};
         if (grad || mass) {
             upstream = recon_scale * inv_n * w * sign_of(resid);
+            upstream_l1 = fabs(upstream);
             if (cfg->use_weighting && cfg->differentiate_weight) {
                 const double wp_pred = w_prime(value, cfg->k);
                 const double wp_gt = w_prime(gt, cfg->k);
-                if (wp_pred > wp_gt)
-                    upstream += recon_scale * inv_n * fabs(resid) * w_prime_deriv(value, cfg->k);
+                if (wp_pred > wp_gt) {
+                    const double dw = recon_scale * inv_n * fabs(resid) * w_prime_deriv(value, cfg->k);
+                    upstream += dw;
+                    upstream_l1 += fabs(dw);
+                }
             }
         }
         if (want_eik) {
@@ -433,7 +472,10 @@ static void point_terms(const tgo_spec* s, const double* coeffs, const double* s
                     for (int a = 0; a < 3; ++a) umass[a] = fabs(sc) * (fabs(sg[a]) + 0.25 * l1[a]);
                 }
             }
-            tgo_backprop_mass(s, p, upstream, umass, mass);
+            /* the upstream's L1 size: the weight term and the
+             * differentiate_weight term are formed separately (fp32
+             * roundings of each) and may cancel in their sum */
+            tgo_backprop_mass(s, p, upstream_l1, umass, mass);
         }
     }
     *recon_out = recon;

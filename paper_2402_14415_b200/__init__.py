@@ -170,6 +170,15 @@ def lib():
     L.tgcu_eikonal_loss.argtypes = [P, P, C.c_int64, C.c_double, P, C.POINTER(C.c_double), C.c_int, P]
     L.tgcu_train_step_fresh_eik.argtypes = [P, P, C.c_int64, P, C.POINTER(_Loss), C.POINTER(_Terms), C.c_int, P]
     L.tgcu_shuffle_order.argtypes = [C.c_uint64, C.c_int64, P]
+    L.tgcu_comm_create.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(P)]
+    L.tgcu_comm_destroy.argtypes = [P]
+    L.tgcu_comm_info.argtypes = [P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.tgcu_comm_barrier.argtypes = [P]
+    L.tgcu_comm_allreduce_host.argtypes = [P, P, C.c_int, C.c_int]
+    L.tgcu_comm_allgather_host.argtypes = [P, P, C.c_int64, P]
+    L.tgcu_comm_exchange_host.argtypes = [P, C.c_int, P, P, P, C.c_int, P, P, P]
+    L.tgcu_slab_connect.argtypes = [P, P, C.c_int, C.POINTER(C.c_int)]
+    L.tgcu_slab_train_step.argtypes = [P, P, C.c_int64, C.c_int64, C.POINTER(_Loss), C.POINTER(_Terms), C.c_int, P]
     _lib = L
     return L
 

@@ -256,4 +256,6 @@ void launch_draw_batch(const float* pool, int64_t pool_n, int64_t n, uint64_t se
 
 struct tgcu_grid {
     tgcu::Grid g;
+    tgcu_comm* comm = nullptr;  // slab grids: the job's communicator (tgcu_slab_connect, comm.cu)
+    bool fused_halo = false;    // boundary planes stored into the neighbours by the brick kernel
 };

@@ -493,6 +493,7 @@ struct StepArgs {
     float tv_gscale;
     int want_tv;
     float lr, b1, b2, eps, inv_bc1, inv_bc2;
+    float c1, c2;  // 1 - beta1, 1 - beta2 formed in fp64 (1 - 0.999f would be 1.3e-5 off)
     double* partials;  // NB x 4: recon, eik, tv, home points
     Status* st;
     float* grad_out;   // optional: full gradient (validation mode, TGCU_EXPORT_GRAD)
@@ -878,6 +879,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             bool home = true;
 #pragma unroll
             for (int a = 0; a < DIM; ++a) home &= tc[a] >= 1;
+#ifndef TGCU_FP32_FORWARD
             // fp64 forward (blend_corner_d): the loss chain amplifies forward errors
             double f = 0.0, fg[DIM];
 #pragma unroll
@@ -889,12 +891,29 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                 blend_corner_d<DIM, ORDER, EIK>(tile + L::at(tc[0] + (c & 1), tc[1] + ((c >> 1) & 1),
                                                              DIM == 3 ? tc[2] + ((c >> 2) & 1) : 0),
                                                 A.s, lc, c, f, fg);
-            double recon, eik;
-            float u, gv[DIM];
-            point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
             AxisF ax[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) ax[a] = axis_factors(A.s, a, lc[a]);
+#else
+            // fp32 forward (A/B builds only)
+            AxisF ax[DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) ax[a] = axis_factors(A.s, a, lc[a]);
+            float f = 0.0f, fg[DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                float cb[K];
+                load_block<K, false>(tile + L::at(tc[0] + (c & 1), tc[1] + ((c >> 1) & 1),
+                                                  DIM == 3 ? tc[2] + ((c >> 2) & 1) : 0),
+                                     cb);
+                blend_corner<DIM, ORDER, EIK>(cb, corner_geom<DIM>(A.s, ax, c), f, fg);
+            }
+#endif
+            double recon, eik;
+            float u, gv[DIM];
+            point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
             if (home) {
                 recon_sum += recon;
                 eik_sum += eik;
@@ -1079,7 +1098,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                 hi[a] = A.want_tv && g3[a] + 1 < A.s.res[a];
                 lo[a] = A.want_tv && g3[a] >= 1;
             }
-            const float c1 = 1.0f - A.b1, c2 = 1.0f - A.b2, lr_bc1 = A.lr * A.inv_bc1;
+            const float c1 = A.c1, c2 = A.c2, lr_bc1 = A.lr * A.inv_bc1;
             if constexpr (K % 2 == 0) {
                 // channel pairs on the packed fp32x2 pipe (FFMA2 / FADD2 / FMUL2)
                 const float2 gsc = make_float2(A.tv_gscale, A.tv_gscale);
@@ -1475,6 +1494,8 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     A.lr = (float)g.adam.lr;
     A.b1 = (float)g.adam.beta1;
     A.b2 = (float)g.adam.beta2;
+    A.c1 = (float)(1.0 - g.adam.beta1);
+    A.c2 = (float)(1.0 - g.adam.beta2);
     A.eps = (float)g.adam.eps;
     A.inv_bc1 = (float)inv_bc1;
     A.inv_bc2 = (float)inv_bc2;

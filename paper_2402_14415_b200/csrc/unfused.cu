@@ -276,13 +276,13 @@ __global__ void k_adam_check(const float* __restrict__ g, long long n, Status* s
 // adam_step pass 2 (adam.cpp:36-55), in place, fp32 state, host fp64 bias
 // corrections.
 __global__ void k_adam_update(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
-                              float* __restrict__ v, long long n, float lr, float b1, float b2, float eps,
-                              float inv_bc1, float inv_bc2) {
+                              float* __restrict__ v, long long n, float lr, float b1, float b2, float c1,
+                              float c2, float eps, float inv_bc1, float inv_bc2) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const float gi = g[i];
-        const float mi = fmaf(b1, m[i], (1.0f - b1) * gi);
-        const float vi = fmaf(b2, v[i], (1.0f - b2) * gi * gi);
+        const float mi = fmaf(b1, m[i], c1 * gi);
+        const float vi = fmaf(b2, v[i], c2 * gi * gi);
         m[i] = mi;
         v[i] = vi;
         p[i] -= lr * (mi * inv_bc1) / (sqrtf(vi * inv_bc2) + eps);
@@ -298,7 +298,8 @@ void launch_adam_check(Grid& g, const float* grad, cudaStream_t s) {
 void launch_adam_update(Grid& g, const float* grad, double inv_bc1, double inv_bc2, cudaStream_t s) {
     k_adam_update<<<grid_blocks(g.NC, 256, 148 * 16), 256, 0, s>>>(
         g.p[g.cur], grad, g.m[g.cur], g.v[g.cur], g.NC, (float)g.adam.lr, (float)g.adam.beta1,
-        (float)g.adam.beta2, (float)g.adam.eps, (float)inv_bc1, (float)inv_bc2);
+        (float)g.adam.beta2, (float)(1.0 - g.adam.beta1), (float)(1.0 - g.adam.beta2), (float)g.adam.eps,
+        (float)inv_bc1, (float)inv_bc2);
     count_launch();
     TGCU_CUDA(cudaGetLastError());
 }

@@ -257,95 +257,101 @@ class SlabGrid:
         return ms.value, n.value
 
 
+TGCU_COMM_NCCL, TGCU_COMM_HOST = 0, 1
+
+
+class Comm:
+    """One rank of a multi-GPU job (tgcu_comm, csrc/comm.cu): a TCP star
+    rooted at rank 0 (addr:port) for the bootstrap and host collectives, and
+    NCCL (backend "nccl", loaded by libtgcu at run time) or host-staged
+    ("host": tests, ranks sharing a device) device collectives. No PyTorch.
+    Defaults: MASTER_ADDR, TGCU_COMM_PORT (else MASTER_PORT + 17, clear of a
+    torch.distributed store on MASTER_PORT), TGCU_COMM_BACKEND (else nccl)."""
+
+    def __init__(self, rank: int, world: int, device: int = 0, addr: Optional[str] = None,
+                 port: Optional[int] = None, backend: Optional[str] = None):
+        import os
+        addr = addr or os.environ.get("MASTER_ADDR", "127.0.0.1")
+        if port is None:
+            port = int(os.environ.get("TGCU_COMM_PORT", int(os.environ.get("MASTER_PORT", "29500")) + 17))
+        backend = backend or os.environ.get("TGCU_COMM_BACKEND", "nccl")
+        if backend not in ("nccl", "host"):
+            raise ValueError(f"Comm: unknown backend {backend!r}")
+        self.rank, self.world, self.backend = rank, world, backend
+        h = C.c_void_p()
+        _check(lib().tgcu_comm_create(addr.encode(), int(port), rank, world, device,
+                                      TGCU_COMM_NCCL if backend == "nccl" else TGCU_COMM_HOST, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tgcu_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def barrier(self):
+        _check(lib().tgcu_comm_barrier(self._h))
+
+    def allreduce(self, values, op: str = "sum") -> np.ndarray:
+        """Host doubles reduced over the ranks in rank order (sum / max / min)."""
+        a = np.ascontiguousarray(np.atleast_1d(np.asarray(values, dtype=np.float64))).copy()
+        _check(lib().tgcu_comm_allreduce_host(self._h, _ptr(a), a.size, {"sum": 0, "max": 1, "min": 2}[op]))
+        return a
+
+    def allgather(self, blob: bytes) -> List[bytes]:
+        n = len(blob)
+        inb = (C.c_ubyte * max(n, 1)).from_buffer_copy(blob or b"\0")
+        out = (C.c_ubyte * max(n * self.world, 1))()
+        _check(lib().tgcu_comm_allgather_host(self._h, inb, n, out))
+        raw = bytes(out)
+        return [raw[r * n:(r + 1) * n] for r in range(self.world)]
+
+    def exchange(self, sends, recvs):
+        """Routed host point-to-point (collective). sends: [(dst, ndarray)],
+        recvs: [(src, ndarray to fill)]."""
+        sends = [(d, np.ascontiguousarray(a)) for d, a in sends]
+        ns, nr = len(sends), len(recvs)
+        dst = (C.c_int * max(ns, 1))(*[d for d, _ in sends])
+        sb = (C.c_void_p * max(ns, 1))(*[a.ctypes.data for _, a in sends])
+        sz = (C.c_int64 * max(ns, 1))(*[a.nbytes for _, a in sends])
+        src = (C.c_int * max(nr, 1))(*[s_ for s_, _ in recvs])
+        rb = (C.c_void_p * max(nr, 1))(*[a.ctypes.data for _, a in recvs])
+        rz = (C.c_int64 * max(nr, 1))(*[a.nbytes for _, a in recvs])
+        _check(lib().tgcu_comm_exchange_host(self._h, ns, dst, sb, sz, nr, src, rb, rz))
+
+
 class SlabTrainer:
-    """One rank of a torch.distributed (NCCL) slab-parallel training run."""
+    """One rank of a slab-parallel training run: the slab grid, attached to
+    the job's Comm (tgcu_slab_connect: initial halo, peer-memory halo set up
+    when every rank can open its neighbours' buffers), stepped with
+    tgcu_slab_train_step. No PyTorch on this path."""
 
     def __init__(self, spec: GridSpec, rank: int, world: int, adam: AdamConfig, device: int = 0,
-                 opts: Optional[InitOptions] = None, ranges=None):
-        import torch.distributed as dist
-        self.dist = dist
+                 opts: Optional[InitOptions] = None, ranges=None, comm: Optional[Comm] = None,
+                 fused_halo: Optional[bool] = None):
+        import os
         self.rank, self.world = rank, world
         nbz = brick_layers(spec.resolution[2])
         self.ranges = ranges or slab_ranges(nbz, world)
         lo, hi = self.ranges[rank]
+        self.comm = comm or Comm(rank, world, device)
+        self.backend = self.comm.backend
         self.slab = SlabGrid(spec, lo, hi, opts, device)
         self.slab.adam_reset(adam)
-        self.exchange()  # halo planes of the initial parameters
-        self.fused_halo = self._setup_fused_halo()
-
-    def _all_ok(self, ok: bool) -> bool:
-        import torch
-        dev = "cpu" if self._staged() else "cuda"
-        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
-        return bool(int(t.item()))
-
-    def _setup_fused_halo(self) -> bool:
-        """Peer-memory halo (tgcu_slab_ipc_export/import): the brick kernel of a
-        boundary brick layer writes the new boundary plane straight into the
-        neighbour's halo plane, so no exchange follows a step. Every rank
-        must succeed (IPC open + a probe round trip) or all keep exchanging.
-        TGCU_FUSED_HALO=0 disables it."""
-        import os
-        if self.world == 1 or os.environ.get("TGCU_FUSED_HALO", "1") == "0":
-            return False
-        ok = True
-        try:
-            blob = self.slab.ipc_export()
-        except Exception:
-            blob, ok = b"", False
-        blobs = [None] * self.world
-        self.dist.all_gather_object(blobs, blob)
-        try:
-            if ok and self.rank > 0:
-                self.slab.ipc_import(0, blobs[self.rank - 1])
-            if ok and self.rank < self.world - 1:
-                self.slab.ipc_import(1, blobs[self.rank + 1])
-        except Exception:
-            ok = False
-        ok = self._all_ok(ok)
-        if ok:
-            self.slab.peer_probe(0)
-            self.dist.barrier()
-            ok = self._all_ok(self.slab.peer_probe(1))
-        if not ok:
-            self.slab.set_peer_planes((0, 0), (0, 0))
-        return ok
-
-    def _staged(self) -> bool:
-        # NCCL moves device memory directly; gloo (CPU tests, one shared GPU)
-        # goes through host copies.
-        return self.dist.get_backend() != "nccl"
-
-    def exchange(self):
-        """Send owned boundary planes to the neighbours, receive their halo planes."""
-        dist = self.dist
-        s_lo, s_hi, r_lo, r_hi, pf = self.slab.halo()
-        staged = self._staged()
-        if staged:
-            import torch
-            torch.cuda.synchronize()
-        sends, recvs = [], []
-        if s_lo:
-            sends.append((device_view(s_lo, pf), self.rank - 1))
-            recvs.append((device_view(r_lo, pf), self.rank - 1))
-        if s_hi:
-            sends.append((device_view(s_hi, pf), self.rank + 1))
-            recvs.append((device_view(r_hi, pf), self.rank + 1))
-        if not sends:
-            return
-        if staged:
-            sbuf = [(t.cpu(), peer) for t, peer in sends]
-            rbuf = [(t.cpu(), peer, t) for t, peer in recvs]
-            reqs = [dist.isend(t, peer) for t, peer in sbuf] + [dist.irecv(t, peer) for t, peer, _ in rbuf]
-            for r in reqs:
-                r.wait()
-            for t, _, dev in rbuf:
-                dev.copy_(t)
-        else:
-            ops = [dist.P2POp(dist.isend, t, p) for t, p in sends] + [dist.P2POp(dist.irecv, t, p) for t, p in recvs]
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        if fused_halo is None:
+            fused_halo = os.environ.get("TGCU_FUSED_HALO", "1") != "0"
+        f = C.c_int(0)
+        _check(lib().tgcu_slab_connect(self.slab.handle, self.comm.handle, 1 if fused_halo else 0, C.byref(f)))
+        self.fused_halo = bool(f.value)
 
     def local_points(self, samples):
         """The points of a global batch this rank's slab needs (host numpy):
@@ -354,21 +360,29 @@ class SlabTrainer:
         a = np.asarray(samples)
         return np.ascontiguousarray(a[slab_point_mask(self.slab.spec, a.astype(np.float64), lo, hi)])
 
-    def step(self, samples_dev, cfg: LossConfig, stream=None, want_terms=False, n_global: int = 0,
+    def step(self, samples, cfg: LossConfig, stream=None, want_terms=False, n_global: int = 0,
              input_ready: bool = False):
-        """One step. samples_dev: the global batch, or this rank's local_points
-        with n_global = the global batch size."""
-        part = self.slab.begin(samples_dev, cfg, stream=stream, n_global=n_global, input_ready=input_ready)
-        t = device_view(part, 5, "<f8")
-        if self._staged():
-            import torch
-            torch.cuda.synchronize()
-            h = t.cpu()
-            self.dist.all_reduce(h)
-            t.copy_(h)
+        """One step (tgcu_slab_train_step). samples: the global batch, or this
+        rank's local_points with n_global = the global batch size; host numpy
+        or a CUDA tensor. want_terms=False: stream-ordered (NCCL backend)."""
+        from . import TGCU_INPUT_READY, _dev_f32, _is_torch
+        flags = 0 if _is_torch(samples) else TGCU_HOST
+        if flags == 0:
+            _dev_f32(samples, 4, "slab samples")
+            if input_ready:
+                flags |= TGCU_INPUT_READY
         else:
-            self.dist.all_reduce(t)
-        terms = self.slab.finish(part, asynchronous=not want_terms, stream=stream)
-        if not self.fused_halo:
-            self.exchange()
-        return terms
+            samples = np.ascontiguousarray(np.asarray(samples, dtype=np.float32)).reshape(-1, 4)
+        st = C.c_void_p(stream) if stream else None
+        if want_terms:
+            t = _Terms()
+            _check(lib().tgcu_slab_train_step(self.slab.handle, _ptr(samples), samples.shape[0], int(n_global),
+                                              C.byref(cfg._c()), C.byref(t), flags, st))
+            return LossTerms._from(t)
+        _check(lib().tgcu_slab_train_step(self.slab.handle, _ptr(samples), samples.shape[0], int(n_global),
+                                          C.byref(cfg._c()), None, flags | TGCU_ASYNC, st))
+        return None
+
+    def close(self):
+        self.slab.close()
+        self.comm.close()

@@ -39,11 +39,16 @@ def test_bench_two_rank_slab_flow():
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    env = dict(os.environ, TGCU_DIST_BACKEND="gloo")
+    # both ranks share the one GPU: gloo for the bench's own barriers / max,
+    # libtgcu's host-staged communicator for the slab step (NCCL refuses two
+    # ranks on one device)
+    env = dict(os.environ, TGCU_DIST_BACKEND="gloo", TGCU_COMM_BACKEND="host")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
-                        "--steps", "4", "--warmup", "3", "--no-query", "--no-cpu-baseline"],
+                        "--steps", "4", "--warmup", "3", "--no-cpu-baseline"],
                        cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     d = _line(r.stdout)
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["loss_last"] == d["loss_last"]
+    assert d["scaling"] == "strong" and d["config"]["grid"] == [256, 256, 256]  # C3 strong scaling
+    assert d["collectives"] == "host" and len(d["per_rank_kernel_ms"]) == 2 and d["single_gpu"]["value"] > 0

@@ -1,4 +1,7 @@
-"""Multi-GPU z-slab partition logic, world size 2 over gloo on CPU.
+"""Multi-GPU z-slab partition logic, world size 2 on CPU, over libtgcu's own
+communicator (tgcu_comm, host backend: the TCP star, fixed-order host
+all-reduce and routed point-to-point that carry the GPU job's bootstrap and
+its host-staged collectives; no PyTorch, no GPU needed).
 
 Each rank runs the owner-computes slab algorithm of paper_2402_14415_b200/slab.py
 with the CPU oracle as compute engine: it keeps the points whose cells touch its
@@ -49,13 +52,11 @@ def _batches():
 def _rank_main(rank, world, port, outdir):
     import sys
     sys.path.insert(0, ROOT)
-    import torch
-    import torch.distributed as dist
     from oracle.pyoracle import Loss, Oracle, Spec
     from paper_2402_14415_b200 import GridSpec
-    from paper_2402_14415_b200.slab import (brick_layers, home_point_mask, owned_planes, slab_point_mask,
+    from paper_2402_14415_b200.slab import (Comm, brick_layers, home_point_mask, owned_planes, slab_point_mask,
                                             slab_ranges)
-    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    comm = Comm(rank, world, addr="127.0.0.1", port=port, backend="host")
     O = Oracle()
     s = Spec(dim=3, res=RES, order=2)
     gs = GridSpec(dim=3, resolution=RES, order=2)
@@ -90,10 +91,9 @@ def _rank_main(rank, world, port, outdir):
         block = own[z0:z1]
         tv_pairs += np.sum((block[:, :, 1:] - block[:, :, :-1]) ** 2) + np.sum((block[:, 1:] - block[:, :-1]) ** 2)
         tv_pairs += np.sum((own[z0 + 1:zt + 1] - own[z0:zt]) ** 2)
-        part = torch.tensor([hv[1] * nh, hv[2] * nh, tv_pairs], dtype=torch.float64)
-        dist.all_reduce(part)
+        part = comm.allreduce([hv[1] * nh, hv[2] * nh, tv_pairs])
         P = (RES[0] - 1) * RES[1] * RES[2] + RES[0] * (RES[1] - 1) * RES[2] + RES[0] * RES[1] * (RES[2] - 1)
-        fit, eik, tv = part[0].item() / N, part[1].item() / N, part[2].item() / (P * K)
+        fit, eik, tv = part[0] / N, part[1] / N, part[2] / (P * K)
         losses.append(fit + cfg.lambda1 * eik + cfg.lambda2 * tv)
         # Adam on the owned coefficients only
         ps = params[z0 * plane:z1 * plane].copy()
@@ -101,24 +101,22 @@ def _rank_main(rank, world, port, outdir):
         assert bad == -1
         params[z0 * plane:z1 * plane] = ps
         # halo exchange of the boundary parameter planes
-        reqs = []
+        sends, recvs = [], []
+        buf_lo, buf_hi = np.zeros(plane), np.zeros(plane)
         if rank > 0:
-            reqs.append(dist.isend(torch.from_numpy(params[z0 * plane:(z0 + 1) * plane].copy()), rank - 1))
-            buf_lo = torch.zeros(plane, dtype=torch.float64)
-            reqs.append(dist.irecv(buf_lo, rank - 1))
+            sends.append((rank - 1, params[z0 * plane:(z0 + 1) * plane].copy()))
+            recvs.append((rank - 1, buf_lo))
         if rank < world - 1:
-            reqs.append(dist.isend(torch.from_numpy(params[(z1 - 1) * plane:z1 * plane].copy()), rank + 1))
-            buf_hi = torch.zeros(plane, dtype=torch.float64)
-            reqs.append(dist.irecv(buf_hi, rank + 1))
-        for r in reqs:
-            r.wait()
+            sends.append((rank + 1, params[(z1 - 1) * plane:z1 * plane].copy()))
+            recvs.append((rank + 1, buf_hi))
+        comm.exchange(sends, recvs)
         if rank > 0:
-            params[(z0 - 1) * plane:z0 * plane] = buf_lo.numpy()
+            params[(z0 - 1) * plane:z0 * plane] = buf_lo
         if rank < world - 1:
-            params[z1 * plane:(z1 + 1) * plane] = buf_hi.numpy()
+            params[z1 * plane:(z1 + 1) * plane] = buf_hi
     np.save(os.path.join(outdir, f"owned{rank}.npy"), params[z0 * plane:z1 * plane])
     np.save(os.path.join(outdir, f"loss{rank}.npy"), np.array(losses))
-    dist.destroy_process_group()
+    comm.close()
 
 
 def test_slab_partition_rules():
@@ -138,13 +136,62 @@ def test_slab_partition_rules():
     assert (keeps[0] & keeps[1]).sum() > 0  # boundary cell layer shared
 
 
-def test_two_slabs_over_gloo_match_single_process(tmp_path):
+def _spawn(fn, world, *args):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    ps = [ctx.Process(target=fn, args=(r, world) + args) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+
+
+def _comm_rank(rank, world, port, outdir):
     import sys
     sys.path.insert(0, ROOT)
-    import torch.multiprocessing as mp
+    from paper_2402_14415_b200.slab import Comm
+    c = Comm(rank, world, addr="127.0.0.1", port=port, backend="host")
+    out = {}
+    out["sum"] = c.allreduce([1.0 + rank, 0.1 * rank, 1e16 if rank == 0 else 1.0])
+    out["max"] = c.allreduce([rank, -rank], op="max")
+    out["min"] = c.allreduce([rank, -rank], op="min")
+    out["gather"] = np.frombuffer(b"".join(c.allgather(bytes([rank, 7 * rank]))), np.uint8)
+    c.barrier()
+    # ring: send a block to both neighbours (world 3 routes through rank 0)
+    sends = [((rank + 1) % world, np.full(5, rank, np.float64)), ((rank - 1) % world, np.full(3, -rank, np.int32))]
+    a, b = np.zeros(5), np.zeros(3, np.int32)
+    c.exchange(sends, [((rank - 1) % world, a), ((rank + 1) % world, b)])
+    out["ring"] = np.concatenate([a, b.astype(np.float64)])
+    np.savez(os.path.join(outdir, f"comm{rank}.npz"), **out)
+    c.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_comm_host_collectives(tmp_path, world):
+    """tgcu_comm (host backend) over world processes: rank-ordered sums (the
+    same bits on every rank), max / min, allgather, barrier, routed p2p."""
+    _spawn(_comm_rank, world, _free_port(), str(tmp_path))
+    res = [np.load(tmp_path / f"comm{r}.npz") for r in range(world)]
+    exp_sum = [sum(1.0 + r for r in range(world)), sum(0.1 * r for r in range(world)),
+               1e16 + (world - 1) * 1.0]
+    acc = 0.0
+    for r in range(world):
+        acc = acc + 0.1 * r  # rank order
+    for r in range(world):
+        assert np.array_equal(res[r]["sum"], res[0]["sum"])
+        assert res[r]["sum"][0] == exp_sum[0] and res[r]["sum"][1] == acc
+        assert list(res[r]["max"]) == [world - 1, 0] and list(res[r]["min"]) == [0, -(world - 1)]
+        assert list(res[r]["gather"]) == [x for k in range(world) for x in (k, 7 * k)]
+        lo, hi = (r - 1) % world, (r + 1) % world
+        assert np.array_equal(res[r]["ring"], np.concatenate([np.full(5, lo), np.full(3, -hi)]).astype(np.float64))
+
+
+def test_two_slabs_over_comm_match_single_process(tmp_path):
+    import sys
+    sys.path.insert(0, ROOT)
     from oracle.pyoracle import Loss, Oracle, Spec
-    port = _free_port()
-    mp.spawn(_rank_main, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    _spawn(_rank_main, 2, _free_port(), str(tmp_path))
     O = Oracle()
     s = Spec(dim=3, res=RES, order=2)
     rng = np.random.default_rng(0)

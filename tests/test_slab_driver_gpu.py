@@ -1,8 +1,9 @@
 """SlabTrainer (the multi-GPU driver bench.py uses at --gpus N) with two ranks.
 
 One GPU is available here, so both ranks run in separate processes on cuda:0
-over gloo (host-staged all-reduce / halo exchange); no kernel of one rank waits
-on the other's. The gathered owned slabs must reproduce a single-grid run,
+over libtgcu's communicator with the host backend (host-staged all-reduce /
+halo exchange over its TCP star; NCCL refuses two ranks on one device); no
+kernel of one rank waits on the other's. No PyTorch on the path. The gathered owned slabs must reproduce a single-grid run,
 with the halo exchanged after each step or written by the brick kernel into
 the neighbour's buffers (fused halo through CUDA IPC, which two processes on
 one device support as NVLink peers do).
@@ -39,29 +40,37 @@ def _rank(rank, world, port, outdir, fused):
     import sys
     sys.path.insert(0, ROOT)
     os.environ["TGCU_FUSED_HALO"] = "1" if fused else "0"
-    import torch
-    import torch.distributed as dist
     import paper_2402_14415_b200 as tg
-    from paper_2402_14415_b200.slab import SlabTrainer
-    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-    torch.cuda.set_device(0)
+    from paper_2402_14415_b200.slab import Comm, SlabTrainer
+    comm = Comm(rank, world, device=0, addr="127.0.0.1", port=port, backend="host")
     spec = tg.GridSpec(dim=3, resolution=RES, order=2)
     init = tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.02, seed=11)
-    tr = SlabTrainer(spec, rank, world, tg.AdamConfig(lr=1e-2), device=0, opts=init)
+    tr = SlabTrainer(spec, rank, world, tg.AdamConfig(lr=1e-2), device=0, opts=init, comm=comm)
     terms = []
-    for b in _batches():
-        terms.append(tr.step(torch.from_numpy(b).cuda(), tg.LossConfig(), want_terms=True).as_array())
+    for i, b in enumerate(_batches()):
+        if i % 2:  # host samples, local shard with the global batch size
+            terms.append(tr.step(tr.local_points(b), tg.LossConfig(), want_terms=True, n_global=len(b)).as_array())
+        else:
+            terms.append(tr.step(b, tg.LossConfig(), want_terms=True).as_array())
+    assert "torch" not in sys.modules
     np.save(os.path.join(outdir, f"own{rank}.npy"), tr.slab.owned_coeffs())
     np.save(os.path.join(outdir, f"fused{rank}.npy"), np.array([tr.fused_halo]))
     np.save(os.path.join(outdir, f"terms{rank}.npy"), np.array(terms))
-    dist.destroy_process_group()
+    tr.close()
 
 
 @pytest.mark.parametrize("fused", [False, True])
 def test_slab_trainer_two_ranks_match_single_grid(tmp_path, fused):
-    import torch.multiprocessing as mp
+    import multiprocessing as mp
     import paper_2402_14415_b200 as tg
-    mp.spawn(_rank, args=(2, _port(), str(tmp_path), fused), nprocs=2, join=True)
+    ctx = mp.get_context("spawn")
+    port = _port()
+    ps = [ctx.Process(target=_rank, args=(r, 2, port, str(tmp_path), fused)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(300)
+    assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
     for r in range(2):
         assert bool(np.load(tmp_path / f"fused{r}.npy")[0]) == fused
     spec = tg.GridSpec(dim=3, resolution=RES, order=2)
