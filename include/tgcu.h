@@ -22,6 +22,7 @@
 #ifndef TGCU_H
 #define TGCU_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -46,10 +47,13 @@ enum {
     TGCU_SORTED = 4,      /* eval: points are sorted by tgcu_sort_points (brick-binned query) */
     TGCU_EXPORT_GRAD = 8, /* train_step: also write the full gradient to the grid grad buffer
                              (validation mode; the fused path otherwise never stores it) */
-    TGCU_INPUT_READY = 16 /* train_step / slab_step_begin with device samples: the caller
+    TGCU_INPUT_READY = 16, /* train_step / slab_step_begin with device samples: the caller
                              guarantees the samples are complete (no pending writes on any
                              stream), so the step's point binning need not wait for earlier
                              work on `stream` and overlaps the previous step's brick kernel */
+    TGCU_HOST_RELEASE = 32 /* train_step with TGCU_HOST | TGCU_ASYNC: return once the host
+                              samples have been copied (the caller may refill the buffer at
+                              once); the step itself stays queued */
 };
 
 /* tg::GridSpec (grid_spec.hpp:19-24). */
@@ -162,7 +166,7 @@ int tgcu_backprop(tgcu_grid* g, const float* pts, const float* upstream, const f
 /* Device gradient buffer owned by the grid (coeff_total floats, zeroed at
  * creation). */
 float* tgcu_grid_grad(tgcu_grid* g);
-int tgcu_grad_zero(tgcu_grid* g, float* grad, void* stream);
+int tgcu_grad_zero(tgcu_grid* g, float* grad, void* stream); /* grad NULL: the grid's own buffer */
 /* Copy a device gradient buffer (NULL = the grid's own) to host fp64. */
 int tgcu_grad_download_f64(tgcu_grid* g, const float* grad, double* out, int64_t n);
 
@@ -316,6 +320,45 @@ int tgcu_slab_connect(tgcu_grid* g, tgcu_comm* c, int fused_halo, int* fused_out
 int tgcu_slab_train_step(tgcu_grid* g, const float* samples, int64_t n, int64_t n_global,
                          const tgcu_loss_config* cfg, tgcu_loss_terms* out, int flags, void* stream);
 
+/* ---- run_schedule on the device (schedule.hpp:13-86, schedule.cpp:13-108) ----
+ * tg::Schedule::Stage, tg::TraceRow. */
+typedef struct {
+    int res[3];  /* vertices per axis (unused axes 2, as Stage's default) */
+    int steps;
+} tgcu_stage;
+typedef struct {
+    int64_t step;  /* global step index */
+    int stage;
+    int res[3];
+    tgcu_loss_terms loss;
+    double wall_ms;
+} tgcu_trace_row;
+/* The problem (tg::TrainProblem, schedule.hpp:60-66): the batch of a global
+ * step — n x 4 floats (x, y, z, gt) in *samples, *flags = TGCU_HOST for host
+ * memory (it may be refilled once the callback is called again), otherwise
+ * device memory on the grid's device, written on `stream` (add
+ * TGCU_INPUT_READY when it is already complete, so its binning can overlap
+ * the previous step). Returns TGCU_OK or a status that aborts the run. */
+typedef int (*tgcu_batch_fn)(void* user, tgcu_grid* g, int64_t global_step, const float** samples, int64_t* n,
+                             int* flags);
+/* TrainProblem::on_stage_start: after any upsample, before the stage's first step. */
+typedef int (*tgcu_stage_fn)(void* user, tgcu_grid* g, int stage);
+/* Schedule::validate (schedule.cpp:13-25), same messages. */
+int tgcu_schedule_validate(const tgcu_stage* stages, int nstages, int dim);
+/* Schedule::progressive (schedule.cpp:27-54): up to 3 stages into out. */
+int tgcu_schedule_progressive(const int target[3], int dim, int total_steps, tgcu_stage out[3], int* nstages);
+/* run_schedule (schedule.cpp:62-108): *grid is the stage-0 grid; on return it
+ * is the final grid (upsampling replaces it: the previous handle is
+ * destroyed). Each step is one fused device step (tgcu_train_step, reuse-batch
+ * eikonal). flags TGCU_ASYNC: a stage's steps are issued without a host round
+ * trip per step (windows of up to 4096, one sync each; wall_ms = the window's
+ * mean). trace (total steps rows) and stage_seconds (nstages) may be NULL.
+ * A non-finite loss -> TGCU_ERR_NUMERICAL "run_schedule: non-finite loss at
+ * stage s step k", the grid at its last committed step. */
+int tgcu_run_schedule(tgcu_grid** grid, const tgcu_stage* stages, int nstages, const tgcu_adam_config* adam,
+                      const tgcu_loss_config* cfg, tgcu_batch_fn batch, tgcu_stage_fn on_stage, void* user, int flags,
+                      void* stream, tgcu_trace_row* trace, double* stage_seconds);
+
 /* Fused steps issued on this grid since creation or the last reported error;
  * error messages of a failed step name it as "step <this index at launch>". */
 int tgcu_grid_steps_launched(const tgcu_grid* g, int64_t* n);
@@ -363,6 +406,22 @@ int tgcu_grid_upsample(tgcu_grid* src, tgcu_grid* dst, int flags, void* stream);
  * For dim 2 this is the CLI's sample_grid_field2 (tools/main.cpp:33-45).
  * values: device (or host with TGCU_HOST) array of prod(lattice) floats. */
 int tgcu_sample_grid_field(tgcu_grid* g, const int lattice[3], float* values, int flags, void* stream);
+
+/* tg::IouOptions (metrics.hpp:12-18). */
+typedef struct {
+    int64_t samples;  /* default 100000 */
+    uint64_t seed;    /* default 7 */
+    double lo[3];     /* default (-1, -1, -1) */
+    double hi[3];     /* default (1, 1, 1) */
+    int dim;          /* default 3 */
+} tgcu_iou_options;
+/* iou (metrics.cpp:104-124): Monte-Carlo IoU of {a < 0} and {b < 0} on the
+ * reference's point stream (Rng(seed).uniform_in_box, drawn in order); a is
+ * evaluated on the device; b is grid b or, when b is NULL, the sphere
+ * |p| - sphere_radius (cmd_bench's probe target). *empty_union = 1 (iou 1)
+ * when neither set has a sample. */
+int tgcu_iou(tgcu_grid* a, tgcu_grid* b, double sphere_radius, const tgcu_iou_options* o, double* iou,
+             int* empty_union);
 
 /* SdfProblem::compute's batch draw (sdf_fit.cpp:21-23) on device: n samples
  * (x, y, z, gt) drawn with replacement from a device pool of pool_n samples,
@@ -417,6 +476,11 @@ int tgcu_save_tgrid(tgcu_grid* g, const char* path, int precision);
 int tgcu_load_tgrid(const char* path, int device, tgcu_grid** out);
 /* tgrid_file_size (grid_io.cpp:36-40); -1 for an invalid spec. */
 int64_t tgcu_tgrid_file_size(const tgcu_grid_spec* spec, int precision);
+
+/* Pinned (page-locked) host memory for batches fed through the pipelined
+ * host path (TGCU_HOST | TGCU_ASYNC); pageable memory is copied synchronously. */
+int tgcu_host_alloc(void** p, size_t bytes);
+int tgcu_host_free(void* p);
 
 /* Number of kernels this library launched since the counter was reset. */
 int64_t tgcu_launch_count(void);

@@ -3,10 +3,19 @@
 // so reference callers (run_schedule, cmd_bench, TrainProblem subclasses) can
 // drive the B200 path with the same names, argument meaning and exception
 // types (errors.hpp:9-34; std::invalid_argument for require_arg failures).
+//
+// When the reference's headers are on the include path (taylorgrid/errors.hpp
+// found by __has_include), the exceptions thrown ARE tg::ConfigError,
+// tg::IngestError, tg::NumericalError and tg::ResourceError, so code that
+// catches the reference's types catches ours; otherwise look-alike classes of
+// the same names live in namespace tgcu. include/tgcu_tg.hpp adds the
+// adapters to the reference's own types (tg::TaylorGrid, tg::Schedule,
+// tg::TrainProblem, tg::ScheduleResult).
 #pragma once
 
 #include <array>
 #include <cstdint>
+#include <exception>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -15,12 +24,26 @@
 
 #include "tgcu.h"
 
+#if defined(__has_include)
+#if __has_include("taylorgrid/errors.hpp")
+#include "taylorgrid/errors.hpp"
+#define TGCU_WITH_REFERENCE_TYPES 1
+#endif
+#endif
+
 namespace tgcu {
 
+#ifdef TGCU_WITH_REFERENCE_TYPES
+using ConfigError = tg::ConfigError;
+using IngestError = tg::IngestError;
+using NumericalError = tg::NumericalError;
+using ResourceError = tg::ResourceError;
+#else
 struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct IngestError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct NumericalError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct ResourceError : std::runtime_error { using std::runtime_error::runtime_error; };
+#endif
 struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
 
 // Status -> the reference's exception classes.
@@ -62,7 +85,9 @@ public:
     explicit Grid(const tgcu_grid_spec& spec, const tgcu_init_options* opts = nullptr, int device = 0) {
         check(tgcu_grid_create(&spec, opts, device, &h_));
     }
-    ~Grid() { tgcu_grid_destroy(h_); }
+    ~Grid() {
+        if (h_) tgcu_grid_destroy(h_);
+    }
     Grid(const Grid&) = delete;
     Grid& operator=(const Grid&) = delete;
     Grid(Grid&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
@@ -149,6 +174,15 @@ public:
         g.h_ = h;
         return g;
     }
+    // Give up ownership of the handle (the caller destroys it).
+    tgcu_grid* release() { return std::exchange(h_, nullptr); }
+    Grid& operator=(Grid&& o) noexcept {
+        if (this != &o) {
+            if (h_) tgcu_grid_destroy(h_);
+            h_ = std::exchange(o.h_, nullptr);
+        }
+        return *this;
+    }
 
 private:
     Grid() = default;
@@ -170,5 +204,149 @@ inline Grid load_tgrid(const char* path, int device = 0) {
     check(tgcu_load_tgrid(path, device, &h));
     return Grid::adopt(h);
 }
+
+// tg::IouOptions / iou (metrics.cpp:104-124) with field a on the device: b is
+// another grid, or (nullptr) the sphere |p| - radius of cmd_bench's probe.
+struct IouOptions {
+    int64_t samples = 100000;
+    uint64_t seed = 7;
+    std::array<double, 3> domain_lo{-1.0, -1.0, -1.0};
+    std::array<double, 3> domain_hi{1.0, 1.0, 1.0};
+    int dim = 3;
+};
+struct IouResult {
+    double iou = 0.0;
+    bool empty_union = false;
+};
+inline IouResult iou(const Grid& a, const Grid* b, double sphere_radius, const IouOptions& o = {}) {
+    tgcu_iou_options c{o.samples, o.seed, {o.domain_lo[0], o.domain_lo[1], o.domain_lo[2]},
+                       {o.domain_hi[0], o.domain_hi[1], o.domain_hi[2]}, o.dim};
+    IouResult r;
+    int empty = 0;
+    check(tgcu_iou(a.handle(), b ? b->handle() : nullptr, sphere_radius, &c, &r.iou, &empty));
+    r.empty_union = empty != 0;
+    return r;
+}
+
+// Schedule::Stage / Schedule / TraceRow (schedule.hpp:16-56).
+struct Stage {
+    std::array<int, 3> resolution{2, 2, 2};
+    int steps = 0;
+};
+struct Schedule {
+    std::vector<Stage> stages;
+    int total_steps() const {
+        int n = 0;
+        for (const Stage& s : stages) n += s.steps;
+        return n;
+    }
+    void validate(int dim) const {
+        const std::vector<tgcu_stage> c = cstages();
+        check(tgcu_schedule_validate(c.data(), static_cast<int>(c.size()), dim));
+    }
+    static Schedule progressive(const std::array<int, 3>& target, int dim, int total_steps) {
+        tgcu_stage out[3];
+        int n = 0;
+        check(tgcu_schedule_progressive(target.data(), dim, total_steps, out, &n));
+        Schedule s;
+        for (int i = 0; i < n; ++i) s.stages.push_back({{out[i].res[0], out[i].res[1], out[i].res[2]}, out[i].steps});
+        return s;
+    }
+    static Schedule single(const std::array<int, 3>& target, int steps) { return Schedule{{Stage{target, steps}}}; }
+    std::vector<tgcu_stage> cstages() const {
+        std::vector<tgcu_stage> c;
+        for (const Stage& s : stages) c.push_back({{s.resolution[0], s.resolution[1], s.resolution[2]}, s.steps});
+        return c;
+    }
+};
+using TraceRow = tgcu_trace_row;
+
+// The device form of tg::TrainProblem (schedule.hpp:60-66): the step's batch
+// (the fused step does the loss, gradient and Adam). batch() returns n x 4
+// floats; host memory may be refilled on the next call.
+class TrainProblem {
+public:
+    virtual ~TrainProblem() = default;
+    struct Batch {
+        const float* samples = nullptr;
+        int64_t n = 0;
+        bool host = true;
+        bool ready = false;  // device batch already complete (its binning may overlap the previous step)
+    };
+    virtual Batch batch(int64_t global_step) = 0;
+    virtual void on_stage_start(Grid& grid, int stage) { (void)grid; (void)stage; }
+};
+
+struct ScheduleResult {
+    Grid grid;
+    std::vector<TraceRow> trace;
+    std::vector<double> stage_seconds;
+};
+
+// run_schedule (schedule.cpp:62-108) on the device: per stage upsample +
+// fresh Adam moments + on_stage_start, then fused steps. asynchronous: no
+// host round trip per step (trace wall_ms = the window's mean).
+inline ScheduleResult run_schedule(TrainProblem& problem, const Schedule& schedule, Grid grid,
+                                   const AdamConfig& adam, const LossConfig& loss, bool asynchronous = true) {
+    struct Ctx {
+        TrainProblem* p;
+        std::exception_ptr err;
+    } ctx{&problem, nullptr};
+    auto batch_fn = [](void* u, tgcu_grid*, int64_t step, const float** smp, int64_t* n, int* flags) -> int {
+        Ctx* c = static_cast<Ctx*>(u);
+        try {
+            const TrainProblem::Batch b = c->p->batch(step);
+            *smp = b.samples;
+            *n = b.n;
+            *flags = (b.host ? TGCU_HOST : 0) | (b.ready ? TGCU_INPUT_READY : 0);
+            return TGCU_OK;
+        } catch (...) {
+            c->err = std::current_exception();
+            return TGCU_ERR_INVALID_ARGUMENT;
+        }
+    };
+    auto stage_fn = [](void* u, tgcu_grid* g, int stage) -> int {
+        Ctx* c = static_cast<Ctx*>(u);
+        try {
+            Grid view = Grid::adopt(g);  // non-owning for the callback's duration
+            c->p->on_stage_start(view, stage);
+            view.release();
+            return TGCU_OK;
+        } catch (...) {
+            c->err = std::current_exception();
+            return TGCU_ERR_INVALID_ARGUMENT;
+        }
+    };
+    const std::vector<tgcu_stage> st = schedule.cstages();
+    ScheduleResult r{std::move(grid), std::vector<TraceRow>(static_cast<size_t>(schedule.total_steps())),
+                     std::vector<double>(st.size())};
+    tgcu_grid* h = r.grid.release();
+    const tgcu_adam_config a{adam.lr, adam.beta1, adam.beta2, adam.eps};
+    const tgcu_loss_config l = loss.c();
+    const int rc = tgcu_run_schedule(&h, st.data(), static_cast<int>(st.size()), &a, &l, batch_fn, stage_fn, &ctx,
+                                     asynchronous ? TGCU_ASYNC : 0, nullptr, r.trace.data(), r.stage_seconds.data());
+    r.grid = Grid::adopt(h);
+    if (ctx.err) std::rethrow_exception(ctx.err);
+    check(rc);
+    return r;
+}
+
+// Pinned host memory for batches fed through the pipelined host path (the
+// library copies pageable memory synchronously).
+template <class T>
+class PinnedBuffer {
+public:
+    explicit PinnedBuffer(size_t n) : n_(n) { check(tgcu_host_alloc(reinterpret_cast<void**>(&p_), n * sizeof(T))); }
+    ~PinnedBuffer() { tgcu_host_free(p_); }
+    PinnedBuffer(const PinnedBuffer&) = delete;
+    PinnedBuffer& operator=(const PinnedBuffer&) = delete;
+    T* data() { return p_; }
+    size_t size() const { return n_; }
+    std::span<T> span() { return {p_, n_}; }
+
+private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
 
 }  // namespace tgcu

@@ -91,7 +91,7 @@ class Oracle:
         L = C.CDLL(path)
         L.tgo_eval.restype = C.c_double
         L.tgo_eval.argtypes = [C.POINTER(_TgoSpec), _D, _D, _D]
-        L.tgo_eval_batch_f32.argtypes = [C.POINTER(_TgoSpec), C.c_void_p, _D, C.c_int64, _D, _D]
+        L.tgo_eval_batch_f32.argtypes = [C.POINTER(_TgoSpec), C.c_void_p, _D, C.c_int64, _D, _D, _D]
         L.tgo_locate.argtypes = [C.POINTER(_TgoSpec), _D, _I, _D, _L]
         L.tgo_backprop.argtypes = [C.POINTER(_TgoSpec), _D, C.c_double, _D, _D]
         L.tgo_adaptive_weight.restype = C.c_double
@@ -145,15 +145,18 @@ class Oracle:
         return (vals, grads) if want_grad else vals
 
     def eval_f32(self, s: Spec, coeffs32, pts, want_grad=False):
-        """eval on fp32-stored coefficients (upcast exactly), batched in C."""
+        """eval on fp32-stored coefficients (upcast exactly), batched in C.
+        want_grad: also (n x 3) spatial gradients and the per-axis L1 size of
+        their terms -> (vals, grads, l1)."""
         sp = self._spec(s)
         c = np.ascontiguousarray(coeffs32, dtype=np.float32)
         pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
         vals = np.empty(len(pts))
         grads = np.zeros((len(pts), 3)) if want_grad else None
+        l1 = np.zeros((len(pts), 3)) if want_grad else None
         self.L.tgo_eval_batch_f32(C.byref(sp), c.ctypes.data_as(C.c_void_p), _dp(pts), len(pts), _dp(vals),
-                                  _dp(grads))
-        return (vals, grads) if want_grad else vals
+                                  _dp(grads), _dp(l1))
+        return (vals, grads, l1) if want_grad else vals
 
     def backprop(self, s: Spec, pts, upstream, upstream_vec, grad):
         sp = self._spec(s)

@@ -176,7 +176,7 @@ double tgo_eval(const tgo_spec* s, const double* coeffs, const double p[3], doub
  * test evaluate the oracle on a multi-GB fp32 device grid downloaded as is
  * (BASELINE C4, 512^3) without a second fp64 copy. */
 void tgo_eval_batch_f32(const tgo_spec* s, const float* coeffs, const double* pts, int64_t n, double* vals,
-                        double* grads) {
+                        double* grads, double* l1) {
     const int K = tgo_coeff_count(s->order, s->dim);
     for (int64_t q = 0; q < n; ++q) {
         const double* p = pts + 3 * q;
@@ -190,19 +190,24 @@ void tgo_eval_batch_f32(const tgo_spec* s, const float* coeffs, const double* pt
         corners_t c;
         make_corners(s, local, vid, &c);
         double value = 0.0;
-        double g[3] = {0.0, 0.0, 0.0};
+        double g[3] = {0.0, 0.0, 0.0}, m[3] = {0.0, 0.0, 0.0};
         for (int i = 0; i < c.count; ++i) {
             double b[10];
             for (int k = 0; k < K; ++k) b[k] = (double)coeffs[c.vid[i] * K + k];
             double tg[3];
-            const double tv = taylor_poly(b, s->order, s->dim, c.delta[i], grads ? tg : NULL);
+            const double tv = taylor_poly(b, s->order, s->dim, c.delta[i], (grads || l1) ? tg : NULL);
             value += c.w[i] * tv;
-            if (grads)
-                for (int a = 0; a < s->dim; ++a) g[a] += c.dw[i][a] * tv + c.w[i] * tg[a];
+            if (grads || l1)
+                for (int a = 0; a < s->dim; ++a) {
+                    g[a] += c.dw[i][a] * tv + c.w[i] * tg[a];
+                    m[a] += fabs(c.dw[i][a] * tv) + fabs(c.w[i] * tg[a]);
+                }
         }
         vals[q] = value;
         if (grads)
             for (int a = 0; a < 3; ++a) grads[3 * q + a] = g[a];
+        if (l1) /* per axis: the L1 size of the terms summed into the spatial gradient */
+            for (int a = 0; a < 3; ++a) l1[3 * q + a] = m[a];
     }
 }
 

@@ -673,6 +673,10 @@ int tgcu_backprop(tgcu_grid* h, const float* pts, const float* upstream, const f
 int tgcu_grad_zero(tgcu_grid* h, float* grad, void* stream) {
     return guard([&] {
         set_device(h->g);
+        if (!grad) {  // NULL: the grid's own buffer
+            ensure_grad(h->g);
+            grad = h->g.grad;
+        }
         TGCU_CUDA(cudaMemsetAsync(grad, 0, sizeof(float) * h->g.NC, as_stream(stream)));
     });
 }
@@ -910,6 +914,9 @@ int tgcu_train_step(tgcu_grid* h, const float* samples, int64_t n, const tgcu_lo
             TGCU_CUDA(cudaEventRecord(g.ev_half[slot], g.cstream2));
             TGCU_CUDA(cudaStreamWaitEvent(g.cstream, g.ev_half[slot], 0));
             TGCU_CUDA(cudaEventRecord(g.ev_ready[slot], g.cstream));
+            // TGCU_HOST_RELEASE: hand the host buffer back once it is copied
+            // (the step itself stays queued)
+            if (flags & TGCU_HOST_RELEASE) TGCU_CUDA(cudaEventSynchronize(g.ev_ready[slot]));
             bin_in.wait = g.ev_ready[slot];
             bin_in.consumed = g.ev_free[slot];
             ds = reinterpret_cast<const float4*>(g.pstage[slot]);
@@ -1301,3 +1308,17 @@ int tgcu_trace(tgcu_grid* h, tgcu_loss_terms* out, int count) {
 }
 
 }  // extern "C"
+
+int tgcu_host_alloc(void** p, size_t bytes) {
+    return guard([&] {
+        require(p != nullptr, "host_alloc: NULL argument");
+        *p = nullptr;
+        TGCU_CUDA(cudaMallocHost(p, bytes == 0 ? 1 : bytes));
+    });
+}
+
+int tgcu_host_free(void* p) {
+    return guard([&] {
+        if (p) TGCU_CUDA(cudaFreeHost(p));
+    });
+}

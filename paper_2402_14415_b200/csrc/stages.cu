@@ -421,3 +421,59 @@ int tgcu_load_tgrid(const char* path, int device, tgcu_grid** out) {
 }
 
 }  // extern "C"
+
+// ---- Monte-Carlo IoU probe (metrics.cpp:104-124) -----------------------------------
+// The reference's probe: points from Rng(seed).uniform_in_box(lo, hi, dim),
+// drawn in order on the host (mt19937_64, rng.hpp:53-57), inside = field < 0
+// for both fields; field a = this grid on the device, field b = grid b or
+// the analytic sphere |p| - radius (cmd_bench's target, tools/main.cpp:604).
+// Chunks of points are evaluated on the device (direct-gather query);
+// counting on the host in point order.
+int tgcu_iou(tgcu_grid* a, tgcu_grid* b, double sphere_radius, const tgcu_iou_options* o, double* iou,
+             int* empty_union) {
+    return guard([&] {
+        require(a != nullptr && o != nullptr && iou != nullptr, "iou: NULL argument");
+        require(o->samples > 0, "iou: sample count must be > 0");
+        require(o->dim == 2 || o->dim == 3, "iou: dim must be 2 or 3");
+        Grid& ga = a->g;
+        require(!ga.slab && (!b || !b->g.slab), "iou: slab grids are not supported");
+        TGCU_CUDA(cudaSetDevice(ga.device));
+        tgcu_rng* rng = nullptr;
+        if (tgcu_rng_create(o->seed, &rng) != TGCU_OK) throw Error(TGCU_ERR_CUDA, tgcu_last_error());
+        const int64_t chunk = std::min<int64_t>(o->samples, 1 << 20);
+        std::vector<double> p64((size_t)(3 * chunk));
+        std::vector<float> p32((size_t)(3 * chunk)), va((size_t)chunk), vb(b ? (size_t)chunk : 0);
+        int64_t inter = 0, uni = 0;
+        try {
+            for (int64_t done = 0; done < o->samples; done += chunk) {
+                const int64_t m = std::min(chunk, o->samples - done);
+                if (tgcu_rng_uniform_box(rng, o->dim, o->lo, o->hi, m, p64.data()) != TGCU_OK)
+                    throw Error(TGCU_ERR_CUDA, tgcu_last_error());
+                for (int64_t i = 0; i < 3 * m; ++i) p32[i] = (float)p64[i];
+                int rc = tgcu_eval(a, p32.data(), m, va.data(), nullptr, TGCU_HOST, nullptr);
+                if (rc == TGCU_OK && b) rc = tgcu_eval(b, p32.data(), m, vb.data(), nullptr, TGCU_HOST, nullptr);
+                if (rc != TGCU_OK) throw Error(rc, tgcu_last_error());
+                for (int64_t i = 0; i < m; ++i) {
+                    const bool in_a = va[i] < 0.0f;
+                    bool in_b;
+                    if (b) {
+                        in_b = vb[i] < 0.0f;
+                    } else {
+                        const double* p = &p64[3 * i];
+                        double r2 = 0.0;
+                        for (int d = 0; d < 3; ++d) r2 += p[d] * p[d];
+                        in_b = std::sqrt(r2) - sphere_radius < 0.0;
+                    }
+                    inter += in_a && in_b;
+                    uni += in_a || in_b;
+                }
+            }
+        } catch (...) {
+            tgcu_rng_destroy(rng);
+            throw;
+        }
+        tgcu_rng_destroy(rng);
+        if (empty_union) *empty_union = uni == 0;
+        *iou = uni == 0 ? 1.0 : (double)inter / (double)uni;
+    });
+}

@@ -879,8 +879,9 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             bool home = true;
 #pragma unroll
             for (int a = 0; a < DIM; ++a) home &= tc[a] >= 1;
-#ifndef TGCU_FP32_FORWARD
-            // fp64 forward (blend_corner_d): the loss chain amplifies forward errors
+#ifdef TGCU_FP64_FORWARD
+            // fp64 forward (blend_corner_d; A/B build): the loss
+            // chain amplifies forward errors
             double f = 0.0, fg[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) fg[a] = 0.0;
@@ -895,7 +896,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
 #pragma unroll
             for (int a = 0; a < DIM; ++a) ax[a] = axis_factors(A.s, a, lc[a]);
 #else
-            // fp32 forward (A/B builds only)
+            // fp32 forward from the fp64 cell offsets (per-axis factors rounded once)
             AxisF ax[DIM];
 #pragma unroll
             for (int a = 0; a < DIM; ++a) ax[a] = axis_factors(A.s, a, lc[a]);

@@ -42,7 +42,8 @@ def assert_close(got, ref, rel, floor=1.0, what=""):
 
 def grad_close(got, ref, mass, rel=1e-5, mass_rel=4e-6, what="grad"):
     """|d| <= rel*|ref| + mass_rel*mass. mass = the oracle's L1 sum of the
-    contributions. Each contribution carries the fp32 record rounding (~2e-7)
+    contributions (with the differentiate_weight term counted apart from the
+    weight term: they are separate fp32-rounded summands that may cancel). Each contribution carries the fp32 record rounding (~2e-7)
     and, through the adaptive weight w' ~ 2 exp(-k|f|) far from the surface
     (sdf_loss.cpp:15-27), the fp32 forward error amplified by k: k * 6e-8 =
     3e-6 relative at k = 50 -> mass_rel = 4e-6."""
@@ -657,7 +658,7 @@ def test_empty_and_degenerate_inputs():
     assert np.isfinite(t.total) and g.adam_t == 1
 
 
-@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("TGCU_RANDOM_CASES", "12"))))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("TGCU_RANDOM_CASES", "40"))))
 def test_fused_step_random_configs(oracle, seed):
     """Seeded random sweep: dimension, order, resolution (2..41 per axis, so
     single-cell axes and partial bricks), batch size (1..20000, below and
