@@ -447,12 +447,15 @@ int tgcu_shuffle_order(uint64_t seed, int64_t n, uint32_t* order);
 
 /* ---- radiance density chain (volume_render.cpp:61-276, sh.cpp:43-107) ---- */
 enum { TGCU_DENSITY_SHIFTED_SOFTPLUS = 0, TGCU_DENSITY_CLAMP_RELU = 1 };
-/* tg::RenderOptions (volume_render.hpp:17-24) without stratified jitter. */
+/* tg::RenderOptions (volume_render.hpp:17-24). */
 typedef struct {
     int n_samples;          /* 1..1024 samples per ray, t_i = near + i (far - near) / n */
     int activation;         /* TGCU_DENSITY_* (apply_activation, volume_render.cpp:19-28) */
     double softplus_shift;  /* default -10 */
     double background[3];   /* default (1, 1, 1) */
+    int jitter;             /* stratified jitter: t_i = near + (i + u_i) (far - near) / n with u_i the
+                               ray's own Rng stream (volume_render.cpp:69-70), ray id = batch index */
+    uint64_t jitter_seed;
 } tgcu_render_options;
 /* photometric_loss (volume_render.cpp:210-276) / render_ray (:194-208),
  * batched: the density is `density` (3D TaylorGrid, current parameters); the

@@ -347,6 +347,7 @@ class Reference:
                                      C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                      C.c_double, C.c_int, _D, _D]
         L.tgr_eval_timed.argtypes = sp + [_D, _D, C.c_int64, _D, C.c_int, _D]
+        L.tgr_init_grid.argtypes = sp + [C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_uint64, _D]
         L.tgr_query_bench.argtypes = sp + [C.c_double, C.c_uint64, _D, C.c_int64, _D, C.c_int, _D]
         L.tgr_sample_sphere.argtypes = [C.c_double, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_double,
                                         C.c_uint64, _D]
@@ -364,7 +365,8 @@ class Reference:
         L.tgr_shuffle_order.argtypes = [C.c_uint64, C.c_int64, C.c_void_p]
         L.tgr_trace_csv.argtypes = [C.c_int, _I, _I, _D, _D, C.c_char_p, C.c_char_p, C.c_int64]
         L.tgr_photometric_loss.argtypes = sp + [_D, _I, _D, _D, C.c_int, _D, C.c_int64, _D, _D, _D, _D, _D,
-                                                C.c_int, C.c_int, C.c_double, _D, _D, _D, _D, _D, _D]
+                                                C.c_int, C.c_int, C.c_double, _D, _D, _D, _D, _D, _D, C.c_int,
+                                                C.c_uint64]
         L.tgr_fit_sdf.argtypes = sp + [_D, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
                                        C.c_int, C.c_double, C.c_double, C.c_uint64, _D, _D, _D, C.c_int]
         self.L = L
@@ -406,6 +408,17 @@ class Reference:
         self._err(self.L.tgr_eval_timed(*_spec_args(s), _dp(coeffs), _dp(pts), len(pts), _dp(vals),
                                         threads, C.byref(secs)))
         return vals, secs.value
+
+    def init_grid(self, s: Spec, mode=0, constant=0.0, epsilon=1e-4, seed=0, cap=4 << 30):
+        """tg::init_grid coefficients (mode 0 Zeros, 1 Constant, 2 SmallUniform).
+        Raises MemoryError (tg::ResourceError) / ValueError with the reference's message."""
+        out = np.zeros(s.V * s.K)
+        rc = self.L.tgr_init_grid(*_spec_args(s), int(mode), float(constant), float(epsilon), int(seed), int(cap),
+                                  _dp(out))
+        if rc == 5:
+            raise MemoryError(self.L.tgr_last_error().decode())
+        self._err(rc)
+        return out
 
     def query_bench(self, s: Spec, pts, threads, epsilon=0.1, seed=7):
         """init_grid(SmallUniform) inside the reference, then parallel_for + eval
@@ -571,8 +584,8 @@ class Reference:
         return buf.value.decode()
 
     def photometric_loss(self, ds: Spec, dc, ss: Spec, deg, sc, rays, n_samples=64, activation=0, shift=-10.0,
-                         bg=(1.0, 1.0, 1.0), want_grad=False, render=False):
-        """tg::photometric_loss / render_ray (threads 1, no jitter)."""
+                         bg=(1.0, 1.0, 1.0), want_grad=False, render=False, jitter=False, jitter_seed=0):
+        """tg::photometric_loss / render_ray (threads 1; RenderOptions::jitter / jitter_seed)."""
         n = len(rays["near"])
         f = lambda a: np.ascontiguousarray(np.asarray(a, dtype=np.float64))  # noqa: E731
         o, d, nr, fr = f(rays["origins"]), f(rays["dirs"]), f(rays["near"]), f(rays["far"])
@@ -589,7 +602,7 @@ class Reference:
         self._err(self.L.tgr_photometric_loss(*_spec_args(ds), _dp(f(dc)), sres, _dp(sorg), _dp(sext), deg,
                                               _dp(f(sc)), n, _dp(o), _dp(d), _dp(nr), _dp(fr), _dp(gt), n_samples,
                                               activation, shift, _dp(f(bg)), _dp(gd), _dp(gs), _dp(col), _dp(res),
-                                              C.byref(loss)))
+                                              C.byref(loss), int(bool(jitter)), int(jitter_seed)))
         return dict(loss=loss.value if gt is not None else 0.0, grad_density=gd, grad_sh=gs, colors=col,
                     residual=res)
 

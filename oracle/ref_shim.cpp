@@ -323,6 +323,28 @@ int tgr_eval_timed(int dim, const int* res, const double* origin, const double* 
     }
 }
 
+// init_grid (taylor_grid.cpp:162-188) with InitOptions {mode 0 Zeros /
+// 1 Constant / 2 SmallUniform, constant, epsilon, seed, cap}: the
+// coefficients (coeff_total doubles) for init parity tests.
+int tgr_init_grid(int dim, const int* res, const double* origin, const double* extent, int order, int mode,
+                  double constant, double epsilon, uint64_t seed, uint64_t cap, double* out) {
+    try {
+        tg::InitOptions opts;
+        opts.mode = mode == 0 ? tg::InitMode::Zeros : (mode == 1 ? tg::InitMode::Constant : tg::InitMode::SmallUniform);
+        opts.constant = constant;
+        opts.epsilon = epsilon;
+        opts.seed = seed;
+        opts.memory_cap_bytes = cap;
+        const tg::TaylorGrid g = tg::init_grid(make_spec(dim, res, origin, extent, order), opts);
+        if (out) std::memcpy(out, g.coeffs.data(), g.coeffs.size() * sizeof(double));
+        return 0;
+    } catch (const tg::ResourceError& e) {
+        return fail(e, 5);
+    } catch (const std::exception& e) {
+        return fail(e, 1);
+    }
+}
+
 // Query throughput of the reference on a grid it initialises itself
 // (init_grid, InitMode::SmallUniform with the given epsilon and seed,
 // taylor_grid.cpp:162-188; memory cap lifted): parallel_for + eval over the
@@ -524,7 +546,8 @@ int tgr_photometric_loss(int dim, const int* res, const double* origin, const do
                          int sh_degree, const double* sh_coeffs, int64_t nrays, const double* origins,
                          const double* dirs, const double* near_, const double* far_, const double* gt,
                          int n_samples, int activation, double shift, const double* bg, double* grad_density,
-                         double* grad_sh, double* colors_out, double* residual_out, double* loss_out) {
+                         double* grad_sh, double* colors_out, double* residual_out, double* loss_out, int jitter,
+                         uint64_t jitter_seed) {
     try {
         const tg::TaylorGrid dg = make_grid(make_spec(dim, res, origin, extent, order), dcoeffs);
         tg::SHColorGrid sg = tg::init_sh_grid(make_spec(3, sh_res, sh_origin, sh_extent, 0), sh_degree);
@@ -534,6 +557,8 @@ int tgr_photometric_loss(int dim, const int* res, const double* origin, const do
         opt.activation = activation == 0 ? tg::DensityActivation::ShiftedSoftplus : tg::DensityActivation::ClampRelu;
         opt.softplus_shift = shift;
         opt.background = {bg[0], bg[1], bg[2]};
+        opt.jitter = jitter != 0;
+        opt.jitter_seed = jitter_seed;
         tg::RayBatch batch;
         for (int64_t r = 0; r < nrays; ++r) {
             batch.origins.push_back({origins[3 * r], origins[3 * r + 1], origins[3 * r + 2]});

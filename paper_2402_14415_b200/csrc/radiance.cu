@@ -40,8 +40,39 @@ struct RayArgs {
     float* colors;           // n x 3 or null
     float* resid;            // n or null
     double* ray_err;         // n squared errors (gt given)
+    const double* jit;       // n x S stratified jitter draws u_i (null: no jitter)
     Status* st;
 };
+
+// Stratified jitter (volume_render.cpp:69-70): ray r draws its n_samples
+// uniforms from Rng(jitter_seed ^ (r * 0x9e3779b97f4a7c15 + 0x2545f4914f6cdd1d)),
+// i.e. std::mt19937_64 seeded per ray, uniform = (x >> 11) * 2^-53
+// (rng.hpp:21). One thread per ray, the 312-word state in local memory.
+__global__ void __launch_bounds__(128) k_jitter(long long n, int S, unsigned long long seed, double* __restrict__ out) {
+    constexpr int NN = 312, MM = 156;
+    constexpr unsigned long long MATRIX = 0xB5026F5AA96619E9ull, UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull;
+    const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    unsigned long long mt[NN];
+    mt[0] = seed ^ ((unsigned long long)r * 0x9e3779b97f4a7c15ull + 0x2545f4914f6cdd1dull);
+    for (int i = 1; i < NN; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (unsigned long long)i;
+    int idx = NN;
+    for (int k = 0; k < S; ++k) {
+        if (idx >= NN) {
+            for (int i = 0; i < NN; ++i) {
+                const unsigned long long x = (mt[i] & UM) | (mt[(i + 1) % NN] & LM);
+                mt[i] = mt[(i + MM) % NN] ^ (x >> 1) ^ ((x & 1ull) ? MATRIX : 0ull);
+            }
+            idx = 0;
+        }
+        unsigned long long y = mt[idx++];
+        y ^= (y >> 29) & 0x5555555555555555ull;
+        y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+        y ^= (y << 37) & 0xFFF7EEE000000000ull;
+        y ^= y >> 43;
+        out[r * S + k] = (double)(y >> 11) * 0x1.0p-53;
+    }
+}
 
 __device__ __forceinline__ double sigmoid_dd(double x) { return 1.0 / (1.0 + exp(-x)); }
 
@@ -71,14 +102,19 @@ struct SampleState {
 };
 
 template <int ORDER, int DEG>
-__device__ __forceinline__ void sample_state(const RayArgs& A, const double* o, const double* d, double near_,
-                                             double far_, double bin, int i, const double* basis, SampleState& st) {
+__device__ __forceinline__ void sample_state(const RayArgs& A, long long ray, const double* o, const double* d,
+                                             double near_, double far_, double bin, int i, const double* basis,
+                                             SampleState& st) {
     constexpr int K = KOf<3, ORDER>::value;
     constexpr int B = (DEG + 1) * (DEG + 1);
     constexpr int C = 3 * B;
-    // t_i = near + i * bin; delta_i = t_{i+1} - t_i, the last one far - t_i (volume_render.cpp:67-72)
-    const double t = __dadd_rn(near_, __dmul_rn((double)i, bin));
-    st.delta = (i + 1 < A.S) ? __dsub_rn(__dadd_rn(near_, __dmul_rn((double)(i + 1), bin)), t) : __dsub_rn(far_, t);
+    // t_i = near + (i [+ u_i]) * bin; delta_i = t_{i+1} - t_i, the last one
+    // far - t_i (volume_render.cpp:67-72)
+    const double* u = A.jit ? A.jit + ray * A.S : nullptr;
+    const double t = __dadd_rn(near_, __dmul_rn(u ? __dadd_rn((double)i, u[i]) : (double)i, bin));
+    st.delta = (i + 1 < A.S)
+                   ? __dsub_rn(__dadd_rn(near_, __dmul_rn(u ? __dadd_rn((double)(i + 1), u[i + 1]) : (double)(i + 1), bin)), t)
+                   : __dsub_rn(far_, t);
 #pragma unroll
     for (int a = 0; a < 3; ++a) st.x[a] = __dadd_rn(o[a], __dmul_rn(t, d[a]));
     // density: eval (fp64 locate, fp32 blend) -> activation
@@ -185,7 +221,7 @@ __global__ void __launch_bounds__(256) k_rays(RayArgs A) {
         SampleState s;
         double step = 1.0, wc[3] = {0.0, 0.0, 0.0};
         if (i < A.S) {
-            sample_state<ORDER, DEG>(A, o, d, near_, far_, bin, i, basis, s);
+            sample_state<ORDER, DEG>(A, r, o, d, near_, far_, bin, i, basis, s);
             step = s.step;
         }
         double tot;
@@ -227,7 +263,7 @@ __global__ void __launch_bounds__(256) k_rays(RayArgs A) {
         SampleState s;
         double step = 1.0, w = 0.0;
         if (i < A.S) {
-            sample_state<ORDER, DEG>(A, o, d, near_, far_, bin, i, basis, s);
+            sample_state<ORDER, DEG>(A, r, o, d, near_, far_, bin, i, basis, s);
             step = s.step;
         }
         double tot;
@@ -339,6 +375,13 @@ void launch_rays(Grid& g, const DevSpec& ss, int deg, const float* scoeffs, cons
     A.resid = resid;
     A.ray_err = ray_err;
     A.st = g.st;
+    double* jit = nullptr;
+    if (o.jitter) {
+        TGCU_CUDA(cudaMallocAsync(&jit, sizeof(double) * n * o.n_samples, s));
+        k_jitter<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, o.n_samples, o.jitter_seed, jit);
+        count_launch();
+        A.jit = jit;
+    }
     const bool grad = gt && (gd || gsh);
     const unsigned blocks = (unsigned)((n + 7) / 8);
     auto go = [&](auto kern) { kern<<<blocks, 256, 0, s>>>(A); };
@@ -357,6 +400,7 @@ void launch_rays(Grid& g, const DevSpec& ss, int deg, const float* scoeffs, cons
         k_sum_scaled<<<1, 1024, 0, s>>>(ray_err, n, 1.0 / (double)n, loss);
         count_launch();
     }
+    if (jit) TGCU_CUDA(cudaFreeAsync(jit, s));
     TGCU_CUDA(cudaGetLastError());
 }
 

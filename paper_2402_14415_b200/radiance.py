@@ -31,16 +31,18 @@ class DensityActivation(IntEnum):
 
 @dataclass
 class RenderOptions:
-    """tg::RenderOptions (volume_render.hpp:17-24), no jitter."""
+    """tg::RenderOptions (volume_render.hpp:17-24)."""
     n_samples: int = 64
     activation: DensityActivation = DensityActivation.ShiftedSoftplus
     softplus_shift: float = -10.0
     background: Sequence[float] = (1.0, 1.0, 1.0)
+    jitter: bool = False  # stratified jitter inside the N bins (per-ray Rng, ray id = batch index)
+    jitter_seed: int = 0
 
 
 class _RO(C.Structure):
     _fields_ = [("n_samples", C.c_int), ("activation", C.c_int), ("softplus_shift", C.c_double),
-                ("background", C.c_double * 3)]
+                ("background", C.c_double * 3), ("jitter", C.c_int), ("jitter_seed", C.c_uint64)]
 
 
 @dataclass
@@ -103,7 +105,7 @@ def _call(density: TaylorGrid, sh: SHColorGrid, rays, gt, opts: RenderOptions, w
     gd = np.zeros(density.coeff_total(), dtype=np.float32) if want_grad else None
     gs = np.zeros(shc.size, dtype=np.float32) if want_grad else None
     ro = _RO(int(opts.n_samples), int(opts.activation), float(opts.softplus_shift),
-             (C.c_double * 3)(*[float(b) for b in opts.background]))
+             (C.c_double * 3)(*[float(b) for b in opts.background]), int(bool(opts.jitter)), int(opts.jitter_seed))
     loss = C.c_double(0.0)
     _check(L.tgcu_photometric_loss(density.handle, C.byref(sh.spec._c()), sh.degree, _ptr(shc), _ptr(r), _ptr(g), n,
                                    C.cast(C.pointer(ro), C.c_void_p), _ptr(cols), _ptr(res), _ptr(gd), _ptr(gs),

@@ -25,8 +25,10 @@ def main():
     R = Reference()
     rng = np.random.default_rng(20240601)
     out = {}
-    cases = [("soft64", 0, 64, 2, (8, 7, 9), 2), ("soft100", 0, 100, 1, (6, 6, 7), 1), ("relu64", 1, 64, 2, (7, 8, 6), 0)]
-    for name, act, ns, order, dres, deg in cases:
+    # jit64: RenderOptions::jitter with a seed (per-ray Rng, volume_render.cpp:69-70)
+    cases = [("soft64", 0, 64, 2, (8, 7, 9), 2, 0), ("soft100", 0, 100, 1, (6, 6, 7), 1, 0),
+             ("relu64", 1, 64, 2, (7, 8, 6), 0, 0), ("jit64", 0, 64, 2, (8, 7, 9), 2, 987654321)]
+    for name, act, ns, order, dres, deg, jseed in cases:
         ds = Spec(3, dres, order=order)
         dc = f32(rng.normal(0, 1.0, ds.V * ds.K))
         dc[::ds.K] = f32(rng.uniform(8.0, 14.0, ds.V) if act == 0 else rng.uniform(-2.0, 6.0, ds.V))
@@ -40,14 +42,15 @@ def main():
         far = f32(near + rng.uniform(0.4, 1.6, n))
         gt = f32(rng.uniform(0, 1, (n, 3)))
         rays = dict(origins=o, dirs=d, near=near, far=far, gt=gt)
-        r = R.photometric_loss(ds, dc, ss, deg, sc, rays, n_samples=ns, activation=act, want_grad=True, render=True)
+        r = R.photometric_loss(ds, dc, ss, deg, sc, rays, n_samples=ns, activation=act, want_grad=True, render=True,
+                               jitter=jseed != 0, jitter_seed=jseed)
         pre = f"{name}_"
         out.update({pre + "meta": np.array([act, ns, order, deg]), pre + "dres": np.array(dres), pre + "dc": dc,
                     pre + "sc": sc, pre + "sres": np.array(ss.res), pre + "sorg": np.array(ss.origin),
                     pre + "sext": np.array(ss.extent), pre + "o": o, pre + "d": d, pre + "near": near,
                     pre + "far": far, pre + "gt": gt, pre + "loss": np.array([r["loss"]]),
                     pre + "gd": r["grad_density"], pre + "gs": r["grad_sh"], pre + "colors": r["colors"],
-                    pre + "resid": r["residual"]})
+                    pre + "resid": r["residual"], pre + "jitter_seed": np.array([jseed], dtype=np.uint64)})
     np.savez_compressed(os.path.join(OUT, "radiance.npz"), **out)
     print("wrote radiance.npz", os.path.getsize(os.path.join(OUT, "radiance.npz")), "bytes")
 

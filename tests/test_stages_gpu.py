@@ -314,3 +314,45 @@ def test_tgrid_errors(z, tmp_path):
             tg.load_tgrid(p)
     with pytest.raises(tg.IngestError, match="cannot open for writing"):
         tg.save_tgrid(tg.init_grid(tg.GridSpec(3, (2, 2, 2))), tmp_path / "no" / "dir.tgrid")
+
+
+@pytest.mark.parametrize("dim,res,order", [(2, (13, 9), 2), (3, (7, 6, 5), 2), (3, (9, 4, 6), 1)])
+def test_init_modes_match_reference(reference, dim, res, order):
+    """init_grid (taylor_grid.cpp:162-188): Zeros, Constant (f0 only) and
+    SmallUniform (the reference Rng stream, uniform(-eps, eps) over every
+    coefficient in order) equal the reference's coefficients rounded to fp32;
+    the memory cap refuses with the reference's message."""
+    from oracle.pyoracle import Spec
+    s = Spec(dim=dim, res=res, order=order)
+    spec = tg.GridSpec(dim=dim, resolution=tuple(res) + ((1,) if dim == 2 else ()), order=order)
+    cases = [(tg.InitMode.Zeros, 0, dict()), (tg.InitMode.Constant, 1, dict(constant=0.3125)),
+             (tg.InitMode.Constant, 1, dict(constant=-1.7)),
+             (tg.InitMode.SmallUniform, 2, dict(epsilon=0.05, seed=17)),
+             (tg.InitMode.SmallUniform, 2, dict(epsilon=1e-4, seed=0))]
+    for mode, rmode, kw in cases:
+        g = tg.init_grid(spec, tg.InitOptions(mode=mode, **kw))
+        ref = reference.init_grid(s, rmode, kw.get("constant", 0.0), kw.get("epsilon", 1e-4), kw.get("seed", 0))
+        assert np.array_equal(g.coeffs, ref.astype(np.float32).astype(np.float64)), (mode, kw)
+        g.close()
+    cap = 8 * s.V * s.K - 1
+    with pytest.raises(MemoryError) as e_ref:
+        reference.init_grid(s, 0, cap=cap)
+    with pytest.raises(tg.ResourceError) as e_ours:
+        tg.init_grid(spec, tg.InitOptions(memory_cap_bytes=cap))
+    assert str(e_ours.value) == str(e_ref.value)
+
+
+def test_all_finite_detects_nan_and_inf():
+    """all_finite (taylor_grid.cpp:190-195) on the device grid."""
+    g = tg.init_grid(tg.GridSpec(dim=3, resolution=(9, 7, 5), order=2),
+                     tg.InitOptions(mode=tg.InitMode.SmallUniform, epsilon=0.1, seed=3))
+    assert g.all_finite()
+    c = g.coeffs
+    for bad in (np.nan, np.inf, -np.inf):
+        for idx in (0, 17, c.size - 1):
+            d = c.copy()
+            d[idx] = bad
+            g.coeffs = d
+            assert not g.all_finite(), (bad, idx)
+    g.coeffs = c
+    assert g.all_finite()
