@@ -8,7 +8,6 @@
 //    it. Points must be brick-sorted (tgcu_sort_points); each CTA finds its
 //    point range by binary search over the brick keys, so no offsets array is
 //    read. This is the coherent-points path.
-#include <cub/cub.cuh>
 
 #include "dispatch.cuh"
 #include "tg_internal.h"
@@ -131,29 +130,6 @@ __device__ __forceinline__ unsigned long long point_key(const DevSpec& s, const 
     return (kb << (DIM * LB)) | kc;
 }
 
-template <int DIM, int LB, class KeyT, class IdxT>
-__global__ void k_point_keys(DevSpec s, const float* __restrict__ pts, long long n, KeyT* __restrict__ keys,
-                             IdxT* __restrict__ idx) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        keys[i] = (KeyT)point_key<DIM, LB>(s, pts + 3 * i, nullptr);
-        idx[i] = (IdxT)i;
-    }
-}
-
-template <class IdxT>
-__global__ void k_gather_points(const float* __restrict__ pts, const IdxT* __restrict__ idx, long long n,
-                                float* __restrict__ out, long long* __restrict__ perm) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long j = (long long)idx[i];
-        out[3 * i] = pts[3 * j];
-        out[3 * i + 1] = pts[3 * j + 1];
-        out[3 * i + 2] = pts[3 * j + 2];
-        if (perm) perm[i] = j;
-    }
-}
-
 template <int DIM>
 constexpr int brick_log2() { return DIM == 3 ? 3 : 4; }
 
@@ -237,51 +213,25 @@ void launch_brick_offsets(Grid& g, const KeyT* keys, const float* pts, int64_t n
     TGCU_CUDA(cudaGetLastError());
 }
 
-// Key = Morton(brick) : Morton(cell in brick), end_bit = D * ceil(log2(max cells)).
-// 32-bit keys and indices whenever they fit (halves the radix passes' bytes).
-template <class KeyT, class IdxT>
-static void sort_points_t(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, int64_t* offsets,
-                          int end_bit, cudaStream_t s) {
-    KeyT *keys = nullptr, *keys_out = nullptr;
-    IdxT *idx = nullptr, *idx_out = nullptr;
-    void* temp = nullptr;
-    size_t temp_bytes = 0;
-    TGCU_CUDA(cudaMallocAsync(&keys, n * sizeof(KeyT), s));
-    TGCU_CUDA(cudaMallocAsync(&keys_out, n * sizeof(KeyT), s));
-    TGCU_CUDA(cudaMallocAsync(&idx, n * sizeof(IdxT), s));
-    TGCU_CUDA(cudaMallocAsync(&idx_out, n * sizeof(IdxT), s));
-    const int blocks = grid_blocks(n, 256, 148 * 32);
-    if (g.spec.dim == 3) k_point_keys<3, 3, KeyT, IdxT><<<blocks, 256, 0, s>>>(g.ds, pts, n, keys, idx);
-    else k_point_keys<2, 4, KeyT, IdxT><<<blocks, 256, 0, s>>>(g.ds, pts, n, keys, idx);
-    count_launch();
-    TGCU_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, keys_out, idx, idx_out, (int64_t)n, 0,
-                                              end_bit, s));
-    TGCU_CUDA(cudaMallocAsync(&temp, temp_bytes, s));
-    TGCU_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_out, idx, idx_out, (int64_t)n, 0,
-                                              end_bit, s));
-    k_gather_points<IdxT><<<blocks, 256, 0, s>>>(pts, idx_out, n, out, reinterpret_cast<long long*>(perm));
-    count_launch();
-    if (offsets) launch_brick_offsets<KeyT>(g, keys_out, nullptr, n, offsets, s);
-    TGCU_CUDA(cudaFreeAsync(temp, s));
-    TGCU_CUDA(cudaFreeAsync(keys, s));
-    TGCU_CUDA(cudaFreeAsync(keys_out, s));
-    TGCU_CUDA(cudaFreeAsync(idx, s));
-    TGCU_CUDA(cudaFreeAsync(idx_out, s));
-    TGCU_CUDA(cudaGetLastError());
-}
+void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xyz, int64_t* perm, long long* off,
+                  float* vals, float* grads, cudaStream_t s);
 
+// Brick sort of query points (tgcu_sort_points): the two-pass partition by
+// Morton brick code (launch_qpart below) writing the sorted coordinates and
+// the source index of each. Points keep no order inside a brick; a NaN point
+// sorts into the origin's brick (the query reports it).
 void launch_sort_points(Grid& g, const float* pts, int64_t n, float* out, int64_t* perm, int64_t* offsets,
                         cudaStream_t s) {
     if (n <= 0) return;
-    int maxc = 1;
-    for (int a = 0; a < g.spec.dim; ++a) maxc = std::max(maxc, g.spec.res[a] - 2);
-    int bits = 1;
-    while ((1 << bits) <= maxc) ++bits;
-    const int end_bit = g.spec.dim * bits;
-    if (end_bit <= 32 && n < (1LL << 31))
-        sort_points_t<unsigned int, unsigned int>(g, pts, n, out, perm, offsets, end_bit, s);
-    else
-        sort_points_t<unsigned long long, unsigned long long>(g, pts, n, out, perm, offsets, end_bit, s);
+    const int64_t codes = query_brick_codes(g);
+    long long* off = reinterpret_cast<long long*>(offsets);
+    long long* tmp = nullptr;
+    if (!off) {
+        TGCU_CUDA(cudaMallocAsync(&tmp, sizeof(long long) * (codes + 1), s));
+        off = tmp;
+    }
+    launch_qpart(g, pts, n, nullptr, out, perm, off, nullptr, nullptr, s);
+    if (tmp) TGCU_CUDA(cudaFreeAsync(tmp, s));
 }
 
 // Where a brick's points come from (k_eval_brick SRC): brick-sorted points
@@ -475,55 +425,429 @@ __global__ void __launch_bounds__(256, query_min_blocks<KOf<DIM, ORDER>::value>(
     }
 }
 
-// ---- binned query of unsorted points ------------------------------------------------
-// A counting sort by query brick replaces the full radix sort: per point its
-// Morton brick code (NaN points are answered here and not binned), global
-// atomic counts, an exclusive scan, and an atomic-cursor scatter of
-// (x, y, z, caller index) records; the brick kernel then writes each value to
-// the caller's slot.
+// ---- two-pass MSD partition of query points by Morton brick code ------------------
+// The brick code kb (KB bits, query_brick_codes() = 2^KB) splits into a
+// coarse digit hi = kb >> LO (2^HI superbricks of 2^LO Morton-consecutive
+// bricks) and a fine digit lo. Pass 1 partitions the points by hi, pass 2
+// partitions every superbrick's segment by lo. Each pass is a counting sort
+// over tiles of kQpTile elements: a histogram kernel (shared-memory counts
+// per tile), a column scan giving every (tile, digit) its output start, and a
+// scatter kernel that sorts its tile by digit in shared memory and then
+// writes whole digit runs (~kQpTile / 2^digit_bits records, contiguous) —
+// no contended global atomics and no scattered 16-byte stores. The brick
+// offsets come out of pass 2's scan. The binned query drops NaN points
+// (answered NaN, status set); the sort keeps them in the origin's brick.
+constexpr int kQpThreads = 512;
+constexpr int kQpTile = 4096;  // elements per CTA, both passes
+constexpr int kQpPer = kQpTile / kQpThreads;
+constexpr int kQpRowBlocks = 32;  // column-scan row blocks
+
+struct QpArgs {
+    DevSpec s;
+    const float* pts;   // n x 3
+    long long n;
+    int KB, LO;         // key bits, fine-digit bits
+    int ntiles;         // pass-1 tiles
+    int* H1;            // [ntiles][NH]: counts -> exclusive column prefixes
+    int* P1;            // [kQpRowBlocks][NH] column-scan partials
+    int* tot;           // [NH] digit totals
+    long long* seg;     // [NH + 1] superbrick segment starts
+    float4* A;          // pass-1 output
+    int* cseg;          // pass-2 tile -> superbrick (-1 past the end)
+    int* cfirst;        // [NH + 1] first pass-2 tile of each superbrick
+    int* H2;            // [maxtiles2][NL]: counts -> output starts
+    long long* off;     // [2^KB + 1] brick offsets
+    float4* B;          // pass-2 output records (or null: sorted xyz + perm)
+    float* out_xyz;
+    long long* perm;
+    float* vals;        // NaN answers (binned query), null for the sort
+    float* grads;
+    Status* st;
+};
+
+// Morton brick code of a point (as point_key; a NaN coordinate counts as
+// the origin's): the fp64 cell rule of locate, brick = cell >> LB.
 template <int DIM, int LB>
-__global__ void __launch_bounds__(256) k_qbin_count(DevSpec s, const float* __restrict__ pts, long long n,
-                                                    int* __restrict__ cnt, float* __restrict__ vals,
-                                                    float* __restrict__ grads, Status* st) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        bool nan = false;
+__device__ __forceinline__ int qp_code(const DevSpec& s, float x, float y, float z) {
+    const float p[3] = {x, y, z};
+    unsigned int b[3] = {0, 0, 0};
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) nan |= isnan(pts[3 * i + a]);
-        if (nan) {
-            atomicMin(&st->nan_point, (unsigned long long)i);
-            vals[i] = __int_as_float(0x7fc00000);
-            if (grads)
-                for (int a = 0; a < 3; ++a) grads[3 * i + a] = __int_as_float(0x7fc00000);
-            continue;
+    for (int a = 0; a < DIM; ++a) {
+        double v = (double)p[a];
+        if (isnan(v)) v = s.origin[a];
+        const double lo = s.origin[a], hi = s.hi[a];
+        const double c = v < lo ? lo : (v > hi ? hi : v);
+        int ci = (int)floor(div_by_h(c - lo, s.h[a], s.inv_h[a]));
+        ci = ci < 0 ? 0 : (ci > s.res[a] - 2 ? s.res[a] - 2 : ci);
+        b[a] = (unsigned int)ci >> LB;
+    }
+    if (DIM == 3) return (int)(spread3_10(b[0]) | (spread3_10(b[1]) << 1) | (spread3_10(b[2]) << 2));
+    return (int)(spread2(b[0]) | (spread2(b[1]) << 1));
+}
+
+// Element j of this CTA's tile: pass 1 reads point j (NaN points of the
+// binned query are answered here and get digit -1), pass 2 reads record j
+// of the tile's superbrick chunk. Returns the digit.
+template <int DIM, int LB, int PASS>
+__device__ __forceinline__ int qp_load(const QpArgs& A, long long e1, long long j, float4& rec, bool answer_nan) {
+    if (j >= e1) return -1;
+    if constexpr (PASS == 1) {
+        const float x = A.pts[3 * j], y = A.pts[3 * j + 1], z = DIM == 3 ? A.pts[3 * j + 2] : 0.f;
+        rec = make_float4(x, y, z, __int_as_float((int)j));
+        if (A.vals && (isnan(x) || isnan(y) || (DIM == 3 && isnan(z)))) {
+            if (answer_nan) {
+                atomicMin(&A.st->nan_point, (unsigned long long)j);
+                A.vals[j] = __int_as_float(0x7fc00000);
+                if (A.grads)
+                    for (int a = 0; a < 3; ++a) A.grads[3 * j + a] = __int_as_float(0x7fc00000);
+            }
+            return -1;
         }
-        unsigned int kb;
-        point_key<DIM, LB>(s, pts + 3 * i, &kb);
-        atomicAdd(&cnt[kb], 1);
+        return qp_code<DIM, LB>(A.s, x, y, z) >> A.LO;
+    } else {
+        rec = A.A[j];
+        return qp_code<DIM, LB>(A.s, rec.x, rec.y, rec.z) & ((1 << A.LO) - 1);
     }
 }
 
-template <int DIM, int LB>
-__global__ void __launch_bounds__(256) k_qbin_scatter(DevSpec s, const float* __restrict__ pts, long long n,
-                                                      int* __restrict__ cursor, float4* __restrict__ binned) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const float x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
-        if (isnan(x) || isnan(y) || (DIM == 3 && isnan(z))) continue;
-        unsigned int kb;
-        point_key<DIM, LB>(s, pts + 3 * i, &kb);
-        const int slot = atomicAdd(&cursor[kb], 1);
-        binned[slot] = make_float4(x, y, z, __int_as_float((int)i));
+// Tile range of this CTA (pass 2: chunk of one superbrick; false = no tile).
+template <int PASS>
+__device__ __forceinline__ bool qp_tile(const QpArgs& A, long long& e0, long long& e1) {
+    if constexpr (PASS == 1) {
+        e0 = (long long)blockIdx.x * kQpTile;
+        e1 = min(A.n, e0 + kQpTile);
+        return true;
+    } else {
+        const int h = A.cseg[blockIdx.x];
+        if (h < 0) return false;
+        e0 = A.seg[h] + (long long)(blockIdx.x - A.cfirst[h]) * kQpTile;
+        e1 = min(A.seg[h + 1], e0 + kQpTile);
+        return true;
     }
 }
 
-__global__ void k_i32_to_i64_copy(const int* __restrict__ a, long long* __restrict__ b, int* __restrict__ c,
-                                  long long n) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        b[i] = a[i];
-        if (i < n - 1) c[i] = a[i];
+template <int DIM, int LB, int PASS>
+__global__ void __launch_bounds__(kQpThreads) k_qp_hist(QpArgs A) {
+    extern __shared__ int h[];
+    const int ND = PASS == 1 ? 1 << (A.KB - A.LO) : 1 << A.LO;
+    long long e0, e1;
+    if (!qp_tile<PASS>(A, e0, e1)) return;
+    for (int i = threadIdx.x; i < ND; i += blockDim.x) h[i] = 0;
+    float4 rec[kQpPer];
+    int d[kQpPer];
+#pragma unroll
+    for (int k = 0; k < kQpPer; ++k)  // all loads in flight first
+        d[k] = qp_load<DIM, LB, PASS>(A, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], true);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kQpPer; ++k)
+        if (d[k] >= 0) atomicAdd(&h[d[k]], 1);
+    __syncthreads();
+    int* row = (PASS == 1 ? A.H1 : A.H2) + (long long)blockIdx.x * ND;
+    for (int i = threadIdx.x; i < ND; i += blockDim.x) row[i] = h[i];
+}
+
+// Pass-1 column scan over the tiles, in row blocks: partial sums per (row
+// block, digit), then the exclusive prefixes in place and the digit totals.
+__global__ void __launch_bounds__(256) k_qp_cols_partial(const int* __restrict__ H, int nrows, int nd,
+                                                        int* __restrict__ P) {
+    const int d = blockIdx.x * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5;
+    const int per = (nrows + kQpRowBlocks - 1) / kQpRowBlocks;
+    const int r0 = min(nrows, (int)blockIdx.y * per), r1 = min(nrows, r0 + per);
+    __shared__ int part[8][32];
+    int sum = 0;
+    if (d < nd)
+        for (int r = r0 + w; r < r1; r += 8) sum += H[(long long)r * nd + d];
+    part[w][threadIdx.x & 31] = sum;
+    __syncthreads();
+    if (w == 0 && d < nd) {
+        int t = 0;
+        for (int k = 0; k < 8; ++k) t += part[k][threadIdx.x & 31];
+        P[(long long)blockIdx.y * nd + d] = t;
     }
+}
+__global__ void __launch_bounds__(256) k_qp_cols_final(int* __restrict__ H, int nrows, int nd, const int* __restrict__ P,
+                                                      int* __restrict__ tot) {
+    const int d = blockIdx.x * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5;
+    const int per = (nrows + kQpRowBlocks - 1) / kQpRowBlocks;
+    const int r0 = min(nrows, (int)blockIdx.y * per), r1 = min(nrows, r0 + per);
+    const int wper = (r1 - r0 + 7) / 8, w0 = min(r1, r0 + w * wper), w1 = min(r1, w0 + wper);
+    __shared__ int part[8][32];
+    int sum = 0;
+    if (d < nd)
+        for (int r = w0; r < w1; ++r) sum += H[(long long)r * nd + d];
+    part[w][threadIdx.x & 31] = sum;
+    __syncthreads();
+    if (d >= nd) return;
+    int base = 0;
+    for (int b = 0; b < (int)blockIdx.y; ++b) base += P[(long long)b * nd + d];
+    for (int k = 0; k < w; ++k) base += part[k][threadIdx.x & 31];
+    // 8 rows per batch: the loads of a batch are in flight together
+    for (int r = w0; r < w1; r += 8) {
+        int v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = r + k < w1 ? H[(long long)(r + k) * nd + d] : 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (r + k < w1) {
+                H[(long long)(r + k) * nd + d] = base;
+                base += v[k];
+            }
+    }
+    if (blockIdx.y == kQpRowBlocks - 1 && w == 7) tot[d] = base;
+}
+
+// Superbrick segment starts (exclusive scan of the totals, one CTA) and the
+// pass-2 tile map: superbrick h gets tiles [cfirst[h], cfirst[h+1]).
+__global__ void __launch_bounds__(1024) k_qp_segments(const int* __restrict__ tot, int NH, long long* __restrict__ seg,
+                                                      int* __restrict__ cfirst, int* __restrict__ cseg, int maxtiles) {
+    __shared__ long long wsum[32];
+    __shared__ int wch[32];
+    __shared__ long long carry;
+    __shared__ int ccarry;
+    if (threadIdx.x == 0) {
+        carry = 0;
+        ccarry = 0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < NH; b0 += 1024) {
+        const int b = b0 + threadIdx.x;
+        const long long t = b < NH ? tot[b] : 0;
+        const int c = (int)((t + kQpTile - 1) / kQpTile);
+        long long x = t;
+        int y = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long xx = __shfl_up_sync(0xffffffffu, x, o);
+            const int yy = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) {
+                x += xx;
+                y += yy;
+            }
+        }
+        if (lane == 31) {
+            wsum[warp] = x;
+            wch[warp] = y;
+        }
+        __syncthreads();
+        long long wb = 0;
+        int cb = 0;
+        for (int k = 0; k < warp; ++k) {
+            wb += wsum[k];
+            cb += wch[k];
+        }
+        const long long sx = carry + wb + x - t;
+        const int sc = ccarry + cb + y - c;
+        if (b < NH) {
+            seg[b] = sx;
+            cfirst[b] = sc;
+            for (int k = 0; k < c && sc + k < maxtiles; ++k) cseg[sc + k] = b;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) {
+            carry = sx + t;
+            ccarry = sc + c;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        seg[NH] = carry;
+        cfirst[NH] = ccarry;
+    }
+    __syncthreads();
+    for (int k = ccarry + threadIdx.x; k < maxtiles; k += blockDim.x) cseg[k] = -1;
+}
+
+// Pass 2 per superbrick (one CTA, a thread per fine digit): prefixes of H2
+// over the superbrick's tiles, the brick offsets (segment start + exclusive
+// scan of the digit totals) and the per-(tile, digit) output starts.
+__global__ void __launch_bounds__(1024) k_qp_scan2(QpArgs A) {
+    const int hsb = blockIdx.x;
+    const int NL = 1 << A.LO;
+    const int ch0 = A.cfirst[hsb], ch1 = A.cfirst[hsb + 1];
+    __shared__ int wsum[32];
+    __shared__ long long rbase;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) rbase = A.seg[hsb];
+    __syncthreads();
+    for (int l0 = 0; l0 < NL; l0 += 1024) {  // NL <= 4096
+        const int lo = l0 + threadIdx.x;
+        int tot = 0;
+        if (lo < NL)
+            for (int c = ch0; c < ch1; c += 8) {  // 8 rows per batch, loads in flight together
+                int v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = c + k < ch1 ? A.H2[(long long)(c + k) * NL + lo] : 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (c + k < ch1) {
+                        A.H2[(long long)(c + k) * NL + lo] = tot;
+                        tot += v[k];
+                    }
+            }
+        int x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        int wb = 0;
+        for (int k = 0; k < warp; ++k) wb += wsum[k];
+        const long long start = rbase + wb + x - tot;
+        if (lo < NL) {
+            A.off[((long long)hsb << A.LO) + lo] = start;
+            for (int c = ch0; c < ch1; ++c) A.H2[(long long)c * NL + lo] += (int)start;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) rbase = start + tot;
+        __syncthreads();
+    }
+    if (hsb == (int)gridDim.x - 1 && threadIdx.x == 0) A.off[(long long)gridDim.x << A.LO] = A.seg[gridDim.x];
+}
+
+// Scatter: the tile's elements sorted by digit in shared memory (counting
+// sort: shared-memory ranks, a block scan of the digit counts), then written
+// out in that order, element j of digit d at gstart[d] + (j - lstart[d]):
+// each digit's run of the tile lands contiguously.
+template <int DIM, int LB, int PASS>
+__global__ void __launch_bounds__(kQpThreads) k_qp_scatter(QpArgs A) {
+    extern __shared__ __align__(16) unsigned char qsm[];
+    const int ND = PASS == 1 ? 1 << (A.KB - A.LO) : 1 << A.LO;
+    float4* recs = reinterpret_cast<float4*>(qsm);                            // [kQpTile]
+    unsigned short* dig = reinterpret_cast<unsigned short*>(recs + kQpTile);  // [kQpTile]
+    int* cnt = reinterpret_cast<int*>(dig + kQpTile);                         // [ND] counts -> local starts
+    int* gst = cnt + ND;                                                       // [ND] global starts
+    __shared__ int wsum[kQpThreads / 32];
+    __shared__ int valid;
+    long long e0, e1;
+    if (!qp_tile<PASS>(A, e0, e1)) return;
+    const int* row = (PASS == 1 ? A.H1 : A.H2) + (long long)blockIdx.x * ND;
+    for (int i = threadIdx.x; i < ND; i += blockDim.x) {
+        cnt[i] = 0;
+        gst[i] = PASS == 1 ? (int)A.seg[i] + row[i] : row[i];
+    }
+    float4 rec[kQpPer];
+    int d[kQpPer], rk[kQpPer];
+#pragma unroll
+    for (int k = 0; k < kQpPer; ++k)
+        d[k] = qp_load<DIM, LB, PASS>(A, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], false);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kQpPer; ++k) rk[k] = d[k] >= 0 ? atomicAdd(&cnt[d[k]], 1) : 0;
+    __syncthreads();
+    // exclusive scan of cnt (ND <= 4096 digits, kQpThreads threads)
+    const int per = (ND + kQpThreads - 1) / kQpThreads;
+    const int i0 = threadIdx.x * per;
+    int loc = 0;
+    for (int i = i0; i < min(ND, i0 + per); ++i) loc += cnt[i];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    int run = x - loc;
+    for (int k = 0; k < warp; ++k) run += wsum[k];
+    for (int i = i0; i < min(ND, i0 + per); ++i) {
+        const int c = cnt[i];
+        cnt[i] = run;
+        run += c;
+    }
+    if (i0 < ND && i0 + per >= ND) valid = run;  // the owner of the last digit: the tile's element count
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kQpPer; ++k)
+        if (d[k] >= 0) {
+            const int j = cnt[d[k]] + rk[k];
+            recs[j] = rec[k];
+            dig[j] = (unsigned short)d[k];
+        }
+    __syncthreads();
+    // the tile's elements in digit order (NaN points of the binned query are
+    // not among them)
+    for (int j = threadIdx.x; j < valid; j += blockDim.x) {
+        const int dj = dig[j];
+        const int pos = gst[dj] + (j - cnt[dj]);
+        const float4 q = recs[j];
+        if (PASS == 1 || A.B) {
+            (PASS == 1 ? A.A : A.B)[pos] = q;
+        } else {
+            A.out_xyz[3 * (long long)pos] = q.x;
+            A.out_xyz[3 * (long long)pos + 1] = q.y;
+            A.out_xyz[3 * (long long)pos + 2] = q.z;
+            if (A.perm) A.perm[pos] = (long long)(unsigned int)__float_as_int(q.w);
+        }
+    }
+}
+
+// Runs both passes. B != null: records (x, y, z, index) grouped by brick;
+// else sorted xyz (+ perm). off: 2^KB + 1 brick offsets.
+void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xyz, int64_t* perm,
+                  long long* off, float* vals, float* grads, cudaStream_t s) {
+    require(n < (1LL << 31), "query partition: more than 2^31 points per call");
+    const int64_t codes = query_brick_codes(g);
+    int KB = 0;
+    while ((1LL << KB) < codes) ++KB;
+    QpArgs A{};
+    A.s = g.ds;
+    A.pts = pts;
+    A.n = n;
+    A.KB = KB;
+    A.LO = std::min(12, std::max((KB + 1) / 2, KB - 12));
+    require(KB - A.LO <= 12, "query partition: " + std::to_string(KB) + " brick-code bits exceed two 12-bit passes");
+    const int NH = 1 << (KB - A.LO), NL = 1 << A.LO;
+    A.ntiles = (int)((n + kQpTile - 1) / kQpTile);
+    const int maxtiles = A.ntiles + NH;
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t bH1 = al(sizeof(int) * (size_t)A.ntiles * NH), bP1 = al(sizeof(int) * kQpRowBlocks * NH),
+                 bTot = al(sizeof(int) * NH), bSeg = al(sizeof(long long) * (NH + 1)), bCf = al(sizeof(int) * (NH + 1)),
+                 bCs = al(sizeof(int) * maxtiles), bH2 = al(sizeof(int) * (size_t)maxtiles * NL),
+                 bA = al(sizeof(float4) * (size_t)std::max<int64_t>(n, 1));
+    char* q = nullptr;
+    TGCU_CUDA(cudaMallocAsync(&q, bH1 + bP1 + bTot + bSeg + bCf + bCs + bH2 + bA, s));
+    char* const scratch = q;
+    A.H1 = reinterpret_cast<int*>(q); q += bH1;
+    A.P1 = reinterpret_cast<int*>(q); q += bP1;
+    A.tot = reinterpret_cast<int*>(q); q += bTot;
+    A.seg = reinterpret_cast<long long*>(q); q += bSeg;
+    A.cfirst = reinterpret_cast<int*>(q); q += bCf;
+    A.cseg = reinterpret_cast<int*>(q); q += bCs;
+    A.H2 = reinterpret_cast<int*>(q); q += bH2;
+    A.A = reinterpret_cast<float4*>(q);
+    A.off = off;
+    A.B = B;
+    A.out_xyz = out_xyz;
+    A.perm = reinterpret_cast<long long*>(perm);
+    A.vals = vals;
+    A.grads = grads;
+    A.st = g.st;
+    const size_t hs1 = sizeof(int) * NH, hs2 = sizeof(int) * NL;
+    const size_t ss1 = (sizeof(float4) + 2) * kQpTile + 2 * hs1, ss2 = (sizeof(float4) + 2) * kQpTile + 2 * hs2;
+    auto run = [&](auto hist1, auto scatter1, auto hist2, auto scatter2) {
+        TGCU_CUDA(cudaFuncSetAttribute(scatter1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ss1));
+        TGCU_CUDA(cudaFuncSetAttribute(scatter2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ss2));
+        hist1<<<A.ntiles, kQpThreads, hs1, s>>>(A);
+        k_qp_cols_partial<<<dim3((NH + 31) / 32, kQpRowBlocks), 256, 0, s>>>(A.H1, A.ntiles, NH, A.P1);
+        k_qp_cols_final<<<dim3((NH + 31) / 32, kQpRowBlocks), 256, 0, s>>>(A.H1, A.ntiles, NH, A.P1, A.tot);
+        k_qp_segments<<<1, 1024, 0, s>>>(A.tot, NH, A.seg, A.cfirst, A.cseg, maxtiles);
+        scatter1<<<A.ntiles, kQpThreads, ss1, s>>>(A);
+        hist2<<<maxtiles, kQpThreads, hs2, s>>>(A);
+        k_qp_scan2<<<NH, 1024, 0, s>>>(A);
+        scatter2<<<maxtiles, kQpThreads, ss2, s>>>(A);
+    };
+    if (g.spec.dim == 3)
+        run(k_qp_hist<3, 3, 1>, k_qp_scatter<3, 3, 1>, k_qp_hist<3, 3, 2>, k_qp_scatter<3, 3, 2>);
+    else
+        run(k_qp_hist<2, 4, 1>, k_qp_scatter<2, 4, 1>, k_qp_hist<2, 4, 2>, k_qp_scatter<2, 4, 2>);
+    count_launch(8);
+    TGCU_CUDA(cudaFreeAsync(scratch, s));
+    TGCU_CUDA(cudaGetLastError());
 }
 
 // Query tile tensor maps (box (B+1) vertices padded to 16 bytes x (B+1) [x (B+1)]).
@@ -567,36 +891,16 @@ static void launch_brick_query(Grid& g, const QuerySrc& Q, float* vals, float* g
 
 void launch_eval_binned(Grid& g, const float* pts, int64_t n, float* vals, float* grads, cudaStream_t s) {
     if (n <= 0) return;
-    require(n < (1LL << 31), "eval: more than 2^31 points per call");
     const int64_t codes = query_brick_codes(g);
-    int *cnt = nullptr, *cursor = nullptr;
     long long* off = nullptr;
     float4* binned = nullptr;
-    void* temp = nullptr;
-    size_t temp_bytes = 0;
-    TGCU_CUDA(cudaMallocAsync(&cnt, sizeof(int) * (codes + 1), s));
-    TGCU_CUDA(cudaMallocAsync(&cursor, sizeof(int) * (codes + 1), s));
     TGCU_CUDA(cudaMallocAsync(&off, sizeof(long long) * (codes + 1), s));
     TGCU_CUDA(cudaMallocAsync(&binned, sizeof(float4) * n, s));
-    TGCU_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * (codes + 1), s));
-    const int blocks = grid_blocks(n, 256, 148 * 32);
-    if (g.spec.dim == 3) k_qbin_count<3, 3><<<blocks, 256, 0, s>>>(g.ds, pts, n, cnt, vals, grads, g.st);
-    else k_qbin_count<2, 4><<<blocks, 256, 0, s>>>(g.ds, pts, n, cnt, vals, grads, g.st);
-    // cursor = off (int) = exclusive scan of cnt over codes + 1 entries
-    TGCU_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, cnt, cursor, (int64_t)(codes + 1), s));
-    TGCU_CUDA(cudaMallocAsync(&temp, temp_bytes, s));
-    TGCU_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, cnt, cursor, (int64_t)(codes + 1), s));
-    k_i32_to_i64_copy<<<grid_blocks(codes + 1, 256), 256, 0, s>>>(cursor, off, cnt, codes + 1);  // cnt := cursor copy
-    if (g.spec.dim == 3) k_qbin_scatter<3, 3><<<blocks, 256, 0, s>>>(g.ds, pts, n, cnt, binned);
-    else k_qbin_scatter<2, 4><<<blocks, 256, 0, s>>>(g.ds, pts, n, cnt, binned);
-    count_launch(3);
+    launch_qpart(g, pts, n, binned, nullptr, nullptr, off, vals, grads, s);
     QuerySrc Q;
     Q.pts = reinterpret_cast<const float*>(binned);
     Q.off = off;
     launch_brick_query<1>(g, Q, vals, grads, s);
-    TGCU_CUDA(cudaFreeAsync(temp, s));
-    TGCU_CUDA(cudaFreeAsync(cnt, s));
-    TGCU_CUDA(cudaFreeAsync(cursor, s));
     TGCU_CUDA(cudaFreeAsync(off, s));
     TGCU_CUDA(cudaFreeAsync(binned, s));
     TGCU_CUDA(cudaGetLastError());
