@@ -466,14 +466,26 @@ struct QpArgs {
 };
 
 // Morton brick code of a point (as point_key; a NaN coordinate counts as
-// the origin's): the fp64 cell rule of locate, brick = cell >> LB.
+// the origin's): the brick of the fp64 cell rule of locate, brick = cell >>
+// LB. The cell coordinate t = (x - origin) / h is first formed in fp32
+// (error < 1e-4 cells up to 2^12 cells per axis); only a point within 1/64
+// of a cell of a brick plane or of the domain edge takes the exact fp64 rule,
+// so the partition's brick equals the query kernel's.
 template <int DIM, int LB>
 __device__ __forceinline__ int qp_code(const DevSpec& s, float x, float y, float z) {
     const float p[3] = {x, y, z};
     unsigned int b[3] = {0, 0, 0};
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
-        double v = (double)p[a];
+        const float tf = (p[a] - (float)s.origin[a]) * s.inv_hf[a];
+        const float tb = tf * (1.0f / (1 << LB));
+        const float fr = tb - floorf(tb);
+        if (tf > 0.015625f && tf < (float)(s.res[a] - 1) - 0.015625f && fr > 0.015625f / (1 << LB) &&
+            fr < 1.0f - 0.015625f / (1 << LB)) {
+            b[a] = (unsigned int)tb;
+            continue;
+        }
+        double v = (double)p[a];  // near a brick plane, the domain edge, or NaN: the exact rule
         if (isnan(v)) v = s.origin[a];
         const double lo = s.origin[a], hi = s.hi[a];
         const double c = v < lo ? lo : (v > hi ? hi : v);
