@@ -696,7 +696,7 @@ def main():
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         import bench_configs
         with ClockSampler(dev) as cclk:
-            line["larger_configs"] = [bench_configs.run(c, 30, 5) for c in ("c1", "c3", "c5")]
+            line["larger_configs"] = [bench_configs.run(c, 30, 5) for c in ("c1", "c3", "c5", "c2det")]
         line["larger_configs_clocks"] = cclk.summary()
         if not args.no_cpu_baseline:
             for ent in line["larger_configs"]:

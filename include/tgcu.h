@@ -359,6 +359,15 @@ int tgcu_run_schedule(tgcu_grid** grid, const tgcu_stage* stages, int nstages, c
                       const tgcu_loss_config* cfg, tgcu_batch_fn batch, tgcu_stage_fn on_stage, void* user, int flags,
                       void* stream, tgcu_trace_row* trace, double* stage_seconds);
 
+/* Deterministic mode (the reference's --deterministic, run_config.cpp:239-242):
+ * the fused step sums every gradient and loss partial in a canonical order
+ * (each brick's binned points sorted by their bits, every cell run of a chunk
+ * in record order), so repeated runs give bit-identical parameters and loss
+ * traces. Costs a per-brick sort and per-cell run sorts per step; a brick may
+ * then hold at most 4096 point copies (TGCU_ERR_CONFIG beyond). Default: off,
+ * or on when the environment has TGCU_DETERMINISTIC=1 at grid creation. */
+int tgcu_grid_set_deterministic(tgcu_grid* g, int on);
+
 /* Fused steps issued on this grid since creation or the last reported error;
  * error messages of a failed step name it as "step <this index at launch>". */
 int tgcu_grid_steps_launched(const tgcu_grid* g, int64_t* n);

@@ -170,6 +170,7 @@ def lib():
     L.tgcu_eikonal_loss.argtypes = [P, P, C.c_int64, C.c_double, P, C.POINTER(C.c_double), C.c_int, P]
     L.tgcu_train_step_fresh_eik.argtypes = [P, P, C.c_int64, P, C.POINTER(_Loss), C.POINTER(_Terms), C.c_int, P]
     L.tgcu_shuffle_order.argtypes = [C.c_uint64, C.c_int64, P]
+    L.tgcu_grid_set_deterministic.argtypes = [P, C.c_int]
     L.tgcu_comm_create.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(P)]
     L.tgcu_comm_destroy.argtypes = [P]
     L.tgcu_comm_info.argtypes = [P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
@@ -441,6 +442,11 @@ class TaylorGrid:
 
     def zero_grad(self):
         _check(lib().tgcu_grad_zero(self._h, C.c_void_p(self.grad_ptr()), None))
+
+    def set_deterministic(self, on: bool = True):
+        """Bit-reproducible fused steps (tgcu_grid_set_deterministic): canonical
+        summation orders, the reference's --deterministic (run_config.cpp:239-242)."""
+        _check(lib().tgcu_grid_set_deterministic(self._h, 1 if on else 0))
 
     def all_finite(self) -> bool:
         r = C.c_int()

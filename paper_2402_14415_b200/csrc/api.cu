@@ -341,6 +341,7 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         st0.nan_bin[0] = st0.nan_bin[1] = ULLONG_MAX;
         TGCU_CUDA(cudaMemcpy(g.st, &st0, sizeof(Status), cudaMemcpyHostToDevice));
         // Brick decomposition (train.cu / query.cu).
+        if (const char* det = std::getenv("TGCU_DETERMINISTIC")) g.deterministic = det[0] == '1';
         g.NB = 1;
         g.zb_global = nbz_global;
         g.code_sh[0] = code_sh[0];
@@ -496,6 +497,9 @@ static void raise_sticky(Grid& g) {
               std::to_string(s.error_step);
     else if (s.error_kind == 2)
         msg = "run_schedule: non-finite loss at stage 0 step " + std::to_string(s.error_step);
+    else if (s.error_kind == 4)
+        msg = "deterministic mode: brick " + std::to_string(s.error_index) +
+              " holds more than 4096 point copies (the canonical-order sort's capacity)";
     else
         msg = "adam_step: non-finite gradient at parameter index " + std::to_string(s.error_index) +
               " (stage 0 step " + std::to_string(s.error_step) + ")";
@@ -1320,5 +1324,12 @@ int tgcu_host_alloc(void** p, size_t bytes) {
 int tgcu_host_free(void* p) {
     return guard([&] {
         if (p) TGCU_CUDA(cudaFreeHost(p));
+    });
+}
+
+int tgcu_grid_set_deterministic(tgcu_grid* h, int on) {
+    return guard([&] {
+        require(h != nullptr, "set_deterministic: NULL grid");
+        h->g.deterministic = on != 0;
     });
 }

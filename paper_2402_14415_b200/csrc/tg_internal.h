@@ -65,7 +65,10 @@ DevSpec make_devspec(const tgcu_grid_spec& s);
 // Brick edge (vertices per axis) of the fused training kernel and the
 // brick-binned query.
 constexpr int kBrick3 = 8;
-constexpr int kBrick2 = 16;
+#ifndef TGCU_BRICK2
+#define TGCU_BRICK2 16
+#endif
+constexpr int kBrick2 = TGCU_BRICK2;
 
 struct Grid {
     tgcu_grid_spec spec{};
@@ -170,6 +173,7 @@ struct Grid {
     // Step breakdown (tgcu_step_breakdown, diagnostics): events at the
     // boundaries of one fused step, summed per segment after each step.
     bool bd_on = false;
+    bool deterministic = false;  // canonical summation orders (tgcu_grid_set_deterministic)
     cudaEvent_t bd_ev[6] = {};
     double bd_sum[5] = {0, 0, 0, 0, 0};
     int bd_steps = 0;

@@ -505,6 +505,7 @@ struct StepArgs {
     float* peer_hi;
     int peer_hi_zb, peer_hi_lz;
     const int* order;  // launch order of the bricks (1D grid): most chunks first
+    int det;           // deterministic mode: canonical record order inside every cell run
 };
 
 // Cell runs of a chunk's records: every cell gets the contiguous slot range
@@ -796,7 +797,27 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             }
             ec = DIM == 3 ? (tc[2] * CE + tc[1]) * CE + tc[0] : tc[1] * CE + tc[0];
             if (tiny) start[tid] = tc[0] | (tc[1] << 8) | (tc[2] << 16);
-            else rank = atomicAdd(&cnt[ec], 1);
+            else if (!A.det) rank = atomicAdd(&cnt[ec], 1);
+        }
+        if (A.det && !tiny) {
+            // Deterministic mode: the stable rank (earlier threads of the
+            // chunk first), so every cell run lists its points in chunk order
+            // and each vertex sums them in a fixed order: warp-local ranks by
+            // __match_any_sync, then the warps take their cells' bases in warp
+            // order (one warp per barrier interval).
+            const bool val = tid < m;
+            const unsigned peers = __match_any_sync(0xffffffffu, val ? ec : S::NCELL + lane);
+            const int leader = __ffs(peers) - 1;
+            const int lrank = __popc(peers & ((1u << lane) - 1u));
+            for (int w = 0; w < NW; ++w) {
+                int b0 = 0;
+                if (warp == w && val && lane == leader) {
+                    b0 = cnt[ec];
+                    cnt[ec] = b0 + __popc(peers);
+                }
+                if (warp == w) rank = __shfl_sync(0xffffffffu, b0, leader) + lrank;
+                __syncthreads();
+            }
         }
 #ifdef TGCU_PHASE_TIMING
         unsigned long long pt_c0 = 0;
@@ -937,6 +958,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             for (int k2 = 0; k2 < REC / 2; ++k2) dst[k2] = make_float2(rv[2 * k2], rv[2 * k2 + 1]);
         }
         __syncthreads();  // records visible
+
 #ifdef TGCU_PHASE_TIMING
         TGCU_PT_SET(pt_x)
         if (tid == 0) pt_2a += pt_x - pt_f0;
@@ -1376,6 +1398,73 @@ void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& 
     TGCU_CUDA(cudaGetLastError());
 }
 
+// Deterministic mode: each brick's binned point copies in canonical order
+// (the float4 records' bits, lexicographic), since the binning scatter
+// reserves slots with shared-memory atomics. Bitonic sort of the brick's run
+// in shared memory: bricks of at most one chunk by 256-thread CTAs (one per
+// brick), the multi-chunk ("heavy", listed first in the launch order) bricks
+// by a persistent kernel of 1024-thread CTAs, up to kDetSortCap copies (a
+// larger brick is an error).
+constexpr int kDetSortCap = 4096;
+__device__ __forceinline__ bool rec_less(const float4& a, const float4& b) {
+    const unsigned a0 = __float_as_uint(a.x), a1 = __float_as_uint(a.y), a2 = __float_as_uint(a.z),
+                   a3 = __float_as_uint(a.w);
+    const unsigned b0 = __float_as_uint(b.x), b1 = __float_as_uint(b.y), b2 = __float_as_uint(b.z),
+                   b3 = __float_as_uint(b.w);
+    if (a0 != b0) return a0 < b0;
+    if (a1 != b1) return a1 < b1;
+    if (a2 != b2) return a2 < b2;
+    return a3 < b3;
+}
+__device__ void sort_run(float4* __restrict__ binned, int p0, int n, float4* rs) {
+    int np = 1;
+    while (np < n) np <<= 1;
+    const float4 pad = make_float4(__int_as_float(-1), __int_as_float(-1), __int_as_float(-1), __int_as_float(-1));
+    for (int i = threadIdx.x; i < np; i += blockDim.x) rs[i] = i < n ? binned[p0 + i] : pad;  // padding sorts last
+    __syncthreads();
+    for (int k = 2; k <= np; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < np; i += blockDim.x) {
+                const int ix = i ^ j;
+                if (ix > i) {
+                    const float4 a = rs[i], c = rs[ix];
+                    if (((i & k) == 0) == rec_less(c, a)) {
+                        rs[i] = c;
+                        rs[ix] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) binned[p0 + i] = rs[i];
+    __syncthreads();
+}
+__global__ void __launch_bounds__(256) k_bin_sort_small(float4* __restrict__ binned, const int* __restrict__ off,
+                                                       int NB, int ch) {
+    __shared__ float4 rs[512];
+    const int b = blockIdx.x;
+    const int p0 = off[b], n = off[b + 1] - p0;
+    if (n <= 1 || n > ch) return;
+    sort_run(binned, p0, n, rs);
+}
+__global__ void __launch_bounds__(1024) k_bin_sort_heavy(float4* __restrict__ binned, const int* __restrict__ off,
+                                                        const int* __restrict__ ord, int NB, Status* st) {
+    extern __shared__ float4 rh[];
+    const int nh = ord[NB];
+    for (int i = blockIdx.x; i < nh; i += gridDim.x) {
+        const int b = ord[i];
+        const int p0 = off[b], n = off[b + 1] - p0;
+        if (n > kDetSortCap) {
+            if (threadIdx.x == 0 && atomicCAS(&st->error, 0, TGCU_ERR_CONFIG) == 0) {
+                st->error_kind = 4;
+                st->error_index = b;
+            }
+            continue;
+        }
+        sort_run(binned, p0, n, rh);
+    }
+}
+
 void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
                        int in_idx,
                        int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
@@ -1465,6 +1554,19 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         else k_bin_scatter<2><<<pblocks, 256, 0, bs>>>(B);
         count_launch(3);
     }
+    if (g.deterministic) {
+        static std::atomic<unsigned long long> det_devs{0};
+        const unsigned long long dbit = 1ull << (g.device & 63);
+        if (!(det_devs.load() & dbit)) {
+            TGCU_CUDA(cudaFuncSetAttribute(k_bin_sort_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(sizeof(float4) * kDetSortCap)));
+            det_devs.fetch_or(dbit);
+        }
+        k_bin_sort_small<<<(unsigned)g.NB, 256, 0, bs>>>(g.binned[k], off, (int)g.NB, ch);
+        k_bin_sort_heavy<<<(unsigned)std::min<int64_t>(g.NB, 148 * 3), 1024, sizeof(float4) * kDetSortCap, bs>>>(
+            g.binned[k], off, ord, (int)g.NB, g.st);
+        count_launch(2);
+    }
     TGCU_CUDA(cudaGetLastError());
     if (in.consumed) TGCU_CUDA(cudaEventRecord(in.consumed, bs));
     TGCU_CUDA(cudaEventRecord(g.ev_bdone[k], bs));
@@ -1481,6 +1583,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     A.v_out = g.v[out_idx];
     A.binned = g.binned[k];
     A.off = off;
+    A.det = g.deterministic ? 1 : 0;
     for (int a = 0; a < 3; ++a) A.nb[a] = g.nb[a];
     A.L.k = cfg.k;
     A.L.inv_n = 1.0 / (double)n_norm;  // the global batch size (slab ranks may read a subset)

@@ -20,6 +20,8 @@ CONFIGS = {
     "c1": dict(res=128, points=1 << 16, near=0.0, sigma=0.01, lr=1e-2, dim=2),
     "c3": dict(res=256, points=1 << 21, near=0.5, sigma=0.01, lr=1e-2),
     "c5": dict(res=512, points=1 << 23, near=0.9, sigma=0.005, lr=5e-3),
+    # C2 in deterministic mode (tgcu_grid_set_deterministic): the cost of bit-reproducibility
+    "c2det": dict(res=128, points=1 << 20, near=0.5, sigma=0.01, lr=1e-2, det=True, shape="sphere"),
 }
 
 
@@ -48,7 +50,11 @@ def run(name, steps, warmup):
     spec = tg.GridSpec(dim=dim, resolution=(res,) * dim + ((1,) if dim == 2 else ()), order=2)
     g = tg.init_grid(spec, tg.InitOptions(memory_cap_bytes=1 << 40))
     g.adam_reset(tg.AdamConfig(lr=cfg["lr"]))
-    if dim == 2:  # C1: circle r=0.5 union box, uniform points (sampling.cpp C1 restatement)
+    g.set_deterministic(cfg.get("det", False))
+    if cfg.get("shape") == "sphere":
+        host = [tg.sample(tg.SHAPE_SPHERE, 3, 1000 + i, cfg["points"], near_frac=0.5, sigma=0.01, param0=0.6)
+                for i in range(2)]
+    elif dim == 2:  # C1: circle r=0.5 union box, uniform points (sampling.cpp C1 restatement)
         host = [tg.sample(tg.SHAPE_C1_2D, 2, 500 + i, cfg["points"]) for i in range(2)]
     else:
         host = [tg.sample(tg.SHAPE_PRIMS, 3, 500 + i, cfg["points"], near_frac=cfg["near"], sigma=cfg["sigma"],
@@ -81,7 +87,7 @@ def run(name, steps, warmup):
         peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"]
     except Exception:
         pass
-    return {"config": name, "grid": [res] * dim, "order": 2, "points_per_step": N, "near_frac": cfg["near"],
+    return {"config": name, "deterministic": bool(cfg.get("det", False)), "grid": [res] * dim, "order": 2, "points_per_step": N, "near_frac": cfg["near"],
             "sigma": cfg["sigma"], "ms_per_step": ms, "points_per_s": N / (ms * 1e-3),
             "brick_kernel_ms": kms / max(kn, 1), "survey_bytes_per_step": bt,
             "step_frac_survey_bytes": bt / (ms * 1e-3) / 1e9 / peak,
