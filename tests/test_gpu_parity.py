@@ -695,3 +695,28 @@ def test_fused_step_random_configs(oracle, seed):
     p1 = c - lr * gref / (np.abs(gref) + 1e-8)
     ok = np.abs(gref) > 1e-3 * (np.abs(gref).max() + 1e-30)
     assert_close(g.coeffs[ok], p1[ok], 1e-6, floor=1.0, what="params after step")
+
+
+def test_wide_2d_grid_brick_codes(oracle):
+    """A 2D grid with 513 bricks along x (res_x 8200 > 512 bricks of 16
+    vertices; the binning's brick code gives each axis as many bits as the
+    grid needs): fused step vs the oracle, points in every brick column."""
+    res = (8200, 20)
+    s = ospec(2, res, 2)
+    rng = np.random.default_rng(31)
+    c = (0.05 * rng.standard_normal(s.V * s.K)).astype(np.float32).astype(np.float64)
+    n = 60000
+    pts = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    pts[:2000, 0] = np.linspace(0.999, 1.0, 2000, dtype=np.float32)  # the last brick columns
+    pts[:, 2] = 0.0
+    gt = (np.linalg.norm(pts[:, :2], axis=1) - 0.5).astype(np.float32)
+    smp = np.concatenate([pts, gt[:, None]], 1).astype(np.float64)
+    gref = np.zeros(s.V * s.K)
+    tref = oracle.total_loss(s, c, smp, Loss(), gref)
+    mass = oracle.total_loss_mass(s, c, smp, Loss())
+    g = tg.init_grid(gspec(2, res, 2))
+    g.coeffs = c
+    g.adam_reset(tg.AdamConfig(lr=1e-2))
+    t = tg.train_step(g, smp, tg.LossConfig(), export_grad=True)
+    assert_close(t.as_array(), tref, 1e-6, floor=1e-30, what="terms")
+    grad_close(g.grad(), gref, mass, what="wide 2D grad")

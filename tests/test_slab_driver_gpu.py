@@ -84,3 +84,29 @@ def test_slab_trainer_two_ranks_match_single_grid(tmp_path, fused):
     for r in range(2):
         t = np.load(tmp_path / f"terms{r}.npy")
         assert np.all(np.abs(t - ref) <= 1e-6 * np.abs(ref) + 1e-30)
+
+
+def test_slab_trainer_nccl_single_rank_matches_single_grid():
+    """The NCCL backend of libtgcu's communicator (dlopen'ed libnccl, unique
+    id over the TCP star, all-reduce of the partials on the step's stream) on
+    the one GPU here: a one-rank job whose slab is the whole grid reproduces
+    the single-grid trajectory bit for bit in the loss terms."""
+    import paper_2402_14415_b200 as tg
+    from paper_2402_14415_b200.slab import Comm, SlabTrainer
+    spec = tg.GridSpec(dim=3, resolution=RES, order=2)
+    init = tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.02, seed=11)
+    comm = Comm(0, 1, device=0, addr="127.0.0.1", port=_port(), backend="nccl")
+    tr = SlabTrainer(spec, 0, 1, tg.AdamConfig(lr=1e-2), device=0, opts=init, comm=comm)
+    assert tr.backend == "nccl" and not tr.fused_halo
+    g = tg.init_grid(spec, init)
+    g.adam_reset(tg.AdamConfig(lr=1e-2))
+    for b in _batches():
+        t_slab = tr.step(b, tg.LossConfig(), want_terms=True).as_array()
+        t_full = tg.train_step(g, b).as_array()
+        assert np.allclose(t_slab, t_full, rtol=1e-6, atol=1e-30)
+    for b in _batches():  # stream-ordered steps (no host sync per step)
+        tr.step(b, tg.LossConfig())
+        tg.train_step(g, b, asynchronous=True)
+    assert np.allclose(tr.slab.sync().as_array(), g.sync().as_array(), rtol=1e-6, atol=1e-30)
+    assert_trajectory_close(tr.slab.owned_coeffs(), g.coeffs, 1e-2, 2 * STEPS, what="nccl slab vs grid")
+    tr.close()
