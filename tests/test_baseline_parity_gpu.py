@@ -156,3 +156,30 @@ def test_c4_512_query_values_vs_oracle(oracle, order):
     inv = torch.empty_like(perm)
     inv[perm] = torch.arange(n, device="cuda")
     assert torch.equal(vs[inv], vals)
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c5"])
+def test_c3_c5_fused_step_vs_oracle(oracle, cfg):
+    """BASELINE configs[2] / [4] shapes: the 64-primitive procedural target on
+    256^3 (2^21 points, 50 % near-surface sigma 0.01) and on 512^3 (90 %
+    near-surface sigma 0.005; 2^20 of the 2^23 points per step, to bound the
+    fp64 oracle's time), on a random (non-zero) grid so every term is active:
+    one fused step's loss terms and full gradient vs the oracle."""
+    from test_gpu_parity import grad_close
+    res, n, near, sigma = ((256,) * 3, 1 << 21, 0.5, 0.01) if cfg == "c3" else ((512,) * 3, 1 << 20, 0.9, 0.005)
+    s = Spec(dim=3, res=res, order=2)
+    g = tg.init_grid(tg.GridSpec(dim=3, resolution=res, order=2),
+                     tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.01, seed=21, memory_cap_bytes=1 << 40))
+    g.adam_reset(tg.AdamConfig(lr=1e-2))
+    c64 = g.coeffs_f32().astype(np.float64)
+    smp = tg.sample(tg.SHAPE_PRIMS, 3, 4100, n, near_frac=near, sigma=sigma, param0=42)
+    t = tg.train_step(g, smp, tg.LossConfig(), export_grad=True)
+    gpu_grad = g.grad()
+    g.close()
+    s64 = smp.astype(np.float64)
+    gref = np.zeros(s.V * s.K)
+    tref = oracle.total_loss(s, c64, s64, Loss(), gref)
+    curve_close(t.as_array()[None], tref[None], 1e-6, f"{cfg} loss terms")
+    mass = oracle.total_loss_mass(s, c64, s64, Loss())
+    del c64
+    grad_close(gpu_grad, gref, mass, what=f"{cfg} fused grad")
