@@ -339,6 +339,7 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         st0.nan_point = ULLONG_MAX;
         st0.bad_grad = ULLONG_MAX;
         st0.nan_bin[0] = st0.nan_bin[1] = ULLONG_MAX;
+        st0.det_over[0] = st0.det_over[1] = ULLONG_MAX;
         TGCU_CUDA(cudaMemcpy(g.st, &st0, sizeof(Status), cudaMemcpyHostToDevice));
         // Brick decomposition (train.cu / query.cu).
         if (const char* det = std::getenv("TGCU_DETERMINISTIC")) g.deterministic = det[0] == '1';
@@ -510,6 +511,7 @@ static void raise_sticky(Grid& g) {
     clean.nan_point = ULLONG_MAX;
     clean.bad_grad = ULLONG_MAX;
     clean.nan_bin[0] = clean.nan_bin[1] = ULLONG_MAX;
+    clean.det_over[0] = clean.det_over[1] = ULLONG_MAX;
     TGCU_CUDA(cudaMemcpy(g.st, &clean, sizeof(Status), cudaMemcpyHostToDevice));
     g.steps_launched = 0;
     throw Error(s.error, msg);

@@ -46,6 +46,8 @@ struct Status {
     unsigned long long overflow;    // bin overflow flag
     unsigned long long nan_bin[2];  // fused step: min NaN sample index found by the
                                     // binning of bin set k (ULLONG_MAX = none)
+    unsigned long long det_over[2]; // deterministic mode: min brick of bin set k too large
+                                    // for the canonical-order sort (ULLONG_MAX = none)
 };
 
 // t = x / h correctly rounded via Markstein's final-correction step with a

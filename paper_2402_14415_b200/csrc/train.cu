@@ -34,10 +34,14 @@
 
 #include <atomic>
 #include <climits>
+#include <cstdlib>
 
 #include "dispatch.cuh"
 #include "tg_internal.h"
 #include "tma.cuh"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace tgcu {
 
@@ -382,6 +386,7 @@ struct FinArgs {
     int use_tv, want_eik;
     Status* st;
     unsigned long long* nan;  // NaN slot of the step's bin set
+    unsigned long long* over; // deterministic-sort overflow slot of the step's bin set
     tgcu_loss_terms* trace;
     long long step;
     int in_idx;
@@ -437,6 +442,7 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
         return;
     }
     const unsigned long long nanp = *F.nan;
+    const unsigned long long over = *F.over;
     const bool any_nan = nanp != ULLONG_MAX || (F.reduced && F.reduced[3] > 0.0);
     const bool any_bad = st->bad_grad != ULLONG_MAX || (F.reduced && F.reduced[4] > 0.0);
     tgcu_loss_terms t;
@@ -451,6 +457,10 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
         err = TGCU_ERR_INVALID_ARGUMENT;
         kind = 1;
         idx = nanp != ULLONG_MAX ? (long long)nanp : -1;
+    } else if (over != ULLONG_MAX) {
+        err = TGCU_ERR_CONFIG;
+        kind = 4;
+        idx = (long long)over;
     } else if (!isfinite(t.total)) {
         err = TGCU_ERR_NUMERICAL;
         kind = 2;
@@ -471,6 +481,7 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
         st->good_t = F.t_after;
     }
     *F.nan = ULLONG_MAX;
+    *F.over = ULLONG_MAX;
     st->bad_grad = ULLONG_MAX;
 }
 
@@ -506,6 +517,7 @@ struct StepArgs {
     int peer_hi_zb, peer_hi_lz;
     const int* order;  // launch order of the bricks (1D grid): most chunks first
     int det;           // deterministic mode: canonical record order inside every cell run
+    int split;         // CTAs per brick (a thread-block cluster along x; 1 = one CTA per brick)
 };
 
 // Cell runs of a chunk's records: every cell gets the contiguous slot range
@@ -679,11 +691,21 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     // brick index and its point range, loaded together with the error flag
     // brick of this CTA: the launch order puts the multi-chunk bricks first so
     // the kernel does not end on a long surface brick
-    const int b = A.order[blockIdx.x];
+    // Split bricks (grids with fewer bricks than CTA slots, e.g. C1): a
+    // cluster of SPL CTAs shares one brick; CTA r takes the brick's chunks r,
+    // r + SPL, ..., and the per-vertex sums of the others reach rank 0 over
+    // distributed shared memory, which then runs TV + Adam alone.
+    const int SPL = A.split;
+    const int crank = SPL > 1 ? (int)cg::this_cluster().block_rank() : 0;
+    const int b = A.order[blockIdx.x / SPL];
     const int bcx = b % A.nb[0], bcy = (b / A.nb[0]) % A.nb[1], bcz = b / (A.nb[0] * A.nb[1]);
     const int err = A.st->error;
     const int p0 = A.off[b], p1 = A.off[b + 1];
+    // (st->error is written only by the finalize of an earlier step, ordered
+    // before this kernel: every CTA of a split cluster sees the same value)
     if (err) return;
+    const int pfirst = p0 + crank * CH;                  // this CTA's first chunk
+    const int nmine = pfirst < p1 ? (p1 - pfirst + SPL * CH - 1) / (SPL * CH) : 0;
 
     extern __shared__ __align__(128) float smem[];
     float* tile = smem;                           // current parameters + halo
@@ -696,6 +718,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     int* bstart = bhist + 64;
     __shared__ int run_total;
     __shared__ double red[4][NT / 32];
+    __shared__ double xsum[3];  // split clusters: this CTA's recon, eik, home-point sums
     __shared__ __align__(8) unsigned long long bars[2];  // tile, mv
 
     const int tid = threadIdx.x;
@@ -724,17 +747,23 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     if (tmap) {
         // one elected thread: the (B+2)^D tile (out-of-grid vertices zero
         // filled) and the owned m, v boxes, each one TMA tensor copy
-        if (tid == 0) {
+        // (split clusters: the tile only where there are points or TV to do,
+        // m and v only in rank 0, which alone runs TV + Adam)
+        if (tid == 0 && (crank == 0 || nmine > 0)) {
             mbar_expect_tx(&bars[0], L::tile_box_bytes);
-            mbar_expect_tx(&bars[1], 2 * L::own_box_bytes);
+            if (crank == 0) mbar_expect_tx(&bars[1], 2 * L::own_box_bytes);
             if constexpr (DIM == 3) {
                 tma_load_3d(tile, &A.tm_tile, &bars[0], (o[0] - 1) * K - L::SHF, o[1] - 1, zrel - 1);
-                tma_load_3d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1], zrel);
-                tma_load_3d(mvs + S::NOWN * K, &A.tm_v_in, &bars[1], o[0] * K, o[1], zrel);
+                if (crank == 0) {
+                    tma_load_3d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1], zrel);
+                    tma_load_3d(mvs + S::NOWN * K, &A.tm_v_in, &bars[1], o[0] * K, o[1], zrel);
+                }
             } else {
                 tma_load_2d(tile, &A.tm_tile, &bars[0], (o[0] - 1) * K - L::SHF, o[1] - 1);
-                tma_load_2d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1]);
-                tma_load_2d(mvs + S::NOWN * K, &A.tm_v_in, &bars[1], o[0] * K, o[1]);
+                if (crank == 0) {
+                    tma_load_2d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1]);
+                    tma_load_2d(mvs + S::NOWN * K, &A.tm_v_in, &bars[1], o[0] * K, o[1]);
+                }
             }
         }
     } else {
@@ -771,11 +800,11 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     // stay in point order with each point's cell in start[]; every vertex
     // scans the few points for its incident cells (3 barriers instead of 8).
     const bool tiny = TINYOK && (p1 - p0) <= kTiny;
-    for (int base = p0; base < p1; base += CH) {
+    for (int base = pfirst; base < p1; base += SPL * CH) {
         const int m = min(CH, p1 - base);
         if (!tiny) {
             for (int i = tid; i < S::NCELL; i += NT) cnt[i] = 0;
-            if (base == p0 && tid < 64) bhist[tid] = 0;
+            if (base == pfirst && tid < 64) bhist[tid] = 0;
             if (tid == 0) run_total = 0;
             __syncthreads();
         }
@@ -836,14 +865,14 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         if (tid == 0) pt_scan += pt_x - pt_s0;
         const unsigned long long pt_b0 = pt_x;
 #endif
-        if (base == p0 && tiny) {
+        if (base == pfirst && tiny) {
             cp_async_wait<0>();
             if (warp == 0) mbar_wait(&bars[0], 0);
             __syncthreads();  // tile and the points' cells (start[]) visible
 #ifdef TGCU_PHASE_TIMING
             TGCU_PT_SET(pt_tile)
 #endif
-        } else if (base == p0 && p1 - p0 <= CH) {
+        } else if (base == pfirst && nmine == 1) {
             // single-chunk brick: identity mapping, just the tile wait
             cp_async_wait<0>();
             if (warp == 0) mbar_wait(&bars[0], 0);
@@ -851,7 +880,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
 #ifdef TGCU_PHASE_TIMING
             TGCU_PT_SET(pt_tile)
 #endif
-        } else if (base == p0) {
+        } else if (base == pfirst) {
             // Load balance: sort the owned vertices by their (first-chunk)
             // workload into 64 buckets so a warp's lanes carry similar loads;
             // the mapping then holds for the brick (points are in random order).
@@ -1094,8 +1123,39 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     if constexpr (PACKED) unpack_p2(P, G);
 #pragma unroll
     for (int q = 0; q < K; ++q) Gs[myv * K + q] = G[q];
+    double xtot[3] = {0.0, 0.0, 0.0};  // split: the other CTAs' loss sums (rank 0, thread 0)
+    if (SPL > 1) {
+        // this CTA's loss sums (fixed-order block reduction) for rank 0
+        {
+            const double v3[3] = {warp_sum_d(recon_sum), warp_sum_d(eik_sum), warp_sum_d((double)home_pts)};
+            if (lane == 0)
+                for (int k2 = 0; k2 < 3; ++k2) red[k2][warp] = v3[k2];
+            __syncthreads();
+            if (tid < 3) {
+                double acc = 0.0;
+                for (int k2 = 0; k2 < NW; ++k2) acc += red[tid][k2];
+                xsum[tid] = acc;
+            }
+        }
+        cg::cluster_group cl = cg::this_cluster();
+        cl.sync();  // every CTA's per-vertex sums (Gs) and loss sums are in place
+        if (crank == 0) {
+            // rank order: the same sums every run
+            for (int r = 1; r < SPL; ++r) {
+                const float* rg = cl.map_shared_rank(Gs, r);
+#pragma unroll
+                for (int q = 0; q < K; ++q) Gs[tid * K + q] += rg[tid * K + q];
+                if (tid == 0) {
+                    const double* rx = cl.map_shared_rank(xsum, r);
+                    for (int k2 = 0; k2 < 3; ++k2) xtot[k2] += rx[k2];
+                }
+            }
+        }
+        cl.sync();  // rank 0 has read the others' shared memory
+        if (crank != 0) return;
+    }
     cp_async_wait<0>();
-    if (p0 == p1 && warp == 0) mbar_wait(&bars[0], 0);  // brick without points: tile not yet waited for
+    if (nmine == 0 && warp == 0) mbar_wait(&bars[0], 0);  // brick without points: tile not yet waited for
     if (warp == 0) mbar_wait(&bars[1], 0);  // m/v rows landed
     __syncthreads();
     TGCU_PT(pt_e1)
@@ -1281,6 +1341,14 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             for (int k2 = 0; k2 < NW; ++k2) acc += red[tid][k2];
             A.partials[4 * b + tid] = acc;
         }
+        if (SPL > 1) {  // the other CTAs' recon, eik and home-point sums (thread 0 holds them)
+            __syncthreads();
+            if (tid == 0) {
+                A.partials[4 * b + 0] += xtot[0];
+                A.partials[4 * b + 1] += xtot[1];
+                A.partials[4 * b + 3] += xtot[2];
+            }
+        }
     }
 #ifdef TGCU_PHASE_TIMING
     if (tid == 0) {
@@ -1388,6 +1456,7 @@ void launch_slab_finish(Grid& g, const double* reduced, const tgcu_loss_config& 
     F.want_eik = cfg.lambda1 > 0.0;
     F.st = g.st;
     F.nan = &g.st->nan_bin[g.slab_set];
+    F.over = &g.st->det_over[g.slab_set];
     F.trace = g.d_trace;
     F.step = step;
     F.in_idx = in_idx;
@@ -1448,17 +1517,15 @@ __global__ void __launch_bounds__(256) k_bin_sort_small(float4* __restrict__ bin
     sort_run(binned, p0, n, rs);
 }
 __global__ void __launch_bounds__(1024) k_bin_sort_heavy(float4* __restrict__ binned, const int* __restrict__ off,
-                                                        const int* __restrict__ ord, int NB, Status* st) {
+                                                        const int* __restrict__ ord, int NB,
+                                                        unsigned long long* __restrict__ over) {
     extern __shared__ float4 rh[];
     const int nh = ord[NB];
     for (int i = blockIdx.x; i < nh; i += gridDim.x) {
         const int b = ord[i];
         const int p0 = off[b], n = off[b + 1] - p0;
-        if (n > kDetSortCap) {
-            if (threadIdx.x == 0 && atomicCAS(&st->error, 0, TGCU_ERR_CONFIG) == 0) {
-                st->error_kind = 4;
-                st->error_index = b;
-            }
+        if (n > kDetSortCap) {  // reported by this step's finalize (like a NaN sample)
+            if (threadIdx.x == 0) atomicMin(over, (unsigned long long)b);
             continue;
         }
         sort_run(binned, p0, n, rh);
@@ -1564,7 +1631,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         }
         k_bin_sort_small<<<(unsigned)g.NB, 256, 0, bs>>>(g.binned[k], off, (int)g.NB, ch);
         k_bin_sort_heavy<<<(unsigned)std::min<int64_t>(g.NB, 148 * 3), 1024, sizeof(float4) * kDetSortCap, bs>>>(
-            g.binned[k], off, ord, (int)g.NB, g.st);
+            g.binned[k], off, ord, (int)g.NB, &g.st->det_over[k]);
         count_launch(2);
     }
     TGCU_CUDA(cudaGetLastError());
@@ -1627,6 +1694,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     F.want_eik = eik;
     F.st = g.st;
     F.nan = &g.st->nan_bin[k];
+    F.over = &g.st->det_over[k];
     F.trace = g.d_trace;
     F.step = step;
     F.in_idx = in_idx;
@@ -1644,7 +1712,18 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         A.tm_m_out = g.tm_own_m[out_idx];
         A.tm_v_out = g.tm_own_v[out_idx];
     }
-    const dim3 bgrid((unsigned)g.NB);
+    // Split bricks over a cluster of CTAs when the grid has fewer bricks than
+    // CTA slots (2 per SM): the largest power of two <= 8 that still fits.
+    int split = 1;
+    if (A.use_tmap) {
+        static int sms = 0;
+        if (!sms) TGCU_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g.device));
+        const char* ev = std::getenv("TGCU_SPLIT");
+        const int cap = ev ? std::max(1, std::min(8, std::atoi(ev))) : 8;
+        while (split * 2 <= cap && g.NB * (int64_t)split * 2 <= 2LL * sms) split *= 2;
+    }
+    A.split = split;
+    const dim3 bgrid((unsigned)(g.NB * split));
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
         constexpr size_t smem = BrickSmem<DIM, ORDER>::bytes;
         static_assert(BrickSmem<DIM, ORDER>::bytes <= 227 * 1024, "brick smem");
@@ -1670,7 +1749,23 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         g.prof_this = g.prof_on && (g.steps_launched % g.prof_every) == 0;
         if (g.prof_this) prof_mark(g, s, 0);
         if (g.bd_on) bd_mark(g, s, 3);
-        kern<<<bgrid, BrickShape<DIM>::NT, smem, s>>>(A);
+        if (split > 1) {
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = bgrid;
+            lc.blockDim = dim3(BrickShape<DIM>::NT);
+            lc.dynamicSmemBytes = smem;
+            lc.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)split;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            TGCU_CUDA(cudaLaunchKernelEx(&lc, kern, A));
+        } else {
+            kern<<<bgrid, BrickShape<DIM>::NT, smem, s>>>(A);
+        }
         TGCU_CUDA(cudaEventRecord(g.ev_bfree[k], s));
         if (g.bd_on) bd_mark(g, s, 4);
         if (g.prof_this) prof_mark(g, s, 1);
