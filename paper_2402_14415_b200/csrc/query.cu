@@ -798,6 +798,87 @@ __global__ void __launch_bounds__(kQpThreads) k_qp_scatter(QpArgs A) {
     }
 }
 
+// Sort only: each brick's points in Morton cell order (warp per brick, in
+// chunks of 256 staged in shared memory for a coalesced write-out: shared-memory cell counts, ranks, a warp scan), written as
+// the sorted coordinates + source indices. Consecutive points of a brick then
+// share corner blocks, which the brick-tile query reads with fewer
+// shared-memory bank conflicts. The cell comes from fp32 coordinates: it only
+// orders points inside their (exactly binned) brick.
+template <int DIM, int LB>
+__global__ void __launch_bounds__(128) k_qp_cellsort(QpArgs A, const float4* __restrict__ C, int nbricks) {
+    constexpr int NCELLB = 1 << (DIM * LB);
+    constexpr int PER = NCELLB / 32;
+    constexpr int CHK = 256;  // records per warp pass (8 per lane)
+    __shared__ int cnt[4][NCELLB];
+    __shared__ float4 stage[4][CHK];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * 4 + w;
+    if (b >= nbricks) return;
+    const long long p0 = A.off[b], p1 = A.off[b + 1];
+    int* ct = cnt[w];
+    float4* st = stage[w];
+    for (long long c0 = p0; c0 < p1; c0 += CHK) {
+        const int m = (int)min((long long)CHK, p1 - c0);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) ct[lane * PER + k] = 0;
+        __syncwarp();
+        float4 rec[CHK / 32];
+        int cc[CHK / 32], rk[CHK / 32];
+#pragma unroll
+        for (int k = 0; k < CHK / 32; ++k) {
+            const int j = lane + 32 * k;
+            cc[k] = -1;
+            if (j < m) {
+                rec[k] = C[c0 + j];
+                const float p[3] = {rec[k].x, rec[k].y, rec[k].z};
+                unsigned int l[3] = {0, 0, 0};
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    const float tf = (p[a] - (float)A.s.origin[a]) * A.s.inv_hf[a];
+                    int ci = tf >= 0.0f ? (int)tf : 0;  // NaN -> 0
+                    ci = min(ci, A.s.res[a] - 2);
+                    l[a] = (unsigned int)ci & ((1u << LB) - 1u);
+                }
+                cc[k] = DIM == 3 ? (int)(spread3_10(l[0]) | (spread3_10(l[1]) << 1) | (spread3_10(l[2]) << 2))
+                                 : (int)(spread2(l[0]) | (spread2(l[1]) << 1));
+                rk[k] = atomicAdd(&ct[cc[k]], 1);
+            }
+        }
+        __syncwarp();
+        int loc = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) loc += ct[lane * PER + k];
+        int x = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        int run = x - loc;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int v = ct[lane * PER + k];
+            ct[lane * PER + k] = run;
+            run += v;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < CHK / 32; ++k)
+            if (cc[k] >= 0) st[ct[cc[k]] + rk[k]] = rec[k];
+        __syncwarp();
+        // coalesced write-out of the chunk in cell order
+        for (int j = lane; j < m; j += 32) {
+            const float4 q = st[j];
+            const long long pos = c0 + j;
+            A.out_xyz[3 * pos] = q.x;
+            A.out_xyz[3 * pos + 1] = q.y;
+            A.out_xyz[3 * pos + 2] = q.z;
+            if (A.perm) A.perm[pos] = (long long)(unsigned int)__float_as_int(q.w);
+        }
+        __syncwarp();
+    }
+}
+
 // Runs both passes. B != null: records (x, y, z, index) grouped by brick;
 // else sorted xyz (+ perm). off: 2^KB + 1 brick offsets.
 void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xyz, int64_t* perm,
@@ -833,7 +914,10 @@ void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xy
     A.H2 = reinterpret_cast<int*>(q); q += bH2;
     A.A = reinterpret_cast<float4*>(q);
     A.off = off;
-    A.B = B;
+    // the sort writes pass 2's records to C, then orders each brick by cell
+    float4* C = nullptr;
+    if (!B) TGCU_CUDA(cudaMallocAsync(&C, sizeof(float4) * (size_t)std::max<int64_t>(n, 1), s));
+    A.B = B ? B : C;
     A.out_xyz = out_xyz;
     A.perm = reinterpret_cast<long long*>(perm);
     A.vals = vals;
@@ -858,6 +942,13 @@ void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xy
     else
         run(k_qp_hist<2, 4, 1>, k_qp_scatter<2, 4, 1>, k_qp_hist<2, 4, 2>, k_qp_scatter<2, 4, 2>);
     count_launch(8);
+    if (C) {
+        const int nbr = (int)codes;
+        if (g.spec.dim == 3) k_qp_cellsort<3, 3><<<(nbr + 3) / 4, 128, 0, s>>>(A, C, nbr);
+        else k_qp_cellsort<2, 4><<<(nbr + 3) / 4, 128, 0, s>>>(A, C, nbr);
+        count_launch();
+        TGCU_CUDA(cudaFreeAsync(C, s));
+    }
     TGCU_CUDA(cudaFreeAsync(scratch, s));
     TGCU_CUDA(cudaGetLastError());
 }

@@ -681,7 +681,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // average, e.g. C5): its branches cost the dense C2 step ~1.4 %.
 constexpr int kTiny = 32;
 
-template <int DIM, int ORDER, bool EIK, bool EXPORT, bool TINYOK>
+template <int DIM, int ORDER, bool EIK, bool EXPORT, bool TINYOK, bool SPLIT = false>
 __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __grid_constant__ StepArgs A) {
     using S = BrickShape<DIM>;
     using L = BrickSmem<DIM, ORDER>;
@@ -695,8 +695,10 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     // cluster of SPL CTAs shares one brick; CTA r takes the brick's chunks r,
     // r + SPL, ..., and the per-vertex sums of the others reach rank 0 over
     // distributed shared memory, which then runs TV + Adam alone.
-    const int SPL = A.split;
-    const int crank = SPL > 1 ? (int)cg::this_cluster().block_rank() : 0;
+    // (a separate instantiation, SPLIT, so the unsplit kernel carries none of it)
+    const int SPL = SPLIT ? A.split : 1;
+    int crank = 0;
+    if constexpr (SPLIT) crank = (int)cg::this_cluster().block_rank();
     const int b = A.order[blockIdx.x / SPL];
     const int bcx = b % A.nb[0], bcy = (b / A.nb[0]) % A.nb[1], bcz = b / (A.nb[0] * A.nb[1]);
     const int err = A.st->error;
@@ -800,6 +802,8 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     // stay in point order with each point's cell in start[]; every vertex
     // scans the few points for its incident cells (3 barriers instead of 8).
     const bool tiny = TINYOK && (p1 - p0) <= kTiny;
+    // one chunk (or none) and no split: thread tid owns vertex tid throughout
+    const bool ident = !SPLIT && (tiny || nmine <= 1);
     for (int base = pfirst; base < p1; base += SPL * CH) {
         const int m = min(CH, p1 - base);
         if (!tiny) {
@@ -855,6 +859,11 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         if (!tiny) {
             __syncthreads();
             cell_runs<S::NCELL, NT>(cnt, start, &run_total);
+            if (base == pfirst && nmine == 1) {
+                // single-chunk brick: the tile wait rides on this barrier
+                cp_async_wait<0>();
+                if (warp == 0) mbar_wait(&bars[0], 0);
+            }
             __syncthreads();
         }
 #ifdef TGCU_PHASE_TIMING
@@ -873,10 +882,8 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             TGCU_PT_SET(pt_tile)
 #endif
         } else if (base == pfirst && nmine == 1) {
-            // single-chunk brick: identity mapping, just the tile wait
-            cp_async_wait<0>();
-            if (warp == 0) mbar_wait(&bars[0], 0);
-            __syncthreads();
+            // single-chunk brick: identity mapping; the tile was waited for
+            // with the cell runs
 #ifdef TGCU_PHASE_TIMING
             TGCU_PT_SET(pt_tile)
 #endif
@@ -1110,7 +1117,9 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                 ++j;
             }
         }
-        __syncthreads();
+        // (a brick of one chunk keeps its sums in registers for TV + Adam: its
+        // records are released by the m/v barrier below instead)
+        if (!ident) __syncthreads();
 #ifdef TGCU_PHASE_TIMING
         TGCU_PT_SET(pt_x)
         if (tid == 0) pt_2b += pt_x - pt_g0;
@@ -1121,10 +1130,12 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     // ---- 3. TV + Adam, thread per vertex; results staged in place ----
     float* Gs = uni;
     if constexpr (PACKED) unpack_p2(P, G);
+    if (!ident) {
 #pragma unroll
-    for (int q = 0; q < K; ++q) Gs[myv * K + q] = G[q];
+        for (int q = 0; q < K; ++q) Gs[myv * K + q] = G[q];
+    }
     double xtot[3] = {0.0, 0.0, 0.0};  // split: the other CTAs' loss sums (rank 0, thread 0)
-    if (SPL > 1) {
+    if constexpr (SPLIT) {
         // this CTA's loss sums (fixed-order block reduction) for rank 0
         {
             const double v3[3] = {warp_sum_d(recon_sum), warp_sum_d(eik_sum), warp_sum_d((double)home_pts)};
@@ -1153,6 +1164,8 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         }
         cl.sync();  // rank 0 has read the others' shared memory
         if (crank != 0) return;
+        if (tid == 0)
+            for (int k2 = 0; k2 < 3; ++k2) xsum[k2] = xtot[k2];  // for the final partials (barriers follow)
     }
     cp_async_wait<0>();
     if (nmine == 0 && warp == 0) mbar_wait(&bars[0], 0);  // brick without points: tile not yet waited for
@@ -1206,7 +1219,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                             gt = __fadd2_rn(gt, __fadd2_rn(pv, make_float2(-pl.x, -pl.y)));
                         }
                     }
-                    return __ffma2_rn(gsc, gt, *reinterpret_cast<const float2*>(gs + q));
+                    return __ffma2_rn(gsc, gt, ident ? make_float2(G[q], G[q + 1]) : *reinterpret_cast<const float2*>(gs + q));
                 };
                 // one finiteness test per vertex (a NaN / inf in any channel
                 // makes the sum non-finite); the channel scan runs only then
@@ -1253,7 +1266,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                         }
                         if (lo[a]) gt += pv - tp[q - offs[a]];
                     }
-                    const float gi = fmaf(A.tv_gscale, gt, gs[q]);
+                    const float gi = fmaf(A.tv_gscale, gt, ident ? G[q] : gs[q]);
                     if constexpr (EXPORT) A.grad_out[gidx + q] = gi;
                     if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
                     const float mn = fmaf(A.b1, mm[q], c1 * gi);
@@ -1266,11 +1279,11 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             }
         }
     }
-    __syncthreads();
     TGCU_PT(pt_e2)
     // copy-out of the staged results (p from Gs, m and v from mvs): three TMA
     // tensor box stores (out-of-grid vertices dropped), or one bulk store per
-    // row and array, issued by one thread each
+    // row and array, issued by one thread each. Every thread makes its own
+    // shared-memory writes visible to the async proxy, then one barrier.
     fence_proxy_async_smem();
     __syncthreads();
     if constexpr (DIM == 3) {
@@ -1330,24 +1343,20 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         }
     }
 
-    // ---- per-brick loss partials (fixed-order block reduction) ----
+    // ---- per-brick loss partials (fixed-order block reduction; after the
+    // copy-out is issued, so the stores overlap it) ----
     {
-        const double v4[4] = {warp_sum_d(recon_sum), warp_sum_d(eik_sum), warp_sum_d(tv_sum), warp_sum_d((double)home_pts)};
+        const double v4[4] = {warp_sum_d(recon_sum), warp_sum_d(eik_sum), warp_sum_d(tv_sum),
+                              warp_sum_d((double)home_pts)};
         if (lane == 0)
             for (int k2 = 0; k2 < 4; ++k2) red[k2][warp] = v4[k2];
         __syncthreads();
         if (tid < 4) {
             double acc = 0.0;
             for (int k2 = 0; k2 < NW; ++k2) acc += red[tid][k2];
+            // split clusters: + the other CTAs' recon, eik, home-point sums
+            if (SPLIT && tid != 2) acc += xsum[tid == 3 ? 2 : tid];
             A.partials[4 * b + tid] = acc;
-        }
-        if (SPL > 1) {  // the other CTAs' recon, eik and home-point sums (thread 0 holds them)
-            __syncthreads();
-            if (tid == 0) {
-                A.partials[4 * b + 0] += xtot[0];
-                A.partials[4 * b + 1] += xtot[1];
-                A.partials[4 * b + 3] += xtot[2];
-            }
         }
     }
 #ifdef TGCU_PHASE_TIMING
@@ -1715,6 +1724,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     // Split bricks over a cluster of CTAs when the grid has fewer bricks than
     // CTA slots (2 per SM): the largest power of two <= 8 that still fits.
     int split = 1;
+#ifndef TGCU_SPLIT_OFF
     if (A.use_tmap) {
         static int sms = 0;
         if (!sms) TGCU_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g.device));
@@ -1722,6 +1732,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         const int cap = ev ? std::max(1, std::min(8, std::atoi(ev))) : 8;
         while (split * 2 <= cap && g.NB * (int64_t)split * 2 <= 2LL * sms) split *= 2;
     }
+#endif
     A.split = split;
     const dim3 bgrid((unsigned)(g.NB * split));
     TGCU_DISPATCH(g.spec.dim, g.spec.order, {
@@ -1736,13 +1747,21 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
                    : pick(k_brick_step<DIM, ORDER, false, true, true>, k_brick_step<DIM, ORDER, false, true, false>))
             : (eik ? pick(k_brick_step<DIM, ORDER, true, false, true>, k_brick_step<DIM, ORDER, true, false, false>)
                    : pick(k_brick_step<DIM, ORDER, false, false, true>, k_brick_step<DIM, ORDER, false, false, false>));
+        if (split > 1)  // the cluster variants (no tiny-brick path)
+            kern = grad_out ? (eik ? k_brick_step<DIM, ORDER, true, true, false, true>
+                                   : k_brick_step<DIM, ORDER, false, true, false, true>)
+                            : (eik ? k_brick_step<DIM, ORDER, true, false, false, true>
+                                   : k_brick_step<DIM, ORDER, false, false, false, true>);
         static std::atomic<unsigned long long> configured_devs{0};
         const unsigned long long cbit = 1ull << (g.device & 63);
         if (!(configured_devs.load() & cbit)) {
             for (auto k : {k_brick_step<DIM, ORDER, true, true, true>, k_brick_step<DIM, ORDER, false, true, true>,
                            k_brick_step<DIM, ORDER, true, false, true>, k_brick_step<DIM, ORDER, false, false, true>,
                            k_brick_step<DIM, ORDER, true, true, false>, k_brick_step<DIM, ORDER, false, true, false>,
-                           k_brick_step<DIM, ORDER, true, false, false>, k_brick_step<DIM, ORDER, false, false, false>})
+                           k_brick_step<DIM, ORDER, true, false, false>, k_brick_step<DIM, ORDER, false, false, false>,
+                           k_brick_step<DIM, ORDER, true, true, false, true>, k_brick_step<DIM, ORDER, false, true, false, true>,
+                           k_brick_step<DIM, ORDER, true, false, false, true>,
+                           k_brick_step<DIM, ORDER, false, false, false, true>})
                 TGCU_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             configured_devs.fetch_or(cbit);
         }
