@@ -1279,11 +1279,11 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             }
         }
     }
+    __syncthreads();
     TGCU_PT(pt_e2)
     // copy-out of the staged results (p from Gs, m and v from mvs): three TMA
     // tensor box stores (out-of-grid vertices dropped), or one bulk store per
-    // row and array, issued by one thread each. Every thread makes its own
-    // shared-memory writes visible to the async proxy, then one barrier.
+    // row and array, issued by one thread each
     fence_proxy_async_smem();
     __syncthreads();
     if constexpr (DIM == 3) {
