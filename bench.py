@@ -593,6 +593,7 @@ def main():
         torch.cuda.synchronize()
         launches = tg.launch_count() - l0
         brick_ms, brick_n = g.profile_end()
+        comm_prof = trainer.comm_profile() if trainer is not None else None
         last = g.sync()
         ms_total = max_over_ranks(ev0.elapsed_time(ev1), ws)
         ms_step = ms_total / args.steps
@@ -685,6 +686,15 @@ def main():
         line["halo"] = ("fused: boundary planes stored into the neighbours' halo by the brick kernel (peer memory)"
                         if getattr(trainer, "fused_halo", False) else "NCCL send/recv of the boundary planes")
         line["collectives"] = getattr(trainer, "backend", None)
+        # per-rank collective phase of the profiled steps: all-reduce of the
+        # loss partials and the halo exchange (0 when the brick kernel stores
+        # the planes into the neighbours), ms per step
+        import torch.distributed as dist
+        cp = [None] * ws
+        ar, hx, nst = comm_prof
+        dist.all_gather_object(cp, (ar / max(nst, 1), hx / max(nst, 1)))
+        line["per_rank_allreduce_ms"] = [c[0] for c in cp]
+        line["per_rank_halo_exchange_ms"] = [c[1] for c in cp]
         if single is not None:
             line["single_gpu"] = single
     if q is not None:

@@ -368,6 +368,12 @@ int tgcu_run_schedule(tgcu_grid** grid, const tgcu_stage* stages, int nstages, c
  * or on when the environment has TGCU_DETERMINISTIC=1 at grid creation. */
 int tgcu_grid_set_deterministic(tgcu_grid* g, int on);
 
+/* Collective phase of the profiled slab steps (those whose brick kernel
+ * tgcu_profile_begin / _every times): summed device ms of the all-reduce of
+ * the partials and of the halo exchange (0 with the fused peer-memory halo,
+ * whose stores run inside the brick kernel), and the number of steps. Resets. */
+int tgcu_slab_comm_profile(tgcu_grid* g, double* allreduce_ms, double* halo_ms, int* steps);
+
 /* Fused steps issued on this grid since creation or the last reported error;
  * error messages of a failed step name it as "step <this index at launch>". */
 int tgcu_grid_steps_launched(const tgcu_grid* g, int64_t* n);

@@ -171,6 +171,7 @@ def lib():
     L.tgcu_train_step_fresh_eik.argtypes = [P, P, C.c_int64, P, C.POINTER(_Loss), C.POINTER(_Terms), C.c_int, P]
     L.tgcu_shuffle_order.argtypes = [C.c_uint64, C.c_int64, P]
     L.tgcu_grid_set_deterministic.argtypes = [P, C.c_int]
+    L.tgcu_slab_comm_profile.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int)]
     L.tgcu_comm_create.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(P)]
     L.tgcu_comm_destroy.argtypes = [P]
     L.tgcu_comm_info.argtypes = [P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]

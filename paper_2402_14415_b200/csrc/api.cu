@@ -460,6 +460,7 @@ int tgcu_grid_destroy(tgcu_grid* h) {
     cudaFreeHost(g.h_ring);
     for (void* b : g.ipc_open) cudaIpcCloseMemHandle(b);
     for (auto e : g.prof_ev) cudaEventDestroy(e);
+    for (auto e : h->coll_ev) cudaEventDestroy(e);
     delete h;
     return TGCU_OK;
 }

@@ -492,6 +492,17 @@ int tgcu_slab_train_step(tgcu_grid* h, const float* samples, int64_t n, int64_t 
         double* part = nullptr;
         if (tgcu_slab_step_begin(h, samples, n, n_global, cfg, &part, flags & ~TGCU_ASYNC, stream) != TGCU_OK)
             throw Error(TGCU_ERR_INVALID_ARGUMENT, tgcu_last_error());
+        // profiled steps (tgcu_profile_begin): events around the collective phase
+        const bool prof = h->g.prof_on && h->g.prof_this;
+        auto mark = [&]() {
+            if (h->coll_used >= h->coll_ev.size()) {
+                cudaEvent_t e;
+                TGCU_CUDA(cudaEventCreate(&e));
+                h->coll_ev.push_back(e);
+            }
+            TGCU_CUDA(cudaEventRecord(h->coll_ev[h->coll_used++], s));
+        };
+        if (prof) mark();
         if (c->backend == TGCU_COMM_NCCL) {
             // in place on the step's stream: the finalize of every rank sees the same sums
             TGCU_NCCL(nccl().AllReduce(part, part, 5, ncclFloat64, ncclSum, c->nc, s));
@@ -502,11 +513,34 @@ int tgcu_slab_train_step(tgcu_grid* h, const float* samples, int64_t n, int64_t 
             c->allreduce_host(hp, 5, 0);
             TGCU_CUDA(cudaMemcpyAsync(part, hp, sizeof(hp), cudaMemcpyHostToDevice, s));
         }
+        if (prof) mark();  // (the finalize between the two phases is not counted)
         const int rc = tgcu_slab_step_finish(h, part, out, flags, stream);
         const std::string msg = rc == TGCU_OK ? std::string() : tgcu_last_error();
         // halo planes of the new parameters (the fused halo already stored them);
         // every rank reaches this point with the same commit decision
+        if (prof) mark();
         if (!h->fused_halo) halo_exchange(h, c, s);
+        if (prof) mark();
         if (rc != TGCU_OK) throw Error(rc, msg);
+    });
+}
+
+int tgcu_slab_comm_profile(tgcu_grid* h, double* allreduce_ms, double* halo_ms, int* steps) {
+    return guard([&] {
+        require(h != nullptr, "slab_comm_profile: NULL grid");
+        double ar = 0.0, hx = 0.0;
+        const size_t n = h->coll_used / 4;
+        for (size_t i = 0; i < n; ++i) {
+            float a = 0.f, b = 0.f;
+            TGCU_CUDA(cudaEventSynchronize(h->coll_ev[4 * i + 3]));
+            TGCU_CUDA(cudaEventElapsedTime(&a, h->coll_ev[4 * i], h->coll_ev[4 * i + 1]));
+            TGCU_CUDA(cudaEventElapsedTime(&b, h->coll_ev[4 * i + 2], h->coll_ev[4 * i + 3]));
+            ar += a;
+            hx += b;
+        }
+        if (allreduce_ms) *allreduce_ms = ar;
+        if (halo_ms) *halo_ms = hx;
+        if (steps) *steps = (int)n;
+        h->coll_used = 0;
     });
 }

@@ -262,4 +262,7 @@ struct tgcu_grid {
     tgcu::Grid g;
     tgcu_comm* comm = nullptr;  // slab grids: the job's communicator (tgcu_slab_connect, comm.cu)
     bool fused_halo = false;    // boundary planes stored into the neighbours by the brick kernel
+    // collective phase of profiled slab steps (all-reduce + halo exchange), event pairs
+    std::vector<cudaEvent_t> coll_ev;
+    size_t coll_used = 0;
 };

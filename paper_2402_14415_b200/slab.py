@@ -383,6 +383,13 @@ class SlabTrainer:
                                           C.byref(cfg._c()), None, flags | TGCU_ASYNC, st))
         return None
 
+    def comm_profile(self):
+        """(all-reduce ms, halo-exchange ms, steps) summed over the profiled
+        steps since the last call (tgcu_slab_comm_profile)."""
+        ar, hx, n = C.c_double(), C.c_double(), C.c_int()
+        _check(lib().tgcu_slab_comm_profile(self.slab.handle, C.byref(ar), C.byref(hx), C.byref(n)))
+        return ar.value, hx.value, n.value
+
     def close(self):
         self.slab.close()
         self.comm.close()

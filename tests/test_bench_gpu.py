@@ -52,3 +52,4 @@ def test_bench_two_rank_slab_flow():
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["loss_last"] == d["loss_last"]
     assert d["scaling"] == "strong" and d["config"]["grid"] == [256, 256, 256]  # C3 strong scaling
     assert d["collectives"] == "host" and len(d["per_rank_kernel_ms"]) == 2 and d["single_gpu"]["value"] > 0
+    assert len(d["per_rank_allreduce_ms"]) == 2 and all(x > 0 for x in d["per_rank_allreduce_ms"])

@@ -59,29 +59,29 @@ def _rank(rank, world, port, outdir, fused):
     tr.close()
 
 
-@pytest.mark.parametrize("fused", [False, True])
-def test_slab_trainer_two_ranks_match_single_grid(tmp_path, fused):
+@pytest.mark.parametrize("world,fused", [(2, False), (2, True), (3, True)])
+def test_slab_trainer_two_ranks_match_single_grid(tmp_path, world, fused):
     import multiprocessing as mp
     import paper_2402_14415_b200 as tg
     ctx = mp.get_context("spawn")
     port = _port()
-    ps = [ctx.Process(target=_rank, args=(r, 2, port, str(tmp_path), fused)) for r in range(2)]
+    ps = [ctx.Process(target=_rank, args=(r, world, port, str(tmp_path), fused)) for r in range(world)]
     for p in ps:
         p.start()
     for p in ps:
         p.join(300)
     assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
-    for r in range(2):
+    for r in range(world):
         assert bool(np.load(tmp_path / f"fused{r}.npy")[0]) == fused
     spec = tg.GridSpec(dim=3, resolution=RES, order=2)
     g = tg.init_grid(spec, tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.02, seed=11))
     g.adam_reset(tg.AdamConfig(lr=1e-2))
     ref = np.array([tg.train_step(g, b).as_array() for b in _batches()])
-    own = np.concatenate([np.load(tmp_path / "own0.npy"), np.load(tmp_path / "own1.npy")])
+    own = np.concatenate([np.load(tmp_path / f"own{r}.npy") for r in range(world)])
     full = g.coeffs
     assert own.shape == full.shape
     assert_trajectory_close(own, full, 1e-2, STEPS, what="slab vs single-grid coeffs")
-    for r in range(2):
+    for r in range(world):
         t = np.load(tmp_path / f"terms{r}.npy")
         assert np.all(np.abs(t - ref) <= 1e-6 * np.abs(ref) + 1e-30)
 
