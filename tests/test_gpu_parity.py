@@ -585,6 +585,68 @@ def test_binned_unsorted_query_matches_direct(oracle, order):
         tg.eval(g, pts)
 
 
+@pytest.mark.parametrize("order,origin,extent", [(1, (-1.0, -1.0, -1.0), (2.0, 2.0, 2.0)),
+                                                (2, (-1.0, -1.0, -1.0), (2.0, 2.0, 2.0)),
+                                                (2, (100.0, -37.5, 3.0), (1.5, 2.0, 0.75))])
+def test_binned_query_gather_large(oracle, order, origin, extent):
+    """The binned query writes each value at its record's pass-1 position and
+    gathers them back in input order (k_qp_unpart; Morton-order brick walk):
+    2^22 + 777 points, among them NaN points and 2^18 points within
+    0 .. 1e-3 cells of brick planes and of the domain edges (where the
+    partition's fp32 brick code hands over to the exact fp64 rule), on the
+    default domain and on one far from the origin; values and spatial
+    gradients identical to the direct-gather kernel on slices below the
+    binning threshold (a point binned into the wrong brick would read the
+    wrong tile), NaN slots left NaN by the partition, a subset against the
+    oracle."""
+    import torch
+    rng = np.random.default_rng(60 + order)
+    res = (90, 81, 77)
+    s = Spec(dim=3, res=res, order=order, origin=origin, extent=extent)
+    c = (0.1 * rng.standard_normal(s.V * s.K)).astype(np.float32)
+    g = tg.init_grid(tg.GridSpec(dim=3, resolution=res, origin=origin, extent=extent, order=order))
+    g.set_coeffs_f32(c)
+    n = (1 << 22) + 777
+    dp = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    tg.sample_uniform_device(3, 77 + order, dp)
+    o, e = np.array(origin), np.array(extent)
+    near = (1 << 18)
+    h = e / (np.array(res) - 1)
+    cells = rng.integers(0, 12, (near, 3)) * 8  # brick planes (8-cell bricks)
+    cells = np.where(rng.random((near, 3)) < 0.2, np.array(res) - 1, cells)  # the far domain edge
+    off = rng.choice([0.0, 1e-7, -1e-7, 1e-6, -1e-6, 1e-5, -1e-5, 1e-4, -1e-4, 1e-3, -1e-3], (near, 3))
+    pl = o + (cells + off) * h
+    keep = rng.random((near, 3)) < 0.5  # the other axes anywhere
+    pl = np.where(keep, pl, o + rng.random((near, 3)) * e)
+    dp[:near] = torch.from_numpy(pl.astype(np.float32)).cuda()
+    dp[near:] = dp[near:] * torch.tensor(e / 2, dtype=torch.float32, device="cuda") + \
+        torch.tensor(o + e / 2, dtype=torch.float32, device="cuda")
+    bad = torch.tensor([near + 3, 1 << 20, n - 1], device="cuda")
+    dp[bad, 1] = float("nan")
+    v_only = tg.eval_device(g, dp, torch.empty(n, dtype=torch.float32, device="cuda"), asynchronous=True)
+    vb = torch.empty(n, dtype=torch.float32, device="cuda")
+    gb = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    tg.eval_device(g, dp, vb, gb, asynchronous=True)
+    vd = torch.empty_like(vb)
+    gd = torch.empty_like(gb)
+    step = (1 << 18) - 1
+    for a in range(0, n, step):  # the direct kernel (below the threshold)
+        tg.eval_device(g, dp[a:a + step], vd[a:a + step], gd[a:a + step], asynchronous=True)
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError, match="NaN coordinate"):  # reported by the next checked call
+        tg.eval_device(g, dp[:near + 8], torch.empty(near + 8, dtype=torch.float32, device="cuda"))
+    g.close()
+    assert torch.isnan(v_only[bad]).all() and torch.isnan(gb[bad]).all()
+    assert int(torch.isnan(v_only).sum()) == 3
+    nn = lambda t: torch.nan_to_num(t, 7.0)  # noqa: E731
+    assert torch.equal(nn(v_only), nn(vb)) and torch.equal(nn(vb), nn(vd)) and torch.equal(nn(gb), nn(gd))
+    sub = np.concatenate([rng.choice(near, 2000, replace=False), rng.choice(n, 2000, replace=False)])
+    pts = dp[torch.from_numpy(sub).cuda()].cpu().numpy().astype(np.float64)
+    ok = ~np.isnan(pts).any(axis=1)
+    ref = oracle.eval(s, c.astype(np.float64), pts[ok])
+    assert_close(v_only.cpu().numpy()[sub][ok], ref, 1e-6, what="binned value")
+
+
 @pytest.mark.parametrize("dim,res", [(2, (37, 29)), (3, (19, 12, 26))])
 @pytest.mark.parametrize("order", [0, 1, 2])
 @pytest.mark.parametrize("name,cfg", [("paper", tg.LossConfig()), ("recon", tg.LossConfig(lambda1=0.0, use_tv=False)),
