@@ -472,6 +472,25 @@ constexpr int kQpTile = 4096;  // elements per CTA, both passes
 constexpr int kQpPer = kQpTile / kQpThreads;
 constexpr int kQpRowBlocks = 32;  // column-scan row blocks
 
+struct QpFast {
+    float o[3], ih[3], lo[3], hi[3], fr[3];  // origin, 1/h, cell bounds, brick-fraction margin
+};
+// (host: formed once per call, read from the kernel parameters)
+inline QpFast qp_fast(const DevSpec& s, int LB) {
+    QpFast f{};
+    for (int a = 0; a < 3; ++a) {
+        f.o[a] = (float)s.origin[a];
+        f.ih[a] = s.inv_hf[a];
+        const double M = std::max(std::fabs(s.origin[a]), std::fabs(s.hi[a]));
+        const double err = (3.0 * M * s.inv_h[a] + 2.0 * s.res[a]) * 0x1p-24;
+        const float eps = (float)std::max(0x1p-10, 8.0 * err);
+        f.lo[a] = eps;
+        f.hi[a] = (float)(s.res[a] - 1) - eps;
+        f.fr[a] = eps / (float)(1 << LB);
+    }
+    return f;
+}
+
 struct QpArgs {
     DevSpec s;
     const float* pts;   // n x 3
@@ -493,6 +512,7 @@ struct QpArgs {
     float* vals;        // NaN answers (binned query), null for the sort
     float* grads;
     Status* st;
+    QpFast qf;             // fp32 brick-code constants
     unsigned short* lpos;  // binned query: each input point's slot in its pass-1 tile's digit
                            // order (0xffff: NaN); pass-1 records then carry the brick code and
                            // pass-2 records their pass-1 position instead of the input index
@@ -508,25 +528,6 @@ struct QpArgs {
 // origin, of 1/h and of the product); eps is 8 times that, at least 2^-10
 // (2^-10 at 512 cells on [-1, 1]: 2.3 % of warps take the exact rule, 32 %
 // at the earlier fixed 1/64).
-struct QpFast {
-    float o[3], ih[3], lo[3], hi[3], fr[3];  // origin, 1/h, cell bounds, brick-fraction margin
-};
-template <int LB>
-__device__ __forceinline__ QpFast qp_fast(const DevSpec& s) {
-    QpFast f;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        f.o[a] = (float)s.origin[a];
-        f.ih[a] = s.inv_hf[a];
-        const double M = fmax(fabs(s.origin[a]), fabs(s.hi[a]));
-        const double err = (3.0 * M * s.inv_h[a] + 2.0 * s.res[a]) * 0x1p-24;
-        const float eps = (float)fmax(0x1p-10, 8.0 * err);
-        f.lo[a] = eps;
-        f.hi[a] = (float)(s.res[a] - 1) - eps;
-        f.fr[a] = eps * (1.0f / (1 << LB));
-    }
-    return f;
-}
 template <int DIM, int LB>
 __device__ __forceinline__ int qp_code(const DevSpec& s, const QpFast& f, float x, float y, float z) {
     const float p[3] = {x, y, z};
@@ -623,7 +624,7 @@ __global__ void __launch_bounds__(kQpThreads, 2) k_qp_hist(QpArgs A) {
     long long e0, e1;
     if (!qp_tile<PASS>(A, e0, e1)) return;
     for (int i = threadIdx.x; i < ND; i += blockDim.x) h[i] = 0;
-    const QpFast qf = qp_fast<LB>(A.s);
+    const QpFast& qf = A.qf;
     float4 rec[kQpPer];
     int d[kQpPer];
 #pragma unroll
@@ -823,7 +824,7 @@ __global__ void __launch_bounds__(kQpThreads, 2) k_qp_scatter(QpArgs A) {
         cnt[i] = 0;
         gst[i] = PASS == 1 ? (int)A.seg[i] + row[i] : row[i];
     }
-    const QpFast qf = qp_fast<LB>(A.s);
+    const QpFast& qf = A.qf;
     float4 rec[kQpPer];
     int d[kQpPer], rk[kQpPer];
 #pragma unroll
@@ -1018,6 +1019,7 @@ void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xy
     A.grads = grads;
     A.st = g.st;
     A.lpos = lpos;
+    A.qf = qp_fast(g.ds, g.spec.dim == 3 ? 3 : 4);
     const size_t hs1 = sizeof(int) * NH, hs2 = sizeof(int) * NL;
     const size_t ss1 = (sizeof(float4) + 2) * kQpTile + 2 * hs1, ss2 = (sizeof(float4) + 2) * kQpTile + 2 * hs2;
     auto run = [&](auto hist1, auto scatter1, auto hist2, auto scatter2) {
