@@ -110,3 +110,35 @@ def test_slab_trainer_nccl_single_rank_matches_single_grid():
     assert np.allclose(tr.slab.sync().as_array(), g.sync().as_array(), rtol=1e-6, atol=1e-30)
     assert_trajectory_close(tr.slab.owned_coeffs(), g.coeffs, 1e-2, 2 * STEPS, what="nccl slab vs grid")
     tr.close()
+
+
+SLAB_DRIVER = os.path.join(ROOT, "tests", "cpp", "slab_driver")
+
+
+@pytest.mark.parametrize("world,fused,backend", [(2, 0, "host"), (3, 1, "host"), (1, 0, "nccl")])
+def test_cpp_slab_driver_processes_match_single_grid(tmp_path, world, fused, backend):
+    """tests/cpp/slab_driver.cpp: `world` C++ processes drive a slab job
+    through the C ABI alone (tgcu_comm_create, tgcu_grid_create_slab,
+    tgcu_slab_connect, tgcu_slab_train_step; full batches and local point
+    shards on alternate steps); gathered owned planes and every rank's loss
+    terms against the single-grid run."""
+    import subprocess
+    import paper_2402_14415_b200 as tg
+    assert os.path.exists(SLAB_DRIVER), "built by __graft_entry__.build()"
+    port = _port()
+    ps = [subprocess.Popen([SLAB_DRIVER, str(r), str(world), str(port), str(fused), backend, str(tmp_path)],
+                           stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(world)]
+    outs = [p.communicate(timeout=300)[0] for p in ps]
+    assert all(p.returncode == 0 for p in ps), outs
+    for r in range(world):
+        assert (tmp_path / f"cpp_fused{r}.txt").read_text() == str(fused), outs
+    spec = tg.GridSpec(dim=3, resolution=RES, order=2)
+    g = tg.init_grid(spec, tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.02, seed=11))
+    g.adam_reset(tg.AdamConfig(lr=1e-2))
+    ref = np.array([tg.train_step(g, b).as_array() for b in _batches()])
+    own = np.concatenate([np.fromfile(tmp_path / f"cpp_own{r}.f64") for r in range(world)])
+    assert own.shape == g.coeffs.shape
+    assert_trajectory_close(own, g.coeffs, 1e-2, STEPS, what="C++ slab job vs single-grid coeffs")
+    for r in range(world):
+        t = np.fromfile(tmp_path / f"cpp_terms{r}.f64").reshape(-1, 4)
+        assert np.all(np.abs(t - ref) <= 1e-6 * np.abs(ref) + 1e-30), (r, t, ref)
