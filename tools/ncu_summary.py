@@ -1,6 +1,6 @@
 """Markdown summary of one ncu `--set full` capture for profiles/.
 
-    python tools/ncu_summary.py gpurun_out/brick_r01.ncu-rep "title" > profiles/r01_brick_step_ncu.md
+    python tools/ncu_summary.py gpurun_out/brick_r01.ncu-rep "title" [launch index] > profiles/r01_brick_step_ncu.md
 
 Key section metrics, DRAM bytes per launch, and the top source lines by warp
 stall samples with their instruction share (needs -lineinfo builds and
@@ -20,12 +20,17 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum
        "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_write.sum"]
 
 
+LAUNCH = []  # --launch-skip i --launch-count 1 (a report holding several kernels)
+
+
 def ncu(rep, *args):
-    return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", rep, *LAUNCH, *args], capture_output=True, text=True).stdout
 
 
 def main():
     rep, title = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else sys.argv[1]
+    if len(sys.argv) > 3:
+        LAUNCH[:] = ["--launch-skip", sys.argv[3], "--launch-count", "1"]
     out = [f"# {title}", "", f"Source: `{rep}` (ncu --set full --clock-control none --import-source on).", ""]
     det = list(csv.reader(io.StringIO(ncu(rep, "--page", "details", "--csv"))))
     kname = det[1][4] if len(det) > 1 else "?"
