@@ -513,6 +513,8 @@ struct QpArgs {
     float* grads;
     Status* st;
     QpFast qf;             // fp32 brick-code constants
+    int* codes;            // pass 1: each input point's brick code, formed by the histogram
+                           // and read back by the scatter (-1: NaN point of the binned query)
     unsigned short* lpos;  // binned query: each input point's slot in its pass-1 tile's digit
                            // order (0xffff: NaN); pass-1 records then carry the brick code and
                            // pass-2 records their pass-1 position instead of the input index
@@ -562,35 +564,43 @@ __device__ __forceinline__ int qp_code(const DevSpec& s, const QpFast& f, float 
 // of the tile's superbrick chunk (all of a thread's loads are issued before
 // the first digit is formed).
 template <int DIM, int PASS>
-__device__ __forceinline__ void qp_fetch(const QpArgs& A, long long e1, long long j, float4& rec) {
+__device__ __forceinline__ void qp_fetch(const QpArgs& A, long long e1, long long j, float4& rec, int& code,
+                                         bool load_code) {
     if (j >= e1) return;
-    if constexpr (PASS == 1)
+    if constexpr (PASS == 1) {
         rec = make_float4(A.pts[3 * j], A.pts[3 * j + 1], DIM == 3 ? A.pts[3 * j + 2] : 0.f, __int_as_float((int)j));
-    else
+        if (load_code) code = __ldcs(A.codes + j);
+    } else {
         rec = A.A[j];
+    }
 }
 // Its digit (NaN points of the binned query are answered in pass 1's
-// histogram and get digit -1).
+// histogram and get digit -1). Pass 1: the histogram (answer_nan) forms the
+// code and stores it in A.codes; the scatter takes it from there (have_code).
 template <int DIM, int LB, int PASS>
 __device__ __forceinline__ int qp_digit(const QpArgs& A, const QpFast& qf, long long e1, long long j, float4& rec,
-                                        bool answer_nan) {
+                                        bool answer_nan, bool have_code, int code) {
     if (j >= e1) return -1;
     if constexpr (PASS == 1) {
-        const float x = rec.x, y = rec.y, z = rec.z;
-        if (A.vals && (isnan(x) || isnan(y) || (DIM == 3 && isnan(z)))) {
-            if (answer_nan) {
-                atomicMin(&A.st->nan_point, (unsigned long long)j);
-                A.vals[j] = __int_as_float(0x7fc00000);
-                if (A.grads)
-                    for (int a = 0; a < 3; ++a) A.grads[3 * j + a] = __int_as_float(0x7fc00000);
+        if (!have_code) {
+            const float x = rec.x, y = rec.y, z = rec.z;
+            if (A.vals && (isnan(x) || isnan(y) || (DIM == 3 && isnan(z)))) {
+                if (answer_nan) {
+                    atomicMin(&A.st->nan_point, (unsigned long long)j);
+                    A.vals[j] = __int_as_float(0x7fc00000);
+                    if (A.grads)
+                        for (int a = 0; a < 3; ++a) A.grads[3 * j + a] = __int_as_float(0x7fc00000);
+                }
+                code = -1;
+            } else {
+                code = qp_code<DIM, LB>(A.s, qf, x, y, z);
             }
-            return -1;
+            if (answer_nan && A.codes) A.codes[j] = code;
         }
-        const int code = qp_code<DIM, LB>(A.s, qf, x, y, z);
+        if (code < 0) return -1;
         if (A.lpos) rec.w = __int_as_float(code);
         return code >> A.LO;
     } else {
-        int code;
         if (A.lpos) {  // the code pass 1 formed; the record now names its pass-1 position
             code = __float_as_int(rec.w);
             rec.w = __int_as_float((int)j);
@@ -626,13 +636,14 @@ __global__ void __launch_bounds__(kQpThreads, 2) k_qp_hist(QpArgs A) {
     for (int i = threadIdx.x; i < ND; i += blockDim.x) h[i] = 0;
     const QpFast& qf = A.qf;
     float4 rec[kQpPer];
-    int d[kQpPer];
+    int d[kQpPer], pc[kQpPer];
 #pragma unroll
     for (int k = 0; k < kQpPer; ++k)  // all loads in flight first
-        qp_fetch<DIM, PASS>(A, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k]);
+        qp_fetch<DIM, PASS>(A, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], pc[k], false);
 #pragma unroll
     for (int k = 0; k < kQpPer; ++k)
-        d[k] = qp_digit<DIM, LB, PASS>(A, qf, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], true);
+        d[k] = qp_digit<DIM, LB, PASS>(A, qf, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], true, false,
+                                       0);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kQpPer; ++k)
@@ -827,12 +838,14 @@ __global__ void __launch_bounds__(kQpThreads, 2) k_qp_scatter(QpArgs A) {
     const QpFast& qf = A.qf;
     float4 rec[kQpPer];
     int d[kQpPer], rk[kQpPer];
+    constexpr bool have = PASS == 1;  // (launch_qpart always provides A.codes)
 #pragma unroll
     for (int k = 0; k < kQpPer; ++k)
-        qp_fetch<DIM, PASS>(A, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k]);
+        qp_fetch<DIM, PASS>(A, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], d[k], have);
 #pragma unroll
     for (int k = 0; k < kQpPer; ++k)
-        d[k] = qp_digit<DIM, LB, PASS>(A, qf, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], false);
+        d[k] = qp_digit<DIM, LB, PASS>(A, qf, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], false, have,
+                                       d[k]);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kQpPer; ++k) rk[k] = d[k] >= 0 ? atomicAdd(&cnt[d[k]], 1) : 0;
@@ -996,9 +1009,10 @@ void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xy
     const size_t bH1 = al(sizeof(int) * (size_t)A.ntiles * NH), bP1 = al(sizeof(int) * kQpRowBlocks * NH),
                  bTot = al(sizeof(int) * NH), bSeg = al(sizeof(long long) * (NH + 1)), bCf = al(sizeof(int) * (NH + 1)),
                  bCs = al(sizeof(int) * maxtiles), bH2 = al(sizeof(int) * (size_t)maxtiles * NL),
-                 bA = al(sizeof(float4) * (size_t)std::max<int64_t>(n, 1));
+                 bA = al(sizeof(float4) * (size_t)std::max<int64_t>(n, 1)),
+                 bCode = al(sizeof(int) * (size_t)std::max<int64_t>(n, 1));
     char* q = nullptr;
-    TGCU_CUDA(cudaMallocAsync(&q, bH1 + bP1 + bTot + bSeg + bCf + bCs + bH2 + bA, s));
+    TGCU_CUDA(cudaMallocAsync(&q, bH1 + bP1 + bTot + bSeg + bCf + bCs + bH2 + bA + bCode, s));
     char* const scratch = q;
     A.H1 = reinterpret_cast<int*>(q); q += bH1;
     A.P1 = reinterpret_cast<int*>(q); q += bP1;
@@ -1007,7 +1021,8 @@ void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xy
     A.cfirst = reinterpret_cast<int*>(q); q += bCf;
     A.cseg = reinterpret_cast<int*>(q); q += bCs;
     A.H2 = reinterpret_cast<int*>(q); q += bH2;
-    A.A = reinterpret_cast<float4*>(q);
+    A.A = reinterpret_cast<float4*>(q); q += bA;
+    A.codes = reinterpret_cast<int*>(q);
     A.off = off;
     // the sort writes pass 2's records to C, then orders each brick by cell
     float4* C = nullptr;
