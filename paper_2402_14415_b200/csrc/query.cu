@@ -515,6 +515,7 @@ struct QpArgs {
     QpFast qf;             // fp32 brick-code constants
     int* codes;            // pass 1: each input point's brick code, formed by the histogram
                            // and read back by the scatter (-1: NaN point of the binned query)
+    int* codesA;           // the sort: the code of each pass-1 output record (pass 2 reads it)
     unsigned short* lpos;  // binned query: each input point's slot in its pass-1 tile's digit
                            // order (0xffff: NaN); pass-1 records then carry the brick code and
                            // pass-2 records their pass-1 position instead of the input index
@@ -572,6 +573,7 @@ __device__ __forceinline__ void qp_fetch(const QpArgs& A, long long e1, long lon
         if (load_code) code = __ldcs(A.codes + j);
     } else {
         rec = A.A[j];
+        if (!A.lpos) code = A.codesA[j];
     }
 }
 // Its digit (NaN points of the binned query are answered in pass 1's
@@ -604,9 +606,7 @@ __device__ __forceinline__ int qp_digit(const QpArgs& A, const QpFast& qf, long 
         if (A.lpos) {  // the code pass 1 formed; the record now names its pass-1 position
             code = __float_as_int(rec.w);
             rec.w = __int_as_float((int)j);
-        } else {
-            code = qp_code<DIM, LB>(A.s, qf, rec.x, rec.y, rec.z);
-        }
+        }  // (else: fetched from A.codesA)
         return code & ((1 << A.LO) - 1);
     }
 }
@@ -640,10 +640,11 @@ __global__ void __launch_bounds__(kQpThreads, 2) k_qp_hist(QpArgs A) {
 #pragma unroll
     for (int k = 0; k < kQpPer; ++k)  // all loads in flight first
         qp_fetch<DIM, PASS>(A, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], pc[k], false);
+    (void)pc;
 #pragma unroll
     for (int k = 0; k < kQpPer; ++k)
         d[k] = qp_digit<DIM, LB, PASS>(A, qf, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], true, false,
-                                       0);
+                                       pc[k]);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kQpPer; ++k)
@@ -826,6 +827,8 @@ __global__ void __launch_bounds__(kQpThreads, 2) k_qp_scatter(QpArgs A) {
     unsigned short* dig = reinterpret_cast<unsigned short*>(recs + kQpTile);  // [kQpTile]
     int* cnt = reinterpret_cast<int*>(dig + kQpTile);                         // [ND] counts -> local starts
     int* gst = cnt + ND;                                                       // [ND] global starts
+    int* scode = gst + ND;        // the sort's pass 1: [kQpTile] codes in digit order
+    int* sin = scode + kQpTile;   // ... and in input order
     __shared__ int wsum[kQpThreads / 32];
     __shared__ int valid;
     long long e0, e1;
@@ -837,15 +840,17 @@ __global__ void __launch_bounds__(kQpThreads, 2) k_qp_scatter(QpArgs A) {
     }
     const QpFast& qf = A.qf;
     float4 rec[kQpPer];
-    int d[kQpPer], rk[kQpPer];
+    int d[kQpPer], rk[kQpPer], cd[kQpPer];
     constexpr bool have = PASS == 1;  // (launch_qpart always provides A.codes)
 #pragma unroll
     for (int k = 0; k < kQpPer; ++k)
-        qp_fetch<DIM, PASS>(A, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], d[k], have);
+        qp_fetch<DIM, PASS>(A, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], cd[k], have);
 #pragma unroll
-    for (int k = 0; k < kQpPer; ++k)
+    for (int k = 0; k < kQpPer; ++k) {
         d[k] = qp_digit<DIM, LB, PASS>(A, qf, e1, e0 + threadIdx.x + (long long)k * kQpThreads, rec[k], false, have,
-                                       d[k]);
+                                       cd[k]);
+        if (PASS == 1 && !A.lpos) sin[threadIdx.x + k * kQpThreads] = cd[k];
+    }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kQpPer; ++k) rk[k] = d[k] >= 0 ? atomicAdd(&cnt[d[k]], 1) : 0;
@@ -879,6 +884,7 @@ __global__ void __launch_bounds__(kQpThreads, 2) k_qp_scatter(QpArgs A) {
         if (d[k] >= 0) {
             recs[j] = rec[k];
             dig[j] = (unsigned short)d[k];
+            if (PASS == 1 && !A.lpos) scode[j] = sin[threadIdx.x + k * kQpThreads];
         }
         if (PASS == 1 && A.lpos) {
             const long long i = e0 + threadIdx.x + (long long)k * kQpThreads;
@@ -894,6 +900,7 @@ __global__ void __launch_bounds__(kQpThreads, 2) k_qp_scatter(QpArgs A) {
         const float4 q = recs[j];
         if (PASS == 1 || A.B) {
             (PASS == 1 ? A.A : A.B)[pos] = q;
+            if (PASS == 1 && !A.lpos) A.codesA[pos] = scode[j];
         } else {
             A.out_xyz[3 * (long long)pos] = q.x;
             A.out_xyz[3 * (long long)pos + 1] = q.y;
@@ -1010,9 +1017,9 @@ void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xy
                  bTot = al(sizeof(int) * NH), bSeg = al(sizeof(long long) * (NH + 1)), bCf = al(sizeof(int) * (NH + 1)),
                  bCs = al(sizeof(int) * maxtiles), bH2 = al(sizeof(int) * (size_t)maxtiles * NL),
                  bA = al(sizeof(float4) * (size_t)std::max<int64_t>(n, 1)),
-                 bCode = al(sizeof(int) * (size_t)std::max<int64_t>(n, 1));
+                 bCode = al(sizeof(int) * (size_t)std::max<int64_t>(n, 1)), bCodeA = lpos ? 0 : bCode;
     char* q = nullptr;
-    TGCU_CUDA(cudaMallocAsync(&q, bH1 + bP1 + bTot + bSeg + bCf + bCs + bH2 + bA + bCode, s));
+    TGCU_CUDA(cudaMallocAsync(&q, bH1 + bP1 + bTot + bSeg + bCf + bCs + bH2 + bA + bCode + bCodeA, s));
     char* const scratch = q;
     A.H1 = reinterpret_cast<int*>(q); q += bH1;
     A.P1 = reinterpret_cast<int*>(q); q += bP1;
@@ -1022,7 +1029,8 @@ void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xy
     A.cseg = reinterpret_cast<int*>(q); q += bCs;
     A.H2 = reinterpret_cast<int*>(q); q += bH2;
     A.A = reinterpret_cast<float4*>(q); q += bA;
-    A.codes = reinterpret_cast<int*>(q);
+    A.codes = reinterpret_cast<int*>(q); q += bCode;
+    A.codesA = lpos ? nullptr : reinterpret_cast<int*>(q);
     A.off = off;
     // the sort writes pass 2's records to C, then orders each brick by cell
     float4* C = nullptr;
@@ -1036,7 +1044,8 @@ void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xy
     A.lpos = lpos;
     A.qf = qp_fast(g.ds, g.spec.dim == 3 ? 3 : 4);
     const size_t hs1 = sizeof(int) * NH, hs2 = sizeof(int) * NL;
-    const size_t ss1 = (sizeof(float4) + 2) * kQpTile + 2 * hs1, ss2 = (sizeof(float4) + 2) * kQpTile + 2 * hs2;
+    const size_t ss1 = (sizeof(float4) + 2) * kQpTile + 2 * hs1 + (lpos ? 0 : 2 * sizeof(int) * kQpTile),
+                 ss2 = (sizeof(float4) + 2) * kQpTile + 2 * hs2;
     auto run = [&](auto hist1, auto scatter1, auto hist2, auto scatter2) {
         TGCU_CUDA(cudaFuncSetAttribute(scatter1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ss1));
         TGCU_CUDA(cudaFuncSetAttribute(scatter2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ss2));

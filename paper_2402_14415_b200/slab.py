@@ -139,6 +139,12 @@ class SlabGrid:
     def handle(self):
         return self._h
 
+    def set_deterministic(self, on: bool = True):
+        """Bit-reproducible slab steps (tgcu_grid_set_deterministic): each brick's
+        sums in a canonical order, so the slabs' parameters equal a single
+        grid's in the same mode bit for bit."""
+        _check(lib().tgcu_grid_set_deterministic(self._h, 1 if on else 0))
+
     def close(self):
         if getattr(self, "_h", None):
             lib().tgcu_grid_destroy(self._h)
