@@ -734,6 +734,10 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     const int o[3] = {bcx * B, bcy * B, DIM == 3 ? (A.zb0 + bcz) * B : 0};
     const int zrel = o[2] - A.s.zoff;  // first owned plane in the stored planes
     const bool tmap = L::TMAP && A.use_tmap;
+    // m and v are needed only by the epilogue: a brick with points issues their
+    // boxes once its tile has landed, so the tile (which the forward waits
+    // for) does not share the memory system with them at the CTA's start
+    const bool mv_late = !SPLIT && tmap && nmine > 0;
 
     if (tid == 0) {
         mbar_init(&bars[0], tmap ? 1 : NT);
@@ -753,16 +757,16 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         // m and v only in rank 0, which alone runs TV + Adam)
         if (tid == 0 && (crank == 0 || nmine > 0)) {
             mbar_expect_tx(&bars[0], L::tile_box_bytes);
-            if (crank == 0) mbar_expect_tx(&bars[1], 2 * L::own_box_bytes);
+            if (crank == 0 && !mv_late) mbar_expect_tx(&bars[1], 2 * L::own_box_bytes);
             if constexpr (DIM == 3) {
                 tma_load_3d(tile, &A.tm_tile, &bars[0], (o[0] - 1) * K - L::SHF, o[1] - 1, zrel - 1);
-                if (crank == 0) {
+                if (crank == 0 && !mv_late) {
                     tma_load_3d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1], zrel);
                     tma_load_3d(mvs + S::NOWN * K, &A.tm_v_in, &bars[1], o[0] * K, o[1], zrel);
                 }
             } else {
                 tma_load_2d(tile, &A.tm_tile, &bars[0], (o[0] - 1) * K - L::SHF, o[1] - 1);
-                if (crank == 0) {
+                if (crank == 0 && !mv_late) {
                     tma_load_2d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1]);
                     tma_load_2d(mvs + S::NOWN * K, &A.tm_v_in, &bars[1], o[0] * K, o[1]);
                 }
@@ -787,6 +791,18 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         if (!mv_row) mbar_arrive(&bars[1]);
     }
 
+    auto issue_mv_late = [&] {  // thread 0, after its warp saw the tile land
+        if (mv_late && tid == 0) {
+            mbar_expect_tx(&bars[1], 2 * L::own_box_bytes);
+            if constexpr (DIM == 3) {
+                tma_load_3d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1], zrel);
+                tma_load_3d(mvs + S::NOWN * K, &A.tm_v_in, &bars[1], o[0] * K, o[1], zrel);
+            } else {
+                tma_load_2d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1]);
+                tma_load_2d(mvs + S::NOWN * K, &A.tm_v_in, &bars[1], o[0] * K, o[1]);
+            }
+        }
+    };
     constexpr bool PACKED = DIM == 3 && ORDER == 2;  // fp32x2 accumulators (corner_grad_p2)
     float G[K];
 #pragma unroll
@@ -863,6 +879,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                 // single-chunk brick: the tile wait rides on this barrier
                 cp_async_wait<0>();
                 if (warp == 0) mbar_wait(&bars[0], 0);
+                issue_mv_late();
             }
             __syncthreads();
         }
@@ -877,6 +894,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         if (base == pfirst && tiny) {
             cp_async_wait<0>();
             if (warp == 0) mbar_wait(&bars[0], 0);
+            issue_mv_late();
             __syncthreads();  // tile and the points' cells (start[]) visible
 #ifdef TGCU_PHASE_TIMING
             TGCU_PT_SET(pt_tile)
@@ -921,6 +939,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             perm[bstart[bk] + r2] = v;
             cp_async_wait<0>();  // own fallback rows (rare: grid-edge bricks)
             if (warp == 0) mbar_wait(&bars[0], 0);  // one warp waits for the tile; the others park here
+            issue_mv_late();
             __syncthreads();
             myv = perm[tid];
 #ifdef TGCU_PHASE_TIMING
