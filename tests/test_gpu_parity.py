@@ -647,6 +647,55 @@ def test_binned_query_gather_large(oracle, order, origin, extent):
     assert_close(v_only.cpu().numpy()[sub][ok], ref, 1e-6, what="binned value")
 
 
+@pytest.mark.parametrize("case", ["one_point", "one_brick", "all_nan", "threshold", "corner_edges"])
+def test_binned_query_skewed_inputs(case):
+    """The binned query's partition, brick kernel and reverse gather on
+    degenerate batches: every point identical, all points inside one brick,
+    all points NaN, exactly the binning threshold, every point on a domain
+    corner / edge; values equal the direct-gather kernel's."""
+    import torch
+    rng = np.random.default_rng(7)
+    res = (70, 66, 61)
+    g = tg.init_grid(gspec(3, res, 2))
+    s = ospec(3, res, 2)
+    g.set_coeffs_f32((0.1 * rng.standard_normal(s.V * s.K)).astype(np.float32))
+    n = (1 << 18) + 3
+    if case == "one_point":
+        p = np.tile(np.array([[0.123, -0.456, 0.789]], np.float32), (n, 1))
+    elif case == "one_brick":
+        p = (rng.random((n, 3)) * 7.9 * 2.0 / 69.0 - 1.0).astype(np.float32)  # cells [0, 8) on each axis
+    elif case == "all_nan":
+        p = np.full((n, 3), np.nan, np.float32)
+    elif case == "threshold":
+        n = 1 << 18
+        p = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    else:
+        p = rng.choice([-1.0, 1.0, -1.0000001, 1.0000001, 0.0], (n, 3)).astype(np.float32)
+    dp = torch.from_numpy(p).cuda()
+    vb = tg.eval_device(g, dp, torch.empty(n, dtype=torch.float32, device="cuda"), asynchronous=True)
+    vd = torch.empty(n, dtype=torch.float32, device="cuda")
+    step = (1 << 18) - 1
+    for a in range(0, n, step):
+        tg.eval_device(g, dp[a:a + step], vd[a:a + step], asynchronous=True)
+    torch.cuda.synchronize()
+    if case == "all_nan":
+        assert torch.isnan(vb).all() and torch.isnan(vd).all()
+        with pytest.raises(ValueError, match="NaN coordinate"):
+            tg.eval_device(g, dp[:4], torch.empty(4, dtype=torch.float32, device="cuda"))
+    else:
+        assert torch.equal(vb, vd)
+        # the sort (partition + cell pass) and the brick-sorted kernel
+        spts = torch.empty_like(dp)
+        perm = torch.empty(n, dtype=torch.int64, device="cuda")
+        offs = torch.empty(tg.query_brick_codes(g) + 1, dtype=torch.int64, device="cuda")
+        tg.sort_points(g, dp, spts, perm, offs)
+        vs = tg.eval_sorted(g, spts, offs)
+        torch.cuda.synchronize()
+        assert torch.equal(spts, dp[perm]) and torch.equal(vs, vd[perm])
+        assert int(offs[-1]) == n and bool((offs[1:] >= offs[:-1]).all())
+    g.close()
+
+
 @pytest.mark.parametrize("dim,res", [(2, (37, 29)), (3, (19, 12, 26))])
 @pytest.mark.parametrize("order", [0, 1, 2])
 @pytest.mark.parametrize("name,cfg", [("paper", tg.LossConfig()), ("recon", tg.LossConfig(lambda1=0.0, use_tv=False)),
