@@ -266,14 +266,15 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         int64_t Vg = 1;
         for (int a = 0; a < s.dim; ++a) Vg *= s.res[a];
         const int B = s.dim == 3 ? kBrick3 : kBrick2;
+        const int BZ = s.dim == 3 ? kBrickZ3 : 1;  // z extent of a brick (slab layer depth)
         const bool slab = zb_lo >= 0;
-        const int nbz_global = s.dim == 3 ? (s.res[2] + B - 1) / B : 1;
+        const int nbz_global = s.dim == 3 ? (s.res[2] + BZ - 1) / BZ : 1;
         int zoff = 0, zstore = s.dim == 3 ? s.res[2] : 1;
         if (slab) {
             require(s.dim == 3, "slab grids need dim 3");
             require(zb_lo < zb_hi && zb_hi <= nbz_global, "slab brick layers out of range");
-            zoff = std::max(0, B * zb_lo - 1);
-            const int zend = std::min(s.res[2], B * zb_hi + 1);
+            zoff = std::max(0, BZ * zb_lo - 1);
+            const int zend = std::min(s.res[2], BZ * zb_hi + 1);
             zstore = zend - zoff;
         }
         const int64_t V = (int64_t)s.res[0] * (s.dim == 3 ? (int64_t)s.res[1] * zstore : s.res[1]);
@@ -348,8 +349,9 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         g.code_sh[0] = code_sh[0];
         g.code_sh[1] = code_sh[1];
         for (int a = 0; a < 3; ++a) {
-            g.brick[a] = a < s.dim ? B : 1;
-            g.nb[a] = a < s.dim ? (s.res[a] + B - 1) / B : 1;
+            const int ba = a == 2 ? BZ : B;
+            g.brick[a] = a < s.dim ? ba : 1;
+            g.nb[a] = a < s.dim ? (s.res[a] + ba - 1) / ba : 1;
         }
         if (slab) {
             g.zb0 = zb_lo;
@@ -407,7 +409,7 @@ int tgcu_grid_create_slab(const tgcu_grid_spec* spec, int zb_lo, int zb_hi, cons
 int tgcu_slab_info(const tgcu_grid* h, int* z_store_lo, int* z_store_n, int* z_own_lo, int* z_own_hi,
                    int* brick_layers) {
     const Grid& g = h->g;
-    const int B = g.spec.dim == 3 ? kBrick3 : kBrick2;
+    const int B = g.spec.dim == 3 ? kBrickZ3 : 1;  // (slab layers: z bricks)
     if (z_store_lo) *z_store_lo = g.ds.zoff;
     if (z_store_n) *z_store_n = g.ds.zstore;
     if (z_own_lo) *z_own_lo = g.slab ? B * g.zb0 : 0;
@@ -1097,7 +1099,7 @@ int tgcu_slab_halo(tgcu_grid* h, float** send_lo, float** send_hi, float** recv_
     return guard([&] {
         Grid& g = h->g;
         require(g.slab, "slab_halo: not a slab grid");
-        const int B = kBrick3;
+        const int B = kBrickZ3;
         const int own_lo = B * g.zb0;
         const int own_hi = std::min(g.spec.res[2], B * (g.zb0 + g.nb[2]));
         const int64_t pf = g.ds.sz * g.K;
@@ -1121,8 +1123,8 @@ struct SlabPlanes {
 };
 SlabPlanes slab_planes(const tgcu::Grid& g) {
     SlabPlanes p;
-    p.own_lo = tgcu::kBrick3 * g.zb0;
-    p.own_hi = std::min(g.spec.res[2], tgcu::kBrick3 * (g.zb0 + g.nb[2]));
+    p.own_lo = tgcu::kBrickZ3 * g.zb0;
+    p.own_hi = std::min(g.spec.res[2], tgcu::kBrickZ3 * (g.zb0 + g.nb[2]));
     p.has_lo = p.own_lo > 0;
     p.has_hi = p.own_hi < g.spec.res[2];
     p.pf = g.ds.sz * g.K;

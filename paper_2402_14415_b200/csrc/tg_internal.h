@@ -65,6 +65,21 @@ DevSpec make_devspec(const tgcu_grid_spec& s);
 // Brick edge (vertices per axis) of the fused training kernel and the
 // brick-binned query.
 constexpr int kBrick3 = 8;
+// z extent of the fused training kernel's 3D brick (vertex planes; x and y
+// are kBrick3). Slab grids are cut into layers of this many planes (slab.py
+// BRICK follows the default). A/B switch: half-depth bricks (4) with m, v in
+// HBM (TGCU_MV_GLOBAL) fit 4 CTAs per SM but measured 12 % slower at C2
+// (DESIGN.md §3.1).
+#ifndef TGCU_BRICKZ3
+#define TGCU_BRICKZ3 8
+#endif
+constexpr int kBrickZ3 = TGCU_BRICKZ3;
+// 3D fused step with m and v read and written in HBM by the epilogue (L2
+// prefetch at the CTA's start) instead of staged in shared memory: half-depth
+// bricks then fit 4 CTAs per SM.
+#ifndef TGCU_MV_GLOBAL
+#define TGCU_MV_GLOBAL (TGCU_BRICKZ3 < 8)
+#endif
 #ifndef TGCU_BRICK2
 #define TGCU_BRICK2 16
 #endif

@@ -47,12 +47,15 @@ namespace tgcu {
 
 template <int DIM>
 struct BrickShape {
-    static constexpr int B = DIM == 3 ? kBrick3 : kBrick2;
-    static constexpr int T = B + 2;   // tile edge (vertices)
-    static constexpr int CE = B + 1;  // cells per axis touching owned vertices
-    static constexpr int NCELL = DIM == 3 ? CE * CE * CE : CE * CE;
-    static constexpr int TVN = DIM == 3 ? T * T * T : T * T;
-    static constexpr int NOWN = DIM == 3 ? B * B * B : B * B;
+    static constexpr int B = DIM == 3 ? kBrick3 : kBrick2;   // x and y extent (vertices)
+    static constexpr int BZ = DIM == 3 ? kBrickZ3 : 1;       // z extent (3D)
+    static constexpr int T = B + 2;   // tile edge (vertices), x and y
+    static constexpr int TZ = BZ + 2;  // tile depth (3D)
+    static constexpr int CE = B + 1;  // cells per axis touching owned vertices (the cell index strides)
+    static constexpr int NCELL = DIM == 3 ? CE * CE * (BZ + 1) : CE * CE;
+    static constexpr int TVN = DIM == 3 ? T * T * TZ : T * T;
+    static constexpr int NOWN = DIM == 3 ? B * B * BZ : B * B;
+    static constexpr bool MVG = DIM == 3 && TGCU_MV_GLOBAL;  // m, v not staged in shared memory
     static constexpr int NT = NOWN;   // one thread per owned vertex
     static constexpr int CH = NT;     // points per chunk
     static constexpr int REC = 8;     // floats per point record
@@ -79,11 +82,11 @@ struct BinArgs {
 // grid's brick indices, dropping bricks outside a slab grid's layers.
 template <int DIM>
 __device__ __forceinline__ int point_brick_code(const DevSpec& s, const BinArgs& A, const float4& q) {
-    constexpr int B = BrickShape<DIM>::B;
     const float pf[3] = {q.x, q.y, q.z};
     int lo[3] = {0, 0, 0}, mask = 0;
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
+        const int B = a == 2 ? BrickShape<DIM>::BZ : BrickShape<DIM>::B;
         const double x = (double)pf[a];
         if (isnan(x)) return -1;
         double local;
@@ -570,10 +573,10 @@ struct BrickSmem {
     // before vertex o-1 (a 16-byte-aligned element offset, as o*K is), the
     // owned boxes B*K floats from vertex o.
     static constexpr bool TMAP = (S::B * K * 4) % 16 == 0 && TROWF <= 256;
-    static constexpr int TROWS = DIM == 3 ? S::T * S::T : S::T;
+    static constexpr int TROWS = DIM == 3 ? S::T * S::TZ : S::T;
     static constexpr int r32(int x) { return (x + 31) / 32 * 32; }
     static constexpr int tile = r32(TROWS * TROWF);               // floats
-    static constexpr int mv = r32(2 * S::NOWN * K);               // m then v
+    static constexpr int mv = S::MVG ? 0 : r32(2 * S::NOWN * K);  // m then v
     static constexpr int REC = ((3 * DIM + 1) + 1) / 2 * 2;       // s0[D] s1[D] u g[D] (even)
     static constexpr int pts = S::CH * REC;                       // cell-ordered records
     static constexpr int gs = S::NOWN * K;
@@ -602,7 +605,7 @@ __device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, flo
     constexpr int GR = (K % 2 == 0) ? 2 : 1;
     constexpr unsigned TBYTES = ((L::SHF * 4 + T * K * 4 + 15) / 16) * 16;
     constexpr unsigned OBYTES = B * K * 4;
-    constexpr int OROWS = DIM == 3 ? B * B : B;
+    constexpr int OROWS = DIM == 3 ? B * S::BZ : B;
     static_assert(L::TROWS + 2 * OROWS <= S::NT, "one staging row per thread");
     const long long nc_bytes = (long long)A.s.res[0] * A.s.res[1] * (DIM == 3 ? A.s.zstore : 1) * K * 4;
     unsigned tx_tile = 0, tx_mv = 0;
@@ -627,7 +630,7 @@ __device__ __forceinline__ void stage_brick(const StepArgs& A, const int* o, flo
                 }
             }
         }
-    } else if (tid < L::TROWS + 2 * OROWS) {
+    } else if (!S::MVG && tid < L::TROWS + 2 * OROWS) {
         const int t = tid - L::TROWS;
         const int which = t / OROWS, r = t - which * OROWS;
         const int ly = r % B, lz = DIM == 3 ? r / B : 0;
@@ -682,7 +685,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 constexpr int kTiny = 32;
 
 template <int DIM, int ORDER, bool EIK, bool EXPORT, bool TINYOK, bool SPLIT = false>
-__global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __grid_constant__ StepArgs A) {
+__global__ void __launch_bounds__(BrickShape<DIM>::NT, DIM == 3 ? 1024 / BrickShape<DIM>::NT : 2) k_brick_step(const __grid_constant__ StepArgs A) {
     using S = BrickShape<DIM>;
     using L = BrickSmem<DIM, ORDER>;
     constexpr int K = KOf<DIM, ORDER>::value;
@@ -731,7 +734,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     unsigned long long pt_tile = 0, pt_2a = 0, pt_scan = 0, pt_bal = 0, pt_2b = 0, pt_x;
 #endif
     // grid = (nb_x, nb_y, nb_z): brick coordinates without integer division
-    const int o[3] = {bcx * B, bcy * B, DIM == 3 ? (A.zb0 + bcz) * B : 0};
+    const int o[3] = {bcx * B, bcy * B, DIM == 3 ? (A.zb0 + bcz) * S::BZ : 0};
     const int zrel = o[2] - A.s.zoff;  // first owned plane in the stored planes
     const bool tmap = L::TMAP && A.use_tmap;
     // m and v are needed only by the epilogue: a brick with points issues their
@@ -757,10 +760,15 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         // m and v only in rank 0, which alone runs TV + Adam)
         if (tid == 0 && (crank == 0 || nmine > 0)) {
             mbar_expect_tx(&bars[0], L::tile_box_bytes);
-            if (crank == 0 && !mv_late) mbar_expect_tx(&bars[1], 2 * L::own_box_bytes);
+            if (crank == 0 && !mv_late && !S::MVG) mbar_expect_tx(&bars[1], 2 * L::own_box_bytes);
             if constexpr (DIM == 3) {
                 tma_load_3d(tile, &A.tm_tile, &bars[0], (o[0] - 1) * K - L::SHF, o[1] - 1, zrel - 1);
-                if (crank == 0 && !mv_late) {
+                if (S::MVG) {
+                    if (crank == 0 && !mv_late) {
+                        tma_prefetch_3d(&A.tm_m_in, o[0] * K, o[1], zrel);
+                        tma_prefetch_3d(&A.tm_v_in, o[0] * K, o[1], zrel);
+                    }
+                } else if (crank == 0 && !mv_late) {
                     tma_load_3d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1], zrel);
                     tma_load_3d(mvs + S::NOWN * K, &A.tm_v_in, &bars[1], o[0] * K, o[1], zrel);
                 }
@@ -774,7 +782,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         }
     } else {
         using LS = BrickSmem<DIM, ORDER>;
-        constexpr int OR = DIM == 3 ? B * B : B;
+        constexpr int OR = DIM == 3 ? B * S::BZ : B;
         stage_brick<DIM, ORDER>(A, o, tile, mvs, &bars[0], &bars[1], tid);
         // threads that did not arrive on a barrier (no row of it) arrive now
         const bool tile_row = tid < LS::TROWS && [&] {
@@ -782,7 +790,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             const int vy = o[1] - 1 + ty, vz = o[2] - 1 + tz;
             return vy >= 0 && vy < A.s.res[1] && (DIM == 2 || (vz >= 0 && vz < A.s.res[2]));
         }();
-        const bool mv_row = tid >= LS::TROWS && tid < LS::TROWS + 2 * OR && [&] {
+        const bool mv_row = !S::MVG && tid >= LS::TROWS && tid < LS::TROWS + 2 * OR && [&] {
             const int t = tid - LS::TROWS, r = t % OR;
             const int ly = r % B, lz = DIM == 3 ? r / B : 0;
             return o[1] + ly < A.s.res[1] && (DIM == 2 || o[2] + lz < A.s.res[2]);
@@ -793,6 +801,11 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
 
     auto issue_mv_late = [&] {  // thread 0, after its warp saw the tile land
         if (mv_late && tid == 0) {
+            if constexpr (S::MVG) {  // into L2 only: the epilogue reads them from HBM
+                tma_prefetch_3d(&A.tm_m_in, o[0] * K, o[1], zrel);
+                tma_prefetch_3d(&A.tm_v_in, o[0] * K, o[1], zrel);
+                return;
+            }
             mbar_expect_tx(&bars[1], 2 * L::own_box_bytes);
             if constexpr (DIM == 3) {
                 tma_load_3d(mvs, &A.tm_m_in, &bars[1], o[0] * K, o[1], zrel);
@@ -1188,7 +1201,7 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
     }
     cp_async_wait<0>();
     if (nmine == 0 && warp == 0) mbar_wait(&bars[0], 0);  // brick without points: tile not yet waited for
-    if (warp == 0) mbar_wait(&bars[1], 0);  // m/v rows landed
+    if (!S::MVG && warp == 0) mbar_wait(&bars[1], 0);  // m/v rows landed
     __syncthreads();
     TGCU_PT(pt_e1)
     double tv_sum = 0.0;
@@ -1204,8 +1217,12 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                 ((DIM == 3 ? (long long)(g3[2] - A.s.zoff) * A.s.sz : 0LL) + (long long)g3[1] * A.s.sy + g3[0]) * K;
             const float* tp = tile + L::at(1 + l3[0], 1 + l3[1], DIM == 3 ? 1 + l3[2] : 0);
             float* gs = Gs + v * K;
-            float* mm = mvs + v * K;
-            float* vv = mvs + S::NOWN * K + v * K;
+            // m, v of this vertex: staged rows in shared memory, or (MVG) HBM
+            // (prefetched into L2), new values stored straight to the out slot
+            const float* mi = S::MVG ? A.m_in + gidx : mvs + v * K;
+            const float* vi = S::MVG ? A.v_in + gidx : mvs + S::NOWN * K + v * K;
+            float* mo = S::MVG ? A.m_out + gidx : mvs + v * K;
+            float* vo = S::MVG ? A.v_out + gidx : mvs + S::NOWN * K + v * K;
             constexpr int offs[3] = {K, L::TROWF, DIM == 3 ? T * L::TROWF : 0};
             bool hi[DIM], lo[DIM];
 #pragma unroll
@@ -1244,6 +1261,12 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                 // makes the sum non-finite); the channel scan runs only then
                 float2 gsum = make_float2(0.f, 0.f);
                 float2 gkeep[K / 2];
+                float2 m2[K / 2], v2[K / 2];  // all loads issued before the channel loop
+#pragma unroll
+                for (int q = 0; q < K; q += 2) {
+                    m2[q / 2] = *reinterpret_cast<const float2*>(mi + q);
+                    v2[q / 2] = *reinterpret_cast<const float2*>(vi + q);
+                }
 #pragma unroll
                 for (int q = 0; q < K; q += 2) {
                     const float2 pv = *reinterpret_cast<const float2*>(tp + q);
@@ -1252,11 +1275,10 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                     gsum = __fadd2_rn(gsum, gi);
                     if constexpr (EXPORT) *reinterpret_cast<float2*>(A.grad_out + gidx + q) = gi;
                     // Adam (adam.cpp:36-55), fp32 state, host fp64 bias corrections
-                    const float2 mn = __ffma2_rn(b1, *reinterpret_cast<const float2*>(mm + q), __fmul2_rn(cc1, gi));
-                    const float2 vn = __ffma2_rn(b2, *reinterpret_cast<const float2*>(vv + q),
-                                                 __fmul2_rn(cc2, __fmul2_rn(gi, gi)));
-                    *reinterpret_cast<float2*>(mm + q) = mn;
-                    *reinterpret_cast<float2*>(vv + q) = vn;
+                    const float2 mn = __ffma2_rn(b1, m2[q / 2], __fmul2_rn(cc1, gi));
+                    const float2 vn = __ffma2_rn(b2, v2[q / 2], __fmul2_rn(cc2, __fmul2_rn(gi, gi)));
+                    *reinterpret_cast<float2*>(mo + q) = mn;
+                    *reinterpret_cast<float2*>(vo + q) = vn;
                     const float2 stp = make_float2(lr_bc1 * mn.x * fast_rcp(fast_sqrt(vn.x * A.inv_bc2) + A.eps),
                                                    lr_bc1 * mn.y * fast_rcp(fast_sqrt(vn.y * A.inv_bc2) + A.eps));
                     *reinterpret_cast<float2*>(gs + q) = __fadd2_rn(pv, make_float2(-stp.x, -stp.y));
@@ -1288,10 +1310,10 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
                     const float gi = fmaf(A.tv_gscale, gt, ident ? G[q] : gs[q]);
                     if constexpr (EXPORT) A.grad_out[gidx + q] = gi;
                     if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
-                    const float mn = fmaf(A.b1, mm[q], c1 * gi);
-                    const float vn = fmaf(A.b2, vv[q], c2 * gi * gi);
-                    mm[q] = mn;
-                    vv[q] = vn;
+                    const float mn = fmaf(A.b1, mi[q], c1 * gi);
+                    const float vn = fmaf(A.b2, vi[q], c2 * gi * gi);
+                    mo[q] = mn;
+                    vo[q] = vn;
                     gs[q] = pv - lr_bc1 * mn * fast_rcp(fast_sqrt(vn * A.inv_bc2) + A.eps);
                 }
                 tv_sum = (double)sq;
@@ -1329,8 +1351,10 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
         if (tid == 0) {
             if constexpr (DIM == 3) {
                 tma_store_3d(&A.tm_p_out, uni, o[0] * K, o[1], zrel);
-                tma_store_3d(&A.tm_m_out, mvs, o[0] * K, o[1], zrel);
-                tma_store_3d(&A.tm_v_out, mvs + S::NOWN * K, o[0] * K, o[1], zrel);
+                if (!S::MVG) {
+                    tma_store_3d(&A.tm_m_out, mvs, o[0] * K, o[1], zrel);
+                    tma_store_3d(&A.tm_v_out, mvs + S::NOWN * K, o[0] * K, o[1], zrel);
+                }
             } else {
                 tma_store_2d(&A.tm_p_out, uni, o[0] * K, o[1]);
                 tma_store_2d(&A.tm_m_out, mvs, o[0] * K, o[1]);
@@ -1339,11 +1363,11 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, 2) k_brick_step(const __g
             bulk_commit();
         }
     } else {
-        constexpr int OROWS = DIM == 3 ? B * B : B;
+        constexpr int OROWS = DIM == 3 ? B * S::BZ : B;
         constexpr int ROWF = B * K;
         const int nvx = min(B, A.s.res[0] - o[0]);
         const int rowf = nvx * K;
-        if (tid < 3 * OROWS) {
+        if (tid < (S::MVG ? 1 : 3) * OROWS) {
             const int which = tid / OROWS, r = tid - which * OROWS;
             const int ly = r % B, lz = DIM == 3 ? r / B : 0;
             const int gy = o[1] + ly, gz = o[2] + lz;
@@ -1449,13 +1473,14 @@ static void ensure_tmaps(Grid& g, bool layout_ok, unsigned tile_row_floats) {
     g.tm_state = -1;
     if (!layout_ok || ((int64_t)g.ds.res[0] * g.K * 4) % 16 != 0) return;
     const int B = g.spec.dim == 3 ? kBrick3 : kBrick2;
+    const unsigned BZ = g.spec.dim == 3 ? (unsigned)kBrickZ3 : 1u;
     const unsigned T = (unsigned)B + 2;
     bool ok = true;
     for (int i = 0; i < 2; ++i) {
-        ok = ok && encode_grid_map(&g.tm_tile[i], g, g.p[i], tile_row_floats, T);
-        ok = ok && encode_grid_map(&g.tm_own_p[i], g, g.p[i], (unsigned)B * g.K, (unsigned)B);
-        ok = ok && encode_grid_map(&g.tm_own_m[i], g, g.m[i], (unsigned)B * g.K, (unsigned)B);
-        ok = ok && encode_grid_map(&g.tm_own_v[i], g, g.v[i], (unsigned)B * g.K, (unsigned)B);
+        ok = ok && encode_grid_map(&g.tm_tile[i], g, g.p[i], tile_row_floats, T, BZ + 2);
+        ok = ok && encode_grid_map(&g.tm_own_p[i], g, g.p[i], (unsigned)B * g.K, (unsigned)B, BZ);
+        ok = ok && encode_grid_map(&g.tm_own_m[i], g, g.m[i], (unsigned)B * g.K, (unsigned)B, BZ);
+        ok = ok && encode_grid_map(&g.tm_own_v[i], g, g.v[i], (unsigned)B * g.K, (unsigned)B, BZ);
     }
     if (ok) g.tm_state = 1;
 }
@@ -1706,9 +1731,9 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     A.peer_lo = g.peer_lo[out_idx];
     A.peer_hi = g.peer_hi[out_idx];
     {
-        const int own_hi = std::min(g.spec.res[2], kBrick3 * (g.zb0 + g.nb[2]));
-        A.peer_hi_zb = (own_hi - 1) / kBrick3;
-        A.peer_hi_lz = (own_hi - 1) % kBrick3;
+        const int own_hi = std::min(g.spec.res[2], kBrickZ3 * (g.zb0 + g.nb[2]));
+        A.peer_hi_zb = (own_hi - 1) / kBrickZ3;
+        A.peer_hi_lz = (own_hi - 1) % kBrickZ3;
     }
     const bool eik = cfg.lambda1 > 0.0;
     FinArgs F;
