@@ -55,5 +55,5 @@ def test_deterministic_runs_are_bit_identical(case):
         assert np.array_equal(x[2], y[2]), "loss traces differ"
     # the canonical order changes only the fp32 summation order
     r = _run(spec, batches, False)
-    assert np.allclose(r[2], a[2], rtol=1e-6, atol=1e-30)
+    assert np.allclose(r[2], a[2], rtol=1e-5, atol=1e-30)  # (up to 10 steps of differently ordered sums)
     assert_trajectory_close(a[0], r[0], 1e-2, len(batches), what="deterministic vs regular")
