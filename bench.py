@@ -264,6 +264,120 @@ def cpu_baseline_train(wl, batches, steps=2):
             "seconds": secs, "loss_last": float(terms[-1, 0])}
 
 
+def stages_leg(device, hbm_peak, cpu=True):
+    """SURVEY 8(f) rows on this GPU next to the reference's own code: upsample
+    (128^3 -> 256^3 order 2), sample_grid_field (256^3 order-2 grid on a 256^3
+    lattice) and the radiance photometric loss with density and SH gradients
+    (128^3 grids, 2^16 rays x 64 samples). Device inputs resident, CUDA events
+    after warm-up; algorithmic bytes: upsample 4K (old + new vertices), lattice
+    4 B per value + 4K B per grid vertex (each read once). The reference
+    (oracle/_ref, one thread) runs a bounded sample of each."""
+    import ctypes as C
+    import torch
+    import paper_2402_14415_b200 as tg
+    from paper_2402_14415_b200.radiance import _RO, make_rays
+    dev = f"cuda:{device}"
+    L = tg.lib()
+
+    def timed(fn, reps=10):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    big = tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.1, seed=1, memory_cap_bytes=1 << 40)
+    R = None
+    if cpu:
+        from oracle.pyoracle import Reference, Spec, reference_available
+        R = Reference() if reference_available() else None
+    out = {}
+    # upsample
+    a, b = 128, 256
+    g = tg.init_grid(tg.GridSpec(dim=3, resolution=(a,) * 3, order=2), big, device=device)
+    dst = tg.init_grid(tg.GridSpec(dim=3, resolution=(b,) * 3, order=2), tg.InitOptions(memory_cap_bytes=1 << 40),
+                       device=device)
+    ms = timed(lambda: tg._check(L.tgcu_grid_upsample(g.handle, dst.handle, tg.TGCU_ASYNC, None)))
+    byt = 4 * 10 * (a ** 3 + b ** 3)
+    up = {"grid": [a, b], "order": 2, "ms": ms, "achieved_gbs": byt / ms / 1e6, "frac": byt / ms / 1e6 / hbm_peak,
+          "new_vertices_per_s": b ** 3 / (ms * 1e-3)}
+    del g, dst
+    if R is not None:
+        sa, sb = 64, 128
+        s = Spec(dim=3, res=(sa,) * 3, order=2)
+        c = np.random.default_rng(1).normal(0.0, 0.1, s.V * s.K)
+        t0 = time.perf_counter()
+        R.upsample(s, c, (sb,) * 3)
+        dt = time.perf_counter() - t0
+        up["cpu_baseline"] = {"value": sb ** 3 / dt, "unit": "new vertices/s", "cores": 1, "kind": "reference",
+                              "sample": f"tg::upsample {sa}^3 -> {sb}^3 order 2", "seconds": dt}
+    out["upsample"] = up
+    # lattice query
+    gres, lat = 256, 256
+    g = tg.init_grid(tg.GridSpec(dim=3, resolution=(gres,) * 3, order=2), big, device=device)
+    vals = torch.empty(lat ** 3, dtype=torch.float32, device=dev)
+    ms = timed(lambda: tg.sample_grid_field(g, (lat,) * 3, out=vals))
+    byt = 4 * lat ** 3 + 4 * 10 * gres ** 3
+    lq = {"grid": gres, "lattice": lat, "order": 2, "ms": ms, "achieved_gbs": byt / ms / 1e6,
+          "frac": byt / ms / 1e6 / hbm_peak, "gvalues_per_s": lat ** 3 / ms / 1e6}
+    del g, vals
+    if R is not None:
+        s = Spec(dim=3, res=(64,) * 3, order=2)
+        c = np.random.default_rng(2).normal(0.0, 0.1, s.V * s.K)
+        t0 = time.perf_counter()
+        R.sample_grid_field(s, c, (128,) * 3)
+        dt = time.perf_counter() - t0
+        lq["cpu_baseline"] = {"value": 128 ** 3 / dt, "unit": "values/s", "cores": 1, "kind": "reference",
+                              "sample": "tg::sample_grid_field, 64^3 order-2 grid, 128^3 lattice", "seconds": dt}
+    out["lattice_query"] = lq
+    # radiance photometric loss with gradients
+    res, deg, n, ns = 128, 2, 1 << 16, 64
+    g = tg.init_grid(tg.GridSpec(dim=3, resolution=(res,) * 3, order=2),
+                     tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=1.0, seed=3), device=device)
+    ss = tg.GridSpec(dim=3, resolution=(res,) * 3, order=0)
+    gen = torch.Generator(device=dev).manual_seed(5)
+    shc = torch.randn(res ** 3 * (deg + 1) ** 2 * 3, device=dev, generator=gen) * 0.5
+    rng = np.random.default_rng(0)
+    o = rng.uniform(-0.9, 0.9, (n, 3))
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    rays = torch.from_numpy(make_rays(o, d, 0.0, 1.0)).to(dev)
+    gt = torch.rand((n, 3), device=dev, generator=gen)
+    gd = torch.zeros(g.coeff_total(), device=dev)
+    gs = torch.zeros_like(shc)
+    ro = _RO(ns, 0, -10.0, (C.c_double * 3)(1.0, 1.0, 1.0), 0, 0)
+    loss = C.c_double()
+    spec = ss._c()
+    ms = timed(lambda: tg._check(L.tgcu_photometric_loss(
+        g.handle, C.byref(spec), deg, C.c_void_p(shc.data_ptr()), C.c_void_p(rays.data_ptr()),
+        C.c_void_p(gt.data_ptr()), n, C.cast(C.pointer(ro), C.c_void_p), None, None, C.c_void_p(gd.data_ptr()),
+        C.c_void_p(gs.data_ptr()), C.byref(loss), 0, None)), reps=5)
+    rad = {"grid": res, "sh_degree": deg, "rays": n, "samples_per_ray": ns, "ms": ms,
+           "gsamples_per_s": n * ns / ms / 1e6, "note": "loss + density and SH gradients (profiles/r02_rays_ncu.md)"}
+    del g, shc, gd, gs
+    if R is not None:
+        m, r2 = 2048, 64
+        ds = Spec(dim=3, res=(r2,) * 3, order=2)
+        sss = Spec(dim=3, res=(r2,) * 3, order=0)
+        dc = np.random.default_rng(3).normal(0.0, 1.0, ds.V * ds.K)
+        sc = np.random.default_rng(4).normal(0.0, 0.5, sss.V * 3 * (deg + 1) ** 2)
+        rr = {"origins": o[:m], "dirs": d[:m], "near": np.zeros(m), "far": np.ones(m), "gt": rng.random((m, 3))}
+        t0 = time.perf_counter()
+        R.photometric_loss(ds, dc, sss, deg, sc, rr, n_samples=ns, want_grad=True)
+        dt = time.perf_counter() - t0
+        rad["cpu_baseline"] = {"value": m * ns / dt, "unit": "samples/s", "cores": 1, "kind": "reference",
+                               "sample": f"tg::photometric_loss with gradients, {m} rays x {ns} samples, "
+                                         f"{r2}^3 grids", "seconds": dt}
+    out["radiance"] = rad
+    torch.cuda.empty_cache()
+    return out
+
+
 def cpu_baseline_query(order, pts_host):
     """The reference's query path (parallel_for + tg::eval, taylor_grid.cpp:197-203)
     on the C4 512^3 grid (built by the reference's init_grid, SmallUniform),
@@ -528,6 +642,7 @@ def main():
     ap.add_argument("--no-query", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C1 / C3 / C5 step timings")
+    ap.add_argument("--no-stages", action="store_true", help="skip the 8(f) legs (upsample, lattice, radiance)")
     ap.add_argument("--e2e-steps", type=int, default=500)
     ap.add_argument("--gen-batches", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--gen-seed", type=int, default=1000, help=argparse.SUPPRESS)
@@ -713,6 +828,8 @@ def main():
                 if ent["config"] in ("c3", "c5"):
                     ent["cpu_baseline"] = cpu_baseline_train(ent["config"], make_batches(ent["config"], 500, 2),
                                                              steps=1)
+    if rank == 0 and ws == 1 and not args.no_stages:
+        line["stages"] = stages_leg(dev, hbm_peak, cpu=not args.no_cpu_baseline)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline_train(wl, host_batches)
         if cb is not None:
