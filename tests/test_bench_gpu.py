@@ -32,6 +32,10 @@ def test_bench_single_gpu_contract():
     assert d["gpu_launches"] == 5 * 20  # 3 binning kernels + brick step + finalize per step
     assert 0 < d["roofline"]["frac"] < 1 and d["e2e"]["h2d_bytes_per_step"] == 16 << 20
     assert "workload" in d["config"]
+    st = d["stages"]  # the 8(f) legs (no reference samples with --no-cpu-baseline)
+    assert st["upsample"]["ms"] > 0 and 0 < st["upsample"]["frac"] < 1
+    assert st["lattice_query"]["ms"] > 0 and 0 < st["lattice_query"]["frac"] < 1
+    assert st["radiance"]["gsamples_per_s"] > 0
 
 
 def test_bench_two_rank_slab_flow():
