@@ -361,7 +361,8 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         TGCU_CUDA(cudaMalloc(&g.bin_count, sizeof(int) * (g.NB + 1)));
         for (int i = 0; i < 2; ++i) {
             TGCU_CUDA(cudaMalloc(&g.bin_off[i], sizeof(int) * (g.NB + 1)));
-            TGCU_CUDA(cudaMalloc(&g.brick_order[i], sizeof(int) * (g.NB + 2)));
+            // NB + 2 ints (order, class counters), then NB int4 (brick, first, end)
+            TGCU_CUDA(cudaMalloc(&g.brick_order[i], sizeof(int) * ((g.NB + 2 + 3) / 4 * 4) + sizeof(int) * 4 * g.NB));
         }
         TGCU_CUDA(cudaMalloc(&g.bin_cursor, sizeof(int) * (g.NB + 1)));
         TGCU_CUDA(cudaMalloc(&g.partials, sizeof(double) * 4 * g.NB));

@@ -133,7 +133,13 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs A) {
 // (they take 4-7x as long, so the kernel should not end on one), the rest
 // after them. ord[NB], ord[NB + 1] count the two classes (zeroed per step);
 // one atomic per warp and class.
-__device__ __forceinline__ void place_brick(int brick, bool valid, int count, int ch, int NB, int* __restrict__ ord) {
+// The brick kernel reads its brick and point range as one 16-byte record
+// (info = int4 (brick, first, end, 0) per launch slot, after the NB + 2 ints).
+__device__ __forceinline__ int4* order_info(int* ord, int NB) {
+    return reinterpret_cast<int4*>(ord + ((NB + 2 + 3) & ~3));
+}
+__device__ __forceinline__ void place_brick(int brick, bool valid, int count, int ch, int NB, int* __restrict__ ord,
+                                            int first) {
     const int lane = threadIdx.x & 31;
     const bool heavy = valid && count > ch, light = valid && count <= ch;
     const unsigned mh = __ballot_sync(0xffffffffu, heavy), ml = __ballot_sync(0xffffffffu, light);
@@ -145,12 +151,18 @@ __device__ __forceinline__ void place_brick(int brick, bool valid, int count, in
     bh = __shfl_sync(0xffffffffu, bh, 0);
     bl = __shfl_sync(0xffffffffu, bl, 0);
     const unsigned lt = (1u << lane) - 1u;
-    if (heavy) ord[bh + __popc(mh & lt)] = brick;
-    if (light) ord[NB - 1 - (bl + __popc(ml & lt))] = brick;
+    const int slot = heavy ? bh + __popc(mh & lt) : NB - 1 - (bl + __popc(ml & lt));
+    if (heavy || light) {
+        ord[slot] = brick;
+        order_info(ord, NB)[slot] = make_int4(brick, first, first + count, 0);
+    }
 }
 
 __global__ void k_identity_order(int* __restrict__ ord, int NB) {
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < NB; b += gridDim.x * blockDim.x) ord[b] = b;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < NB; b += gridDim.x * blockDim.x) {
+        ord[b] = b;
+        order_info(ord, NB)[b] = make_int4(b, 0, 0, 0);
+    }
 }
 
 // Exclusive scan of NB brick counts -> off[0..NB], cursor = off. One CTA.
@@ -187,7 +199,7 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const int* __restrict__ count
             off[i] = excl;
             cursor[i] = excl;
         }
-        place_brick(i, i < NB, c, ch, NB, ord);
+        place_brick(i, i < NB, c, ch, NB, ord, excl);
         __syncthreads();
         if (threadIdx.x == blockDim.x - 1) carry = excl + c;
         __syncthreads();
@@ -350,7 +362,7 @@ __global__ void __launch_bounds__(256) k_bin_cols(int* __restrict__ H, int ncta,
         const int c0 = prev;
         if (lane < nb) off[b0 + lane] = c0 + x - t;
         if (tile == (int)gridDim.x - 1 && lane == 0) off[NB] = c0 + block_sum;
-        place_brick(b0 + lane, lane < nb, t, chunk, NB, ord);
+        place_brick(b0 + lane, lane < nb, t, chunk, NB, ord, c0 + x - t);
     }
 }
 
@@ -518,7 +530,8 @@ struct StepArgs {
     float* peer_lo;
     float* peer_hi;
     int peer_hi_zb, peer_hi_lz;
-    const int* order;  // launch order of the bricks (1D grid): most chunks first
+    const int* order;  // launch order of the bricks (1D grid): most chunks first (+ order_info)
+    int NB;
     int det;           // deterministic mode: canonical record order inside every cell run
     int split;         // CTAs per brick (a thread-block cluster along x; 1 = one CTA per brick)
 };
@@ -702,10 +715,12 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, DIM == 3 ? 1024 / BrickSh
     const int SPL = SPLIT ? A.split : 1;
     int crank = 0;
     if constexpr (SPLIT) crank = (int)cg::this_cluster().block_rank();
-    const int b = A.order[blockIdx.x / SPL];
+    // brick and point range in one load (no dependent off[] lookup)
+    const int4 bi = order_info(const_cast<int*>(A.order), (int)A.NB)[blockIdx.x / SPL];
+    const int b = bi.x;
     const int bcx = b % A.nb[0], bcy = (b / A.nb[0]) % A.nb[1], bcz = b / (A.nb[0] * A.nb[1]);
     const int err = A.st->error;
-    const int p0 = A.off[b], p1 = A.off[b + 1];
+    const int p0 = bi.y, p1 = bi.z;
     // (st->error is written only by the finalize of an earlier step, ordered
     // before this kernel: every CTA of a split cluster sees the same value)
     if (err) return;
@@ -1728,6 +1743,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     A.grad_out = grad_out;
     A.zb0 = g.zb0;
     A.order = g.brick_order[k];
+    A.NB = (int)g.NB;
     A.peer_lo = g.peer_lo[out_idx];
     A.peer_hi = g.peer_hi[out_idx];
     {
