@@ -67,7 +67,7 @@ def run(name, steps, warmup):
     g.sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if cfg.get("dim", 3) == 2:
-        steps = max(steps, 400)  # C1 steps take ~25 us: a longer window
+        steps = max(steps, 4000)  # C1 steps take ~25 us: a longer window
     e0.record()
     for i in range(steps):
         tg.train_step(g, dev[i % 2], lc, asynchronous=True, input_ready=True)
