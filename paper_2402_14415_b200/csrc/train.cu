@@ -1782,7 +1782,9 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         A.tm_v_out = g.tm_own_v[out_idx];
     }
     // Split bricks over a cluster of CTAs when the grid has fewer bricks than
-    // CTA slots (2 per SM): the largest power of two <= 8 that still fits.
+    // SMs: the largest power of two <= 8 that keeps one CTA per SM (C1, 64
+    // bricks: split 2, 22.6 us per step; split 4 on two CTA slots per SM:
+    // 23.9 us).
     int split = 1;
 #ifndef TGCU_SPLIT_OFF
     if (A.use_tmap) {
@@ -1790,7 +1792,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         if (!sms) TGCU_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g.device));
         const char* ev = std::getenv("TGCU_SPLIT");
         const int cap = ev ? std::max(1, std::min(8, std::atoi(ev))) : 8;
-        while (split * 2 <= cap && g.NB * (int64_t)split * 2 <= 2LL * sms) split *= 2;
+        while (split * 2 <= cap && g.NB * (int64_t)split * 2 <= (int64_t)sms) split *= 2;
     }
 #endif
     A.split = split;
