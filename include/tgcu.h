@@ -368,6 +368,22 @@ int tgcu_run_schedule(tgcu_grid** grid, const tgcu_stage* stages, int nstages, c
  * or on when the environment has TGCU_DETERMINISTIC=1 at grid creation. */
 int tgcu_grid_set_deterministic(tgcu_grid* g, int on);
 
+/* Fused-step path (no reference counterpart: an implementation choice behind
+ * tgcu_train_step). TGCU_STEP_BRICK: binning + the brick kernel + finalize
+ * (any grid). TGCU_STEP_SINGLE: the whole step as one cooperative launch
+ * (thread per point, gradients reduced in L2, thread per coefficient for TV +
+ * Adam) — for small grids such as BASELINE configs[0] (2D 128^2), where the
+ * brick path's five launches are latency-bound. TGCU_STEP_AUTO (default)
+ * takes the single launch for grids with fewer bricks than SMs, at most 2^20
+ * coefficients and 2^18 points per step, and never for slab grids or in
+ * deterministic mode. Environment TGCU_STEP_PATH=brick|single at grid
+ * creation sets the same. Results agree within the fused step's tolerances
+ * (summation order of the gradient differs). */
+#define TGCU_STEP_AUTO 0
+#define TGCU_STEP_BRICK 1
+#define TGCU_STEP_SINGLE 2
+int tgcu_grid_set_step_path(tgcu_grid* g, int path);
+
 /* Collective phase of the profiled slab steps (those whose brick kernel
  * tgcu_profile_begin / _every times): summed device ms of the all-reduce of
  * the partials and of the halo exchange (0 with the fused peer-memory halo,

@@ -171,6 +171,7 @@ def lib():
     L.tgcu_train_step_fresh_eik.argtypes = [P, P, C.c_int64, P, C.POINTER(_Loss), C.POINTER(_Terms), C.c_int, P]
     L.tgcu_shuffle_order.argtypes = [C.c_uint64, C.c_int64, P]
     L.tgcu_grid_set_deterministic.argtypes = [P, C.c_int]
+    L.tgcu_grid_set_step_path.argtypes = [P, C.c_int]
     L.tgcu_slab_comm_profile.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int)]
     L.tgcu_comm_create.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(P)]
     L.tgcu_comm_destroy.argtypes = [P]
@@ -443,6 +444,15 @@ class TaylorGrid:
 
     def zero_grad(self):
         _check(lib().tgcu_grad_zero(self._h, C.c_void_p(self.grad_ptr()), None))
+
+    STEP_AUTO, STEP_BRICK, STEP_SINGLE = 0, 1, 2
+
+    def set_step_path(self, path: int):
+        """Fused-step path (tgcu_grid_set_step_path): STEP_AUTO, STEP_BRICK
+        (binning + brick kernel + finalize) or STEP_SINGLE (one cooperative
+        launch, for small grids such as BASELINE configs[0])."""
+        _check(lib().tgcu_grid_set_step_path(self._h, int(path)))
+        return self
 
     def set_deterministic(self, on: bool = True):
         """Bit-reproducible fused steps (tgcu_grid_set_deterministic): canonical

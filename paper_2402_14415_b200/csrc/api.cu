@@ -344,6 +344,9 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         TGCU_CUDA(cudaMemcpy(g.st, &st0, sizeof(Status), cudaMemcpyHostToDevice));
         // Brick decomposition (train.cu / query.cu).
         if (const char* det = std::getenv("TGCU_DETERMINISTIC")) g.deterministic = det[0] == '1';
+        if (const char* pdl = std::getenv("TGCU_SMALL_PDL")) g.small_pdl = pdl[0] != '0';
+        if (const char* sp = std::getenv("TGCU_STEP_PATH"))
+            g.step_path = std::string(sp) == "brick" ? 1 : (std::string(sp) == "single" ? 2 : 0);
         g.NB = 1;
         g.zb_global = nbz_global;
         g.code_sh[0] = code_sh[0];
@@ -447,6 +450,8 @@ int tgcu_grid_destroy(tgcu_grid* h) {
     cudaFree(g.bin_codes);
     cudaFree(g.bin_chain);
     cudaFree(g.partials);
+    cudaFree(g.sacc);
+    cudaFree(g.spart);
     cudaFree(g.d_trace);
     cudaFree(g.slab_red);
     cudaFreeHost(g.h_terms);
@@ -1330,6 +1335,14 @@ int tgcu_host_alloc(void** p, size_t bytes) {
 int tgcu_host_free(void* p) {
     return guard([&] {
         if (p) TGCU_CUDA(cudaFreeHost(p));
+    });
+}
+
+int tgcu_grid_set_step_path(tgcu_grid* h, int path) {
+    return guard([&] {
+        require(h != nullptr, "set_step_path: NULL grid");
+        require(path >= TGCU_STEP_AUTO && path <= TGCU_STEP_SINGLE, "set_step_path: path must be 0 (auto), 1 (brick) or 2 (single)");
+        h->g.step_path = path;
     });
 }
 

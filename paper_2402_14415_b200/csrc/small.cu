@@ -1,0 +1,400 @@
+// Two-launch fused training step for small grids (BASELINE configs[0], C1:
+// a 128^2 2D grid with 65,536 points per step, 64 bricks on 148 SMs).
+//
+// The brick path (train.cu) needs five launches per step (three binning
+// kernels, the brick kernel, the finalize), each latency-bound at this size
+// (DESIGN.md §9). Here one step of run_schedule's inner loop
+// (schedule.cpp:66-92: zero_grad -> total_loss -> finite check -> adam_step)
+// is two kernels chained by programmatic dependent launch (PDL: each grid is
+// scheduled while its predecessor runs and waits in griddepcontrol.wait for
+// its completion, so the launch latency between them is hidden):
+//   k_small_points  thread per point: fp64 locate (grid_spec.cpp:45-69), the
+//                   2^D corner blocks read straight from the L2-resident
+//                   parameters, the forward (taylor_grid.cpp:100-119), the fp64
+//                   per-point loss chain (sdf_loss.cpp:51-74) and each corner's
+//                   coefficient gradient (accumulate_cell,
+//                   taylor_grid.cpp:123-152) added into an fp32 accumulator
+//                   with vector reductions in L2 (red.global.add.v2/v4);
+//   k_small_coeffs  thread per coefficient (coalesced): TV gradient from the
+//                   parameter stencil (sdf_loss.cpp:161-210) + the accumulated
+//                   point gradient, the finite check, Adam (adam.cpp:36-55)
+//                   into the other ping-pong slot, the accumulator zeroed for
+//                   the next step ("fused with gradient zeroing"); the last CTA
+//                   to finish reduces every CTA's loss partials in CTA order
+//                   and commits (finalize.cuh, the brick path's code).
+// The kernel boundary is the grid-wide barrier, so nothing assumes that the
+// CTAs of a grid are co-resident (a cooperative single launch with an
+// in-kernel grid barrier measured 16.4 us per C1 step).
+// Summation order of a coefficient's point contributions follows the L2
+// atomics (not bit-reproducible); deterministic mode keeps the brick path.
+#include <climits>
+#include <cstdlib>
+
+#include "dispatch.cuh"
+#include "finalize.cuh"
+#include "tg_internal.h"
+#include "tma.cuh"
+
+namespace tgcu {
+
+struct SmallArgs {
+    DevSpec s;
+    const float4* pts;
+    int n;
+    int nc;  // coefficients V*K
+    const float* p_in;
+    float* p_out;
+    const float* m_in;
+    float* m_out;
+    const float* v_in;
+    float* v_out;
+    float* acc;       // fp32 point-gradient accumulator (zero between steps)
+    float* grad_out;  // optional: full gradient (TGCU_EXPORT_GRAD)
+    LossDev L;
+    float tv_gscale;
+    int want_tv;
+    float lr, b1, b2, eps, inv_bc1, inv_bc2, c1, c2;
+    double* partials;  // (points CTAs + coefficient CTAs) x 4: recon, eik, tv, points
+    int ncta_pts;      // CTAs of k_small_points (their partials come first)
+    Status* st;
+    unsigned long long* nan;
+    FinArgs F;
+    unsigned* ticket;  // coefficient CTAs done with their partials (zero between launches)
+};
+
+constexpr int kSmallNT = 256;
+
+#ifdef TGCU_PHASE_TIMING
+// Instrumented build only (tools/small_phase.py): per step, the first CTA
+// start and the last CTA end of each kernel.
+__device__ unsigned long long g_sring[256 * 4];
+#define TGCU_SRING(slot, op)                                                   \
+    if (threadIdx.x == 0) {                                                    \
+        unsigned long long t_;                                                 \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+        op(&g_sring[4 * (A.F.step & 255) + (slot)], t_);                       \
+    }
+#else
+#define TGCU_SRING(slot, op)
+#endif
+
+// PDL: wait until the previous grid on the stream has completed (its memory
+// operations visible); let the next grid be scheduled (once every CTA of
+// this grid has triggered or exited). Triggering only after the wait keeps at
+// most two grids of the chain resident at a time.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+// Block reduction of four doubles (fixed order) -> out[0..3].
+__device__ __forceinline__ void block_partials(double (*red)[kSmallNT / 32], double a, double b, double c, double d,
+                                               double* out) {
+    constexpr int NW = kSmallNT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double v4[4] = {warp_sum_d(a), warp_sum_d(b), warp_sum_d(c), warp_sum_d(d)};
+    if (lane == 0)
+        for (int k = 0; k < 4; ++k) red[k][warp] = v4[k];
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double s = 0.0;
+        for (int k = 0; k < NW; ++k) s += red[threadIdx.x][k];
+        out[threadIdx.x] = s;
+    }
+}
+
+template <int DIM, int ORDER, bool EIK>
+__global__ void __launch_bounds__(kSmallNT) k_small_points(const __grid_constant__ SmallArgs A) {
+    constexpr int K = KOf<DIM, ORDER>::value;
+    constexpr int NC = 1 << DIM;
+    __shared__ double red[4][kSmallNT / 32];
+    pdl_wait();
+    // When to let the coefficient grid be scheduled: in 2D both grids fit an
+    // SM together (2 x 256 x 80 + 256 x 64 registers), and an early trigger
+    // hides its launch (C1: 12.9 vs 16.2 us per step); in 3D (114 registers
+    // here) its CTAs resident beside this grid would halve this grid's
+    // occupancy (3D 48^3, 2^17 points: 63.3 vs 54.5 us per step), so it
+    // follows the points.
+    constexpr bool kEarly = DIM == 2;
+    if (kEarly) pdl_trigger();
+    // (st->error is written only by an earlier step's finalize)
+    if (A.st->error) return;
+    TGCU_SRING(0, atomicMin)
+    const int nthr = gridDim.x * kSmallNT;
+    const long long sy = A.s.sy, sz = A.s.sz;
+    double recon_sum = 0.0, eik_sum = 0.0;
+    int npts = 0;
+    for (int i = blockIdx.x * kSmallNT + threadIdx.x; i < A.n; i += nthr) {
+        const float4 q = __ldg(A.pts + i);
+        const float pf[3] = {q.x, q.y, q.z};
+        bool nanp = false;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) nanp |= isnan(pf[a]);
+        if (nanp) {  // dropped, reported by the finalize (as the binning does)
+            atomicMin(A.nan, (unsigned long long)i);
+            continue;
+        }
+        double lc[DIM];
+        AxisF ax[DIM];
+        long long base = 0;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            const int c = locate_axis(A.s, a, (double)pf[a], lc[a]);
+            base += (long long)c * (a == 0 ? 1LL : (a == 1 ? sy : sz));
+            ax[a] = axis_factors(A.s, a, lc[a]);
+        }
+        auto vid = [&](int c) {
+            return base + (c & 1) + ((c >> 1) & 1) * sy + (DIM == 3 ? ((c >> 2) & 1) * sz : 0LL);
+        };
+        float cb[NC][K];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) load_block<K, true>(A.p_in + vid(c) * K, cb[c]);
+        float f = 0.0f, fg[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) blend_corner<DIM, ORDER, EIK>(cb[c], corner_geom<DIM>(A.s, ax, c), f, fg);
+        double recon, eik;
+        float u, gv[DIM];
+        point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
+        recon_sum += recon;
+        eik_sum += eik;
+        ++npts;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            float G[K];
+#pragma unroll
+            for (int k2 = 0; k2 < K; ++k2) G[k2] = 0.0f;
+            corner_grad<DIM, ORDER, K>(corner_geom<DIM>(A.s, ax, c), u, gv, G);
+            red_block<K>(A.acc + vid(c) * K, G);
+        }
+    }
+    if (!kEarly) pdl_trigger();
+    block_partials(red, recon_sum, eik_sum, 0.0, (double)npts, A.partials + 4 * blockIdx.x);
+    TGCU_SRING(1, atomicMax)
+}
+
+template <int DIM, int ORDER, bool EXPORT>
+__global__ void __launch_bounds__(kSmallNT) k_small_coeffs(const __grid_constant__ SmallArgs A) {
+    constexpr int K = KOf<DIM, ORDER>::value;
+    __shared__ double red[4][kSmallNT / 32];
+    __shared__ int last;
+    pdl_wait();  // every point's reductions have landed in L2
+    pdl_trigger();
+    if (A.st->error) return;
+    TGCU_SRING(2, atomicMin)
+    const int nthr = gridDim.x * kSmallNT;
+    const int tid = threadIdx.x;
+    double tv_sum = 0.0;
+    {
+        const int r0 = A.s.res[0], r1 = A.s.res[1];
+        const int offs[3] = {K, r0 * K, r0 * r1 * K};
+        const float c1 = A.c1, c2 = A.c2, lr_bc1 = A.lr * A.inv_bc1;
+        // rounds of R coefficients per thread: every load of a round is
+        // issued before its arithmetic (the phase is L2-latency bound)
+        constexpr int R = 4;
+        for (int base = blockIdx.x * kSmallNT + tid; base < A.nc; base += R * nthr) {
+            float pv[R], pn[R][2 * DIM], pg[R], mi[R], vi[R];
+            unsigned nb[R];  // neighbour present: bit 2a = v+e_a, bit 2a+1 = v-e_a
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int idx = base + r * nthr;
+                const int j = idx < A.nc ? idx : 0;
+                const int vtx = j / K;
+                const int g3[3] = {vtx % r0, DIM == 3 ? (vtx / r0) % r1 : vtx / r0, DIM == 3 ? vtx / (r0 * r1) : 0};
+                nb[r] = 0;
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    const bool hi = A.want_tv && g3[a] + 1 < A.s.res[a], lo = A.want_tv && g3[a] >= 1;
+                    nb[r] |= (hi ? 1u : 0u) << (2 * a) | (lo ? 1u : 0u) << (2 * a + 1);
+                    pn[r][2 * a] = __ldg(A.p_in + (hi ? j + offs[a] : j));
+                    pn[r][2 * a + 1] = __ldg(A.p_in + (lo ? j - offs[a] : j));
+                }
+                pv[r] = __ldg(A.p_in + j);
+                pg[r] = __ldcg(A.acc + j);
+                mi[r] = __ldg(A.m_in + j);
+                vi[r] = __ldg(A.v_in + j);
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int idx = base + r * nthr;
+                if (idx >= A.nc) break;
+                float gt = 0.0f, sq = 0.0f;
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    if (nb[r] >> (2 * a) & 1u) {  // pair (v, v+e_a)
+                        const float d = pn[r][2 * a] - pv[r];
+                        sq = fmaf(d, d, sq);
+                        gt -= d;
+                    }
+                    if (nb[r] >> (2 * a + 1) & 1u) gt += pv[r] - pn[r][2 * a + 1];  // pair (v-e_a, v)
+                }
+                __stcg(A.acc + idx, 0.0f);
+                const float gi = fmaf(A.tv_gscale, gt, pg[r]);
+                if constexpr (EXPORT) A.grad_out[idx] = gi;
+                if (!isfinite(gi)) atomicMin(&A.st->bad_grad, (unsigned long long)idx);
+                const float mn = fmaf(A.b1, mi[r], c1 * gi);
+                const float vn = fmaf(A.b2, vi[r], c2 * gi * gi);
+                A.m_out[idx] = mn;
+                A.v_out[idx] = vn;
+                A.p_out[idx] = pv[r] - lr_bc1 * mn * fast_rcp(fast_sqrt(vn * A.inv_bc2) + A.eps);
+                tv_sum += (double)sq;
+            }
+        }
+    }
+    // per-CTA TV partial; the last CTA to finish reduces all partials (the
+    // points kernel's first, then these, in CTA order) and commits
+    block_partials(red, 0.0, 0.0, tv_sum, 0.0, A.partials + 4 * (A.ncta_pts + blockIdx.x));
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        last = atomicAdd(A.ticket, 1u) == gridDim.x - 1;
+        if (last) *A.ticket = 0u;  // every CTA has taken its ticket
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        finalize_body<kSmallNT>(A.F, red, tid);
+    }
+    TGCU_SRING(3, atomicMax)
+}
+
+bool small_step_eligible(const Grid& g, int64_t n) {
+    if (g.slab || g.deterministic) return false;
+    if (g.NC >= (int64_t)INT_MAX || n >= (int64_t)INT_MAX) return false;
+    if (g.step_path == 1) return false;
+    if (g.step_path == 2) return true;
+    // auto: grids with fewer bricks than SMs (the brick kernel cannot fill
+    // the GPU) whose state stays in L2, at batch sizes where the L2
+    // reductions stay cheap
+    return g.NB < 148 && g.NC <= (int64_t)kSmallMaxCoeffs && n <= kSmallMaxPoints;
+}
+
+static int sm_count(int device) {
+    static int cnt[64] = {};
+    int& c = cnt[device & 63];
+    if (!c) TGCU_CUDA(cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, device));
+    return c;
+}
+
+void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
+                       int in_idx, int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
+                       const BinInput& in, cudaStream_t s, bool fresh_eik) {
+    if (!g.sacc) {
+        TGCU_CUDA(cudaMalloc(&g.sacc, sizeof(float) * g.NC));
+        TGCU_CUDA(cudaMemsetAsync(g.sacc, 0, sizeof(float) * g.NC, s));
+    }
+    const int k = g.bin_set;  // the NaN slot of this step
+    g.bin_set ^= 1;
+    const bool eik = cfg.lambda1 > 0.0;
+    const void* kp = nullptr;
+    const void* kc = nullptr;
+    TGCU_DISPATCH(g.spec.dim, g.spec.order, {
+        kp = eik ? (const void*)k_small_points<DIM, ORDER, true> : (const void*)k_small_points<DIM, ORDER, false>;
+        kc = grad_out ? (const void*)k_small_coeffs<DIM, ORDER, true> : (const void*)k_small_coeffs<DIM, ORDER, false>;
+    });
+    // points: a thread per point (C1: 256 CTAs, 5.6 us; 148 CTAs with two
+    // points per thread measured 13 us); coefficients: one CTA per SM at most
+    // (rounds of 4 per thread)
+    const int sms = sm_count(g.device);
+    int pcap = 8192;
+    if (const char* ev = std::getenv("TGCU_SMALL_PCTAS")) pcap = std::max(1, std::atoi(ev));
+    const int np = (int)std::max<int64_t>(1, std::min<int64_t>(pcap, (n + kSmallNT - 1) / kSmallNT));
+    const int nq = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (g.NC + kSmallNT - 1) / kSmallNT));
+    if (g.spart_cap < 4 * (np + nq)) {
+        if (g.spart) TGCU_CUDA(cudaFree(g.spart));
+        // partials + the CTA ticket (one more double, zeroed once)
+        g.spart_cap = 4 * (np + nq);
+        TGCU_CUDA(cudaMalloc(&g.spart, sizeof(double) * (g.spart_cap + 1)));
+        TGCU_CUDA(cudaMemsetAsync(g.spart + g.spart_cap, 0, sizeof(double), s));
+    }
+    if (in.wait) TGCU_CUDA(cudaStreamWaitEvent(s, in.wait, 0));
+
+    SmallArgs A{};
+    A.s = g.ds;
+    A.pts = samples;
+    A.n = (int)n;
+    A.nc = (int)g.NC;
+    const int out_idx = 1 - in_idx;
+    A.p_in = g.p[in_idx];
+    A.p_out = g.p[out_idx];
+    A.m_in = g.m[in_idx];
+    A.m_out = g.m[out_idx];
+    A.v_in = g.v[in_idx];
+    A.v_out = g.v[out_idx];
+    A.acc = g.sacc;
+    A.grad_out = grad_out;
+    A.L.k = cfg.k;
+    A.L.inv_n = 1.0 / (double)n_norm;
+    A.L.eik_scale = cfg.lambda1;
+    A.L.use_weighting = cfg.use_weighting;
+    A.L.differentiate_weight = cfg.differentiate_weight;
+    A.L.fresh_eik = fresh_eik ? 1 : 0;
+    A.want_tv = cfg.use_tv ? 1 : 0;
+    A.tv_gscale = (cfg.use_tv && cfg.lambda2 > 0.0) ? (float)(2.0 * cfg.lambda2 * g.tv_inv_norm) : 0.0f;
+    A.lr = (float)g.adam.lr;
+    A.b1 = (float)g.adam.beta1;
+    A.b2 = (float)g.adam.beta2;
+    A.c1 = (float)(1.0 - g.adam.beta1);
+    A.c2 = (float)(1.0 - g.adam.beta2);
+    A.eps = (float)g.adam.eps;
+    A.inv_bc1 = (float)inv_bc1;
+    A.inv_bc2 = (float)inv_bc2;
+    A.partials = g.spart;
+    A.ncta_pts = np;
+    A.ticket = reinterpret_cast<unsigned*>(g.spart + g.spart_cap);
+    A.st = g.st;
+    A.nan = &g.st->nan_bin[k];
+    FinArgs& F = A.F;
+    F.partials = g.spart;
+    F.NB = np + nq;
+    F.n = (double)n_norm;
+    F.lambda1 = cfg.lambda1;
+    F.lambda2 = cfg.lambda2;
+    F.inv_norm = g.tv_inv_norm;
+    F.use_tv = cfg.use_tv;
+    F.want_eik = eik;
+    F.st = g.st;
+    F.nan = &g.st->nan_bin[k];
+    F.over = &g.st->det_over[k];
+    F.trace = g.d_trace;
+    F.step = step;
+    F.in_idx = in_idx;
+    F.t_after = t_after;
+    F.slab_out = nullptr;
+    F.reduced = nullptr;
+
+    g.prof_this = g.prof_on && (g.steps_launched % g.prof_every) == 0;
+    if (g.prof_this) prof_mark(g, s, 0);
+    void* args[] = {&A};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t lc{};
+    lc.blockDim = dim3(kSmallNT);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = s;
+    lc.attrs = at;
+    lc.numAttrs = g.small_pdl ? 1 : 0;
+    lc.gridDim = dim3((unsigned)np);
+    TGCU_CUDA(cudaLaunchKernelExC(&lc, kp, args));
+    lc.gridDim = dim3((unsigned)nq);
+    TGCU_CUDA(cudaLaunchKernelExC(&lc, kc, args));
+    if (g.prof_this) prof_mark(g, s, 1);
+    if (in.consumed) TGCU_CUDA(cudaEventRecord(in.consumed, s));
+    count_launch(2);
+}
+
+}  // namespace tgcu
+
+#ifdef TGCU_PHASE_TIMING
+extern "C" int tgcu_small_ring_dump(unsigned long long* out, int reset) {
+    if (reset) {
+        static unsigned long long init[256 * 4];
+        for (int i = 0; i < 256; ++i) {
+            init[4 * i] = init[4 * i + 2] = ~0ull;
+            init[4 * i + 1] = init[4 * i + 3] = 0ull;
+        }
+        return cudaMemcpyToSymbol(tgcu::g_sring, init, sizeof(init)) == cudaSuccess ? 0 : 6;
+    }
+    return cudaMemcpyFromSymbol(out, tgcu::g_sring, sizeof(unsigned long long) * 1024) == cudaSuccess ? 0 : 6;
+}
+#endif

@@ -189,6 +189,13 @@ struct Grid {
     // boundaries of one fused step, summed per segment after each step.
     bool bd_on = false;
     bool deterministic = false;  // canonical summation orders (tgcu_grid_set_deterministic)
+    // Fused-step path (tgcu_grid_set_step_path / TGCU_STEP_PATH): 0 auto,
+    // 1 brick kernel (train.cu), 2 small-grid path (small.cu).
+    int step_path = 0;
+    float* sacc = nullptr;       // small-grid step: fp32 gradient accumulator (NC, zero between steps)
+    double* spart = nullptr;     // small-grid step: per-CTA loss partials + CTA ticket
+    int spart_cap = 0;           // doubles
+    bool small_pdl = true;       // small-grid step: programmatic dependent launch (TGCU_SMALL_PDL=0 off)
     cudaEvent_t bd_ev[6] = {};
     double bd_sum[5] = {0, 0, 0, 0, 0};
     int bd_steps = 0;
@@ -254,6 +261,15 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
                        int in_idx,
                        int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
                        double* slab_out, const BinInput& in, cudaStream_t s, bool fresh_eik = false);
+// Two-launch fused step for small grids (small.cu): the auto rule's
+// limits (coefficients, points per step) and the launcher, same arguments as
+// launch_train_step without the slab phase.
+constexpr int64_t kSmallMaxCoeffs = int64_t(1) << 20;
+constexpr int64_t kSmallMaxPoints = int64_t(1) << 18;
+bool small_step_eligible(const Grid& g, int64_t n);
+void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
+                       int in_idx, int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
+                       const BinInput& in, cudaStream_t s, bool fresh_eik);
 // Fresh-uniform eikonal points (n x 3 floats, device) -> float4 records with
 // gt = kEikMark (tg_device.cuh), for the fused step's point list.
 void launch_pack_eik(const float* p3, int64_t n, float4* dst, cudaStream_t s);

@@ -39,6 +39,7 @@
 #include "dispatch.cuh"
 #include "tg_internal.h"
 #include "tma.cuh"
+#include "finalize.cuh"
 
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
@@ -393,112 +394,6 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_scatter_tiles(BinArgs A, co
     }
 }
 
-struct FinArgs {
-    const double* partials;
-    int NB;
-    double n;
-    double lambda1, lambda2, inv_norm;
-    int use_tv, want_eik;
-    Status* st;
-    unsigned long long* nan;  // NaN slot of the step's bin set
-    unsigned long long* over; // deterministic-sort overflow slot of the step's bin set
-    tgcu_loss_terms* trace;
-    long long step;
-    int in_idx;
-    long long t_after;
-    double* slab_out;       // slab phase 1: write local {recon, eik, tv, has_nan, has_bad}, no commit
-    const double* reduced;  // slab phase 2: globally summed {recon, eik, tv, n_nan, n_bad}
-};
-
-template <int NTH>
-__device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid) {
-    double recon = 0.0, eik = 0.0, tvs = 0.0;
-    if (!F.reduced) {
-        double a = 0.0, b = 0.0, c = 0.0;
-        // 16-byte loads, unrolled so a thread's loads are all in flight
-        // before its (fixed-order) sums
-        const double2* P2 = reinterpret_cast<const double2*>(F.partials);
-#pragma unroll 4
-        for (int i = tid; i < F.NB; i += NTH) {
-            const double2 x = __ldg(P2 + 2 * i), y = __ldg(P2 + 2 * i + 1);
-            a += x.x;
-            b += x.y;
-            c += y.x;
-        }
-        a = warp_sum_d(a);
-        b = warp_sum_d(b);
-        c = warp_sum_d(c);
-        if ((tid & 31) == 0) {
-            red[0][tid >> 5] = a;
-            red[1][tid >> 5] = b;
-            red[2][tid >> 5] = c;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            for (int k = 0; k < NTH / 32; ++k) {
-                recon += red[0][k];
-                eik += red[1][k];
-                tvs += red[2][k];
-            }
-        }
-    } else if (tid == 0) {
-        recon = F.reduced[0];
-        eik = F.reduced[1];
-        tvs = F.reduced[2];
-    }
-    if (tid != 0) return;
-    Status* st = F.st;
-    if (F.slab_out) {
-        F.slab_out[0] = recon;
-        F.slab_out[1] = eik;
-        F.slab_out[2] = tvs;
-        F.slab_out[3] = *F.nan != ULLONG_MAX ? 1.0 : 0.0;
-        F.slab_out[4] = st->bad_grad != ULLONG_MAX ? 1.0 : 0.0;
-        return;
-    }
-    const unsigned long long nanp = *F.nan;
-    const unsigned long long over = *F.over;
-    const bool any_nan = nanp != ULLONG_MAX || (F.reduced && F.reduced[3] > 0.0);
-    const bool any_bad = st->bad_grad != ULLONG_MAX || (F.reduced && F.reduced[4] > 0.0);
-    tgcu_loss_terms t;
-    t.fit = recon / F.n;
-    t.eik = F.want_eik ? eik / F.n : 0.0;
-    t.tv = F.use_tv ? tvs * F.inv_norm : 0.0;
-    t.total = t.fit + F.lambda1 * t.eik + F.lambda2 * t.tv;
-    F.trace[F.step % kTraceCap] = t;
-    int err = 0, kind = 0;
-    long long idx = -1;
-    if (any_nan) {
-        err = TGCU_ERR_INVALID_ARGUMENT;
-        kind = 1;
-        idx = nanp != ULLONG_MAX ? (long long)nanp : -1;
-    } else if (over != ULLONG_MAX) {
-        err = TGCU_ERR_CONFIG;
-        kind = 4;
-        idx = (long long)over;
-    } else if (!isfinite(t.total)) {
-        err = TGCU_ERR_NUMERICAL;
-        kind = 2;
-    } else if (any_bad) {
-        err = TGCU_ERR_NUMERICAL;
-        kind = 3;
-        idx = st->bad_grad != ULLONG_MAX ? (long long)st->bad_grad : -1;
-    }
-    if (err) {
-        st->error = err;
-        st->error_kind = kind;
-        st->error_step = F.step;
-        st->error_index = idx;
-        st->good_idx = F.in_idx;
-        st->good_t = F.t_after - 1;
-    } else {
-        st->good_idx = 1 - F.in_idx;
-        st->good_t = F.t_after;
-    }
-    *F.nan = ULLONG_MAX;
-    *F.over = ULLONG_MAX;
-    st->bad_grad = ULLONG_MAX;
-}
 
 struct StepArgs {
     // TMA tensor maps (use_tmap): parameter tile (load), owned boxes of
@@ -1604,6 +1499,12 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
                        int in_idx,
                        int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
                        double* slab_out, const BinInput& in, cudaStream_t s, bool fresh_eik) {
+    // Small grids: the whole step as one cooperative launch (small.cu)
+    if (!slab_out && small_step_eligible(g, n)) {
+        launch_small_step(g, samples, n, n_norm, cfg, in_idx, step, inv_bc1, inv_bc2, t_after, grad_out, in, s,
+                          fresh_eik);
+        return;
+    }
     // Binning runs on the binning stream into bin set k; the brick kernel
     // (caller's stream) waits for it and releases the set when done, so the
     // binning of the next step overlaps this step's brick kernel whenever its

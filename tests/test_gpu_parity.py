@@ -60,6 +60,16 @@ def grad_close(got, ref, mass, rel=1e-5, mass_rel=4e-6, what="grad"):
 # ---- K1 forward -------------------------------------------------------------------------
 
 
+
+@pytest.fixture(params=["brick", "small"])
+def step_path(request, monkeypatch):
+    """Both fused-step paths (tgcu_grid_set_step_path, read from
+    TGCU_STEP_PATH at grid creation): the brick kernel (train.cu) and the
+    two-launch small-grid step (small.cu) that the auto rule picks for these
+    grids."""
+    monkeypatch.setenv("TGCU_STEP_PATH", "brick" if request.param == "brick" else "single")
+    return request.param
+
 @pytest.mark.parametrize("dim", [2, 3])
 @pytest.mark.parametrize("order", [0, 1, 2])
 def test_eval_golden(dim, order):
@@ -146,7 +156,7 @@ def test_backprop_locality_80():
 @pytest.mark.parametrize("name,cfg", [("paper", tg.LossConfig()),
                                       ("recon", tg.LossConfig(lambda1=0.0, use_tv=False)),
                                       ("dw", tg.LossConfig(differentiate_weight=True))])
-def test_total_loss_golden_unfused_and_fused(oracle, dim, name, cfg):
+def test_total_loss_golden_unfused_and_fused(oracle, dim, name, cfg, step_path):
     z = load_golden("loss.npz")
     k = f"d{dim}_{name}_"
     spec = gspec(dim, z[k + "res"], 2)
@@ -206,7 +216,7 @@ def test_adam_golden_and_errors():
     assert np.array_equal(g.coeffs, before)
 
 
-def test_training_trajectory_golden():
+def test_training_trajectory_golden(step_path):
     """30 fused steps (2D, order 2, zero init, paper loss, lr 1e-2) vs the reference loss curve."""
     z = load_golden("train.npz")
     g = tg.init_grid(gspec(2, z["train_res"], 2))
@@ -219,7 +229,7 @@ def test_training_trajectory_golden():
     assert_close(g.coeffs, z["train_final"], 1e-3, floor=1e-2, what="final coeffs")
 
 
-def test_async_trajectory_matches_sync():
+def test_async_trajectory_matches_sync(step_path):
     z = load_golden("train.npz")
     g1 = tg.init_grid(gspec(2, z["train_res"], 2))
     g2 = tg.init_grid(gspec(2, z["train_res"], 2))
@@ -235,7 +245,7 @@ def test_async_trajectory_matches_sync():
     assert_trajectory_close(g2.coeffs, g1.coeffs, 1e-2, len(z["train_batches"]), what="async coeffs")
 
 
-def test_nonfinite_loss_aborts_and_keeps_params():
+def test_nonfinite_loss_aborts_and_keeps_params(step_path):
     z = load_golden("train.npz")
     g = tg.init_grid(gspec(2, z["train_res"], 2))
     g.adam_reset(tg.AdamConfig(lr=1e-2))
@@ -259,7 +269,7 @@ def test_nonfinite_loss_aborts_and_keeps_params():
         tg.train_step(g, nan_pt)
 
 
-def test_overlapped_binning_trajectory_and_nan_step():
+def test_overlapped_binning_trajectory_and_nan_step(step_path):
     """Binning of step i+1 on the binning stream (input_ready device batches,
     pipelined host batches, mixed with stream-ordered steps) overlaps step i's
     brick kernel: same trajectory as synchronous steps, and a NaN sample is
@@ -451,7 +461,7 @@ def test_slab_with_no_local_points_matches_full_grid():
 
 
 @pytest.mark.parametrize("dim", [2, 3])
-def test_fused_step_fresh_uniform_eikonal(oracle, reference, dim):
+def test_fused_step_fresh_uniform_eikonal(oracle, reference, dim, step_path):
     """LossConfig(eikonal_point_source=FreshUniform): the fused step takes the
     reconstruction term on the batch and the eikonal term on |batch| points
     drawn from the step's Rng (reference order). Checked against the
@@ -529,7 +539,7 @@ def test_recon_and_eikonal_loss_standalone(oracle, reference, dim):
         tg.eikonal_loss(g, np.zeros((0, 3)))
 
 
-def test_pipelined_host_steps_match_device_steps():
+def test_pipelined_host_steps_match_device_steps(step_path):
     """TGCU_HOST|TGCU_ASYNC (copy-stream pipelined host input) gives the same
     trajectory as device-resident async steps; host arrays alternate slots."""
     import torch
@@ -701,7 +711,7 @@ def test_binned_query_skewed_inputs(case):
 @pytest.mark.parametrize("order", [0, 1, 2])
 @pytest.mark.parametrize("name,cfg", [("paper", tg.LossConfig()), ("recon", tg.LossConfig(lambda1=0.0, use_tv=False)),
                                       ("dw", tg.LossConfig(differentiate_weight=True, lambda1=3e-3))])
-def test_fused_step_all_orders_vs_oracle(oracle, dim, res, order, name, cfg):
+def test_fused_step_all_orders_vs_oracle(oracle, dim, res, order, name, cfg, step_path):
     """Fused step (binning, brick kernel with edge bricks, finalize) for every
     order and dimension: loss terms, full gradient and the first Adam update
     against the fp64 oracle; resolutions not multiples of the brick edge."""
@@ -771,7 +781,7 @@ def test_empty_and_degenerate_inputs():
 
 
 @pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("TGCU_RANDOM_CASES", "40"))))
-def test_fused_step_random_configs(oracle, seed):
+def test_fused_step_random_configs(oracle, seed, step_path):
     """Seeded random sweep: dimension, order, resolution (2..41 per axis, so
     single-cell axes and partial bricks), batch size (1..20000, below and
     above the 512-point chunk), loss switches and learning rate — fused step

@@ -65,6 +65,10 @@ def run(name, steps, warmup):
     for i in range(warmup):
         tg.train_step(g, dev[i % 2], lc, asynchronous=True, input_ready=True)
     g.sync()
+    tg.reset_launch_count()
+    tg.train_step(g, dev[0], lc, asynchronous=True, input_ready=True)
+    launches = tg.launch_count()  # per step: 2 = small-grid path (small.cu), 5+ = brick path
+    g.sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if cfg.get("dim", 3) == 2:
         steps = max(steps, 4000)  # C1 steps take ~25 us: a longer window
@@ -96,7 +100,9 @@ def run(name, steps, warmup):
         pass
     return {"config": name, "deterministic": bool(cfg.get("det", False)), "grid": [res] * dim, "order": 2, "points_per_step": N, "near_frac": cfg["near"],
             "sigma": cfg["sigma"], "ms_per_step": ms, "points_per_s": N / (ms * 1e-3),
-            "brick_kernel_ms": kms / max(kn, 1), "survey_bytes_per_step": bt,
+            "step_path": "small (2 launches)" if launches == 2 else f"brick ({launches} launches)",
+            "launches_per_step": launches,
+            "brick_kernel_ms" if launches != 2 else "step_kernels_ms": kms / max(kn, 1), "survey_bytes_per_step": bt,
             "step_frac_survey_bytes": bt / (ms * 1e-3) / 1e9 / peak,
             "kernel_frac_survey_bytes": bt / (kms / max(kn, 1) * 1e-3) / 1e9 / peak,
             "kernel_frac_our_bytes": ours / (kms / max(kn, 1) * 1e-3) / 1e9 / peak, "peak_gbs": peak,

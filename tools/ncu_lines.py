@@ -5,7 +5,10 @@ CUDA source line: warp-stall samples, instructions executed, top stall reasons.
     python tools/ncu_lines.py src.csv [top]
 """
 import csv
+import os
 import sys
+
+SORTI = os.environ.get("NCU_SORT") == "inst"  # sort by instructions executed
 
 
 def main():
@@ -38,7 +41,7 @@ def main():
     tot_s = sum(a[0] for a in agg) or 1
     tot_i = sum(a[1] for a in agg) or 1
     print(f"total samples {tot_s}, instructions executed (warp) {tot_i}")
-    for samp, ins, f, ln, src, st in sorted(agg, key=lambda a: -a[0])[:top]:
+    for samp, ins, f, ln, src, st in sorted(agg, key=lambda a: -(a[1] if SORTI else a[0]))[:top]:
         ss = sorted(st.items(), key=lambda kv: -kv[1])[:3]
         print(f"{100*samp/tot_s:5.1f}% {100*ins/tot_i:5.1f}%i {f}:{ln:<5} {src:<70} "
               + " ".join(f"{k[6:]}={v}" for k, v in ss))
