@@ -30,6 +30,14 @@ struct FinArgs {
 template <int NTH>
 __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid) {
     double recon = 0.0, eik = 0.0, tvs = 0.0;
+    // the status words thread 0 decides on, loaded before the reduction so
+    // their L2 round trip overlaps it
+    unsigned long long nanp = 0, over = 0, badg = 0;
+    if (tid == 0) {
+        nanp = __ldcg(F.nan);
+        over = __ldcg(F.over);
+        badg = __ldcg(&F.st->bad_grad);
+    }
     if (!F.reduced) {
         double a = 0.0, b = 0.0, c = 0.0;
         // 16-byte loads, unrolled so a thread's loads are all in flight
@@ -69,14 +77,12 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
         F.slab_out[0] = recon;
         F.slab_out[1] = eik;
         F.slab_out[2] = tvs;
-        F.slab_out[3] = *F.nan != ULLONG_MAX ? 1.0 : 0.0;
-        F.slab_out[4] = st->bad_grad != ULLONG_MAX ? 1.0 : 0.0;
+        F.slab_out[3] = nanp != ULLONG_MAX ? 1.0 : 0.0;
+        F.slab_out[4] = badg != ULLONG_MAX ? 1.0 : 0.0;
         return;
     }
-    const unsigned long long nanp = *F.nan;
-    const unsigned long long over = *F.over;
     const bool any_nan = nanp != ULLONG_MAX || (F.reduced && F.reduced[3] > 0.0);
-    const bool any_bad = st->bad_grad != ULLONG_MAX || (F.reduced && F.reduced[4] > 0.0);
+    const bool any_bad = badg != ULLONG_MAX || (F.reduced && F.reduced[4] > 0.0);
     tgcu_loss_terms t;
     t.fit = recon / F.n;
     t.eik = F.want_eik ? eik / F.n : 0.0;
@@ -99,7 +105,7 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
     } else if (any_bad) {
         err = TGCU_ERR_NUMERICAL;
         kind = 3;
-        idx = st->bad_grad != ULLONG_MAX ? (long long)st->bad_grad : -1;
+        idx = badg != ULLONG_MAX ? (long long)badg : -1;
     }
     if (err) {
         st->error = err;
