@@ -60,6 +60,7 @@ struct SmallArgs {
     unsigned long long* nan;
     FinArgs F;
     unsigned* ticket;  // coefficient CTAs done with their partials (zero between launches)
+    int early;         // points grid triggers the coefficient grid's launch at its start
 };
 
 constexpr int kSmallNT = 256;
@@ -101,37 +102,57 @@ __device__ __forceinline__ void block_partials(double (*red)[kSmallNT / 32], dou
     }
 }
 
+// Lanes per point: a point's corners form 2^(D-1) x-pairs (two vertex blocks
+// adjacent in memory, read as 2K contiguous floats and reduced into as one
+// 2K-float segment). In 3D the four pairs go to four consecutive lanes whose
+// partial blends are summed with shuffles (63 registers instead of 114;
+// 3D 32^3 28.5 vs 32.2 us per step); in 2D one lane takes both pairs — two
+// lanes per point measured slower at C1 (14.4 vs 12.7 us per step: the
+// fp64 locate and loss chain run once per lane).
+template <int DIM>
+struct SmallLanes {
+    static constexpr int P = DIM == 3 ? 4 : 1;       // lanes per point
+    static constexpr int NP = (1 << (DIM - 1)) / P;  // corner pairs per lane
+};
+
 template <int DIM, int ORDER, bool EIK>
 __global__ void __launch_bounds__(kSmallNT) k_small_points(const __grid_constant__ SmallArgs A) {
     constexpr int K = KOf<DIM, ORDER>::value;
-    constexpr int NC = 1 << DIM;
+    constexpr int P = SmallLanes<DIM>::P, NP = SmallLanes<DIM>::NP;
     __shared__ double red[4][kSmallNT / 32];
     pdl_wait();
-    // When to let the coefficient grid be scheduled: in 2D both grids fit an
-    // SM together (2 x 256 x 80 + 256 x 64 registers), and an early trigger
-    // hides its launch (C1: 12.9 vs 16.2 us per step); in 3D (114 registers
-    // here) its CTAs resident beside this grid would halve this grid's
-    // occupancy (3D 48^3, 2^17 points: 63.3 vs 54.5 us per step), so it
-    // follows the points.
-    constexpr bool kEarly = DIM == 2;
-    if (kEarly) pdl_trigger();
+    // When to let the coefficient grid be scheduled: early in 2D, where both
+    // grids fit an SM together and the early trigger hides the launch (C1:
+    // 12.9 vs 16.2 us per step); in 3D after the points (an early-resident
+    // coefficient grid cost the points grid occupancy: 3D 48^3, 2^17 points,
+    // 63.3 vs 54.5 us per step with one thread per point).
+    const bool early = A.early;
+    if (early) pdl_trigger();
     // (st->error is written only by an earlier step's finalize)
     if (A.st->error) return;
     TGCU_SRING(0, atomicMin)
-    const int nthr = gridDim.x * kSmallNT;
+    const int t = threadIdx.x & (P - 1);             // lane within the point's group
+    const int gstride = gridDim.x * (kSmallNT / P);  // points per sweep
     const long long sy = A.s.sy, sz = A.s.sz;
     double recon_sum = 0.0, eik_sum = 0.0;
     int npts = 0;
-    for (int i = blockIdx.x * kSmallNT + threadIdx.x; i < A.n; i += nthr) {
-        const float4 q = __ldg(A.pts + i);
-        const float pf[3] = {q.x, q.y, q.z};
+    // A warp runs the sweep to its last point as a whole (the group sums are
+    // full-warp shuffles): lanes past the end or on a NaN point compute on a
+    // harmless point and store nothing.
+    for (int i = blockIdx.x * (kSmallNT / P) + (int)(threadIdx.x / P);
+         P == 1 ? i < A.n : __any_sync(0xffffffffu, i < A.n); i += gstride) {
+        bool valid = i < A.n;
+        float4 q = valid ? __ldg(A.pts + i) : make_float4(0.f, 0.f, 0.f, 0.f);
         bool nanp = false;
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) nanp |= isnan(pf[a]);
+        for (int a = 0; a < DIM; ++a) nanp |= isnan(a == 0 ? q.x : (a == 1 ? q.y : q.z));
         if (nanp) {  // dropped, reported by the finalize (as the binning does)
-            atomicMin(A.nan, (unsigned long long)i);
-            continue;
+            if (t == 0) atomicMin(A.nan, (unsigned long long)i);
+            if (P == 1) continue;
+            valid = false;
+            q = make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        const float pf[3] = {q.x, q.y, q.z};
         double lc[DIM];
         AxisF ax[DIM];
         long long base = 0;
@@ -141,33 +162,56 @@ __global__ void __launch_bounds__(kSmallNT) k_small_points(const __grid_constant
             base += (long long)c * (a == 0 ? 1LL : (a == 1 ? sy : sz));
             ax[a] = axis_factors(A.s, a, lc[a]);
         }
-        auto vid = [&](int c) {
-            return base + (c & 1) + ((c >> 1) & 1) * sy + (DIM == 3 ? ((c >> 2) & 1) * sz : 0LL);
-        };
-        float cb[NC][K];
+        // pair j of this lane = corner pair pr = t*NP + j: corners 2pr, 2pr+1,
+        // first vertex base + (y, z) offset of pr
+        auto pair_vertex = [&](int pr) { return base + (pr & 1) * sy + (DIM == 3 ? (pr >> 1) * sz : 0LL); };
+        float cb[NP][2][K];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) load_block<K, true>(A.p_in + vid(c) * K, cb[c]);
+        for (int j = 0; j < NP; ++j) {
+            const long long v0 = pair_vertex(t * NP + j);
+            load_block<K, true>(A.p_in + v0 * K, cb[j][0]);
+            load_block<K, true>(A.p_in + (v0 + 1) * K, cb[j][1]);
+        }
         float f = 0.0f, fg[DIM];
 #pragma unroll
         for (int a = 0; a < DIM; ++a) fg[a] = 0.0f;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) blend_corner<DIM, ORDER, EIK>(cb[c], corner_geom<DIM>(A.s, ax, c), f, fg);
+        for (int j = 0; j < NP; ++j)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+                blend_corner<DIM, ORDER, EIK>(cb[j][b], corner_geom<DIM>(A.s, ax, 2 * (t * NP + j) + b), f, fg);
+#pragma unroll
+        for (int o = 1; o < P; o <<= 1) {  // the group's sum (a group never spans warps)
+            f += __shfl_xor_sync(0xffffffffu, f, o);
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) fg[a] += __shfl_xor_sync(0xffffffffu, fg[a], o);
+        }
         double recon, eik;
         float u, gv[DIM];
         point_loss<DIM, EIK>(A.L, f, fg, q.w, recon, eik, u, gv);
-        recon_sum += recon;
-        eik_sum += eik;
-        ++npts;
+        if (!valid) continue;  // (after the group's shuffles)
+        if (t == 0) {
+            recon_sum += recon;
+            eik_sum += eik;
+            ++npts;
+        }
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            float G[K];
+        for (int j = 0; j < NP; ++j) {
+            const int pr = t * NP + j;
+            float G[2 * K];
 #pragma unroll
-            for (int k2 = 0; k2 < K; ++k2) G[k2] = 0.0f;
-            corner_grad<DIM, ORDER, K>(corner_geom<DIM>(A.s, ax, c), u, gv, G);
-            red_block<K>(A.acc + vid(c) * K, G);
+            for (int b = 0; b < 2; ++b) {
+                float Gb[K];
+#pragma unroll
+                for (int k2 = 0; k2 < K; ++k2) Gb[k2] = 0.0f;
+                corner_grad<DIM, ORDER, K>(corner_geom<DIM>(A.s, ax, 2 * pr + b), u, gv, Gb);
+#pragma unroll
+                for (int k2 = 0; k2 < K; ++k2) G[b * K + k2] = Gb[k2];
+            }
+            red_block<2 * K>(A.acc + pair_vertex(pr) * K, G);
         }
     }
-    if (!kEarly) pdl_trigger();
+    if (!early) pdl_trigger();
     block_partials(red, recon_sum, eik_sum, 0.0, (double)npts, A.partials + 4 * blockIdx.x);
     TGCU_SRING(1, atomicMax)
 }
@@ -291,14 +335,22 @@ void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         kp = eik ? (const void*)k_small_points<DIM, ORDER, true> : (const void*)k_small_points<DIM, ORDER, false>;
         kc = grad_out ? (const void*)k_small_coeffs<DIM, ORDER, true> : (const void*)k_small_coeffs<DIM, ORDER, false>;
     });
-    // points: a thread per point (C1: 256 CTAs, 5.6 us; 148 CTAs with two
-    // points per thread measured 13 us); coefficients: one CTA per SM at most
-    // (rounds of 4 per thread)
+    // points: one sweep (C1, a thread per point: 256 CTAs 5.6 us; 148 CTAs
+    // with two points per thread 13 us);
+    // coefficients: one CTA per SM at most (rounds of 4 per thread)
     const int sms = sm_count(g.device);
-    int pcap = 8192;
-    if (const char* ev = std::getenv("TGCU_SMALL_PCTAS")) pcap = std::max(1, std::atoi(ev));
-    const int np = (int)std::max<int64_t>(1, std::min<int64_t>(pcap, (n + kSmallNT - 1) / kSmallNT));
-    const int nq = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (g.NC + kSmallNT - 1) / kSmallNT));
+    static const int pcap = [] {  // TGCU_SMALL_PCTAS: A/B knob, read once
+        const char* ev = std::getenv("TGCU_SMALL_PCTAS");
+        return ev ? std::max(1, std::atoi(ev)) : 8192;
+    }();
+    const int lanes = g.spec.dim == 3 ? SmallLanes<3>::P : SmallLanes<2>::P;  // lanes per point
+    const int np = (int)std::max<int64_t>(1, std::min<int64_t>(pcap, (n * lanes + kSmallNT - 1) / kSmallNT));
+    static const int qcap_env = [] {  // TGCU_SMALL_QCTAS: A/B knob, read once
+        const char* ev = std::getenv("TGCU_SMALL_QCTAS");
+        return ev ? std::max(1, std::atoi(ev)) : 0;
+    }();
+    const int qcap = qcap_env ? qcap_env : sms;
+    const int nq = (int)std::max<int64_t>(1, std::min<int64_t>(qcap, (g.NC + kSmallNT - 1) / kSmallNT));
     if (g.spart_cap < 4 * (np + nq)) {
         if (g.spart) TGCU_CUDA(cudaFree(g.spart));
         // partials + the CTA ticket (one more double, zeroed once)
@@ -340,6 +392,11 @@ void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     A.inv_bc2 = (float)inv_bc2;
     A.partials = g.spart;
     A.ncta_pts = np;
+    static const int early_env = [] {  // TGCU_SMALL_EARLY=0/1: A/B knob, read once
+        const char* ev = std::getenv("TGCU_SMALL_EARLY");
+        return ev ? std::atoi(ev) : -1;
+    }();
+    A.early = early_env >= 0 ? early_env : (g.spec.dim == 2 ? 1 : 0);
     A.ticket = reinterpret_cast<unsigned*>(g.spart + g.spart_cap);
     A.st = g.st;
     A.nan = &g.st->nan_bin[k];

@@ -31,6 +31,12 @@ def time_path(tg, torch, dim, res, n, path, steps):
     for i in range(100):
         tg.train_step(g, dev[i % 2], cfg, asynchronous=True, input_ready=True)
     g.sync()
+    # host cost per call while the launch queue is not yet full
+    h0 = time.perf_counter()
+    for i in range(100):
+        tg.train_step(g, dev[i % 2], cfg, asynchronous=True, input_ready=True)
+    host_free = 1e6 * (time.perf_counter() - h0) / 100
+    g.sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     t0 = time.perf_counter()
@@ -40,7 +46,7 @@ def time_path(tg, torch, dim, res, n, path, steps):
     e1.record()
     torch.cuda.synchronize()
     last = g.sync()
-    return 1e3 * e0.elapsed_time(e1) / steps, 1e6 * (t1 - t0) / steps, last.total
+    return 1e3 * e0.elapsed_time(e1) / steps, 1e6 * (t1 - t0) / steps, last.total, host_free
 
 
 def parity(tg, oracle_mod, dim, res, n, path):
@@ -79,9 +85,10 @@ def main():
     for name in a.grids.split(","):
         dim, res, n = GRIDS[name]
         for path, pname in ((tg.TaylorGrid.STEP_BRICK, "brick"), (tg.TaylorGrid.STEP_SINGLE, "single")):
-            dev_us, host_us, loss = time_path(tg, torch, dim, res, n, path, a.steps)
+            dev_us, host_us, loss, host_free = time_path(tg, torch, dim, res, n, path, a.steps)
             terr, gerr = parity(tg, O, dim, res, min(n, 1 << 15), path)
-            print(f"{name:6s} {pname:6s} device {dev_us:7.2f} us/step  host {host_us:6.2f} us/call  "
+            print(f"{name:6s} {pname:6s} device {dev_us:7.2f} us/step  host {host_us:6.2f} us/call "
+                  f"(queue not full: {host_free:6.2f})  "
                   f"loss {loss:.6g}  terms rel {terr:.2e}  grad rel {gerr:.2e}", flush=True)
 
 
