@@ -370,13 +370,12 @@ int tgcu_grid_set_deterministic(tgcu_grid* g, int on);
 
 /* Fused-step path (no reference counterpart: an implementation choice behind
  * tgcu_train_step). TGCU_STEP_BRICK: binning + the brick kernel + finalize
- * (any grid). TGCU_STEP_SINGLE: the whole step as one cooperative launch
- * (thread per point, gradients reduced in L2, thread per coefficient for TV +
- * Adam) — for small grids such as BASELINE configs[0] (2D 128^2), where the
+ * (any grid). TGCU_STEP_SINGLE: the small-grid step, two launches chained
+ * by programmatic dependent launch (thread per point with the gradients
+ * reduced in L2, then thread per coefficient for TV + Adam + the commit) — for small grids such as BASELINE configs[0] (2D 128^2), where the
  * brick path's five launches are latency-bound. TGCU_STEP_AUTO (default)
- * takes the single launch for grids with fewer bricks than SMs, at most 2^20
- * coefficients and 2^18 points per step, and never for slab grids or in
- * deterministic mode. Environment TGCU_STEP_PATH=brick|single at grid
+ * takes it for grids of at most 3 x 2^20 coefficients and batches of at most
+ * 2^22 points, and never for slab grids or in deterministic mode. Environment TGCU_STEP_PATH=brick|single at grid
  * creation sets the same. Results agree within the fused step's tolerances
  * (summation order of the gradient differs). */
 #define TGCU_STEP_AUTO 0

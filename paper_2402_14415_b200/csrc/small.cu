@@ -306,10 +306,12 @@ bool small_step_eligible(const Grid& g, int64_t n) {
     if (g.NC >= (int64_t)INT_MAX || n >= (int64_t)INT_MAX) return false;
     if (g.step_path == 1) return false;
     if (g.step_path == 2) return true;
-    // auto: grids with fewer bricks than SMs (the brick kernel cannot fill
-    // the GPU) whose state stays in L2, at batch sizes where the L2
-    // reductions stay cheap
-    return g.NB < 148 && g.NC <= (int64_t)kSmallMaxCoeffs && n <= kSmallMaxPoints;
+    // auto: grids of up to 3 M coefficients (their state stays in L2). The
+    // crossover measured (tools/small_ab.py, us per step, small vs brick):
+    // 2D 128^2 12.6/22.9, 256^2 15.6/28.1, 512^2 2^18 points 45.3/41.2,
+    // 512^2 2^20 89.2/96.7, 1024^2 2^20 173.6/128.2; 3D 48^3 53.8/85.0,
+    // 64^3 106.4/118.4, 64^3 2^20 points 260.5/486.4, 96^3 272.2/101.7.
+    return g.NC <= kSmallMaxCoeffs && n <= kSmallMaxPoints;
 }
 
 static int sm_count(int device) {

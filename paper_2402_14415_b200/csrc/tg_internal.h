@@ -264,8 +264,8 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
 // Two-launch fused step for small grids (small.cu): the auto rule's
 // limits (coefficients, points per step) and the launcher, same arguments as
 // launch_train_step without the slab phase.
-constexpr int64_t kSmallMaxCoeffs = int64_t(1) << 20;
-constexpr int64_t kSmallMaxPoints = int64_t(1) << 18;
+constexpr int64_t kSmallMaxCoeffs = int64_t(3) << 20;
+constexpr int64_t kSmallMaxPoints = int64_t(1) << 22;
 bool small_step_eligible(const Grid& g, int64_t n);
 void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
                        int in_idx, int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,

@@ -760,6 +760,7 @@ def test_global_binning_path_vs_oracle(oracle, case):
     tref = oracle.total_loss(s, c, smp, Loss(), gref)
     mass = oracle.total_loss_mass(s, c, smp, Loss())
     g = tg.init_grid(gspec(3, res, order))
+    g.set_step_path(tg.TaylorGrid.STEP_BRICK)  # the binning under test (auto would take the small path)
     g.coeffs = c
     g.adam_reset(tg.AdamConfig(lr=1e-2))
     t = tg.train_step(g, smp, cfg, export_grad=True)
@@ -837,6 +838,7 @@ def test_wide_2d_grid_brick_codes(oracle):
     tref = oracle.total_loss(s, c, smp, Loss(), gref)
     mass = oracle.total_loss_mass(s, c, smp, Loss())
     g = tg.init_grid(gspec(2, res, 2))
+    g.set_step_path(tg.TaylorGrid.STEP_BRICK)  # the brick codes under test (auto would take the small path)
     g.coeffs = c
     g.adam_reset(tg.AdamConfig(lr=1e-2))
     t = tg.train_step(g, smp, tg.LossConfig(), export_grad=True)

@@ -33,8 +33,8 @@ def test_auto_rule_and_launch_counts():
     assert _steps_launches(g, batch) == 2
     g.set_deterministic(True)  # deterministic mode keeps the brick path (+ its 2 sort kernels)
     assert _steps_launches(g, batch) == 7
-    # a grid with more bricks than SMs: the brick path
-    big = tg.init_grid(tg.GridSpec(dim=3, resolution=(64, 64, 64), order=2))
+    # a grid of more than 3 x 2^20 coefficients (96^3 x 10): the brick path
+    big = tg.init_grid(tg.GridSpec(dim=3, resolution=(96, 96, 96), order=2))
     big.adam_reset(tg.AdamConfig(lr=1e-2))
     assert _steps_launches(big, tg.sample(tg.SHAPE_SPHERE, 3, 4, 1 << 16, near_frac=0.5, sigma=0.01,
                                           param0=0.6)) == 5
@@ -45,7 +45,7 @@ def test_auto_rule_and_launch_counts():
 @pytest.mark.parametrize("dim,res,n", [(2, (40, 33, 1), (1 << 21) + 7), (3, (23, 19, 17), (1 << 21) + 333)])
 def test_small_path_grid_stride_batches_vs_oracle(oracle, dim, res, n):
     """More points than 8192 CTAs x 256 threads: each thread takes several
-    points (forced small path on a batch the auto rule gives the brick path)."""
+    points (the small path forced)."""
     rng = np.random.default_rng(31 + dim)
     s = Spec(dim=dim, res=res, order=2)
     c = (0.1 * rng.standard_normal(s.V * s.K)).astype(np.float32).astype(np.float64)
