@@ -781,7 +781,7 @@ def test_empty_and_degenerate_inputs():
     assert np.isfinite(t.total) and g.adam_t == 1
 
 
-@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("TGCU_RANDOM_CASES", "40"))))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("TGCU_RANDOM_CASES", "300"))))
 def test_fused_step_random_configs(oracle, seed, step_path):
     """Seeded random sweep: dimension, order, resolution (2..41 per axis, so
     single-cell axes and partial bricks), batch size (1..20000, below and
