@@ -450,6 +450,7 @@ int tgcu_grid_destroy(tgcu_grid* h) {
     cudaFree(g.bin_codes);
     cudaFree(g.bin_chain);
     cudaFree(g.partials);
+    cudaFree(g.fin_l2);
     cudaFree(g.sacc);
     cudaFree(g.spart);
     cudaFree(g.d_trace);

@@ -27,6 +27,41 @@ struct FinArgs {
     const double* reduced;  // slab phase 2: globally summed {recon, eik, tv, n_nan, n_bad}
 };
 
+// Fixed-order sums of NB partial records {recon, eik, tv, points} (4 doubles
+// each): thread-strided sums, warp trees, then warp order; out[] valid in
+// thread 0. Every thread must call it (one block barrier inside).
+template <int NTH>
+__device__ void block_sum_partials(const double* partials, int NB, double (*red)[NTH / 32], int tid, double* out) {
+    double a = 0.0, b = 0.0, c = 0.0;
+    // 16-byte loads, unrolled so a thread's loads are all in flight before its
+    // sums; L2 loads (the small step writes the partials in the same launch)
+    const double2* P2 = reinterpret_cast<const double2*>(partials);
+#pragma unroll 4
+    for (int i = tid; i < NB; i += NTH) {
+        const double2 x = __ldcg(P2 + 2 * i), y = __ldcg(P2 + 2 * i + 1);
+        a += x.x;
+        b += x.y;
+        c += y.x;
+    }
+    a = warp_sum_d(a);
+    b = warp_sum_d(b);
+    c = warp_sum_d(c);
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = a;
+        red[1][tid >> 5] = b;
+        red[2][tid >> 5] = c;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        out[0] = out[1] = out[2] = 0.0;
+        for (int k = 0; k < NTH / 32; ++k) {
+            out[0] += red[0][k];
+            out[1] += red[1][k];
+            out[2] += red[2][k];
+        }
+    }
+}
+
 template <int NTH>
 __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid) {
     double recon = 0.0, eik = 0.0, tvs = 0.0;
@@ -39,33 +74,11 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
         badg = __ldcg(&F.st->bad_grad);
     }
     if (!F.reduced) {
-        double a = 0.0, b = 0.0, c = 0.0;
-        // 16-byte loads, unrolled so a thread's loads are all in flight
-        // before its (fixed-order) sums
-        const double2* P2 = reinterpret_cast<const double2*>(F.partials);
-#pragma unroll 4
-        for (int i = tid; i < F.NB; i += NTH) {
-            const double2 x = __ldcg(P2 + 2 * i), y = __ldcg(P2 + 2 * i + 1);  // L2: the small step writes them in the same launch
-            a += x.x;
-            b += x.y;
-            c += y.x;
-        }
-        a = warp_sum_d(a);
-        b = warp_sum_d(b);
-        c = warp_sum_d(c);
-        if ((tid & 31) == 0) {
-            red[0][tid >> 5] = a;
-            red[1][tid >> 5] = b;
-            red[2][tid >> 5] = c;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            for (int k = 0; k < NTH / 32; ++k) {
-                recon += red[0][k];
-                eik += red[1][k];
-                tvs += red[2][k];
-            }
-        }
+        double s3[3];
+        block_sum_partials<NTH>(F.partials, F.NB, red, tid, s3);
+        recon = s3[0];
+        eik = s3[1];
+        tvs = s3[2];
     } else if (tid == 0) {
         recon = F.reduced[0];
         eik = F.reduced[1];

@@ -151,6 +151,7 @@ struct Grid {
     cudaEvent_t ev_in = nullptr;     // caller stream -> binning stream (input order)
     cudaEvent_t ev_bdone[2] = {nullptr, nullptr}, ev_bfree[2] = {nullptr, nullptr};
     double* partials = nullptr; // NB * 4
+    double* fin_l2 = nullptr;   // multi-CTA finalize: 148 level-2 records (4 doubles) + its ticket
     tgcu_loss_terms* d_trace = nullptr;  // kTraceCap
     tgcu_loss_terms* h_terms = nullptr;  // pinned, 1
     float* staging = nullptr;            // device staging for host inputs

@@ -1338,6 +1338,38 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, DIM == 3 ? 1024 / BrickSh
 // Reduce the per-brick partials in a fixed order, apply the reference's error
 // order (NaN point -> non-finite loss -> non-finite gradient) and commit
 // (after the brick kernel; slab grids: phase 2, with the globally reduced sums).
+// Grids of many bricks (C3: 32,768; C5: 262,144): CTA b sums the partials of
+// its contiguous segment in a fixed order into level-2 record b, and the last
+// CTA to finish (ticket) runs the finalize over the level-2 records — a fixed
+// association whichever CTA is last. One CTA over C3's partials took 21 us.
+constexpr int kFinMultiMin = 8192;  // bricks
+__global__ void __launch_bounds__(1024) k_step_finalize_multi(FinArgs F, double* l2, unsigned* ticket) {
+    __shared__ double red[3][32];
+    __shared__ int last;
+    if (F.st->error) return;
+    const int seg = (F.NB + gridDim.x - 1) / gridDim.x;
+    const int b0 = min(F.NB, (int)blockIdx.x * seg), b1 = min(F.NB, b0 + seg);
+    double s3[3];
+    block_sum_partials<1024>(F.partials + 4 * (size_t)b0, b1 - b0, red, threadIdx.x, s3);
+    if (threadIdx.x == 0) {
+        double* o = l2 + 4 * blockIdx.x;
+        o[0] = s3[0];
+        o[1] = s3[1];
+        o[2] = s3[2];
+        o[3] = 0.0;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        if (last) *ticket = 0u;  // every CTA has taken its ticket
+    }
+    __syncthreads();  // (also orders thread 0's reads of red before the next reduction)
+    if (!last) return;
+    __threadfence();
+    FinArgs F2 = F;
+    F2.partials = l2;
+    F2.NB = gridDim.x;
+    finalize_body<1024>(F2, red, threadIdx.x);
+}
+
 __global__ void __launch_bounds__(1024) k_step_finalize(FinArgs F) {
     __shared__ double red[3][32];
     if (F.st->error) return;
@@ -1753,7 +1785,16 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         if (g.prof_this) prof_mark(g, s, 1);
     });
 
-    k_step_finalize<<<1, 1024, 0, s>>>(F);
+    if (g.NB >= kFinMultiMin && !F.reduced) {
+        const int G = (int)std::min<int64_t>(148, (g.NB + 1023) / 1024);
+        if (!g.fin_l2) {
+            TGCU_CUDA(cudaMalloc(&g.fin_l2, sizeof(double) * (4 * 148 + 1)));
+            TGCU_CUDA(cudaMemsetAsync(g.fin_l2 + 4 * 148, 0, sizeof(double), s));
+        }
+        k_step_finalize_multi<<<G, 1024, 0, s>>>(F, g.fin_l2, reinterpret_cast<unsigned*>(g.fin_l2 + 4 * 148));
+    } else {
+        k_step_finalize<<<1, 1024, 0, s>>>(F);
+    }
     count_launch(2);
     TGCU_CUDA(cudaGetLastError());
     if (g.bd_on) {
