@@ -345,6 +345,7 @@ static int create_grid(const tgcu_grid_spec* spec, const tgcu_init_options* opts
         // Brick decomposition (train.cu / query.cu).
         if (const char* det = std::getenv("TGCU_DETERMINISTIC")) g.deterministic = det[0] == '1';
         if (const char* pdl = std::getenv("TGCU_SMALL_PDL")) g.small_pdl = pdl[0] != '0';
+        if (const char* pdl = std::getenv("TGCU_BRICK_PDL")) g.brick_pdl = pdl[0] != '0';
         if (const char* sp = std::getenv("TGCU_STEP_PATH"))
             g.step_path = std::string(sp) == "brick" ? 1 : (std::string(sp) == "single" ? 2 : 0);
         g.NB = 1;

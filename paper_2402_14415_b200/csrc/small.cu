@@ -83,8 +83,7 @@ __device__ unsigned long long g_sring[256 * 4];
 // operations visible); let the next grid be scheduled (once every CTA of
 // this grid has triggered or exited). Triggering only after the wait keeps at
 // most two grids of the chain resident at a time.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+// (pdl_wait / pdl_trigger: tma.cuh)
 
 // Block reduction of four doubles (fixed order) -> out[0..3].
 __device__ __forceinline__ void block_partials(double (*red)[kSmallNT / 32], double a, double b, double c, double d,

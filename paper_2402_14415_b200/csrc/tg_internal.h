@@ -196,6 +196,7 @@ struct Grid {
     float* sacc = nullptr;       // small-grid step: fp32 gradient accumulator (NC, zero between steps)
     double* spart = nullptr;     // small-grid step: per-CTA loss partials + CTA ticket
     int spart_cap = 0;           // doubles
+    bool brick_pdl = true;       // brick path: brick kernel and finalize chained by PDL (TGCU_BRICK_PDL=0 off)
     bool small_pdl = true;       // small-grid step: programmatic dependent launch (TGCU_SMALL_PDL=0 off)
     cudaEvent_t bd_ev[6] = {};
     double bd_sum[5] = {0, 0, 0, 0, 0};

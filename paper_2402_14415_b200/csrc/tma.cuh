@@ -43,6 +43,14 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
         "r"(phase)
         : "memory");
 }
+// Programmatic dependent launch (a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): wait until the
+// previous grid on the stream has completed with its memory visible; let the
+// next grid be scheduled once every CTA of this one has triggered or exited.
+// Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 __device__ __forceinline__ float fast_sqrt(float x) {
     float r;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));

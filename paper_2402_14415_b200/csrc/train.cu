@@ -607,6 +607,12 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, DIM == 3 ? 1024 / BrickSh
     // r + SPL, ..., and the per-vertex sums of the others reach rank 0 over
     // distributed shared memory, which then runs TV + Adam alone.
     // (a separate instantiation, SPLIT, so the unsplit kernel carries none of it)
+    // programmatic dependent launch (launch_train_step): wait for the previous
+    // step's finalize (st, partials), then let this step's finalize be
+    // scheduled — it becomes resident only once the last brick CTA has
+    // started, i.e. for the last wave
+    pdl_wait();
+    pdl_trigger();
     const int SPL = SPLIT ? A.split : 1;
     int crank = 0;
     if constexpr (SPLIT) crank = (int)cg::this_cluster().block_rank();
@@ -1346,6 +1352,8 @@ constexpr int kFinMultiMin = 8192;  // bricks
 __global__ void __launch_bounds__(1024) k_step_finalize_multi(FinArgs F, double* l2, unsigned* ticket) {
     __shared__ double red[3][32];
     __shared__ int last;
+    pdl_wait();
+    pdl_trigger();
     if (F.st->error) return;
     const int seg = (F.NB + gridDim.x - 1) / gridDim.x;
     const int b0 = min(F.NB, (int)blockIdx.x * seg), b1 = min(F.NB, b0 + seg);
@@ -1370,10 +1378,14 @@ __global__ void __launch_bounds__(1024) k_step_finalize_multi(FinArgs F, double*
     finalize_body<1024>(F2, red, threadIdx.x);
 }
 
-__global__ void __launch_bounds__(1024) k_step_finalize(FinArgs F) {
-    __shared__ double red[3][32];
+// (256 threads measured 0.3 % slower at C2: 4,096 partials per thread block)
+constexpr int kFinThreads = 1024;
+__global__ void __launch_bounds__(kFinThreads) k_step_finalize(FinArgs F) {
+    __shared__ double red[3][kFinThreads / 32];
+    pdl_wait();
+    pdl_trigger();
     if (F.st->error) return;
-    finalize_body<1024>(F, red, threadIdx.x);
+    finalize_body<kFinThreads>(F, red, threadIdx.x);
 }
 
 // ---- TMA tensor maps of the fused step --------------------------------------
@@ -1763,38 +1775,61 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         g.prof_this = g.prof_on && (g.steps_launched % g.prof_every) == 0;
         if (g.prof_this) prof_mark(g, s, 0);
         if (g.bd_on) bd_mark(g, s, 3);
-        if (split > 1) {
+        {
             cudaLaunchConfig_t lc{};
             lc.gridDim = bgrid;
             lc.blockDim = dim3(BrickShape<DIM>::NT);
             lc.dynamicSmemBytes = smem;
             lc.stream = s;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = (unsigned)split;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
+            cudaLaunchAttribute at[2];
+            int na = 0;
+            if (g.brick_pdl) {
+                at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                at[na].val.programmaticStreamSerializationAllowed = 1;
+                ++na;
+            }
+            if (split > 1) {
+                at[na].id = cudaLaunchAttributeClusterDimension;
+                at[na].val.clusterDim.x = (unsigned)split;
+                at[na].val.clusterDim.y = 1;
+                at[na].val.clusterDim.z = 1;
+                ++na;
+            }
             lc.attrs = at;
-            lc.numAttrs = 1;
+            lc.numAttrs = na;
             TGCU_CUDA(cudaLaunchKernelEx(&lc, kern, A));
-        } else {
-            kern<<<bgrid, BrickShape<DIM>::NT, smem, s>>>(A);
         }
-        TGCU_CUDA(cudaEventRecord(g.ev_bfree[k], s));
         if (g.bd_on) bd_mark(g, s, 4);
         if (g.prof_this) prof_mark(g, s, 1);
     });
 
-    if (g.NB >= kFinMultiMin && !F.reduced) {
-        const int G = (int)std::min<int64_t>(148, (g.NB + 1023) / 1024);
-        if (!g.fin_l2) {
-            TGCU_CUDA(cudaMalloc(&g.fin_l2, sizeof(double) * (4 * 148 + 1)));
-            TGCU_CUDA(cudaMemsetAsync(g.fin_l2 + 4 * 148, 0, sizeof(double), s));
-        }
-        k_step_finalize_multi<<<G, 1024, 0, s>>>(F, g.fin_l2, reinterpret_cast<unsigned*>(g.fin_l2 + 4 * 148));
-    } else {
-        k_step_finalize<<<1, 1024, 0, s>>>(F);
+    // the finalize follows the brick kernel directly on s (programmatic
+    // dependent launch hides its launch latency); the bin set is released after it
+    if (g.NB >= kFinMultiMin && !g.fin_l2) {
+        TGCU_CUDA(cudaMalloc(&g.fin_l2, sizeof(double) * (4 * 148 + 1)));
+        TGCU_CUDA(cudaMemsetAsync(g.fin_l2 + 4 * 148, 0, sizeof(double), s));
     }
+    {
+        cudaLaunchConfig_t lc{};
+        lc.blockDim = dim3(1024);
+        lc.dynamicSmemBytes = 0;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = g.brick_pdl ? 1 : 0;
+        if (g.NB >= kFinMultiMin) {
+            lc.gridDim = dim3((unsigned)std::min<int64_t>(148, (g.NB + 1023) / 1024));
+            TGCU_CUDA(cudaLaunchKernelEx(&lc, k_step_finalize_multi, F, g.fin_l2,
+                                         reinterpret_cast<unsigned*>(g.fin_l2 + 4 * 148)));
+        } else {
+            lc.gridDim = dim3(1);
+            lc.blockDim = dim3(kFinThreads);
+            TGCU_CUDA(cudaLaunchKernelEx(&lc, k_step_finalize, F));
+        }
+    }
+    TGCU_CUDA(cudaEventRecord(g.ev_bfree[k], s));
     count_launch(2);
     TGCU_CUDA(cudaGetLastError());
     if (g.bd_on) {
