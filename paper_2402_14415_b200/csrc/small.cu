@@ -61,6 +61,7 @@ struct SmallArgs {
     FinArgs F;
     unsigned* ticket;  // coefficient CTAs done with their partials (zero between launches)
     int early;         // points grid triggers the coefficient grid's launch at its start
+    int pts_ready;     // samples complete before the launch (may be read before the PDL wait)
 };
 
 constexpr int kSmallNT = 256;
@@ -119,6 +120,13 @@ __global__ void __launch_bounds__(kSmallNT) k_small_points(const __grid_constant
     constexpr int K = KOf<DIM, ORDER>::value;
     constexpr int P = SmallLanes<DIM>::P, NP = SmallLanes<DIM>::NP;
     __shared__ double red[4][kSmallNT / 32];
+    // The first point of this thread is loaded before the wait when the
+    // batch is known complete (input-ready or event-ordered samples), so its
+    // load overlaps the previous grid's tail; a batch produced by a kernel
+    // just before this one on the stream is read after the wait.
+    const int i0 = blockIdx.x * (kSmallNT / P) + (int)(threadIdx.x / P);
+    float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (A.pts_ready && i0 < A.n) q0 = __ldg(A.pts + i0);
     pdl_wait();
     // When to let the coefficient grid be scheduled: early in 2D, where both
     // grids fit an SM together and the early trigger hides the launch (C1:
@@ -138,10 +146,9 @@ __global__ void __launch_bounds__(kSmallNT) k_small_points(const __grid_constant
     // A warp runs the sweep to its last point as a whole (the group sums are
     // full-warp shuffles): lanes past the end or on a NaN point compute on a
     // harmless point and store nothing.
-    for (int i = blockIdx.x * (kSmallNT / P) + (int)(threadIdx.x / P);
-         P == 1 ? i < A.n : __any_sync(0xffffffffu, i < A.n); i += gstride) {
+    for (int i = i0; P == 1 ? i < A.n : __any_sync(0xffffffffu, i < A.n); i += gstride) {
         bool valid = i < A.n;
-        float4 q = valid ? __ldg(A.pts + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 q = valid ? (i == i0 && A.pts_ready ? q0 : __ldg(A.pts + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
         bool nanp = false;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) nanp |= isnan(a == 0 ? q.x : (a == 1 ? q.y : q.z));
@@ -220,42 +227,59 @@ __global__ void __launch_bounds__(kSmallNT) k_small_coeffs(const __grid_constant
     constexpr int K = KOf<DIM, ORDER>::value;
     __shared__ double red[4][kSmallNT / 32];
     __shared__ int last;
+    const int nthr = gridDim.x * kSmallNT;
+    const int tid = threadIdx.x;
+    const int r0 = A.s.res[0], r1 = A.s.res[1];
+    const int offs[3] = {K, r0 * K, r0 * r1 * K};
+    // Rounds of R coefficients per thread, every load of a round issued before
+    // its arithmetic (the kernel is L2-latency bound). The parameters and
+    // moments were written by the previous step's coefficient grid, which
+    // completed before the points grid passed its own wait (and, in 2D, let
+    // this grid be scheduled): the first round's p / m / v loads are issued
+    // before this grid's wait and overlap the points grid; the accumulator
+    // (being reduced into by the points grid) is read after it.
+    constexpr int R = 4;
+    float pv[R], pn[R][2 * DIM], pg[R], mi[R], vi[R];
+    unsigned nb[R];  // neighbour present: bit 2a = v+e_a, bit 2a+1 = v-e_a
+    auto load_round = [&](int base) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int idx = base + r * nthr;
+            const int j = idx < A.nc ? idx : 0;
+            const int vtx = j / K;
+            const int g3[3] = {vtx % r0, DIM == 3 ? (vtx / r0) % r1 : vtx / r0, DIM == 3 ? vtx / (r0 * r1) : 0};
+            nb[r] = 0;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                const bool hi = A.want_tv && g3[a] + 1 < A.s.res[a], lo = A.want_tv && g3[a] >= 1;
+                nb[r] |= (hi ? 1u : 0u) << (2 * a) | (lo ? 1u : 0u) << (2 * a + 1);
+                pn[r][2 * a] = __ldg(A.p_in + (hi ? j + offs[a] : j));
+                pn[r][2 * a + 1] = __ldg(A.p_in + (lo ? j - offs[a] : j));
+            }
+            pv[r] = __ldg(A.p_in + j);
+            mi[r] = __ldg(A.m_in + j);
+            vi[r] = __ldg(A.v_in + j);
+        }
+    };
+    auto load_acc = [&](int base) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int idx = base + r * nthr;
+            pg[r] = __ldcg(A.acc + (idx < A.nc ? idx : 0));
+        }
+    };
+    const int base0 = blockIdx.x * kSmallNT + tid;
+    load_round(base0);
     pdl_wait();  // every point's reductions have landed in L2
     pdl_trigger();
     if (A.st->error) return;
     TGCU_SRING(2, atomicMin)
-    const int nthr = gridDim.x * kSmallNT;
-    const int tid = threadIdx.x;
     double tv_sum = 0.0;
     {
-        const int r0 = A.s.res[0], r1 = A.s.res[1];
-        const int offs[3] = {K, r0 * K, r0 * r1 * K};
         const float c1 = A.c1, c2 = A.c2, lr_bc1 = A.lr * A.inv_bc1;
-        // rounds of R coefficients per thread: every load of a round is
-        // issued before its arithmetic (the phase is L2-latency bound)
-        constexpr int R = 4;
-        for (int base = blockIdx.x * kSmallNT + tid; base < A.nc; base += R * nthr) {
-            float pv[R], pn[R][2 * DIM], pg[R], mi[R], vi[R];
-            unsigned nb[R];  // neighbour present: bit 2a = v+e_a, bit 2a+1 = v-e_a
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int idx = base + r * nthr;
-                const int j = idx < A.nc ? idx : 0;
-                const int vtx = j / K;
-                const int g3[3] = {vtx % r0, DIM == 3 ? (vtx / r0) % r1 : vtx / r0, DIM == 3 ? vtx / (r0 * r1) : 0};
-                nb[r] = 0;
-#pragma unroll
-                for (int a = 0; a < DIM; ++a) {
-                    const bool hi = A.want_tv && g3[a] + 1 < A.s.res[a], lo = A.want_tv && g3[a] >= 1;
-                    nb[r] |= (hi ? 1u : 0u) << (2 * a) | (lo ? 1u : 0u) << (2 * a + 1);
-                    pn[r][2 * a] = __ldg(A.p_in + (hi ? j + offs[a] : j));
-                    pn[r][2 * a + 1] = __ldg(A.p_in + (lo ? j - offs[a] : j));
-                }
-                pv[r] = __ldg(A.p_in + j);
-                pg[r] = __ldcg(A.acc + j);
-                mi[r] = __ldg(A.m_in + j);
-                vi[r] = __ldg(A.v_in + j);
-            }
+        for (int base = base0; base < A.nc; base += R * nthr) {
+            if (base != base0) load_round(base);
+            load_acc(base);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int idx = base + r * nthr;
@@ -393,6 +417,7 @@ void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     A.inv_bc2 = (float)inv_bc2;
     A.partials = g.spart;
     A.ncta_pts = np;
+    A.pts_ready = (in.ready || in.wait) ? 1 : 0;
     static const int early_env = [] {  // TGCU_SMALL_EARLY=0/1: A/B knob, read once
         const char* ev = std::getenv("TGCU_SMALL_EARLY");
         return ev ? std::atoi(ev) : -1;

@@ -86,6 +86,7 @@ def main():
     ap.add_argument("--steps", type=int, default=4000)
     ap.add_argument("--grids", default="c1,3d32,3d48")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--paths", default="brick,single")
     a = ap.parse_args()
     import torch
     import paper_2402_14415_b200 as tg
@@ -93,7 +94,9 @@ def main():
     O = Oracle()
     for name in a.grids.split(","):
         dim, res, n = GRIDS[name]
-        for path, pname in ((tg.TaylorGrid.STEP_BRICK, "brick"), (tg.TaylorGrid.STEP_SINGLE, "single")):
+        pmap = {"brick": tg.TaylorGrid.STEP_BRICK, "single": tg.TaylorGrid.STEP_SINGLE}
+        for pname in a.paths.split(","):
+            path = pmap[pname]
             dev_us, host_us, loss, host_free = time_path(tg, torch, dim, res, n, path, a.steps)
             terr, gerr = (0.0, 0.0) if a.no_parity else parity(tg, O, dim, res, min(n, 1 << 15), path)
             print(f"{name:6s} {pname:6s} device {dev_us:7.2f} us/step  host {host_us:6.2f} us/call "
