@@ -264,6 +264,26 @@ def cpu_baseline_train(wl, batches, steps=2):
             "seconds": secs, "loss_last": float(terms[-1, 0])}
 
 
+def cpu_baseline_c1(steps=40):
+    """C1 (BASELINE configs[0]: 2D 128^2 order 2, 65,536 uniform points of the
+    circle-union-box target per step, lr 1e-2) through the reference's own
+    tg::total_loss + tg::adam_step (oracle/_ref), all host threads, `steps`
+    steps on two seeded batches from the package's host sampler."""
+    from oracle.pyoracle import Loss, Reference, Spec, reference_available
+    if not reference_available():
+        return None
+    import paper_2402_14415_b200 as tg
+    batches = [tg.sample(tg.SHAPE_C1_2D, 2, 500 + i, 1 << 16) for i in range(2)]
+    R = Reference()
+    threads = int(min(os.cpu_count() or 1, 64))
+    _, terms, secs = R.train(Spec(dim=2, res=(128, 128, 1), order=2), None, np.array(batches, dtype=np.float64),
+                             Loss(), lr=1e-2, threads=threads, steps=steps)
+    pts = steps * (1 << 16)
+    return {"value": pts / secs, "unit": "points/s", "cores": threads, "kind": "reference",
+            "sample": f"{steps} full C1 steps ({pts} points) through tg::total_loss + tg::adam_step "
+                      f"(oracle/_ref, threads={threads})", "seconds": secs, "loss_last": float(terms[-1, 0])}
+
+
 def stages_leg(device, hbm_peak, cpu=True):
     """SURVEY 8(f) rows on this GPU next to the reference's own code: upsample
     (128^3 -> 256^3 order 2), sample_grid_field (256^3 order-2 grid on a 256^3
@@ -825,6 +845,8 @@ def main():
         line["larger_configs_clocks"] = cclk.summary()
         if not args.no_cpu_baseline:
             for ent in line["larger_configs"]:
+                if ent["config"] == "c1":
+                    ent["cpu_baseline"] = cpu_baseline_c1()
                 if ent["config"] in ("c3", "c5"):
                     ent["cpu_baseline"] = cpu_baseline_train(ent["config"], make_batches(ent["config"], 500, 2),
                                                              steps=1)
