@@ -12,7 +12,7 @@ import paper_2402_14415_b200 as tg
 dev = [torch.from_numpy(tg.sample(tg.SHAPE_C1_2D, 2, 500 + i, 1 << 16)).cuda() for i in range(2)]
 cfg = tg.LossConfig()
 keep = []
-for inst in range(8):
+for inst in range(12):
     g = tg.init_grid(tg.GridSpec(dim=2, resolution=(128, 128, 1), order=2))
     g.adam_reset(tg.AdamConfig(lr=1e-2))
     for i in range(200):
@@ -23,6 +23,6 @@ for inst in range(8):
     for i in range(4000):
         tg.train_step(g, dev[i % 2], cfg, asynchronous=True, input_ready=True)
     e1.record(); torch.cuda.synchronize()
-    print(inst, round(1e3 * e0.elapsed_time(e1) / 4000, 2), hex(g.coeff_ptr()) if hasattr(g, "coeff_ptr") else "", flush=True)
+    print(inst, round(1e3 * e0.elapsed_time(e1) / 4000, 2), hex(g.device_coeffs_ptr()), hex(dev[0].data_ptr()), flush=True)
     keep.append(g)
     pad = torch.empty(int(1.3e6) * (inst + 1), dtype=torch.uint8, device="cuda"); keep.append(pad)
