@@ -383,6 +383,25 @@ int tgcu_grid_set_deterministic(tgcu_grid* g, int on);
 #define TGCU_STEP_SINGLE 2
 int tgcu_grid_set_step_path(tgcu_grid* g, int path);
 
+/* CUDA-graph replay of small-grid training steps (no reference counterpart:
+ * the reference's run_schedule loop, schedule.cpp:66-92, issued without a
+ * host call per step). tgcu_train_graph_create captures nsteps (even, >= 2)
+ * fused steps of the small-grid path on device batches samples[0..nsteps-1]
+ * (n x 4 floats each, device pointers kept by the graph: refill their
+ * contents between replays, ordered on the replay stream) on a non-default
+ * stream; nothing runs at capture. tgcu_train_graph_launch replays them: the
+ * same steps as nsteps tgcu_train_step(TGCU_ASYNC | TGCU_INPUT_READY) calls
+ * (Adam t, trace rows and ping-pong slot advance on the device; errors are
+ * sticky and reported by tgcu_sync, as for asynchronous steps). Fails with
+ * TGCU_ERR_INVALID_ARGUMENT for a grid on the brick path (slab, deterministic,
+ * large grids or TGCU_STEP_BRICK), an odd nsteps, or a replay after an odd
+ * number of other steps. */
+typedef struct tgcu_graph tgcu_graph;
+int tgcu_train_graph_create(tgcu_grid* g, const float* const* samples, int nsteps, int64_t n,
+                            const tgcu_loss_config* cfg, void* stream, tgcu_graph** out);
+int tgcu_train_graph_launch(tgcu_graph* graph, void* stream);
+int tgcu_train_graph_destroy(tgcu_graph* graph);
+
 /* Collective phase of the profiled slab steps (those whose brick kernel
  * tgcu_profile_begin / _every times): summed device ms of the all-reduce of
  * the partials and of the halo exchange (0 with the fused peer-memory halo,

@@ -25,7 +25,7 @@ __all__ = [
     "backprop_spatial_chain", "backprop_value_and_spatial", "adaptive_weight", "tv_loss",
     "total_loss", "adam_step", "train_step", "sample", "sample_uniform", "shape_sdf",
     "ConfigError", "IngestError", "NumericalError", "ResourceError", "CudaError", "lib",
-    "launch_count", "reset_launch_count", "LIB_PATH", "upsample", "multilinear_resample", "ScalarField3",
+    "launch_count", "reset_launch_count", "LIB_PATH", "TrainGraph", "upsample", "multilinear_resample", "ScalarField3",
     "ScalarField2", "sample_grid_field", "sample_grid_field2", "StoragePrecision", "save_tgrid", "load_tgrid",
     "tgrid_file_size", "draw_batch",
 ]
@@ -172,6 +172,10 @@ def lib():
     L.tgcu_shuffle_order.argtypes = [C.c_uint64, C.c_int64, P]
     L.tgcu_grid_set_deterministic.argtypes = [P, C.c_int]
     L.tgcu_grid_set_step_path.argtypes = [P, C.c_int]
+    L.tgcu_train_graph_create.argtypes = [P, C.POINTER(C.c_void_p), C.c_int, C.c_int64, C.POINTER(_Loss), P,
+                                          C.POINTER(P)]
+    L.tgcu_train_graph_launch.argtypes = [P, P]
+    L.tgcu_train_graph_destroy.argtypes = [P]
     L.tgcu_slab_comm_profile.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int)]
     L.tgcu_comm_create.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(P)]
     L.tgcu_comm_destroy.argtypes = [P]
@@ -728,6 +732,53 @@ def train_step(grid: TaylorGrid, samples, cfg: LossConfig = LossConfig(), asynch
     _check(lib().tgcu_train_step(grid.handle, _ptr(s), s.shape[0], C.byref(cfg._c()), C.byref(t), flags,
                                  C.c_void_p(stream) if stream else None))
     return LossTerms._from(t)
+
+
+class TrainGraph:
+    """CUDA-graph replay of small-grid fused steps (tgcu_train_graph_*): the
+    steps train_step(grid, batches[i], cfg, asynchronous=True,
+    input_ready=True) for i in 0..len(batches)-1 (an even count), captured
+    once on `stream` (a torch.cuda.Stream or raw handle; a new stream if None)
+    and replayed without a host call per step. The batches are CUDA float32
+    (n, 4) tensors whose storage the graph keeps: refill them in place between
+    replays. Errors are sticky and surface at grid.sync()."""
+
+    def __init__(self, grid: TaylorGrid, batches, cfg: LossConfig = LossConfig(), stream=None):
+        import torch
+        self.grid = grid
+        self.batches = [_dev_f32(b, 4, "samples") for b in batches]
+        n = self.batches[0].shape[0]
+        if any(b.shape[0] != n for b in self.batches):
+            raise ValueError("train_graph_create: every batch needs the same size")
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.batches[0].device)
+        ptrs = (C.c_void_p * len(self.batches))(*[b.data_ptr() for b in self.batches])
+        h = C.c_void_p()
+        _check(lib().tgcu_train_graph_create(grid.handle, ptrs, len(self.batches), n, C.byref(cfg._c()),
+                                             C.c_void_p(self._raw(self.stream)), C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def _raw(stream):
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+    @property
+    def steps(self) -> int:
+        return len(self.batches)
+
+    def replay(self, stream=None):
+        s = self.stream if stream is None else stream
+        _check(lib().tgcu_train_graph_launch(self._h, C.c_void_p(self._raw(s))))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tgcu_train_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ---- seeded inputs ------------------------------------------------------------------

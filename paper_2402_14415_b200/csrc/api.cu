@@ -453,6 +453,8 @@ int tgcu_grid_destroy(tgcu_grid* h) {
     cudaFree(g.partials);
     cudaFree(g.fin_l2);
     cudaFree(g.sacc);
+    cudaFree(g.d_ctr);
+    cudaFree(g.d_bc);
     cudaFree(g.spart);
     cudaFree(g.d_trace);
     cudaFree(g.slab_red);

@@ -23,6 +23,8 @@ struct FinArgs {
     long long step;
     int in_idx;
     long long t_after;
+    long long* ctr;         // graph-replayed steps: {t, step} on the device (step / t_after read
+                            // from it, then advanced); nullptr: step / t_after above
     double* slab_out;       // slab phase 1: write local {recon, eik, tv, has_nan, has_bad}, no commit
     const double* reduced;  // slab phase 2: globally summed {recon, eik, tv, n_nan, n_bad}
 };
@@ -101,7 +103,9 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
     t.eik = F.want_eik ? eik / F.n : 0.0;
     t.tv = F.use_tv ? tvs * F.inv_norm : 0.0;
     t.total = t.fit + F.lambda1 * t.eik + F.lambda2 * t.tv;
-    F.trace[F.step % kTraceCap] = t;
+    const long long step = F.ctr ? F.ctr[1] : F.step;
+    const long long t_after = F.ctr ? F.ctr[0] + 1 : F.t_after;
+    F.trace[step % kTraceCap] = t;
     int err = 0, kind = 0;
     long long idx = -1;
     if (any_nan) {
@@ -123,17 +127,21 @@ __device__ void finalize_body(const FinArgs& F, double (*red)[NTH / 32], int tid
     if (err) {
         st->error = err;
         st->error_kind = kind;
-        st->error_step = F.step;
+        st->error_step = step;
         st->error_index = idx;
         st->good_idx = F.in_idx;
-        st->good_t = F.t_after - 1;
+        st->good_t = t_after - 1;
     } else {
         st->good_idx = 1 - F.in_idx;
-        st->good_t = F.t_after;
+        st->good_t = t_after;
     }
     *F.nan = ULLONG_MAX;
     *F.over = ULLONG_MAX;
     st->bad_grad = ULLONG_MAX;
+    if (F.ctr) {  // the next replayed step's t and trace slot (a failed step leaves the
+        F.ctr[0] = t_after;  // later ones no-ops; the host resets the counter with its state)
+        F.ctr[1] = step + 1;
+    }
 }
 
 }  // namespace tgcu

@@ -28,7 +28,10 @@
 // Summation order of a coefficient's point contributions follows the L2
 // atomics (not bit-reproducible); deterministic mode keeps the brick path.
 #include <climits>
+#include <cmath>
 #include <cstdlib>
+#include <string>
+#include <vector>
 
 #include "dispatch.cuh"
 #include "finalize.cuh"
@@ -62,7 +65,14 @@ struct SmallArgs {
     unsigned* ticket;  // coefficient CTAs done with their partials (zero between launches)
     int early;         // points grid triggers the coefficient grid's launch at its start
     int pts_ready;     // samples complete before the launch (may be read before the PDL wait)
+    const long long* ctr;  // graph-replayed steps: {t, step} on the device (F.ctr), else nullptr
+    const float2* bc;      // with ctr: (1/(1 - b1^t), 1/(1 - b2^t)) for t = 1..kBcTab, host-rounded
 };
+
+// Bias-correction table of graph-replayed steps: entry t-1 holds the values
+// the host would pass for Adam step t (both are exactly 1.0f from t = 65536 on,
+// 0.999^65536 ~ 3e-29).
+constexpr int kBcTab = 65536;
 
 constexpr int kSmallNT = 256;
 
@@ -270,13 +280,22 @@ __global__ void __launch_bounds__(kSmallNT) k_small_coeffs(const __grid_constant
     };
     const int base0 = blockIdx.x * kSmallNT + tid;
     load_round(base0);
+    // graph replay: this step's t from the device counter (advanced by the
+    // previous step's finalize, complete before the points grid's wait)
+    float inv_bc1 = A.inv_bc1, inv_bc2 = A.inv_bc2;
+    if (A.ctr) {
+        const long long t_after = A.ctr[0] + 1;
+        const float2 bcv = A.bc[(t_after < kBcTab ? t_after : kBcTab) - 1];
+        inv_bc1 = bcv.x;
+        inv_bc2 = bcv.y;
+    }
     pdl_wait();  // every point's reductions have landed in L2
     pdl_trigger();
     if (A.st->error) return;
     TGCU_SRING(2, atomicMin)
     double tv_sum = 0.0;
     {
-        const float c1 = A.c1, c2 = A.c2, lr_bc1 = A.lr * A.inv_bc1;
+        const float c1 = A.c1, c2 = A.c2, lr_bc1 = A.lr * inv_bc1;
         for (int base = base0; base < A.nc; base += R * nthr) {
             if (base != base0) load_round(base);
             load_acc(base);
@@ -302,7 +321,7 @@ __global__ void __launch_bounds__(kSmallNT) k_small_coeffs(const __grid_constant
                 const float vn = fmaf(A.b2, vi[r], c2 * gi * gi);
                 A.m_out[idx] = mn;
                 A.v_out[idx] = vn;
-                A.p_out[idx] = pv[r] - lr_bc1 * mn * fast_rcp(fast_sqrt(vn * A.inv_bc2) + A.eps);
+                A.p_out[idx] = pv[r] - lr_bc1 * mn * fast_rcp(fast_sqrt(vn * inv_bc2) + A.eps);
                 tv_sum += (double)sq;
             }
         }
@@ -344,13 +363,44 @@ static int sm_count(int device) {
     return c;
 }
 
-void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
-                       int in_idx, int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
-                       const BinInput& in, cudaStream_t s, bool fresh_eik) {
+// CTA counts of the two kernels for a batch of n points.
+static void small_grid_dims(const Grid& g, int64_t n, int* np, int* nq) {
+    const int sms = sm_count(g.device);
+    static const int pcap = [] {  // TGCU_SMALL_PCTAS: A/B knob, read once
+        const char* ev = std::getenv("TGCU_SMALL_PCTAS");
+        return ev ? std::max(1, std::atoi(ev)) : 8192;
+    }();
+    static const int qcap_env = [] {  // TGCU_SMALL_QCTAS: A/B knob, read once
+        const char* ev = std::getenv("TGCU_SMALL_QCTAS");
+        return ev ? std::max(1, std::atoi(ev)) : 0;
+    }();
+    // points: one sweep (C1, a thread per point: 256 CTAs 5.6 us; 148 CTAs
+    // with two points per thread 13 us); coefficients: one CTA per SM at most
+    // (rounds of 4 per thread; 222-384 CTAs measured slower at C1)
+    const int lanes = g.spec.dim == 3 ? SmallLanes<3>::P : SmallLanes<2>::P;  // lanes per point
+    *np = (int)std::max<int64_t>(1, std::min<int64_t>(pcap, (n * lanes + kSmallNT - 1) / kSmallNT));
+    const int qcap = qcap_env ? qcap_env : sms;
+    *nq = (int)std::max<int64_t>(1, std::min<int64_t>(qcap, (g.NC + kSmallNT - 1) / kSmallNT));
+}
+
+// Device buffers of the small-grid step (before a graph capture, where
+// allocation is not allowed): the accumulator, the partials + CTA ticket.
+static void ensure_small_buffers(Grid& g, int np, int nq, cudaStream_t s) {
     if (!g.sacc) {
         TGCU_CUDA(cudaMalloc(&g.sacc, sizeof(float) * g.NC));
         TGCU_CUDA(cudaMemsetAsync(g.sacc, 0, sizeof(float) * g.NC, s));
     }
+    if (g.spart_cap < 4 * (np + nq)) {
+        if (g.spart) TGCU_CUDA(cudaFree(g.spart));
+        g.spart_cap = 4 * (np + nq);
+        TGCU_CUDA(cudaMalloc(&g.spart, sizeof(double) * (g.spart_cap + 1)));
+        TGCU_CUDA(cudaMemsetAsync(g.spart + g.spart_cap, 0, sizeof(double), s));
+    }
+}
+
+void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
+                       int in_idx, int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
+                       const BinInput& in, cudaStream_t s, bool fresh_eik, bool graph) {
     const int k = g.bin_set;  // the NaN slot of this step
     g.bin_set ^= 1;
     const bool eik = cfg.lambda1 > 0.0;
@@ -360,29 +410,9 @@ void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         kp = eik ? (const void*)k_small_points<DIM, ORDER, true> : (const void*)k_small_points<DIM, ORDER, false>;
         kc = grad_out ? (const void*)k_small_coeffs<DIM, ORDER, true> : (const void*)k_small_coeffs<DIM, ORDER, false>;
     });
-    // points: one sweep (C1, a thread per point: 256 CTAs 5.6 us; 148 CTAs
-    // with two points per thread 13 us);
-    // coefficients: one CTA per SM at most (rounds of 4 per thread)
-    const int sms = sm_count(g.device);
-    static const int pcap = [] {  // TGCU_SMALL_PCTAS: A/B knob, read once
-        const char* ev = std::getenv("TGCU_SMALL_PCTAS");
-        return ev ? std::max(1, std::atoi(ev)) : 8192;
-    }();
-    const int lanes = g.spec.dim == 3 ? SmallLanes<3>::P : SmallLanes<2>::P;  // lanes per point
-    const int np = (int)std::max<int64_t>(1, std::min<int64_t>(pcap, (n * lanes + kSmallNT - 1) / kSmallNT));
-    static const int qcap_env = [] {  // TGCU_SMALL_QCTAS: A/B knob, read once
-        const char* ev = std::getenv("TGCU_SMALL_QCTAS");
-        return ev ? std::max(1, std::atoi(ev)) : 0;
-    }();
-    const int qcap = qcap_env ? qcap_env : sms;
-    const int nq = (int)std::max<int64_t>(1, std::min<int64_t>(qcap, (g.NC + kSmallNT - 1) / kSmallNT));
-    if (g.spart_cap < 4 * (np + nq)) {
-        if (g.spart) TGCU_CUDA(cudaFree(g.spart));
-        // partials + the CTA ticket (one more double, zeroed once)
-        g.spart_cap = 4 * (np + nq);
-        TGCU_CUDA(cudaMalloc(&g.spart, sizeof(double) * (g.spart_cap + 1)));
-        TGCU_CUDA(cudaMemsetAsync(g.spart + g.spart_cap, 0, sizeof(double), s));
-    }
+    int np = 1, nq = 1;
+    small_grid_dims(g, n, &np, &nq);
+    ensure_small_buffers(g, np, nq, s);
     if (in.wait) TGCU_CUDA(cudaStreamWaitEvent(s, in.wait, 0));
 
     SmallArgs A{};
@@ -444,6 +474,11 @@ void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     F.t_after = t_after;
     F.slab_out = nullptr;
     F.reduced = nullptr;
+    if (graph) {
+        A.ctr = g.d_ctr;
+        A.bc = reinterpret_cast<const float2*>(g.d_bc);
+        F.ctr = g.d_ctr;
+    }
 
     g.prof_this = g.prof_on && (g.steps_launched % g.prof_every) == 0;
     if (g.prof_this) prof_mark(g, s, 0);
@@ -466,7 +501,126 @@ void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
     count_launch(2);
 }
 
+// Counter reset of graph-replayed steps: {t, step} = the host's state.
+__global__ void k_set_ctr(long long* ctr, long long t, long long step) {
+    ctr[0] = t;
+    ctr[1] = step;
+}
+
 }  // namespace tgcu
+
+struct tgcu_graph {
+    tgcu_grid* h = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int nsteps = 0;
+    int cur0 = 0;  // ping-pong slot at capture (and at every replay: nsteps is even)
+};
+
+extern "C" int tgcu_train_graph_create(tgcu_grid* h, const float* const* samples, int nsteps, int64_t n,
+                                       const tgcu_loss_config* cfg, void* stream, tgcu_graph** out) {
+    using namespace tgcu;
+    return guard([&] {
+        require(h != nullptr && out != nullptr && samples != nullptr, "train_graph_create: NULL argument");
+        require(cfg != nullptr, "total_loss: NULL config");
+        require(cfg->lambda1 >= 0.0 && cfg->lambda2 >= 0.0, "LossConfig: lambda weights must be >= 0");
+        require(cfg->k > 0.0, "LossConfig: weight sharpness k must be > 0");
+        require(n > 0, "total_loss: empty batch");
+        require(nsteps >= 2 && nsteps % 2 == 0,
+                "train_graph_create: nsteps must be even and >= 2 (each replay returns to the captured ping-pong slot)");
+        for (int i = 0; i < nsteps; ++i) require(samples[i] != nullptr, "train_graph_create: NULL batch");
+        Grid& g = h->g;
+        TGCU_CUDA(cudaSetDevice(g.device));
+        require(small_step_eligible(g, n),
+                "train_graph_create: only the small-grid step path can be captured (tgcu_grid_set_step_path)");
+        // flush queued work and report a pending error before capturing
+        const int rc = tgcu_sync(h, nullptr);
+        if (rc != TGCU_OK) throw Error(rc, tgcu_last_error());
+        ensure_optimizer(g);
+        cudaStream_t s = as_stream(stream);
+        require(s != nullptr, "train_graph_create: capture needs a non-default stream");
+        if (!g.d_ctr) {
+            TGCU_CUDA(cudaMalloc(&g.d_ctr, 2 * sizeof(long long)));
+            std::vector<float> bc(2 * kBcTab);
+            for (int t = 1; t <= kBcTab; ++t) {  // launch_train_step's values (api.cu)
+                bc[2 * (t - 1)] = (float)(1.0 / (1.0 - std::pow(g.adam.beta1, (double)t)));
+                bc[2 * (t - 1) + 1] = (float)(1.0 / (1.0 - std::pow(g.adam.beta2, (double)t)));
+            }
+            TGCU_CUDA(cudaMalloc(&g.d_bc, sizeof(float) * bc.size()));
+            TGCU_CUDA(cudaMemcpy(g.d_bc, bc.data(), sizeof(float) * bc.size(), cudaMemcpyHostToDevice));
+            g.ctr_t = g.ctr_step = -1;
+        }
+        int np = 1, nq = 1;
+        small_grid_dims(g, n, &np, &nq);
+        ensure_small_buffers(g, np, nq, s);
+        TGCU_CUDA(cudaStreamSynchronize(s));
+        auto* gr = new tgcu_graph;
+        gr->h = h;
+        gr->nsteps = nsteps;
+        gr->cur0 = g.cur;
+        const bool prof = g.prof_on;
+        const int bin_set = g.bin_set;
+        g.prof_on = false;
+        BinInput in;
+        in.ready = true;  // the batches' contents are the caller's to order before each replay
+        TGCU_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            int cur = g.cur;
+            for (int i = 0; i < nsteps; ++i) {
+                launch_small_step(g, reinterpret_cast<const float4*>(samples[i]), n, n, *cfg, cur, 0, 0.0, 0.0, 0,
+                                  nullptr, in, s, false, true);
+                cur = 1 - cur;
+            }
+        } catch (...) {
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(s, &junk);
+            if (junk) cudaGraphDestroy(junk);
+            g.prof_on = prof;
+            g.bin_set = bin_set;
+            delete gr;
+            throw;
+        }
+        g.prof_on = prof;
+        g.bin_set = bin_set;
+        count_launch(-2 * nsteps);  // captured, not launched (counted per replay)
+        TGCU_CUDA(cudaStreamEndCapture(s, &gr->graph));
+        TGCU_CUDA(cudaGraphInstantiate(&gr->exec, gr->graph, 0));
+        *out = gr;
+    });
+}
+
+extern "C" int tgcu_train_graph_launch(tgcu_graph* gr, void* stream) {
+    using namespace tgcu;
+    return guard([&] {
+        require(gr != nullptr, "train_graph_launch: NULL graph");
+        Grid& g = gr->h->g;
+        TGCU_CUDA(cudaSetDevice(g.device));
+        require(g.cur == gr->cur0, "train_graph_launch: the grid's current ping-pong slot (" + std::to_string(g.cur) +
+                                       ") is not the one captured (" + std::to_string(gr->cur0) +
+                                       "): an odd number of steps ran since the capture");
+        cudaStream_t s = as_stream(stream);
+        if (g.ctr_t != g.t || g.ctr_step != g.steps_launched) {  // steps ran outside the graph, or an error reset
+            k_set_ctr<<<1, 1, 0, s>>>(g.d_ctr, g.t, g.steps_launched);
+            TGCU_CUDA(cudaGetLastError());
+            count_launch(1);
+        }
+        TGCU_CUDA(cudaGraphLaunch(gr->exec, s));
+        count_launch(2 * gr->nsteps);
+        // optimistic, as tgcu_train_step: a failed step is rolled back by tgcu_sync
+        g.t += gr->nsteps;
+        g.steps_launched += gr->nsteps;
+        g.ctr_t = g.t;
+        g.ctr_step = g.steps_launched;
+    });
+}
+
+extern "C" int tgcu_train_graph_destroy(tgcu_graph* gr) {
+    if (!gr) return TGCU_OK;
+    if (gr->exec) cudaGraphExecDestroy(gr->exec);
+    if (gr->graph) cudaGraphDestroy(gr->graph);
+    delete gr;
+    return TGCU_OK;
+}
 
 #ifdef TGCU_PHASE_TIMING
 extern "C" int tgcu_small_ring_dump(unsigned long long* out, int reset) {

@@ -196,6 +196,12 @@ struct Grid {
     float* sacc = nullptr;       // small-grid step: fp32 gradient accumulator (NC, zero between steps)
     double* spart = nullptr;     // small-grid step: per-CTA loss partials + CTA ticket
     int spart_cap = 0;           // doubles
+    // Graph-replayed small-grid steps (tgcu_train_graph_*): {t, step} on the
+    // device, advanced by each step's finalize; the bias-correction table; the
+    // counter values the device holds after the last replay (-1: unknown).
+    long long* d_ctr = nullptr;
+    float* d_bc = nullptr;
+    long long ctr_t = -1, ctr_step = -1;
     bool brick_pdl = true;       // brick path: brick kernel and finalize chained by PDL (TGCU_BRICK_PDL=0 off)
     bool small_pdl = true;       // small-grid step: programmatic dependent launch (TGCU_SMALL_PDL=0 off)
     cudaEvent_t bd_ev[6] = {};
@@ -271,7 +277,7 @@ constexpr int64_t kSmallMaxPoints = int64_t(1) << 22;
 bool small_step_eligible(const Grid& g, int64_t n);
 void launch_small_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm, const tgcu_loss_config& cfg,
                        int in_idx, int64_t step, double inv_bc1, double inv_bc2, int64_t t_after, float* grad_out,
-                       const BinInput& in, cudaStream_t s, bool fresh_eik);
+                       const BinInput& in, cudaStream_t s, bool fresh_eik, bool graph = false);
 // Fresh-uniform eikonal points (n x 3 floats, device) -> float4 records with
 // gt = kEikMark (tg_device.cuh), for the fused step's point list.
 void launch_pack_eik(const float* p3, int64_t n, float4* dst, cudaStream_t s);

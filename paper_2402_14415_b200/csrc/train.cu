@@ -1697,7 +1697,7 @@ void launch_train_step(Grid& g, const float4* samples, int64_t n, int64_t n_norm
         A.peer_hi_lz = (own_hi - 1) % kBrickZ3;
     }
     const bool eik = cfg.lambda1 > 0.0;
-    FinArgs F;
+    FinArgs F{};
     F.partials = g.partials;
     F.NB = (int)g.NB;
     F.n = (double)n_norm;

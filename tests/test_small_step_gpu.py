@@ -109,3 +109,76 @@ def test_small_path_async_after_brick_steps_and_back():
     n = len(z["train_batches"])
     np.testing.assert_allclose(g2.trace(n)[:, 0], g1.trace(n)[:, 0], rtol=1e-5)
     assert_trajectory_close(g2.coeffs, g1.coeffs, 1e-2, n, what="mixed-path coeffs")
+
+
+@pytest.mark.parametrize("dim,res", [(2, (40, 33, 1)), (3, (21, 18, 23))])
+def test_train_graph_replays_match_calls(dim, res):
+    """tgcu_train_graph_*: replays of captured small-grid steps train exactly
+    like the same steps issued call by call (Adam t, ping-pong slot and trace
+    rows advanced on the device), also mixed with calls."""
+    import torch
+    spec = tg.GridSpec(dim=dim, resolution=res, order=2)
+    shape = tg.SHAPE_C1_2D if dim == 2 else tg.SHAPE_SPHERE
+    kw = {} if dim == 2 else dict(near_frac=0.5, sigma=0.01, param0=0.6)
+    batches = [torch.from_numpy(tg.sample(shape, dim, 40 + i, 3000, **kw)).cuda() for i in range(4)]
+    torch.cuda.synchronize()
+    g1, g2 = tg.init_grid(spec), tg.init_grid(spec)
+    for g in (g1, g2):
+        g.adam_reset(tg.AdamConfig(lr=1e-2))
+    order = [0, 1] + [0, 1, 2, 3] * 3 + [2]   # 2 calls, 3 replays of 4, 1 call
+    for i in order:
+        tg.train_step(g1, batches[i], asynchronous=True, input_ready=True)
+    g1.sync()
+    s = torch.cuda.Stream()
+    tg.train_step(g2, batches[0], asynchronous=True, input_ready=True, stream=s.cuda_stream)
+    tg.train_step(g2, batches[1], asynchronous=True, input_ready=True, stream=s.cuda_stream)
+    graph = tg.TrainGraph(g2, batches, stream=s)
+    for _ in range(3):
+        graph.replay()
+    tg.train_step(g2, batches[2], asynchronous=True, input_ready=True, stream=s.cuda_stream)
+    g2.sync()
+    n = len(order)
+    assert g2.adam_t == g1.adam_t == n
+    np.testing.assert_allclose(g2.trace(n)[:, 0], g1.trace(n)[:, 0], rtol=1e-5)
+    assert_trajectory_close(g2.coeffs, g1.coeffs, 1e-2, n, what="graph coeffs")
+    graph.close()
+
+
+def test_train_graph_refusals_and_errors():
+    import torch
+    spec = tg.GridSpec(dim=2, resolution=(24, 20, 1), order=2)
+    batches = [torch.from_numpy(tg.sample(tg.SHAPE_C1_2D, 2, 7 + i, 2000)).cuda() for i in range(2)]
+    torch.cuda.synchronize()
+    g = tg.init_grid(spec)
+    g.adam_reset(tg.AdamConfig(lr=1e-2))
+    with pytest.raises(ValueError, match="even"):
+        tg.TrainGraph(g, batches[:1])
+    gb = tg.init_grid(spec)
+    gb.adam_reset(tg.AdamConfig(lr=1e-2))
+    gb.set_step_path(tg.TaylorGrid.STEP_BRICK)
+    with pytest.raises(ValueError, match="small-grid step path"):
+        tg.TrainGraph(gb, batches)
+    graph = tg.TrainGraph(g, batches)
+    graph.replay()
+    tg.train_step(g, batches[0])  # one step outside: the other ping-pong slot is current
+    with pytest.raises(ValueError, match="ping-pong slot"):
+        graph.replay()
+    tg.train_step(g, batches[1])
+    graph.replay()
+    g.sync()
+    assert g.adam_t == 6
+    good = g.coeffs
+    # a NaN coordinate in the second captured batch: that step fails, the grid
+    # keeps the state after the first one, and replays work again afterwards
+    keep = batches[1][3, 0].item()
+    batches[1][3, 0] = float("nan")
+    graph.replay(torch.cuda.current_stream())
+    with pytest.raises(ValueError, match=r"NaN coordinate \(sample 3\) at stage 0 step 7"):
+        g.sync()
+    assert g.adam_t == 7
+    assert not np.array_equal(g.coeffs, good)  # step 6 (the first replayed) committed
+    batches[1][3, 0] = keep
+    tg.train_step(g, batches[1])  # back to the captured slot
+    graph.replay()
+    g.sync()
+    assert g.adam_t == 10 and np.all(np.isfinite(g.coeffs))

@@ -80,6 +80,24 @@ def run(name, steps, warmup):
     ms = e0.elapsed_time(e1) / steps
     # the brick kernel's time from a second, profiled window (its per-launch
     # events would otherwise sit inside the timed steps: +45 % at C1)
+    graph_leg = None
+    if launches == 2:  # small-grid path: the same steps replayed from a CUDA graph (tgcu_train_graph_*)
+        gs = torch.cuda.Stream()
+        graph = tg.TrainGraph(g, [dev[i % 2] for i in range(100)], lc, stream=gs)
+        for _ in range(3):
+            graph.replay()
+        g.sync()
+        reps = max(1, steps // 100)
+        with torch.cuda.stream(gs):
+            e0.record(gs)
+            for _ in range(reps):
+                graph.replay()
+            e1.record(gs)
+        torch.cuda.synchronize()
+        graph_leg = {"ms_per_step": e0.elapsed_time(e1) / (reps * 100), "steps": reps * 100,
+                     "api": "tgcu_train_graph_launch: 100 captured steps per replay (no host call per step)"}
+        graph.close()
+        g.sync()
     g.profile_begin()
     for i in range(steps):
         tg.train_step(g, dev[i % 2], lc, asynchronous=True, input_ready=True)
@@ -106,7 +124,7 @@ def run(name, steps, warmup):
             "step_frac_survey_bytes": bt / (ms * 1e-3) / 1e9 / peak,
             "kernel_frac_survey_bytes": bt / (kms / max(kn, 1) * 1e-3) / 1e9 / peak,
             "kernel_frac_our_bytes": ours / (kms / max(kn, 1) * 1e-3) / 1e9 / peak, "peak_gbs": peak,
-            "loss_last": last.total, "steps": steps}
+            "loss_last": last.total, "steps": steps, **({"graph": graph_leg} if graph_leg else {})}
 
 
 def main():
