@@ -349,4 +349,26 @@ private:
     size_t n_ = 0;
 };
 
+// CUDA-graph replay of small-grid training steps (tgcu_train_graph_*): the
+// steps on device batches batches[0..n-1] (n even; n_pts x 4 floats each,
+// kept by the graph) captured once on a non-default stream, replayed with
+// replay(stream). Errors surface at the grid's next sync, as for asynchronous
+// steps.
+class TrainGraph {
+public:
+    TrainGraph(Grid& g, const std::vector<const float*>& batches, int64_t n_pts, const LossConfig& cfg,
+               void* stream) {
+        const tgcu_loss_config c = cfg.c();
+        check(tgcu_train_graph_create(g.handle(), batches.data(), static_cast<int>(batches.size()), n_pts, &c,
+                                      stream, &h_));
+    }
+    ~TrainGraph() { tgcu_train_graph_destroy(h_); }
+    TrainGraph(const TrainGraph&) = delete;
+    TrainGraph& operator=(const TrainGraph&) = delete;
+    void replay(void* stream) { check(tgcu_train_graph_launch(h_, stream)); }
+
+private:
+    tgcu_graph* h_ = nullptr;
+};
+
 }  // namespace tgcu
