@@ -57,6 +57,20 @@ int main() {
         std::printf("IngestError: %s\n", e.what());
     }
     std::printf("upsample + lattice + tgrid ok (f(centre) %.4f)\n", lat[364]);
+    // both fused-step paths through the C ABI (this grid takes the small-grid
+    // path by default): the same loss terms on the same samples
+    {
+        smp[4 * 5 + 3] = 0.1f;
+        tgcu::Grid a(gs), b(gs);
+        a.adam_reset({1e-2, 0.9, 0.999, 1e-8});
+        b.adam_reset({1e-2, 0.9, 0.999, 1e-8});
+        if (tgcu_grid_set_step_path(b.handle(), TGCU_STEP_BRICK) != TGCU_OK) return 10;
+        if (tgcu_grid_set_step_path(b.handle(), 7) != TGCU_ERR_INVALID_ARGUMENT) return 11;
+        const auto ta2 = a.train_step(smp, lc);
+        const auto tb2 = b.train_step(smp, lc);
+        if (!(std::fabs(ta2.total - tb2.total) <= 1e-6 * std::fabs(tb2.total))) return 12;
+        std::printf("step paths: small %.9g brick %.9g\n", ta2.total, tb2.total);
+    }
     std::printf("shim ok\n");
     return 0;
 }
