@@ -517,6 +517,8 @@ struct tgcu_graph {
     int cur0 = 0;  // ping-pong slot at capture (and at every replay: nsteps is even)
 };
 
+extern "C" int tgcu_train_graph_destroy(tgcu_graph* gr);
+
 extern "C" int tgcu_train_graph_create(tgcu_grid* h, const float* const* samples, int nsteps, int64_t n,
                                        const tgcu_loss_config* cfg, void* stream, tgcu_graph** out) {
     using namespace tgcu;
@@ -583,8 +585,12 @@ extern "C" int tgcu_train_graph_create(tgcu_grid* h, const float* const* samples
         g.prof_on = prof;
         g.bin_set = bin_set;
         count_launch(-2 * nsteps);  // captured, not launched (counted per replay)
-        TGCU_CUDA(cudaStreamEndCapture(s, &gr->graph));
-        TGCU_CUDA(cudaGraphInstantiate(&gr->exec, gr->graph, 0));
+        cudaError_t e = cudaStreamEndCapture(s, &gr->graph);
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&gr->exec, gr->graph, 0);
+        if (e != cudaSuccess) {
+            tgcu_train_graph_destroy(gr);
+            throw Error(TGCU_ERR_CUDA, std::string("train_graph_create: ") + cudaGetErrorString(e));
+        }
         *out = gr;
     });
 }
