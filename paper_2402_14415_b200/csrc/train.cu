@@ -38,6 +38,10 @@
 
 #include "dispatch.cuh"
 #include "tg_internal.h"
+
+#ifndef TGCU_TV_SHFL
+#define TGCU_TV_SHFL 1
+#endif
 #include "tma.cuh"
 #include "finalize.cuh"
 
@@ -1128,6 +1132,108 @@ __global__ void __launch_bounds__(BrickShape<DIM>::NT, DIM == 3 ? 1024 / BrickSh
         bool vok = true;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) vok &= g3[a] < A.s.res[a];
+#if TGCU_TV_SHFL
+        // The x / y stencil neighbours of a channel pair come from the
+        // neighbouring lanes (a warp holds 32 / B brick rows of B vertices, x
+        // along the lanes) by shuffles; only row / warp-edge lanes and the z
+        // neighbours read the tile, whose row pitch gives the tile reads 2-way
+        // bank conflicts (C2 0.2652 -> 0.2626 ms per step, C3 1.2598 -> 1.2517,
+        // same-box A/B; TGCU_TV_SHFL=0 builds the all-loads form). Not in the
+        // sparse-batch variant (C5: 8.632 -> 8.671 ms, its epilogues overlap
+        // each other more than the point phases). Every lane runs it (the
+        // shuffles are full-warp); lanes of out-of-grid vertices store nothing
+        // global.
+        if constexpr (K % 2 == 0 && !S::MVG && !TINYOK) {
+            constexpr int RPW = 32 / B;  // brick rows per warp
+            const int xr = lane % B, yr = lane / B;
+            const long long gidx =
+                ((DIM == 3 ? (long long)(g3[2] - A.s.zoff) * A.s.sz : 0LL) + (long long)g3[1] * A.s.sy + g3[0]) * K;
+            const float* tp = tile + L::at(1 + l3[0], 1 + l3[1], DIM == 3 ? 1 + l3[2] : 0);
+            float* gs = Gs + v * K;
+            const float* mi = mvs + v * K;
+            const float* vi = mvs + S::NOWN * K + v * K;
+            float* mo = mvs + v * K;
+            float* vo = mvs + S::NOWN * K + v * K;
+            constexpr int offs[3] = {K, L::TROWF, DIM == 3 ? T * L::TROWF : 0};
+            bool hi[DIM], lo[DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                hi[a] = A.want_tv && g3[a] + 1 < A.s.res[a];
+                lo[a] = A.want_tv && g3[a] >= 1;
+            }
+            const float c1 = A.c1, c2 = A.c2, lr_bc1 = A.lr * A.inv_bc1;
+            const float2 gsc = make_float2(A.tv_gscale, A.tv_gscale);
+            const float2 b1 = make_float2(A.b1, A.b1), b2 = make_float2(A.b2, A.b2);
+            const float2 cc1 = make_float2(c1, c1), cc2 = make_float2(c2, c2);
+            float2 sq2 = make_float2(0.f, 0.f);
+            auto shf = [](float2 x, int d, bool down) {
+                return down ? make_float2(__shfl_down_sync(0xffffffffu, x.x, d), __shfl_down_sync(0xffffffffu, x.y, d))
+                            : make_float2(__shfl_up_sync(0xffffffffu, x.x, d), __shfl_up_sync(0xffffffffu, x.y, d));
+            };
+            auto ld2 = [](const float* p) { return *reinterpret_cast<const float2*>(p); };
+            float2 gsum = make_float2(0.f, 0.f);
+            float2 gkeep[K / 2];
+            float2 m2[K / 2], v2[K / 2];
+#pragma unroll
+            for (int q = 0; q < K; q += 2) {
+                m2[q / 2] = ld2(mi + q);
+                v2[q / 2] = ld2(vi + q);
+            }
+#pragma unroll
+            for (int q = 0; q < K; q += 2) {
+                const float2 pv = ld2(tp + q);
+                float2 nb[DIM][2];  // [axis][+, -]
+                nb[0][0] = shf(pv, 1, true);
+                nb[0][1] = shf(pv, 1, false);
+                nb[1][0] = shf(pv, B, true);
+                nb[1][1] = shf(pv, B, false);
+                if (xr == B - 1 && hi[0]) nb[0][0] = ld2(tp + offs[0] + q);
+                if (xr == 0 && lo[0]) nb[0][1] = ld2(tp - offs[0] + q);
+                if (yr == RPW - 1 && hi[1]) nb[1][0] = ld2(tp + offs[1] + q);
+                if (yr == 0 && lo[1]) nb[1][1] = ld2(tp - offs[1] + q);
+                if constexpr (DIM == 3) {
+                    if (hi[2]) nb[2][0] = ld2(tp + offs[2] + q);
+                    if (lo[2]) nb[2][1] = ld2(tp - offs[2] + q);
+                }
+                const float2 npv = make_float2(-pv.x, -pv.y);
+                float2 gt = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    if (hi[a]) {  // pair (v, v+e_a): TV sum and -d
+                        const float2 d = __fadd2_rn(nb[a][0], npv);
+                        sq2 = __ffma2_rn(d, d, sq2);
+                        gt = __fadd2_rn(gt, make_float2(-d.x, -d.y));
+                    }
+                    if (lo[a]) {  // pair (v-e_a, v): +(pv - p_lo)
+                        const float2 pl = nb[a][1];
+                        gt = __fadd2_rn(gt, __fadd2_rn(pv, make_float2(-pl.x, -pl.y)));
+                    }
+                }
+                const float2 gi =
+                    __ffma2_rn(gsc, gt, ident ? make_float2(G[q], G[q + 1]) : *reinterpret_cast<const float2*>(gs + q));
+                gkeep[q / 2] = gi;
+                gsum = __fadd2_rn(gsum, gi);
+                if constexpr (EXPORT)
+                    if (vok) *reinterpret_cast<float2*>(A.grad_out + gidx + q) = gi;
+                const float2 mn = __ffma2_rn(b1, m2[q / 2], __fmul2_rn(cc1, gi));
+                const float2 vn = __ffma2_rn(b2, v2[q / 2], __fmul2_rn(cc2, __fmul2_rn(gi, gi)));
+                *reinterpret_cast<float2*>(mo + q) = mn;
+                *reinterpret_cast<float2*>(vo + q) = vn;
+                const float2 stp = make_float2(lr_bc1 * mn.x * fast_rcp(fast_sqrt(vn.x * A.inv_bc2) + A.eps),
+                                               lr_bc1 * mn.y * fast_rcp(fast_sqrt(vn.y * A.inv_bc2) + A.eps));
+                *reinterpret_cast<float2*>(gs + q) = __fadd2_rn(pv, make_float2(-stp.x, -stp.y));
+            }
+            if (vok && !isfinite(gsum.x + gsum.y)) {
+#pragma unroll
+                for (int q = 0; q < K; q += 2) {
+                    const float2 gi = gkeep[q / 2];
+                    if (!isfinite(gi.x)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q));
+                    if (!isfinite(gi.y)) atomicMin(&A.st->bad_grad, (unsigned long long)(gidx + q + 1));
+                }
+            }
+            tv_sum = vok ? (double)(sq2.x + sq2.y) : 0.0;
+        } else
+#endif
         if (vok) {
             const long long gidx =
                 ((DIM == 3 ? (long long)(g3[2] - A.s.zoff) * A.s.sz : 0LL) + (long long)g3[1] * A.s.sy + g3[0]) * K;
