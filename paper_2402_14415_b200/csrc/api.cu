@@ -602,6 +602,16 @@ int tgcu_grid_all_finite(tgcu_grid* h, int* out) {
     });
 }
 
+// TGCU_QUERY_DIRECT=1: unsorted batches of any size take k_eval_direct
+// (diagnostic: grouping experiments, A/B against the binned path).
+static bool query_force_direct() {
+    static const bool on = [] {
+        const char* e = std::getenv("TGCU_QUERY_DIRECT");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 int tgcu_eval(tgcu_grid* h, const float* pts, int64_t n, float* values, float* spatial_grad, int flags,
               void* stream) {
     return guard([&] {
@@ -624,7 +634,7 @@ int tgcu_eval(tgcu_grid* h, const float* pts, int64_t n, float* values, float* s
         }
         if (flags & TGCU_SORTED)
             launch_eval_sorted(g, dp, n, nullptr, dv, dg, s);
-        else if (n >= kBinnedQueryMin && !g.slab)
+        else if (n >= kBinnedQueryMin && !g.slab && !query_force_direct())
             launch_eval_binned(g, dp, n, dv, dg, s);  // large unsorted batches: bin by brick, smem tiles
         else
             launch_eval_direct(g, dp, n, dv, dg, s);
