@@ -9,6 +9,7 @@
 //    point range by binary search over the brick keys, so no offsets array is
 //    read. This is the coherent-points path.
 
+#include <cstdlib>
 #include <functional>
 
 #include "dispatch.cuh"
@@ -519,6 +520,7 @@ struct QpArgs {
     unsigned short* lpos;  // binned query: each input point's slot in its pass-1 tile's digit
                            // order (0xffff: NaN); pass-1 records then carry the brick code and
                            // pass-2 records their pass-1 position instead of the input index
+    int fuse_h2;           // pass-1 scatter counts pass 2's tile histograms (H2 zeroed; no pass-2 histogram kernel)
 };
 
 // Morton brick code of a point (as point_key; a NaN coordinate counts as
@@ -898,6 +900,13 @@ __global__ void __launch_bounds__(kQpThreads, 2) k_qp_scatter(QpArgs A) {
         const int dj = dig[j];
         const int pos = gst[dj] + (j - cnt[dj]);
         const float4 q = recs[j];
+        if (PASS == 1 && A.fuse_h2) {
+            // pass 2 tiles each superbrick's segment in kQpTile chunks from
+            // cfirst[dj] (qp_tile<2>): this record's tile and low digit
+            const int code = A.lpos ? __float_as_int(q.w) : scode[j];
+            const int t2 = __ldg(A.cfirst + dj) + (int)((pos - __ldg(A.seg + dj)) / kQpTile);
+            atomicAdd(A.H2 + (long long)t2 * (1 << A.LO) + (code & ((1 << A.LO) - 1)), 1);
+        }
         if (PASS == 1 || A.B) {
             (PASS == 1 ? A.A : A.B)[pos] = q;
             if (PASS == 1 && !A.lpos) A.codesA[pos] = scode[j];
@@ -995,6 +1004,16 @@ __global__ void __launch_bounds__(128, 6) k_qp_cellsort(QpArgs A, const float4* 
 
 // Runs both passes. B != null: records (x, y, z, index) grouped by brick;
 // else sorted xyz (+ perm). off: 2^KB + 1 brick offsets.
+// TGCU_QP_FUSE_H2=0/1: pass 2's tile histograms from the pass-1 scatter
+// (L2 reductions) instead of a histogram pass over the pass-1 records.
+static int qp_fuse_h2() {
+    static const int on = [] {
+        const char* e = std::getenv("TGCU_QP_FUSE_H2");
+        return e ? std::atoi(e) : 0;
+    }();
+    return on;
+}
+
 void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xyz, int64_t* perm,
                   long long* off, float* vals, float* grads, cudaStream_t s, unsigned short* lpos,
                   const std::function<void(const QpArgs&)>& after) {
@@ -1043,6 +1062,7 @@ void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xy
     A.st = g.st;
     A.lpos = lpos;
     A.qf = qp_fast(g.ds, g.spec.dim == 3 ? 3 : 4);
+    A.fuse_h2 = qp_fuse_h2();
     const size_t hs1 = sizeof(int) * NH, hs2 = sizeof(int) * NL;
     const size_t ss1 = (sizeof(float4) + 2) * kQpTile + 2 * hs1 + (lpos ? 0 : 2 * sizeof(int) * kQpTile),
                  ss2 = (sizeof(float4) + 2) * kQpTile + 2 * hs2;
@@ -1053,8 +1073,9 @@ void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xy
         k_qp_cols_partial<<<dim3((NH + 31) / 32, kQpRowBlocks), 256, 0, s>>>(A.H1, A.ntiles, NH, A.P1);
         k_qp_cols_final<<<dim3((NH + 31) / 32, kQpRowBlocks), 256, 0, s>>>(A.H1, A.ntiles, NH, A.P1, A.tot);
         k_qp_segments<<<1, 1024, 0, s>>>(A.tot, NH, A.seg, A.cfirst, A.cseg, maxtiles);
+        if (A.fuse_h2) TGCU_CUDA(cudaMemsetAsync(A.H2, 0, sizeof(int) * (size_t)maxtiles * NL, s));
         scatter1<<<A.ntiles, kQpThreads, ss1, s>>>(A);
-        hist2<<<maxtiles, kQpThreads, hs2, s>>>(A);
+        if (!A.fuse_h2) hist2<<<maxtiles, kQpThreads, hs2, s>>>(A);
         k_qp_scan2<<<NH, 1024, 0, s>>>(A);
         scatter2<<<maxtiles, kQpThreads, ss2, s>>>(A);
     };
@@ -1062,7 +1083,7 @@ void launch_qpart(Grid& g, const float* pts, int64_t n, float4* B, float* out_xy
         run(k_qp_hist<3, 3, 1>, k_qp_scatter<3, 3, 1>, k_qp_hist<3, 3, 2>, k_qp_scatter<3, 3, 2>);
     else
         run(k_qp_hist<2, 4, 1>, k_qp_scatter<2, 4, 1>, k_qp_hist<2, 4, 2>, k_qp_scatter<2, 4, 2>);
-    count_launch(8);
+    count_launch(A.fuse_h2 ? 7 : 8);
     if (C) {
         const int nbr = (int)codes;
         if (g.spec.dim == 3) k_qp_cellsort<3, 3><<<(nbr + 3) / 4, 128, 0, s>>>(A, C, nbr);
