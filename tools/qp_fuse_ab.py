@@ -3,7 +3,9 @@ scatter vs a histogram pass over the pass-1 records) on the C4 query:
 512^3, 2^26 uniform points; binned eval o1/o2 (with gradients for o2) and
 tgcu_sort_points. Each arm runs in a child process (the knob is read once);
 values, gradients, the brick offsets and the sorted point multiset must be
-identical across arms. Run: python tools/qp_fuse_ab.py
+identical across arms. Run: python tools/qp_fuse_ab.py [TGCU_QP_FUSE_H2|TGCU_QP_LUT]
+(TGCU_QP_LUT: a table-driven Morton spread in the pass-1 histogram, measured
+neutral in profiles/r02_qp_lut_ab.jsonl and removed again; the knob is inert now).
 """
 import hashlib
 import json
@@ -38,7 +40,7 @@ def child():
     n = 1 << 26
     pts = torch.empty((n, 3), dtype=torch.float32, device="cuda")
     tg.sample_uniform_device(3, 4242, pts)
-    out = {"fuse_h2": os.environ.get("TGCU_QP_FUSE_H2", "0")}
+    out = {"fuse_h2": os.environ.get("TGCU_QP_FUSE_H2", "0"), "lut": os.environ.get("TGCU_QP_LUT", "0")}
     for order in (1, 2):
         g = tg.init_grid(tg.GridSpec(dim=3, resolution=(512,) * 3, order=order),
                          tg.InitOptions(mode=tg.InitMode.HashGaussian, epsilon=0.1, seed=7, memory_cap_bytes=1 << 40))
@@ -67,10 +69,13 @@ if __name__ == "__main__":
     else:
         res = []
         for arm in ("0", "1", "0", "1"):
-            r = subprocess.run([sys.executable, __file__], env=dict(os.environ, QP_CHILD="1", TGCU_QP_FUSE_H2=arm),
+            knob = sys.argv[1] if len(sys.argv) > 1 else "TGCU_QP_FUSE_H2"
+            env = dict(os.environ, QP_CHILD="1", TGCU_QP_FUSE_H2="0", TGCU_QP_LUT="0")
+            env[knob] = arm
+            r = subprocess.run([sys.executable, __file__], env=env,
                                capture_output=True, text=True, check=True)
             res.append(json.loads(r.stdout.strip().splitlines()[-1]))
             print(json.dumps(res[-1]), flush=True)
-        keys = [k for k in res[0] if not k.endswith("_ms") and k != "fuse_h2"]
+        keys = [k for k in res[0] if not k.endswith("_ms") and k not in ("fuse_h2", "lut")]
         same = all(r[k] == res[0][k] for r in res for k in keys)
         print(json.dumps({"identical_outputs": same}))
