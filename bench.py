@@ -86,6 +86,9 @@ def mem_available_bytes():
     return 0
 
 
+E2E_WINDOWS = 5
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled while the timed legs run."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -745,13 +748,19 @@ def main():
             step(pinned[i % NBATCH].numpy(), sp, asynchronous=e2e_async)
         g.sync()
         torch.cuda.synchronize()
-        barrier(ws)
-        t0 = time.perf_counter()
-        for i in range(ne):
-            step(pinned[i % NBATCH].numpy(), sp, asynchronous=e2e_async)  # H2D inside, D2H of LossTerms
-        e2e_last = g.sync()
-        torch.cuda.synchronize()
-        e2e_s = max_over_ranks(time.perf_counter() - t0, ws)
+        # E2E_WINDOWS back-to-back windows of ne steps, each timed whole (max
+        # over ranks); the median window is reported, so one host stall (a
+        # ~0.1 s scheduling hiccup against a ~0.16 s window) does not set it
+        e2e_windows = []
+        for _w in range(E2E_WINDOWS):
+            barrier(ws)
+            t0 = time.perf_counter()
+            for i in range(ne):
+                step(pinned[i % NBATCH].numpy(), sp, asynchronous=e2e_async)  # H2D inside, D2H of LossTerms
+            e2e_last = g.sync()
+            torch.cuda.synchronize()
+            e2e_windows.append(max_over_ranks(time.perf_counter() - t0, ws))
+        e2e_s = sorted(e2e_windows)[len(e2e_windows) // 2]
         barrier(ws)
 
         q = None
@@ -810,7 +819,9 @@ def main():
                 "d2h_bytes_per_step": 32 * ws,
                 "api": ("tgcu_train_step(TGCU_HOST|TGCU_ASYNC): pipelined H2D on a copy stream, per-step LossTerms "
                         "D2H to pinned memory" if ws == 1 else "SlabTrainer.step with host samples, synchronous"),
-                "loss_last": e2e_last.total},
+                "loss_last": e2e_last.total, "steps_per_window": ne,
+                "window_points_per_s": [round(npts_global * ne / w) for w in e2e_windows],
+                "statistic": f"median of {E2E_WINDOWS} windows"},
         "gpu_launches": int(launches),
         "clocks": clk,
         "loss_last": last.total,
